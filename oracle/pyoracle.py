@@ -1,0 +1,241 @@
+"""oracle/pyoracle.py -- TEST INFRASTRUCTURE ONLY.
+
+ctypes bindings for the parity checkers: the C restatement
+(``build/libtg_oracle.so``, tg_oracle.c) and the reference's own sources built
+into ``_ref/libtgref_*.so`` (ref_harness.cpp).  Imported only by tests/,
+``__graft_entry__.smoke()`` and bench.py's cpu_baseline / reference legs.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_LIB = os.path.join(HERE, "build", "libtg_oracle.so")
+REF_LIBS = {
+    "mt": "libtgref_mt.so",            # O1: unmodified reference
+    "philox": "libtgref_philox.so",    # O2: reference + Philox streams
+    "philox_hb": "libtgref_philox_hb.so",
+    "plane": "libtgref_plane.so",
+    "plane_hb": "libtgref_plane_hb.so",
+}
+
+RULE = {"metropolis": 0, "heat_bath": 1}
+RNG = {"slot": 0, "plane": 1}
+
+
+class _Problem(C.Structure):
+    _fields_ = [("n", C.c_int), ("n_couplings", C.c_int), ("ci", C.c_void_p), ("cj", C.c_void_p),
+                ("cw", C.c_void_p), ("fields", C.c_void_p), ("n_pairs", C.c_int),
+                ("pa", C.c_void_p), ("pb", C.c_void_p)]
+
+
+class _RunCfg(C.Structure):
+    _fields_ = [("n_betas", C.c_int), ("betas", C.c_void_p), ("n_penalties", C.c_int),
+                ("penalties", C.c_void_p), ("total_sweeps", C.c_int64),
+                ("sweeps_per_swap", C.c_int64), ("seed", C.c_uint64), ("rule", C.c_int),
+                ("rng_mode", C.c_int)]
+
+
+class _Outputs(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in (
+        "f", "g", "feasible", "digest", "states", "grid_states", "round_acc_p", "round_acc_b",
+        "attempts_p", "accepts_p", "attempts_b", "accepts_b", "final_grid", "final_f",
+        "final_g", "final_state_id")]
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+_port = None
+_refs = {}
+
+
+def port_lib():
+    global _port
+    if _port is None:
+        if not os.path.exists(PORT_LIB):
+            raise RuntimeError(f"oracle port not built: {PORT_LIB} (run `make -C oracle port`)")
+        _port = C.CDLL(PORT_LIB)
+        _port.tgo_run_2dpt.restype = C.c_int
+        _port.tgo_digest.restype = C.c_uint64
+        _port.tgo_encode_state.restype = C.c_uint64
+        _port.tgo_derive.restype = C.c_uint64
+        _port.tgo_derive.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
+        _port.tgo_bits.restype = C.c_uint64
+        _port.tgo_bits.argtypes = [C.c_uint64, C.c_uint64]
+        _port.tgo_plane.restype = C.c_uint64
+        _port.tgo_plane.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_int]
+        for fn in ("tgo_p_swap_probability", "tgo_beta_swap_probability",
+                   "tgo_general_swap_probability"):
+            getattr(_port, fn).restype = C.c_double
+        _port.tgo_p_swap_probability.argtypes = [C.c_double] * 3
+        _port.tgo_beta_swap_probability.argtypes = [C.c_double] * 2
+        _port.tgo_general_swap_probability.argtypes = [C.c_double] * 4
+    return _port
+
+
+def ref_available(variant: str = "philox") -> bool:
+    return os.path.exists(os.path.join(HERE, "_ref", REF_LIBS[variant]))
+
+
+def ref_lib(variant: str):
+    if variant not in _refs:
+        path = os.path.join(HERE, "_ref", REF_LIBS[variant])
+        if not os.path.exists(path):
+            raise RuntimeError(f"reference oracle not built: {path} (run `make -C oracle ref`)")
+        lib = C.CDLL(path)
+        lib.tgr_run_2dpt.restype = C.c_int
+        lib.tgr_run_2dpt_timed.restype = C.c_int
+        _refs[variant] = lib
+    return _refs[variant]
+
+
+@dataclass
+class OracleResult:
+    f: np.ndarray
+    g: np.ndarray
+    feasible: np.ndarray
+    digest: np.ndarray
+    states: Optional[np.ndarray]
+    attempts_p: np.ndarray
+    accepts_p: np.ndarray
+    attempts_b: np.ndarray
+    accepts_b: np.ndarray
+    round_acc_p: Optional[np.ndarray]
+    round_acc_b: Optional[np.ndarray]
+    final_grid: Optional[np.ndarray]
+    grid_states: Optional[np.ndarray] = None
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+        self.msg = msg
+
+
+def _marshal(pr, betas, penalties, total_sweeps, sps, seed, rule, rng_mode):
+    keep = {
+        "ci": np.ascontiguousarray(pr.ci, dtype=np.int32),
+        "cj": np.ascontiguousarray(pr.cj, dtype=np.int32),
+        "cw": np.ascontiguousarray(pr.cw, dtype=np.float64),
+        "h": np.ascontiguousarray(pr.fields, dtype=np.float64),
+        "pa": np.ascontiguousarray(pr.pa, dtype=np.int32),
+        "pb": np.ascontiguousarray(pr.pb, dtype=np.int32),
+        "betas": np.ascontiguousarray(betas, dtype=np.float64),
+        "pens": np.ascontiguousarray(penalties, dtype=np.float64),
+    }
+    p = _Problem(pr.n, len(keep["ci"]), _ptr(keep["ci"]), _ptr(keep["cj"]), _ptr(keep["cw"]),
+                 _ptr(keep["h"]), len(keep["pa"]), _ptr(keep["pa"]), _ptr(keep["pb"]))
+    c = _RunCfg(len(keep["betas"]), _ptr(keep["betas"]), len(keep["pens"]), _ptr(keep["pens"]),
+                int(total_sweeps), int(sps), int(seed) & 0xFFFFFFFFFFFFFFFF, RULE[rule], RNG[rng_mode])
+    return p, c, keep
+
+
+def run(pr, betas, penalties, total_sweeps, sps=1, seed=1, rule="metropolis", rng="slot",
+        impl="port", states=False, grid=False, round_counters=False, threads=1,
+        final_grid=True) -> OracleResult:
+    """Run one 2D-PT trajectory on the C port (impl='port') or on a reference
+    build (impl='ref:<variant>')."""
+    p, c, keep = _marshal(pr, betas, penalties, total_sweeps, sps, seed, rule, rng)
+    I, J = len(keep["betas"]), len(keep["pens"])
+    R = I * J
+    rounds = int(total_sweeps) // max(int(sps), 1)
+    npp, nbb = I * max(J - 1, 0), max(I - 1, 0) * J
+    o = dict(
+        f=np.zeros(rounds), g=np.zeros(rounds), feasible=np.zeros(rounds, np.uint8),
+        digest=np.zeros(rounds, np.uint64),
+        states=np.zeros((rounds, pr.n), np.int8) if states else None,
+        grid_states=np.zeros((rounds, R, pr.n), np.int8) if grid else None,
+        round_acc_p=np.zeros((rounds, npp), np.int64) if round_counters else None,
+        round_acc_b=np.zeros((rounds, nbb), np.int64) if round_counters else None,
+        attempts_p=np.zeros(npp, np.int64), accepts_p=np.zeros(npp, np.int64),
+        attempts_b=np.zeros(nbb, np.int64), accepts_b=np.zeros(nbb, np.int64),
+        final_grid=np.zeros((R, pr.n), np.int8) if final_grid else None,
+    )
+    out = _Outputs(*[_ptr(o.get(k)) for k, _ in _Outputs._fields_])
+    err = C.create_string_buffer(512)
+    if impl == "port":
+        rc = port_lib().tgo_run_2dpt(C.byref(p), C.byref(c), C.byref(out), err, 512)
+    else:
+        variant = impl.split(":", 1)[1]
+        rc = ref_lib(variant).tgr_run_2dpt(C.byref(p), C.byref(c), C.byref(out), int(threads),
+                                           0, err, 512)
+    if rc != 0:
+        raise OracleError(rc, err.value.decode())
+    return OracleResult(o["f"], o["g"], o["feasible"].astype(bool), o["digest"], o["states"],
+                        o["attempts_p"], o["accepts_p"], o["attempts_b"], o["accepts_b"],
+                        o["round_acc_p"], o["round_acc_b"], o["final_grid"], o["grid_states"])
+
+
+def ref_timed(variant, pr, betas, penalties, total_sweeps, sps=1, seed=1, threads=1) -> float:
+    """Run the reference build once; returns the last target f (for timing legs)."""
+    p, c, keep = _marshal(pr, betas, penalties, total_sweeps, sps, seed, "metropolis", "slot")
+    err = C.create_string_buffer(512)
+    f = C.c_double(0.0)
+    rc = ref_lib(variant).tgr_run_2dpt_timed(C.byref(p), C.byref(c), int(threads), C.byref(f), err, 512)
+    if rc != 0:
+        raise OracleError(rc, err.value.decode())
+    return f.value
+
+
+def energy(pr, penalty: float, state: np.ndarray):
+    p, _, keep = _marshal(pr, [1.0], [penalty], 1, 1, 1, "metropolis", "slot")
+    s = np.ascontiguousarray(state, dtype=np.int8)
+    f, g = C.c_double(), C.c_double()
+    rc = port_lib().tgo_energy_breakdown(C.byref(p), C.c_double(penalty), _ptr(s), C.byref(f), C.byref(g))
+    if rc:
+        raise OracleError(rc, "energy")
+    return f.value, g.value
+
+
+def digest(state: np.ndarray) -> int:
+    s = np.ascontiguousarray(state, dtype=np.int8)
+    return int(port_lib().tgo_digest(_ptr(s), int(s.size)))
+
+
+def canonical_order(pr):
+    p, _, keep = _marshal(pr, [1.0], [0.0], 1, 1, 1, "metropolis", "slot")
+    color = np.zeros(pr.n, np.int32)
+    order = np.zeros(pr.n, np.int32)
+    nc = C.c_int32()
+    port_lib().tgo_canonical_order(C.byref(p), _ptr(color), _ptr(order), C.byref(nc))
+    return order, color, nc.value
+
+
+def philox(ctr, key):
+    c = np.asarray(ctr, dtype=np.uint32)
+    k = np.asarray(key, dtype=np.uint32)
+    o = np.zeros(4, np.uint32)
+    port_lib().tgo_philox(_ptr(c), _ptr(k), _ptr(o))
+    return o
+
+
+def derive_seed(master, purpose, index) -> int:
+    return int(port_lib().tgo_derive(master, purpose, index))
+
+
+def stream_bits(seed, n) -> int:
+    return int(port_lib().tgo_bits(seed, n))
+
+
+def plane_u53(gseed, t, site, lane) -> int:
+    return int(port_lib().tgo_plane(gseed, t, site, lane))
+
+
+def p_swap_probability(beta, dp, dg):
+    return port_lib().tgo_p_swap_probability(beta, dp, dg)
+
+
+def beta_swap_probability(db, de):
+    return port_lib().tgo_beta_swap_probability(db, de)
+
+
+def general_swap_probability(ba, bb, dea, deb):
+    return port_lib().tgo_general_swap_probability(ba, bb, dea, deb)

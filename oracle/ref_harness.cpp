@@ -1,0 +1,187 @@
+// oracle/ref_harness.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" adapter over the reference library's own entry point,
+// tempergrid::run_2dpt (/root/reference/proj/include/tempergrid/engine.hpp:62-63,
+// src/engine.cpp:83-219), compiled together with the reference sources into
+// oracle/_ref/libtgref_*.so (recipe: oracle/Makefile).  It takes the same
+// plain-array structs as the C port (tg_oracle.h) so tests can run the port,
+// the reference and the B200 engine on identical inputs.  Exceptions map to
+// the CLI's exit codes (cli.cpp:659-668): config_error -> 2, resource_error -> 3.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "tempergrid/constraints.hpp"
+#include "tempergrid/engine.hpp"
+#include "tempergrid/errors.hpp"
+#include "tempergrid/ising.hpp"
+#include "tempergrid/schedule.hpp"
+
+#include "philox_ref.h"
+#include "tg_oracle.h"
+
+namespace tgref_ctx {
+extern thread_local std::uint64_t master;
+extern thread_local int n_replicas;
+}  // namespace tgref_ctx
+
+#ifdef TGREF_NO_CTX
+namespace tgref_ctx {
+thread_local std::uint64_t master = 0;
+thread_local int n_replicas = 0;
+}  // namespace tgref_ctx
+#endif
+
+namespace {
+
+void put_err(char* err, int errlen, const std::string& msg) {
+    if (!err || errlen <= 0) return;
+    std::strncpy(err, msg.c_str(), static_cast<std::size_t>(errlen - 1));
+    err[errlen - 1] = '\0';
+}
+
+std::uint64_t digest(const tempergrid::SpinState& s) {
+    std::uint64_t d = 0;
+    for (std::size_t i = 0; i < s.size(); ++i)
+        if (s[i] > 0) d += tgo_digest_term(i);
+    return d;
+}
+
+}  // namespace
+
+extern "C" int tgr_run_2dpt(const tgo_problem* p, const tgo_run_cfg* cfg, tgo_outputs* out,
+                            int threads, int store_grid, char* err, int errlen) {
+    using namespace tempergrid;
+    try {
+        std::vector<Coupling> cs;
+        for (int k = 0; k < p->n_couplings; ++k) cs.push_back({p->ci[k], p->cj[k], p->cw[k]});
+        std::vector<double> h(p->fields, p->fields + p->n);
+        IsingModel cost(p->n, std::move(cs), std::move(h));
+        std::vector<std::pair<int, int>> pairs;
+        for (int k = 0; k < p->n_pairs; ++k) pairs.emplace_back(p->pa[k], p->pb[k]);
+        ConstrainedProblem problem{std::move(cost), ConstraintSet(p->n, std::move(pairs))};
+        Schedule schedule;
+        schedule.betas.assign(cfg->betas, cfg->betas + cfg->n_betas);
+        schedule.penalties.assign(cfg->penalties, cfg->penalties + cfg->n_penalties);
+        RunConfig rc;
+        rc.total_sweeps = cfg->total_sweeps;
+        rc.sweeps_per_swap = cfg->sweeps_per_swap;
+        rc.seed = cfg->seed;
+        rc.threads = threads;
+        rc.store_target_only = !(store_grid || out->grid_states || out->final_grid);
+        tgref_ctx::master = cfg->seed;
+        tgref_ctx::n_replicas = cfg->n_betas * cfg->n_penalties;
+
+        const Trace trace = run_2dpt(problem, schedule, rc);
+
+        const int n = p->n;
+        const int R = cfg->n_betas * cfg->n_penalties;
+        for (std::size_t k = 0; k < trace.records.size(); ++k) {
+            const TraceRecord& r = trace.records[k];
+            if (out->f) out->f[k] = r.f;
+            if (out->g) out->g[k] = r.g;
+            if (out->feasible) out->feasible[k] = r.feasible ? 1 : 0;
+            if (out->digest) out->digest[k] = digest(r.state);
+            if (out->states) std::memcpy(out->states + k * n, r.state.data(), n);
+            if (out->grid_states)
+                for (int q = 0; q < R; ++q)
+                    std::memcpy(out->grid_states + (k * R + q) * n, r.grid[q].data(), n);
+        }
+        if (!trace.records.empty()) {
+            const TraceRecord& last = trace.records.back();
+            if (out->final_grid)
+                for (int q = 0; q < R; ++q)
+                    std::memcpy(out->final_grid + static_cast<std::size_t>(q) * n,
+                                last.grid[q].data(), n);
+        }
+        // Cumulative acceptance rates are what the reference reports
+        // (engine.cpp:197-208); accepts = rate * attempts is exact for the
+        // counts involved, so recover integer counters per round.
+        const int I = cfg->n_betas, J = cfg->n_penalties;
+        std::vector<std::int64_t> att_p(I * std::max(0, J - 1), 0), att_b(std::max(0, I - 1) * J, 0);
+        {
+            // attempts are a deterministic function of the round schedule
+            int direction = 1;
+            for (std::size_t k = 0; k < trace.records.size(); ++k) {
+                const std::int64_t rn = static_cast<std::int64_t>(k) + 1;
+                const int even = rn % 2 == 0;
+                bool dp, db;
+                if (I == 1 && J == 1) dp = db = false;
+                else if (I == 1) { dp = true; db = false; }
+                else if (J == 1) { dp = false; db = true; }
+                else { dp = direction == 1; db = !dp; }
+                if (dp) for (int i = 0; i < I; ++i) for (int q = even; q + 1 < J; q += 2) ++att_p[i * (J - 1) + q];
+                if (db) for (int j = 0; j < J; ++j) for (int b = even; b + 1 < I; b += 2) ++att_b[b * J + j];
+                const TraceRecord& r = trace.records[k];
+                if (out->round_acc_p)
+                    for (std::size_t q = 0; q < att_p.size(); ++q)
+                        out->round_acc_p[k * att_p.size() + q] =
+                            static_cast<std::int64_t>(r.acceptance_rates_p[q] * att_p[q] + 0.5);
+                if (out->round_acc_b)
+                    for (std::size_t q = 0; q < att_b.size(); ++q)
+                        out->round_acc_b[k * att_b.size() + q] =
+                            static_cast<std::int64_t>(r.acceptance_rates_beta[q] * att_b[q] + 0.5);
+                if (even) direction = -direction;
+            }
+            if (!trace.records.empty()) {
+                const TraceRecord& r = trace.records.back();
+                for (std::size_t q = 0; q < att_p.size(); ++q) {
+                    if (out->attempts_p) out->attempts_p[q] = att_p[q];
+                    if (out->accepts_p) out->accepts_p[q] = static_cast<std::int64_t>(r.acceptance_rates_p[q] * att_p[q] + 0.5);
+                }
+                for (std::size_t q = 0; q < att_b.size(); ++q) {
+                    if (out->attempts_b) out->attempts_b[q] = att_b[q];
+                    if (out->accepts_b) out->accepts_b[q] = static_cast<std::int64_t>(r.acceptance_rates_beta[q] * att_b[q] + 0.5);
+                }
+            }
+        }
+        return 0;
+    } catch (const tempergrid::config_error& e) {
+        put_err(err, errlen, e.what());
+        return 2;
+    } catch (const tempergrid::resource_error& e) {
+        put_err(err, errlen, e.what());
+        return 3;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
+// Timing entry for bench.py's reference arm: run_2dpt on the given inputs,
+// discarding the trace (the reference still builds it in RAM, engine.cpp:189-214).
+extern "C" int tgr_run_2dpt_timed(const tgo_problem* p, const tgo_run_cfg* cfg, int threads,
+                                  double* f_last, char* err, int errlen) {
+    using namespace tempergrid;
+    try {
+        std::vector<Coupling> cs;
+        for (int k = 0; k < p->n_couplings; ++k) cs.push_back({p->ci[k], p->cj[k], p->cw[k]});
+        std::vector<double> h(p->fields, p->fields + p->n);
+        IsingModel cost(p->n, std::move(cs), std::move(h));
+        std::vector<std::pair<int, int>> pairs;
+        for (int k = 0; k < p->n_pairs; ++k) pairs.emplace_back(p->pa[k], p->pb[k]);
+        ConstrainedProblem problem{std::move(cost), ConstraintSet(p->n, std::move(pairs))};
+        Schedule schedule;
+        schedule.betas.assign(cfg->betas, cfg->betas + cfg->n_betas);
+        schedule.penalties.assign(cfg->penalties, cfg->penalties + cfg->n_penalties);
+        RunConfig rc;
+        rc.total_sweeps = cfg->total_sweeps;
+        rc.sweeps_per_swap = cfg->sweeps_per_swap;
+        rc.seed = cfg->seed;
+        rc.threads = threads;
+        tgref_ctx::master = cfg->seed;
+        tgref_ctx::n_replicas = cfg->n_betas * cfg->n_penalties;
+        const Trace trace = run_2dpt(problem, schedule, rc);
+        if (f_last) *f_last = trace.records.empty() ? 0.0 : trace.records.back().f;
+        return 0;
+    } catch (const tempergrid::config_error& e) {
+        put_err(err, errlen, e.what());
+        return 2;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return 1;
+    }
+}

@@ -1,0 +1,583 @@
+/*
+ * oracle/tg_oracle.c -- TEST INFRASTRUCTURE ONLY (parity checker for tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline leg; the product never
+ * links it).  Plain-C restatement of the reference 2D-PT hot path; every
+ * function cites the reference lines it follows (paths under
+ * /root/reference/proj).  The only departures from the reference are the ones
+ * the parity contract names: the mt19937_64 engine is replaced by the Philox
+ * stream of philox_ref.h, a heat-bath update rule is offered next to
+ * Metropolis, and an alternative RNG association (bit-plane draws keyed by the
+ * physical state) is offered next to the reference's per-slot streams.
+ * Floating-point expressions are written in the reference's evaluation order
+ * so that the port is bit-identical to the reference objects (checked against
+ * oracle/_ref in tests/test_oracle_ref.py).
+ */
+#include "tg_oracle.h"
+
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "philox_ref.h"
+
+#define REFRESH_INTERVAL 256 /* engine.cpp:79 kRefreshInterval */
+
+static void set_err(char* err, int errlen, const char* fmt, ...) {
+    if (!err || errlen <= 0) return;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(err, (size_t)errlen, fmt, ap);
+    va_end(ap);
+}
+
+/* ------------------------------------------------------------------ model */
+
+typedef struct {
+    int i, j;
+    double w;
+} coupling_t;
+
+typedef struct {
+    int n;
+    int m;
+    coupling_t* c; /* sorted canonical (i<j) */
+    double* h;
+    int* off;      /* CSR, neighbour order of ising.cpp:55-61 */
+    int* nbr;
+    double* nbw;
+} model_t;
+
+static int cmp_coupling(const void* a, const void* b) {
+    const coupling_t* x = (const coupling_t*)a;
+    const coupling_t* y = (const coupling_t*)b;
+    if (x->i != y->i) return x->i < y->i ? -1 : 1;
+    if (x->j != y->j) return x->j < y->j ? -1 : 1;
+    return 0;
+}
+
+static void model_free(model_t* m) {
+    free(m->c); free(m->h); free(m->off); free(m->nbr); free(m->nbw);
+    memset(m, 0, sizeof(*m));
+}
+
+/* IsingModel::IsingModel, ising.cpp:21-62 (validation, canonical sort, CSR). */
+static int model_build(model_t* m, int n, int nc, const int* ci, const int* cj,
+                       const double* cw, const double* h, char* err, int errlen) {
+    memset(m, 0, sizeof(*m));
+    if (n <= 0) { set_err(err, errlen, "model: n_spins must be positive"); return TGO_CONFIG_ERROR; }
+    m->n = n;
+    m->m = nc;
+    m->c = (coupling_t*)malloc(sizeof(coupling_t) * (size_t)(nc > 0 ? nc : 1));
+    m->h = (double*)malloc(sizeof(double) * (size_t)n);
+    for (int i = 0; i < n; ++i) m->h[i] = h ? h[i] : 0.0;
+    for (int k = 0; k < nc; ++k) {
+        int a = ci[k], b = cj[k];
+        if (a == b) { set_err(err, errlen, "model: self-loop on spin %d", a); model_free(m); return TGO_CONFIG_ERROR; }
+        if (a > b) { int t = a; a = b; b = t; }
+        if (a < 0 || b >= n) {
+            set_err(err, errlen, "model: coupling index out of range: (%d, %d)", a, b);
+            model_free(m);
+            return TGO_CONFIG_ERROR;
+        }
+        m->c[k].i = a; m->c[k].j = b; m->c[k].w = cw[k];
+    }
+    /* std::sort is not stable, but keys are unique after the duplicate check. */
+    qsort(m->c, (size_t)nc, sizeof(coupling_t), cmp_coupling);
+    for (int k = 1; k < nc; ++k)
+        if (m->c[k - 1].i == m->c[k].i && m->c[k - 1].j == m->c[k].j) {
+            set_err(err, errlen, "model: duplicate coupling (%d, %d)", m->c[k].i, m->c[k].j);
+            model_free(m);
+            return TGO_CONFIG_ERROR;
+        }
+    int* deg = (int*)calloc((size_t)n, sizeof(int));
+    for (int k = 0; k < nc; ++k) { deg[m->c[k].i]++; deg[m->c[k].j]++; }
+    m->off = (int*)malloc(sizeof(int) * (size_t)(n + 1));
+    m->off[0] = 0;
+    for (int i = 0; i < n; ++i) m->off[i + 1] = m->off[i] + deg[i];
+    m->nbr = (int*)malloc(sizeof(int) * (size_t)(m->off[n] > 0 ? m->off[n] : 1));
+    m->nbw = (double*)malloc(sizeof(double) * (size_t)(m->off[n] > 0 ? m->off[n] : 1));
+    int* cur = deg; /* reuse as cursor */
+    for (int i = 0; i < n; ++i) cur[i] = m->off[i];
+    for (int k = 0; k < nc; ++k) {
+        const coupling_t c = m->c[k];
+        m->nbr[cur[c.i]] = c.j; m->nbw[cur[c.i]++] = c.w;
+        m->nbr[cur[c.j]] = c.i; m->nbw[cur[c.j]++] = c.w;
+    }
+    free(deg);
+    return TGO_OK;
+}
+
+/* energy, ising.cpp:70-77 */
+static double model_energy(const model_t* m, const int8_t* s) {
+    double e = 0.0;
+    for (int k = 0; k < m->m; ++k) {
+        const coupling_t c = m->c[k];
+        e -= c.w * (double)s[c.i] * (double)s[c.j];
+    }
+    for (int i = 0; i < m->n; ++i) e -= m->h[i] * (double)s[i];
+    return e;
+}
+
+/* local_fields, ising.cpp:79-88 */
+static void model_local_fields(const model_t* m, const int8_t* s, double* local) {
+    for (int i = 0; i < m->n; ++i) {
+        double sum = m->h[i];
+        for (int k = m->off[i]; k < m->off[i + 1]; ++k) sum += m->nbw[k] * (double)s[m->nbr[k]];
+        local[i] = sum;
+    }
+}
+
+/* apply_flip, ising.cpp:90-96 */
+static void model_apply_flip(const model_t* m, int8_t* s, int i, double* local) {
+    s[i] = (int8_t)-s[i];
+    const double two_si = 2.0 * (double)s[i];
+    for (int k = m->off[i]; k < m->off[i + 1]; ++k) local[m->nbr[k]] += two_si * m->nbw[k];
+}
+
+/* ------------------------------------------------------------ constraints */
+
+typedef struct {
+    int n;
+    int m;
+    int* pa; /* normalised a<b, input order */
+    int* pb;
+    int* off;
+    int* partners;
+} cset_t;
+
+static void cset_free(cset_t* c) {
+    free(c->pa); free(c->pb); free(c->off); free(c->partners);
+    memset(c, 0, sizeof(*c));
+}
+
+/* ConstraintSet::ConstraintSet, constraints.cpp:16-39 */
+static int cset_build(cset_t* c, int n, int np, const int* pa, const int* pb, char* err, int errlen) {
+    memset(c, 0, sizeof(*c));
+    c->n = n;
+    c->m = np;
+    c->pa = (int*)malloc(sizeof(int) * (size_t)(np > 0 ? np : 1));
+    c->pb = (int*)malloc(sizeof(int) * (size_t)(np > 0 ? np : 1));
+    for (int k = 0; k < np; ++k) {
+        int a = pa[k], b = pb[k];
+        if (a == b) { set_err(err, errlen, "constraint: pair on a single spin %d", a); cset_free(c); return TGO_CONFIG_ERROR; }
+        if (a > b) { int t = a; a = b; b = t; }
+        if (a < 0 || b >= n) {
+            set_err(err, errlen, "constraint: index out of range: (%d, %d)", a, b);
+            cset_free(c);
+            return TGO_CONFIG_ERROR;
+        }
+        c->pa[k] = a; c->pb[k] = b;
+    }
+    int* deg = (int*)calloc((size_t)n, sizeof(int));
+    for (int k = 0; k < np; ++k) { deg[c->pa[k]]++; deg[c->pb[k]]++; }
+    c->off = (int*)malloc(sizeof(int) * (size_t)(n + 1));
+    c->off[0] = 0;
+    for (int i = 0; i < n; ++i) c->off[i + 1] = c->off[i] + deg[i];
+    c->partners = (int*)malloc(sizeof(int) * (size_t)(c->off[n] > 0 ? c->off[n] : 1));
+    for (int i = 0; i < n; ++i) deg[i] = c->off[i];
+    for (int k = 0; k < np; ++k) {
+        c->partners[deg[c->pa[k]]++] = c->pb[k];
+        c->partners[deg[c->pb[k]]++] = c->pa[k];
+    }
+    free(deg);
+    return TGO_OK;
+}
+
+/* ConstraintSet::evaluate, constraints.cpp:41-48 */
+static double cset_evaluate(const cset_t* c, const int8_t* s) {
+    double g = 0.0;
+    for (int k = 0; k < c->m; ++k) {
+        const double d = (double)s[c->pa[k]] - (double)s[c->pb[k]];
+        g += d * d;
+    }
+    return g;
+}
+
+/* ConstraintSet::delta_flip, constraints.hpp:32-37 */
+static double cset_delta_flip(const cset_t* c, const int8_t* s, int i) {
+    double d = 0.0;
+    for (int k = c->off[i]; k < c->off[i + 1]; ++k) d += 4.0 * (double)s[i] * (double)s[c->partners[k]];
+    return d;
+}
+
+/* ------------------------------------------------------- effective model */
+
+typedef struct {
+    model_t merged;
+    const cset_t* cs;
+    double penalty;
+    double offset;
+} view_t;
+
+typedef struct {
+    int a, b, ord;
+    double w;
+} wentry_t;
+
+static int cmp_wentry(const void* x, const void* y) {
+    const wentry_t* p = (const wentry_t*)x;
+    const wentry_t* q = (const wentry_t*)y;
+    if (p->a != q->a) return p->a < q->a ? -1 : 1;
+    if (p->b != q->b) return p->b < q->b ? -1 : 1;
+    return p->ord < q->ord ? -1 : (p->ord > q->ord);
+}
+
+/* build_effective, constraints.cpp:122-140: every pair merged as a +2P
+ * coupling (std::map accumulation order: cost weight first, then pairs in
+ * input order), offset 2P*m. */
+static int view_build(view_t* v, const model_t* cost, const cset_t* cs, double penalty,
+                      char* err, int errlen) {
+    memset(v, 0, sizeof(*v));
+    if (penalty < 0.0) { set_err(err, errlen, "build_effective: penalty must be >= 0"); return TGO_CONFIG_ERROR; }
+    const int tot = cost->m + cs->m;
+    wentry_t* e = (wentry_t*)malloc(sizeof(wentry_t) * (size_t)(tot > 0 ? tot : 1));
+    int k = 0;
+    for (int q = 0; q < cost->m; ++q, ++k) { e[k].a = cost->c[q].i; e[k].b = cost->c[q].j; e[k].w = cost->c[q].w; e[k].ord = k; }
+    for (int q = 0; q < cs->m; ++q, ++k) { e[k].a = cs->pa[q]; e[k].b = cs->pb[q]; e[k].w = 2.0 * penalty; e[k].ord = k; }
+    qsort(e, (size_t)tot, sizeof(wentry_t), cmp_wentry);
+    int* mi = (int*)malloc(sizeof(int) * (size_t)(tot > 0 ? tot : 1));
+    int* mj = (int*)malloc(sizeof(int) * (size_t)(tot > 0 ? tot : 1));
+    double* mw = (double*)malloc(sizeof(double) * (size_t)(tot > 0 ? tot : 1));
+    int nm = 0;
+    for (int q = 0; q < tot;) {
+        double w = 0.0;
+        int r = q;
+        while (r < tot && e[r].a == e[q].a && e[r].b == e[q].b) { w += e[r].w; ++r; }
+        mi[nm] = e[q].a; mj[nm] = e[q].b; mw[nm] = w; ++nm;
+        q = r;
+    }
+    int rc = model_build(&v->merged, cost->n, nm, mi, mj, mw, cost->h, err, errlen);
+    free(e); free(mi); free(mj); free(mw);
+    if (rc) return rc;
+    v->cs = cs;
+    v->penalty = penalty;
+    v->offset = 2.0 * penalty * (double)cs->m;
+    return TGO_OK;
+}
+
+/* energy_breakdown, constraints.cpp:142-147 */
+static void view_breakdown(const view_t* v, const int8_t* s, double* f, double* g) {
+    const double gg = cset_evaluate(v->cs, s);
+    const double eff = model_energy(&v->merged, s) + v->offset;
+    *g = gg;
+    *f = eff - v->penalty * gg;
+}
+
+/* ------------------------------------------------------------- replicas */
+
+typedef struct {
+    int8_t* spins;
+    double* local;
+    double f, g;
+    int id; /* physical state id = initial slot; travels with the state */
+} rstate_t;
+
+/* refresh_sweep_state, mc.cpp:14-19 */
+static void refresh(const view_t* v, rstate_t* st) {
+    model_local_fields(&v->merged, st->spins, st->local);
+    view_breakdown(v, st->spins, &st->f, &st->g);
+}
+
+typedef struct {
+    int mode;
+    uint64_t slot_seed;  /* SLOT: derive_seed(seed, replica, slot) */
+    uint64_t* slot_ctr;  /* SLOT: 64-bit outputs consumed so far */
+    const uint64_t* gseed; /* PLANE: per-group keys */
+    uint64_t t;          /* PLANE: global sweep index */
+} draw_ctx_t;
+
+static inline uint64_t next_u53(draw_ctx_t* d, const rstate_t* st, int site) {
+    if (d->mode == TGO_RNG_SLOT) {
+        const uint64_t b = tgo_stream_bits(d->slot_seed, (*d->slot_ctr)++);
+        return b >> 11; /* rng.hpp:53-55 */
+    }
+    return tgo_plane_u53(d->gseed[st->id >> 5], d->t, (uint32_t)site, st->id & 31);
+}
+
+/* metropolis_sweep, mc.cpp:21-35 (rule 0); heat-bath variant (rule 1) with
+ * the same one-draw-per-spin contract and the same f/g bookkeeping. */
+static void sweep(const view_t* v, double beta, rstate_t* st, draw_ctx_t* d, int rule) {
+    const int n = v->merged.n;
+    for (int i = 0; i < n; ++i) {
+        const double local_i = st->local[i];
+        const double de = 2.0 * (double)st->spins[i] * local_i;
+        const double u = tgo_u53_to_unit(next_u53(d, st, i));
+        int flip;
+        if (rule == TGO_RULE_METROPOLIS) {
+            flip = (de <= 0.0 || u < exp(-beta * de));
+        } else {
+            const double p = 1.0 / (1.0 + exp(-2.0 * beta * local_i));
+            const int8_t nv = (u < p) ? (int8_t)1 : (int8_t)-1;
+            flip = nv != st->spins[i];
+        }
+        if (flip) {
+            const double dg = cset_delta_flip(v->cs, st->spins, i);
+            model_apply_flip(&v->merged, st->spins, i, st->local);
+            st->f += de - v->penalty * dg;
+            st->g += dg;
+        }
+    }
+}
+
+/* ------------------------------------------------------------ public API */
+
+double tgo_p_swap_probability(double beta, double d_penalty, double dg) {
+    const double x = beta * d_penalty * dg; /* engine.cpp:18-21 */
+    return x >= 0.0 ? 1.0 : exp(x);
+}
+double tgo_beta_swap_probability(double d_beta, double d_energy) {
+    const double x = d_beta * d_energy; /* engine.cpp:23-26 */
+    return x >= 0.0 ? 1.0 : exp(x);
+}
+double tgo_general_swap_probability(double beta_a, double beta_b, double de_a, double de_b) {
+    const double x = beta_a * de_a + beta_b * de_b; /* engine.cpp:28-32 */
+    return x >= 0.0 ? 1.0 : exp(x);
+}
+
+uint64_t tgo_digest(const int8_t* s, int n) {
+    uint64_t d = 0;
+    for (int i = 0; i < n; ++i)
+        if (s[i] > 0) d += tgo_digest_term((uint64_t)i);
+    return d;
+}
+
+uint64_t tgo_encode_state(const int8_t* s, int n) { /* oracle.cpp:17-22 */
+    uint64_t e = 0;
+    for (int i = 0; i < n && i < 64; ++i)
+        if (s[i] > 0) e |= (uint64_t)1 << i;
+    return e;
+}
+
+void tgo_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    tgo_philox4x32_10(ctr, key, out);
+}
+uint64_t tgo_derive(uint64_t master, uint64_t purpose, uint64_t index) {
+    return tgo_derive_seed(master, purpose, index);
+}
+uint64_t tgo_bits(uint64_t seed, uint64_t n) { return tgo_stream_bits(seed, n); }
+uint64_t tgo_plane(uint64_t gseed, uint64_t t, uint32_t site, int lane) {
+    return tgo_plane_u53(gseed, t, site, lane);
+}
+
+int tgo_energy_breakdown(const tgo_problem* p, double penalty, const int8_t* s, double* f,
+                         double* g) {
+    model_t cost;
+    cset_t cs;
+    view_t v;
+    char err[256];
+    int rc = model_build(&cost, p->n, p->n_couplings, p->ci, p->cj, p->cw, p->fields, err, 256);
+    if (rc) return rc;
+    rc = cset_build(&cs, p->n, p->n_pairs, p->pa, p->pb, err, 256);
+    if (rc) { model_free(&cost); return rc; }
+    rc = view_build(&v, &cost, &cs, penalty, err, 256);
+    if (!rc) { view_breakdown(&v, s, f, g); model_free(&v.merged); }
+    cset_free(&cs);
+    model_free(&cost);
+    return rc;
+}
+
+/* Greedy colouring in index order over cost couplings and chain pairs, then
+ * the canonical order: stable sort by (colour, chain degree, cost degree).
+ * This is the relabel under which a sequential index-order sweep equals a
+ * chromatic sweep (no two same-colour spins are adjacent). */
+int tgo_canonical_order(const tgo_problem* p, int32_t* color, int32_t* order, int32_t* n_colors) {
+    const int n = p->n;
+    int* dc = (int*)calloc((size_t)n, sizeof(int));
+    int* dq = (int*)calloc((size_t)n, sizeof(int));
+    int* deg = (int*)calloc((size_t)n, sizeof(int));
+    for (int k = 0; k < p->n_couplings; ++k) { dc[p->ci[k]]++; dc[p->cj[k]]++; }
+    for (int k = 0; k < p->n_pairs; ++k) { dq[p->pa[k]]++; dq[p->pb[k]]++; }
+    for (int i = 0; i < n; ++i) deg[i] = dc[i] + dq[i];
+    int* off = (int*)malloc(sizeof(int) * (size_t)(n + 1));
+    off[0] = 0;
+    for (int i = 0; i < n; ++i) off[i + 1] = off[i] + deg[i];
+    int* adj = (int*)malloc(sizeof(int) * (size_t)(off[n] > 0 ? off[n] : 1));
+    int* cur = (int*)malloc(sizeof(int) * (size_t)(n > 0 ? n : 1));
+    for (int i = 0; i < n; ++i) cur[i] = off[i];
+    for (int k = 0; k < p->n_couplings; ++k) { adj[cur[p->ci[k]]++] = p->cj[k]; adj[cur[p->cj[k]]++] = p->ci[k]; }
+    for (int k = 0; k < p->n_pairs; ++k) { adj[cur[p->pa[k]]++] = p->pb[k]; adj[cur[p->pb[k]]++] = p->pa[k]; }
+    int maxc = 0;
+    unsigned char* used = (unsigned char*)calloc((size_t)n + 2, 1);
+    for (int i = 0; i < n; ++i) {
+        for (int k = off[i]; k < off[i + 1]; ++k)
+            if (adj[k] < i) used[color[adj[k]]] = 1;
+        int c = 0;
+        while (used[c]) ++c;
+        color[i] = c;
+        if (c + 1 > maxc) maxc = c + 1;
+        for (int k = off[i]; k < off[i + 1]; ++k)
+            if (adj[k] < i) used[color[adj[k]]] = 0;
+    }
+    /* stable counting sort by key (color, dq, dc) */
+    int nq = 0, ncd = 0;
+    for (int i = 0; i < n; ++i) { if (dq[i] + 1 > nq) nq = dq[i] + 1; if (dc[i] + 1 > ncd) ncd = dc[i] + 1; }
+    int pos = 0;
+    for (int c = 0; c < maxc; ++c)
+        for (int q = 0; q < nq; ++q)
+            for (int d = 0; d < ncd; ++d)
+                for (int i = 0; i < n; ++i)
+                    if (color[i] == c && dq[i] == q && dc[i] == d) order[pos++] = i;
+    *n_colors = maxc;
+    free(dc); free(dq); free(deg); free(off); free(adj); free(cur); free(used);
+    return TGO_OK;
+}
+
+static int check_monotone(const double* v, int len, const char* what, char* err, int errlen) {
+    /* engine.cpp:41-52 */
+    if (len <= 0) { set_err(err, errlen, "%s vector must be non-empty", what); return TGO_CONFIG_ERROR; }
+    for (int k = 0; k < len; ++k)
+        if (!isfinite(v[k])) { set_err(err, errlen, "%s entries must be finite", what); return TGO_CONFIG_ERROR; }
+    for (int k = 1; k < len; ++k)
+        if (v[k] <= v[k - 1]) { set_err(err, errlen, "%s vector must be strictly increasing", what); return TGO_CONFIG_ERROR; }
+    return TGO_OK;
+}
+
+int tgo_run_2dpt(const tgo_problem* prob, const tgo_run_cfg* cfg, tgo_outputs* out, char* err,
+                 int errlen) {
+    model_t cost;
+    cset_t cs;
+    int rc = model_build(&cost, prob->n, prob->n_couplings, prob->ci, prob->cj, prob->cw,
+                         prob->fields, err, errlen);
+    if (rc) return rc;
+    rc = cset_build(&cs, prob->n, prob->n_pairs, prob->pa, prob->pb, err, errlen);
+    if (rc) { model_free(&cost); return rc; }
+
+    /* engine.cpp:85-87, 53-59 */
+    if ((rc = check_monotone(cfg->betas, cfg->n_betas, "beta", err, errlen)) ||
+        (rc = check_monotone(cfg->penalties, cfg->n_penalties, "penalty", err, errlen))) {
+        cset_free(&cs); model_free(&cost); return rc;
+    }
+    if (cfg->sweeps_per_swap < 1) { set_err(err, errlen, "run: sweeps_per_swap must be >= 1"); rc = TGO_CONFIG_ERROR; }
+    else if (cfg->total_sweeps < cfg->sweeps_per_swap) { set_err(err, errlen, "run: total_sweeps must be >= sweeps_per_swap"); rc = TGO_CONFIG_ERROR; }
+    if (rc) { cset_free(&cs); model_free(&cost); return rc; }
+
+    const int I = cfg->n_betas, J = cfg->n_penalties, R = I * J, n = prob->n;
+    view_t* views = (view_t*)calloc((size_t)J, sizeof(view_t));
+    for (int j = 0; j < J; ++j) {
+        rc = view_build(&views[j], &cost, &cs, cfg->penalties[j], err, errlen);
+        if (rc) {
+            for (int q = 0; q < j; ++q) model_free(&views[q].merged);
+            free(views); cset_free(&cs); model_free(&cost); return rc;
+        }
+    }
+
+    rstate_t* rep = (rstate_t*)calloc((size_t)R, sizeof(rstate_t));
+    uint64_t* slot_seed = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)R);
+    uint64_t* slot_ctr = (uint64_t*)calloc((size_t)R, sizeof(uint64_t));
+    const int n_groups = (R + 31) / 32;
+    uint64_t* gseed = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)n_groups);
+    for (int g = 0; g < n_groups; ++g) gseed[g] = tgo_derive_seed(cfg->seed, TGO_PURPOSE_PLANE, (uint64_t)g);
+    for (int r = 0; r < R; ++r) { /* engine.cpp:98-106 */
+        rep[r].spins = (int8_t*)malloc((size_t)n);
+        rep[r].local = (double*)malloc(sizeof(double) * (size_t)n);
+        rep[r].id = r;
+        const uint64_t iseed = tgo_derive_seed(cfg->seed, TGO_PURPOSE_INIT, (uint64_t)r);
+        for (int i = 0; i < n; ++i) /* random_state, ising.cpp:15-19 */
+            rep[r].spins[i] = (tgo_stream_bits(iseed, (uint64_t)i) >> 63) ? (int8_t)1 : (int8_t)-1;
+        refresh(&views[r % J], &rep[r]);
+        slot_seed[r] = tgo_derive_seed(cfg->seed, TGO_PURPOSE_REPLICA, (uint64_t)r);
+    }
+    const uint64_t swap_seed = tgo_derive_seed(cfg->seed, TGO_PURPOSE_SWAP, 0);
+    uint64_t swap_ctr = 0;
+
+    const int np = I * (J > 1 ? J - 1 : 0);
+    const int nb = (I > 1 ? I - 1 : 0) * J;
+    int64_t* att_p = (int64_t*)calloc((size_t)(np + 1), sizeof(int64_t));
+    int64_t* acc_p = (int64_t*)calloc((size_t)(np + 1), sizeof(int64_t));
+    int64_t* att_b = (int64_t*)calloc((size_t)(nb + 1), sizeof(int64_t));
+    int64_t* acc_b = (int64_t*)calloc((size_t)(nb + 1), sizeof(int64_t));
+
+    const int64_t sps = cfg->sweeps_per_swap;
+    const int64_t n_swap = cfg->total_sweeps / sps;
+    int direction = 1;
+    for (int64_t rn = 1; rn <= n_swap; ++rn) { /* engine.cpp:121-217 */
+        const int even_swap = (rn % 2 == 0) ? 1 : 0;
+        for (int r = 0; r < R; ++r) {
+            const view_t* v = &views[r % J];
+            const double beta = cfg->betas[r / J];
+            for (int64_t s = 0; s < sps; ++s) {
+                draw_ctx_t d;
+                d.mode = cfg->rng_mode;
+                d.slot_seed = slot_seed[r];
+                d.slot_ctr = &slot_ctr[r];
+                d.gseed = gseed;
+                d.t = (uint64_t)((rn - 1) * sps + s);
+                sweep(v, beta, &rep[r], &d, cfg->rule);
+            }
+            if (rn % REFRESH_INTERVAL == 0) refresh(v, &rep[r]);
+        }
+        int do_p, do_b;
+        if (I == 1 && J == 1) { do_p = do_b = 0; }
+        else if (I == 1) { do_p = 1; do_b = 0; }
+        else if (J == 1) { do_p = 0; do_b = 1; }
+        else { do_p = direction == 1; do_b = !do_p; }
+
+        if (do_p) { /* engine.cpp:148-167 */
+            for (int i = 0; i < I; ++i)
+                for (int p = even_swap; p + 1 < J; p += 2) {
+                    rstate_t* a = &rep[i * J + p];
+                    rstate_t* b = &rep[i * J + p + 1];
+                    const double x = cfg->betas[i] * (cfg->penalties[p + 1] - cfg->penalties[p]) * (b->g - a->g);
+                    const double u = tgo_u53_to_unit(tgo_stream_bits(swap_seed, swap_ctr++) >> 11);
+                    ++att_p[i * (J - 1) + p];
+                    if (x >= 0.0 || u < exp(x)) {
+                        rstate_t t = *a; *a = *b; *b = t;
+                        refresh(&views[p], a);
+                        refresh(&views[p + 1], b);
+                        ++acc_p[i * (J - 1) + p];
+                    }
+                }
+        }
+        if (do_b) { /* engine.cpp:168-187 */
+            for (int j = 0; j < J; ++j)
+                for (int b = even_swap; b + 1 < I; b += 2) {
+                    rstate_t* lo = &rep[b * J + j];
+                    rstate_t* hi = &rep[(b + 1) * J + j];
+                    const double pj = cfg->penalties[j];
+                    const double e_lo = lo->f + pj * lo->g;
+                    const double e_hi = hi->f + pj * hi->g;
+                    const double x = (cfg->betas[b + 1] - cfg->betas[b]) * (e_hi - e_lo);
+                    const double u = tgo_u53_to_unit(tgo_stream_bits(swap_seed, swap_ctr++) >> 11);
+                    ++att_b[b * J + j];
+                    if (x >= 0.0 || u < exp(x)) {
+                        rstate_t t = *lo; *lo = *hi; *hi = t;
+                        ++acc_b[b * J + j];
+                    }
+                }
+        }
+        /* record, engine.cpp:189-214 */
+        const rstate_t* tg = &rep[R - 1];
+        const int64_t k = rn - 1;
+        if (out->f) out->f[k] = tg->f;
+        if (out->g) out->g[k] = tg->g;
+        if (out->feasible) out->feasible[k] = (uint8_t)(tg->g == 0.0);
+        if (out->digest) out->digest[k] = tgo_digest(tg->spins, n);
+        if (out->states) memcpy(out->states + k * n, tg->spins, (size_t)n);
+        if (out->grid_states)
+            for (int r = 0; r < R; ++r) memcpy(out->grid_states + (k * R + r) * n, rep[r].spins, (size_t)n);
+        if (out->round_acc_p && np) memcpy(out->round_acc_p + k * np, acc_p, sizeof(int64_t) * (size_t)np);
+        if (out->round_acc_b && nb) memcpy(out->round_acc_b + k * nb, acc_b, sizeof(int64_t) * (size_t)nb);
+        if (even_swap) direction = -direction;
+    }
+    if (out->attempts_p) memcpy(out->attempts_p, att_p, sizeof(int64_t) * (size_t)np);
+    if (out->accepts_p) memcpy(out->accepts_p, acc_p, sizeof(int64_t) * (size_t)np);
+    if (out->attempts_b) memcpy(out->attempts_b, att_b, sizeof(int64_t) * (size_t)nb);
+    if (out->accepts_b) memcpy(out->accepts_b, acc_b, sizeof(int64_t) * (size_t)nb);
+    for (int r = 0; r < R; ++r) {
+        if (out->final_grid) memcpy(out->final_grid + (size_t)r * n, rep[r].spins, (size_t)n);
+        if (out->final_f) out->final_f[r] = rep[r].f;
+        if (out->final_g) out->final_g[r] = rep[r].g;
+        if (out->final_state_id) out->final_state_id[r] = rep[r].id;
+    }
+
+    for (int r = 0; r < R; ++r) { free(rep[r].spins); free(rep[r].local); }
+    free(rep); free(slot_seed); free(slot_ctr); free(gseed);
+    free(att_p); free(acc_p); free(att_b); free(acc_b);
+    for (int j = 0; j < J; ++j) model_free(&views[j].merged);
+    free(views);
+    cset_free(&cs);
+    model_free(&cost);
+    return TGO_OK;
+}

@@ -1,0 +1,104 @@
+/*
+ * oracle/tg_oracle.h -- TEST INFRASTRUCTURE ONLY.  C restatement ("port") of
+ * the reference 2D-PT hot path, used by tests/ and by bench.py's cpu_baseline
+ * leg as the parity checker.  Nothing in paper_2506_14781_b200/ links it.
+ *
+ * Restates (file:line under /root/reference/proj):
+ *   IsingModel ctor / CSR / energy / local_fields / apply_flip   src/ising.cpp:21-96
+ *   ConstraintSet ctor / evaluate / delta_flip                   src/constraints.cpp:16-48,
+ *                                                                include/tempergrid/constraints.hpp:32-37
+ *   build_effective / energy_breakdown                           src/constraints.cpp:122-147
+ *   make_sweep_state / refresh_sweep_state / metropolis_sweep    src/mc.cpp:7-35
+ *   swap probabilities, validation, run_2dpt round loop          src/engine.cpp:18-219
+ *   encode_state                                                 src/oracle.cpp:17-22
+ */
+#ifndef TG_ORACLE_H
+#define TG_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { TGO_OK = 0, TGO_CONFIG_ERROR = 2, TGO_RESOURCE_ERROR = 3 };
+enum { TGO_RULE_METROPOLIS = 0, TGO_RULE_HEAT_BATH = 1 };
+/* RNG association: SLOT = reference (stream stays with the grid slot,
+ * engine.cpp:36-39,160,182); PLANE = bit-plane draws keyed by physical state. */
+enum { TGO_RNG_SLOT = 0, TGO_RNG_PLANE = 1 };
+
+typedef struct {
+    int n;
+    int n_couplings;
+    const int* ci;
+    const int* cj;
+    const double* cw;
+    const double* fields; /* length n */
+    int n_pairs;
+    const int* pa;
+    const int* pb;
+} tgo_problem;
+
+typedef struct {
+    int n_betas;
+    const double* betas;
+    int n_penalties;
+    const double* penalties;
+    int64_t total_sweeps;
+    int64_t sweeps_per_swap;
+    uint64_t seed;
+    int rule;
+    int rng_mode;
+} tgo_run_cfg;
+
+/* Caller-allocated outputs; any pointer may be NULL. */
+typedef struct {
+    double* f;              /* [rounds] target f */
+    double* g;              /* [rounds] target g */
+    uint8_t* feasible;      /* [rounds] */
+    uint64_t* digest;       /* [rounds] target-state digest */
+    int8_t* states;         /* [rounds * n] target states */
+    int8_t* grid_states;    /* [rounds * R * n] every slot's state (store_target_only=false) */
+    int64_t* round_acc_p;   /* [rounds * I*(J-1)] cumulative P accepts */
+    int64_t* round_acc_b;   /* [rounds * (I-1)*J] cumulative beta accepts */
+    int64_t* attempts_p;    /* [I*(J-1)] final */
+    int64_t* accepts_p;
+    int64_t* attempts_b;    /* [(I-1)*J] final */
+    int64_t* accepts_b;
+    int8_t* final_grid;     /* [R * n] final state at each slot */
+    double* final_f;        /* [R] per slot */
+    double* final_g;        /* [R] per slot */
+    int32_t* final_state_id;/* [R] physical state id (initial slot) now at each slot */
+} tgo_outputs;
+
+int tgo_run_2dpt(const tgo_problem* prob, const tgo_run_cfg* cfg, tgo_outputs* out,
+                 char* err, int errlen);
+
+/* engine.cpp:18-32 */
+double tgo_p_swap_probability(double beta, double d_penalty, double dg);
+double tgo_beta_swap_probability(double d_beta, double d_energy);
+double tgo_general_swap_probability(double beta_a, double beta_b, double de_a, double de_b);
+
+/* Cost energy f, constraint g, and effective total of one state (ising.cpp:70-77,
+ * constraints.cpp:41-48,142-147). */
+int tgo_energy_breakdown(const tgo_problem* prob, double penalty, const int8_t* s,
+                         double* f, double* g);
+uint64_t tgo_digest(const int8_t* s, int n);
+uint64_t tgo_encode_state(const int8_t* s, int n);
+
+/* Greedy index-order colouring of the cost+chain graph and the canonical
+ * site order (stable sort by colour, chain degree, cost degree). */
+int tgo_canonical_order(const tgo_problem* prob, int32_t* color, int32_t* order,
+                        int32_t* n_colors);
+
+/* Philox helpers for KAT tests. */
+void tgo_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+uint64_t tgo_derive(uint64_t master, uint64_t purpose, uint64_t index);
+uint64_t tgo_bits(uint64_t seed, uint64_t n);
+uint64_t tgo_plane(uint64_t gseed, uint64_t t, uint32_t site, int lane);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif
