@@ -1,0 +1,175 @@
+/*
+ * tempergrid_b200.h -- C ABI of the B200-native 2D parallel-tempering engine.
+ *
+ * This is the drop-in boundary for the hot path of the reference library
+ * `tempergrid` (arXiv 2506.14781): the RNG, sweep, swap and observable
+ * machinery under
+ *     Trace tempergrid::run_2dpt(const ConstrainedProblem&, const Schedule&,
+ *                                const RunConfig&)
+ *   (/root/reference/proj/include/tempergrid/engine.hpp:62-63,
+ *    /root/reference/proj/src/engine.cpp:83-219).
+ * The reference has no FFI of its own; these entry points are what a
+ * reference-side binding needs to replace run_2dpt (INTEGRATION.md shows the
+ * C++ shim and a ctypes stub).  Plain pointers and sizes only; no exceptions
+ * cross the boundary.  Status codes mirror the reference CLI's exit codes
+ * (cli.cpp:659-668): config_error -> 2, resource_error -> 3.
+ *
+ * Ownership: the caller owns every host buffer (copied in or written out);
+ * the context owns all device memory.  One context is driven by one host
+ * thread.  Multi-GPU: one context per GPU/process, joined by
+ * tg_create_distributed with an NCCL unique id.
+ */
+#ifndef TEMPERGRID_B200_H
+#define TEMPERGRID_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TG_ABI_VERSION 1
+
+typedef struct tg_ctx tg_ctx;
+
+enum tg_status {
+    TG_OK = 0,
+    TG_ERR_INTERNAL = 1,
+    TG_ERR_CONFIG = 2,   /* reference config_error   (errors.hpp:10-12)  */
+    TG_ERR_RESOURCE = 3, /* reference resource_error (errors.hpp:16-18)  */
+    TG_ERR_CUDA = 4,     /* no device / CUDA or NCCL failure              */
+    TG_ERR_SINK = 5      /* the record sink asked to stop                 */
+};
+
+/* Update rule. METROPOLIS restates metropolis_sweep (mc.cpp:21-35);
+ * HEAT_BATH is the north-star p-bit rule s_i = +1 iff u < sigma(2 beta h_i). */
+enum tg_rule { TG_RULE_METROPOLIS = 0, TG_RULE_HEAT_BATH = 1 };
+
+/* Engine.  SLOT: int8 spins, one CTA per replica, FP64 fields, draws from the
+ * reference's per-slot streams (bit-exact vs the reference fed Philox draws).
+ * PLANE: multi-spin-coded bit planes (32 replicas per word), threshold tables,
+ * lazily consumed bit-plane draws keyed by physical replica; requires J = +-1,
+ * h = 0 (the integer-coupling instances).  AUTO picks PLANE when eligible. */
+enum tg_engine { TG_ENGINE_AUTO = 0, TG_ENGINE_SLOT = 1, TG_ENGINE_PLANE = 2 };
+
+/* What each round record carries beyond (f, g, feasible). */
+enum tg_record_flags {
+    TG_REC_DIGEST = 1,   /* 64-bit digest of the target state (every round) */
+    TG_REC_STATE = 2,    /* target state, int8 in caller spin order          */
+    TG_REC_GRID = 4,     /* every slot's state (store_target_only = false)   */
+    TG_REC_COUNTERS = 8  /* cumulative per-pair accept counters              */
+};
+
+typedef struct {
+    int64_t total_sweeps;    /* RunConfig::total_sweeps   (engine.hpp:27) */
+    int64_t sweeps_per_swap; /* RunConfig::sweeps_per_swap (engine.hpp:28) */
+    uint64_t seed;           /* RunConfig::seed            (engine.hpp:29) */
+    int32_t rule;            /* tg_rule */
+    int32_t engine;          /* tg_engine */
+    int32_t record_flags;    /* tg_record_flags bitmask */
+    int32_t record_every;    /* deliver a record every k rounds (1 = every round, as the reference) */
+} tg_run_config;
+
+typedef struct {
+    int64_t round;        /* 1-based (TraceRecord::round) */
+    int64_t sweep_count;  /* round * sweeps_per_swap */
+    double f;             /* target replica cost energy */
+    double g;             /* target replica constraint value, reference units sum (s_a-s_b)^2 */
+    int32_t feasible;     /* g == 0 */
+    int32_t target_state; /* physical replica id currently at slot I*J-1 */
+    uint64_t digest;      /* sum over +1 spins of mix64(i+1) (caller order), if TG_REC_DIGEST */
+} tg_record;
+
+/* Record sink, called on the thread that called tg_run/tg_advance, in round
+ * order.  states: n_recs x n int8 (TG_REC_STATE) or n_recs x R x n (TG_REC_GRID),
+ * else NULL.  acc_p: n_recs x I*(J-1), acc_b: n_recs x (I-1)*J cumulative accept
+ * counts (TG_REC_COUNTERS), else NULL.  Return nonzero to stop (TG_ERR_SINK). */
+typedef int (*tg_sink_fn)(void* user, const tg_record* recs, int64_t n_recs,
+                          const int8_t* states, const int64_t* acc_p, const int64_t* acc_b);
+
+int tg_abi_version(void);
+
+/* Context on CUDA device `device` (single-GPU: rank 0 of 1). */
+int tg_create(int device, tg_ctx** out);
+/* Context for rank `rank` of `world_size`, one per GPU/process.  nccl_id is
+ * the 128-byte ncclUniqueId created by rank 0 and broadcast by the caller. */
+int tg_create_distributed(int device, int rank, int world_size, const void* nccl_id, tg_ctx** out);
+/* Create a fresh NCCL unique id (128 bytes) on rank 0. */
+int tg_nccl_unique_id(void* out128);
+void tg_destroy(tg_ctx* ctx);
+/* Last error message of ctx (or of the failed create when ctx == NULL). */
+size_t tg_last_error(const tg_ctx* ctx, char* buf, size_t len);
+
+/* ConstrainedProblem (constraints.hpp:44-48): n spins, cost couplings
+ * (ci[k], cj[k], w[k]) with any order and i != j, fields[n], and chain
+ * constraint pairs (pa[k], pb[k]).  Validated like IsingModel /
+ * ConstraintSet (ising.cpp:21-46, constraints.cpp:16-26). */
+int tg_set_problem(tg_ctx* ctx, int n, int n_couplings, const int32_t* ci, const int32_t* cj,
+                   const double* w, const double* fields, int n_pairs, const int32_t* pa,
+                   const int32_t* pb);
+/* Schedule (schedule.hpp:35-42): strictly increasing finite betas[I] and
+ * penalties[J] >= 0 (engine.cpp:41-52, constraints.cpp:123-124). */
+int tg_set_schedule(tg_ctx* ctx, int n_betas, const double* betas, int n_penalties,
+                    const double* penalties);
+
+/* run_2dpt: tg_init + tg_advance(total_sweeps / sweeps_per_swap rounds). */
+int tg_run(tg_ctx* ctx, const tg_run_config* cfg, tg_sink_fn sink, void* user);
+/* Initialise replicas (engine.cpp:98-107) and the round counter. */
+int tg_init(tg_ctx* ctx, const tg_run_config* cfg);
+/* Continue for n_rounds rounds from the current state (resume-capable). */
+int tg_advance(tg_ctx* ctx, int64_t n_rounds, tg_sink_fn sink, void* user);
+
+/* Current configuration at grid slot `slot` (row-major i*J+j), caller order. */
+int tg_get_state(tg_ctx* ctx, int slot, int8_t* out);
+/* Cumulative attempt/accept counters (engine.cpp:109-112 layouts). */
+int tg_get_counters(tg_ctx* ctx, int64_t* attempts_p, int64_t* accepts_p, int64_t* attempts_b,
+                    int64_t* accepts_b);
+/* Per-slot f and g after the last completed round. */
+int tg_get_energies(tg_ctx* ctx, double* f, double* g);
+
+typedef struct {
+    int32_t engine;        /* engine actually selected */
+    int32_t n_colors;      /* colour classes of the canonical order */
+    int32_t n_replicas;    /* I*J (whole grid) */
+    int32_t local_replicas;/* replicas swept by this rank */
+    int32_t words;         /* plane engine: 32-replica words per site on this rank */
+    int32_t device_sms;
+    int64_t rounds_done;
+    double last_sweep_ms;  /* device time of the sweep kernels of the last tg_advance */
+    double last_swap_ms;   /* device time of the swap/record kernels of the last tg_advance */
+    int64_t sweep_launches;
+    int64_t other_launches;
+} tg_info;
+int tg_get_info(tg_ctx* ctx, tg_info* info);
+/* cudaStream_t the context launches on (for external CUDA-event timing). */
+void* tg_stream(tg_ctx* ctx);
+/* Enable per-kernel CUDA-event timing inside tg_advance (default off). */
+int tg_set_profiling(tg_ctx* ctx, int on);
+
+/* Host-only helper (no device needed): greedy colouring of cost+chain edges
+ * and the canonical sweep order (stable sort by colour, chain degree, cost
+ * degree); order[k] = caller spin at internal position k. */
+int tg_canonical_order(int n, int n_couplings, const int32_t* ci, const int32_t* cj, int n_pairs,
+                       const int32_t* pa, const int32_t* pb, int32_t* order, int32_t* color,
+                       int32_t* n_colors);
+
+/* Swap-probability helpers of the reference (engine.hpp:15-24). */
+double tg_p_swap_probability(double beta, double d_penalty, double dg);
+double tg_beta_swap_probability(double d_beta, double d_energy);
+double tg_general_swap_probability(double beta_a, double beta_b, double de_a, double de_b);
+
+/* Host replay of one swap phase over gathered per-replica (f, g) -- the
+ * exact routine the device swap kernel runs, exported so the multi-rank
+ * exchange logic can be tested without a GPU.  slot_state[R] (state id at
+ * each slot) and the counters are updated in place. */
+int tg_swap_phase_host(int n_betas, const double* betas, int n_penalties, const double* penalties,
+                       int64_t round, int direction, uint64_t seed, uint64_t swap_base,
+                       const double* f_state, const double* g_state, int32_t* slot_state,
+                       int64_t* accepts_p, int64_t* accepts_b);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TEMPERGRID_B200_H */

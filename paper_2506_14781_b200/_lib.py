@@ -1,0 +1,95 @@
+"""ctypes binding of the C ABI (include/tempergrid_b200.h).
+
+The engine library must be built in-tree (``python -m paper_2506_14781_b200.build``);
+importing this module without it raises immediately -- there is no CPU
+fallback for the hot path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libtempergrid_b200.so")
+
+TG_OK, TG_ERR_INTERNAL, TG_ERR_CONFIG, TG_ERR_RESOURCE, TG_ERR_CUDA, TG_ERR_SINK = range(6)
+RULES = {"metropolis": 0, "heat_bath": 1}
+ENGINES = {"auto": 0, "slot": 1, "plane": 2}
+REC_DIGEST, REC_STATE, REC_GRID, REC_COUNTERS = 1, 2, 4, 8
+
+
+class RunConfigC(C.Structure):
+    _fields_ = [("total_sweeps", C.c_int64), ("sweeps_per_swap", C.c_int64), ("seed", C.c_uint64),
+                ("rule", C.c_int32), ("engine", C.c_int32), ("record_flags", C.c_int32),
+                ("record_every", C.c_int32)]
+
+
+class RecordC(C.Structure):
+    _fields_ = [("round", C.c_int64), ("sweep_count", C.c_int64), ("f", C.c_double),
+                ("g", C.c_double), ("feasible", C.c_int32), ("target_state", C.c_int32),
+                ("digest", C.c_uint64)]
+
+
+class InfoC(C.Structure):
+    _fields_ = [("engine", C.c_int32), ("n_colors", C.c_int32), ("n_replicas", C.c_int32),
+                ("local_replicas", C.c_int32), ("words", C.c_int32), ("device_sms", C.c_int32),
+                ("rounds_done", C.c_int64), ("last_sweep_ms", C.c_double),
+                ("last_swap_ms", C.c_double), ("sweep_launches", C.c_int64),
+                ("other_launches", C.c_int64)]
+
+
+SINK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(RecordC), C.c_int64, C.POINTER(C.c_int8),
+                   C.POINTER(C.c_int64), C.POINTER(C.c_int64))
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load the engine library; raises if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"tempergrid B200 engine not built ({LIB_PATH} missing); run "
+            "`python -m paper_2506_14781_b200.build` -- there is no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    vp, i32p, f64p = C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_double)
+    L.tg_abi_version.restype = C.c_int
+    L.tg_create.argtypes = [C.c_int, C.POINTER(vp)]
+    L.tg_create_distributed.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(vp)]
+    L.tg_nccl_unique_id.argtypes = [C.c_void_p]
+    L.tg_destroy.argtypes = [vp]
+    L.tg_destroy.restype = None
+    L.tg_last_error.argtypes = [vp, C.c_char_p, C.c_size_t]
+    L.tg_last_error.restype = C.c_size_t
+    L.tg_set_problem.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int, vp, vp]
+    L.tg_set_schedule.argtypes = [vp, C.c_int, vp, C.c_int, vp]
+    L.tg_run.argtypes = [vp, C.POINTER(RunConfigC), SINK, C.c_void_p]
+    L.tg_init.argtypes = [vp, C.POINTER(RunConfigC)]
+    L.tg_advance.argtypes = [vp, C.c_int64, SINK, C.c_void_p]
+    L.tg_get_state.argtypes = [vp, C.c_int, vp]
+    L.tg_get_counters.argtypes = [vp, vp, vp, vp, vp]
+    L.tg_get_energies.argtypes = [vp, vp, vp]
+    L.tg_get_info.argtypes = [vp, C.POINTER(InfoC)]
+    L.tg_stream.argtypes = [vp]
+    L.tg_stream.restype = C.c_void_p
+    L.tg_set_profiling.argtypes = [vp, C.c_int]
+    L.tg_canonical_order.argtypes = [C.c_int, C.c_int, vp, vp, C.c_int, vp, vp, vp, vp, vp]
+    for fn, n in (("tg_p_swap_probability", 3), ("tg_beta_swap_probability", 2),
+                  ("tg_general_swap_probability", 4)):
+        getattr(L, fn).restype = C.c_double
+        getattr(L, fn).argtypes = [C.c_double] * n
+    L.tg_swap_phase_host.argtypes = [C.c_int, vp, C.c_int, vp, C.c_int64, C.c_int, C.c_uint64,
+                                     C.c_uint64, vp, vp, vp, vp, vp]
+    _lib = L
+    return L
+
+
+EXPORTED = [
+    "tg_abi_version", "tg_create", "tg_create_distributed", "tg_nccl_unique_id", "tg_destroy",
+    "tg_last_error", "tg_set_problem", "tg_set_schedule", "tg_run", "tg_init", "tg_advance",
+    "tg_get_state", "tg_get_counters", "tg_get_energies", "tg_get_info", "tg_stream",
+    "tg_set_profiling", "tg_canonical_order", "tg_p_swap_probability", "tg_beta_swap_probability",
+    "tg_general_swap_probability", "tg_swap_phase_host",
+]

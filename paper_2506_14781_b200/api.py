@@ -1,0 +1,324 @@
+"""Python mirror of the reference's run_2dpt API over the C ABI.
+
+Same names, argument meaning and error behaviour as
+``tempergrid::run_2dpt`` (/root/reference/proj/include/tempergrid/engine.hpp:26-63)
+-- ``RunConfig``, ``Schedule``, ``TraceRecord``, ``Trace`` -- with the
+reference's exceptions mapped from the C status codes (config_error -> 2,
+resource_error -> 3).  Extra ``RunConfig`` fields select the update rule and
+the engine; their defaults keep the reference's Metropolis rule.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .instances import ConfigError, Problem, ResourceError
+
+
+class EngineError(RuntimeError):
+    pass
+
+
+def _raise(code: int, msg: str):
+    if code == _lib.TG_ERR_CONFIG:
+        raise ConfigError(msg)
+    if code == _lib.TG_ERR_RESOURCE:
+        raise ResourceError(msg)
+    raise EngineError(f"[{code}] {msg}")
+
+
+@dataclass
+class Schedule:
+    """schedule.hpp:35-42 (betas per row, penalties per column)."""
+    betas: Sequence[float]
+    penalties: Sequence[float]
+
+
+@dataclass
+class RunConfig:
+    """engine.hpp:26-32 plus engine options."""
+    total_sweeps: int = 0
+    sweeps_per_swap: int = 1
+    seed: int = 1
+    store_target_only: bool = True
+    threads: int = 1                 # accepted for API parity; results never depend on it
+    rule: str = "metropolis"         # or "heat_bath"
+    engine: str = "auto"             # "slot" | "plane" | "auto"
+    record_every: int = 1
+    store_states: bool = True        # TraceRecord.state for every record
+    digest: bool = True
+
+
+@dataclass
+class TraceRecord:
+    """engine.hpp:39-50"""
+    round: int
+    sweep_count: int
+    f: float
+    g: float
+    feasible: bool
+    state: Optional[np.ndarray]
+    acceptance_rates_p: List[float]
+    acceptance_rates_beta: List[float]
+    grid: Optional[np.ndarray] = None
+    digest: int = 0
+    target_state: int = -1
+
+
+@dataclass
+class Trace:
+    """engine.hpp:52-56"""
+    betas: List[float]
+    penalties: List[float]
+    sweeps_per_swap: int
+    records: List[TraceRecord] = field(default_factory=list)
+
+
+def p_swap_probability(beta: float, d_penalty: float, dg: float) -> float:
+    return _lib.lib().tg_p_swap_probability(beta, d_penalty, dg)
+
+
+def beta_swap_probability(d_beta: float, d_energy: float) -> float:
+    return _lib.lib().tg_beta_swap_probability(d_beta, d_energy)
+
+
+def general_swap_probability(beta_a: float, beta_b: float, de_a: float, de_b: float) -> float:
+    return _lib.lib().tg_general_swap_probability(beta_a, beta_b, de_a, de_b)
+
+
+def _arr(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def attempts_per_round(I: int, J: int, rnd: int):
+    """Deterministic attempt counts of round `rnd` (engine.cpp:121-187)."""
+    even = 1 if rnd % 2 == 0 else 0
+    direction = 1 if ((rnd - 1) // 2) % 2 == 0 else -1
+    if I == 1 and J == 1:
+        dp = db = False
+    elif I == 1:
+        dp, db = True, False
+    elif J == 1:
+        dp, db = False, True
+    else:
+        dp, db = direction == 1, direction != 1
+    ap = np.zeros(I * max(J - 1, 0), np.int64)
+    ab = np.zeros(max(I - 1, 0) * J, np.int64)
+    if dp:
+        for i in range(I):
+            for p in range(even, J - 1, 2):
+                ap[i * (J - 1) + p] += 1
+    if db:
+        for j in range(J):
+            for b in range(even, I - 1, 2):
+                ab[b * J + j] += 1
+    return ap, ab
+
+
+class Engine:
+    """One engine context (one GPU).  Thin owner of a ``tg_ctx``."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world_size: int = 1,
+                 nccl_id: Optional[bytes] = None):
+        self._L = _lib.lib()
+        h = C.c_void_p()
+        if world_size == 1:
+            rc = self._L.tg_create(device, C.byref(h))
+        else:
+            buf = C.create_string_buffer(bytes(nccl_id), 128)
+            rc = self._L.tg_create_distributed(device, rank, world_size, buf, C.byref(h))
+        if rc != 0:
+            _raise(rc, self._err(None))
+        self._h = h
+        self.problem: Optional[Problem] = None
+        self.schedule: Optional[Schedule] = None
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        rc = _lib.lib().tg_nccl_unique_id(buf)
+        if rc != 0:
+            raise EngineError("ncclGetUniqueId failed")
+        return buf.raw
+
+    def _err(self, h) -> str:
+        buf = C.create_string_buffer(1024)
+        self._L.tg_last_error(h, buf, 1024)
+        return buf.value.decode()
+
+    def _check(self, rc: int):
+        if rc != 0:
+            _raise(rc, self._err(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.tg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ------------------------------------------------------------ setup
+    def set_problem(self, pr: Problem):
+        self._keep_p = [_arr(pr.ci, np.int32), _arr(pr.cj, np.int32), _arr(pr.cw, np.float64),
+                        _arr(pr.fields, np.float64), _arr(pr.pa, np.int32), _arr(pr.pb, np.int32)]
+        ci, cj, cw, h, pa, pb = self._keep_p
+        self._check(self._L.tg_set_problem(self._h, pr.n, len(ci), _p(ci), _p(cj), _p(cw), _p(h),
+                                           len(pa), _p(pa), _p(pb)))
+        self.problem = pr
+
+    def set_schedule(self, betas, penalties):
+        b, p = _arr(betas, np.float64), _arr(penalties, np.float64)
+        self._check(self._L.tg_set_schedule(self._h, len(b), _p(b), len(p), _p(p)))
+        self.schedule = Schedule(list(b), list(p))
+
+    def _cfg(self, cfg: RunConfig) -> _lib.RunConfigC:
+        flags = 0
+        if cfg.digest:
+            flags |= _lib.REC_DIGEST
+        if cfg.store_states:
+            flags |= _lib.REC_STATE
+        if not cfg.store_target_only:
+            flags |= _lib.REC_GRID
+        flags |= _lib.REC_COUNTERS
+        if cfg.rule not in _lib.RULES:
+            raise ConfigError(f"run: unknown rule {cfg.rule}")
+        if cfg.engine not in _lib.ENGINES:
+            raise ConfigError(f"run: unknown engine {cfg.engine}")
+        return _lib.RunConfigC(int(cfg.total_sweeps), int(cfg.sweeps_per_swap),
+                               int(cfg.seed) & 0xFFFFFFFFFFFFFFFF, _lib.RULES[cfg.rule],
+                               _lib.ENGINES[cfg.engine], flags, max(int(cfg.record_every), 1))
+
+    def init(self, cfg: RunConfig, flags: Optional[int] = None):
+        c = self._cfg(cfg)
+        if flags is not None:
+            c.record_flags = flags
+        self._check(self._L.tg_init(self._h, C.byref(c)))
+        self._cfg_py = cfg
+
+    def advance(self, n_rounds: int, sink: Optional[Callable] = None):
+        cb = _make_sink(sink) if sink else C.cast(None, _lib.SINK)
+        self._check(self._L.tg_advance(self._h, int(n_rounds), cb, None))
+
+    def run(self, cfg: RunConfig, sink: Optional[Callable] = None, flags: Optional[int] = None):
+        c = self._cfg(cfg)
+        if flags is not None:
+            c.record_flags = flags
+        cb = _make_sink(sink) if sink else C.cast(None, _lib.SINK)
+        self._check(self._L.tg_run(self._h, C.byref(c), cb, None))
+
+    # ------------------------------------------------------------ queries
+    def state(self, slot: int) -> np.ndarray:
+        out = np.zeros(self.problem.n, np.int8)
+        self._check(self._L.tg_get_state(self._h, int(slot), _p(out)))
+        return out
+
+    def grid(self) -> np.ndarray:
+        R = len(self.schedule.betas) * len(self.schedule.penalties)
+        return np.stack([self.state(r) for r in range(R)])
+
+    def counters(self):
+        I, J = len(self.schedule.betas), len(self.schedule.penalties)
+        ap, cp = np.zeros(I * max(J - 1, 0), np.int64), np.zeros(I * max(J - 1, 0), np.int64)
+        ab, cb = np.zeros(max(I - 1, 0) * J, np.int64), np.zeros(max(I - 1, 0) * J, np.int64)
+        self._check(self._L.tg_get_counters(self._h, _p(ap), _p(cp), _p(ab), _p(cb)))
+        return ap, cp, ab, cb
+
+    def energies(self):
+        R = len(self.schedule.betas) * len(self.schedule.penalties)
+        f, g = np.zeros(R), np.zeros(R)
+        self._check(self._L.tg_get_energies(self._h, _p(f), _p(g)))
+        return f, g
+
+    def info(self) -> dict:
+        i = _lib.InfoC()
+        self._check(self._L.tg_get_info(self._h, C.byref(i)))
+        return {k: getattr(i, k) for k, _ in _lib.InfoC._fields_}
+
+    def stream_ptr(self) -> int:
+        return int(self._L.tg_stream(self._h) or 0)
+
+    def set_profiling(self, on: bool):
+        self._check(self._L.tg_set_profiling(self._h, 1 if on else 0))
+
+
+def _make_sink(fn: Callable):
+    def _cb(user, recs, n, states, acc_p, acc_b):
+        try:
+            return int(fn(recs, int(n), states, acc_p, acc_b) or 0)
+        except Exception:  # noqa: BLE001 - report through the C status
+            import traceback
+            traceback.print_exc()
+            return 1
+    return _lib.SINK(_cb)
+
+
+def run_2dpt(problem: Problem, schedule: Schedule, cfg: RunConfig, device: int = 0,
+             engine: Optional[Engine] = None) -> Trace:
+    """Drop-in for ``tempergrid::run_2dpt`` (engine.cpp:83-219) on a B200."""
+    I, J = len(schedule.betas), len(schedule.penalties)
+    R, n = I * J, problem.n
+    trace = Trace(list(map(float, schedule.betas)), list(map(float, schedule.penalties)),
+                  int(cfg.sweeps_per_swap))
+    eng = engine or Engine(device)
+    try:
+        eng.set_problem(problem)
+        eng.set_schedule(schedule.betas, schedule.penalties)
+        np_, nb_ = I * max(J - 1, 0), max(I - 1, 0) * J
+        att_p = np.zeros(np_, np.int64)
+        att_b = np.zeros(nb_, np.int64)
+        last_round = [0]
+
+        def sink(recs, cnt, states, acc_p, acc_b):
+            per = (R * n) if not cfg.store_target_only else (n if cfg.store_states else 0)
+            st = (np.ctypeslib.as_array(states, shape=(cnt * per,)).copy() if per and states
+                  else None)
+            ap = np.ctypeslib.as_array(acc_p, shape=(cnt * np_,)).copy() if np_ else np.zeros(0, np.int64)
+            ab = np.ctypeslib.as_array(acc_b, shape=(cnt * nb_,)).copy() if nb_ else np.zeros(0, np.int64)
+            for k in range(cnt):
+                r = recs[k]
+                # cumulative attempts up to this round (deterministic)
+                while last_round[0] < r.round:
+                    last_round[0] += 1
+                    a1, a2 = attempts_per_round(I, J, last_round[0])
+                    att_p[:] += a1
+                    att_b[:] += a2
+                cp = ap[k * np_:(k + 1) * np_]
+                cb = ab[k * nb_:(k + 1) * nb_]
+                rp = [float(c) / a if a else 0.0 for c, a in zip(cp, att_p)]
+                rb = [float(c) / a if a else 0.0 for c, a in zip(cb, att_b)]
+                state = grid = None
+                if st is not None:
+                    chunk = st[k * per:(k + 1) * per]
+                    if cfg.store_target_only:
+                        state = chunk.copy()
+                    else:
+                        grid = chunk.reshape(R, n).copy()
+                        state = grid[R - 1].copy()
+                trace.records.append(TraceRecord(int(r.round), int(r.sweep_count), float(r.f),
+                                                 float(r.g), bool(r.feasible), state, rp, rb, grid,
+                                                 int(r.digest), int(r.target_state)))
+            return 0
+
+        eng.run(cfg, sink)
+    finally:
+        if engine is None:
+            eng.close()
+    return trace

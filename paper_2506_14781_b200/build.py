@@ -1,0 +1,93 @@
+"""Build the sm_100a engine library in-tree (paper_2506_14781_b200/libtempergrid_b200.so).
+
+    python -m paper_2506_14781_b200.build          # engine only
+    python -m paper_2506_14781_b200.build --all    # engine + oracle checkers
+
+nvcc cross-compiles for sm_100a without a GPU.  The .so is git-ignored but
+travels to the GPU box with the repo snapshot.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "libtempergrid_b200.so")
+CPPLIB = os.path.join(PKG, "libtempergrid_cpp.so")
+SOURCES = ["kernels.cu", "capi.cu"]
+HEADERS = ["engine.cuh", "kernels.cuh", "philox.cuh"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_engine(force: bool = False, verbose: bool = False) -> str:
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps.append(os.path.join(ROOT, "include", "tempergrid_b200.h"))
+    if not force and not _stale(LIB, deps):
+        return LIB
+    cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v",
+           "-Xcompiler", "-fPIC", "-shared", "-o", LIB,
+           *[os.path.join(CSRC, f) for f in SOURCES], "-lnccl"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    log = os.path.join(PKG, "build_ptxas.log")
+    with open(log, "w") as fh:
+        fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building %s" % LIB)
+    if verbose:
+        sys.stdout.write(res.stderr)
+    return LIB
+
+
+def build_cpp(force: bool = False) -> str:
+    """C++ mirror of the reference API (tempergrid::run_2dpt over the C ABI)."""
+    src = os.path.join(CSRC, "tempergrid_api.cpp")
+    hdr = os.path.join(CSRC, "tempergrid", "tempergrid.hpp")
+    if not os.path.exists(src):
+        return ""
+    if not force and not _stale(CPPLIB, [src, hdr, LIB]):
+        return CPPLIB
+    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", CSRC, "-I", os.path.join(ROOT, "include"),
+           "-o", CPPLIB, src, "-L", PKG, "-ltempergrid_b200", "-Wl,-rpath,$ORIGIN"]
+    subprocess.run(cmd, check=True)
+    return CPPLIB
+
+
+def build_oracle() -> None:
+    targets = ["port"]
+    if os.path.isdir("/root/reference/proj"):
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), *targets], check=True)
+
+
+def main(argv=None) -> int:
+    argv = sys.argv[1:] if argv is None else argv
+    force = "--force" in argv
+    build_engine(force=force, verbose="-v" in argv)
+    build_cpp(force=force)
+    if "--all" in argv:
+        build_oracle()
+    print(LIB)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

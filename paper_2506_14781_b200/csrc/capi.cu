@@ -1,0 +1,1042 @@
+// capi.cu -- host driver behind the C ABI (include/tempergrid_b200.h).
+//
+// Owns the device copy of one ConstrainedProblem in canonical colour order,
+// the replica grid labels, and the round loop of run_2dpt
+// (/root/reference/proj/src/engine.cpp:83-219): per round one sweep launch
+// (all sweeps_per_swap sweeps, every colour phase), the (f, g) exchange
+// (NCCL all-gather when the grid is split over GPUs), one swap/record launch,
+// and an optional target-state extract; records drain to the caller's sink
+// in round order.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/tempergrid_b200.h"
+#include "engine.cuh"
+#include "kernels.cuh"
+
+using namespace tg;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct TgFail {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    throw TgFail{code, buf};
+}
+
+#define CK(x)                                                                                  \
+    do {                                                                                       \
+        cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess) fail(TG_ERR_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                                    __FILE__, __LINE__);                                       \
+    } while (0)
+#define NK(x)                                                                                  \
+    do {                                                                                       \
+        ncclResult_t r_ = (x);                                                                 \
+        if (r_ != ncclSuccess) fail(TG_ERR_CUDA, "%s: %s", #x, ncclGetErrorString(r_));        \
+    } while (0)
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) CK(cudaMalloc(&p, sizeof(T) * count));
+    }
+    void upload(const std::vector<T>& v, cudaStream_t s) {
+        alloc(v.size());
+        if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, s));
+    }
+    void zero(cudaStream_t s) {
+        if (n) CK(cudaMemsetAsync(p, 0, sizeof(T) * n, s));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DBuf() { release(); }
+};
+
+int nbits(int d) {
+    int b = 0;
+    while ((1 << b) <= d) ++b;
+    return d == 0 ? 0 : b;
+}
+
+}  // namespace
+
+struct tg_ctx {
+    std::string err;
+    int device = 0, rank = 0, world = 1;
+    int sms = 0;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    bool profiling = false;
+
+    // problem (caller order) + canonical relabel
+    bool have_problem = false;
+    int n = 0;
+    std::vector<int> ci, cj, pa, pb;
+    std::vector<double> cw, h;
+    std::vector<int> order, inv, color;  // order[k] = caller index at internal k
+    int n_colors = 0;
+    std::vector<int> color_start;
+
+    bool have_schedule = false;
+    std::vector<double> betas, pens;
+
+    // run state
+    bool initialised = false;
+    tg_run_config cfg{};
+    int engine = 0;
+    int I = 0, J = 0, R = 0, R_local = 0, state0 = 0, W = 0;
+    int64_t rounds_done = 0;
+    uint64_t swap_base = 0;
+    int kpw = 0, ktab_row = 0, n_types = 0, m_cost = 0;
+    int plane_grid = 0, plane_block = kPlaneThreads;
+    size_t slot_smem = 0;
+
+    DBuf<double> d_betas, d_pens, d_f, d_g;
+    DBuf<int32_t> d_slot_state, d_state_slot, d_perm;
+    DBuf<int64_t> d_acc_p, d_acc_b, d_rec_acc;
+    DBuf<TgRecordDev> d_rec;
+    DBuf<int8_t> d_rec_states;
+    // plane
+    DBuf<uint32_t> d_spins32, d_kp, d_active;
+    DBuf<int32_t> d_nbr, d_cnt_c, d_cnt_q;
+    DBuf<Chunk> d_chunks;
+    DBuf<int> d_chunk_off, d_color_start;
+    DBuf<PlaneType> d_types;
+    DBuf<uint2> d_wkey;
+    DBuf<uint64_t> d_ktab;
+    // slot
+    DBuf<int8_t> d_spins8, d_cm;
+    DBuf<int> d_off;
+    DBuf<int32_t> d_snbr;
+    DBuf<double> d_sw, d_h;
+    DBuf<uint64_t> d_slot_key;
+
+    int rec_cap = 0;
+    std::vector<TgRecordDev> h_rec;
+    std::vector<int8_t> h_states;
+    std::vector<int64_t> h_acc;
+    std::vector<cudaEvent_t> ev;
+    double last_sweep_ms = 0, last_swap_ms = 0;
+    int64_t sweep_launches = 0, other_launches = 0;
+
+    ~tg_ctx() {
+        for (auto e : ev) cudaEventDestroy(e);
+        if (comm) ncclCommDestroy(comm);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+template <class F>
+int guard(tg_ctx* ctx, F&& f) {
+    try {
+        f();
+        if (ctx) ctx->err.clear();
+        return TG_OK;
+    } catch (const TgFail& e) {
+        if (ctx) ctx->err = e.msg; else g_create_error = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what(); else g_create_error = e.what();
+        return TG_ERR_INTERNAL;
+    }
+}
+
+// Greedy colouring in index order and canonical order (see tg_canonical_order).
+void canonical(int n, const std::vector<int>& ci, const std::vector<int>& cj,
+               const std::vector<int>& pa, const std::vector<int>& pb, std::vector<int>& order,
+               std::vector<int>& color, int& n_colors) {
+    std::vector<int> dc(n, 0), dq(n, 0), off(n + 1, 0);
+    for (size_t k = 0; k < ci.size(); ++k) { dc[ci[k]]++; dc[cj[k]]++; }
+    for (size_t k = 0; k < pa.size(); ++k) { dq[pa[k]]++; dq[pb[k]]++; }
+    for (int i = 0; i < n; ++i) off[i + 1] = off[i] + dc[i] + dq[i];
+    std::vector<int> adj(off[n]), cur(off.begin(), off.end() - 1);
+    for (size_t k = 0; k < ci.size(); ++k) { adj[cur[ci[k]]++] = cj[k]; adj[cur[cj[k]]++] = ci[k]; }
+    for (size_t k = 0; k < pa.size(); ++k) { adj[cur[pa[k]]++] = pb[k]; adj[cur[pb[k]]++] = pa[k]; }
+    color.assign(n, 0);
+    std::vector<char> used(n + 2, 0);
+    n_colors = 0;
+    for (int i = 0; i < n; ++i) {
+        for (int k = off[i]; k < off[i + 1]; ++k) if (adj[k] < i) used[color[adj[k]]] = 1;
+        int c = 0;
+        while (used[c]) ++c;
+        color[i] = c;
+        n_colors = std::max(n_colors, c + 1);
+        for (int k = off[i]; k < off[i + 1]; ++k) if (adj[k] < i) used[color[adj[k]]] = 0;
+    }
+    order.resize(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        if (color[a] != color[b]) return color[a] < color[b];
+        if (dq[a] != dq[b]) return dq[a] < dq[b];
+        return dc[a] < dc[b];
+    });
+}
+
+void check_vec(const std::vector<double>& v, const char* what) {  // engine.cpp:41-52
+    if (v.empty()) fail(TG_ERR_CONFIG, "%s vector must be non-empty", what);
+    for (double x : v) if (!std::isfinite(x)) fail(TG_ERR_CONFIG, "%s entries must be finite", what);
+    for (size_t k = 1; k < v.size(); ++k)
+        if (v[k] <= v[k - 1]) fail(TG_ERR_CONFIG, "%s vector must be strictly increasing", what);
+}
+
+bool plane_eligible(const tg_ctx& c, std::string* why) {
+    for (double w : c.cw) if (!(w == 1.0 || w == -1.0)) { if (why) *why = "couplings must be +-1"; return false; }
+    for (double x : c.h) if (x != 0.0) { if (why) *why = "fields must be 0"; return false; }
+    std::vector<int> dc(c.n, 0), dq(c.n, 0);
+    for (size_t k = 0; k < c.ci.size(); ++k) { dc[c.ci[k]]++; dc[c.cj[k]]++; }
+    for (size_t k = 0; k < c.pa.size(); ++k) { dq[c.pa[k]]++; dq[c.pb[k]]++; }
+    for (int i = 0; i < c.n; ++i)
+        if (dc[i] > kMaxDC || dq[i] > kMaxDQ) { if (why) *why = "degree bound exceeded"; return false; }
+    return true;
+}
+
+// 53-bit acceptance threshold: the draw u = U53 * 2^-53 accepts iff U53 < K;
+// K >= 2^53 encodes "always" (u < 1).  Reference expressions of mc.cpp:27-28
+// (Metropolis) and of the heat-bath rule, evaluated with the host libm.
+uint64_t threshold_metropolis(double beta, double de) {
+    if (de <= 0.0) return 1ull << 53;
+    const double T = std::exp(-beta * de);
+    return (uint64_t)std::ceil(T * 0x1.0p53);
+}
+uint64_t threshold_heat_bath(double beta, double local) {
+    const double p = 1.0 / (1.0 + std::exp(-2.0 * beta * local));
+    return (uint64_t)std::ceil(p * 0x1.0p53);
+}
+
+void build_plane(tg_ctx& c) {
+    cudaStream_t st = c.stream;
+    const int n = c.n;
+    // internal adjacency
+    std::vector<std::vector<int32_t>> cost(n), chain(n);
+    for (size_t k = 0; k < c.ci.size(); ++k) {
+        const int a = c.inv[c.ci[k]], b = c.inv[c.cj[k]];
+        const int32_t sgn = c.cw[k] < 0 ? (int32_t)0x80000000u : 0;
+        cost[a].push_back(b | sgn);
+        cost[b].push_back(a | sgn);
+    }
+    for (size_t k = 0; k < c.pa.size(); ++k) {
+        const int a = c.inv[c.pa[k]], b = c.inv[c.pb[k]];
+        chain[a].push_back(b);
+        chain[b].push_back(a);
+    }
+    // types
+    std::map<std::pair<int, int>, int> type_of;
+    std::vector<PlaneType> types;
+    for (int i = 0; i < n; ++i) {
+        auto key = std::make_pair((int)cost[i].size(), (int)chain[i].size());
+        if (!type_of.count(key)) {
+            PlaneType t{};
+            t.dc = key.first;
+            t.dq = key.second;
+            t.ncb = nbits(t.dc);
+            t.nqb = nbits(t.dq);
+            t.ncl = std::max(4, 1 << (t.ncb + t.nqb));
+            type_of[key] = (int)types.size();
+            types.push_back(t);
+        }
+    }
+    if ((int)types.size() > kMaxTypes) fail(TG_ERR_RESOURCE, "plane engine: too many site types");
+    int kpw = 0, krow = 0;
+    for (auto& t : types) {
+        t.kp_off = kpw;
+        t.ktab_off = krow;
+        kpw += kKWords * t.ncl;
+        krow += t.ncl;
+    }
+    c.kpw = kpw;
+    c.ktab_row = krow;
+    c.n_types = (int)types.size();
+    // nbr array + chunks (colour-major; canonical order keeps types contiguous)
+    std::vector<int32_t> nbr;
+    std::vector<Chunk> chunks;
+    std::vector<int> chunk_off(c.n_colors + 1, 0);
+    std::vector<int> base(n + 1, 0);
+    for (int i = 0; i < n; ++i) {
+        base[i] = (int)nbr.size();
+        for (int32_t e : cost[i]) nbr.push_back(e);
+        for (int32_t e : chain[i]) nbr.push_back(e);
+    }
+    for (int col = 0; col < c.n_colors; ++col) {
+        chunk_off[col] = (int)chunks.size();
+        int i = c.color_start[col];
+        const int end = c.color_start[col + 1];
+        while (i < end) {
+            const int ty = type_of[{(int)cost[i].size(), (int)chain[i].size()}];
+            int j = i;
+            while (j < end && j - i < 32 &&
+                   type_of[{(int)cost[j].size(), (int)chain[j].size()}] == ty)
+                ++j;
+            chunks.push_back(Chunk{i, j - i, ty, base[i]});
+            i = j;
+        }
+    }
+    chunk_off[c.n_colors] = (int)chunks.size();
+    // words, keys, masks
+    c.W = (c.R_local + 31) / 32;
+    std::vector<uint32_t> active(c.W, 0u);
+    std::vector<uint2> wkey(c.W);
+    for (int w = 0; w < c.W; ++w) {
+        for (int l = 0; l < 32; ++l) if (w * 32 + l < c.R_local) active[w] |= 1u << l;
+        const uint64_t k = derive_seed(c.cfg.seed, kPurposePlane, (uint64_t)(c.state0 / 32 + w));
+        wkey[w] = make_uint2((uint32_t)k, (uint32_t)(k >> 32));
+    }
+    // thresholds per (slot, type, class)
+    std::vector<uint64_t> ktab((size_t)c.R * krow, 0ull);
+    for (int slot = 0; slot < c.R; ++slot) {
+        const double beta = c.betas[slot / c.J], P = c.pens[slot % c.J];
+        for (const auto& t : types) {
+            for (int cl = 0; cl < t.ncl; ++cl) {
+                const int ncnt = cl & ((1 << t.ncb) - 1);
+                const int qcnt = cl >> t.ncb;
+                uint64_t K = 0;
+                if (ncnt <= t.dc && qcnt <= t.dq) {
+                    // s_i * local_i (Metropolis, counts of satisfied bonds) or
+                    // local_i (heat bath, counts of +1 contributions)
+                    const double v = (double)(2 * ncnt - t.dc) + 2.0 * P * (double)(2 * qcnt - t.dq);
+                    K = c.cfg.rule == TG_RULE_METROPOLIS ? threshold_metropolis(beta, 2.0 * v)
+                                                         : threshold_heat_bath(beta, v);
+                }
+                ktab[(size_t)slot * krow + t.ktab_off + cl] = K;
+            }
+        }
+    }
+    c.m_cost = (int)c.ci.size();
+    c.d_nbr.upload(nbr, st);
+    c.d_chunks.upload(chunks, st);
+    c.d_chunk_off.upload(chunk_off, st);
+    c.d_color_start.upload(c.color_start, st);
+    c.d_types.upload(types, st);
+    c.d_active.upload(active, st);
+    c.d_wkey.upload(wkey, st);
+    c.d_ktab.upload(ktab, st);
+    c.d_kp.alloc((size_t)c.W * kpw);
+    c.d_kp.zero(st);
+    c.d_spins32.alloc((size_t)n * c.W);
+    c.d_cnt_c.alloc((size_t)c.W * 32);
+    c.d_cnt_q.alloc((size_t)c.W * 32);
+    c.d_cnt_c.zero(st);
+    c.d_cnt_q.zero(st);
+    // cooperative grid: a multiple of W warps, all blocks co-resident
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)plane_sweep_fn(c.cfg.rule),
+                                                     kPlaneThreads, 0));
+    if (per_sm < 1) fail(TG_ERR_RESOURCE, "plane engine: kernel does not fit on an SM");
+    int blocks = per_sm * c.sms;
+    const int wpb = kPlaneThreads / 32;
+    while (blocks > 1 && ((blocks * wpb) % c.W) != 0) --blocks;
+    if ((blocks * wpb) % c.W != 0) fail(TG_ERR_RESOURCE, "plane engine: cannot tile %d words", c.W);
+    c.plane_grid = blocks;
+}
+
+void build_slot(tg_ctx& c) {
+    cudaStream_t st = c.stream;
+    const int n = c.n;
+    if (n > 200 * 1024) fail(TG_ERR_RESOURCE, "slot engine: %d spins exceed shared memory", n);
+    std::vector<std::map<int, std::pair<double, int>>> adj(n);
+    for (size_t k = 0; k < c.ci.size(); ++k) {
+        const int a = c.inv[c.ci[k]], b = c.inv[c.cj[k]];
+        adj[a][b].first += c.cw[k];
+        adj[b][a].first += c.cw[k];
+    }
+    for (size_t k = 0; k < c.pa.size(); ++k) {
+        const int a = c.inv[c.pa[k]], b = c.inv[c.pb[k]];
+        adj[a][b].second += 1;
+        adj[b][a].second += 1;
+    }
+    std::vector<int> off(n + 1, 0);
+    std::vector<int32_t> nbr;
+    std::vector<double> w;
+    std::vector<int8_t> cm;
+    for (int i = 0; i < n; ++i) {
+        for (auto& kv : adj[i]) {
+            nbr.push_back(kv.first);
+            w.push_back(kv.second.first);
+            cm.push_back((int8_t)kv.second.second);
+        }
+        off[i + 1] = (int)nbr.size();
+    }
+    std::vector<double> hi(n);
+    for (int i = 0; i < n; ++i) hi[i] = c.h[c.order[i]];
+    std::vector<uint64_t> keys(c.R);
+    for (int r = 0; r < c.R; ++r) keys[r] = derive_seed(c.cfg.seed, kPurposeReplica, (uint64_t)r);
+    c.d_off.upload(off, st);
+    c.d_snbr.upload(nbr, st);
+    c.d_sw.upload(w, st);
+    c.d_cm.upload(cm, st);
+    c.d_h.upload(hi, st);
+    c.d_color_start.upload(c.color_start, st);
+    c.d_slot_key.upload(keys, st);
+    c.d_spins8.alloc((size_t)c.R_local * n);
+    c.slot_smem = (size_t)n;
+    CK(cudaFuncSetAttribute((const void*)slot_sweep_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)std::max<size_t>(c.slot_smem, 48 * 1024)));
+}
+
+PlaneArgs plane_args(tg_ctx& c) {
+    PlaneArgs a{};
+    a.n = c.n;
+    a.W = c.W;
+    a.n_colors = c.n_colors;
+    a.local_states = c.R_local;
+    a.rule = c.cfg.rule;
+    a.n_types = c.n_types;
+    a.kpw = c.kpw;
+    a.m_cost = c.m_cost;
+    a.spins = c.d_spins32.p;
+    a.nbr = c.d_nbr.p;
+    a.chunks = c.d_chunks.p;
+    a.chunk_off = c.d_chunk_off.p;
+    a.color_start = c.d_color_start.p;
+    a.types = c.d_types.p;
+    a.kp = c.d_kp.p;
+    a.active = c.d_active.p;
+    a.wkey = c.d_wkey.p;
+    a.cnt_c = c.d_cnt_c.p;
+    a.cnt_q = c.d_cnt_q.p;
+    a.f_loc = c.d_f.p + c.state0;
+    a.g_loc = c.d_g.p + c.state0;
+    return a;
+}
+
+SlotArgs slot_args(tg_ctx& c) {
+    SlotArgs a{};
+    a.n = c.n;
+    a.n_colors = c.n_colors;
+    a.local_states = c.R_local;
+    a.state0 = c.state0;
+    a.rule = c.cfg.rule;
+    a.I = c.I;
+    a.J = c.J;
+    a.spins = c.d_spins8.p;
+    a.off = c.d_off.p;
+    a.nbr = c.d_snbr.p;
+    a.w = c.d_sw.p;
+    a.cm = c.d_cm.p;
+    a.h = c.d_h.p;
+    a.color_start = c.d_color_start.p;
+    a.betas = c.d_betas.p;
+    a.pens = c.d_pens.p;
+    a.state_slot = c.d_state_slot.p;
+    a.slot_key = c.d_slot_key.p;
+    a.f_loc = c.d_f.p + c.state0;
+    a.g_loc = c.d_g.p + c.state0;
+    return a;
+}
+
+SwapArgs swap_args(tg_ctx& c) {
+    SwapArgs a{};
+    a.I = c.I;
+    a.J = c.J;
+    a.R = c.R;
+    a.betas = c.d_betas.p;
+    a.pens = c.d_pens.p;
+    a.f_all = c.d_f.p;
+    a.g_all = c.d_g.p;
+    a.slot_state = c.d_slot_state.p;
+    a.state_slot = c.d_state_slot.p;
+    a.acc_p = c.d_acc_p.p;
+    a.acc_b = c.d_acc_b.p;
+    a.swap_seed = derive_seed(c.cfg.seed, kPurposeSwap, 0);
+    a.rec = c.d_rec.p;
+    a.rec_cap = c.rec_cap;
+    a.rec_acc = c.d_rec_acc.p;
+    a.plane = c.engine == TG_ENGINE_PLANE;
+    a.W = c.W;
+    a.state0 = c.state0;
+    a.local_states = c.R_local;
+    a.n_types = c.n_types;
+    a.kpw = c.kpw;
+    a.types = c.d_types.p;
+    a.ktab = c.d_ktab.p;
+    a.ktab_row = c.ktab_row;
+    a.kp = c.d_kp.p;
+    return a;
+}
+
+void launch_sweep(tg_ctx& c, int64_t t0) {
+    const int sps = (int)c.cfg.sweeps_per_swap;
+    if (c.engine == TG_ENGINE_PLANE) {
+        PlaneArgs a = plane_args(c);
+        int64_t t = t0;
+        int nsw = sps;
+        void* args[] = {&a, &t, &nsw};
+        CK(cudaLaunchCooperativeKernel(plane_sweep_fn(c.cfg.rule), dim3(c.plane_grid),
+                                       dim3(kPlaneThreads), args, 0, c.stream));
+    } else {
+        SlotArgs a = slot_args(c);
+        int64_t t = t0;
+        int nsw = sps;
+        void* args[] = {&a, &t, &nsw};
+        CK(cudaLaunchKernel(slot_sweep_fn(), dim3(c.R_local), dim3(kSlotThreads), args,
+                            c.slot_smem, c.stream));
+    }
+    c.sweep_launches++;
+}
+
+// Labels and thresholds for the current slot assignment: run the swap
+// kernel's plane-rebuild with a round that attempts nothing.
+void rebuild_planes(tg_ctx& c) {
+    if (c.engine != TG_ENGINE_PLANE) return;
+    SwapArgs a = swap_args(c);
+    // round 1 of a 1x1-like schedule attempts nothing: fake I=J=1 for the swap part
+    a.I = 1;
+    a.J = 1;
+    swap_kernel<<<1, kSwapThreads, 0, c.stream>>>(a, 1, 0, c.rec_cap, 0);
+    CK(cudaGetLastError());
+}
+
+void do_init(tg_ctx& c, const tg_run_config* cfg) {
+    if (!c.have_problem) fail(TG_ERR_CONFIG, "run: no problem set");
+    if (!c.have_schedule) fail(TG_ERR_CONFIG, "run: no schedule set");
+    if (cfg->sweeps_per_swap < 1) fail(TG_ERR_CONFIG, "run: sweeps_per_swap must be >= 1");
+    if (cfg->total_sweeps < cfg->sweeps_per_swap)
+        fail(TG_ERR_CONFIG, "run: total_sweeps must be >= sweeps_per_swap");
+    if (cfg->rule != TG_RULE_METROPOLIS && cfg->rule != TG_RULE_HEAT_BATH)
+        fail(TG_ERR_CONFIG, "run: unknown update rule %d", cfg->rule);
+    c.cfg = *cfg;
+    if (c.cfg.record_every < 1) c.cfg.record_every = 1;
+    c.I = (int)c.betas.size();
+    c.J = (int)c.pens.size();
+    c.R = c.I * c.J;
+    std::string why;
+    int eng = cfg->engine;
+    if (eng == TG_ENGINE_AUTO) eng = plane_eligible(c, nullptr) ? TG_ENGINE_PLANE : TG_ENGINE_SLOT;
+    if (eng == TG_ENGINE_PLANE && !plane_eligible(c, &why))
+        fail(TG_ERR_CONFIG, "plane engine: instance not eligible (%s)", why.c_str());
+    if (eng != TG_ENGINE_PLANE && eng != TG_ENGINE_SLOT) fail(TG_ERR_CONFIG, "unknown engine %d", eng);
+    c.engine = eng;
+    if (c.R % c.world != 0) fail(TG_ERR_CONFIG, "grid of %d replicas does not split over %d ranks", c.R, c.world);
+    c.R_local = c.R / c.world;
+    c.state0 = c.rank * c.R_local;
+    if (eng == TG_ENGINE_PLANE && c.world > 1 && c.R_local % 32 != 0)
+        fail(TG_ERR_CONFIG, "plane engine: %d replicas per rank is not a multiple of 32", c.R_local);
+    cudaStream_t st = c.stream;
+    CK(cudaSetDevice(c.device));
+    c.d_betas.upload(c.betas, st);
+    c.d_pens.upload(c.pens, st);
+    c.d_f.alloc(c.R);
+    c.d_g.alloc(c.R);
+    c.d_f.zero(st);
+    c.d_g.zero(st);
+    std::vector<int32_t> ident(c.R);
+    for (int r = 0; r < c.R; ++r) ident[r] = r;
+    c.d_slot_state.upload(ident, st);
+    c.d_state_slot.upload(ident, st);
+    c.d_perm.upload(c.order, st);
+    const int np = c.I * std::max(0, c.J - 1), nb = std::max(0, c.I - 1) * c.J;
+    c.d_acc_p.alloc(std::max(np, 1));
+    c.d_acc_b.alloc(std::max(nb, 1));
+    c.d_acc_p.zero(st);
+    c.d_acc_b.zero(st);
+    // record ring
+    const int flags = c.cfg.record_flags;
+    size_t per_state = (flags & TG_REC_GRID) ? (size_t)c.R * c.n : ((flags & TG_REC_STATE) ? (size_t)c.n : 0);
+    int cap = 1024;
+    if (per_state) cap = (int)std::max<size_t>(1, std::min<size_t>(1024, (size_t)(256u << 20) / per_state));
+    c.rec_cap = cap;
+    c.d_rec.alloc(cap + 1);  // +1: scratch entry for table rebuilds
+    c.d_rec_acc.release();
+    if (flags & TG_REC_COUNTERS) c.d_rec_acc.alloc((size_t)(cap + 1) * (np + nb + 1));
+    c.d_rec_states.release();
+    if (per_state) c.d_rec_states.alloc((size_t)cap * per_state);
+    c.h_rec.resize(cap);
+    c.h_states.resize((size_t)cap * per_state);
+    c.h_acc.resize((flags & TG_REC_COUNTERS) ? (size_t)cap * (np + nb + 1) : 0);
+    if (eng == TG_ENGINE_PLANE) build_plane(c); else build_slot(c);
+    // initial configurations (engine.cpp:98-106)
+    if (eng == TG_ENGINE_PLANE) {
+        plane_init_kernel<<<c.sms * 4, 256, 0, st>>>(c.d_spins32.p, c.n, c.W, c.R_local, c.state0, c.cfg.seed);
+    } else {
+        slot_init_kernel<<<c.sms * 4, 256, 0, st>>>(c.d_spins8.p, c.n, c.R_local, c.state0, c.cfg.seed);
+    }
+    CK(cudaGetLastError());
+    rebuild_planes(c);
+    c.rounds_done = 0;
+    c.swap_base = 0;
+    c.initialised = true;
+    CK(cudaStreamSynchronize(st));
+}
+
+struct SinkCtx {
+    tg_sink_fn fn;
+    void* user;
+};
+
+void drain(tg_ctx& c, int filled, int64_t first_round, const SinkCtx& sink) {
+    if (filled <= 0) return;
+    cudaStream_t st = c.stream;
+    CK(cudaMemcpyAsync(c.h_rec.data(), c.d_rec.p, sizeof(TgRecordDev) * filled, cudaMemcpyDeviceToHost, st));
+    const int flags = c.cfg.record_flags;
+    const size_t per_state = (flags & TG_REC_GRID) ? (size_t)c.R * c.n : ((flags & TG_REC_STATE) ? (size_t)c.n : 0);
+    if (per_state)
+        CK(cudaMemcpyAsync(c.h_states.data(), c.d_rec_states.p, per_state * filled, cudaMemcpyDeviceToHost, st));
+    const int np = c.I * std::max(0, c.J - 1), nb = std::max(0, c.I - 1) * c.J;
+    if (flags & TG_REC_COUNTERS)
+        CK(cudaMemcpyAsync(c.h_acc.data(), c.d_rec_acc.p, sizeof(int64_t) * (size_t)filled * (np + nb),
+                           cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!sink.fn) return;
+    // split counters into P / beta arrays
+    std::vector<int64_t> ap((size_t)filled * np), ab((size_t)filled * nb);
+    if (flags & TG_REC_COUNTERS)
+        for (int k = 0; k < filled; ++k) {
+            std::copy_n(c.h_acc.data() + (size_t)k * (np + nb), np, ap.data() + (size_t)k * np);
+            std::copy_n(c.h_acc.data() + (size_t)k * (np + nb) + np, nb, ab.data() + (size_t)k * nb);
+        }
+    std::vector<tg_record> out;
+    std::vector<int8_t> outs;
+    std::vector<int64_t> oap, oab;
+    for (int k = 0; k < filled; ++k) {
+        const int64_t round = first_round + k;
+        if (round % c.cfg.record_every != 0) continue;
+        const TgRecordDev& d = c.h_rec[k];
+        tg_record r;
+        r.round = round;
+        r.sweep_count = round * c.cfg.sweeps_per_swap;
+        r.f = d.f;
+        r.g = d.g;
+        r.feasible = d.feasible;
+        r.target_state = d.target_state;
+        r.digest = d.digest;
+        out.push_back(r);
+        if (per_state) outs.insert(outs.end(), c.h_states.begin() + (size_t)k * per_state,
+                                   c.h_states.begin() + (size_t)(k + 1) * per_state);
+        if (flags & TG_REC_COUNTERS) {
+            oap.insert(oap.end(), ap.begin() + (size_t)k * np, ap.begin() + (size_t)(k + 1) * np);
+            oab.insert(oab.end(), ab.begin() + (size_t)k * nb, ab.begin() + (size_t)(k + 1) * nb);
+        }
+    }
+    if (out.empty()) return;
+    const int rc = sink.fn(sink.user, out.data(), (int64_t)out.size(), per_state ? outs.data() : nullptr,
+                           (flags & TG_REC_COUNTERS) ? oap.data() : nullptr,
+                           (flags & TG_REC_COUNTERS) ? oab.data() : nullptr);
+    if (rc) fail(TG_ERR_SINK, "record sink requested stop at round %lld", (long long)(first_round + filled - 1));
+}
+
+void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
+    if (!c.initialised) fail(TG_ERR_CONFIG, "advance: context not initialised (tg_init)");
+    cudaStream_t st = c.stream;
+    const int flags = c.cfg.record_flags;
+    const bool need_extract = (flags & (TG_REC_DIGEST | TG_REC_STATE | TG_REC_GRID)) != 0;
+    const size_t per_state = (flags & TG_REC_GRID) ? (size_t)c.R * c.n : ((flags & TG_REC_STATE) ? (size_t)c.n : 0);
+    SwapArgs sa = swap_args(c);
+    const int sps = (int)c.cfg.sweeps_per_swap;
+    cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+    if (c.profiling) {
+        if (c.ev.empty()) {
+            c.ev.resize(3);
+            for (auto& e : c.ev) CK(cudaEventCreate(&e));
+        }
+        e0 = c.ev[0]; e1 = c.ev[1]; e2 = c.ev[2];
+    }
+    double sweep_ms = 0, swap_ms = 0;
+    int filled = 0;
+    int64_t first_round = c.rounds_done + 1;
+    for (int64_t k = 0; k < n_rounds; ++k) {
+        const int64_t round = c.rounds_done + 1;
+        if (c.profiling) CK(cudaEventRecord(e0, st));
+        launch_sweep(c, (round - 1) * sps);
+        if (c.profiling) CK(cudaEventRecord(e1, st));
+        if (c.world > 1) {
+            NK(ncclGroupStart());
+            NK(ncclAllGather(c.d_f.p + c.state0, c.d_f.p, c.R_local, ncclDouble, c.comm, st));
+            NK(ncclAllGather(c.d_g.p + c.state0, c.d_g.p, c.R_local, ncclDouble, c.comm, st));
+            NK(ncclGroupEnd());
+        }
+        swap_kernel<<<1, kSwapThreads, 0, st>>>(sa, round, c.swap_base, filled, flags);
+        CK(cudaGetLastError());
+        c.other_launches++;
+        if (need_extract) {
+            ExtractArgs e{};
+            e.n = c.n;
+            e.R = c.R;
+            e.W = c.W;
+            e.plane = c.engine == TG_ENGINE_PLANE;
+            e.all_slots = (flags & TG_REC_GRID) ? 1 : 0;
+            e.local_states = c.R_local;
+            e.state0 = c.state0;
+            e.slot_state = c.d_slot_state.p;
+            e.spins32 = c.d_spins32.p;
+            e.spins8 = c.d_spins8.p;
+            e.perm = c.d_perm.p;
+            e.states = per_state ? c.d_rec_states.p + (size_t)filled * per_state : nullptr;
+            uint64_t* dg = (flags & TG_REC_DIGEST) ? &c.d_rec.p[filled].digest : nullptr;
+            e.digest = dg;
+            const long long total = (long long)(e.all_slots ? c.R : 1) * c.n;
+            const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)c.sms * 8);
+            extract_kernel<<<std::max(blocks, 1), 256, 0, st>>>(e);
+            CK(cudaGetLastError());
+            c.other_launches++;
+            if (c.world > 1) {
+                if (dg) NK(ncclAllReduce(dg, dg, 1, ncclUint64, ncclSum, c.comm, st));
+                if (e.states) NK(ncclAllReduce(e.states, e.states, per_state, ncclInt8, ncclSum, c.comm, st));
+            }
+        }
+        if (c.profiling) {
+            CK(cudaEventRecord(e2, st));
+            CK(cudaEventSynchronize(e2));
+            float a = 0, b = 0;
+            CK(cudaEventElapsedTime(&a, e0, e1));
+            CK(cudaEventElapsedTime(&b, e1, e2));
+            sweep_ms += a;
+            swap_ms += b;
+        }
+        c.swap_base += (uint64_t)round_attempts(c.I, c.J, round);
+        c.rounds_done = round;
+        ++filled;
+        if (filled == c.rec_cap) {
+            drain(c, filled, first_round, sink);
+            filled = 0;
+            first_round = c.rounds_done + 1;
+        }
+    }
+    drain(c, filled, first_round, sink);
+    CK(cudaStreamSynchronize(st));
+    c.last_sweep_ms = sweep_ms;
+    c.last_swap_ms = swap_ms;
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+
+extern "C" {
+
+int tg_abi_version(void) { return TG_ABI_VERSION; }
+
+static int create_impl(int device, int rank, int world, const void* nccl_id, tg_ctx** out) {
+    if (!out) return TG_ERR_CONFIG;
+    *out = nullptr;
+    tg_ctx* c = new tg_ctx();
+    const int rc = guard(nullptr, [&] {
+        int count = 0;
+        cudaError_t e = cudaGetDeviceCount(&count);
+        if (e != cudaSuccess || count == 0)
+            fail(TG_ERR_CUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+        if (device < 0 || device >= count) fail(TG_ERR_CONFIG, "device %d out of range", device);
+        c->device = device;
+        c->rank = rank;
+        c->world = world;
+        CK(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10)
+            fail(TG_ERR_CUDA, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor);
+        c->sms = prop.multiProcessorCount;
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        if (world > 1) {
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof(id));
+            NK(ncclCommInitRank(&c->comm, world, id, rank));
+        }
+    });
+    if (rc != TG_OK) {
+        delete c;
+        return rc;
+    }
+    *out = c;
+    return TG_OK;
+}
+
+int tg_create(int device, tg_ctx** out) { return create_impl(device, 0, 1, nullptr, out); }
+
+int tg_create_distributed(int device, int rank, int world_size, const void* nccl_id, tg_ctx** out) {
+    if (world_size < 1 || rank < 0 || rank >= world_size || (world_size > 1 && !nccl_id)) {
+        g_create_error = "tg_create_distributed: bad rank/world/id";
+        return TG_ERR_CONFIG;
+    }
+    return create_impl(device, rank, world_size, nccl_id, out);
+}
+
+int tg_nccl_unique_id(void* out128) {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return TG_ERR_CUDA;
+    std::memcpy(out128, &id, sizeof(id));
+    return TG_OK;
+}
+
+void tg_destroy(tg_ctx* ctx) { delete ctx; }
+
+size_t tg_last_error(const tg_ctx* ctx, char* buf, size_t len) {
+    const std::string& s = ctx ? ctx->err : g_create_error;
+    if (buf && len) {
+        const size_t k = std::min(len - 1, s.size());
+        std::memcpy(buf, s.data(), k);
+        buf[k] = '\0';
+    }
+    return s.size();
+}
+
+int tg_set_problem(tg_ctx* ctx, int n, int n_couplings, const int32_t* ci, const int32_t* cj,
+                   const double* w, const double* fields, int n_pairs, const int32_t* pa,
+                   const int32_t* pb) {
+    if (!ctx) return TG_ERR_CONFIG;
+    return guard(ctx, [&] {
+        // IsingModel validation (ising.cpp:21-46) and ConstraintSet (constraints.cpp:16-26)
+        if (n <= 0) fail(TG_ERR_CONFIG, "model: n_spins must be positive");
+        if (n_couplings < 0 || n_pairs < 0) fail(TG_ERR_CONFIG, "model: negative counts");
+        std::vector<std::pair<int, int>> keys;
+        std::vector<int> a(n_couplings), b(n_couplings), qa(n_pairs), qb(n_pairs);
+        for (int k = 0; k < n_couplings; ++k) {
+            int x = ci[k], y = cj[k];
+            if (x == y) fail(TG_ERR_CONFIG, "model: self-loop on spin %d", x);
+            if (x > y) std::swap(x, y);
+            if (x < 0 || y >= n) fail(TG_ERR_CONFIG, "model: coupling index out of range: (%d, %d)", x, y);
+            if (!std::isfinite(w[k])) fail(TG_ERR_CONFIG, "model: coupling weights must be finite");
+            a[k] = x;
+            b[k] = y;
+            keys.emplace_back(x, y);
+        }
+        std::sort(keys.begin(), keys.end());
+        for (size_t k = 1; k < keys.size(); ++k)
+            if (keys[k] == keys[k - 1])
+                fail(TG_ERR_CONFIG, "model: duplicate coupling (%d, %d)", keys[k].first, keys[k].second);
+        for (int k = 0; k < n_pairs; ++k) {
+            int x = pa[k], y = pb[k];
+            if (x == y) fail(TG_ERR_CONFIG, "constraint: pair on a single spin %d", x);
+            if (x > y) std::swap(x, y);
+            if (x < 0 || y >= n) fail(TG_ERR_CONFIG, "constraint: index out of range: (%d, %d)", x, y);
+            qa[k] = x;
+            qb[k] = y;
+        }
+        ctx->n = n;
+        ctx->ci = a;
+        ctx->cj = b;
+        ctx->cw.assign(w, w + n_couplings);
+        ctx->h.assign(n, 0.0);
+        if (fields) for (int i = 0; i < n; ++i) ctx->h[i] = fields[i];
+        for (double x : ctx->h) if (!std::isfinite(x)) fail(TG_ERR_CONFIG, "model: fields must be finite");
+        ctx->pa = qa;
+        ctx->pb = qb;
+        canonical(n, ctx->ci, ctx->cj, ctx->pa, ctx->pb, ctx->order, ctx->color, ctx->n_colors);
+        ctx->inv.assign(n, 0);
+        for (int k = 0; k < n; ++k) ctx->inv[ctx->order[k]] = k;
+        ctx->color_start.assign(ctx->n_colors + 1, 0);
+        for (int k = 0; k < n; ++k) ctx->color_start[ctx->color[ctx->order[k]] + 1]++;
+        for (int q = 0; q < ctx->n_colors; ++q) ctx->color_start[q + 1] += ctx->color_start[q];
+        ctx->have_problem = true;
+        ctx->initialised = false;
+    });
+}
+
+int tg_set_schedule(tg_ctx* ctx, int n_betas, const double* betas, int n_penalties,
+                    const double* penalties) {
+    if (!ctx) return TG_ERR_CONFIG;
+    return guard(ctx, [&] {
+        std::vector<double> b(betas, betas + std::max(n_betas, 0));
+        std::vector<double> p(penalties, penalties + std::max(n_penalties, 0));
+        check_vec(b, "beta");
+        check_vec(p, "penalty");
+        for (double x : p) if (x < 0.0) fail(TG_ERR_CONFIG, "build_effective: penalty must be >= 0");
+        ctx->betas = b;
+        ctx->pens = p;
+        ctx->have_schedule = true;
+        ctx->initialised = false;
+    });
+}
+
+int tg_init(tg_ctx* ctx, const tg_run_config* cfg) {
+    if (!ctx || !cfg) return TG_ERR_CONFIG;
+    return guard(ctx, [&] { do_init(*ctx, cfg); });
+}
+
+int tg_advance(tg_ctx* ctx, int64_t n_rounds, tg_sink_fn sink, void* user) {
+    if (!ctx) return TG_ERR_CONFIG;
+    return guard(ctx, [&] { do_advance(*ctx, n_rounds, SinkCtx{sink, user}); });
+}
+
+int tg_run(tg_ctx* ctx, const tg_run_config* cfg, tg_sink_fn sink, void* user) {
+    if (!ctx || !cfg) return TG_ERR_CONFIG;
+    return guard(ctx, [&] {
+        do_init(*ctx, cfg);
+        do_advance(*ctx, cfg->total_sweeps / cfg->sweeps_per_swap, SinkCtx{sink, user});
+    });
+}
+
+int tg_get_state(tg_ctx* ctx, int slot, int8_t* out) {
+    if (!ctx) return TG_ERR_CONFIG;
+    return guard(ctx, [&] {
+        tg_ctx& c = *ctx;
+        if (!c.initialised) fail(TG_ERR_CONFIG, "get_state: context not initialised");
+        if (slot < 0 || slot >= c.R) fail(TG_ERR_CONFIG, "get_state: slot %d out of range", slot);
+        // reuse the extract kernel on a one-slot view: temporarily point slot R-1 at `slot`
+        std::vector<int32_t> ss(c.R);
+        CK(cudaMemcpyAsync(ss.data(), c.d_slot_state.p, sizeof(int32_t) * c.R, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        DBuf<int32_t> view;
+        std::vector<int32_t> v(c.R, ss[slot]);
+        view.upload(v, c.stream);
+        DBuf<int8_t> dst;
+        dst.alloc(c.n);
+        ExtractArgs e{};
+        e.n = c.n;
+        e.R = c.R;
+        e.W = c.W;
+        e.plane = c.engine == TG_ENGINE_PLANE;
+        e.all_slots = 0;
+        e.local_states = c.R_local;
+        e.state0 = c.state0;
+        e.slot_state = view.p;
+        e.spins32 = c.d_spins32.p;
+        e.spins8 = c.d_spins8.p;
+        e.perm = c.d_perm.p;
+        e.states = dst.p;
+        e.digest = nullptr;
+        extract_kernel<<<std::max(1, std::min((c.n + 255) / 256, c.sms * 8)), 256, 0, c.stream>>>(e);
+        CK(cudaGetLastError());
+        if (c.world > 1) NK(ncclAllReduce(dst.p, dst.p, c.n, ncclInt8, ncclSum, c.comm, c.stream));
+        CK(cudaMemcpyAsync(out, dst.p, c.n, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int tg_get_counters(tg_ctx* ctx, int64_t* attempts_p, int64_t* accepts_p, int64_t* attempts_b,
+                    int64_t* accepts_b) {
+    if (!ctx) return TG_ERR_CONFIG;
+    return guard(ctx, [&] {
+        tg_ctx& c = *ctx;
+        if (!c.initialised) fail(TG_ERR_CONFIG, "get_counters: context not initialised");
+        const int np = c.I * std::max(0, c.J - 1), nb = std::max(0, c.I - 1) * c.J;
+        if (accepts_p && np) CK(cudaMemcpyAsync(accepts_p, c.d_acc_p.p, sizeof(int64_t) * np, cudaMemcpyDeviceToHost, c.stream));
+        if (accepts_b && nb) CK(cudaMemcpyAsync(accepts_b, c.d_acc_b.p, sizeof(int64_t) * nb, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        std::vector<int64_t> ap(np, 0), ab(nb, 0);
+        for (int64_t r = 1; r <= c.rounds_done; ++r) {
+            int even, dp, db;
+            round_phase(c.I, c.J, r, even, dp, db);
+            if (dp) for (int i = 0; i < c.I; ++i) for (int p = even; p + 1 < c.J; p += 2) ap[i * (c.J - 1) + p]++;
+            if (db) for (int j = 0; j < c.J; ++j) for (int b = even; b + 1 < c.I; b += 2) ab[b * c.J + j]++;
+        }
+        if (attempts_p) std::copy(ap.begin(), ap.end(), attempts_p);
+        if (attempts_b) std::copy(ab.begin(), ab.end(), attempts_b);
+    });
+}
+
+int tg_get_energies(tg_ctx* ctx, double* f, double* g) {
+    if (!ctx) return TG_ERR_CONFIG;
+    return guard(ctx, [&] {
+        tg_ctx& c = *ctx;
+        if (!c.initialised) fail(TG_ERR_CONFIG, "get_energies: context not initialised");
+        std::vector<double> fs(c.R), gs(c.R);
+        std::vector<int32_t> ss(c.R);
+        CK(cudaMemcpyAsync(fs.data(), c.d_f.p, sizeof(double) * c.R, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaMemcpyAsync(gs.data(), c.d_g.p, sizeof(double) * c.R, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaMemcpyAsync(ss.data(), c.d_slot_state.p, sizeof(int32_t) * c.R, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        for (int s = 0; s < c.R; ++s) {
+            if (f) f[s] = fs[ss[s]];
+            if (g) g[s] = gs[ss[s]];
+        }
+    });
+}
+
+int tg_get_info(tg_ctx* ctx, tg_info* info) {
+    if (!ctx || !info) return TG_ERR_CONFIG;
+    std::memset(info, 0, sizeof(*info));
+    info->engine = ctx->engine;
+    info->n_colors = ctx->n_colors;
+    info->n_replicas = ctx->R;
+    info->local_replicas = ctx->R_local;
+    info->words = ctx->W;
+    info->device_sms = ctx->sms;
+    info->rounds_done = ctx->rounds_done;
+    info->last_sweep_ms = ctx->last_sweep_ms;
+    info->last_swap_ms = ctx->last_swap_ms;
+    info->sweep_launches = ctx->sweep_launches;
+    info->other_launches = ctx->other_launches;
+    return TG_OK;
+}
+
+void* tg_stream(tg_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int tg_set_profiling(tg_ctx* ctx, int on) {
+    if (!ctx) return TG_ERR_CONFIG;
+    ctx->profiling = on != 0;
+    return TG_OK;
+}
+
+int tg_canonical_order(int n, int n_couplings, const int32_t* ci, const int32_t* cj, int n_pairs,
+                       const int32_t* pa, const int32_t* pb, int32_t* order, int32_t* color,
+                       int32_t* n_colors) {
+    return guard(nullptr, [&] {
+        if (n <= 0) fail(TG_ERR_CONFIG, "model: n_spins must be positive");
+        std::vector<int> a(ci, ci + n_couplings), b(cj, cj + n_couplings), x(pa, pa + n_pairs), y(pb, pb + n_pairs);
+        for (int k = 0; k < n_couplings; ++k)
+            if (a[k] < 0 || a[k] >= n || b[k] < 0 || b[k] >= n || a[k] == b[k]) fail(TG_ERR_CONFIG, "bad coupling");
+        for (int k = 0; k < n_pairs; ++k)
+            if (x[k] < 0 || x[k] >= n || y[k] < 0 || y[k] >= n || x[k] == y[k]) fail(TG_ERR_CONFIG, "bad pair");
+        std::vector<int> ord, col;
+        int nc = 0;
+        canonical(n, a, b, x, y, ord, col, nc);
+        for (int i = 0; i < n; ++i) {
+            if (order) order[i] = ord[i];
+            if (color) color[i] = col[i];
+        }
+        if (n_colors) *n_colors = nc;
+    });
+}
+
+double tg_p_swap_probability(double beta, double d_penalty, double dg) {
+    const double x = beta * d_penalty * dg;
+    return x >= 0.0 ? 1.0 : std::exp(x);
+}
+double tg_beta_swap_probability(double d_beta, double d_energy) {
+    const double x = d_beta * d_energy;
+    return x >= 0.0 ? 1.0 : std::exp(x);
+}
+double tg_general_swap_probability(double beta_a, double beta_b, double de_a, double de_b) {
+    const double x = beta_a * de_a + beta_b * de_b;
+    return x >= 0.0 ? 1.0 : std::exp(x);
+}
+
+int tg_swap_phase_host(int n_betas, const double* betas, int n_penalties, const double* penalties,
+                       int64_t round, int /*direction*/, uint64_t seed, uint64_t swap_base,
+                       const double* f_state, const double* g_state, int32_t* slot_state,
+                       int64_t* accepts_p, int64_t* accepts_b) {
+    const int I = n_betas, J = n_penalties;
+    if (I < 1 || J < 1 || round < 1) return TG_ERR_CONFIG;
+    const uint64_t swap_seed = derive_seed(seed, kPurposeSwap, 0);
+    const int64_t n_att = round_attempts(I, J, round);
+    for (int k = 0; k < n_att; ++k) {
+        int sa, sb, ctr, is_p;
+        if (swap_attempt(I, J, betas, penalties, round, k, f_state, g_state, slot_state, swap_seed,
+                         swap_base, sa, sb, ctr, is_p)) {
+            std::swap(slot_state[sa], slot_state[sb]);
+            if (is_p) { if (accepts_p) accepts_p[ctr]++; }
+            else if (accepts_b) accepts_b[ctr]++;
+        }
+    }
+    return TG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,193 @@
+// engine.cuh -- device data layout shared by the sweep, swap and record
+// kernels (kernels.cu) and the host driver (capi.cu).
+//
+// Two sweep engines implement the reference sweep (mc.cpp:21-35) over the
+// canonical colour order, in which the reference's sequential index-order
+// pass is a chromatic pass:
+//   * SLOT  -- int8 spins, one CTA per replica with its configuration in
+//              shared memory, FP64 fields, 64-bit draws from the replica's
+//              grid-slot stream (the reference's RNG association).
+//   * PLANE -- multi-spin coding: bit l of word w at site i is the spin of
+//              physical replica 32w+l; 32 replicas per 32-bit lane op, threshold
+//              planes instead of exp(), lazily consumed bit-plane draws.
+// Swaps permute grid labels (slot_state / state_slot); spin states never move.
+#pragma once
+
+#include <stdint.h>
+
+#include "philox.cuh"
+
+namespace tg {
+
+constexpr int kKPlanes = 53;              // planes of a 53-bit threshold
+constexpr int kKWords = kKPlanes + 1;     // + the "always" word
+constexpr int kMaxDC = 7;                 // plane engine: cost degree bound
+constexpr int kMaxDQ = 3;                 // plane engine: chain degree bound
+constexpr int kVPlanes = 8;               // vertical counter planes
+constexpr int kMaxTypes = 32;
+
+// One (cost degree, chain degree) class of sites in the plane engine.
+struct PlaneType {
+    int dc, dq;      // cost / chain degree of every site of this type
+    int ncb, nqb;    // bits of the n_c / n_q bit-sliced counters
+    int ncl;         // classes = 1 << (ncb+nqb), padded to >= 4
+    int kp_off;      // word offset of this type's [54][ncl] block inside one word block
+    int ktab_off;    // offset of this type's classes inside one slot row of ktab
+    int pad;
+};
+
+// A run of <= 32 consecutive sites of one colour and one type.
+struct Chunk {
+    int start;       // first internal site
+    int len;         // 1..32
+    int type;        // PlaneType index
+    int nbr_base;    // offset into nbr[] of site `start`
+};
+
+struct PlaneArgs {
+    int n;                // sites
+    int W;                // 32-replica words per site on this rank
+    int n_colors;
+    int local_states;     // replicas on this rank (<= 32*W)
+    int rule;
+    int n_types;
+    int kpw;              // words per word-block of kp
+    int m_cost;           // number of cost couplings (whole instance)
+    uint32_t* spins;      // [n][W]
+    const int32_t* nbr;   // per site: dc cost neighbours (bit31 = J<0), dq chain partners
+    const Chunk* chunks;  // all colours, concatenated
+    const int* chunk_off; // [n_colors+1]
+    const int* color_start; // [n_colors+1] internal site ranges
+    const PlaneType* types;
+    const uint32_t* kp;   // [W][kpw] threshold planes for the current labels
+    const uint32_t* active; // [W] lane masks of real replicas
+    const uint2* wkey;    // [W] Philox key of each word group
+    int32_t* cnt_c;       // [32W] unsatisfied cost bonds (accumulated)
+    int32_t* cnt_q;       // [32W] unsatisfied chain bonds
+    double* f_loc;        // [local_states]
+    double* g_loc;
+};
+
+struct SlotArgs {
+    int n;
+    int n_colors;
+    int local_states;
+    int state0;           // global id of local state 0
+    int rule;
+    int I, J;
+    int8_t* spins;        // [local_states][n]
+    const int* off;       // merged CSR [n+1], neighbours in increasing index order
+    const int32_t* nbr;
+    const double* w;      // cost weight J (0 for pure chain entries)
+    const int8_t* cm;     // chain multiplicity of the entry
+    const double* h;      // fields
+    const int* color_start;
+    const double* betas;
+    const double* pens;
+    const int32_t* state_slot; // [R] slot of each physical state
+    const uint64_t* slot_key;  // [R] derive_seed(seed, replica, slot)
+    double* f_loc;
+    double* g_loc;
+};
+
+struct SwapArgs {
+    int I, J, R;
+    const double* betas;
+    const double* pens;
+    const double* f_all;   // [R] per physical state
+    const double* g_all;
+    int32_t* slot_state;   // [R]
+    int32_t* state_slot;   // [R]
+    int64_t* acc_p;        // [I*(J-1)]
+    int64_t* acc_b;        // [(I-1)*J]
+    uint64_t swap_seed;
+    // record
+    void* rec;             // tg_record ring
+    int rec_cap;
+    int64_t* rec_acc;      // [cap][np+nb] or null
+    // plane-engine label tables
+    int plane;
+    int W, state0, local_states, n_types, kpw;
+    const PlaneType* types;
+    const uint64_t* ktab;  // [R][ktab_row]: 53-bit thresholds (>= 2^53: always)
+    int ktab_row;
+    uint32_t* kp;
+};
+
+// ---------------------------------------------------------------- swaps
+
+// Reference round schedule (engine.cpp:121-146,216): parity alternates every
+// round; the direction (P first) flips after every even round.
+TG_HD void round_phase(int I, int J, int64_t round, int& even, int& do_p, int& do_b) {
+    even = (round % 2 == 0) ? 1 : 0;
+    const int direction = (((round - 1) / 2) % 2 == 0) ? 1 : -1;
+    if (I == 1 && J == 1) { do_p = do_b = 0; }
+    else if (I == 1) { do_p = 1; do_b = 0; }
+    else if (J == 1) { do_p = 0; do_b = 1; }
+    else { do_p = direction == 1; do_b = !do_p; }
+}
+
+TG_HD int pairs_in(int len, int even) { return len - even >= 2 ? (len - even) / 2 : 0; }
+
+TG_HD int64_t round_attempts(int I, int J, int64_t round) {
+    int even, dp, db;
+    round_phase(I, J, round, even, dp, db);
+    return dp ? (int64_t)I * pairs_in(J, even) : (db ? (int64_t)J * pairs_in(I, even) : 0);
+}
+
+TG_HD double dadd_mul(double f, double p, double g) {
+#if defined(__CUDA_ARCH__)
+    return __dadd_rn(f, __dmul_rn(p, g));  // no FMA contraction: match the reference
+#else
+    return f + p * g;
+#endif
+}
+
+TG_HD double dexp(double x) {
+#if defined(__CUDA_ARCH__)
+    return exp(x);
+#else
+    return __builtin_exp(x);
+#endif
+}
+
+// Attempt k of the round: P phase rows i ascending, pairs p = even, even+2..
+// (engine.cpp:148-167); beta phase columns j ascending, pairs b = even, ..
+// (engine.cpp:168-187).  One swap-stream draw per attempt in that order.
+// Returns 1 on accept and reports the two slots and the counter index.
+TG_HD int swap_attempt(int I, int J, const double* betas, const double* pens, int64_t round,
+                       int k, const double* f_all, const double* g_all, const int32_t* slot_state,
+                       uint64_t swap_seed, uint64_t swap_base, int& slot_a, int& slot_b,
+                       int& counter, int& is_p) {
+    int even, dp, db;
+    round_phase(I, J, round, even, dp, db);
+    const double u = (double)(stream_bits(swap_seed, swap_base + (uint64_t)k) >> 11) * 0x1.0p-53;
+    double x;
+    if (dp) {
+        const int per = pairs_in(J, even);
+        const int i = k / per;
+        const int p = even + 2 * (k % per);
+        slot_a = i * J + p;
+        slot_b = slot_a + 1;
+        const int a = slot_state[slot_a], b = slot_state[slot_b];
+        x = betas[i] * (pens[p + 1] - pens[p]) * (g_all[b] - g_all[a]);
+        counter = i * (J - 1) + p;
+        is_p = 1;
+    } else {
+        const int per = pairs_in(I, even);
+        const int j = k / per;
+        const int b = even + 2 * (k % per);
+        slot_a = b * J + j;
+        slot_b = (b + 1) * J + j;
+        const int lo = slot_state[slot_a], hi = slot_state[slot_b];
+        const double pj = pens[j];
+        const double e_lo = dadd_mul(f_all[lo], pj, g_all[lo]);
+        const double e_hi = dadd_mul(f_all[hi], pj, g_all[hi]);
+        x = (betas[b + 1] - betas[b]) * (e_hi - e_lo);
+        counter = b * J + j;
+        is_p = 0;
+    }
+    return (x >= 0.0 || u < dexp(x)) ? 1 : 0;
+}
+
+}  // namespace tg

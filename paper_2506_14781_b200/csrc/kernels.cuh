@@ -1,0 +1,46 @@
+// kernels.cuh -- launch interface of kernels.cu for the host driver.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "engine.cuh"
+
+namespace tg {
+
+constexpr int kPlaneThreads = 512;
+constexpr int kSlotThreads = 256;
+constexpr int kSwapThreads = 1024;
+
+// Device image of tg_record (same layout as the C-ABI struct).
+struct TgRecordDev {
+    int64_t round;
+    int64_t sweep_count;
+    double f;
+    double g;
+    int32_t feasible;
+    int32_t target_state;
+    uint64_t digest;
+};
+
+struct ExtractArgs {
+    int n, R, W, plane, all_slots, local_states, state0;
+    const int32_t* slot_state;
+    const uint32_t* spins32;
+    const int8_t* spins8;
+    const int32_t* perm;  // internal -> caller index
+    int8_t* states;       // [1 or R][n] caller order, or null
+    uint64_t* digest;     // record digest slot, or null
+};
+
+void* plane_sweep_fn(int rule);
+void* slot_sweep_fn();
+
+__global__ void swap_kernel(SwapArgs a, int64_t round, uint64_t swap_base, int rec_idx,
+                            int rec_flags);
+__global__ void extract_kernel(ExtractArgs e);
+__global__ void plane_init_kernel(uint32_t* spins, int n, int W, int local_states, int state0,
+                                  uint64_t seed);
+__global__ void slot_init_kernel(int8_t* spins, int n, int local_states, int state0, uint64_t seed);
+
+}  // namespace tg
