@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""bench.py -- spin-flips/s of the 2D-PT hot path on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json config 5, the configuration the metric is quoted on):
+random bipartite 3-regular Ising graph, J = +-1, h = 0, copy-constraint chain
+pairs on 10% of the nodes, N = 2^20 physical spins, 16 x 16 (beta, P) grid
+(beta geometric 0.2-5, P_cfg linear 0-4 -> P_ref = P_cfg/4 rounded to 1/64),
+one sweep per swap round, Metropolis.  Synthetic instance, seed 1 (there is no
+public benchmark suite).
+
+A "step" = ROUNDS rounds of (one chromatic sweep of all 256 replicas, one
+swap phase, one trace record).  spin-flips/s = N x replicas x sweeps / time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Rank 0 prints ONE JSON line.  Under torchrun each rank sweeps 256/N replicas
+(column blocks of the grid) and the per-round (f, g) all-gather runs over
+NCCL inside the engine; timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "spin-flips/s (whole box) at 1/2/4/8 B200 and % of sweep roofline vs CPU ref"
+UNIT = "spin-flips/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1 << 20, help="physical spins")
+    ap.add_argument("--rounds", type=int, default=100, help="rounds per step")
+    ap.add_argument("--sps", type=int, default=1, help="sweeps per swap")
+    ap.add_argument("--rule", default="metropolis")
+    ap.add_argument("--engine", default="plane")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sweeps", type=int, default=2, help="marginal sweeps of the CPU sample")
+    return ap.parse_args()
+
+
+def workload(n):
+    from paper_2506_14781_b200 import instances as I
+    pr = I.bipartite_3regular(n, seed=1)
+    betas, pens = I.config_schedule("c5")
+    return pr, betas, pens
+
+
+def b_alg(pr):
+    """Algorithmic bytes per spin update: (mean degree + 1) int8."""
+    deg = 2.0 * (pr.n_couplings + pr.n_pairs) / pr.n
+    return deg + 1.0
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[2 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_setup(gpus):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def reduce_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------- CPU legs
+
+def cpu_reference_rate(pr, betas, pens, sweeps, threads):
+    """Marginal updates/s of the unmodified reference run_2dpt (oracle/_ref O1
+    when built here, else the C port) from two run lengths."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    kind = "reference" if O.ref_available("mt") else "port"
+    R = len(betas) * len(pens)
+
+    def run(S):
+        t = time.perf_counter()
+        if kind == "reference":
+            O.ref_timed("mt", pr, betas, pens, S, 1, seed=1, threads=threads)
+        else:
+            O.run(pr, betas, pens, S, 1, seed=1, final_grid=False)
+        return time.perf_counter() - t
+
+    t1 = run(1)
+    t2 = run(1 + sweeps)
+    dt = max(t2 - t1, 1e-9)
+    rate = pr.n * R * sweeps / dt
+    return rate, kind, dt
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    pr, betas, pens = workload(args.n)
+    threads = os.cpu_count() or 1
+    vals = []
+    kind = "reference"
+    dts = []
+    for k in range(args.warmup + args.steps):
+        rate, kind, dt = cpu_reference_rate(pr, betas, pens, args.cpu_sweeps, threads)
+        if k >= args.warmup:
+            vals.append(rate)
+            dts.append(dt)
+    value = statistics.median(vals)
+    sample = (f"run_2dpt on the full workload (N={pr.n}, 16x16 grid), marginal rate of "
+              f"{1 + args.cpu_sweeps} vs 1 sweeps, RunConfig.threads={threads}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.median(dts), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C5 bipartite 3-regular N=2^{pr.n.bit_length() - 1} 16x16 sps=1 "
+                               "Metropolis (CPU reference, mt19937_64)",
+                   "n_spins": pr.n, "replicas": 256, "sweeps_per_step": args.cpu_sweeps},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- GPU leg
+
+def run_ours(args, rank, world, local):
+    import numpy as np
+    import torch
+    from paper_2506_14781_b200.api import Engine, RunConfig
+
+    torch.cuda.set_device(local)
+    pr, betas, pens = workload(args.n)
+    R = len(betas) * len(pens)
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        obj = [Engine.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    eng = Engine(local, rank, world, nccl_id)
+    eng.set_problem(pr)
+    eng.set_schedule(betas, pens)
+    total = args.rounds * args.sps * (args.warmup + args.steps + 1)
+    cfg = RunConfig(total_sweeps=total, sweeps_per_swap=args.sps, seed=1, rule=args.rule,
+                    engine=args.engine, store_states=False, digest=False)
+    eng.init(cfg, flags=0)
+    eng.set_profiling(True)
+    stream = torch.cuda.ExternalStream(eng.stream_ptr())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def step():
+        eng.advance(args.rounds)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    info0 = eng.info()
+    sweep_ms = 0.0
+    step_ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()  # L2 flush between timed steps (not timed)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            sweep_ms += eng.info()["last_sweep_ms"]
+    torch.cuda.synchronize()
+    barrier(world)
+    info1 = eng.info()
+    total_ms = reduce_max(sum(step_ms), world)
+    sweeps = args.steps * args.rounds * args.sps
+    updates = float(pr.n) * R * sweeps  # all ranks together
+    value = updates / (total_ms / 1e3)
+    launches = (info1["sweep_launches"] - info0["sweep_launches"]) + \
+               (info1["other_launches"] - info0["other_launches"])
+    # roofline of the dominant kernel (the sweep): algorithmic bytes per launch / mean launch time
+    n_sweep_launches = info1["sweep_launches"] - info0["sweep_launches"]
+    mean_sweep_s = reduce_max(sweep_ms, world) / 1e3 / max(n_sweep_launches, 1)
+    bal = b_alg(pr)
+    # updates of this rank per launch of the dominant kernel
+    bytes_per_launch = bal * pr.n * (R / world) * sweeps / max(n_sweep_launches, 1)
+    peaks = load_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    smem_peak_gbs = 148 * 128 * sm_max * 1e6 / 1e9  # SURVEY.md §8d official smem roofline
+    achieved_gbs = bytes_per_launch / mean_sweep_s / 1e9
+    clocks = clk.summary()
+    eng.close()
+
+    # e2e: the public API with host buffers -- H2D of the instance, init, the
+    # same rounds, records to a host sink, D2H of the target configuration.
+    e2e = None
+    if world == 1:
+        from paper_2506_14781_b200.api import run_2dpt, Schedule
+        cfg2 = RunConfig(total_sweeps=args.rounds * args.sps, sweeps_per_swap=args.sps, seed=2,
+                         rule=args.rule, engine=args.engine, store_states=False, digest=False)
+        h2d = sum(a.nbytes for a in (pr.ci, pr.cj, pr.cw, pr.fields, pr.pa, pr.pb)) + 8 * (
+            len(betas) + len(pens))
+        times = []
+        for k in range(args.warmup + args.steps):
+            t = time.perf_counter()
+            e = Engine(local)
+            e.set_problem(pr)
+            e.set_schedule(betas, pens)
+            recs = []
+            e.run(cfg2, lambda r, n, s, a, b: recs.append(n) or 0, flags=0)
+            tgt = e.state(R - 1)
+            e.close()
+            dt = time.perf_counter() - t
+            if k >= args.warmup:
+                times.append(dt)
+        d2h = tgt.nbytes + 48 * args.rounds
+        e2e = {"value": float(pr.n) * R * args.rounds * args.sps / statistics.median(times),
+               "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": 1e3 * statistics.median(times)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, kind, dt = cpu_reference_rate(pr, betas, pens, args.cpu_sweeps, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
+               "sample": f"unmodified reference run_2dpt (mt19937_64, Metropolis, FP64) on the "
+                         f"same N={pr.n} instance and 16x16 grid; marginal rate of "
+                         f"{1 + args.cpu_sweeps} vs 1 sweeps ({dt:.1f} s of sweeping)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic",
+            "config": {"workload": f"C5 bipartite 3-regular N=2^{pr.n.bit_length() - 1} 16x16 "
+                                   f"sps={args.sps} {args.rule}",
+                       "n_spins": pr.n, "replicas": R, "rounds_per_step": args.rounds,
+                       "engine": args.engine, "parallelism": f"replica-split x{world}",
+                       "l2": "flushed between timed steps (256 MB write)"},
+            "roofline": {"bound": "smem", "achieved": achieved_gbs, "peak": smem_peak_gbs,
+                         "unit": "GB/s", "frac": achieved_gbs / smem_peak_gbs, "traffic": None,
+                         "kernel": "plane_sweep_kernel",
+                         "bytes_per_update": bal,
+                         "mean_launch_ms": mean_sweep_s * 1e3,
+                         "peak_note": "148 SM x 128 B/clk x sm_max_mhz (MEASURED_PEAKS.json), "
+                                      "SURVEY.md §8d"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -18,8 +18,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtempergrid_b200.so")
 CPPLIB = os.path.join(PKG, "libtempergrid_cpp.so")
-SOURCES = ["kernels.cu", "capi.cu"]
-HEADERS = ["engine.cuh", "kernels.cuh", "philox.cuh"]
+SOURCES = ["kernels.cu", "capi.cu", "plane_sweep.cu"]
+HEADERS = ["engine.cuh", "kernels.cuh", "philox.cuh", "plane_device.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -38,22 +38,39 @@ def _stale(target: str, deps) -> bool:
 
 
 def build_engine(force: bool = False, verbose: bool = False) -> str:
+    """Compile each translation unit to an object in parallel, then link."""
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "tempergrid_b200.h"))
     if not force and not _stale(LIB, deps):
         return LIB
-    cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v",
-           "-Xcompiler", "-fPIC", "-shared", "-o", LIB,
-           *[os.path.join(CSRC, f) for f in SOURCES], "-lnccl"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(PKG, "build_ptxas.log")
-    with open(log, "w") as fh:
-        fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+    units = [("kernels.cu", "kernels.o", []), ("capi.cu", "capi.o", []),
+             ("plane_sweep.cu", "plane_r0.o", ["-DTG_PLANE_RULE=0"]),
+             ("plane_sweep.cu", "plane_r1.o", ["-DTG_PLANE_RULE=1"])]
+    procs = []
+    for src, obj, extra in units:
+        cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v",
+               "-Xcompiler", "-fPIC", *extra, "-c", os.path.join(CSRC, src),
+               "-o", os.path.join(objdir, obj)]
+        procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                            text=True)))
+    log = []
+    ok = True
+    for cmd, pr in procs:
+        out, err = pr.communicate()
+        log.append(" ".join(cmd) + "\n" + out + err)
+        ok &= pr.returncode == 0
+    with open(os.path.join(PKG, "build_ptxas.log"), "w") as fh:
+        fh.write("\n".join(log))
+    if not ok:
+        sys.stderr.write("\n".join(log))
         raise RuntimeError("nvcc failed building %s" % LIB)
+    link = [nvcc(), *ARCH, "-shared", "-o", LIB,
+            *[os.path.join(objdir, u[1]) for u in units], "-lnccl"]
+    subprocess.run(link, check=True)
     if verbose:
-        sys.stdout.write(res.stderr)
+        sys.stdout.write("\n".join(log))
     return LIB
 
 

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -115,8 +116,13 @@ struct tg_ctx {
     int I = 0, J = 0, R = 0, R_local = 0, state0 = 0, W = 0;
     int64_t rounds_done = 0;
     uint64_t swap_base = 0;
-    int kpw = 0, ktab_row = 0, n_types = 0, m_cost = 0;
+    int kpw = 0, ktab_row = 0, n_types = 0, m_cost = 0, WV = 1;
+    std::vector<PlaneType> h_types;
+    std::vector<uint32_t> h_active;
+    std::vector<uint2> h_wkey;
     int plane_grid = 0, plane_block = kPlaneThreads;
+    int fused_grid = 0, fused_fast = 0, fused_block = kPlaneThreads;
+    size_t fused_smem = 0;
     size_t slot_smem = 0;
 
     DBuf<double> d_betas, d_pens, d_f, d_g;
@@ -126,7 +132,7 @@ struct tg_ctx {
     DBuf<int8_t> d_rec_states;
     // plane
     DBuf<uint32_t> d_spins32, d_kp, d_active;
-    DBuf<int32_t> d_nbr, d_cnt_c, d_cnt_q;
+    DBuf<int32_t> d_nbr, d_cnt_c, d_cnt_q, d_cnt2;
     DBuf<Chunk> d_chunks;
     DBuf<int> d_chunk_off, d_color_start;
     DBuf<PlaneType> d_types;
@@ -301,8 +307,15 @@ void build_plane(tg_ctx& c) {
         }
     }
     chunk_off[c.n_colors] = (int)chunks.size();
-    // words, keys, masks
-    c.W = (c.R_local + 31) / 32;
+    // words, keys, masks: rows padded to a whole number of WV-word passes
+    const int w_log = (c.R_local + 31) / 32;
+    c.WV = w_log > 2 ? 4 : w_log;
+    if (const char* e = std::getenv("TG_PLANE_WV")) {  // tuning override: 1, 2 or 4
+        const int v = std::atoi(e);
+        if (v == 1 || v == 2 || v == 4) c.WV = std::min(v, w_log > 2 ? 4 : (w_log > 1 ? 2 : 1));
+    }
+    c.W = (w_log + c.WV - 1) / c.WV * c.WV;
+    if (c.W > kMaxWordsArg) fail(TG_ERR_RESOURCE, "plane engine: %d replicas per rank exceed %d", c.R_local, 32 * kMaxWordsArg);
     std::vector<uint32_t> active(c.W, 0u);
     std::vector<uint2> wkey(c.W);
     for (int w = 0; w < c.W; ++w) {
@@ -336,8 +349,9 @@ void build_plane(tg_ctx& c) {
     c.d_chunk_off.upload(chunk_off, st);
     c.d_color_start.upload(c.color_start, st);
     c.d_types.upload(types, st);
-    c.d_active.upload(active, st);
-    c.d_wkey.upload(wkey, st);
+    c.h_types = types;
+    c.h_active = active;
+    c.h_wkey = wkey;
     c.d_ktab.upload(ktab, st);
     c.d_kp.alloc((size_t)c.W * kpw);
     c.d_kp.zero(st);
@@ -346,16 +360,38 @@ void build_plane(tg_ctx& c) {
     c.d_cnt_q.alloc((size_t)c.W * 32);
     c.d_cnt_c.zero(st);
     c.d_cnt_q.zero(st);
+    c.d_cnt2.alloc((size_t)4 * c.W * 32);
+    c.d_cnt2.zero(st);
     // cooperative grid: a multiple of W warps, all blocks co-resident
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)plane_sweep_fn(c.cfg.rule),
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)plane_sweep_fn(c.cfg.rule, c.WV),
                                                      kPlaneThreads, 0));
     if (per_sm < 1) fail(TG_ERR_RESOURCE, "plane engine: kernel does not fit on an SM");
     int blocks = per_sm * c.sms;
     const int wpb = kPlaneThreads / 32;
-    while (blocks > 1 && ((blocks * wpb) % c.W) != 0) --blocks;
-    if ((blocks * wpb) % c.W != 0) fail(TG_ERR_RESOURCE, "plane engine: cannot tile %d words", c.W);
+    const int passes = c.W / c.WV;
+    blocks -= blocks % passes;  // each block owns one pass of WV words
+    if (blocks < passes) fail(TG_ERR_RESOURCE, "plane engine: cannot tile %d words", c.W);
     c.plane_grid = blocks;
+    // fused round-loop kernel (single GPU)
+    c.fused_fast = 1;
+    for (const auto& t : types) if (t.ncb > 2 || t.nqb > 1) c.fused_fast = 0;
+    if (const char* e = std::getenv("TG_PLANE_FAST")) c.fused_fast = c.fused_fast && std::atoi(e) != 0;
+    c.fused_grid = 0;
+    if (c.world == 1 && c.R <= 2048) {
+        const void* fn = plane_rounds_fn(c.cfg.rule, c.WV, c.fused_fast);
+        c.fused_smem = (size_t)c.R * (2 * sizeof(double) + 2 * sizeof(int32_t));
+        if (c.fused_smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.fused_smem));
+        int fb = 0;
+        c.fused_block = c.fused_fast ? kPlaneThreadsFast : kPlaneThreads;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fb, fn, c.fused_block, c.fused_smem));
+        if (fb >= 1) {
+            int g = fb * c.sms;
+            g -= g % passes;
+            if (g >= passes) c.fused_grid = g;
+        }
+    }
 }
 
 void build_slot(tg_ctx& c) {
@@ -417,10 +453,12 @@ PlaneArgs plane_args(tg_ctx& c) {
     a.chunks = c.d_chunks.p;
     a.chunk_off = c.d_chunk_off.p;
     a.color_start = c.d_color_start.p;
-    a.types = c.d_types.p;
+    for (int q = 0; q < c.n_types && q < kMaxTypes; ++q) a.ty[q] = c.h_types[q];
+    for (int w = 0; w < c.W && w < kMaxWordsArg; ++w) {
+        a.wkey[w] = c.h_wkey[w];
+        a.active[w] = c.h_active[w];
+    }
     a.kp = c.d_kp.p;
-    a.active = c.d_active.p;
-    a.wkey = c.d_wkey.p;
     a.cnt_c = c.d_cnt_c.p;
     a.cnt_q = c.d_cnt_q.p;
     a.f_loc = c.d_f.p + c.state0;
@@ -490,7 +528,7 @@ void launch_sweep(tg_ctx& c, int64_t t0) {
         int64_t t = t0;
         int nsw = sps;
         void* args[] = {&a, &t, &nsw};
-        CK(cudaLaunchCooperativeKernel(plane_sweep_fn(c.cfg.rule), dim3(c.plane_grid),
+        CK(cudaLaunchCooperativeKernel(plane_sweep_fn(c.cfg.rule, c.WV), dim3(c.plane_grid),
                                        dim3(kPlaneThreads), args, 0, c.stream));
     } else {
         SlotArgs a = slot_args(c);
@@ -643,30 +681,100 @@ void drain(tg_ctx& c, int filled, int64_t first_round, const SinkCtx& sink) {
     if (rc) fail(TG_ERR_SINK, "record sink requested stop at round %lld", (long long)(first_round + filled - 1));
 }
 
+// Device time of the sweep launches and of everything between them for the
+// `filled` rounds of the current chunk (events recorded without host syncs).
+void profile_chunk(tg_ctx& c, int filled, double& sweep_ms, double& other_ms) {
+    CK(cudaEventRecord(c.ev[2 * filled], c.stream));
+    CK(cudaEventSynchronize(c.ev[2 * filled]));
+    for (int k = 0; k < filled; ++k) {
+        float a = 0, b = 0;
+        CK(cudaEventElapsedTime(&a, c.ev[2 * k], c.ev[2 * k + 1]));
+        CK(cudaEventElapsedTime(&b, c.ev[2 * k + 1], c.ev[2 * k + 2]));
+        sweep_ms += a;
+        other_ms += b;
+    }
+}
+
+// Single-GPU plane engine: whole rounds inside one persistent kernel per
+// record chunk (no host round trip, no separate swap launch).
+void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
+    cudaStream_t st = c.stream;
+    const int flags = c.cfg.record_flags;
+    if (c.profiling && c.ev.size() < 2) {
+        for (auto e : c.ev) cudaEventDestroy(e);
+        c.ev.assign(2, nullptr);
+        for (auto& e : c.ev) CK(cudaEventCreate(&e));
+    }
+    double sweep_ms = 0;
+    int64_t left = n_rounds;
+    while (left > 0) {
+        const int n = (int)std::min<int64_t>(left, c.rec_cap);
+        CK(cudaMemsetAsync(c.d_rec.p, 0, sizeof(TgRecordDev) * n, st));
+        PlaneArgs a = plane_args(c);
+        RoundArgs r{};
+        r.I = c.I; r.J = c.J; r.R = c.R; r.sps = (int)c.cfg.sweeps_per_swap;
+        r.round0 = c.rounds_done + 1;
+        r.n_rounds = n;
+        r.rec_flags = flags & (TG_REC_DIGEST | TG_REC_STATE | TG_REC_COUNTERS);
+        r.swap_base0 = c.swap_base;
+        r.swap_seed = derive_seed(c.cfg.seed, kPurposeSwap, 0);
+        r.betas = c.d_betas.p; r.pens = c.d_pens.p;
+        r.slot_state = c.d_slot_state.p; r.state_slot = c.d_state_slot.p;
+        r.acc_p = c.d_acc_p.p; r.acc_b = c.d_acc_b.p;
+        r.f_all = c.d_f.p; r.g_all = c.d_g.p;
+        r.cnt = c.d_cnt2.p; r.cnt_stride = c.W * 32;
+        r.ktab = c.d_ktab.p; r.ktab_row = c.ktab_row; r.kp = c.d_kp.p;
+        r.rec = c.d_rec.p; r.rec_acc = c.d_rec_acc.p;
+        r.rec_states = (flags & TG_REC_STATE) ? c.d_rec_states.p : nullptr;
+        r.perm = c.d_perm.p;
+        void* args[] = {&a, &r};
+        if (c.profiling) CK(cudaEventRecord(c.ev[0], st));
+        CK(cudaLaunchCooperativeKernel(plane_rounds_fn(c.cfg.rule, c.WV, c.fused_fast),
+                                       dim3(c.fused_grid), dim3(c.fused_block), args, c.fused_smem, st));
+        if (c.profiling) CK(cudaEventRecord(c.ev[1], st));
+        c.sweep_launches++;
+        const int64_t first = c.rounds_done + 1;
+        for (int k = 0; k < n; ++k) c.swap_base += (uint64_t)round_attempts(c.I, c.J, first + k);
+        c.rounds_done += n;
+        left -= n;
+        drain(c, n, first, sink);
+        if (c.profiling) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));
+            sweep_ms += ms;
+        }
+    }
+    CK(cudaStreamSynchronize(st));
+    c.last_sweep_ms = sweep_ms;
+    c.last_swap_ms = 0;
+}
+
 void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
     if (!c.initialised) fail(TG_ERR_CONFIG, "advance: context not initialised (tg_init)");
+    if (c.engine == TG_ENGINE_PLANE && c.world == 1 && c.fused_grid > 0 &&
+        !(c.cfg.record_flags & TG_REC_GRID)) {
+        do_advance_fused(c, n_rounds, sink);
+        return;
+    }
     cudaStream_t st = c.stream;
     const int flags = c.cfg.record_flags;
     const bool need_extract = (flags & (TG_REC_DIGEST | TG_REC_STATE | TG_REC_GRID)) != 0;
     const size_t per_state = (flags & TG_REC_GRID) ? (size_t)c.R * c.n : ((flags & TG_REC_STATE) ? (size_t)c.n : 0);
     SwapArgs sa = swap_args(c);
     const int sps = (int)c.cfg.sweeps_per_swap;
-    cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
-    if (c.profiling) {
-        if (c.ev.empty()) {
-            c.ev.resize(3);
-            for (auto& e : c.ev) CK(cudaEventCreate(&e));
-        }
-        e0 = c.ev[0]; e1 = c.ev[1]; e2 = c.ev[2];
+    if (c.profiling && (int)c.ev.size() < 2 * c.rec_cap + 1) {
+        for (auto e : c.ev) cudaEventDestroy(e);
+        c.ev.assign(2 * c.rec_cap + 1, nullptr);
+        for (auto& e : c.ev) CK(cudaEventCreate(&e));
     }
     double sweep_ms = 0, swap_ms = 0;
     int filled = 0;
     int64_t first_round = c.rounds_done + 1;
     for (int64_t k = 0; k < n_rounds; ++k) {
         const int64_t round = c.rounds_done + 1;
-        if (c.profiling) CK(cudaEventRecord(e0, st));
+        if (c.profiling) CK(cudaEventRecord(c.ev[2 * filled], st));
         launch_sweep(c, (round - 1) * sps);
-        if (c.profiling) CK(cudaEventRecord(e1, st));
+        if (c.profiling) CK(cudaEventRecord(c.ev[2 * filled + 1], st));
         if (c.world > 1) {
             NK(ncclGroupStart());
             NK(ncclAllGather(c.d_f.p + c.state0, c.d_f.p, c.R_local, ncclDouble, c.comm, st));
@@ -702,24 +810,17 @@ void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
                 if (e.states) NK(ncclAllReduce(e.states, e.states, per_state, ncclInt8, ncclSum, c.comm, st));
             }
         }
-        if (c.profiling) {
-            CK(cudaEventRecord(e2, st));
-            CK(cudaEventSynchronize(e2));
-            float a = 0, b = 0;
-            CK(cudaEventElapsedTime(&a, e0, e1));
-            CK(cudaEventElapsedTime(&b, e1, e2));
-            sweep_ms += a;
-            swap_ms += b;
-        }
         c.swap_base += (uint64_t)round_attempts(c.I, c.J, round);
         c.rounds_done = round;
         ++filled;
         if (filled == c.rec_cap) {
+            if (c.profiling) profile_chunk(c, filled, sweep_ms, swap_ms);
             drain(c, filled, first_round, sink);
             filled = 0;
             first_round = c.rounds_done + 1;
         }
     }
+    if (c.profiling && filled) profile_chunk(c, filled, sweep_ms, swap_ms);
     drain(c, filled, first_round, sink);
     CK(cudaStreamSynchronize(st));
     c.last_sweep_ms = sweep_ms;

@@ -24,7 +24,8 @@ constexpr int kKWords = kKPlanes + 1;     // + the "always" word
 constexpr int kMaxDC = 7;                 // plane engine: cost degree bound
 constexpr int kMaxDQ = 3;                 // plane engine: chain degree bound
 constexpr int kVPlanes = 8;               // vertical counter planes
-constexpr int kMaxTypes = 32;
+constexpr int kMaxTypes = 16;
+constexpr int kMaxWordsArg = 32;       // plane engine: <= 1024 replicas per rank
 
 // One (cost degree, chain degree) class of sites in the plane engine.
 struct PlaneType {
@@ -46,7 +47,7 @@ struct Chunk {
 
 struct PlaneArgs {
     int n;                // sites
-    int W;                // 32-replica words per site on this rank
+    int W;                // 32-replica words per site row (padded to the pass width)
     int n_colors;
     int local_states;     // replicas on this rank (<= 32*W)
     int rule;
@@ -58,10 +59,10 @@ struct PlaneArgs {
     const Chunk* chunks;  // all colours, concatenated
     const int* chunk_off; // [n_colors+1]
     const int* color_start; // [n_colors+1] internal site ranges
-    const PlaneType* types;
     const uint32_t* kp;   // [W][kpw] threshold planes for the current labels
-    const uint32_t* active; // [W] lane masks of real replicas
-    const uint2* wkey;    // [W] Philox key of each word group
+    PlaneType ty[kMaxTypes];     // by value: constant bank
+    uint2 wkey[kMaxWordsArg];    // Philox key of each word group (block-uniform -> uniform regs)
+    uint32_t active[kMaxWordsArg]; // lane masks of real replicas (0 for padding words)
     int32_t* cnt_c;       // [32W] unsatisfied cost bonds (accumulated)
     int32_t* cnt_q;       // [32W] unsatisfied chain bonds
     double* f_loc;        // [local_states]
@@ -88,6 +89,33 @@ struct SlotArgs {
     const uint64_t* slot_key;  // [R] derive_seed(seed, replica, slot)
     double* f_loc;
     double* g_loc;
+};
+
+// Fused single-GPU round loop (plane engine).
+struct RoundArgs {
+    int I, J, R, sps;
+    int64_t round0;        // first round (1-based) of this launch
+    int n_rounds;
+    int rec_flags;         // 1 digest, 2 target state, 8 counters
+    uint64_t swap_base0;   // swap-stream draws consumed before round0
+    uint64_t swap_seed;
+    const double* betas;
+    const double* pens;
+    int32_t* slot_state;   // [R] global labels (read at start, published per round)
+    int32_t* state_slot;
+    int64_t* acc_p;
+    int64_t* acc_b;
+    double* f_all;
+    double* g_all;
+    int32_t* cnt;          // [2 parities][2 (cost, chain)][cnt_stride]
+    int cnt_stride;
+    const uint64_t* ktab;
+    int ktab_row;
+    uint32_t* kp;
+    void* rec;             // TgRecordDev[n_rounds], digests pre-zeroed
+    int64_t* rec_acc;
+    int8_t* rec_states;    // [n_rounds][n] or null
+    const int32_t* perm;
 };
 
 struct SwapArgs {

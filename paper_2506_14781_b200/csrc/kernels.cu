@@ -1,6 +1,6 @@
 // kernels.cu -- sm_100a kernels of the 2D-PT hot path.
 //
-//   plane_sweep_kernel   multi-spin-coded chromatic sweeps (PLANE engine)
+//   (plane_sweep_kernel lives in plane_sweep.cu, one object per update rule)
 //   slot_sweep_kernel    int8 / FP64 chromatic sweeps, one CTA per replica (SLOT engine)
 //   swap_kernel          P / beta label swaps, round record, threshold-plane rebuild
 //   extract_kernel       target-state digest / snapshot for the trace
@@ -13,269 +13,19 @@
 
 #include "engine.cuh"
 #include "kernels.cuh"
+#include "plane_device.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace tg {
 
-// ------------------------------------------------------------ helpers
-
-__device__ __forceinline__ uint32_t sel(uint32_t m, uint32_t a1, uint32_t a0) {
-    return (m & a1) | (~m & a0);
-}
-
-// Select, per lane bit, leaves[class(lane)] where class bits are cb[0..B).
-template <int B>
-__device__ __forceinline__ uint32_t mux_tree(const uint32_t* cb, const uint32_t* leaves) {
-    constexpr int L = 1 << B;
-    uint32_t v[L < 4 ? 4 : L];
-    if constexpr (L >= 4) {
-#pragma unroll
-        for (int q = 0; q < L / 4; ++q) {
-            const uint4 t = __ldg(reinterpret_cast<const uint4*>(leaves) + q);
-            v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
-        }
-    } else {
-#pragma unroll
-        for (int q = 0; q < L; ++q) v[q] = __ldg(leaves + q);
-    }
-#pragma unroll
-    for (int lvl = 0; lvl < B; ++lvl) {
-#pragma unroll
-        for (int c = 0; c < (L >> (lvl + 1)); ++c) v[c] = sel(cb[lvl], v[2 * c + 1], v[2 * c]);
-    }
-    return v[0];
-}
-
-// Add a one-bit-per-lane mask to a bit-sliced counter of NB bits.
-template <int NB>
-__device__ __forceinline__ void bs_add(uint32_t* c, uint32_t v) {
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-        const uint32_t carry = c[b] & v;
-        c[b] ^= v;
-        v = carry;
-    }
-}
-
-// Add a 3-bit bit-sliced number (m0,m1,m2) into a kVPlanes vertical counter.
-__device__ __forceinline__ void vc_add3(uint32_t (&v)[kVPlanes], uint32_t m0, uint32_t m1,
-                                        uint32_t m2) {
-    uint32_t carry = v[0] & m0;
-    v[0] ^= m0;
-    {
-        const uint32_t t = v[1] ^ m1;
-        const uint32_t c = (v[1] & m1) | (t & carry);
-        v[1] = t ^ carry;
-        carry = c;
-    }
-    {
-        const uint32_t t = v[2] ^ m2;
-        const uint32_t c = (v[2] & m2) | (t & carry);
-        v[2] = t ^ carry;
-        carry = c;
-    }
-#pragma unroll
-    for (int p = 3; p < kVPlanes; ++p) {
-        const uint32_t t = v[p] & carry;
-        v[p] ^= carry;
-        carry = t;
-    }
-}
-
-// 32x32 bit-matrix transpose across a warp (row = lane).
-__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x) {
-    const int lane = threadIdx.x & 31;
-    uint32_t m = 0x0000FFFFu;
-#pragma unroll
-    for (int j = 16; j; j >>= 1, m ^= (m << j)) {
-        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
-        x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
-    }
-    return x;
-}
-
-// Per-lane totals of a warp's vertical counters -> atomics per replica.
-__device__ __forceinline__ void vc_flush(uint32_t (&v)[kVPlanes], int32_t* cnt, int w,
-                                         int local_states) {
-    uint32_t any = 0;
-#pragma unroll
-    for (int p = 0; p < kVPlanes; ++p) any |= v[p];
-    if (!__any_sync(0xffffffffu, any)) return;
-    int total = 0;
-#pragma unroll
-    for (int p = 0; p < kVPlanes; ++p) {
-        total += __popc(warp_transpose32(v[p])) << p;
-        v[p] = 0;
-    }
-    const int m = w * 32 + (threadIdx.x & 31);
-    if (total && m < local_states) atomicAdd(cnt + m, total);
-}
-
-// ---------------------------------------------------- plane engine sweep
-
-// One warp updates the 32 sites of chunk `ch` for the 32 replicas of word w.
-template <int NCB, int NQB, int RULE>
-__device__ __forceinline__ void plane_chunk(const PlaneArgs& a, const Chunk ch, int w, uint64_t t,
-                                            bool count, int lower, uint32_t (&vc)[kVPlanes],
-                                            uint32_t (&vq)[kVPlanes], uint32_t k0, uint32_t k1) {
-    constexpr int DCM = (1 << NCB) - 1;
-    constexpr int DQM = (1 << NQB) - 1;
-    constexpr int B = NCB + NQB;
-    const int lane = threadIdx.x & 31;
-    const PlaneType ty = a.types[ch.type];
-    const int dc = ty.dc, dq = ty.dq, deg = dc + dq;
-    const bool valid = lane < ch.len;
-    const int site = ch.start + lane;
-    const int W = a.W;
-
-    uint32_t s = 0;
-    uint32_t x[DCM > 0 ? DCM : 1];
-    uint32_t y[DQM > 0 ? DQM : 1];
-    uint32_t cb[B > 0 ? B : 1];
-#pragma unroll
-    for (int b = 0; b < (B > 0 ? B : 1); ++b) cb[b] = 0u;
-    uint32_t lowx = 0, lowy = 0;  // bit k: neighbour k has a lower colour
-    if (valid) {
-        s = a.spins[(size_t)site * W + w];
-        const int32_t* nb = a.nbr + ch.nbr_base + (size_t)lane * deg;
-#pragma unroll
-        for (int k = 0; k < DCM; ++k) {
-            x[k] = 0u;
-            if (k < dc) {
-                const int32_t e = __ldg(nb + k);
-                const int j = e & 0x7fffffff;
-                const uint32_t neg = e < 0 ? 0xffffffffu : 0u;
-                x[k] = a.spins[(size_t)j * W + w] ^ neg;  // bit: J_ij s_j = +1
-                lowx |= (uint32_t)(j < lower) << k;
-                const uint32_t v = RULE == 0 ? ~(s ^ x[k]) : x[k];
-                bs_add<NCB>(cb, v);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < DQM; ++k) {
-            y[k] = 0u;
-            if (k < dq) {
-                const int j = __ldg(nb + dc + k);
-                y[k] = a.spins[(size_t)j * W + w];
-                lowy |= (uint32_t)(j < lower) << k;
-                const uint32_t v = RULE == 0 ? ~(s ^ y[k]) : y[k];
-                bs_add<NQB>(cb + NCB, v);
-            }
-        }
-    }
-    const uint32_t* kpb = a.kp + (size_t)w * a.kpw + ty.kp_off;
-    const int ncl = ty.ncl;
-    const uint32_t act = valid ? __ldg(a.active + w) : 0u;
-    const uint32_t always = mux_tree<B>(cb, kpb + kKPlanes * ncl) & act;
-    uint32_t und = act & ~always;
-    uint32_t lt = 0;
-#pragma unroll 1
-    for (int blk = 0; blk < 14; ++blk) {
-        if (!__any_sync(0xffffffffu, und)) break;
-        const u32x4 r = philox4x32_10(
-            u32x4{(uint32_t)site, (uint32_t)t, (uint32_t)(t >> 32), (uint32_t)blk}, k0, k1);
-        const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int b = blk * 4 + q;
-            if (b < kKPlanes) {
-                const uint32_t tb = mux_tree<B>(cb, kpb + b * ncl);
-                lt |= und & tb & ~rr[q];
-                und &= ~(tb ^ rr[q]);
-            }
-        }
-    }
-    const uint32_t take = (always | lt) & act;
-    const uint32_t ns = RULE == 0 ? (s ^ take) : ((s & ~act) | take);
-    if (valid) a.spins[(size_t)site * W + w] = ns;
-
-    if (count) {
-        uint32_t m[3] = {0u, 0u, 0u};
-#pragma unroll
-        for (int k = 0; k < DCM; ++k)
-            if (valid && k < dc && ((lowx >> k) & 1u)) bs_add<3>(m, (ns ^ x[k]) & act);
-        vc_add3(vc, m[0], m[1], m[2]);
-        uint32_t q[3] = {0u, 0u, 0u};
-#pragma unroll
-        for (int k = 0; k < DQM; ++k)
-            if (valid && k < dq && ((lowy >> k) & 1u)) bs_add<3>(q, (ns ^ y[k]) & act);
-        vc_add3(vq, q[0], q[1], q[2]);
-    }
-}
-
-template <int RULE>
-__device__ __forceinline__ void plane_dispatch(const PlaneArgs& a, const Chunk ch, int ncb, int nqb,
-                                               int w, uint64_t t, bool count, int lower,
-                                               uint32_t (&vc)[kVPlanes], uint32_t (&vq)[kVPlanes],
-                                               uint32_t k0, uint32_t k1) {
-#define TG_CASE(C, Q) \
-    case (C) * 4 + (Q): plane_chunk<C, Q, RULE>(a, ch, w, t, count, lower, vc, vq, k0, k1); break;
-    switch (ncb * 4 + nqb) {
-        TG_CASE(0, 0) TG_CASE(0, 1) TG_CASE(0, 2)
-        TG_CASE(1, 0) TG_CASE(1, 1) TG_CASE(1, 2)
-        TG_CASE(2, 0) TG_CASE(2, 1) TG_CASE(2, 2)
-        TG_CASE(3, 0) TG_CASE(3, 1) TG_CASE(3, 2)
-        default: break;
-    }
-#undef TG_CASE
-}
-
-template <int RULE>
-__global__ void __launch_bounds__(kPlaneThreads, 1)
-plane_sweep_kernel(PlaneArgs a, int64_t t0, int n_sweeps) {
-    cg::grid_group grid = cg::this_grid();
-    const int wpb = blockDim.x >> 5;
-    const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
-    const int nw = gridDim.x * wpb;  // host guarantees nw % W == 0
-    const int w = gw % a.W;
-    const uint2 key = a.wkey[w];
-    for (int sw = 0; sw < n_sweeps; ++sw) {
-        const uint64_t t = (uint64_t)(t0 + sw);
-        const bool count = (sw == n_sweeps - 1);
-        for (int c = 0; c < a.n_colors; ++c) {
-            uint32_t vc[kVPlanes], vq[kVPlanes];
-#pragma unroll
-            for (int p = 0; p < kVPlanes; ++p) { vc[p] = 0u; vq[p] = 0u; }
-            const int c0 = a.chunk_off[c];
-            const int items = (a.chunk_off[c + 1] - c0) * a.W;
-            const int lower = a.color_start[c];
-            int done = 0;
-            for (int item = gw; item < items; item += nw) {
-                const Chunk ch = a.chunks[c0 + item / a.W];
-                const PlaneType& ty = a.types[ch.type];
-                plane_dispatch<RULE>(a, ch, ty.ncb, ty.nqb, w, t, count, lower, vc, vq, key.x,
-                                     key.y);
-                if (count && ++done == 32) {
-                    vc_flush(vc, a.cnt_c, w, a.local_states);
-                    vc_flush(vq, a.cnt_q, w, a.local_states);
-                    done = 0;
-                }
-            }
-            if (count) {
-                vc_flush(vc, a.cnt_c, w, a.local_states);
-                vc_flush(vq, a.cnt_q, w, a.local_states);
-            }
-            grid.sync();
-        }
-    }
-    // Per-replica f and g (reference units) from the unsatisfied-bond counts:
-    // f = -(m - 2 u_c) for J = +-1, h = 0; g = sum (s_a - s_b)^2 = 4 u_q.
-    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < a.local_states;
-         m += gridDim.x * blockDim.x) {
-        const int uc = a.cnt_c[m], uq = a.cnt_q[m];
-        a.f_loc[m] = -((double)a.m_cost - 2.0 * (double)uc);
-        a.g_loc[m] = 4.0 * (double)uq;
-        a.cnt_c[m] = 0;
-        a.cnt_q[m] = 0;
-    }
-}
-
-template __global__ void plane_sweep_kernel<0>(PlaneArgs, int64_t, int);
-template __global__ void plane_sweep_kernel<1>(PlaneArgs, int64_t, int);
-
-void* plane_sweep_fn(int rule) {
-    return rule == 0 ? (void*)plane_sweep_kernel<0> : (void*)plane_sweep_kernel<1>;
+void* plane_sweep_fn_r0(int wv);
+void* plane_sweep_fn_r1(int wv);
+void* plane_sweep_fn(int rule, int wv) { return rule == 0 ? plane_sweep_fn_r0(wv) : plane_sweep_fn_r1(wv); }
+void* plane_rounds_fn_r0(int wv, int fast);
+void* plane_rounds_fn_r1(int wv, int fast);
+void* plane_rounds_fn(int rule, int wv, int fast) {
+    return rule == 0 ? plane_rounds_fn_r0(wv, fast) : plane_rounds_fn_r1(wv, fast);
 }
 
 // ----------------------------------------------------- slot engine sweep

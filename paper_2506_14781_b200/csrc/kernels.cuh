@@ -9,6 +9,8 @@
 namespace tg {
 
 constexpr int kPlaneThreads = 512;
+constexpr int kPlaneThreadsFast = 256;  // fused FAST kernel: 3 x 256 threads per SM, <= 85 regs
+constexpr int kPlaneMinBlocksFast = 3;
 constexpr int kSlotThreads = 256;
 constexpr int kSwapThreads = 1024;
 
@@ -33,7 +35,9 @@ struct ExtractArgs {
     uint64_t* digest;     // record digest slot, or null
 };
 
-void* plane_sweep_fn(int rule);
+void* plane_sweep_fn(int rule, int wv);
+void* plane_rounds_fn(int rule, int wv, int fast);
+int plane_words_per_pass(int W);
 void* slot_sweep_fn();
 
 __global__ void swap_kernel(SwapArgs a, int64_t round, uint64_t swap_base, int rec_idx,

@@ -1,0 +1,131 @@
+// plane_device.cuh -- bit-sliced device helpers of the PLANE engine.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "engine.cuh"
+
+namespace tg {
+
+// ------------------------------------------------------------ helpers
+
+__device__ __forceinline__ uint32_t sel(uint32_t m, uint32_t a1, uint32_t a0) {
+    return (m & a1) | (~m & a0);
+}
+
+// Select, per lane bit, leaves[class(lane)] where class bits are cb[0..B).
+template <int B>
+__device__ __forceinline__ uint32_t mux_tree(const uint32_t* cb, const uint32_t* leaves) {
+    constexpr int L = 1 << B;
+    uint32_t v[L < 4 ? 4 : L];
+    if constexpr (L >= 4) {
+#pragma unroll
+        for (int q = 0; q < L / 4; ++q) {
+            const uint4 t = __ldg(reinterpret_cast<const uint4*>(leaves) + q);
+            v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < L; ++q) v[q] = __ldg(leaves + q);
+    }
+#pragma unroll
+    for (int lvl = 0; lvl < B; ++lvl) {
+#pragma unroll
+        for (int c = 0; c < (L >> (lvl + 1)); ++c) v[c] = sel(cb[lvl], v[2 * c + 1], v[2 * c]);
+    }
+    return v[0];
+}
+
+// Add a one-bit-per-lane mask to a bit-sliced counter of NB bits.
+template <int NB>
+__device__ __forceinline__ void bs_add(uint32_t* c, uint32_t v) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const uint32_t carry = c[b] & v;
+        c[b] ^= v;
+        v = carry;
+    }
+}
+
+// 32x32 bit-matrix transpose across a warp (row = lane).
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x) {
+    const int lane = threadIdx.x & 31;
+    uint32_t m = 0x0000FFFFu;
+#pragma unroll
+    for (int j = 16; j; j >>= 1, m ^= (m << j)) {
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+        x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
+    }
+    return x;
+}
+
+
+template <int WV>
+__device__ __forceinline__ void load_row(const uint32_t* p, uint32_t (&r)[WV]) {
+    if constexpr (WV % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < WV / 4; ++q) {
+            const uint4 v = reinterpret_cast<const uint4*>(p)[q];
+            r[4 * q] = v.x; r[4 * q + 1] = v.y; r[4 * q + 2] = v.z; r[4 * q + 3] = v.w;
+        }
+    } else if constexpr (WV == 2) {
+        const uint2 v = *reinterpret_cast<const uint2*>(p);
+        r[0] = v.x; r[1] = v.y;
+    } else {
+#pragma unroll
+        for (int q = 0; q < WV; ++q) r[q] = p[q];
+    }
+}
+
+template <int WV>
+__device__ __forceinline__ void store_row(uint32_t* p, const uint32_t (&r)[WV]) {
+    if constexpr (WV % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < WV / 4; ++q)
+            reinterpret_cast<uint4*>(p)[q] = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+    } else if constexpr (WV == 2) {
+        *reinterpret_cast<uint2*>(p) = make_uint2(r[0], r[1]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < WV; ++q) p[q] = r[q];
+    }
+}
+
+// Lazy MSB-first comparison of the 53-bit uniforms of 32 lanes against the
+// lanes' thresholds, 4 planes per Philox4x32-10 block.
+template <int B>
+__device__ __forceinline__ void compare_block(const uint32_t* cb, const uint32_t* kpb, int ncl,
+                                              int blk, const u32x4& r, uint32_t& und,
+                                              uint32_t& lt) {
+    const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int b = blk * 4 + q;
+        if (b < kKPlanes) {
+            const uint32_t tb = mux_tree<B>(cb, kpb + b * ncl);
+            lt |= und & tb & ~rr[q];
+            und &= ~(tb ^ rr[q]);
+        }
+    }
+}
+
+
+// compare_block with a one-level threshold select: lanes with c set use
+// leaves k1, the others k0 (planes of two classes of one type).
+__device__ __forceinline__ void compare_block_sel(uint32_t c, const uint32_t* k0, const uint32_t* k1,
+                                                  int ncl, int blk, const u32x4& r, uint32_t& und,
+                                                  uint32_t& lt) {
+    const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int b = blk * 4 + q;
+        if (b < kKPlanes) {
+            const uint32_t tb = sel(c, __ldg(k1 + b * ncl), __ldg(k0 + b * ncl));
+            lt |= und & tb & ~rr[q];
+            und &= ~(tb ^ rr[q]);
+        }
+    }
+}
+
+}  // namespace tg

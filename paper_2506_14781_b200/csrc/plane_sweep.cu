@@ -1,0 +1,418 @@
+// plane_sweep.cu -- PLANE engine sweep kernel (multi-spin coding), compiled
+// once per update rule (-DTG_PLANE_RULE=0 Metropolis, =1 heat bath).
+//
+// Restates metropolis_sweep (/root/reference/proj/src/mc.cpp:21-35) over the
+// canonical colour order for J = +-1, h = 0 instances: bit l of word w at a
+// site is the spin of physical replica 32w+l; a lane's flip probability is
+// replaced by its 53-bit threshold K (exact host-side exp, engine.cpp
+// semantics) compared MSB-first against bit planes of Philox draws.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "engine.cuh"
+#include "kernels.cuh"
+#include "plane_device.cuh"
+
+namespace cg = cooperative_groups;
+
+#ifndef TG_PLANE_RULE
+#define TG_PLANE_RULE 0
+#endif
+#define TG_CAT2(a, b) a##b
+#define TG_CAT(a, b) TG_CAT2(a, b)
+
+namespace tg {
+
+// One thread = one site of the chunk; all WV words (32 replicas each) of the
+// site row [wb, wb+WV) are loaded as one vector, updated, stored back.
+template <int NCB, int NQB, int RULE, int WV>
+__device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, const PlaneType& ty,
+                                           int wb, uint64_t t, bool count, int lower,
+                                           int (&acc_c)[WV], int (&acc_q)[WV]) {
+    constexpr int DCM = (1 << NCB) - 1;
+    constexpr int DQM = (1 << NQB) - 1;
+    constexpr int B = NCB + NQB;
+    const int lane = threadIdx.x & 31;
+    const int dc = ty.dc, dq = ty.dq, deg = dc + dq;
+    const bool valid = lane < ch.len;
+    const int site = ch.start + lane;
+    const int Wp = a.W;
+
+    uint32_t s[WV];
+    uint32_t x[DCM > 0 ? DCM : 1][WV];
+    uint32_t y[DQM > 0 ? DQM : 1][WV];
+    uint32_t lowx = 0, lowy = 0;
+#pragma unroll
+    for (int w = 0; w < WV; ++w) s[w] = 0u;
+    if (valid) {
+        load_row<WV>(a.spins + (size_t)site * Wp + wb, s);
+        const int32_t* nb = a.nbr + ch.nbr_base + (size_t)lane * deg;
+#pragma unroll
+        for (int k = 0; k < DCM; ++k) {
+            if (k < dc) {
+                const int32_t e = __ldg(nb + k);
+                const int j = e & 0x7fffffff;
+                const uint32_t neg = e < 0 ? 0xffffffffu : 0u;
+                load_row<WV>(a.spins + (size_t)j * Wp + wb, x[k]);
+#pragma unroll
+                for (int w = 0; w < WV; ++w) x[k][w] ^= neg;  // bit: J_ij s_j = +1
+                lowx |= (uint32_t)(j < lower) << k;
+            } else {
+#pragma unroll
+                for (int w = 0; w < WV; ++w) x[k][w] = 0u;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < DQM; ++k) {
+            if (k < dq) {
+                const int j = __ldg(nb + dc + k);
+                load_row<WV>(a.spins + (size_t)j * Wp + wb, y[k]);
+                lowy |= (uint32_t)(j < lower) << k;
+            } else {
+#pragma unroll
+                for (int w = 0; w < WV; ++w) y[k][w] = 0u;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < (DCM > 0 ? DCM : 1); ++k)
+#pragma unroll
+            for (int w = 0; w < WV; ++w) x[k][w] = 0u;
+#pragma unroll
+        for (int k = 0; k < (DQM > 0 ? DQM : 1); ++k)
+#pragma unroll
+            for (int w = 0; w < WV; ++w) y[k][w] = 0u;
+    }
+    const int ncl = ty.ncl;
+    uint32_t ns[WV];
+#pragma unroll
+    for (int w = 0; w < WV; ++w) {
+        uint32_t cb[B > 0 ? B : 1];
+#pragma unroll
+        for (int b = 0; b < (B > 0 ? B : 1); ++b) cb[b] = 0u;
+#pragma unroll
+        for (int k = 0; k < DCM; ++k)
+            if (k < dc) bs_add<NCB>(cb, RULE == 0 ? ~(s[w] ^ x[k][w]) : x[k][w]);
+#pragma unroll
+        for (int k = 0; k < DQM; ++k)
+            if (k < dq) bs_add<NQB>(cb + NCB, RULE == 0 ? ~(s[w] ^ y[k][w]) : y[k][w]);
+        const uint32_t* kpb = a.kp + (size_t)(wb + w) * a.kpw + ty.kp_off;
+        const uint32_t act = valid ? a.active[wb + w] : 0u;
+        const uint32_t always = mux_tree<B>(cb, kpb + kKPlanes * ncl) & act;
+        // Metropolis without chain partners: de = 2(2 n_c - dc) > 0 only for
+        // n_c > dc/2; for dc <= 3 those classes differ in bit 0 at most, so
+        // the threshold of an undecided lane is a 1-level select.
+        const bool pruned = (RULE == 0 && NQB == 0 && NCB == 2 && dc == 3);
+        uint32_t und = act & ~always;
+        uint32_t lt = 0;
+        const uint2 key = a.wkey[wb + w];
+        const uint32_t thi = (uint32_t)(t >> 32), tlo = (uint32_t)t;
+        // The first two blocks (8 planes) are almost always needed by some
+        // lane of the warp: issue them unconditionally as independent chains.
+        const u32x4 r0 = philox4x32_10(u32x4{(uint32_t)site, tlo, thi, 0u}, key.x, key.y);
+        const u32x4 r1 = philox4x32_10(u32x4{(uint32_t)site, tlo, thi, 1u}, key.x, key.y);
+        if (pruned) {
+            compare_block_sel(cb[0], kpb + 2, kpb + 3, ncl, 0, r0, und, lt);
+            compare_block_sel(cb[0], kpb + 2, kpb + 3, ncl, 1, r1, und, lt);
+        } else {
+            compare_block<B>(cb, kpb, ncl, 0, r0, und, lt);
+            compare_block<B>(cb, kpb, ncl, 1, r1, und, lt);
+        }
+#pragma unroll 1
+        for (int blk = 2; blk < 14; ++blk) {
+            if (!__any_sync(0xffffffffu, und)) break;
+            const u32x4 r = philox4x32_10(u32x4{(uint32_t)site, tlo, thi, (uint32_t)blk}, key.x, key.y);
+            if (pruned) compare_block_sel(cb[0], kpb + 2, kpb + 3, ncl, blk, r, und, lt);
+            else compare_block<B>(cb, kpb, ncl, blk, r, und, lt);
+        }
+        const uint32_t take = (always | lt) & act;
+        ns[w] = RULE == 0 ? (s[w] ^ take) : ((s[w] & ~act) | take);
+        if (count) {
+            // unsatisfied bonds to lower-colour neighbours, counted once per
+            // edge at its higher-colour endpoint, summed per replica lane.
+            if constexpr (NCB > 0) {
+                uint32_t m[NCB];
+#pragma unroll
+                for (int b = 0; b < NCB; ++b) m[b] = 0u;
+#pragma unroll
+                for (int k = 0; k < DCM; ++k)
+                    if (k < dc && ((lowx >> k) & 1u)) bs_add<NCB>(m, (ns[w] ^ x[k][w]) & act);
+                int tot = 0;
+#pragma unroll
+                for (int b = 0; b < NCB; ++b) tot += __popc(warp_transpose32(m[b])) << b;
+                acc_c[w] += tot;
+            }
+            if constexpr (NQB > 0) {
+                uint32_t m[NQB];
+#pragma unroll
+                for (int b = 0; b < NQB; ++b) m[b] = 0u;
+#pragma unroll
+                for (int k = 0; k < DQM; ++k)
+                    if (k < dq && ((lowy >> k) & 1u)) bs_add<NQB>(m, (ns[w] ^ y[k][w]) & act);
+                int tot = 0;
+#pragma unroll
+                for (int b = 0; b < NQB; ++b) tot += __popc(warp_transpose32(m[b])) << b;
+                acc_q[w] += tot;
+            }
+        }
+    }
+    if (valid) store_row<WV>(a.spins + (size_t)site * Wp + wb, ns);
+}
+
+// FAST = 1: only site types with cost degree <= 3 and chain degree <= 1
+// (the config-5 graphs); the host picks the kernel from the type table.
+template <int RULE, int WV, int FAST>
+__device__ __forceinline__ void plane_dispatch(const PlaneArgs& a, const Chunk& ch, int wb,
+                                               uint64_t t, bool count, int lower,
+                                               int (&acc_c)[WV], int (&acc_q)[WV]) {
+    const PlaneType& ty = a.ty[ch.type];
+#define TG_CASE(C, Q) \
+    case (C) * 4 + (Q): plane_site<C, Q, RULE, WV>(a, ch, ty, wb, t, count, lower, acc_c, acc_q); break;
+    if constexpr (FAST) {
+        switch (ty.ncb * 4 + ty.nqb) {
+            TG_CASE(1, 0) TG_CASE(1, 1) TG_CASE(2, 0) TG_CASE(2, 1)
+            default: break;
+        }
+    } else {
+        switch (ty.ncb * 4 + ty.nqb) {
+            TG_CASE(1, 0) TG_CASE(1, 1) TG_CASE(1, 2)
+            TG_CASE(2, 0) TG_CASE(2, 1) TG_CASE(2, 2)
+            TG_CASE(3, 0) TG_CASE(3, 1) TG_CASE(3, 2)
+            default: break;
+        }
+    }
+#undef TG_CASE
+}
+
+// One colour phase of one sweep over this warp's items; unsatisfied-bond
+// counts (last sweep of a round) go to cnt_c/cnt_q.
+template <int RULE, int WV, int FAST>
+__device__ __forceinline__ void plane_phase(const PlaneArgs& a, int c, uint64_t t, bool count,
+                                            int gidx, int ngroups, int wb,
+                                            int32_t* cnt_c, int32_t* cnt_q) {
+    int acc_c[WV], acc_q[WV];
+#pragma unroll
+    for (int w = 0; w < WV; ++w) { acc_c[w] = 0; acc_q[w] = 0; }
+    const int c0 = a.chunk_off[c];
+    const int n_chunks = a.chunk_off[c + 1] - c0;
+    const int lower = a.color_start[c];
+    for (int item = gidx; item < n_chunks; item += ngroups) {
+        const Chunk ch = a.chunks[c0 + item];
+        plane_dispatch<RULE, WV, FAST>(a, ch, wb, t, count, lower, acc_c, acc_q);
+    }
+    if (count) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int w = 0; w < WV; ++w) {
+            const int m = (wb + w) * 32 + lane;
+            if (m < a.local_states) {
+                if (acc_c[w]) atomicAdd(cnt_c + m, acc_c[w]);
+                if (acc_q[w]) atomicAdd(cnt_q + m, acc_q[w]);
+            }
+        }
+    }
+}
+
+// Sweep-only cooperative kernel (multi-GPU path): all sweeps of one round;
+// the (f, g) exchange and the swap run after it.  Work item = (chunk of <= 32
+// same-type sites of one colour, pass of WV words).
+template <int RULE, int WV>
+__global__ void __launch_bounds__(kPlaneThreads, 1)
+plane_sweep_kernel(const __grid_constant__ PlaneArgs a, int64_t t0, int n_sweeps) {
+    cg::grid_group grid = cg::this_grid();
+    const int wpb = blockDim.x >> 5;
+    // each block owns one pass of WV words (block-uniform Philox keys); the
+    // blocks of a pass split its chunks (host: gridDim % passes == 0)
+    const int passes = a.W / WV;
+    const int wb = (int)(blockIdx.x % passes) * WV;
+    const int gidx = (int)(blockIdx.x / passes) * wpb + (threadIdx.x >> 5);
+    const int ngroups = (int)(gridDim.x / passes) * wpb;
+    for (int sw = 0; sw < n_sweeps; ++sw) {
+        const uint64_t t = (uint64_t)(t0 + sw);
+        const bool count = (sw == n_sweeps - 1);
+        for (int c = 0; c < a.n_colors; ++c) {
+            plane_phase<RULE, WV, 0>(a, c, t, count, gidx, ngroups, wb, a.cnt_c, a.cnt_q);
+            grid.sync();
+        }
+    }
+    // Per-replica f and g (reference units) from the unsatisfied-bond counts:
+    // f = -(m - 2 u_c) for J = +-1, h = 0; g = sum (s_a - s_b)^2 = 4 u_q.
+    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < a.local_states;
+         m += gridDim.x * blockDim.x) {
+        const int uc = a.cnt_c[m], uq = a.cnt_q[m];
+        a.f_loc[m] = -((double)a.m_cost - 2.0 * (double)uc);
+        a.g_loc[m] = 4.0 * (double)uq;
+        a.cnt_c[m] = 0;
+        a.cnt_q[m] = 0;
+    }
+}
+
+// Persistent single-GPU kernel: n_rounds whole rounds of run_2dpt
+// (engine.cpp:121-216) without leaving the device.  Per round: sps sweeps
+// (one grid barrier per colour phase), then every block derives all
+// replicas' (f, g) from the bond counts, replays the identical swap phase on
+// its shared-memory copy of the labels, and rebuilds its share of the
+// threshold planes; block 0 publishes labels, counters and the record; one
+// more grid barrier closes the round.
+template <int RULE, int WV, int FAST>
+__global__ void __launch_bounds__(FAST ? kPlaneThreadsFast : kPlaneThreads, FAST ? kPlaneMinBlocksFast : 1)
+plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__ RoundArgs r) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sm_d[];
+    double* s_f = sm_d;
+    double* s_g = sm_d + r.R;
+    int32_t* s_slot = reinterpret_cast<int32_t*>(sm_d + 2 * r.R);
+    int32_t* s_state = s_slot + r.R;
+    const int tid = threadIdx.x;
+    const int wpb = blockDim.x >> 5;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int gw = blockIdx.x * wpb + warp;
+    const int nw = gridDim.x * wpb;
+    const int passes = a.W / WV;
+    const int wb = (int)(blockIdx.x % passes) * WV;
+    const int gidx = (int)(blockIdx.x / passes) * wpb + warp;
+    const int ngroups = (int)(gridDim.x / passes) * wpb;
+    const int np = r.I * (r.J > 1 ? r.J - 1 : 0);
+    const int nb = (r.I > 1 ? r.I - 1 : 0) * r.J;
+    for (int m = tid; m < r.R; m += blockDim.x) {
+        s_slot[m] = r.slot_state[m];
+        s_state[m] = r.state_slot[m];
+    }
+    uint64_t swap_base = r.swap_base0;
+    for (int k = 0; k < r.n_rounds; ++k) {
+        const int64_t round = r.round0 + k;
+        const int par = (int)(round & 1);
+        int32_t* cc = r.cnt + (size_t)par * 2 * r.cnt_stride;
+        int32_t* cq = cc + r.cnt_stride;
+        for (int sw = 0; sw < r.sps; ++sw) {
+            const uint64_t t = (uint64_t)((round - 1) * r.sps + sw);
+            const bool count = (sw == r.sps - 1);
+            for (int c = 0; c < a.n_colors; ++c) {
+                plane_phase<RULE, WV, FAST>(a, c, t, count, gidx, ngroups, wb, cc, cq);
+                grid.sync();
+            }
+        }
+        // (f, g) of every replica, reference units: f = -(m - 2 u_c), g = 4 u_q
+        for (int m = tid; m < r.R; m += blockDim.x) {
+            s_f[m] = -((double)a.m_cost - 2.0 * (double)cc[m]);
+            s_g[m] = 4.0 * (double)cq[m];
+        }
+        __syncthreads();
+        // swap phase (engine.cpp:148-187), replayed identically by every block
+        const int64_t n_att = round_attempts(r.I, r.J, round);
+        for (int q = tid; q < n_att; q += blockDim.x) {
+            int sa, sb, ctr, is_p;
+            if (swap_attempt(r.I, r.J, r.betas, r.pens, round, q, s_f, s_g, s_slot, r.swap_seed,
+                             swap_base, sa, sb, ctr, is_p)) {
+                const int xa = s_slot[sa], xb = s_slot[sb];
+                s_slot[sa] = xb;
+                s_slot[sb] = xa;
+                s_state[xb] = sa;
+                s_state[xa] = sb;
+                if (blockIdx.x == 0) {
+                    if (is_p) r.acc_p[ctr] += 1; else r.acc_b[ctr] += 1;
+                }
+            }
+        }
+        swap_base += (uint64_t)n_att;
+        __syncthreads();
+        if (blockIdx.x == 0) {
+            // counters of the other parity are free again: zero them
+            int32_t* other = r.cnt + (size_t)(par ^ 1) * 2 * r.cnt_stride;
+            for (int m = tid; m < 2 * r.cnt_stride; m += blockDim.x) other[m] = 0;
+            for (int m = tid; m < r.R; m += blockDim.x) {
+                r.slot_state[m] = s_slot[m];
+                r.state_slot[m] = s_state[m];
+                r.f_all[m] = s_f[m];
+                r.g_all[m] = s_g[m];
+            }
+            if (tid == 0) {  // record, engine.cpp:189-208
+                TgRecordDev* rec = reinterpret_cast<TgRecordDev*>(r.rec) + k;
+                const int tg = s_slot[r.R - 1];
+                rec->round = round;
+                rec->sweep_count = round * r.sps;
+                rec->f = s_f[tg];
+                rec->g = s_g[tg];
+                rec->feasible = s_g[tg] == 0.0 ? 1 : 0;
+                rec->target_state = tg;
+            }
+            if ((r.rec_flags & 8) && r.rec_acc) {
+                int64_t* dst = r.rec_acc + (size_t)k * (np + nb);
+                for (int q = tid; q < np; q += blockDim.x) dst[q] = r.acc_p[q];
+                for (int q = tid; q < nb; q += blockDim.x) dst[np + q] = r.acc_b[q];
+            }
+        }
+        // threshold planes for the new labels: warp job = (word, type, class)
+        {
+            int combos = 0;
+            for (int ty = 0; ty < a.n_types; ++ty) combos += a.ty[ty].ncl;
+            const int total = a.W * combos;
+            for (int job = gw; job < total; job += nw) {
+                const int w = job / combos;
+                int c = job % combos, ty = 0;
+                while (c >= a.ty[ty].ncl) { c -= a.ty[ty].ncl; ++ty; }
+                const PlaneType& pt = a.ty[ty];
+                const int m = w * 32 + lane;
+                uint64_t K = 0;
+                const bool live = m < a.local_states;
+                if (live) K = r.ktab[(size_t)s_state[m] * r.ktab_row + pt.ktab_off + c];
+                uint32_t* dst = r.kp + (size_t)w * a.kpw + pt.kp_off + c;
+                for (int b = 0; b < kKPlanes; ++b) {
+                    const uint32_t word = __ballot_sync(0xffffffffu, live && ((K >> (52 - b)) & 1ull));
+                    if (lane == (b & 31)) dst[b * pt.ncl] = word;
+                }
+                const uint32_t alw = __ballot_sync(0xffffffffu, live && K >= (1ull << 53));
+                if (lane == (kKPlanes & 31)) dst[kKPlanes * pt.ncl] = alw;
+            }
+        }
+        // target-state digest / snapshot for the trace (optional)
+        if (r.rec_flags & 3) {
+            const int tg = s_slot[r.R - 1];
+            uint64_t dsum = 0;
+            for (int i = blockIdx.x * blockDim.x + tid; i < a.n; i += gridDim.x * blockDim.x) {
+                const bool up = (a.spins[(size_t)i * a.W + (tg >> 5)] >> (tg & 31)) & 1u;
+                const int ci = r.perm[i];
+                if (r.rec_flags & 2) r.rec_states[(size_t)k * a.n + ci] = up ? 1 : -1;
+                if (up) dsum += digest_term((uint64_t)ci);
+            }
+            if (r.rec_flags & 1) {
+#pragma unroll
+                for (int o = 16; o; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+                if (lane == 0 && dsum)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(
+                                  &(reinterpret_cast<TgRecordDev*>(r.rec) + k)->digest),
+                              (unsigned long long)dsum);
+            }
+        }
+        grid.sync();
+    }
+}
+
+template __global__ void plane_sweep_kernel<TG_PLANE_RULE, 1>(const __grid_constant__ PlaneArgs, int64_t, int);
+template __global__ void plane_sweep_kernel<TG_PLANE_RULE, 2>(const __grid_constant__ PlaneArgs, int64_t, int);
+template __global__ void plane_sweep_kernel<TG_PLANE_RULE, 4>(const __grid_constant__ PlaneArgs, int64_t, int);
+template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 1, 0>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
+template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 2, 0>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
+template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 4, 0>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
+template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 4, 1>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
+template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 2, 1>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
+template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 1, 1>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
+
+
+
+void* TG_CAT(plane_rounds_fn_r, TG_PLANE_RULE)(int wv, int fast) {
+    if (wv >= 4) return fast ? (void*)plane_rounds_kernel<TG_PLANE_RULE, 4, 1>
+                             : (void*)plane_rounds_kernel<TG_PLANE_RULE, 4, 0>;
+    if (wv >= 2) return fast ? (void*)plane_rounds_kernel<TG_PLANE_RULE, 2, 1>
+                             : (void*)plane_rounds_kernel<TG_PLANE_RULE, 2, 0>;
+    return fast ? (void*)plane_rounds_kernel<TG_PLANE_RULE, 1, 1>
+                : (void*)plane_rounds_kernel<TG_PLANE_RULE, 1, 0>;
+}
+
+void* TG_CAT(plane_sweep_fn_r, TG_PLANE_RULE)(int wv) {
+    return wv >= 4 ? (void*)plane_sweep_kernel<TG_PLANE_RULE, 4>
+                   : (wv >= 2 ? (void*)plane_sweep_kernel<TG_PLANE_RULE, 2>
+                              : (void*)plane_sweep_kernel<TG_PLANE_RULE, 1>);
+}
+
+}  // namespace tg

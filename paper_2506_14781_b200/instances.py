@@ -146,8 +146,31 @@ def min_copies(n_logical_degree: int, max_degree: int) -> int:
 def canonical_order(pr: Problem) -> Tuple[np.ndarray, np.ndarray, int]:
     """Greedy index-order colouring of cost+chain edges, then a stable sort by
     (colour, chain degree, cost degree).  Returns (order, colour, n_colours).
-    The engine library computes the same order natively (tg_canonical_order);
-    tests check that the two agree."""
+    Uses the engine library's host helper (tg_canonical_order) when it is
+    built, else the pure-Python restatement below; tests check they agree."""
+    try:
+        return canonical_order_native(pr)
+    except Exception:  # noqa: BLE001 - library not built: host-only fallback
+        return canonical_order_py(pr)
+
+
+def canonical_order_native(pr: Problem) -> Tuple[np.ndarray, np.ndarray, int]:
+    import ctypes as C
+    from . import _lib
+    L = _lib.lib()
+    arrs = [np.ascontiguousarray(a, dtype=np.int32) for a in (pr.ci, pr.cj, pr.pa, pr.pb)]
+    order = np.zeros(pr.n, np.int32)
+    color = np.zeros(pr.n, np.int32)
+    nc = C.c_int32()
+    P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    rc = L.tg_canonical_order(pr.n, len(arrs[0]), P(arrs[0]), P(arrs[1]), len(arrs[2]), P(arrs[2]),
+                              P(arrs[3]), P(order), P(color), C.byref(nc))
+    if rc != 0:
+        raise ConfigError("canonical_order: invalid problem")
+    return order.astype(np.int64), color.astype(np.int64), int(nc.value)
+
+
+def canonical_order_py(pr: Problem) -> Tuple[np.ndarray, np.ndarray, int]:
     n = pr.n
     adj: List[List[int]] = [[] for _ in range(n)]
     dc = np.zeros(n, dtype=np.int64)
