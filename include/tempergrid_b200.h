@@ -159,6 +159,11 @@ double tg_p_swap_probability(double beta, double d_penalty, double dg);
 double tg_beta_swap_probability(double d_beta, double d_energy);
 double tg_general_swap_probability(double beta_a, double beta_b, double de_a, double de_b);
 
+/* Replica partition of a multi-GPU run (host-only): rank `rank` of `world`
+ * sweeps physical replicas [*state0, *state0 + *count) of the I*J grid
+ * (engine TG_ENGINE_PLANE needs count % 32 == 0 when world > 1). */
+int tg_partition(int n_replicas, int rank, int world, int engine, int32_t* state0, int32_t* count);
+
 /* Host replay of one swap phase over gathered per-replica (f, g) -- the
  * exact routine the device swap kernel runs, exported so the multi-rank
  * exchange logic can be tested without a GPU.  slot_state[R] (state id at

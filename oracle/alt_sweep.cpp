@@ -65,8 +65,8 @@ void metropolis_sweep(const EffectiveModel& view, double beta, SweepState& state
     // Every configuration sweeps first in the slot it was created in, so the
     // slot stream seen at its first sweep names the physical state.
     if (state.plane_id < 0) state.plane_id = slot_of_seed(rng.seed());
-    const std::uint64_t gseed =
-        tgo_derive_seed(tgref_ctx::master, TGO_PURPOSE_PLANE, (std::uint64_t)(state.plane_id >> 5));
+    const std::uint64_t pkey = tgo_derive_seed(tgref_ctx::master, TGO_PURPOSE_PLANE, 0);
+    const std::uint32_t grp = (std::uint32_t)(state.plane_id >> 5);
     const int lane = state.plane_id & 31;
     const std::uint64_t t = state.plane_t++;
 #endif
@@ -74,7 +74,7 @@ void metropolis_sweep(const EffectiveModel& view, double beta, SweepState& state
         const double local_i = state.local[i];
         const double de = 2.0 * static_cast<double>(state.spins[i]) * local_i;
 #if ALT_PLANE
-        const double u = tgo_u53_to_unit(tgo_plane_u53(gseed, t, (std::uint32_t)i, lane));
+        const double u = tgo_u53_to_unit(tgo_plane_u53(pkey, grp, t, (std::uint32_t)i, lane));
 #else
         const double u = rng.uniform01();
 #endif

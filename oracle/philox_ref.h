@@ -20,11 +20,13 @@
  *   uniform01 = (bits >> 11) * 2^-53        (rng.hpp:53-55)
  *   spin      = (bits >> 63) ? +1 : -1      (rng.hpp:79)
  *
- * Bit-plane draws (engine "msc"): the 53-bit uniform of physical state
+ * Bit-plane draws (engine "plane"): the 53-bit uniform of physical state
  * m = 32*grp + lane at sweep t, site i is
- *   U53 = sum_{b=0..52} bit_lane( philox(ctr={i, lo32(t), hi32(t), b>>2},
- *                                       key(derive_seed(seed, PLANE, grp)))[b&3] ) << (52-b)
+ *   U53 = sum_{b=0..52} bit_lane( philox(ctr={i, lo32(t), hi32(t), (b>>2) | grp<<4},
+ *                                       key(derive_seed(seed, PLANE, 0)))[b&3] ) << (52-b)
  *   u   = U53 * 2^-53.
+ * One key per run (the stream identity of a 32-replica group lives in the
+ * counter), so the device key schedule is a compile-time-addressed constant.
  */
 #ifndef TG_PHILOX_REF_H
 #define TG_PHILOX_REF_H
@@ -90,13 +92,14 @@ static inline uint64_t tgo_stream_bits(uint64_t seed, uint64_t n) {
 
 static inline double tgo_u53_to_unit(uint64_t u53) { return (double)u53 * 0x1.0p-53; }
 
-/* 53-bit plane-assembled uniform for physical state lane `lane` of group key
- * `gseed` at sweep t, site i (see header comment). */
-static inline uint64_t tgo_plane_u53(uint64_t gseed, uint64_t t, uint32_t site, int lane) {
-    const uint32_t key[2] = {(uint32_t)gseed, (uint32_t)(gseed >> 32)};
+/* 53-bit plane-assembled uniform of lane `lane` of 32-replica group `grp`
+ * under run key `pkey` = derive_seed(seed, PLANE, 0), at sweep t, site i
+ * (see header comment). */
+static inline uint64_t tgo_plane_u53(uint64_t pkey, uint32_t grp, uint64_t t, uint32_t site, int lane) {
+    const uint32_t key[2] = {(uint32_t)pkey, (uint32_t)(pkey >> 32)};
     uint64_t u = 0;
     for (int blk = 0; blk < 14; ++blk) {
-        const uint32_t ctr[4] = {site, (uint32_t)t, (uint32_t)(t >> 32), (uint32_t)blk};
+        const uint32_t ctr[4] = {site, (uint32_t)t, (uint32_t)(t >> 32), (uint32_t)blk | (grp << 4)};
         uint32_t o[4];
         tgo_philox4x32_10(ctr, key, o);
         for (int w = 0; w < 4; ++w) {

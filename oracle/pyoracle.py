@@ -70,7 +70,7 @@ def port_lib():
         _port.tgo_bits.restype = C.c_uint64
         _port.tgo_bits.argtypes = [C.c_uint64, C.c_uint64]
         _port.tgo_plane.restype = C.c_uint64
-        _port.tgo_plane.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_int]
+        _port.tgo_plane.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32, C.c_int]
         for fn in ("tgo_p_swap_probability", "tgo_beta_swap_probability",
                    "tgo_general_swap_probability"):
             getattr(_port, fn).restype = C.c_double
@@ -225,8 +225,8 @@ def stream_bits(seed, n) -> int:
     return int(port_lib().tgo_bits(seed, n))
 
 
-def plane_u53(gseed, t, site, lane) -> int:
-    return int(port_lib().tgo_plane(gseed, t, site, lane))
+def plane_u53(pkey, grp, t, site, lane) -> int:
+    return int(port_lib().tgo_plane(pkey, grp, t, site, lane))
 
 
 def p_swap_probability(beta, dp, dg):
@@ -239,3 +239,29 @@ def beta_swap_probability(db, de):
 
 def general_swap_probability(ba, bb, dea, deb):
     return port_lib().tgo_general_swap_probability(ba, bb, dea, deb)
+
+
+def ref_sparsify(n, couplings, fields, copies, max_degree, variant="mt"):
+    """The reference's own sparsify (constraints.cpp:50-120) via oracle/_ref."""
+    lib = ref_lib(variant)
+    c = np.asarray(couplings, dtype=np.float64).reshape(-1, 3)
+    ci = np.ascontiguousarray(c[:, 0], dtype=np.int32)
+    cj = np.ascontiguousarray(c[:, 1], dtype=np.int32)
+    cw = np.ascontiguousarray(c[:, 2])
+    h = np.ascontiguousarray(fields, dtype=np.float64)
+    cap_n = n * copies
+    cap_e = len(ci) + 1
+    oci, ocj = np.zeros(cap_e, np.int32), np.zeros(cap_e, np.int32)
+    ow = np.zeros(cap_e)
+    oh = np.zeros(cap_n)
+    opa, opb = np.zeros(cap_n, np.int32), np.zeros(cap_n, np.int32)
+    nc, npp = C.c_int(), C.c_int()
+    err = C.create_string_buffer(512)
+    lib.tgr_sparsify.restype = C.c_int
+    rc = lib.tgr_sparsify(n, len(ci), _ptr(ci), _ptr(cj), _ptr(cw), _ptr(h), copies, max_degree,
+                          _ptr(oci), _ptr(ocj), _ptr(ow), C.byref(nc), _ptr(oh), _ptr(opa),
+                          _ptr(opb), C.byref(npp), err, 512)
+    if rc < 0:
+        raise OracleError(-rc, err.value.decode())
+    return (rc, oci[:nc.value].copy(), ocj[:nc.value].copy(), ow[:nc.value].copy(), oh[:rc].copy(),
+            opa[:npp.value].copy(), opb[:npp.value].copy())

@@ -185,3 +185,40 @@ extern "C" int tgr_run_2dpt_timed(const tgo_problem* p, const tgo_run_cfg* cfg, 
         return 1;
     }
 }
+
+// tempergrid::sparsify (constraints.cpp:50-120) on a logical model; writes the
+// physical couplings (canonical order) and chain pairs.  Returns the number
+// of physical spins, or -code on error.  Capacities are the caller's.
+extern "C" int tgr_sparsify(int n, int n_couplings, const int* ci, const int* cj, const double* cw,
+                            const double* fields, int copies, int max_degree, int* out_ci,
+                            int* out_cj, double* out_w, int* out_nc, double* out_h, int* out_pa,
+                            int* out_pb, int* out_np, char* err, int errlen) {
+    using namespace tempergrid;
+    try {
+        std::vector<Coupling> cs;
+        for (int k = 0; k < n_couplings; ++k) cs.push_back({ci[k], cj[k], cw[k]});
+        IsingModel logical(n, std::move(cs), std::vector<double>(fields, fields + n));
+        const SparsifyResult r = sparsify(logical, copies, max_degree);
+        const auto& pc = r.problem.cost.couplings();
+        for (std::size_t k = 0; k < pc.size(); ++k) {
+            out_ci[k] = pc[k].i;
+            out_cj[k] = pc[k].j;
+            out_w[k] = pc[k].weight;
+        }
+        *out_nc = static_cast<int>(pc.size());
+        for (int i = 0; i < r.problem.cost.n_spins(); ++i) out_h[i] = r.problem.cost.fields()[i];
+        const auto& pp = r.problem.constraints.pairs();
+        for (std::size_t k = 0; k < pp.size(); ++k) {
+            out_pa[k] = pp[k].first;
+            out_pb[k] = pp[k].second;
+        }
+        *out_np = static_cast<int>(pp.size());
+        return r.problem.cost.n_spins();
+    } catch (const tempergrid::config_error& e) {
+        put_err(err, errlen, e.what());
+        return -2;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return -1;
+    }
+}

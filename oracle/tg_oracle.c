@@ -284,7 +284,7 @@ typedef struct {
     int mode;
     uint64_t slot_seed;  /* SLOT: derive_seed(seed, replica, slot) */
     uint64_t* slot_ctr;  /* SLOT: 64-bit outputs consumed so far */
-    const uint64_t* gseed; /* PLANE: per-group keys */
+    uint64_t pkey;       /* PLANE: run key derive_seed(seed, PLANE, 0) */
     uint64_t t;          /* PLANE: global sweep index */
 } draw_ctx_t;
 
@@ -293,7 +293,7 @@ static inline uint64_t next_u53(draw_ctx_t* d, const rstate_t* st, int site) {
         const uint64_t b = tgo_stream_bits(d->slot_seed, (*d->slot_ctr)++);
         return b >> 11; /* rng.hpp:53-55 */
     }
-    return tgo_plane_u53(d->gseed[st->id >> 5], d->t, (uint32_t)site, st->id & 31);
+    return tgo_plane_u53(d->pkey, (uint32_t)(st->id >> 5), d->t, (uint32_t)site, st->id & 31);
 }
 
 /* metropolis_sweep, mc.cpp:21-35 (rule 0); heat-bath variant (rule 1) with
@@ -357,8 +357,8 @@ uint64_t tgo_derive(uint64_t master, uint64_t purpose, uint64_t index) {
     return tgo_derive_seed(master, purpose, index);
 }
 uint64_t tgo_bits(uint64_t seed, uint64_t n) { return tgo_stream_bits(seed, n); }
-uint64_t tgo_plane(uint64_t gseed, uint64_t t, uint32_t site, int lane) {
-    return tgo_plane_u53(gseed, t, site, lane);
+uint64_t tgo_plane(uint64_t pkey, uint32_t grp, uint64_t t, uint32_t site, int lane) {
+    return tgo_plane_u53(pkey, grp, t, site, lane);
 }
 
 int tgo_energy_breakdown(const tgo_problem* p, double penalty, const int8_t* s, double* f,
@@ -466,9 +466,7 @@ int tgo_run_2dpt(const tgo_problem* prob, const tgo_run_cfg* cfg, tgo_outputs* o
     rstate_t* rep = (rstate_t*)calloc((size_t)R, sizeof(rstate_t));
     uint64_t* slot_seed = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)R);
     uint64_t* slot_ctr = (uint64_t*)calloc((size_t)R, sizeof(uint64_t));
-    const int n_groups = (R + 31) / 32;
-    uint64_t* gseed = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)n_groups);
-    for (int g = 0; g < n_groups; ++g) gseed[g] = tgo_derive_seed(cfg->seed, TGO_PURPOSE_PLANE, (uint64_t)g);
+    const uint64_t pkey = tgo_derive_seed(cfg->seed, TGO_PURPOSE_PLANE, 0);
     for (int r = 0; r < R; ++r) { /* engine.cpp:98-106 */
         rep[r].spins = (int8_t*)malloc((size_t)n);
         rep[r].local = (double*)malloc(sizeof(double) * (size_t)n);
@@ -502,7 +500,7 @@ int tgo_run_2dpt(const tgo_problem* prob, const tgo_run_cfg* cfg, tgo_outputs* o
                 d.mode = cfg->rng_mode;
                 d.slot_seed = slot_seed[r];
                 d.slot_ctr = &slot_ctr[r];
-                d.gseed = gseed;
+                d.pkey = pkey;
                 d.t = (uint64_t)((rn - 1) * sps + s);
                 sweep(v, beta, &rep[r], &d, cfg->rule);
             }
@@ -573,7 +571,7 @@ int tgo_run_2dpt(const tgo_problem* prob, const tgo_run_cfg* cfg, tgo_outputs* o
     }
 
     for (int r = 0; r < R; ++r) { free(rep[r].spins); free(rep[r].local); }
-    free(rep); free(slot_seed); free(slot_ctr); free(gseed);
+    free(rep); free(slot_seed); free(slot_ctr);
     free(att_p); free(acc_p); free(att_b); free(acc_b);
     for (int j = 0; j < J; ++j) model_free(&views[j].merged);
     free(views);

@@ -95,7 +95,7 @@ int tgo_canonical_order(const tgo_problem* prob, int32_t* color, int32_t* order,
 void tgo_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 uint64_t tgo_derive(uint64_t master, uint64_t purpose, uint64_t index);
 uint64_t tgo_bits(uint64_t seed, uint64_t n);
-uint64_t tgo_plane(uint64_t gseed, uint64_t t, uint32_t site, int lane);
+uint64_t tgo_plane(uint64_t pkey, uint32_t grp, uint64_t t, uint32_t site, int lane);
 
 #ifdef __cplusplus
 }

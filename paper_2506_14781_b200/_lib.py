@@ -80,6 +80,7 @@ def lib() -> C.CDLL:
                   ("tg_general_swap_probability", 4)):
         getattr(L, fn).restype = C.c_double
         getattr(L, fn).argtypes = [C.c_double] * n
+    L.tg_partition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]
     L.tg_swap_phase_host.argtypes = [C.c_int, vp, C.c_int, vp, C.c_int64, C.c_int, C.c_uint64,
                                      C.c_uint64, vp, vp, vp, vp, vp]
     _lib = L
@@ -91,5 +92,5 @@ EXPORTED = [
     "tg_last_error", "tg_set_problem", "tg_set_schedule", "tg_run", "tg_init", "tg_advance",
     "tg_get_state", "tg_get_counters", "tg_get_energies", "tg_get_info", "tg_stream",
     "tg_set_profiling", "tg_canonical_order", "tg_p_swap_probability", "tg_beta_swap_probability",
-    "tg_general_swap_probability", "tg_swap_phase_host",
+    "tg_general_swap_probability", "tg_swap_phase_host", "tg_partition",
 ]

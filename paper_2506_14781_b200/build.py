@@ -67,7 +67,7 @@ def build_engine(force: bool = False, verbose: bool = False) -> str:
         sys.stderr.write("\n".join(log))
         raise RuntimeError("nvcc failed building %s" % LIB)
     link = [nvcc(), *ARCH, "-shared", "-o", LIB,
-            *[os.path.join(objdir, u[1]) for u in units], "-lnccl"]
+            *[os.path.join(objdir, u[1]) for u in units], "-ldl"]
     subprocess.run(link, check=True)
     if verbose:
         sys.stdout.write("\n".join(log))

@@ -8,6 +8,7 @@
 // and an optional target-state extract; records drain to the caller's sink
 // in round order.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -31,6 +32,44 @@ namespace {
 
 thread_local std::string g_create_error;
 
+// NCCL is resolved at run time (dlopen) and only when a context spans more
+// than one GPU: linking it would pin whichever libnccl.so.2 loads first into
+// the process, and PyTorch needs its own bundled build.  Under torchrun,
+// PyTorch is imported first, so its copy is the one dlopen returns.
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    const char* (*GetErrorString)(ncclResult_t);
+};
+
+const NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a{};
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+        a.CommInitRank = (decltype(a.CommInitRank))dlsym(h, "ncclCommInitRank");
+        a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
+        a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
+        a.AllReduce = (decltype(a.AllReduce))dlsym(h, "ncclAllReduce");
+        a.GroupStart = (decltype(a.GroupStart))dlsym(h, "ncclGroupStart");
+        a.GroupEnd = (decltype(a.GroupEnd))dlsym(h, "ncclGroupEnd");
+        a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.AllReduce &&
+               a.GroupStart && a.GroupEnd && a.GetErrorString;
+        return a;
+    }();
+    return api;
+}
+
 struct TgFail {
     int code;
     std::string msg;
@@ -53,8 +92,9 @@ struct TgFail {
     } while (0)
 #define NK(x)                                                                                  \
     do {                                                                                       \
+        if (!nccl().ok) fail(TG_ERR_CUDA, "NCCL library (libnccl.so.2) not available");         \
         ncclResult_t r_ = (x);                                                                 \
-        if (r_ != ncclSuccess) fail(TG_ERR_CUDA, "%s: %s", #x, ncclGetErrorString(r_));        \
+        if (r_ != ncclSuccess) fail(TG_ERR_CUDA, "%s: %s", #x, nccl().GetErrorString(r_));      \
     } while (0)
 
 template <class T>
@@ -155,10 +195,13 @@ struct tg_ctx {
 
     ~tg_ctx() {
         for (auto e : ev) cudaEventDestroy(e);
-        if (comm) ncclCommDestroy(comm);
+        if (comm) nccl().CommDestroy(comm);
         if (stream) cudaStreamDestroy(stream);
     }
 };
+
+extern "C" int tg_partition(int n_replicas, int rank, int world, int engine, int32_t* state0,
+                            int32_t* count);
 
 namespace {
 
@@ -454,10 +497,9 @@ PlaneArgs plane_args(tg_ctx& c) {
     a.chunk_off = c.d_chunk_off.p;
     a.color_start = c.d_color_start.p;
     for (int q = 0; q < c.n_types && q < kMaxTypes; ++q) a.ty[q] = c.h_types[q];
-    for (int w = 0; w < c.W && w < kMaxWordsArg; ++w) {
-        a.wkey[w] = c.h_wkey[w];
-        a.active[w] = c.h_active[w];
-    }
+    for (int w = 0; w < c.W && w < kMaxWordsArg; ++w) a.active[w] = c.h_active[w];
+    philox_key_schedule(derive_seed(c.cfg.seed, kPurposePlane, 0), a.pks);
+    a.w_global0 = c.state0 / 32;
     a.kp = c.d_kp.p;
     a.cnt_c = c.d_cnt_c.p;
     a.cnt_q = c.d_cnt_q.p;
@@ -573,11 +615,14 @@ void do_init(tg_ctx& c, const tg_run_config* cfg) {
         fail(TG_ERR_CONFIG, "plane engine: instance not eligible (%s)", why.c_str());
     if (eng != TG_ENGINE_PLANE && eng != TG_ENGINE_SLOT) fail(TG_ERR_CONFIG, "unknown engine %d", eng);
     c.engine = eng;
-    if (c.R % c.world != 0) fail(TG_ERR_CONFIG, "grid of %d replicas does not split over %d ranks", c.R, c.world);
-    c.R_local = c.R / c.world;
-    c.state0 = c.rank * c.R_local;
-    if (eng == TG_ENGINE_PLANE && c.world > 1 && c.R_local % 32 != 0)
-        fail(TG_ERR_CONFIG, "plane engine: %d replicas per rank is not a multiple of 32", c.R_local);
+    {
+        int32_t s0 = 0, cnt = 0;
+        if (tg_partition(c.R, c.rank, c.world, eng, &s0, &cnt) != TG_OK)
+            fail(TG_ERR_CONFIG, "grid of %d replicas does not split over %d ranks%s", c.R, c.world,
+                 eng == TG_ENGINE_PLANE ? " in 32-replica words" : "");
+        c.state0 = s0;
+        c.R_local = cnt;
+    }
     cudaStream_t st = c.stream;
     CK(cudaSetDevice(c.device));
     c.d_betas.upload(c.betas, st);
@@ -776,10 +821,10 @@ void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         launch_sweep(c, (round - 1) * sps);
         if (c.profiling) CK(cudaEventRecord(c.ev[2 * filled + 1], st));
         if (c.world > 1) {
-            NK(ncclGroupStart());
-            NK(ncclAllGather(c.d_f.p + c.state0, c.d_f.p, c.R_local, ncclDouble, c.comm, st));
-            NK(ncclAllGather(c.d_g.p + c.state0, c.d_g.p, c.R_local, ncclDouble, c.comm, st));
-            NK(ncclGroupEnd());
+            NK(nccl().GroupStart());
+            NK(nccl().AllGather(c.d_f.p + c.state0, c.d_f.p, c.R_local, ncclDouble, c.comm, st));
+            NK(nccl().AllGather(c.d_g.p + c.state0, c.d_g.p, c.R_local, ncclDouble, c.comm, st));
+            NK(nccl().GroupEnd());
         }
         swap_kernel<<<1, kSwapThreads, 0, st>>>(sa, round, c.swap_base, filled, flags);
         CK(cudaGetLastError());
@@ -806,8 +851,8 @@ void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
             CK(cudaGetLastError());
             c.other_launches++;
             if (c.world > 1) {
-                if (dg) NK(ncclAllReduce(dg, dg, 1, ncclUint64, ncclSum, c.comm, st));
-                if (e.states) NK(ncclAllReduce(e.states, e.states, per_state, ncclInt8, ncclSum, c.comm, st));
+                if (dg) NK(nccl().AllReduce(dg, dg, 1, ncclUint64, ncclSum, c.comm, st));
+                if (e.states) NK(nccl().AllReduce(e.states, e.states, per_state, ncclInt8, ncclSum, c.comm, st));
             }
         }
         c.swap_base += (uint64_t)round_attempts(c.I, c.J, round);
@@ -858,7 +903,7 @@ static int create_impl(int device, int rank, int world, const void* nccl_id, tg_
         if (world > 1) {
             ncclUniqueId id;
             std::memcpy(&id, nccl_id, sizeof(id));
-            NK(ncclCommInitRank(&c->comm, world, id, rank));
+            NK(nccl().CommInitRank(&c->comm, world, id, rank));
         }
     });
     if (rc != TG_OK) {
@@ -881,7 +926,7 @@ int tg_create_distributed(int device, int rank, int world_size, const void* nccl
 
 int tg_nccl_unique_id(void* out128) {
     ncclUniqueId id;
-    if (ncclGetUniqueId(&id) != ncclSuccess) return TG_ERR_CUDA;
+    if (!nccl().ok || nccl().GetUniqueId(&id) != ncclSuccess) return TG_ERR_CUDA;
     std::memcpy(out128, &id, sizeof(id));
     return TG_OK;
 }
@@ -1015,7 +1060,7 @@ int tg_get_state(tg_ctx* ctx, int slot, int8_t* out) {
         e.digest = nullptr;
         extract_kernel<<<std::max(1, std::min((c.n + 255) / 256, c.sms * 8)), 256, 0, c.stream>>>(e);
         CK(cudaGetLastError());
-        if (c.world > 1) NK(ncclAllReduce(dst.p, dst.p, c.n, ncclInt8, ncclSum, c.comm, c.stream));
+        if (c.world > 1) NK(nccl().AllReduce(dst.p, dst.p, c.n, ncclInt8, ncclSum, c.comm, c.stream));
         CK(cudaMemcpyAsync(out, dst.p, c.n, cudaMemcpyDeviceToHost, c.stream));
         CK(cudaStreamSynchronize(c.stream));
     });
@@ -1118,6 +1163,16 @@ double tg_beta_swap_probability(double d_beta, double d_energy) {
 double tg_general_swap_probability(double beta_a, double beta_b, double de_a, double de_b) {
     const double x = beta_a * de_a + beta_b * de_b;
     return x >= 0.0 ? 1.0 : std::exp(x);
+}
+
+int tg_partition(int n_replicas, int rank, int world, int engine, int32_t* state0, int32_t* count) {
+    if (n_replicas < 1 || world < 1 || rank < 0 || rank >= world) return TG_ERR_CONFIG;
+    if (n_replicas % world != 0) return TG_ERR_CONFIG;
+    const int per = n_replicas / world;
+    if (engine == TG_ENGINE_PLANE && world > 1 && per % 32 != 0) return TG_ERR_CONFIG;
+    if (state0) *state0 = rank * per;
+    if (count) *count = per;
+    return TG_OK;
 }
 
 int tg_swap_phase_host(int n_betas, const double* betas, int n_penalties, const double* penalties,

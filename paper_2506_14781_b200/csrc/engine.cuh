@@ -61,7 +61,8 @@ struct PlaneArgs {
     const int* color_start; // [n_colors+1] internal site ranges
     const uint32_t* kp;   // [W][kpw] threshold planes for the current labels
     PlaneType ty[kMaxTypes];     // by value: constant bank
-    uint2 wkey[kMaxWordsArg];    // Philox key of each word group (block-uniform -> uniform regs)
+    uint32_t pks[20];            // plane-draw Philox key schedule (run key, 10 rounds)
+    int w_global0;               // global index of this rank's first 32-replica group
     uint32_t active[kMaxWordsArg]; // lane masks of real replicas (0 for padding words)
     int32_t* cnt_c;       // [32W] unsatisfied cost bonds (accumulated)
     int32_t* cnt_q;       // [32W] unsatisfied chain bonds

@@ -10,7 +10,7 @@ namespace tg {
 
 constexpr int kPlaneThreads = 512;
 constexpr int kPlaneThreadsFast = 256;  // fused FAST kernel: 3 x 256 threads per SM, <= 85 regs
-constexpr int kPlaneMinBlocksFast = 3;
+constexpr int kPlaneMinBlocksFast = 4;
 constexpr int kSlotThreads = 256;
 constexpr int kSwapThreads = 1024;
 

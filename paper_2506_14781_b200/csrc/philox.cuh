@@ -72,6 +72,32 @@ TG_HD u32x4 philox4x32_10(u32x4 c, uint32_t k0, uint32_t k1) {
     return c;
 }
 
+// Philox4x32-10 with a precomputed key schedule ks[2r], ks[2r+1] = key of
+// round r.  With ks in the kernel's constant bank (compile-time offsets) the
+// rounds need no key additions at all: the XOR takes the constant operand.
+TG_HD u32x4 philox4x32_10_ks(u32x4 c, const uint32_t* ks) {
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+    for (int r = 0; r < 10; ++r) {
+        uint32_t hi0, lo0, hi1, lo1;
+        mulhilo(kPhiloxM0, c.x, hi0, lo0);
+        mulhilo(kPhiloxM1, c.z, hi1, lo1);
+        c = u32x4{hi1 ^ c.y ^ ks[2 * r], lo1, hi0 ^ c.w ^ ks[2 * r + 1], lo0};
+    }
+    return c;
+}
+
+inline void philox_key_schedule(uint64_t key, uint32_t ks[20]) {
+    uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+    for (int r = 0; r < 10; ++r) {
+        ks[2 * r] = k0;
+        ks[2 * r + 1] = k1;
+        k0 += kPhiloxW0;
+        k1 += kPhiloxW1;
+    }
+}
+
 // n-th 64-bit output of stream(seed): counter n>>1, words (0,1) or (2,3).
 TG_HD uint64_t stream_bits(uint64_t seed, uint64_t n) {
     const uint64_t blk = n >> 1;

@@ -105,12 +105,12 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
         const bool pruned = (RULE == 0 && NQB == 0 && NCB == 2 && dc == 3);
         uint32_t und = act & ~always;
         uint32_t lt = 0;
-        const uint2 key = a.wkey[wb + w];
         const uint32_t thi = (uint32_t)(t >> 32), tlo = (uint32_t)t;
+        const uint32_t grp4 = (uint32_t)(a.w_global0 + wb + w) << 4;  // stream id in the counter
         // The first two blocks (8 planes) are almost always needed by some
         // lane of the warp: issue them unconditionally as independent chains.
-        const u32x4 r0 = philox4x32_10(u32x4{(uint32_t)site, tlo, thi, 0u}, key.x, key.y);
-        const u32x4 r1 = philox4x32_10(u32x4{(uint32_t)site, tlo, thi, 1u}, key.x, key.y);
+        const u32x4 r0 = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | 0u}, a.pks);
+        const u32x4 r1 = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | 1u}, a.pks);
         if (pruned) {
             compare_block_sel(cb[0], kpb + 2, kpb + 3, ncl, 0, r0, und, lt);
             compare_block_sel(cb[0], kpb + 2, kpb + 3, ncl, 1, r1, und, lt);
@@ -121,7 +121,7 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
 #pragma unroll 1
         for (int blk = 2; blk < 14; ++blk) {
             if (!__any_sync(0xffffffffu, und)) break;
-            const u32x4 r = philox4x32_10(u32x4{(uint32_t)site, tlo, thi, (uint32_t)blk}, key.x, key.y);
+            const u32x4 r = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | (uint32_t)blk}, a.pks);
             if (pruned) compare_block_sel(cb[0], kpb + 2, kpb + 3, ncl, blk, r, und, lt);
             else compare_block<B>(cb, kpb, ncl, blk, r, und, lt);
         }
