@@ -242,13 +242,18 @@ void canonical(int n, const std::vector<int>& ci, const std::vector<int>& cj,
         n_colors = std::max(n_colors, c + 1);
         for (int k = off[i]; k < off[i + 1]; ++k) if (adj[k] < i) used[color[adj[k]]] = 0;
     }
+    // stable counting sort by (colour, chain degree, cost degree)
+    int mq = 0, mc = 0;
+    for (int i = 0; i < n; ++i) { mq = std::max(mq, dq[i]); mc = std::max(mc, dc[i]); }
+    const size_t nk = (size_t)n_colors * (mq + 1) * (mc + 1);
+    std::vector<int> bucket(nk + 1, 0), keyv(n);
+    for (int i = 0; i < n; ++i) {
+        keyv[i] = (color[i] * (mq + 1) + dq[i]) * (mc + 1) + dc[i];
+        bucket[keyv[i] + 1]++;
+    }
+    for (size_t k = 0; k < nk; ++k) bucket[k + 1] += bucket[k];
     order.resize(n);
-    for (int i = 0; i < n; ++i) order[i] = i;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-        if (color[a] != color[b]) return color[a] < color[b];
-        if (dq[a] != dq[b]) return dq[a] < dq[b];
-        return dc[a] < dc[b];
-    });
+    for (int i = 0; i < n; ++i) order[bucket[keyv[i]]++] = i;
 }
 
 void check_vec(const std::vector<double>& v, const char* what) {  // engine.cpp:41-52
@@ -285,34 +290,45 @@ uint64_t threshold_heat_bath(double beta, double local) {
 void build_plane(tg_ctx& c) {
     cudaStream_t st = c.stream;
     const int n = c.n;
-    // internal adjacency
-    std::vector<std::vector<int32_t>> cost(n), chain(n);
-    for (size_t k = 0; k < c.ci.size(); ++k) {
-        const int a = c.inv[c.ci[k]], b = c.inv[c.cj[k]];
-        const int32_t sgn = c.cw[k] < 0 ? (int32_t)0x80000000u : 0;
-        cost[a].push_back(b | sgn);
-        cost[b].push_back(a | sgn);
+    // internal adjacency as flat CSR (cost entries carry the J<0 sign bit)
+    std::vector<int> dcv(n, 0), dqv(n, 0);
+    for (size_t k = 0; k < c.ci.size(); ++k) { dcv[c.inv[c.ci[k]]]++; dcv[c.inv[c.cj[k]]]++; }
+    for (size_t k = 0; k < c.pa.size(); ++k) { dqv[c.inv[c.pa[k]]]++; dqv[c.inv[c.pb[k]]]++; }
+    std::vector<int> base(n + 1, 0);
+    for (int i = 0; i < n; ++i) base[i + 1] = base[i] + dcv[i] + dqv[i];
+    std::vector<int32_t> nbr(base[n]);
+    {
+        std::vector<int> cc(n), cq(n);
+        for (int i = 0; i < n; ++i) { cc[i] = base[i]; cq[i] = base[i] + dcv[i]; }
+        for (size_t k = 0; k < c.ci.size(); ++k) {
+            const int x = c.inv[c.ci[k]], y = c.inv[c.cj[k]];
+            const int32_t sgn = c.cw[k] < 0 ? (int32_t)0x80000000u : 0;
+            nbr[cc[x]++] = y | sgn;
+            nbr[cc[y]++] = x | sgn;
+        }
+        for (size_t k = 0; k < c.pa.size(); ++k) {
+            const int x = c.inv[c.pa[k]], y = c.inv[c.pb[k]];
+            nbr[cq[x]++] = y;
+            nbr[cq[y]++] = x;
+        }
     }
-    for (size_t k = 0; k < c.pa.size(); ++k) {
-        const int a = c.inv[c.pa[k]], b = c.inv[c.pb[k]];
-        chain[a].push_back(b);
-        chain[b].push_back(a);
-    }
-    // types
-    std::map<std::pair<int, int>, int> type_of;
+    // site types (cost degree, chain degree)
+    std::vector<int> tid_of((kMaxDC + 1) * (kMaxDQ + 1), -1);
+    std::vector<int> site_type(n);
     std::vector<PlaneType> types;
     for (int i = 0; i < n; ++i) {
-        auto key = std::make_pair((int)cost[i].size(), (int)chain[i].size());
-        if (!type_of.count(key)) {
+        const int key = dcv[i] * (kMaxDQ + 1) + dqv[i];
+        if (tid_of[key] < 0) {
             PlaneType t{};
-            t.dc = key.first;
-            t.dq = key.second;
+            t.dc = dcv[i];
+            t.dq = dqv[i];
             t.ncb = nbits(t.dc);
             t.nqb = nbits(t.dq);
             t.ncl = std::max(4, 1 << (t.ncb + t.nqb));
-            type_of[key] = (int)types.size();
+            tid_of[key] = (int)types.size();
             types.push_back(t);
         }
+        site_type[i] = tid_of[key];
     }
     if ((int)types.size() > kMaxTypes) fail(TG_ERR_RESOURCE, "plane engine: too many site types");
     int kpw = 0, krow = 0;
@@ -325,26 +341,17 @@ void build_plane(tg_ctx& c) {
     c.kpw = kpw;
     c.ktab_row = krow;
     c.n_types = (int)types.size();
-    // nbr array + chunks (colour-major; canonical order keeps types contiguous)
-    std::vector<int32_t> nbr;
+    // chunks (colour-major; the canonical order keeps types contiguous)
     std::vector<Chunk> chunks;
     std::vector<int> chunk_off(c.n_colors + 1, 0);
-    std::vector<int> base(n + 1, 0);
-    for (int i = 0; i < n; ++i) {
-        base[i] = (int)nbr.size();
-        for (int32_t e : cost[i]) nbr.push_back(e);
-        for (int32_t e : chain[i]) nbr.push_back(e);
-    }
     for (int col = 0; col < c.n_colors; ++col) {
         chunk_off[col] = (int)chunks.size();
         int i = c.color_start[col];
         const int end = c.color_start[col + 1];
         while (i < end) {
-            const int ty = type_of[{(int)cost[i].size(), (int)chain[i].size()}];
+            const int ty = site_type[i];
             int j = i;
-            while (j < end && j - i < 32 &&
-                   type_of[{(int)cost[j].size(), (int)chain[j].size()}] == ty)
-                ++j;
+            while (j < end && j - i < 32 && site_type[j] == ty) ++j;
             chunks.push_back(Chunk{i, j - i, ty, base[i]});
             i = j;
         }
@@ -419,7 +426,12 @@ void build_plane(tg_ctx& c) {
     // fused round-loop kernel (single GPU)
     c.fused_fast = 1;
     for (const auto& t : types) if (t.ncb > 2 || t.nqb > 1) c.fused_fast = 0;
-    if (const char* e = std::getenv("TG_PLANE_FAST")) c.fused_fast = c.fused_fast && std::atoi(e) != 0;
+    // The 64-register FAST variant trades spills for occupancy and measured
+    // slower on B200 (see profiles/); opt in with TG_PLANE_FAST=1.
+    {
+        const char* e = std::getenv("TG_PLANE_FAST");
+        c.fused_fast = c.fused_fast && e && std::atoi(e) != 0;
+    }
     c.fused_grid = 0;
     if (c.world == 1 && c.R <= 2048) {
         const void* fn = plane_rounds_fn(c.cfg.rule, c.WV, c.fused_fast);
@@ -441,29 +453,39 @@ void build_slot(tg_ctx& c) {
     cudaStream_t st = c.stream;
     const int n = c.n;
     if (n > 200 * 1024) fail(TG_ERR_RESOURCE, "slot engine: %d spins exceed shared memory", n);
-    std::vector<std::map<int, std::pair<double, int>>> adj(n);
+    // merged adjacency (cost weight J, chain multiplicity) in increasing
+    // neighbour order, like the reference's merged CSR (constraints.cpp:122-140)
+    struct E { uint64_t key; double w; int cm; };
+    std::vector<E> ent;
+    ent.reserve(2 * (c.ci.size() + c.pa.size()));
     for (size_t k = 0; k < c.ci.size(); ++k) {
-        const int a = c.inv[c.ci[k]], b = c.inv[c.cj[k]];
-        adj[a][b].first += c.cw[k];
-        adj[b][a].first += c.cw[k];
+        const uint64_t x = (uint64_t)c.inv[c.ci[k]], y = (uint64_t)c.inv[c.cj[k]];
+        ent.push_back({x << 32 | y, c.cw[k], 0});
+        ent.push_back({y << 32 | x, c.cw[k], 0});
     }
     for (size_t k = 0; k < c.pa.size(); ++k) {
-        const int a = c.inv[c.pa[k]], b = c.inv[c.pb[k]];
-        adj[a][b].second += 1;
-        adj[b][a].second += 1;
+        const uint64_t x = (uint64_t)c.inv[c.pa[k]], y = (uint64_t)c.inv[c.pb[k]];
+        ent.push_back({x << 32 | y, 0.0, 1});
+        ent.push_back({y << 32 | x, 0.0, 1});
     }
+    std::stable_sort(ent.begin(), ent.end(), [](const E& p, const E& q) { return p.key < q.key; });
     std::vector<int> off(n + 1, 0);
     std::vector<int32_t> nbr;
     std::vector<double> w;
     std::vector<int8_t> cm;
-    for (int i = 0; i < n; ++i) {
-        for (auto& kv : adj[i]) {
-            nbr.push_back(kv.first);
-            w.push_back(kv.second.first);
-            cm.push_back((int8_t)kv.second.second);
-        }
-        off[i + 1] = (int)nbr.size();
+    for (size_t k = 0; k < ent.size();) {
+        size_t q = k;
+        double wsum = 0.0;
+        int csum = 0;
+        while (q < ent.size() && ent[q].key == ent[k].key) { wsum += ent[q].w; csum += ent[q].cm; ++q; }
+        const int i = (int)(ent[k].key >> 32);
+        nbr.push_back((int32_t)(ent[k].key & 0xffffffffu));
+        w.push_back(wsum);
+        cm.push_back((int8_t)csum);
+        off[i + 1]++;
+        k = q;
     }
+    for (int i = 0; i < n; ++i) off[i + 1] += off[i];
     std::vector<double> hi(n);
     for (int i = 0; i < n; ++i) hi[i] = c.h[c.order[i]];
     std::vector<uint64_t> keys(c.R);
@@ -951,7 +973,7 @@ int tg_set_problem(tg_ctx* ctx, int n, int n_couplings, const int32_t* ci, const
         // IsingModel validation (ising.cpp:21-46) and ConstraintSet (constraints.cpp:16-26)
         if (n <= 0) fail(TG_ERR_CONFIG, "model: n_spins must be positive");
         if (n_couplings < 0 || n_pairs < 0) fail(TG_ERR_CONFIG, "model: negative counts");
-        std::vector<std::pair<int, int>> keys;
+        std::vector<uint64_t> keys;
         std::vector<int> a(n_couplings), b(n_couplings), qa(n_pairs), qb(n_pairs);
         for (int k = 0; k < n_couplings; ++k) {
             int x = ci[k], y = cj[k];
@@ -961,12 +983,13 @@ int tg_set_problem(tg_ctx* ctx, int n, int n_couplings, const int32_t* ci, const
             if (!std::isfinite(w[k])) fail(TG_ERR_CONFIG, "model: coupling weights must be finite");
             a[k] = x;
             b[k] = y;
-            keys.emplace_back(x, y);
+            keys.push_back((uint64_t)x << 32 | (uint64_t)y);
         }
         std::sort(keys.begin(), keys.end());
         for (size_t k = 1; k < keys.size(); ++k)
             if (keys[k] == keys[k - 1])
-                fail(TG_ERR_CONFIG, "model: duplicate coupling (%d, %d)", keys[k].first, keys[k].second);
+                fail(TG_ERR_CONFIG, "model: duplicate coupling (%d, %d)", (int)(keys[k] >> 32),
+                     (int)(keys[k] & 0xffffffffu));
         for (int k = 0; k < n_pairs; ++k) {
             int x = pa[k], y = pb[k];
             if (x == y) fail(TG_ERR_CONFIG, "constraint: pair on a single spin %d", x);
