@@ -48,14 +48,18 @@ __device__ __forceinline__ void bs_add(uint32_t* c, uint32_t v) {
     }
 }
 
-// 32x32 bit-matrix transpose across a warp (row = lane).
+// 32x32 bit-matrix transpose across a warp (row = lane): five block-swap
+// stages; the partner's row is rotated into place and bit-selected.
 __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x) {
-    const int lane = threadIdx.x & 31;
+    const uint32_t lane = threadIdx.x & 31;
     uint32_t m = 0x0000FFFFu;
 #pragma unroll
     for (int j = 16; j; j >>= 1, m ^= (m << j)) {
         const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
-        x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
+        const bool hi = (lane & j) != 0;
+        const uint32_t rot = __funnelshift_l(y, y, hi ? 32 - j : j);  // y >> j / y << j, wrapped
+        const uint32_t keep = hi ? ~m : m;
+        x = (x & keep) | (rot & ~keep);
     }
     return x;
 }
@@ -111,17 +115,18 @@ __device__ __forceinline__ void compare_block(const uint32_t* cb, const uint32_t
 }
 
 
-// compare_block with a one-level threshold select: lanes with c set use
-// leaves k1, the others k0 (planes of two classes of one type).
-__device__ __forceinline__ void compare_block_sel(uint32_t c, const uint32_t* k0, const uint32_t* k1,
-                                                  int ncl, int blk, const u32x4& r, uint32_t& und,
-                                                  uint32_t& lt) {
+// compare_block with a one-level threshold select between two adjacent
+// classes (k01[0] for lanes with c clear, k01[1] with c set), one 8-byte load
+// per plane.
+__device__ __forceinline__ void compare_block_sel(uint32_t c, const uint32_t* k01, int ncl, int blk,
+                                                  const u32x4& r, uint32_t& und, uint32_t& lt) {
     const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int b = blk * 4 + q;
         if (b < kKPlanes) {
-            const uint32_t tb = sel(c, __ldg(k1 + b * ncl), __ldg(k0 + b * ncl));
+            const uint2 kk = __ldg(reinterpret_cast<const uint2*>(k01 + b * ncl));
+            const uint32_t tb = sel(c, kk.y, kk.x);
             lt |= und & tb & ~rr[q];
             und &= ~(tb ^ rr[q]);
         }

@@ -112,8 +112,8 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
         const u32x4 r0 = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | 0u}, a.pks);
         const u32x4 r1 = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | 1u}, a.pks);
         if (pruned) {
-            compare_block_sel(cb[0], kpb + 2, kpb + 3, ncl, 0, r0, und, lt);
-            compare_block_sel(cb[0], kpb + 2, kpb + 3, ncl, 1, r1, und, lt);
+            compare_block_sel(cb[0], kpb + 2, ncl, 0, r0, und, lt);
+            compare_block_sel(cb[0], kpb + 2, ncl, 1, r1, und, lt);
         } else {
             compare_block<B>(cb, kpb, ncl, 0, r0, und, lt);
             compare_block<B>(cb, kpb, ncl, 1, r1, und, lt);
@@ -122,7 +122,7 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
         for (int blk = 2; blk < 14; ++blk) {
             if (!__any_sync(0xffffffffu, und)) break;
             const u32x4 r = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | (uint32_t)blk}, a.pks);
-            if (pruned) compare_block_sel(cb[0], kpb + 2, kpb + 3, ncl, blk, r, und, lt);
+            if (pruned) compare_block_sel(cb[0], kpb + 2, ncl, blk, r, und, lt);
             else compare_block<B>(cb, kpb, ncl, blk, r, und, lt);
         }
         const uint32_t take = (always | lt) & act;
@@ -139,7 +139,8 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
                     if (k < dc && ((lowx >> k) & 1u)) bs_add<NCB>(m, (ns[w] ^ x[k][w]) & act);
                 int tot = 0;
 #pragma unroll
-                for (int b = 0; b < NCB; ++b) tot += __popc(warp_transpose32(m[b])) << b;
+                for (int b = 0; b < NCB; ++b)
+                    if (__any_sync(0xffffffffu, m[b])) tot += __popc(warp_transpose32(m[b])) << b;
                 acc_c[w] += tot;
             }
             if constexpr (NQB > 0) {
@@ -151,7 +152,8 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
                     if (k < dq && ((lowy >> k) & 1u)) bs_add<NQB>(m, (ns[w] ^ y[k][w]) & act);
                 int tot = 0;
 #pragma unroll
-                for (int b = 0; b < NQB; ++b) tot += __popc(warp_transpose32(m[b])) << b;
+                for (int b = 0; b < NQB; ++b)
+                    if (__any_sync(0xffffffffu, m[b])) tot += __popc(warp_transpose32(m[b])) << b;
                 acc_q[w] += tot;
             }
         }
@@ -196,6 +198,7 @@ __device__ __forceinline__ void plane_phase(const PlaneArgs& a, int c, uint64_t 
     const int c0 = a.chunk_off[c];
     const int n_chunks = a.chunk_off[c + 1] - c0;
     const int lower = a.color_start[c];
+    count = count && lower > 0;  // colour 0 has no lower-colour neighbours: nothing to count
     for (int item = gidx; item < n_chunks; item += ngroups) {
         const Chunk ch = a.chunks[c0 + item];
         plane_dispatch<RULE, WV, FAST>(a, ch, wb, t, count, lower, acc_c, acc_q);
