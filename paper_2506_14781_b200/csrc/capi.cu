@@ -435,11 +435,12 @@ void build_plane(tg_ctx& c) {
     c.fused_grid = 0;
     if (c.world == 1 && c.R <= 2048) {
         const void* fn = plane_rounds_fn(c.cfg.rule, c.WV, c.fused_fast);
-        c.fused_smem = (size_t)c.R * (2 * sizeof(double) + 2 * sizeof(int32_t));
+        c.fused_block = c.fused_fast ? kPlaneThreadsFast : kPlaneThreads;
+        c.fused_smem = (size_t)c.R * (2 * sizeof(double) + 2 * sizeof(int32_t)) + 8 +
+                       (size_t)(c.fused_block / 32) * kTailCap * 7 * sizeof(int32_t);
         if (c.fused_smem > 48 * 1024)
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.fused_smem));
         int fb = 0;
-        c.fused_block = c.fused_fast ? kPlaneThreadsFast : kPlaneThreads;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fb, fn, c.fused_block, c.fused_smem));
         if (fb >= 1) {
             int g = fb * c.sms;
@@ -521,6 +522,9 @@ PlaneArgs plane_args(tg_ctx& c) {
     for (int q = 0; q < c.n_types && q < kMaxTypes; ++q) a.ty[q] = c.h_types[q];
     for (int w = 0; w < c.W && w < kMaxWordsArg; ++w) a.active[w] = c.h_active[w];
     philox_key_schedule(derive_seed(c.cfg.seed, kPurposePlane, 0), a.pks);
+    a.state_slot = c.d_state_slot.p;
+    a.ktab = c.d_ktab.p;
+    a.ktab_row = c.ktab_row;
     a.w_global0 = c.state0 / 32;
     a.kp = c.d_kp.p;
     a.cnt_c = c.d_cnt_c.p;

@@ -61,6 +61,9 @@ struct PlaneArgs {
     const int* color_start; // [n_colors+1] internal site ranges
     const uint32_t* kp;   // [W][kpw] threshold planes for the current labels
     PlaneType ty[kMaxTypes];     // by value: constant bank
+    const int32_t* state_slot;   // [R] slot of each physical state (tail thresholds)
+    const uint64_t* ktab;        // [R][ktab_row] 53-bit thresholds
+    int ktab_row;
     uint32_t pks[20];            // plane-draw Philox key schedule (run key, 10 rounds)
     int w_global0;               // global index of this rank's first 32-replica group
     uint32_t active[kMaxWordsArg]; // lane masks of real replicas (0 for padding words)

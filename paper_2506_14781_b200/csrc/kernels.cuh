@@ -13,6 +13,7 @@ constexpr int kPlaneThreadsFast = 256;  // fused FAST kernel: 3 x 256 threads pe
 constexpr int kPlaneMinBlocksFast = 4;
 constexpr int kSlotThreads = 256;
 constexpr int kSwapThreads = 1024;
+constexpr int kTailCap = 160;   // per-warp deferred-tail queue entries (plane_sweep.cu)
 
 // Device image of tg_record (same layout as the C-ABI struct).
 struct TgRecordDev {

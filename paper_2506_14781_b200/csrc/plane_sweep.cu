@@ -23,12 +23,164 @@ namespace cg = cooperative_groups;
 
 namespace tg {
 
+// Deferred tail of the lazy threshold comparison.  After the two
+// unconditional Philox blocks (8 planes) a (site, word) still has undecided
+// lanes with probability ~2^-8 per lane; instead of running the whole warp
+// through further blocks for the few that need them, such words are queued
+// per warp (shared memory) and resolved 32 at a time, one per thread.
+// kTailCap (kernels.cuh) = 160 > 31 queued before a site + 4 words x 32 lanes.
+// Measured r1: the deferred tail saves ~1.1 Philox blocks per word but its
+// drains (re-loads, per-lane threshold look-ups, call spills) cost more on
+// B200 than they save (1.10e12 vs 1.29e12 flips/s); kept behind kPlaneTail.
+#ifndef TG_PLANE_TAIL
+#define TG_PLANE_TAIL 0
+#endif
+constexpr int kPlaneTail = TG_PLANE_TAIL;
+struct TailQ {
+    int* site;
+    int* word;       // local word index
+    int* type;
+    int* nbr_off;    // offset of the site's neighbour list in a.nbr
+    uint32_t* und;   // lanes still undecided after 8 planes
+    uint32_t* s;     // configuration word before the update
+    uint32_t* nsp;   // provisional new word (undecided lanes not taken)
+};
+
+__device__ __forceinline__ TailQ tail_view(char* base, int warp) {
+    char* p = base + (size_t)warp * kTailCap * 7 * sizeof(int);
+    TailQ q;
+    q.site = reinterpret_cast<int*>(p);
+    q.word = q.site + kTailCap;
+    q.type = q.word + kTailCap;
+    q.nbr_off = q.type + kTailCap;
+    q.und = reinterpret_cast<uint32_t*>(q.nbr_off + kTailCap);
+    q.s = q.und + kTailCap;
+    q.nsp = q.s + kTailCap;
+    return q;
+}
+
+// Resolve queued words (all of them when flush, else while >= 32 remain).
+// Decisions are identical to running the lazy loop in place: same planes,
+// same thresholds (ktab, host-computed), same order of planes per lane.
+template <int RULE>
+__device__ __noinline__ int tail_drain(const PlaneArgs& a, TailQ q, int qn, uint64_t t, bool count,
+                                       int lower, int32_t* cnt_c, int32_t* cnt_q, bool flush) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    while (qn >= 32 || (flush && qn > 0)) {
+        const int n = qn < 32 ? qn : 32;
+        const int e = qn - n + lane;
+        const bool mine = lane < n;
+        int site = 0, w = 0, nbo = 0;
+        uint32_t und = 0, s = 0, nsp = 0;
+        PlaneType ty = a.ty[0];
+        if (mine) {
+            site = q.site[e]; w = q.word[e]; nbo = q.nbr_off[e];
+            und = q.und[e]; s = q.s[e]; nsp = q.nsp[e];
+            ty = a.ty[q.type[e]];
+        }
+        // neighbour words (unchanged during this colour phase) and class bits
+        uint32_t x[kMaxDC], y[kMaxDQ];
+        uint32_t c3[3] = {0u, 0u, 0u}, q2[2] = {0u, 0u};
+        uint32_t lowx = 0, lowy = 0;
+#pragma unroll
+        for (int k = 0; k < kMaxDC; ++k) {
+            x[k] = 0u;
+            if (mine && k < ty.dc) {
+                const int32_t ev = __ldg(a.nbr + nbo + k);
+                const int j = ev & 0x7fffffff;
+                x[k] = a.spins[(size_t)j * a.W + w] ^ (ev < 0 ? 0xffffffffu : 0u);
+                lowx |= (uint32_t)(j < lower) << k;
+                bs_add<3>(c3, RULE == 0 ? ~(s ^ x[k]) : x[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kMaxDQ; ++k) {
+            y[k] = 0u;
+            if (mine && k < ty.dq) {
+                const int j = __ldg(a.nbr + nbo + ty.dc + k);
+                y[k] = a.spins[(size_t)j * a.W + w];
+                lowy |= (uint32_t)(j < lower) << k;
+                bs_add<2>(q2, RULE == 0 ? ~(s ^ y[k]) : y[k]);
+            }
+        }
+        const uint32_t grp4 = (uint32_t)(a.w_global0 + w) << 4;
+        const uint32_t thi = (uint32_t)(t >> 32), tlo = (uint32_t)t;
+        uint32_t rest = und, extra = 0;
+        // up to 4 undecided lanes per pass, each with its 53-bit threshold
+        while (__any_sync(0xffffffffu, rest)) {
+            uint64_t K[4] = {0ull, 0ull, 0ull, 0ull};
+            uint32_t bit[4] = {0u, 0u, 0u, 0u};
+            uint32_t pu = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (rest) {
+                    const int l = __ffs(rest) - 1;
+                    rest &= rest - 1;
+                    const uint32_t cls =
+                        (((c3[0] >> l) & 1u) | (((c3[1] >> l) & 1u) << 1) | (((c3[2] >> l) & 1u) << 2)) |
+                        ((((q2[0] >> l) & 1u) | (((q2[1] >> l) & 1u) << 1)) << ty.ncb);
+                    const int slot = a.state_slot[a.w_global0 * 32 + w * 32 + l];
+                    K[j] = __ldg(a.ktab + (size_t)slot * a.ktab_row + ty.ktab_off + cls);
+                    bit[j] = 1u << l;
+                    pu |= bit[j];
+                }
+            }
+            uint32_t lt = 0;
+#pragma unroll 1
+            for (int blk = 2; blk < 14; ++blk) {
+                if (!__any_sync(0xffffffffu, pu)) break;
+                const u32x4 r = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | (uint32_t)blk},
+                                                 a.pks);
+                const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                    const int b = blk * 4 + qq;
+                    if (b < kKPlanes) {
+                        uint32_t tb = 0;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if ((K[j] >> (52 - b)) & 1ull) tb |= bit[j];
+                        lt |= pu & tb & ~rr[qq];
+                        pu &= ~(tb ^ rr[qq]);
+                    }
+                }
+            }
+            extra |= lt;
+        }
+        if (mine && extra) {
+            uint32_t* word = a.spins + (size_t)site * a.W + w;
+            *word = RULE == 0 ? (*word ^ extra) : (*word | extra);
+            if (count) {
+                // bonds to lower-colour neighbours toggle satisfaction for taken lanes
+                uint32_t ex = extra;
+                while (ex) {
+                    const int l = __ffs(ex) - 1;
+                    ex &= ex - 1;
+                    int dcnt = 0, dqnt = 0;
+#pragma unroll
+                    for (int k = 0; k < kMaxDC; ++k)
+                        if (k < ty.dc && ((lowx >> k) & 1u)) dcnt += 1 - 2 * (int)(((nsp ^ x[k]) >> l) & 1u);
+#pragma unroll
+                    for (int k = 0; k < kMaxDQ; ++k)
+                        if (k < ty.dq && ((lowy >> k) & 1u)) dqnt += 1 - 2 * (int)(((nsp ^ y[k]) >> l) & 1u);
+                    if (dcnt) atomicAdd(cnt_c + w * 32 + l, dcnt);
+                    if (dqnt) atomicAdd(cnt_q + w * 32 + l, dqnt);
+                }
+            }
+        }
+        qn -= n;
+        __syncwarp();
+    }
+    return qn;
+}
+
 // One thread = one site of the chunk; all WV words (32 replicas each) of the
 // site row [wb, wb+WV) are loaded as one vector, updated, stored back.
-template <int NCB, int NQB, int RULE, int WV>
+template <int NCB, int NQB, int RULE, int WV, int TAIL>
 __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, const PlaneType& ty,
                                            int wb, uint64_t t, bool count, int lower,
-                                           int (&acc_c)[WV], int (&acc_q)[WV]) {
+                                           int (&acc_c)[WV], int (&acc_q)[WV], TailQ& tq, int& qn) {
     constexpr int DCM = (1 << NCB) - 1;
     constexpr int DQM = (1 << NQB) - 1;
     constexpr int B = NCB + NQB;
@@ -118,15 +270,34 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
             compare_block<B>(cb, kpb, ncl, 0, r0, und, lt);
             compare_block<B>(cb, kpb, ncl, 1, r1, und, lt);
         }
+        if constexpr (!TAIL) {
 #pragma unroll 1
-        for (int blk = 2; blk < 14; ++blk) {
-            if (!__any_sync(0xffffffffu, und)) break;
-            const u32x4 r = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | (uint32_t)blk}, a.pks);
-            if (pruned) compare_block_sel(cb[0], kpb + 2, ncl, blk, r, und, lt);
-            else compare_block<B>(cb, kpb, ncl, blk, r, und, lt);
+            for (int blk = 2; blk < 14; ++blk) {
+                if (!__any_sync(0xffffffffu, und)) break;
+                const u32x4 r = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | (uint32_t)blk}, a.pks);
+                if (pruned) compare_block_sel(cb[0], kpb + 2, ncl, blk, r, und, lt);
+                else compare_block<B>(cb, kpb, ncl, blk, r, und, lt);
+            }
         }
         const uint32_t take = (always | lt) & act;
         ns[w] = RULE == 0 ? (s[w] ^ take) : ((s[w] & ~act) | take);
+        if constexpr (TAIL) {
+            // queue words with undecided lanes; their provisional word does not take them
+            const uint32_t need = __ballot_sync(0xffffffffu, und != 0u);
+            if (need) {
+                if (und) {
+                    const int pos = qn + __popc(need & ((1u << lane) - 1u));
+                    tq.site[pos] = site;
+                    tq.word[pos] = wb + w;
+                    tq.type[pos] = ch.type;
+                    tq.nbr_off[pos] = ch.nbr_base + lane * deg;
+                    tq.und[pos] = und;
+                    tq.s[pos] = s[w];
+                    tq.nsp[pos] = ns[w];
+                }
+                qn += __popc(need);
+            }
+        }
         if (count) {
             // unsatisfied bonds to lower-colour neighbours, counted once per
             // edge at its higher-colour endpoint, summed per replica lane.
@@ -163,13 +334,13 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
 
 // FAST = 1: only site types with cost degree <= 3 and chain degree <= 1
 // (the config-5 graphs); the host picks the kernel from the type table.
-template <int RULE, int WV, int FAST>
+template <int RULE, int WV, int FAST, int TAIL>
 __device__ __forceinline__ void plane_dispatch(const PlaneArgs& a, const Chunk& ch, int wb,
                                                uint64_t t, bool count, int lower,
-                                               int (&acc_c)[WV], int (&acc_q)[WV]) {
+                                               int (&acc_c)[WV], int (&acc_q)[WV], TailQ& tq, int& qn) {
     const PlaneType& ty = a.ty[ch.type];
 #define TG_CASE(C, Q) \
-    case (C) * 4 + (Q): plane_site<C, Q, RULE, WV>(a, ch, ty, wb, t, count, lower, acc_c, acc_q); break;
+    case (C) * 4 + (Q): plane_site<C, Q, RULE, WV, TAIL>(a, ch, ty, wb, t, count, lower, acc_c, acc_q, tq, qn); break;
     if constexpr (FAST) {
         switch (ty.ncb * 4 + ty.nqb) {
             TG_CASE(1, 0) TG_CASE(1, 1) TG_CASE(2, 0) TG_CASE(2, 1)
@@ -188,10 +359,10 @@ __device__ __forceinline__ void plane_dispatch(const PlaneArgs& a, const Chunk& 
 
 // One colour phase of one sweep over this warp's items; unsatisfied-bond
 // counts (last sweep of a round) go to cnt_c/cnt_q.
-template <int RULE, int WV, int FAST>
+template <int RULE, int WV, int FAST, int TAIL>
 __device__ __forceinline__ void plane_phase(const PlaneArgs& a, int c, uint64_t t, bool count,
                                             int gidx, int ngroups, int wb,
-                                            int32_t* cnt_c, int32_t* cnt_q) {
+                                            int32_t* cnt_c, int32_t* cnt_q, TailQ& tq) {
     int acc_c[WV], acc_q[WV];
 #pragma unroll
     for (int w = 0; w < WV; ++w) { acc_c[w] = 0; acc_q[w] = 0; }
@@ -199,10 +370,13 @@ __device__ __forceinline__ void plane_phase(const PlaneArgs& a, int c, uint64_t 
     const int n_chunks = a.chunk_off[c + 1] - c0;
     const int lower = a.color_start[c];
     count = count && lower > 0;  // colour 0 has no lower-colour neighbours: nothing to count
+    int qn = 0;
     for (int item = gidx; item < n_chunks; item += ngroups) {
         const Chunk ch = a.chunks[c0 + item];
-        plane_dispatch<RULE, WV, FAST>(a, ch, wb, t, count, lower, acc_c, acc_q);
+        plane_dispatch<RULE, WV, FAST, TAIL>(a, ch, wb, t, count, lower, acc_c, acc_q, tq, qn);
+        if (TAIL && qn >= 32) qn = tail_drain<RULE>(a, tq, qn, t, count, lower, cnt_c, cnt_q, false);
     }
+    if (TAIL && qn > 0) tail_drain<RULE>(a, tq, qn, t, count, lower, cnt_c, cnt_q, true);
     if (count) {
         const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -234,7 +408,8 @@ plane_sweep_kernel(const __grid_constant__ PlaneArgs a, int64_t t0, int n_sweeps
         const uint64_t t = (uint64_t)(t0 + sw);
         const bool count = (sw == n_sweeps - 1);
         for (int c = 0; c < a.n_colors; ++c) {
-            plane_phase<RULE, WV, 0>(a, c, t, count, gidx, ngroups, wb, a.cnt_c, a.cnt_q);
+            TailQ tq{};
+            plane_phase<RULE, WV, 0, 0>(a, c, t, count, gidx, ngroups, wb, a.cnt_c, a.cnt_q, tq);
             grid.sync();
         }
     }
@@ -266,6 +441,7 @@ plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__
     double* s_g = sm_d + r.R;
     int32_t* s_slot = reinterpret_cast<int32_t*>(sm_d + 2 * r.R);
     int32_t* s_state = s_slot + r.R;
+    TailQ tq = tail_view(reinterpret_cast<char*>(s_state + r.R + (r.R & 1)), threadIdx.x >> 5);
     const int tid = threadIdx.x;
     const int wpb = blockDim.x >> 5;
     const int warp = tid >> 5, lane = tid & 31;
@@ -291,7 +467,7 @@ plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__
             const uint64_t t = (uint64_t)((round - 1) * r.sps + sw);
             const bool count = (sw == r.sps - 1);
             for (int c = 0; c < a.n_colors; ++c) {
-                plane_phase<RULE, WV, FAST>(a, c, t, count, gidx, ngroups, wb, cc, cq);
+                plane_phase<RULE, WV, FAST, kPlaneTail>(a, c, t, count, gidx, ngroups, wb, cc, cq, tq);
                 grid.sync();
             }
         }
