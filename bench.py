@@ -46,16 +46,35 @@ def parse():
     ap.add_argument("--sps", type=int, default=1, help="sweeps per swap")
     ap.add_argument("--rule", default="metropolis")
     ap.add_argument("--engine", default="plane")
+    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c4"],
+                    help="c5: config 5 (the metric's config, default); c2/c4: Wishart float32 "
+                         "configs on the slot engine")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sweeps", type=int, default=2, help="marginal sweeps of the CPU sample")
     return ap.parse_args()
 
 
-def workload(n):
+def workload(n, kind="c5"):
     from paper_2506_14781_b200 import instances as I
+    if kind == "c2":   # N=32 logical, alpha=0.5, degree <= 3 chains (928 spins), 16x8 grid
+        pr = I.wishart_planted(32, 0.5, seed=1)
+        betas, pens = I.wishart_schedule(pr, 16, 8)
+        return pr, betas, pens
+    if kind == "c4":   # N=256 logical, alpha=0.5 (64768 spins), 32x32 grid
+        pr = I.wishart_planted(256, 0.5, seed=1)
+        betas, pens = I.wishart_schedule(pr, 32, 32)
+        return pr, betas, pens
     pr = I.bipartite_3regular(n, seed=1)
     betas, pens = I.config_schedule("c5")
     return pr, betas, pens
+
+
+def workload_name(args, pr, R, rule):
+    if args.workload == "c5":
+        return f"C5 bipartite 3-regular N=2^{pr.n.bit_length() - 1} 16x16 sps={args.sps} {rule}"
+    nl = pr.meta.get("n_logical")
+    return (f"{args.workload.upper()} Wishart N={nl} logical -> {pr.n} physical (deg<=3), "
+            f"{R} replicas sps={args.sps} {rule}")
 
 
 def b_alg(pr):
@@ -179,7 +198,7 @@ def cpu_reference_rate(pr, betas, pens, sweeps, threads):
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
-    pr, betas, pens = workload(args.n)
+    pr, betas, pens = workload(args.n, args.workload)
     threads = os.cpu_count() or 1
     vals = []
     kind = "reference"
@@ -197,8 +216,8 @@ def run_reference_arm(args, rank, world):
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * statistics.median(dts), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C5 bipartite 3-regular N=2^{pr.n.bit_length() - 1} 16x16 sps=1 "
-                               "Metropolis (CPU reference, mt19937_64)",
+        "config": {"workload": workload_name(args, pr, 256, "Metropolis") +
+                               " (CPU reference, mt19937_64)",
                    "n_spins": pr.n, "replicas": 256, "sweeps_per_step": args.cpu_sweeps},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": sample},
@@ -215,7 +234,7 @@ def run_ours(args, rank, world, local):
     from paper_2506_14781_b200.api import Engine, RunConfig
 
     torch.cuda.set_device(local)
-    pr, betas, pens = workload(args.n)
+    pr, betas, pens = workload(args.n, args.workload)
     R = len(betas) * len(pens)
     nccl_id = None
     if world > 1:
@@ -320,8 +339,7 @@ def run_ours(args, rank, world, local):
             "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic",
-            "config": {"workload": f"C5 bipartite 3-regular N=2^{pr.n.bit_length() - 1} 16x16 "
-                                   f"sps={args.sps} {args.rule}",
+            "config": {"workload": workload_name(args, pr, R, args.rule),
                        "n_spins": pr.n, "replicas": R, "rounds_per_step": args.rounds,
                        "engine": args.engine, "parallelism": f"replica-split x{world}",
                        "l2": "flushed between timed steps (256 MB write)"},
@@ -342,6 +360,8 @@ def run_ours(args, rank, world, local):
 
 def main():
     args = parse()
+    if args.workload != "c5":
+        args.engine = "slot"  # float32 Wishart couplings: the FP64 slot engine
     rank, world, local = dist_setup(args.gpus)
     if args.impl == "reference":
         run_reference_arm(args, rank, world)

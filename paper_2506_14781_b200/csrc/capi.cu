@@ -183,6 +183,9 @@ struct tg_ctx {
     DBuf<int> d_off;
     DBuf<int32_t> d_snbr;
     DBuf<double> d_sw, d_h;
+    DBuf<int2> d_ent;
+    DBuf<float> d_h32;
+    float slot_eps = 0.0f, slot_beta_max = 0.0f;
     DBuf<uint64_t> d_slot_key;
 
     int rec_cap = 0;
@@ -489,6 +492,29 @@ void build_slot(tg_ctx& c) {
     for (int i = 0; i < n; ++i) off[i + 1] += off[i];
     std::vector<double> hi(n);
     for (int i = 0; i < n; ++i) hi[i] = c.h[c.order[i]];
+    // FP32 fast-path tables and the bound on |local_fp32 - local_fp64|
+    if (n >= (1 << 28)) fail(TG_ERR_RESOURCE, "slot engine: too many spins for the packed CSR");
+    std::vector<int2> ent2(nbr.size());
+    std::vector<float> h32(n);
+    double pmax = 0.0, bmax = 0.0, eps = 0.0;
+    for (double p : c.pens) pmax = std::max(pmax, p);
+    for (double b : c.betas) bmax = std::max(bmax, std::fabs(b));
+    for (int i = 0; i < n; ++i) {
+        h32[i] = (float)hi[i];
+        double S = std::fabs(hi[i]);
+        for (int e = off[i]; e < off[i + 1]; ++e) {
+            const float wf = (float)w[e];
+            int bits;
+            std::memcpy(&bits, &wf, 4);
+            ent2[e] = make_int2(nbr[e] | ((int)cm[e] << 28), bits);
+            S += std::fabs(w[e]) + (double)cm[e] * 2.0 * pmax;
+        }
+        eps = std::max(eps, (double)(off[i + 1] - off[i] + 3) * S * 0x1.0p-22);
+    }
+    c.slot_eps = (float)(eps * 1.0001 + 1e-30);
+    c.slot_beta_max = (float)(bmax * 1.0001);
+    c.d_ent.upload(ent2, st);
+    c.d_h32.upload(h32, st);
     std::vector<uint64_t> keys(c.R);
     for (int r = 0; r < c.R; ++r) keys[r] = derive_seed(c.cfg.seed, kPurposeReplica, (uint64_t)r);
     c.d_off.upload(off, st);
@@ -549,6 +575,10 @@ SlotArgs slot_args(tg_ctx& c) {
     a.w = c.d_sw.p;
     a.cm = c.d_cm.p;
     a.h = c.d_h.p;
+    a.ent = c.d_ent.p;
+    a.h32 = c.d_h32.p;
+    a.eps_local = c.slot_eps;
+    a.beta_max = c.slot_beta_max;
     a.color_start = c.d_color_start.p;
     a.betas = c.d_betas.p;
     a.pens = c.d_pens.p;

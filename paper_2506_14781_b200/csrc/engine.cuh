@@ -86,6 +86,10 @@ struct SlotArgs {
     const double* w;      // cost weight J (0 for pure chain entries)
     const int8_t* cm;     // chain multiplicity of the entry
     const double* h;      // fields
+    const int2* ent;      // FP32 fast path: {j | cm<<28, float bits of J}
+    const float* h32;
+    float eps_local;      // bound on |local_fp32 - local_fp64| over all sites
+    float beta_max;
     const int* color_start;
     const double* betas;
     const double* pens;

@@ -49,6 +49,46 @@ __device__ __forceinline__ void slot_update(const SlotArgs& a, int8_t* s, int i,
     }
 }
 
+// FP32 fast path with a certified fallback: the FP32 local field, exponent and
+// uniform carry explicit error bounds (eps_local from the host, ulp terms for
+// the products, __expf and the u53 -> float rounding).  When the FP32 decision
+// is certain it equals the FP64 decision of slot_update; otherwise (a band of
+// relative width ~1e-5 around the threshold) the FP64 path decides.  Results
+// are therefore identical to the all-FP64 kernel.
+__device__ __forceinline__ void slot_update_fast(const SlotArgs& a, int8_t* s, int i, uint64_t u53,
+                                                 double beta, double two_p, float beta32,
+                                                 float two_p32) {
+    const int e0 = __ldg(a.off + i), e1 = __ldg(a.off + i + 1);
+    float l32 = __ldg(a.h32 + i);
+    for (int e = e0; e < e1; ++e) {
+        const int2 v = __ldg(a.ent + e);
+        const float wgt = __int_as_float(v.y) + (float)(v.x >> 28) * two_p32;
+        l32 = fmaf(wgt, (float)s[v.x & 0x0fffffff], l32);
+    }
+    const float si = (float)s[i];
+    const float uf = (float)u53 * 0x1.0p-53f;            // rel. error <= 2^-24
+    const float eb = 2.0f * a.beta_max * a.eps_local;      // bound on the exponent error from the field
+    if (a.rule == 0) {
+        const float de32 = 2.0f * si * l32;
+        const float tol = 2.0f * a.eps_local;
+        if (de32 < -tol) { s[i] = (int8_t)-s[i]; return; }  // de64 <= 0 for sure
+        if (de32 > tol) {
+            const float x = -beta32 * de32;
+            const float T = __expf(x);
+            const float band = T * (2.0f * eb + fabsf(x) * 0x1.0p-19f + 0x1.0p-18f) + uf * 0x1.0p-22f;
+            if (uf < T - band) { s[i] = (int8_t)-s[i]; return; }
+            if (uf > T + band) return;
+        }
+    } else {
+        const float y = 2.0f * beta32 * l32;
+        const float p = __frcp_rn(1.0f + __expf(-y));
+        const float band = eb + fabsf(y) * 0x1.0p-19f + 0x1.0p-18f + uf * 0x1.0p-22f;
+        if (uf < p - band) { s[i] = 1; return; }
+        if (uf > p + band) { s[i] = -1; return; }
+    }
+    slot_update(a, s, i, u53, beta, two_p);  // near the threshold: decide in FP64
+}
+
 __global__ void __launch_bounds__(kSlotThreads)
 slot_sweep_kernel(SlotArgs a, int64_t t0, int n_sweeps) {
     extern __shared__ int8_t sm[];
@@ -60,6 +100,7 @@ slot_sweep_kernel(SlotArgs a, int64_t t0, int n_sweeps) {
     const int slot = a.state_slot[a.state0 + m];
     const double beta = a.betas[slot / a.J];
     const double two_p = 2.0 * a.pens[slot % a.J];
+    const float beta32 = (float)beta, two_p32 = (float)two_p;
     const uint64_t key = a.slot_key[slot];
     const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
     __syncthreads();
@@ -74,11 +115,12 @@ slot_sweep_kernel(SlotArgs a, int64_t t0, int n_sweeps) {
                         philox4x32_10(u32x4{(uint32_t)q, (uint32_t)(q >> 32), 0u, 0u}, k0, k1);
                     const int64_t i0 = (int64_t)(2 * q - base);
                     if (i0 >= cs && i0 < ce)
-                        slot_update(a, s, (int)i0, ((uint64_t)o.x | ((uint64_t)o.y << 32)) >> 11,
-                                    beta, two_p);
+                        slot_update_fast(a, s, (int)i0, ((uint64_t)o.x | ((uint64_t)o.y << 32)) >> 11,
+                                         beta, two_p, beta32, two_p32);
                     if (i0 + 1 >= cs && i0 + 1 < ce)
-                        slot_update(a, s, (int)i0 + 1,
-                                    ((uint64_t)o.z | ((uint64_t)o.w << 32)) >> 11, beta, two_p);
+                        slot_update_fast(a, s, (int)i0 + 1,
+                                         ((uint64_t)o.z | ((uint64_t)o.w << 32)) >> 11, beta, two_p,
+                                         beta32, two_p32);
                 }
             }
             __syncthreads();
