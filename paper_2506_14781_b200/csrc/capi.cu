@@ -161,7 +161,7 @@ struct tg_ctx {
     std::vector<uint32_t> h_active;
     std::vector<uint2> h_wkey;
     int plane_grid = 0, plane_block = kPlaneThreads;
-    int fused_grid = 0, fused_fast = 0, fused_block = kPlaneThreads;
+    int fused_grid = 0, fused_fast = 0, fused_block = kPlaneThreads, fused_wv = 4;
     size_t fused_smem = 0;
     size_t slot_smem = 0;
 
@@ -437,18 +437,23 @@ void build_plane(tg_ctx& c) {
     }
     c.fused_grid = 0;
     if (c.world == 1 && c.R <= 2048) {
-        const void* fn = plane_rounds_fn(c.cfg.rule, c.WV, c.fused_fast);
+        c.fused_wv = c.WV;
+        if (const char* e = std::getenv("TG_PLANE_LOOP")) if (std::atoi(e)) c.fused_wv = 0;
+        const void* fn = plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast);
         c.fused_block = c.fused_fast ? kPlaneThreadsFast : kPlaneThreads;
         c.fused_smem = (size_t)c.R * (2 * sizeof(double) + 2 * sizeof(int32_t)) + 8 +
-                       (size_t)(c.fused_block / 32) * kTailCap * 7 * sizeof(int32_t);
+                       (size_t)(c.fused_block / 32) *
+                           std::max<size_t>(std::max<size_t>(kTailCap * 7, (size_t)2 * c.W * 32),
+                                            (size_t)2 * (5 * 32 * 4 + 4 * 32)) * sizeof(int32_t);
         if (c.fused_smem > 48 * 1024)
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.fused_smem));
         int fb = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fb, fn, c.fused_block, c.fused_smem));
         if (fb >= 1) {
             int g = fb * c.sms;
-            g -= g % passes;
-            if (g >= passes) c.fused_grid = g;
+            const int fp = c.fused_wv ? passes : 1;
+            g -= g % fp;
+            if (g >= fp) c.fused_grid = g;
         }
     }
 }
@@ -830,7 +835,7 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         r.perm = c.d_perm.p;
         void* args[] = {&a, &r};
         if (c.profiling) CK(cudaEventRecord(c.ev[0], st));
-        CK(cudaLaunchCooperativeKernel(plane_rounds_fn(c.cfg.rule, c.WV, c.fused_fast),
+        CK(cudaLaunchCooperativeKernel(plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast),
                                        dim3(c.fused_grid), dim3(c.fused_block), args, c.fused_smem, st));
         if (c.profiling) CK(cudaEventRecord(c.ev[1], st));
         c.sweep_launches++;

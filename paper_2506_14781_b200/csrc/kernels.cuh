@@ -9,8 +9,9 @@
 namespace tg {
 
 constexpr int kPlaneThreads = 512;
-constexpr int kPlaneThreadsFast = 256;  // fused FAST kernel: 3 x 256 threads per SM, <= 85 regs
-constexpr int kPlaneMinBlocksFast = 4;
+constexpr int kPlaneThreadsFast = 512;
+constexpr int kPlaneMinBlocksFast = 1;
+constexpr int kPlaneMinBlocksLoop = 2;   // looped-row variant: 2 x 512 threads per SM
 constexpr int kSlotThreads = 256;
 constexpr int kSwapThreads = 1024;
 constexpr int kTailCap = 160;   // per-warp deferred-tail queue entries (plane_sweep.cu)

@@ -7,6 +7,7 @@
 // replaced by its 53-bit threshold K (exact host-side exp, engine.cpp
 // semantics) compared MSB-first against bit planes of Philox draws.
 #include <cooperative_groups.h>
+#include <cuda_pipeline.h>
 #include <cuda_runtime.h>
 
 #include "engine.cuh"
@@ -177,10 +178,12 @@ __device__ __noinline__ int tail_drain(const PlaneArgs& a, TailQ q, int qn, uint
 
 // One thread = one site of the chunk; all WV words (32 replicas each) of the
 // site row [wb, wb+WV) are loaded as one vector, updated, stored back.
-template <int NCB, int NQB, int RULE, int WV, int TAIL>
+template <int NCB, int NQB, int RULE, int WV, int TAIL, int PF = 0>
 __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, const PlaneType& ty,
                                            int wb, uint64_t t, bool count, int lower,
-                                           int (&acc_c)[WV], int (&acc_q)[WV], TailQ& tq, int& qn) {
+                                           int (&acc_c)[WV], int (&acc_q)[WV], TailQ& tq, int& qn,
+                                           const uint32_t* pfrow = nullptr,
+                                           const int32_t* pfidx = nullptr) {
     constexpr int DCM = (1 << NCB) - 1;
     constexpr int DQM = (1 << NQB) - 1;
     constexpr int B = NCB + NQB;
@@ -197,15 +200,20 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
 #pragma unroll
     for (int w = 0; w < WV; ++w) s[w] = 0u;
     if (valid) {
-        load_row<WV>(a.spins + (size_t)site * Wp + wb, s);
+        // rows come from global memory, or from this warp's shared-memory
+        // stage filled by cp.async one chunk ahead (PF): row r of lane l at
+        // pfrow[(r*32 + l)*WV], neighbour entries at pfidx[k*32 + l]
+        if constexpr (PF) load_row<WV>(pfrow + (size_t)lane * WV, s);
+        else load_row<WV>(a.spins + (size_t)site * Wp + wb, s);
         const int32_t* nb = a.nbr + ch.nbr_base + (size_t)lane * deg;
 #pragma unroll
         for (int k = 0; k < DCM; ++k) {
             if (k < dc) {
-                const int32_t e = __ldg(nb + k);
+                const int32_t e = PF ? pfidx[k * 32 + lane] : __ldg(nb + k);
                 const int j = e & 0x7fffffff;
                 const uint32_t neg = e < 0 ? 0xffffffffu : 0u;
-                load_row<WV>(a.spins + (size_t)j * Wp + wb, x[k]);
+                if constexpr (PF) load_row<WV>(pfrow + (size_t)((1 + k) * 32 + lane) * WV, x[k]);
+                else load_row<WV>(a.spins + (size_t)j * Wp + wb, x[k]);
 #pragma unroll
                 for (int w = 0; w < WV; ++w) x[k][w] ^= neg;  // bit: J_ij s_j = +1
                 lowx |= (uint32_t)(j < lower) << k;
@@ -217,8 +225,9 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
 #pragma unroll
         for (int k = 0; k < DQM; ++k) {
             if (k < dq) {
-                const int j = __ldg(nb + dc + k);
-                load_row<WV>(a.spins + (size_t)j * Wp + wb, y[k]);
+                const int j = PF ? pfidx[(dc + k) * 32 + lane] : __ldg(nb + dc + k);
+                if constexpr (PF) load_row<WV>(pfrow + (size_t)((1 + dc + k) * 32 + lane) * WV, y[k]);
+                else load_row<WV>(a.spins + (size_t)j * Wp + wb, y[k]);
                 lowy |= (uint32_t)(j < lower) << k;
             } else {
 #pragma unroll
@@ -390,6 +399,251 @@ __device__ __forceinline__ void plane_phase(const PlaneArgs& a, int c, uint64_t 
     }
 }
 
+
+// Software-pipelined phase for the FAST site types (deg <= 4) with WV = 4:
+// while chunk k is computed, the neighbour entries and the five 16-byte rows
+// of chunk k+1 stream into this warp's other shared-memory stage with
+// cp.async (LDGSTS) -- the L2 latency of the random neighbour gathers is
+// hidden behind a chunk of Philox/compare work instead of stalling the warp.
+constexpr int kPfRows = 5;                     // own row + up to 4 neighbours
+constexpr int kPfStageWords = kPfRows * 32 * 4 + 4 * 32;  // rows + neighbour entries
+template <int RULE>
+__device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64_t t, bool count,
+                                               int gidx, int ngroups, int wb, int32_t* cnt_c,
+                                               int32_t* cnt_q, uint32_t* pf) {
+    constexpr int WV = 4;
+    int acc_c[WV], acc_q[WV];
+#pragma unroll
+    for (int w = 0; w < WV; ++w) { acc_c[w] = 0; acc_q[w] = 0; }
+    const int c0 = a.chunk_off[c];
+    const int n_chunks = a.chunk_off[c + 1] - c0;
+    const int lower = a.color_start[c];
+    count = count && lower > 0;
+    const int lane = threadIdx.x & 31;
+    const int Wp = a.W;
+    TailQ tq{};
+    int qn = 0;
+    auto issue = [&](int item, int stage) {
+        const Chunk ch = a.chunks[c0 + item];
+        const PlaneType& ty = a.ty[ch.type];
+        const int deg = ty.dc + ty.dq;
+        uint32_t* rows = pf + stage * kPfStageWords;
+        int32_t* idx = reinterpret_cast<int32_t*>(rows + kPfRows * 32 * 4);
+        if (lane < ch.len) {
+            const int site = ch.start + lane;
+            __pipeline_memcpy_async(rows + lane * 4, a.spins + (size_t)site * Wp + wb, 16);
+            for (int k = 0; k < deg; ++k) {
+                const int32_t e = __ldg(a.nbr + ch.nbr_base + lane * deg + k);
+                idx[k * 32 + lane] = e;
+                __pipeline_memcpy_async(rows + ((1 + k) * 32 + lane) * 4,
+                                        a.spins + (size_t)(e & 0x7fffffff) * Wp + wb, 16);
+            }
+        }
+        __pipeline_commit();
+        return ch;
+    };
+    Chunk cur{};
+    if (gidx < n_chunks) cur = issue(gidx, 0);
+    int k = 0;
+    for (int item = gidx; item < n_chunks; item += ngroups, ++k) {
+        const int nxt = item + ngroups;
+        Chunk next{};
+        if (nxt < n_chunks) next = issue(nxt, (k + 1) & 1);
+        else __pipeline_commit();
+        __pipeline_wait_prior(1);
+        __syncwarp();
+        const uint32_t* rows = pf + (k & 1) * kPfStageWords;
+        const int32_t* idx = reinterpret_cast<const int32_t*>(rows + kPfRows * 32 * 4);
+        const PlaneType& ty = a.ty[cur.type];
+        switch (ty.ncb * 4 + ty.nqb) {
+            case 1 * 4 + 0: plane_site<1, 0, RULE, WV, 0, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
+            case 1 * 4 + 1: plane_site<1, 1, RULE, WV, 0, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
+            case 2 * 4 + 0: plane_site<2, 0, RULE, WV, 0, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
+            case 2 * 4 + 1: plane_site<2, 1, RULE, WV, 0, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
+            default: break;
+        }
+        __syncwarp();
+        cur = next;
+    }
+    __pipeline_wait_prior(0);
+    if (count) {
+#pragma unroll
+        for (int w = 0; w < WV; ++w) {
+            const int m = (wb + w) * 32 + lane;
+            if (m < a.local_states) {
+                if (acc_c[w]) atomicAdd(cnt_c + m, acc_c[w]);
+                if (acc_q[w]) atomicAdd(cnt_q + m, acc_q[w]);
+            }
+        }
+    }
+}
+
+// Looped variant (WV == 0): one thread = one site for ALL words of its row,
+// words processed one at a time (#pragma unroll 1).  Neighbour indices are
+// loaded once per site; per-word row words are 4-byte loads that hit L1 after
+// the first word touches the row's sector.  Far fewer live registers than the
+// vector-row variant; energy counts go to a per-warp shared-memory accumulator.
+template <int NCB, int NQB, int RULE>
+__device__ __forceinline__ void plane_site_loop(const PlaneArgs& a, const Chunk& ch,
+                                                const PlaneType& ty, uint64_t t, bool count,
+                                                int lower, int* sacc_c, int* sacc_q) {
+    constexpr int DCM = (1 << NCB) - 1;
+    constexpr int DQM = (1 << NQB) - 1;
+    constexpr int B = NCB + NQB;
+    const int lane = threadIdx.x & 31;
+    const int dc = ty.dc, dq = ty.dq, deg = dc + dq;
+    const bool valid = lane < ch.len;
+    const int site = ch.start + lane;
+    const int Wp = a.W;
+    int jx[DCM > 0 ? DCM : 1], jy[DQM > 0 ? DQM : 1];
+    uint32_t negx = 0, lowx = 0, lowy = 0;
+#pragma unroll
+    for (int k = 0; k < DCM; ++k) {
+        jx[k] = site;
+        if (valid && k < dc) {
+            const int32_t e = __ldg(a.nbr + ch.nbr_base + lane * deg + k);
+            jx[k] = e & 0x7fffffff;
+            negx |= (uint32_t)(e < 0) << k;
+            lowx |= (uint32_t)(jx[k] < lower) << k;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < DQM; ++k) {
+        jy[k] = site;
+        if (valid && k < dq) {
+            jy[k] = __ldg(a.nbr + ch.nbr_base + lane * deg + dc + k);
+            lowy |= (uint32_t)(jy[k] < lower) << k;
+        }
+    }
+    const int ncl = ty.ncl;
+    const bool pruned = (RULE == 0 && NQB == 0 && NCB == 2 && dc == 3);
+    const uint32_t thi = (uint32_t)(t >> 32), tlo = (uint32_t)t;
+    const uint32_t* srow = a.spins + (size_t)site * Wp;
+#pragma unroll 1
+    for (int w = 0; w < Wp; ++w) {
+        const uint32_t act = valid ? a.active[w] : 0u;
+        if (!__any_sync(0xffffffffu, act)) break;  // padding words
+        uint32_t s = 0u, x[DCM > 0 ? DCM : 1], y[DQM > 0 ? DQM : 1];
+        uint32_t cb[B > 0 ? B : 1];
+#pragma unroll
+        for (int b = 0; b < (B > 0 ? B : 1); ++b) cb[b] = 0u;
+        if (valid) s = srow[w];
+#pragma unroll
+        for (int k = 0; k < DCM; ++k) {
+            x[k] = 0u;
+            if (valid && k < dc) {
+                x[k] = a.spins[(size_t)jx[k] * Wp + w] ^ (((negx >> k) & 1u) ? 0xffffffffu : 0u);
+                bs_add<NCB>(cb, RULE == 0 ? ~(s ^ x[k]) : x[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < DQM; ++k) {
+            y[k] = 0u;
+            if (valid && k < dq) {
+                y[k] = a.spins[(size_t)jy[k] * Wp + w];
+                bs_add<NQB>(cb + NCB, RULE == 0 ? ~(s ^ y[k]) : y[k]);
+            }
+        }
+        const uint32_t* kpb = a.kp + (size_t)w * a.kpw + ty.kp_off;
+        const uint32_t always = mux_tree<B>(cb, kpb + kKPlanes * ncl) & act;
+        uint32_t und = act & ~always;
+        uint32_t lt = 0;
+        const uint32_t grp4 = (uint32_t)(a.w_global0 + w) << 4;
+        const u32x4 r0 = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | 0u}, a.pks);
+        const u32x4 r1 = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | 1u}, a.pks);
+        if (pruned) {
+            compare_block_sel(cb[0], kpb + 2, ncl, 0, r0, und, lt);
+            compare_block_sel(cb[0], kpb + 2, ncl, 1, r1, und, lt);
+        } else {
+            compare_block<B>(cb, kpb, ncl, 0, r0, und, lt);
+            compare_block<B>(cb, kpb, ncl, 1, r1, und, lt);
+        }
+#pragma unroll 1
+        for (int blk = 2; blk < 14; ++blk) {
+            if (!__any_sync(0xffffffffu, und)) break;
+            const u32x4 r = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | (uint32_t)blk}, a.pks);
+            if (pruned) compare_block_sel(cb[0], kpb + 2, ncl, blk, r, und, lt);
+            else compare_block<B>(cb, kpb, ncl, blk, r, und, lt);
+        }
+        const uint32_t take = (always | lt) & act;
+        const uint32_t ns = RULE == 0 ? (s ^ take) : ((s & ~act) | take);
+        if (valid) a.spins[(size_t)site * Wp + w] = ns;
+        if (count) {
+            if constexpr (NCB > 0) {
+                uint32_t m[NCB];
+#pragma unroll
+                for (int b = 0; b < NCB; ++b) m[b] = 0u;
+#pragma unroll
+                for (int k = 0; k < DCM; ++k)
+                    if (k < dc && ((lowx >> k) & 1u)) bs_add<NCB>(m, (ns ^ x[k]) & act);
+                int tot = 0;
+#pragma unroll
+                for (int b = 0; b < NCB; ++b)
+                    if (__any_sync(0xffffffffu, m[b])) tot += __popc(warp_transpose32(m[b])) << b;
+                if (tot) sacc_c[w * 32 + lane] += tot;
+            }
+            if constexpr (NQB > 0) {
+                uint32_t m[NQB];
+#pragma unroll
+                for (int b = 0; b < NQB; ++b) m[b] = 0u;
+#pragma unroll
+                for (int k = 0; k < DQM; ++k)
+                    if (k < dq && ((lowy >> k) & 1u)) bs_add<NQB>(m, (ns ^ y[k]) & act);
+                int tot = 0;
+#pragma unroll
+                for (int b = 0; b < NQB; ++b)
+                    if (__any_sync(0xffffffffu, m[b])) tot += __popc(warp_transpose32(m[b])) << b;
+                if (tot) sacc_q[w * 32 + lane] += tot;
+            }
+        }
+    }
+}
+
+template <int RULE, int FAST>
+__device__ __forceinline__ void plane_phase_loop(const PlaneArgs& a, int c, uint64_t t, bool count,
+                                                 int gidx, int ngroups, int32_t* cnt_c,
+                                                 int32_t* cnt_q, int* sacc) {
+    const int c0 = a.chunk_off[c];
+    const int n_chunks = a.chunk_off[c + 1] - c0;
+    const int lower = a.color_start[c];
+    count = count && lower > 0;
+    const int lane = threadIdx.x & 31;
+    int* sacc_c = sacc;
+    int* sacc_q = sacc + a.W * 32;
+    if (count)
+        for (int w = 0; w < a.W; ++w) { sacc_c[w * 32 + lane] = 0; sacc_q[w * 32 + lane] = 0; }
+    for (int item = gidx; item < n_chunks; item += ngroups) {
+        const Chunk ch = a.chunks[c0 + item];
+        const PlaneType& ty = a.ty[ch.type];
+#define TG_LCASE(C, Q) \
+        case (C) * 4 + (Q): plane_site_loop<C, Q, RULE>(a, ch, ty, t, count, lower, sacc_c, sacc_q); break;
+        if constexpr (FAST) {
+            switch (ty.ncb * 4 + ty.nqb) {
+                TG_LCASE(1, 0) TG_LCASE(1, 1) TG_LCASE(2, 0) TG_LCASE(2, 1)
+                default: break;
+            }
+        } else {
+            switch (ty.ncb * 4 + ty.nqb) {
+                TG_LCASE(1, 0) TG_LCASE(1, 1) TG_LCASE(1, 2)
+                TG_LCASE(2, 0) TG_LCASE(2, 1) TG_LCASE(2, 2)
+                TG_LCASE(3, 0) TG_LCASE(3, 1) TG_LCASE(3, 2)
+                default: break;
+            }
+        }
+#undef TG_LCASE
+    }
+    if (count) {
+        __syncwarp();
+        for (int w = 0; w < a.W; ++w) {
+            const int m = w * 32 + lane;
+            if (m < a.local_states) {
+                if (sacc_c[m]) atomicAdd(cnt_c + m, sacc_c[m]);
+                if (sacc_q[m]) atomicAdd(cnt_q + m, sacc_q[m]);
+            }
+        }
+    }
+}
+
 // Sweep-only cooperative kernel (multi-GPU path): all sweeps of one round;
 // the (f, g) exchange and the swap run after it.  Work item = (chunk of <= 32
 // same-type sites of one colour, pass of WV words).
@@ -433,7 +687,8 @@ plane_sweep_kernel(const __grid_constant__ PlaneArgs a, int64_t t0, int n_sweeps
 // threshold planes; block 0 publishes labels, counters and the record; one
 // more grid barrier closes the round.
 template <int RULE, int WV, int FAST>
-__global__ void __launch_bounds__(FAST ? kPlaneThreadsFast : kPlaneThreads, FAST ? kPlaneMinBlocksFast : 1)
+__global__ void __launch_bounds__(FAST ? kPlaneThreadsFast : kPlaneThreads,
+                                  WV == 0 ? kPlaneMinBlocksLoop : (FAST ? kPlaneMinBlocksFast : 1))
 plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__ RoundArgs r) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double sm_d[];
@@ -441,14 +696,17 @@ plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__
     double* s_g = sm_d + r.R;
     int32_t* s_slot = reinterpret_cast<int32_t*>(sm_d + 2 * r.R);
     int32_t* s_state = s_slot + r.R;
-    TailQ tq = tail_view(reinterpret_cast<char*>(s_state + r.R + (r.R & 1)), threadIdx.x >> 5);
+    char* sm_tail = reinterpret_cast<char*>(s_state + r.R + (r.R & 1));
+    TailQ tq = tail_view(sm_tail, threadIdx.x >> 5);
+    int* sacc = reinterpret_cast<int*>(sm_tail) + (size_t)(threadIdx.x >> 5) * 2 * a.W * 32;
+    uint32_t* pfbuf = reinterpret_cast<uint32_t*>(sm_tail) + (size_t)(threadIdx.x >> 5) * 2 * kPfStageWords;
     const int tid = threadIdx.x;
     const int wpb = blockDim.x >> 5;
     const int warp = tid >> 5, lane = tid & 31;
     const int gw = blockIdx.x * wpb + warp;
     const int nw = gridDim.x * wpb;
-    const int passes = a.W / WV;
-    const int wb = (int)(blockIdx.x % passes) * WV;
+    const int passes = WV ? a.W / WV : 1;
+    const int wb = WV ? (int)(blockIdx.x % passes) * WV : 0;
     const int gidx = (int)(blockIdx.x / passes) * wpb + warp;
     const int ngroups = (int)(gridDim.x / passes) * wpb;
     const int np = r.I * (r.J > 1 ? r.J - 1 : 0);
@@ -467,7 +725,9 @@ plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__
             const uint64_t t = (uint64_t)((round - 1) * r.sps + sw);
             const bool count = (sw == r.sps - 1);
             for (int c = 0; c < a.n_colors; ++c) {
-                plane_phase<RULE, WV, FAST, kPlaneTail>(a, c, t, count, gidx, ngroups, wb, cc, cq, tq);
+                if constexpr (WV == 0) plane_phase_loop<RULE, FAST>(a, c, t, count, gidx, ngroups, cc, cq, sacc);
+                else if constexpr (FAST && WV == 4) plane_phase_pf<RULE>(a, c, t, count, gidx, ngroups, wb, cc, cq, pfbuf);
+                else plane_phase<RULE, WV, FAST, kPlaneTail>(a, c, t, count, gidx, ngroups, wb, cc, cq, tq);
                 grid.sync();
             }
         }
@@ -576,10 +836,14 @@ template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 4, 0>(const __grid_c
 template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 4, 1>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
 template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 2, 1>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
 template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 1, 1>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
+template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 0, 1>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
+template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 0, 0>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
 
 
 
 void* TG_CAT(plane_rounds_fn_r, TG_PLANE_RULE)(int wv, int fast) {
+    if (wv == 0) return fast ? (void*)plane_rounds_kernel<TG_PLANE_RULE, 0, 1>
+                             : (void*)plane_rounds_kernel<TG_PLANE_RULE, 0, 0>;
     if (wv >= 4) return fast ? (void*)plane_rounds_kernel<TG_PLANE_RULE, 4, 1>
                              : (void*)plane_rounds_kernel<TG_PLANE_RULE, 4, 0>;
     if (wv >= 2) return fast ? (void*)plane_rounds_kernel<TG_PLANE_RULE, 2, 1>
