@@ -171,7 +171,7 @@ struct tg_ctx {
     DBuf<TgRecordDev> d_rec;
     DBuf<int8_t> d_rec_states;
     // plane
-    DBuf<uint32_t> d_spins32, d_kp, d_active;
+    DBuf<uint32_t> d_spins32, d_kp, d_kpc, d_active;
     DBuf<int32_t> d_nbr, d_cnt_c, d_cnt_q, d_cnt2;
     DBuf<Chunk> d_chunks;
     DBuf<int> d_chunk_off, d_color_start;
@@ -408,6 +408,8 @@ void build_plane(tg_ctx& c) {
     c.d_ktab.upload(ktab, st);
     c.d_kp.alloc((size_t)c.W * kpw);
     c.d_kp.zero(st);
+    c.d_kpc.alloc((size_t)c.W * c.n_types * 128);
+    c.d_kpc.zero(st);
     c.d_spins32.alloc((size_t)n * c.W);
     c.d_cnt_c.alloc((size_t)c.W * 32);
     c.d_cnt_q.alloc((size_t)c.W * 32);
@@ -429,12 +431,9 @@ void build_plane(tg_ctx& c) {
     // fused round-loop kernel (single GPU)
     c.fused_fast = 1;
     for (const auto& t : types) if (t.ncb > 2 || t.nqb > 1) c.fused_fast = 0;
-    // The 64-register FAST variant trades spills for occupancy and measured
-    // slower on B200 (see profiles/); opt in with TG_PLANE_FAST=1.
-    {
-        const char* e = std::getenv("TG_PLANE_FAST");
-        c.fused_fast = c.fused_fast && e && std::atoi(e) != 0;
-    }
+    // FAST: specialised kernel for site types with cost degree <= 3 and chain
+    // degree <= 1 (config 5), cp.async row prefetch; TG_PLANE_FAST=0 disables.
+    if (const char* e = std::getenv("TG_PLANE_FAST")) c.fused_fast = c.fused_fast && std::atoi(e) != 0;
     c.fused_grid = 0;
     if (c.world == 1 && c.R <= 2048) {
         c.fused_wv = c.WV;
@@ -558,6 +557,7 @@ PlaneArgs plane_args(tg_ctx& c) {
     a.ktab_row = c.ktab_row;
     a.w_global0 = c.state0 / 32;
     a.kp = c.d_kp.p;
+    a.kpc = c.d_kpc.p;
     a.cnt_c = c.d_cnt_c.p;
     a.cnt_q = c.d_cnt_q.p;
     a.f_loc = c.d_f.p + c.state0;
@@ -621,6 +621,7 @@ SwapArgs swap_args(tg_ctx& c) {
     a.ktab = c.d_ktab.p;
     a.ktab_row = c.ktab_row;
     a.kp = c.d_kp.p;
+    a.kpc = c.d_kpc.p;
     return a;
 }
 
@@ -829,7 +830,7 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         r.acc_p = c.d_acc_p.p; r.acc_b = c.d_acc_b.p;
         r.f_all = c.d_f.p; r.g_all = c.d_g.p;
         r.cnt = c.d_cnt2.p; r.cnt_stride = c.W * 32;
-        r.ktab = c.d_ktab.p; r.ktab_row = c.ktab_row; r.kp = c.d_kp.p;
+        r.ktab = c.d_ktab.p; r.ktab_row = c.ktab_row; r.kp = c.d_kp.p; r.kpc = c.d_kpc.p;
         r.rec = c.d_rec.p; r.rec_acc = c.d_rec_acc.p;
         r.rec_states = (flags & TG_REC_STATE) ? c.d_rec_states.p : nullptr;
         r.perm = c.d_perm.p;

@@ -60,6 +60,7 @@ struct PlaneArgs {
     const int* chunk_off; // [n_colors+1]
     const int* color_start; // [n_colors+1] internal site ranges
     const uint32_t* kp;   // [W][kpw] threshold planes for the current labels
+    const uint32_t* kpc;  // [W][n_types][2][64] class-major planes of classes 2,3 (pruned Metropolis types)
     PlaneType ty[kMaxTypes];     // by value: constant bank
     const int32_t* state_slot;   // [R] slot of each physical state (tail thresholds)
     const uint64_t* ktab;        // [R][ktab_row] 53-bit thresholds
@@ -120,6 +121,7 @@ struct RoundArgs {
     const uint64_t* ktab;
     int ktab_row;
     uint32_t* kp;
+    uint32_t* kpc;
     void* rec;             // TgRecordDev[n_rounds], digests pre-zeroed
     int64_t* rec_acc;
     int8_t* rec_states;    // [n_rounds][n] or null
@@ -148,6 +150,7 @@ struct SwapArgs {
     const uint64_t* ktab;  // [R][ktab_row]: 53-bit thresholds (>= 2^53: always)
     int ktab_row;
     uint32_t* kp;
+    uint32_t* kpc;
 };
 
 // ---------------------------------------------------------------- swaps

@@ -221,9 +221,14 @@ __global__ void __launch_bounds__(kSwapThreads) swap_kernel(SwapArgs a, int64_t 
             live = true;
         }
         uint32_t* dst = a.kp + (size_t)w * a.kpw + pt.kp_off + c;
+        uint32_t* dstc = (c == 2 || c == 3) ? a.kpc + ((size_t)w * a.n_types + ty) * 128 + (c - 2) * 64
+                                            : nullptr;
         for (int b = 0; b < kKPlanes; ++b) {
             const uint32_t word = __ballot_sync(0xffffffffu, live && ((K >> (52 - b)) & 1ull));
-            if (lane == 0) dst[b * pt.ncl] = word;
+            if (lane == 0) {
+                dst[b * pt.ncl] = word;
+                if (dstc) dstc[b] = word;
+            }
         }
         const uint32_t alw = __ballot_sync(0xffffffffu, live && K >= (1ull << 53));
         if (lane == 0) dst[kKPlanes * pt.ncl] = alw;

@@ -133,4 +133,16 @@ __device__ __forceinline__ void compare_block_sel(uint32_t c, const uint32_t* k0
     }
 }
 
+// Pruned compare of 4 planes with thresholds already in registers: lanes
+// with c set compare against class-3 planes k3, the others against k2.
+__device__ __forceinline__ void compare4_sel(uint32_t c, const uint4& k2, const uint4& k3,
+                                             const u32x4& r, uint32_t& und, uint32_t& lt) {
+    const uint32_t t0 = sel(c, k3.x, k2.x), t1 = sel(c, k3.y, k2.y);
+    const uint32_t t2 = sel(c, k3.z, k2.z), t3 = sel(c, k3.w, k2.w);
+    lt |= und & t0 & ~r.x; und &= ~(t0 ^ r.x);
+    lt |= und & t1 & ~r.y; und &= ~(t1 ^ r.y);
+    lt |= und & t2 & ~r.z; und &= ~(t2 ^ r.z);
+    lt |= und & t3 & ~r.w; und &= ~(t3 ^ r.w);
+}
+
 }  // namespace tg

@@ -272,9 +272,12 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
         // lane of the warp: issue them unconditionally as independent chains.
         const u32x4 r0 = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | 0u}, a.pks);
         const u32x4 r1 = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | 1u}, a.pks);
+        // class-major planes of the two threshold classes (pruned types)
+        const uint4* kc2 = reinterpret_cast<const uint4*>(
+            a.kpc + ((size_t)(wb + w) * a.n_types + ch.type) * 128);
         if (pruned) {
-            compare_block_sel(cb[0], kpb + 2, ncl, 0, r0, und, lt);
-            compare_block_sel(cb[0], kpb + 2, ncl, 1, r1, und, lt);
+            compare4_sel(cb[0], __ldg(kc2 + 0), __ldg(kc2 + 16), r0, und, lt);
+            compare4_sel(cb[0], __ldg(kc2 + 1), __ldg(kc2 + 17), r1, und, lt);
         } else {
             compare_block<B>(cb, kpb, ncl, 0, r0, und, lt);
             compare_block<B>(cb, kpb, ncl, 1, r1, und, lt);
@@ -284,7 +287,7 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
             for (int blk = 2; blk < 14; ++blk) {
                 if (!__any_sync(0xffffffffu, und)) break;
                 const u32x4 r = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | (uint32_t)blk}, a.pks);
-                if (pruned) compare_block_sel(cb[0], kpb + 2, ncl, blk, r, und, lt);
+                if (pruned) compare4_sel(cb[0], __ldg(kc2 + blk), __ldg(kc2 + 16 + blk), r, und, lt);
                 else compare_block<B>(cb, kpb, ncl, blk, r, und, lt);
             }
         }
@@ -796,9 +799,14 @@ plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__
                 const bool live = m < a.local_states;
                 if (live) K = r.ktab[(size_t)s_state[m] * r.ktab_row + pt.ktab_off + c];
                 uint32_t* dst = r.kp + (size_t)w * a.kpw + pt.kp_off + c;
+                uint32_t* dstc = (c == 2 || c == 3)
+                    ? r.kpc + ((size_t)w * a.n_types + ty) * 128 + (c - 2) * 64 : nullptr;
                 for (int b = 0; b < kKPlanes; ++b) {
                     const uint32_t word = __ballot_sync(0xffffffffu, live && ((K >> (52 - b)) & 1ull));
-                    if (lane == (b & 31)) dst[b * pt.ncl] = word;
+                    if (lane == (b & 31)) {
+                        dst[b * pt.ncl] = word;
+                        if (dstc) dstc[b] = word;
+                    }
                 }
                 const uint32_t alw = __ballot_sync(0xffffffffu, live && K >= (1ull << 53));
                 if (lane == (kKPlanes & 31)) dst[kKPlanes * pt.ncl] = alw;
