@@ -37,6 +37,11 @@ namespace tg {
 #define TG_PLANE_TAIL 0
 #endif
 constexpr int kPlaneTail = TG_PLANE_TAIL;
+// In-warp compaction of undecided (site, word) pairs in the FAST/prefetch path.
+#ifndef TG_PF_TAIL
+#define TG_PF_TAIL 2
+#endif
+constexpr int kPfTail = TG_PF_TAIL;
 struct TailQ {
     int* site;
     int* word;       // local word index
@@ -246,6 +251,143 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
     }
     const int ncl = ty.ncl;
     uint32_t ns[WV];
+    if constexpr (TAIL == 2) {
+        // ---- pass 1: class bits and the first 8 planes of every word
+        uint32_t cbw[WV][B > 0 ? B : 1], alw[WV], undw[WV], ltw[WV];
+        const bool pruned = (RULE == 0 && NQB == 0 && NCB == 2 && dc == 3);
+        const uint32_t thi = (uint32_t)(t >> 32), tlo = (uint32_t)t;
+        const int ncl = ty.ncl;
+#pragma unroll
+        for (int w = 0; w < WV; ++w) {
+#pragma unroll
+            for (int b = 0; b < (B > 0 ? B : 1); ++b) cbw[w][b] = 0u;
+#pragma unroll
+            for (int k = 0; k < DCM; ++k)
+                if (k < dc) bs_add<NCB>(cbw[w], RULE == 0 ? ~(s[w] ^ x[k][w]) : x[k][w]);
+#pragma unroll
+            for (int k = 0; k < DQM; ++k)
+                if (k < dq) bs_add<NQB>(cbw[w] + NCB, RULE == 0 ? ~(s[w] ^ y[k][w]) : y[k][w]);
+            const uint32_t* kpb = a.kp + (size_t)(wb + w) * a.kpw + ty.kp_off;
+            const uint32_t act = valid ? a.active[wb + w] : 0u;
+            alw[w] = mux_tree<B>(cbw[w], kpb + kKPlanes * ncl) & act;
+            undw[w] = act & ~alw[w];
+            ltw[w] = 0u;
+            const uint32_t grp4 = (uint32_t)(a.w_global0 + wb + w) << 4;
+            const u32x4 r0 = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | 0u}, a.pks);
+            const u32x4 r1 = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | 1u}, a.pks);
+            if (pruned) {
+                const uint4* kc2 = reinterpret_cast<const uint4*>(
+                    a.kpc + ((size_t)(wb + w) * a.n_types + ch.type) * 128);
+                compare4_sel(cbw[w][0], __ldg(kc2 + 0), __ldg(kc2 + 16), r0, undw[w], ltw[w]);
+                compare4_sel(cbw[w][0], __ldg(kc2 + 1), __ldg(kc2 + 17), r1, undw[w], ltw[w]);
+            } else {
+                compare_block<B>(cbw[w], kpb, ncl, 0, r0, undw[w], ltw[w]);
+                compare_block<B>(cbw[w], kpb, ncl, 1, r1, undw[w], ltw[w]);
+            }
+        }
+        // ---- pass 2: (thread, word) pairs still undecided are packed onto
+        // consecutive lanes and finish the lazy comparison together, one pair
+        // per lane, instead of each word dragging the whole warp through
+        // further Philox blocks.
+        uint32_t pend[WV];
+        int off[WV + 1];
+        off[0] = 0;
+#pragma unroll
+        for (int w = 0; w < WV; ++w) {
+            pend[w] = __ballot_sync(0xffffffffu, undw[w] != 0u);
+            off[w + 1] = off[w] + __popc(pend[w]);
+        }
+        const int P = off[WV];
+        for (int b0 = 0; b0 < P; b0 += 32) {
+            const int pi = b0 + lane;
+            const bool mine = pi < P;
+            int pw = 0;
+#pragma unroll
+            for (int w = 1; w < WV; ++w) pw += (pi >= off[w]) ? 1 : 0;
+            int src = 0;
+            if (mine) {  // rank-th set bit of pend[pw]
+                uint32_t mm = 0u;
+                int r = pi;
+#pragma unroll
+                for (int w = 0; w < WV; ++w) if (w == pw) { mm = pend[w]; r -= off[w]; }
+#pragma unroll
+                for (int st = 16; st > 0; st >>= 1) {
+                    const int c = __popc(mm & ((1u << st) - 1u));
+                    if (r >= c) { r -= c; mm >>= st; src += st; }
+                }
+            }
+            uint32_t u = 0u, cbp[B > 0 ? B : 1];
+#pragma unroll
+            for (int b = 0; b < (B > 0 ? B : 1); ++b) cbp[b] = 0u;
+#pragma unroll
+            for (int w = 0; w < WV; ++w) {
+                const uint32_t v = __shfl_sync(0xffffffffu, undw[w], src);
+                if (w == pw) u = v;
+#pragma unroll
+                for (int b = 0; b < (B > 0 ? B : 1); ++b) {
+                    const uint32_t cv = __shfl_sync(0xffffffffu, cbw[w][b], src);
+                    if (w == pw) cbp[b] = cv;
+                }
+            }
+            if (!mine) u = 0u;
+            const int psite = ch.start + src;
+            const uint32_t pgrp4 = (uint32_t)(a.w_global0 + wb + pw) << 4;
+            const uint32_t* kpb = a.kp + (size_t)(wb + pw) * a.kpw + ty.kp_off;
+            const uint4* kc2 = reinterpret_cast<const uint4*>(
+                a.kpc + ((size_t)(wb + pw) * a.n_types + ch.type) * 128);
+            uint32_t lx = 0u;
+#pragma unroll 1
+            for (int blk = 2; blk < 14; ++blk) {
+                if (!__any_sync(0xffffffffu, u)) break;
+                const u32x4 r = philox4x32_10_ks(u32x4{(uint32_t)psite, tlo, thi, pgrp4 | (uint32_t)blk}, a.pks);
+                if (pruned) compare4_sel(cbp[0], __ldg(kc2 + blk), __ldg(kc2 + 16 + blk), r, u, lx);
+                else compare_block<B>(cbp, kpb, ncl, blk, r, u, lx);
+            }
+            // return each pair's extra "take" lanes to its owner
+#pragma unroll
+            for (int w = 0; w < WV; ++w) {
+                const int mypi = off[w] + __popc(pend[w] & ((1u << lane) - 1u));
+                const int dst = mypi - b0;
+                const uint32_t v = __shfl_sync(0xffffffffu, lx, dst & 31);
+                if (undw[w] != 0u && dst >= 0 && dst < 32) ltw[w] |= v;
+            }
+        }
+        // ---- pass 3: new words, energy counts
+#pragma unroll
+        for (int w = 0; w < WV; ++w) {
+            const uint32_t act = valid ? a.active[wb + w] : 0u;
+            const uint32_t take = (alw[w] | ltw[w]) & act;
+            ns[w] = RULE == 0 ? (s[w] ^ take) : ((s[w] & ~act) | take);
+            if (count) {
+                if constexpr (NCB > 0) {
+                    uint32_t m[NCB];
+#pragma unroll
+                    for (int b = 0; b < NCB; ++b) m[b] = 0u;
+#pragma unroll
+                    for (int k = 0; k < DCM; ++k)
+                        if (k < dc && ((lowx >> k) & 1u)) bs_add<NCB>(m, (ns[w] ^ x[k][w]) & act);
+                    int tot = 0;
+#pragma unroll
+                    for (int b = 0; b < NCB; ++b)
+                        if (__any_sync(0xffffffffu, m[b])) tot += __popc(warp_transpose32(m[b])) << b;
+                    acc_c[w] += tot;
+                }
+                if constexpr (NQB > 0) {
+                    uint32_t m[NQB];
+#pragma unroll
+                    for (int b = 0; b < NQB; ++b) m[b] = 0u;
+#pragma unroll
+                    for (int k = 0; k < DQM; ++k)
+                        if (k < dq && ((lowy >> k) & 1u)) bs_add<NQB>(m, (ns[w] ^ y[k][w]) & act);
+                    int tot = 0;
+#pragma unroll
+                    for (int b = 0; b < NQB; ++b)
+                        if (__any_sync(0xffffffffu, m[b])) tot += __popc(warp_transpose32(m[b])) << b;
+                    acc_q[w] += tot;
+                }
+            }
+        }
+    } else {
 #pragma unroll
     for (int w = 0; w < WV; ++w) {
         uint32_t cb[B > 0 ? B : 1];
@@ -340,6 +482,7 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
                 acc_q[w] += tot;
             }
         }
+    }
     }
     if (valid) store_row<WV>(a.spins + (size_t)site * Wp + wb, ns);
 }
@@ -459,10 +602,10 @@ __device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64
         const int32_t* idx = reinterpret_cast<const int32_t*>(rows + kPfRows * 32 * 4);
         const PlaneType& ty = a.ty[cur.type];
         switch (ty.ncb * 4 + ty.nqb) {
-            case 1 * 4 + 0: plane_site<1, 0, RULE, WV, 0, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
-            case 1 * 4 + 1: plane_site<1, 1, RULE, WV, 0, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
-            case 2 * 4 + 0: plane_site<2, 0, RULE, WV, 0, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
-            case 2 * 4 + 1: plane_site<2, 1, RULE, WV, 0, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
+            case 1 * 4 + 0: plane_site<1, 0, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
+            case 1 * 4 + 1: plane_site<1, 1, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
+            case 2 * 4 + 0: plane_site<2, 0, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
+            case 2 * 4 + 1: plane_site<2, 1, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
             default: break;
         }
         __syncwarp();
