@@ -173,6 +173,7 @@ struct tg_ctx {
     // plane
     DBuf<uint32_t> d_spins32, d_kp, d_kpc, d_active;
     DBuf<int32_t> d_nbr, d_cnt_c, d_cnt_q, d_cnt2;
+    DBuf<int> d_work;
     DBuf<Chunk> d_chunks;
     DBuf<int> d_chunk_off, d_color_start;
     DBuf<PlaneType> d_types;
@@ -417,6 +418,8 @@ void build_plane(tg_ctx& c) {
     c.d_cnt_q.zero(st);
     c.d_cnt2.alloc((size_t)4 * c.W * 32);
     c.d_cnt2.zero(st);
+    c.d_work.alloc((size_t)2 * c.n_colors * std::max(1, c.W));
+    c.d_work.zero(st);
     // cooperative grid: a multiple of W warps, all blocks co-resident
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)plane_sweep_fn(c.cfg.rule, c.WV),
@@ -830,6 +833,8 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         r.acc_p = c.d_acc_p.p; r.acc_b = c.d_acc_b.p;
         r.f_all = c.d_f.p; r.g_all = c.d_g.p;
         r.cnt = c.d_cnt2.p; r.cnt_stride = c.W * 32;
+        // dynamic chunk grabbing measured 3% slower than the static split (r1); opt in
+        r.work = (std::getenv("TG_PLANE_DYNAMIC") ? c.d_work.p : nullptr);
         r.ktab = c.d_ktab.p; r.ktab_row = c.ktab_row; r.kp = c.d_kp.p; r.kpc = c.d_kpc.p;
         r.rec = c.d_rec.p; r.rec_acc = c.d_rec_acc.p;
         r.rec_states = (flags & TG_REC_STATE) ? c.d_rec_states.p : nullptr;

@@ -117,6 +117,7 @@ struct RoundArgs {
     double* f_all;
     double* g_all;
     int32_t* cnt;          // [2 parities][2 (cost, chain)][cnt_stride]
+    int* work;             // [2 parities][n_colors][passes] chunk counters (dynamic distribution)
     int cnt_stride;
     const uint64_t* ktab;
     int ktab_row;

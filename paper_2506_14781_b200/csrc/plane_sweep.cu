@@ -556,7 +556,7 @@ constexpr int kPfStageWords = kPfRows * 32 * 4 + 4 * 32;  // rows + neighbour en
 template <int RULE>
 __device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64_t t, bool count,
                                                int gidx, int ngroups, int wb, int32_t* cnt_c,
-                                               int32_t* cnt_q, uint32_t* pf) {
+                                               int32_t* cnt_q, uint32_t* pf, int* work) {
     constexpr int WV = 4;
     int acc_c[WV], acc_q[WV];
 #pragma unroll
@@ -588,11 +588,19 @@ __device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64
         __pipeline_commit();
         return ch;
     };
+    // dynamic chunk distribution: warps of this pass grab chunks from a
+    // global counter (balances the colour phase before the grid barrier)
+    auto grab = [&]() {
+        int v = 0;
+        if (lane == 0) v = work ? atomicAdd(work, 1) : 0;
+        return work ? __shfl_sync(0xffffffffu, v, 0) : 0;
+    };
+    int item = work ? grab() : gidx;
     Chunk cur{};
-    if (gidx < n_chunks) cur = issue(gidx, 0);
+    if (item < n_chunks) cur = issue(item, 0);
     int k = 0;
-    for (int item = gidx; item < n_chunks; item += ngroups, ++k) {
-        const int nxt = item + ngroups;
+    while (item < n_chunks) {
+        const int nxt = work ? grab() : item + ngroups;
         Chunk next{};
         if (nxt < n_chunks) next = issue(nxt, (k + 1) & 1);
         else __pipeline_commit();
@@ -610,6 +618,8 @@ __device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64
         }
         __syncwarp();
         cur = next;
+        item = nxt;
+        ++k;
     }
     __pipeline_wait_prior(0);
     if (count) {
@@ -872,7 +882,10 @@ plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__
             const bool count = (sw == r.sps - 1);
             for (int c = 0; c < a.n_colors; ++c) {
                 if constexpr (WV == 0) plane_phase_loop<RULE, FAST>(a, c, t, count, gidx, ngroups, cc, cq, sacc);
-                else if constexpr (FAST && WV == 4) plane_phase_pf<RULE>(a, c, t, count, gidx, ngroups, wb, cc, cq, pfbuf);
+                else if constexpr (FAST && WV == 4)
+                    plane_phase_pf<RULE>(a, c, t, count, gidx, ngroups, wb, cc, cq, pfbuf,
+                                         r.work ? r.work + ((size_t)(par * a.n_colors + c) * passes +
+                                                            wb / WV) : nullptr);
                 else plane_phase<RULE, WV, FAST, kPlaneTail>(a, c, t, count, gidx, ngroups, wb, cc, cq, tq);
                 grid.sync();
             }
@@ -905,6 +918,10 @@ plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__
             // counters of the other parity are free again: zero them
             int32_t* other = r.cnt + (size_t)(par ^ 1) * 2 * r.cnt_stride;
             for (int m = tid; m < 2 * r.cnt_stride; m += blockDim.x) other[m] = 0;
+            if (r.work) {
+                int* ow = r.work + (size_t)(par ^ 1) * a.n_colors * passes;
+                for (int m = tid; m < a.n_colors * passes; m += blockDim.x) ow[m] = 0;
+            }
             for (int m = tid; m < r.R; m += blockDim.x) {
                 r.slot_state[m] = s_slot[m];
                 r.state_slot[m] = s_state[m];
