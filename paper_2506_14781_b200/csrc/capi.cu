@@ -184,7 +184,9 @@ struct tg_ctx {
     DBuf<int> d_off;
     DBuf<int32_t> d_snbr;
     DBuf<double> d_sw, d_h;
-    DBuf<int2> d_ent;
+    DBuf<int2> d_ent, d_entp;
+    DBuf<double> d_wp;
+    int slot_D = 0;
     DBuf<float> d_h32;
     float slot_eps = 0.0f, slot_beta_max = 0.0f;
     DBuf<uint64_t> d_slot_key;
@@ -518,6 +520,29 @@ void build_slot(tg_ctx& c) {
         }
         eps = std::max(eps, (double)(off[i + 1] - off[i] + 3) * S * 0x1.0p-22);
     }
+    // padded fixed-degree copy (D = 4 or 8) for the unrolled kernel
+    int maxdeg = 0;
+    for (int i = 0; i < n; ++i) maxdeg = std::max(maxdeg, off[i + 1] - off[i]);
+    c.slot_D = maxdeg <= 4 ? 4 : (maxdeg <= 8 ? 8 : 0);
+    if (n >= (1 << 27)) c.slot_D = 0;
+    if (const char* e = std::getenv("TG_SLOT_GENERAL")) if (std::atoi(e)) c.slot_D = 0;
+    if (c.slot_D) {
+        const int D = c.slot_D;
+        std::vector<int2> entp((size_t)n * D);
+        std::vector<double> wp((size_t)n * D, 0.0);
+        for (int i = 0; i < n; ++i) {
+            for (int k = 0; k < D; ++k) entp[(size_t)i * D + k] = make_int2(i, 0);  // pad: w = 0
+            for (int e = off[i]; e < off[i + 1]; ++e) {
+                const int k = e - off[i];
+                int2 v = ent2[e];
+                if (nbr[e] > i) v.x |= 1 << 27;  // forward edge, counted once in (f, g)
+                entp[(size_t)i * D + k] = v;
+                wp[(size_t)i * D + k] = w[e];
+            }
+        }
+        c.d_entp.upload(entp, st);
+        c.d_wp.upload(wp, st);
+    }
     c.slot_eps = (float)(eps * 1.0001 + 1e-30);
     c.slot_beta_max = (float)(bmax * 1.0001);
     c.d_ent.upload(ent2, st);
@@ -535,6 +560,9 @@ void build_slot(tg_ctx& c) {
     c.slot_smem = (size_t)n;
     CK(cudaFuncSetAttribute((const void*)slot_sweep_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)std::max<size_t>(c.slot_smem, 48 * 1024)));
+    if (c.slot_D)
+        CK(cudaFuncSetAttribute(slot_sweep_fn_d(c.slot_D), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)std::max<size_t>(c.slot_smem, 48 * 1024)));
 }
 
 PlaneArgs plane_args(tg_ctx& c) {
@@ -584,6 +612,9 @@ SlotArgs slot_args(tg_ctx& c) {
     a.cm = c.d_cm.p;
     a.h = c.d_h.p;
     a.ent = c.d_ent.p;
+    a.entp = c.d_entp.p;
+    a.wp = c.d_wp.p;
+    a.D = c.slot_D;
     a.h32 = c.d_h32.p;
     a.eps_local = c.slot_eps;
     a.beta_max = c.slot_beta_max;
@@ -642,8 +673,8 @@ void launch_sweep(tg_ctx& c, int64_t t0) {
         int64_t t = t0;
         int nsw = sps;
         void* args[] = {&a, &t, &nsw};
-        CK(cudaLaunchKernel(slot_sweep_fn(), dim3(c.R_local), dim3(kSlotThreads), args,
-                            c.slot_smem, c.stream));
+        CK(cudaLaunchKernel(c.slot_D ? slot_sweep_fn_d(c.slot_D) : slot_sweep_fn(), dim3(c.R_local),
+                            dim3(kSlotThreads), args, c.slot_smem, c.stream));
     }
     c.sweep_launches++;
 }

@@ -88,6 +88,9 @@ struct SlotArgs {
     const int8_t* cm;     // chain multiplicity of the entry
     const double* h;      // fields
     const int2* ent;      // FP32 fast path: {j | cm<<28, float bits of J}
+    const int2* entp;     // padded [n][D] copy of ent; bit 27 = forward edge (j > i); pads point at i with w = 0
+    const double* wp;     // padded [n][D] FP64 cost weights (energy pass)
+    int D;                // padded degree (0: general CSR kernel)
     const float* h32;
     float eps_local;      // bound on |local_fp32 - local_fp64| over all sites
     float beta_max;

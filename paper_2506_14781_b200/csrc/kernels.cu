@@ -160,6 +160,135 @@ slot_sweep_kernel(SlotArgs a, int64_t t0, int n_sweeps) {
 
 void* slot_sweep_fn() { return (void*)slot_sweep_kernel; }
 
+// ---------------------------------------------- slot engine, padded degree
+
+// Fixed-degree variant: every site has D padded entries, so the field and
+// energy loops unroll without branches.  Same decisions as slot_update_fast.
+template <int D>
+__device__ __forceinline__ void slot_update_d(const SlotArgs& a, int8_t* s, int i, uint64_t u53,
+                                              double beta, double two_p, float beta32,
+                                              float two_p32) {
+    const int2* ep = a.entp + (size_t)i * D;
+    float l32 = __ldg(a.h32 + i);
+#pragma unroll
+    for (int k = 0; k < D; k += 2) {
+        const int4 v = __ldg(reinterpret_cast<const int4*>(ep + k));
+        const float w0 = __int_as_float(v.y) + (float)((v.x >> 28) & 15) * two_p32;
+        const float w1 = __int_as_float(v.w) + (float)((v.z >> 28) & 15) * two_p32;
+        l32 = fmaf(w0, (float)s[v.x & 0x07ffffff], l32);
+        l32 = fmaf(w1, (float)s[v.z & 0x07ffffff], l32);
+    }
+    const float si = (float)s[i];
+    const float uf = (float)u53 * 0x1.0p-53f;
+    const float eb = 2.0f * a.beta_max * a.eps_local;
+    if (a.rule == 0) {
+        const float de32 = 2.0f * si * l32;
+        const float tol = 2.0f * a.eps_local;
+        if (de32 < -tol) { s[i] = (int8_t)-s[i]; return; }
+        if (de32 > tol) {
+            const float x = -beta32 * de32;
+            const float T = __expf(x);
+            const float band = T * (2.0f * eb + fabsf(x) * 0x1.0p-19f + 0x1.0p-18f) + uf * 0x1.0p-22f;
+            if (uf < T - band) { s[i] = (int8_t)-s[i]; return; }
+            if (uf > T + band) return;
+        }
+    } else {
+        const float y = 2.0f * beta32 * l32;
+        const float p = __frcp_rn(1.0f + __expf(-y));
+        const float band = eb + fabsf(y) * 0x1.0p-19f + 0x1.0p-18f + uf * 0x1.0p-22f;
+        if (uf < p - band) { s[i] = 1; return; }
+        if (uf > p + band) { s[i] = -1; return; }
+    }
+    slot_update(a, s, i, u53, beta, two_p);  // near the threshold: decide in FP64
+}
+
+template <int D>
+__global__ void __launch_bounds__(kSlotThreads)
+slot_sweep_kernel_d(SlotArgs a, int64_t t0, int n_sweeps) {
+    extern __shared__ int8_t sm[];
+    const int m = blockIdx.x;
+    const int n = a.n;
+    int8_t* s = sm;
+    int8_t* gs = a.spins + (size_t)m * n;
+    {   // 16-byte staging of the configuration (rows are 16-byte aligned iff n % 16 == 0)
+        const int n16 = (n & 15) ? 0 : (n >> 4);
+        for (int q = threadIdx.x; q < n16; q += blockDim.x)
+            reinterpret_cast<int4*>(s)[q] = reinterpret_cast<const int4*>(gs)[q];
+        for (int i = (n16 << 4) + threadIdx.x; i < n; i += blockDim.x) s[i] = gs[i];
+    }
+    const int slot = a.state_slot[a.state0 + m];
+    const double beta = a.betas[slot / a.J];
+    const double two_p = 2.0 * a.pens[slot % a.J];
+    const float beta32 = (float)beta, two_p32 = (float)two_p;
+    const uint64_t key = a.slot_key[slot];
+    const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+    __syncthreads();
+    for (int sw = 0; sw < n_sweeps; ++sw) {
+        const uint64_t base = (uint64_t)(t0 + sw) * (uint64_t)n;
+        for (int c = 0; c < a.n_colors; ++c) {
+            const int cs = a.color_start[c], ce = a.color_start[c + 1];
+            if (ce > cs) {
+                const uint64_t q0 = (base + cs) >> 1, q1 = (base + ce - 1) >> 1;
+                for (uint64_t q = q0 + threadIdx.x; q <= q1; q += blockDim.x) {
+                    const u32x4 o =
+                        philox4x32_10(u32x4{(uint32_t)q, (uint32_t)(q >> 32), 0u, 0u}, k0, k1);
+                    const int64_t i0 = (int64_t)(2 * q - base);
+                    if (i0 >= cs && i0 < ce)
+                        slot_update_d<D>(a, s, (int)i0, ((uint64_t)o.x | ((uint64_t)o.y << 32)) >> 11,
+                                         beta, two_p, beta32, two_p32);
+                    if (i0 + 1 >= cs && i0 + 1 < ce)
+                        slot_update_d<D>(a, s, (int)i0 + 1, ((uint64_t)o.z | ((uint64_t)o.w << 32)) >> 11,
+                                         beta, two_p, beta32, two_p32);
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // f, g over forward edges (bit 27), FP64 cost weights
+    double fl = 0.0, gl = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double si = (double)s[i];
+        fl -= a.h[i] * si;
+        const int2* ep = a.entp + (size_t)i * D;
+        const double* wp = a.wp + (size_t)i * D;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const int2 v = __ldg(ep + k);
+            const double sj = (double)s[v.x & 0x07ffffff];
+            const bool fwd = (v.x >> 27) & 1;
+            const double cmf = (double)((v.x >> 28) & 15);
+            const double d = si - sj;
+            fl -= fwd ? __ldg(wp + k) * si * sj : 0.0;
+            gl += fwd ? cmf * d * d : 0.0;
+        }
+    }
+    {
+        const int n16 = (n & 15) ? 0 : (n >> 4);
+        for (int q = threadIdx.x; q < n16; q += blockDim.x)
+            reinterpret_cast<int4*>(gs)[q] = reinterpret_cast<const int4*>(s)[q];
+        for (int i = (n16 << 4) + threadIdx.x; i < n; i += blockDim.x) gs[i] = s[i];
+    }
+    __shared__ double red_f[kSlotThreads / 32], red_g[kSlotThreads / 32];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        fl += __shfl_xor_sync(0xffffffffu, fl, o);
+        gl += __shfl_xor_sync(0xffffffffu, gl, o);
+    }
+    if ((threadIdx.x & 31) == 0) { red_f[threadIdx.x >> 5] = fl; red_g[threadIdx.x >> 5] = gl; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double F = 0.0, G = 0.0;
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { F += red_f[q]; G += red_g[q]; }
+        a.f_loc[m] = F;
+        a.g_loc[m] = G;
+    }
+}
+
+void* slot_sweep_fn_d(int D) {
+    return D == 4 ? (void*)slot_sweep_kernel_d<4> : (D == 8 ? (void*)slot_sweep_kernel_d<8> : nullptr);
+}
+
+
 // ------------------------------------------------------------ swap kernel
 
 __global__ void __launch_bounds__(kSwapThreads) swap_kernel(SwapArgs a, int64_t round,

@@ -41,6 +41,7 @@ void* plane_sweep_fn(int rule, int wv);
 void* plane_rounds_fn(int rule, int wv, int fast);
 int plane_words_per_pass(int W);
 void* slot_sweep_fn();
+void* slot_sweep_fn_d(int D);  // padded-degree variant, D in {4, 8}
 
 __global__ void swap_kernel(SwapArgs a, int64_t round, uint64_t swap_base, int rec_idx,
                             int rec_flags);
