@@ -147,6 +147,27 @@ void* tg_stream(tg_ctx* ctx);
 /* Enable per-kernel CUDA-event timing inside tg_advance (default off). */
 int tg_set_profiling(tg_ctx* ctx, int on);
 
+/* ---------------------------------------------------------------- batches
+ * Independent instances in one launch (config 3: 64 Wishart instances, each
+ * with its own 16x16 grid).  Every instance has its own problem, schedule
+ * (same I x J shape across the batch) and seed; results equal independent
+ * tg_run / run_2dpt calls instance by instance.  SLOT engine
+ * semantics (per-slot reference streams).  The sink receives records per
+ * instance, in round order within each instance. */
+typedef int (*tg_batch_sink_fn)(void* user, int32_t instance, const tg_record* recs,
+                                int64_t n_recs, const int8_t* states, const int64_t* acc_p,
+                                const int64_t* acc_b);
+int tg_batch_clear(tg_ctx* ctx);
+int tg_batch_add(tg_ctx* ctx, int n, int n_couplings, const int32_t* ci, const int32_t* cj,
+                 const double* w, const double* fields, int n_pairs, const int32_t* pa,
+                 const int32_t* pb, int n_betas, const double* betas, int n_penalties,
+                 const double* penalties, uint64_t seed, int32_t* index);
+/* cfg->seed is ignored (per-instance seeds); engine must be AUTO or SLOT. */
+int tg_batch_run(tg_ctx* ctx, const tg_run_config* cfg, tg_batch_sink_fn sink, void* user);
+int tg_batch_get_state(tg_ctx* ctx, int instance, int slot, int8_t* out);
+int tg_batch_get_counters(tg_ctx* ctx, int instance, int64_t* attempts_p, int64_t* accepts_p,
+                          int64_t* attempts_b, int64_t* accepts_b);
+
 /* Host-only helper (no device needed): greedy colouring of cost+chain edges
  * and the canonical sweep order (stable sort by colour, chain degree, cost
  * degree); order[k] = caller spin at internal position k. */

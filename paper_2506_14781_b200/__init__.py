@@ -10,11 +10,12 @@ from .instances import (ConfigError, Problem, ResourceError, bipartite_3regular,
                         config_schedule, five_node_complete, k10_pm1, sparsify, to_canonical,
                         wishart_planted, wishart_schedule)
 from .api import (Engine, EngineError, RunConfig, Schedule, Trace, TraceRecord,
-                  beta_swap_probability, general_swap_probability, p_swap_probability, run_2dpt)
+                  beta_swap_probability, general_swap_probability, p_swap_probability, run_2dpt,
+                  run_2dpt_batch)
 
 __all__ = [
     "ConfigError", "ResourceError", "EngineError", "Problem", "Engine", "RunConfig", "Schedule",
-    "Trace", "TraceRecord", "run_2dpt", "p_swap_probability", "beta_swap_probability",
+    "Trace", "TraceRecord", "run_2dpt", "run_2dpt_batch", "p_swap_probability", "beta_swap_probability",
     "general_swap_probability", "sparsify", "canonical_order", "to_canonical",
     "five_node_complete", "k10_pm1", "wishart_planted", "bipartite_3regular", "config_schedule",
     "wishart_schedule",

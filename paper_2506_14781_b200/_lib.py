@@ -38,6 +38,8 @@ class InfoC(C.Structure):
                 ("other_launches", C.c_int64)]
 
 
+BATCH_SINK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.POINTER(RecordC), C.c_int64,
+                         C.POINTER(C.c_int8), C.POINTER(C.c_int64), C.POINTER(C.c_int64))
 SINK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(RecordC), C.c_int64, C.POINTER(C.c_int8),
                    C.POINTER(C.c_int64), C.POINTER(C.c_int64))
 
@@ -80,6 +82,12 @@ def lib() -> C.CDLL:
                   ("tg_general_swap_probability", 4)):
         getattr(L, fn).restype = C.c_double
         getattr(L, fn).argtypes = [C.c_double] * n
+    L.tg_batch_clear.argtypes = [vp]
+    L.tg_batch_add.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int, vp, vp, C.c_int, vp,
+                               C.c_int, vp, C.c_uint64, vp]
+    L.tg_batch_run.argtypes = [vp, C.POINTER(RunConfigC), BATCH_SINK, C.c_void_p]
+    L.tg_batch_get_state.argtypes = [vp, C.c_int, C.c_int, vp]
+    L.tg_batch_get_counters.argtypes = [vp, C.c_int, vp, vp, vp, vp]
     L.tg_partition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]
     L.tg_swap_phase_host.argtypes = [C.c_int, vp, C.c_int, vp, C.c_int64, C.c_int, C.c_uint64,
                                      C.c_uint64, vp, vp, vp, vp, vp]
@@ -92,5 +100,6 @@ EXPORTED = [
     "tg_last_error", "tg_set_problem", "tg_set_schedule", "tg_run", "tg_init", "tg_advance",
     "tg_get_state", "tg_get_counters", "tg_get_energies", "tg_get_info", "tg_stream",
     "tg_set_profiling", "tg_canonical_order", "tg_p_swap_probability", "tg_beta_swap_probability",
-    "tg_general_swap_probability", "tg_swap_phase_host", "tg_partition",
+    "tg_general_swap_probability", "tg_swap_phase_host", "tg_partition", "tg_batch_clear",
+    "tg_batch_add", "tg_batch_run", "tg_batch_get_state", "tg_batch_get_counters",
 ]

@@ -322,3 +322,88 @@ def run_2dpt(problem: Problem, schedule: Schedule, cfg: RunConfig, device: int =
         if engine is None:
             eng.close()
     return trace
+
+
+def run_2dpt_batch(problems: Sequence[Problem], schedules: Sequence[Schedule], cfg: RunConfig,
+                   seeds: Sequence[int], device: int = 0, engine: Optional[Engine] = None,
+                   sink: Optional[Callable] = None) -> List[Trace]:
+    """Independent instances in one launch (SURVEY.md §8b ``run_2dpt_batch``,
+    config 3).  Result b equals ``run_2dpt(problems[b], schedules[b], cfg with
+    seed=seeds[b])`` under the SLOT engine.  With ``sink`` set, records are
+    streamed to ``sink(instance, records, n, states, acc_p, acc_b)`` instead of
+    being collected into Traces."""
+    if not (len(problems) == len(schedules) == len(seeds)):
+        raise ConfigError("batch: problems, schedules and seeds differ in length")
+    eng = engine or Engine(device)
+    L = eng._L
+    try:
+        L.tg_batch_clear(eng._h)
+        keep = []
+        for pr, sc, sd in zip(problems, schedules, seeds):
+            arrs = [_arr(pr.ci, np.int32), _arr(pr.cj, np.int32), _arr(pr.cw, np.float64),
+                    _arr(pr.fields, np.float64), _arr(pr.pa, np.int32), _arr(pr.pb, np.int32),
+                    _arr(sc.betas, np.float64), _arr(sc.penalties, np.float64)]
+            keep.append(arrs)
+            ci, cj, cw, h, pa, pb, b, p = arrs
+            eng._check(L.tg_batch_add(eng._h, pr.n, len(ci), _p(ci), _p(cj), _p(cw), _p(h), len(pa),
+                                      _p(pa), _p(pb), len(b), _p(b), len(p), _p(p),
+                                      int(sd) & 0xFFFFFFFFFFFFFFFF, None))
+        c = eng._cfg(cfg)
+        c.engine = _lib.ENGINES["slot"] if cfg.engine == "auto" else c.engine
+        traces = [Trace(list(map(float, sc.betas)), list(map(float, sc.penalties)),
+                        int(cfg.sweeps_per_swap)) for sc in schedules]
+        I, J = len(schedules[0].betas), len(schedules[0].penalties)
+        R = I * J
+        np_, nb_ = I * max(J - 1, 0), max(I - 1, 0) * J
+        att = [[np.zeros(np_, np.int64), np.zeros(nb_, np.int64), 0] for _ in problems]
+
+        def _cb(user, b, recs, n, states, acc_p, acc_b):
+            try:
+                if sink is not None:
+                    return int(sink(b, recs, int(n), states, acc_p, acc_b) or 0)
+                pr = problems[b]
+                per = (R * pr.n) if not cfg.store_target_only else (pr.n if cfg.store_states else 0)
+                st = (np.ctypeslib.as_array(states, shape=(n * per,)).copy() if per and states else None)
+                ap = np.ctypeslib.as_array(acc_p, shape=(n * np_,)).copy() if np_ else np.zeros(0, np.int64)
+                ab = np.ctypeslib.as_array(acc_b, shape=(n * nb_,)).copy() if nb_ else np.zeros(0, np.int64)
+                a = att[b]
+                for k in range(n):
+                    r = recs[k]
+                    while a[2] < r.round:
+                        a[2] += 1
+                        x1, x2 = attempts_per_round(I, J, a[2])
+                        a[0][:] += x1
+                        a[1][:] += x2
+                    cp, cb_ = ap[k * np_:(k + 1) * np_], ab[k * nb_:(k + 1) * nb_]
+                    rp = [float(v) / q if q else 0.0 for v, q in zip(cp, a[0])]
+                    rb = [float(v) / q if q else 0.0 for v, q in zip(cb_, a[1])]
+                    state = grid = None
+                    if st is not None:
+                        chunk = st[k * per:(k + 1) * per]
+                        if cfg.store_target_only:
+                            state = chunk.copy()
+                        else:
+                            grid = chunk.reshape(R, pr.n).copy()
+                            state = grid[R - 1].copy()
+                    traces[b].records.append(TraceRecord(int(r.round), int(r.sweep_count), float(r.f),
+                                                         float(r.g), bool(r.feasible), state, rp, rb,
+                                                         grid, int(r.digest), int(r.target_state)))
+                return 0
+            except Exception:  # noqa: BLE001
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        cb = _lib.BATCH_SINK(_cb)
+        eng._check(L.tg_batch_run(eng._h, C.byref(c), cb, None))
+        eng._batch_problems = problems
+        return traces
+    finally:
+        if engine is None:
+            eng.close()
+
+
+def batch_state(engine: Engine, instance: int, slot: int, n: int) -> np.ndarray:
+    out = np.zeros(n, np.int8)
+    engine._check(engine._L.tg_batch_get_state(engine._h, int(instance), int(slot), _p(out)))
+    return out

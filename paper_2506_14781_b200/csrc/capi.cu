@@ -127,6 +127,51 @@ int nbits(int d) {
     return d == 0 ? 0 : b;
 }
 
+
+struct BatchInst {
+    int n = 0;
+    std::vector<int> ci, cj, pa, pb;
+    std::vector<double> cw, h, betas, pens;
+    uint64_t seed = 1;
+};
+
+struct S2Prep {
+    int n = 0, n_colors = 0, D = 4;
+    std::vector<int> order, inv, color, color_start, off;
+    std::vector<int32_t> nbr;
+    std::vector<double> w, h;
+    std::vector<int8_t> cm;
+    std::vector<float> h32;
+    std::vector<int2> entp;
+    std::vector<double> wp;
+    float eps = 0.f, beta_max = 0.f;
+};
+
+
+struct Slot2 {
+    int B = 0, I = 0, J = 0, R = 0, Rp = 0, G = 0, D = 4, max_colors = 0, slots = 1;
+    int rec_cap = 0, grid = 0;
+    tg_run_config cfg{};
+    std::vector<S2Prep> prep;
+    std::vector<int> state_off;
+    DBuf<SInst> d_inst;
+    DBuf<int2> d_entp;
+    DBuf<double> d_wp, d_w, d_h, d_betas, d_pens, d_part_f, d_part_g, d_f, d_g;
+    DBuf<int> d_off, d_cstart, d_item_pref, d_energy_pref, d_perm;
+    DBuf<int32_t> d_nbr, d_slot_state, d_state_slot;
+    DBuf<int8_t> d_cm, d_spins, d_rec_states;
+    DBuf<float> d_h32;
+    DBuf<uint64_t> d_keys, d_swap_seed, d_seeds;
+    DBuf<int64_t> d_acc_p, d_acc_b, d_rec_acc;
+    DBuf<TgRecordDev> d_rec;
+    std::vector<TgRecordDev> h_rec;
+    std::vector<int64_t> h_acc;
+    std::vector<int8_t> h_states;
+    int64_t rounds_done = 0;
+    uint64_t swap_base = 0;
+    bool ready = false;
+};
+
 }  // namespace
 
 struct tg_ctx {
@@ -190,6 +235,11 @@ struct tg_ctx {
     DBuf<float> d_h32;
     float slot_eps = 0.0f, slot_beta_max = 0.0f;
     DBuf<uint64_t> d_slot_key;
+
+    // SLOT engine v2 (single instance and batches)
+    std::vector<BatchInst> batch;
+    Slot2 s2;
+    bool use_s2 = false;
 
     int rec_cap = 0;
     std::vector<TgRecordDev> h_rec;
@@ -260,6 +310,48 @@ void canonical(int n, const std::vector<int>& ci, const std::vector<int>& cj,
     for (size_t k = 0; k < nk; ++k) bucket[k + 1] += bucket[k];
     order.resize(n);
     for (int i = 0; i < n; ++i) order[bucket[keyv[i]]++] = i;
+}
+
+// IsingModel / ConstraintSet validation (ising.cpp:21-46, constraints.cpp:16-26)
+void load_problem(BatchInst& bi, int n, int n_couplings, const int32_t* ci, const int32_t* cj,
+                  const double* w, const double* fields, int n_pairs, const int32_t* pa,
+                  const int32_t* pb) {
+    if (n <= 0) fail(TG_ERR_CONFIG, "model: n_spins must be positive");
+    if (n_couplings < 0 || n_pairs < 0) fail(TG_ERR_CONFIG, "model: negative counts");
+    std::vector<uint64_t> keys;
+    std::vector<int> a(n_couplings), b(n_couplings), qa(n_pairs), qb(n_pairs);
+    for (int k = 0; k < n_couplings; ++k) {
+        int x = ci[k], y = cj[k];
+        if (x == y) fail(TG_ERR_CONFIG, "model: self-loop on spin %d", x);
+        if (x > y) std::swap(x, y);
+        if (x < 0 || y >= n) fail(TG_ERR_CONFIG, "model: coupling index out of range: (%d, %d)", x, y);
+        if (!std::isfinite(w[k])) fail(TG_ERR_CONFIG, "model: coupling weights must be finite");
+        a[k] = x;
+        b[k] = y;
+        keys.push_back((uint64_t)x << 32 | (uint64_t)y);
+    }
+    std::sort(keys.begin(), keys.end());
+    for (size_t k = 1; k < keys.size(); ++k)
+        if (keys[k] == keys[k - 1])
+            fail(TG_ERR_CONFIG, "model: duplicate coupling (%d, %d)", (int)(keys[k] >> 32),
+                 (int)(keys[k] & 0xffffffffu));
+    for (int k = 0; k < n_pairs; ++k) {
+        int x = pa[k], y = pb[k];
+        if (x == y) fail(TG_ERR_CONFIG, "constraint: pair on a single spin %d", x);
+        if (x > y) std::swap(x, y);
+        if (x < 0 || y >= n) fail(TG_ERR_CONFIG, "constraint: index out of range: (%d, %d)", x, y);
+        qa[k] = x;
+        qb[k] = y;
+    }
+    bi.n = n;
+    bi.ci = a;
+    bi.cj = b;
+    bi.cw.assign(w, w + n_couplings);
+    bi.h.assign(n, 0.0);
+    if (fields) for (int i = 0; i < n; ++i) bi.h[i] = fields[i];
+    for (double x : bi.h) if (!std::isfinite(x)) fail(TG_ERR_CONFIG, "model: fields must be finite");
+    bi.pa = qa;
+    bi.pb = qb;
 }
 
 void check_vec(const std::vector<double>& v, const char* what) {  // engine.cpp:41-52
@@ -691,6 +783,8 @@ void rebuild_planes(tg_ctx& c) {
     CK(cudaGetLastError());
 }
 
+void s2_build(tg_ctx& c, const tg_run_config* cfg);
+
 void do_init(tg_ctx& c, const tg_run_config* cfg) {
     if (!c.have_problem) fail(TG_ERR_CONFIG, "run: no problem set");
     if (!c.have_schedule) fail(TG_ERR_CONFIG, "run: no schedule set");
@@ -721,6 +815,19 @@ void do_init(tg_ctx& c, const tg_run_config* cfg) {
     }
     cudaStream_t st = c.stream;
     CK(cudaSetDevice(c.device));
+    c.use_s2 = false;
+    if (eng == TG_ENGINE_SLOT && c.world == 1 && !std::getenv("TG_SLOT_V1")) {
+        // single instance = batch of one on the replica-fastest SLOT engine
+        BatchInst bi;
+        bi.n = c.n; bi.ci = c.ci; bi.cj = c.cj; bi.pa = c.pa; bi.pb = c.pb;
+        bi.cw = c.cw; bi.h = c.h; bi.betas = c.betas; bi.pens = c.pens; bi.seed = cfg->seed;
+        c.batch.assign(1, bi);
+        s2_build(c, &c.cfg);
+        c.use_s2 = true;
+        c.rounds_done = 0;
+        c.initialised = true;
+        return;
+    }
     c.d_betas.upload(c.betas, st);
     c.d_pens.upload(c.pens, st);
     c.d_f.alloc(c.R);
@@ -770,6 +877,14 @@ struct SinkCtx {
     tg_sink_fn fn;
     void* user;
 };
+
+struct BatchSinkCtx {
+    tg_batch_sink_fn fn;
+    void* user;
+};
+
+void s2_build(tg_ctx& c, const tg_run_config* cfg);
+void s2_advance(tg_ctx& c, int64_t n_rounds, const BatchSinkCtx& sink);
 
 void drain(tg_ctx& c, int filled, int64_t first_round, const SinkCtx& sink) {
     if (filled <= 0) return;
@@ -892,8 +1007,20 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
     c.last_swap_ms = 0;
 }
 
+int single_sink_adapter(void* user, int32_t, const tg_record* recs, int64_t n, const int8_t* st,
+                        const int64_t* ap, const int64_t* ab) {
+    const SinkCtx* sc = static_cast<const SinkCtx*>(user);
+    return sc->fn ? sc->fn(sc->user, recs, n, st, ap, ab) : 0;
+}
+
 void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
     if (!c.initialised) fail(TG_ERR_CONFIG, "advance: context not initialised (tg_init)");
+    if (c.use_s2) {
+        SinkCtx sc = sink;
+        s2_advance(c, n_rounds, BatchSinkCtx{sink.fn ? &single_sink_adapter : nullptr, &sc});
+        c.rounds_done = c.s2.rounds_done;
+        return;
+    }
     if (c.engine == TG_ENGINE_PLANE && c.world == 1 && c.fused_grid > 0 &&
         !(c.cfg.record_flags & TG_REC_GRID)) {
         do_advance_fused(c, n_rounds, sink);
@@ -970,6 +1097,423 @@ void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
     c.last_swap_ms = swap_ms;
 }
 
+// ------------------------------------------------ SLOT engine v2 (host side)
+
+// One instance prepared for the device: canonical order, merged CSR (FP64
+// fallback), padded degree-D entries (FP32 fast path + forward-edge flags),
+// and the FP32 error bound (see kernels.cu slot_update_fast).
+void s2_prepare(S2Prep& P, const BatchInst& bi) {
+    const int n = bi.n;
+    P.n = n;
+    canonical(n, bi.ci, bi.cj, bi.pa, bi.pb, P.order, P.color, P.n_colors);
+    P.inv.assign(n, 0);
+    for (int k = 0; k < n; ++k) P.inv[P.order[k]] = k;
+    P.color_start.assign(P.n_colors + 1, 0);
+    for (int k = 0; k < n; ++k) P.color_start[P.color[P.order[k]] + 1]++;
+    for (int q = 0; q < P.n_colors; ++q) P.color_start[q + 1] += P.color_start[q];
+    struct E { uint64_t key; double w; int cm; };
+    std::vector<E> ent;
+    ent.reserve(2 * (bi.ci.size() + bi.pa.size()));
+    for (size_t k = 0; k < bi.ci.size(); ++k) {
+        const uint64_t x = (uint64_t)P.inv[bi.ci[k]], y = (uint64_t)P.inv[bi.cj[k]];
+        ent.push_back({x << 32 | y, bi.cw[k], 0});
+        ent.push_back({y << 32 | x, bi.cw[k], 0});
+    }
+    for (size_t k = 0; k < bi.pa.size(); ++k) {
+        const uint64_t x = (uint64_t)P.inv[bi.pa[k]], y = (uint64_t)P.inv[bi.pb[k]];
+        ent.push_back({x << 32 | y, 0.0, 1});
+        ent.push_back({y << 32 | x, 0.0, 1});
+    }
+    std::stable_sort(ent.begin(), ent.end(), [](const E& p, const E& q) { return p.key < q.key; });
+    P.off.assign(n + 1, 0);
+    P.nbr.clear(); P.w.clear(); P.cm.clear();
+    for (size_t k = 0; k < ent.size();) {
+        size_t q = k;
+        double ws = 0.0;
+        int cs = 0;
+        while (q < ent.size() && ent[q].key == ent[k].key) { ws += ent[q].w; cs += ent[q].cm; ++q; }
+        P.nbr.push_back((int32_t)(ent[k].key & 0xffffffffu));
+        P.w.push_back(ws);
+        P.cm.push_back((int8_t)cs);
+        P.off[(int)(ent[k].key >> 32) + 1]++;
+        k = q;
+    }
+    for (int i = 0; i < n; ++i) P.off[i + 1] += P.off[i];
+    int maxdeg = 0;
+    for (int i = 0; i < n; ++i) maxdeg = std::max(maxdeg, P.off[i + 1] - P.off[i]);
+    if (maxdeg > 16) fail(TG_ERR_RESOURCE, "slot engine: merged degree %d > 16", maxdeg);
+    if (n >= (1 << 27)) fail(TG_ERR_RESOURCE, "slot engine: %d spins exceed the packed index", n);
+    P.D = maxdeg <= 4 ? 4 : (maxdeg <= 8 ? 8 : 16);
+    double pmax = 0.0, bmax = 0.0, eps = 0.0;
+    for (double p : bi.pens) pmax = std::max(pmax, p);
+    for (double b : bi.betas) bmax = std::max(bmax, std::fabs(b));
+    P.h.resize(n);
+    P.h32.resize(n);
+    P.entp.assign((size_t)n * P.D, make_int2(0, 0));
+    P.wp.assign((size_t)n * P.D, 0.0);
+    for (int i = 0; i < n; ++i) {
+        P.h[i] = bi.h[P.order[i]];
+        P.h32[i] = (float)P.h[i];
+        double S = std::fabs(P.h[i]);
+        for (int k = 0; k < P.D; ++k) P.entp[(size_t)i * P.D + k] = make_int2(i, 0);  // pad: weight 0
+        for (int e = P.off[i]; e < P.off[i + 1]; ++e) {
+            const float wf = (float)P.w[e];
+            int bits;
+            std::memcpy(&bits, &wf, 4);
+            int x = P.nbr[e] | ((int)P.cm[e] << 28);
+            if (P.nbr[e] > i) x |= 1 << 27;
+            P.entp[(size_t)i * P.D + (e - P.off[i])] = make_int2(x, bits);
+            P.wp[(size_t)i * P.D + (e - P.off[i])] = P.w[e];
+            S += std::fabs(P.w[e]) + (double)P.cm[e] * 2.0 * pmax;
+        }
+        eps = std::max(eps, (double)(P.off[i + 1] - P.off[i] + 3) * S * 0x1.0p-22);
+    }
+    P.eps = (float)(eps * 1.0001 + 1e-30);
+    P.beta_max = (float)(bmax * 1.0001);
+}
+
+S2Args s2_args(tg_ctx& c) {
+    Slot2& S = c.s2;
+    S2Args a{};
+    a.B = S.B; a.I = S.I; a.J = S.J; a.R = S.R; a.Rp = S.Rp; a.G = S.G;
+    a.rule = S.cfg.rule; a.max_colors = S.max_colors;
+    a.inst = S.d_inst.p; a.spins = S.d_spins.p; a.entp = S.d_entp.p; a.wp = S.d_wp.p;
+    a.off = S.d_off.p; a.nbr = S.d_nbr.p; a.w = S.d_w.p; a.cm = S.d_cm.p;
+    a.h = S.d_h.p; a.h32 = S.d_h32.p; a.color_start = S.d_cstart.p;
+    a.item_pref = S.d_item_pref.p; a.energy_pref = S.d_energy_pref.p;
+    a.betas = S.d_betas.p; a.pens = S.d_pens.p; a.state_slot = S.d_state_slot.p;
+    a.slot_key = S.d_keys.p; a.part_f = S.d_part_f.p; a.part_g = S.d_part_g.p;
+    a.f = S.d_f.p; a.g = S.d_g.p;
+    return a;
+}
+
+S2Swap s2_swap(tg_ctx& c) {
+    Slot2& S = c.s2;
+    S2Swap s{};
+    s.R = S.R; s.I = S.I; s.J = S.J; s.rec_cap = S.rec_cap;
+    s.betas = S.d_betas.p; s.pens = S.d_pens.p; s.f = S.d_f.p; s.g = S.d_g.p;
+    s.slot_state = S.d_slot_state.p; s.state_slot = S.d_state_slot.p;
+    s.acc_p = S.d_acc_p.p; s.acc_b = S.d_acc_b.p; s.swap_seed = S.d_swap_seed.p;
+    s.rec = S.d_rec.p; s.rec_acc = S.d_rec_acc.p; s.rec_states = S.d_rec_states.p;
+    s.perm = S.d_perm.p;
+    return s;
+}
+
+void s2_build(tg_ctx& c, const tg_run_config* cfg) {
+    Slot2& S = c.s2;
+    cudaStream_t st = c.stream;
+    const int B = (int)c.batch.size();
+    if (B < 1) fail(TG_ERR_CONFIG, "batch: no instances");
+    S.B = B;
+    S.I = (int)c.batch[0].betas.size();
+    S.J = (int)c.batch[0].pens.size();
+    for (const auto& bi : c.batch)
+        if ((int)bi.betas.size() != S.I || (int)bi.pens.size() != S.J)
+            fail(TG_ERR_CONFIG, "batch: every instance needs the same I x J grid shape");
+    S.R = S.I * S.J;
+    S.Rp = (S.R + 31) / 32 * 32;
+    S.G = S.Rp / 32;
+    S.cfg = *cfg;
+    if (S.cfg.record_every < 1) S.cfg.record_every = 1;
+    S.prep.assign(B, S2Prep{});
+    S.state_off.clear();
+    for (int b = 0; b < B; ++b) s2_prepare(S.prep[b], c.batch[b]);
+    int D = 4;
+    for (const auto& P : S.prep) D = std::max(D, P.D);
+    S.D = D;
+    // concatenate
+    std::vector<SInst> inst(B);
+    std::vector<int2> entp;
+    std::vector<double> wp, w, h, betas, pens;
+    std::vector<int> off, cstart, perm;
+    std::vector<int32_t> nbr;
+    std::vector<int8_t> cm;
+    std::vector<float> h32;
+    std::vector<uint64_t> keys((size_t)B * S.R), swap_seed(B), seeds(B);
+    long long spin_off = 0;
+    int chunk_off = 0, state_off = 0, max_colors = 0;
+    for (int b = 0; b < B; ++b) {
+        S2Prep& P = S.prep[b];
+        SInst& in = inst[b];
+        in.n = P.n;
+        in.D = D;
+        in.n_colors = P.n_colors;
+        in.color_off = (int)cstart.size();
+        cstart.insert(cstart.end(), P.color_start.begin(), P.color_start.end());
+        in.spin_off = spin_off;
+        spin_off += (long long)P.n * S.Rp;
+        in.entp_off = (int)entp.size();
+        for (int i = 0; i < P.n; ++i)
+            for (int k = 0; k < D; ++k) {
+                entp.push_back(k < P.D ? P.entp[(size_t)i * P.D + k] : make_int2(i, 0));
+                wp.push_back(k < P.D ? P.wp[(size_t)i * P.D + k] : 0.0);
+            }
+        in.csr_off = (int)off.size();
+        off.insert(off.end(), P.off.begin(), P.off.end());
+        in.nbr_off = (int)nbr.size();
+        nbr.insert(nbr.end(), P.nbr.begin(), P.nbr.end());
+        w.insert(w.end(), P.w.begin(), P.w.end());
+        cm.insert(cm.end(), P.cm.begin(), P.cm.end());
+        in.h_off = (int)h.size();
+        h.insert(h.end(), P.h.begin(), P.h.end());
+        h32.insert(h32.end(), P.h32.begin(), P.h32.end());
+        perm.insert(perm.end(), P.order.begin(), P.order.end());
+        in.n_chunks = (P.n + 31) / 32;
+        in.chunk_off = chunk_off;
+        chunk_off += in.n_chunks;
+        in.state_off = state_off;
+        S.state_off.push_back(state_off);
+        state_off += P.n;
+        in.eps = P.eps;
+        in.beta_max = P.beta_max;
+        max_colors = std::max(max_colors, P.n_colors);
+        betas.insert(betas.end(), c.batch[b].betas.begin(), c.batch[b].betas.end());
+        pens.insert(pens.end(), c.batch[b].pens.begin(), c.batch[b].pens.end());
+        seeds[b] = c.batch[b].seed;
+        for (int r = 0; r < S.R; ++r)
+            keys[(size_t)b * S.R + r] = derive_seed(c.batch[b].seed, kPurposeReplica, (uint64_t)r);
+        swap_seed[b] = derive_seed(c.batch[b].seed, kPurposeSwap, 0);
+    }
+    S.max_colors = max_colors;
+    // item prefix tables: per colour, per instance, upper bound of Philox pairs x groups
+    std::vector<int> item_pref((size_t)max_colors * (B + 1), 0), energy_pref(B + 1, 0);
+    for (int col = 0; col < max_colors; ++col)
+        for (int b = 0; b < B; ++b) {
+            const S2Prep& P = S.prep[b];
+            const int len = col < P.n_colors ? P.color_start[col + 1] - P.color_start[col] : 0;
+            const int ub = len > 0 ? (len + 3) / 2 : 0;
+            item_pref[(size_t)col * (B + 1) + b + 1] = item_pref[(size_t)col * (B + 1) + b] + ub * S.G;
+        }
+    for (int b = 0; b < B; ++b) energy_pref[b + 1] = energy_pref[b] + inst[b].n_chunks * S.G;
+    S.d_inst.upload(inst, st);
+    S.d_entp.upload(entp, st);
+    S.d_wp.upload(wp, st);
+    S.d_off.upload(off, st);
+    S.d_nbr.upload(nbr, st);
+    S.d_w.upload(w, st);
+    S.d_cm.upload(cm, st);
+    S.d_h.upload(h, st);
+    S.d_h32.upload(h32, st);
+    S.d_cstart.upload(cstart, st);
+    S.d_item_pref.upload(item_pref, st);
+    S.d_energy_pref.upload(energy_pref, st);
+    S.d_betas.upload(betas, st);
+    S.d_pens.upload(pens, st);
+    S.d_keys.upload(keys, st);
+    S.d_swap_seed.upload(swap_seed, st);
+    S.d_seeds.upload(seeds, st);
+    S.d_perm.upload(perm, st);
+    S.d_spins.alloc((size_t)spin_off);
+    S.d_part_f.alloc((size_t)chunk_off * S.Rp);
+    S.d_part_g.alloc((size_t)chunk_off * S.Rp);
+    S.d_f.alloc((size_t)B * S.R);
+    S.d_g.alloc((size_t)B * S.R);
+    std::vector<int32_t> ident((size_t)B * S.R);
+    for (int b = 0; b < B; ++b)
+        for (int r = 0; r < S.R; ++r) ident[(size_t)b * S.R + r] = r;
+    S.d_slot_state.upload(ident, st);
+    S.d_state_slot.upload(ident, st);
+    const int np = S.I * std::max(0, S.J - 1), nb = std::max(0, S.I - 1) * S.J;
+    S.d_acc_p.alloc((size_t)B * std::max(np, 1));
+    S.d_acc_b.alloc((size_t)B * std::max(nb, 1));
+    S.d_acc_p.zero(st);
+    S.d_acc_b.zero(st);
+    // records
+    const int flags = S.cfg.record_flags;
+    S.slots = (flags & TG_REC_GRID) ? S.R : 1;
+    const size_t per_round_states = (flags & (TG_REC_STATE | TG_REC_GRID)) ? (size_t)state_off * S.slots : 0;
+    int cap = 1024;
+    if (per_round_states) cap = (int)std::max<size_t>(1, std::min<size_t>(1024, (size_t)(256u << 20) / per_round_states));
+    S.rec_cap = cap;
+    S.d_rec.alloc((size_t)B * cap);
+    S.d_rec_acc.release();
+    if (flags & TG_REC_COUNTERS) S.d_rec_acc.alloc((size_t)B * cap * (np + nb + 1));
+    S.d_rec_states.release();
+    if (per_round_states) S.d_rec_states.alloc(per_round_states * cap);
+    S.h_rec.resize((size_t)B * cap);
+    S.h_acc.resize((flags & TG_REC_COUNTERS) ? (size_t)B * cap * (np + nb + 1) : 0);
+    S.h_states.resize(per_round_states * cap);
+    // cooperative grid
+    const void* fn = slot2_sweep_fn(S.D);
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSlot2Threads, 0));
+    if (per_sm < 1) fail(TG_ERR_RESOURCE, "slot engine: sweep kernel does not fit on an SM");
+    S.grid = per_sm * c.sms;
+    // initial configurations (engine.cpp:98-106)
+    S2Args a = s2_args(c);
+    slot2_init_kernel<<<dim3(c.sms * 4, B), 256, 0, st>>>(a, S.d_seeds.p);
+    CK(cudaGetLastError());
+    S.rounds_done = 0;
+    S.swap_base = 0;
+    S.ready = true;
+    CK(cudaStreamSynchronize(st));
+}
+
+void s2_drain(tg_ctx& c, int filled, int64_t first_round, const BatchSinkCtx& sink) {
+    Slot2& S = c.s2;
+    if (filled <= 0) return;
+    cudaStream_t st = c.stream;
+    const int B = S.B, cap = S.rec_cap, flags = S.cfg.record_flags;
+    const int np = S.I * std::max(0, S.J - 1), nb = std::max(0, S.I - 1) * S.J;
+    CK(cudaMemcpy2DAsync(S.h_rec.data(), sizeof(TgRecordDev) * cap, S.d_rec.p, sizeof(TgRecordDev) * cap,
+                         sizeof(TgRecordDev) * filled, B, cudaMemcpyDeviceToHost, st));
+    if (flags & TG_REC_COUNTERS)
+        CK(cudaMemcpy2DAsync(S.h_acc.data(), sizeof(int64_t) * cap * (np + nb), S.d_rec_acc.p,
+                             sizeof(int64_t) * cap * (np + nb), sizeof(int64_t) * filled * (np + nb), B,
+                             cudaMemcpyDeviceToHost, st));
+    if (S.d_rec_states.p) CK(cudaMemcpyAsync(S.h_states.data(), S.d_rec_states.p, S.h_states.size(),
+                                             cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!sink.fn) return;
+    for (int b = 0; b < B; ++b) {
+        const int n = S.prep[b].n;
+        const size_t per = (size_t)n * S.slots;
+        std::vector<tg_record> out;
+        std::vector<int8_t> outs;
+        std::vector<int64_t> oap, oab;
+        for (int k = 0; k < filled; ++k) {
+            const int64_t round = first_round + k;
+            if (round % S.cfg.record_every != 0) continue;
+            const TgRecordDev& d = S.h_rec[(size_t)b * cap + k];
+            tg_record r;
+            r.round = round;
+            r.sweep_count = round * S.cfg.sweeps_per_swap;
+            r.f = d.f; r.g = d.g; r.feasible = d.feasible; r.target_state = d.target_state;
+            r.digest = d.digest;
+            out.push_back(r);
+            if (S.d_rec_states.p) {
+                const int8_t* src = S.h_states.data() + (size_t)S.state_off[b] * S.slots * cap +
+                                    (size_t)k * per;
+                outs.insert(outs.end(), src, src + per);
+            }
+            if (flags & TG_REC_COUNTERS) {
+                const int64_t* src = S.h_acc.data() + ((size_t)b * cap + k) * (np + nb);
+                oap.insert(oap.end(), src, src + np);
+                oab.insert(oab.end(), src + np, src + np + nb);
+            }
+        }
+        if (out.empty()) continue;
+        const int rc = sink.fn(sink.user, b, out.data(), (int64_t)out.size(),
+                               S.d_rec_states.p ? outs.data() : nullptr,
+                               (flags & TG_REC_COUNTERS) ? oap.data() : nullptr,
+                               (flags & TG_REC_COUNTERS) ? oab.data() : nullptr);
+        if (rc) fail(TG_ERR_SINK, "record sink requested stop (instance %d)", b);
+    }
+}
+
+void s2_advance(tg_ctx& c, int64_t n_rounds, const BatchSinkCtx& sink) {
+    Slot2& S = c.s2;
+    if (!S.ready) fail(TG_ERR_CONFIG, "advance: batch not initialised");
+    cudaStream_t st = c.stream;
+    const int flags = S.cfg.record_flags;
+    const int sps = (int)S.cfg.sweeps_per_swap;
+    if (c.profiling && c.ev.size() < 2) {
+        for (auto e : c.ev) cudaEventDestroy(e);
+        c.ev.assign(2, nullptr);
+        for (auto& e : c.ev) CK(cudaEventCreate(&e));
+    }
+    S2Args a = s2_args(c);
+    S2Swap s = s2_swap(c);
+    double sweep_ms = 0.0;
+    int filled = 0;
+    int64_t first = S.rounds_done + 1;
+    for (int64_t k = 0; k < n_rounds; ++k) {
+        const int64_t round = S.rounds_done + 1;
+        int64_t t0 = (round - 1) * sps;
+        int nsw = sps, de = 1;
+        void* args[] = {&a, &t0, &nsw, &de};
+        if (c.profiling) CK(cudaEventRecord(c.ev[0], st));
+        CK(cudaLaunchCooperativeKernel(slot2_sweep_fn(S.D), dim3(S.grid), dim3(kSlot2Threads), args, 0, st));
+        if (c.profiling) CK(cudaEventRecord(c.ev[1], st));
+        c.sweep_launches++;
+        slot2_swap_kernel<<<S.B, kSwapThreads, 0, st>>>(s, round, S.swap_base, filled, flags);
+        CK(cudaGetLastError());
+        c.other_launches++;
+        if (flags & (TG_REC_DIGEST | TG_REC_STATE | TG_REC_GRID)) {
+            slot2_extract_kernel<<<dim3(std::max(1, c.sms / 2), S.B), 256, 0, st>>>(
+                a, s, filled, (flags & TG_REC_GRID) ? 1 : 0);
+            CK(cudaGetLastError());
+            c.other_launches++;
+        }
+        if (c.profiling && (k + 1 == n_rounds || (k & 63) == 63)) {
+            // sampled: one sweep launch in 64 (and the last) is timed, scaled to all
+            CK(cudaEventSynchronize(c.ev[1]));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));
+            const int64_t span = (k & 63) + 1;
+            sweep_ms += ms * (double)span;
+        }
+        S.swap_base += (uint64_t)round_attempts(S.I, S.J, round);
+        S.rounds_done = round;
+        if (++filled == S.rec_cap) {
+            s2_drain(c, filled, first, sink);
+            filled = 0;
+            first = S.rounds_done + 1;
+        }
+    }
+    s2_drain(c, filled, first, sink);
+    CK(cudaStreamSynchronize(st));
+    c.last_sweep_ms = sweep_ms;
+}
+
+
+void s2_get_state(tg_ctx& c, int b, int slot, int8_t* out) {
+    Slot2& S = c.s2;
+    if (!S.ready) fail(TG_ERR_CONFIG, "get_state: not initialised");
+    if (b < 0 || b >= S.B) fail(TG_ERR_CONFIG, "instance %d out of range", b);
+    if (slot < 0 || slot >= S.R) fail(TG_ERR_CONFIG, "get_state: slot %d out of range", slot);
+    int32_t m = 0;
+    CK(cudaMemcpyAsync(&m, S.d_slot_state.p + (size_t)b * S.R + slot, sizeof(int32_t),
+                       cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    const S2Prep& P = S.prep[b];
+    std::vector<int8_t> col(P.n);
+    long long off = 0;
+    for (int q = 0; q < b; ++q) off += (long long)S.prep[q].n * S.Rp;
+    CK(cudaMemcpy2DAsync(col.data(), 1, S.d_spins.p + off + m, S.Rp, 1, P.n, cudaMemcpyDeviceToHost,
+                         c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    for (int i = 0; i < P.n; ++i) out[P.order[i]] = col[i];
+}
+
+void s2_counters(tg_ctx& c, int b, int64_t* attempts_p, int64_t* accepts_p, int64_t* attempts_b,
+                 int64_t* accepts_b) {
+    Slot2& S = c.s2;
+    if (!S.ready) fail(TG_ERR_CONFIG, "get_counters: not initialised");
+    if (b < 0 || b >= S.B) fail(TG_ERR_CONFIG, "instance %d out of range", b);
+    const int np = S.I * std::max(0, S.J - 1), nb = std::max(0, S.I - 1) * S.J;
+    if (accepts_p && np)
+        CK(cudaMemcpyAsync(accepts_p, S.d_acc_p.p + (size_t)b * np, sizeof(int64_t) * np,
+                           cudaMemcpyDeviceToHost, c.stream));
+    if (accepts_b && nb)
+        CK(cudaMemcpyAsync(accepts_b, S.d_acc_b.p + (size_t)b * nb, sizeof(int64_t) * nb,
+                           cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    std::vector<int64_t> ap(np, 0), ab(nb, 0);
+    for (int64_t r = 1; r <= S.rounds_done; ++r) {
+        int even, dp, db;
+        round_phase(S.I, S.J, r, even, dp, db);
+        if (dp) for (int i = 0; i < S.I; ++i) for (int p = even; p + 1 < S.J; p += 2) ap[i * (S.J - 1) + p]++;
+        if (db) for (int j = 0; j < S.J; ++j) for (int q = even; q + 1 < S.I; q += 2) ab[q * S.J + j]++;
+    }
+    if (attempts_p) std::copy(ap.begin(), ap.end(), attempts_p);
+    if (attempts_b) std::copy(ab.begin(), ab.end(), attempts_b);
+}
+
+void s2_energies(tg_ctx& c, int b, double* f, double* g) {
+    Slot2& S = c.s2;
+    std::vector<double> fs(S.R), gs(S.R);
+    std::vector<int32_t> ss(S.R);
+    CK(cudaMemcpyAsync(fs.data(), S.d_f.p + (size_t)b * S.R, sizeof(double) * S.R, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(gs.data(), S.d_g.p + (size_t)b * S.R, sizeof(double) * S.R, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(ss.data(), S.d_slot_state.p + (size_t)b * S.R, sizeof(int32_t) * S.R,
+                       cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    for (int q = 0; q < S.R; ++q) {
+        if (f) f[q] = fs[ss[q]];
+        if (g) g[q] = gs[ss[q]];
+    }
+}
 }  // namespace
 
 // ================================================================ C ABI
@@ -1046,43 +1590,15 @@ int tg_set_problem(tg_ctx* ctx, int n, int n_couplings, const int32_t* ci, const
                    const int32_t* pb) {
     if (!ctx) return TG_ERR_CONFIG;
     return guard(ctx, [&] {
-        // IsingModel validation (ising.cpp:21-46) and ConstraintSet (constraints.cpp:16-26)
-        if (n <= 0) fail(TG_ERR_CONFIG, "model: n_spins must be positive");
-        if (n_couplings < 0 || n_pairs < 0) fail(TG_ERR_CONFIG, "model: negative counts");
-        std::vector<uint64_t> keys;
-        std::vector<int> a(n_couplings), b(n_couplings), qa(n_pairs), qb(n_pairs);
-        for (int k = 0; k < n_couplings; ++k) {
-            int x = ci[k], y = cj[k];
-            if (x == y) fail(TG_ERR_CONFIG, "model: self-loop on spin %d", x);
-            if (x > y) std::swap(x, y);
-            if (x < 0 || y >= n) fail(TG_ERR_CONFIG, "model: coupling index out of range: (%d, %d)", x, y);
-            if (!std::isfinite(w[k])) fail(TG_ERR_CONFIG, "model: coupling weights must be finite");
-            a[k] = x;
-            b[k] = y;
-            keys.push_back((uint64_t)x << 32 | (uint64_t)y);
-        }
-        std::sort(keys.begin(), keys.end());
-        for (size_t k = 1; k < keys.size(); ++k)
-            if (keys[k] == keys[k - 1])
-                fail(TG_ERR_CONFIG, "model: duplicate coupling (%d, %d)", (int)(keys[k] >> 32),
-                     (int)(keys[k] & 0xffffffffu));
-        for (int k = 0; k < n_pairs; ++k) {
-            int x = pa[k], y = pb[k];
-            if (x == y) fail(TG_ERR_CONFIG, "constraint: pair on a single spin %d", x);
-            if (x > y) std::swap(x, y);
-            if (x < 0 || y >= n) fail(TG_ERR_CONFIG, "constraint: index out of range: (%d, %d)", x, y);
-            qa[k] = x;
-            qb[k] = y;
-        }
-        ctx->n = n;
-        ctx->ci = a;
-        ctx->cj = b;
-        ctx->cw.assign(w, w + n_couplings);
-        ctx->h.assign(n, 0.0);
-        if (fields) for (int i = 0; i < n; ++i) ctx->h[i] = fields[i];
-        for (double x : ctx->h) if (!std::isfinite(x)) fail(TG_ERR_CONFIG, "model: fields must be finite");
-        ctx->pa = qa;
-        ctx->pb = qb;
+        BatchInst bi;
+        load_problem(bi, n, n_couplings, ci, cj, w, fields, n_pairs, pa, pb);
+        ctx->n = bi.n;
+        ctx->ci = bi.ci;
+        ctx->cj = bi.cj;
+        ctx->cw = bi.cw;
+        ctx->h = bi.h;
+        ctx->pa = bi.pa;
+        ctx->pb = bi.pb;
         canonical(n, ctx->ci, ctx->cj, ctx->pa, ctx->pb, ctx->order, ctx->color, ctx->n_colors);
         ctx->inv.assign(n, 0);
         for (int k = 0; k < n; ++k) ctx->inv[ctx->order[k]] = k;
@@ -1132,6 +1648,7 @@ int tg_get_state(tg_ctx* ctx, int slot, int8_t* out) {
     if (!ctx) return TG_ERR_CONFIG;
     return guard(ctx, [&] {
         tg_ctx& c = *ctx;
+        if (c.use_s2) { s2_get_state(c, 0, slot, out); return; }
         if (!c.initialised) fail(TG_ERR_CONFIG, "get_state: context not initialised");
         if (slot < 0 || slot >= c.R) fail(TG_ERR_CONFIG, "get_state: slot %d out of range", slot);
         // reuse the extract kernel on a one-slot view: temporarily point slot R-1 at `slot`
@@ -1170,6 +1687,7 @@ int tg_get_counters(tg_ctx* ctx, int64_t* attempts_p, int64_t* accepts_p, int64_
     if (!ctx) return TG_ERR_CONFIG;
     return guard(ctx, [&] {
         tg_ctx& c = *ctx;
+        if (c.use_s2) { s2_counters(c, 0, attempts_p, accepts_p, attempts_b, accepts_b); return; }
         if (!c.initialised) fail(TG_ERR_CONFIG, "get_counters: context not initialised");
         const int np = c.I * std::max(0, c.J - 1), nb = std::max(0, c.I - 1) * c.J;
         if (accepts_p && np) CK(cudaMemcpyAsync(accepts_p, c.d_acc_p.p, sizeof(int64_t) * np, cudaMemcpyDeviceToHost, c.stream));
@@ -1191,6 +1709,7 @@ int tg_get_energies(tg_ctx* ctx, double* f, double* g) {
     if (!ctx) return TG_ERR_CONFIG;
     return guard(ctx, [&] {
         tg_ctx& c = *ctx;
+        if (c.use_s2) { s2_energies(c, 0, f, g); return; }
         if (!c.initialised) fail(TG_ERR_CONFIG, "get_energies: context not initialised");
         std::vector<double> fs(c.R), gs(c.R);
         std::vector<int32_t> ss(c.R);
@@ -1228,6 +1747,63 @@ int tg_set_profiling(tg_ctx* ctx, int on) {
     if (!ctx) return TG_ERR_CONFIG;
     ctx->profiling = on != 0;
     return TG_OK;
+}
+
+int tg_batch_clear(tg_ctx* ctx) {
+    if (!ctx) return TG_ERR_CONFIG;
+    ctx->batch.clear();
+    ctx->s2.ready = false;
+    ctx->use_s2 = false;
+    return TG_OK;
+}
+
+int tg_batch_add(tg_ctx* ctx, int n, int n_couplings, const int32_t* ci, const int32_t* cj,
+                 const double* w, const double* fields, int n_pairs, const int32_t* pa,
+                 const int32_t* pb, int n_betas, const double* betas, int n_penalties,
+                 const double* penalties, uint64_t seed, int32_t* index) {
+    if (!ctx) return TG_ERR_CONFIG;
+    return guard(ctx, [&] {
+        BatchInst bi;
+        load_problem(bi, n, n_couplings, ci, cj, w, fields, n_pairs, pa, pb);
+        bi.betas.assign(betas, betas + std::max(n_betas, 0));
+        bi.pens.assign(penalties, penalties + std::max(n_penalties, 0));
+        check_vec(bi.betas, "beta");
+        check_vec(bi.pens, "penalty");
+        for (double x : bi.pens) if (x < 0.0) fail(TG_ERR_CONFIG, "build_effective: penalty must be >= 0");
+        bi.seed = seed;
+        ctx->batch.push_back(std::move(bi));
+        ctx->s2.ready = false;
+        if (index) *index = (int32_t)ctx->batch.size() - 1;
+    });
+}
+
+int tg_batch_run(tg_ctx* ctx, const tg_run_config* cfg, tg_batch_sink_fn sink, void* user) {
+    if (!ctx || !cfg) return TG_ERR_CONFIG;
+    return guard(ctx, [&] {
+        if (cfg->sweeps_per_swap < 1) fail(TG_ERR_CONFIG, "run: sweeps_per_swap must be >= 1");
+        if (cfg->total_sweeps < cfg->sweeps_per_swap)
+            fail(TG_ERR_CONFIG, "run: total_sweeps must be >= sweeps_per_swap");
+        if (cfg->rule != TG_RULE_METROPOLIS && cfg->rule != TG_RULE_HEAT_BATH)
+            fail(TG_ERR_CONFIG, "run: unknown update rule %d", cfg->rule);
+        if (cfg->engine != TG_ENGINE_AUTO && cfg->engine != TG_ENGINE_SLOT)
+            fail(TG_ERR_CONFIG, "batch: only the SLOT engine runs batches");
+        if (ctx->world != 1) fail(TG_ERR_CONFIG, "batch: single-GPU contexts only");
+        ctx->use_s2 = false;
+        ctx->initialised = false;
+        s2_build(*ctx, cfg);
+        s2_advance(*ctx, cfg->total_sweeps / cfg->sweeps_per_swap, BatchSinkCtx{sink, user});
+    });
+}
+
+int tg_batch_get_state(tg_ctx* ctx, int instance, int slot, int8_t* out) {
+    if (!ctx) return TG_ERR_CONFIG;
+    return guard(ctx, [&] { s2_get_state(*ctx, instance, slot, out); });
+}
+
+int tg_batch_get_counters(tg_ctx* ctx, int instance, int64_t* attempts_p, int64_t* accepts_p,
+                          int64_t* attempts_b, int64_t* accepts_b) {
+    if (!ctx) return TG_ERR_CONFIG;
+    return guard(ctx, [&] { s2_counters(*ctx, instance, attempts_p, accepts_p, attempts_b, accepts_b); });
 }
 
 int tg_canonical_order(int n, int n_couplings, const int32_t* ci, const int32_t* cj, int n_pairs,

@@ -157,6 +157,63 @@ struct SwapArgs {
     uint32_t* kpc;
 };
 
+// ------------------------------------------------- SLOT engine v2 (batched)
+
+struct SInst {              // one instance of a batch (device table)
+    int n, D, n_colors, color_off;
+    long long spin_off;     // into spins: n * Rp int8
+    int entp_off;           // into entp / wp: n * D
+    int csr_off;            // into off: n + 1
+    int nbr_off;            // into nbr / w / cm
+    int h_off;              // into h / h32 / perm (also the instance's site offset)
+    int chunk_off;          // into part_f / part_g rows: ceil(n / 32) chunks
+    int n_chunks;
+    int state_off;          // sum of n over earlier instances (record snapshots)
+    float eps, beta_max;    // FP32 fast-path error bound, max |beta|
+};
+
+struct S2Args {
+    int B, I, J, R, Rp, G, rule, max_colors;
+    const SInst* inst;
+    int8_t* spins;                 // [b][site][Rp]
+    const int2* entp;              // padded degree-D entries {j | cm<<28 | fwd<<27, float J}
+    const double* wp;              // padded FP64 J (energy)
+    const int* off;                // merged CSR per instance (FP64 fallback)
+    const int32_t* nbr;
+    const double* w;
+    const int8_t* cm;
+    const double* h;
+    const float* h32;
+    const int* color_start;        // per instance n_colors + 1
+    const int* item_pref;          // [max_colors][B+1] prefix sums of sweep-item upper bounds
+    const int* energy_pref;        // [B+1] prefix sums of energy items
+    const double* betas;           // [B][I]
+    const double* pens;            // [B][J]
+    const int32_t* state_slot;     // [B][R]
+    const uint64_t* slot_key;      // [B][R]
+    double* part_f;                // [sum chunks][Rp]
+    double* part_g;
+    double* f;                     // [B][R]
+    double* g;
+};
+
+struct S2Swap {
+    int R, I, J, rec_cap;
+    const double* betas;
+    const double* pens;
+    const double* f;
+    const double* g;
+    int32_t* slot_state;           // [B][R]
+    int32_t* state_slot;
+    int64_t* acc_p;                // [B][I(J-1)]
+    int64_t* acc_b;                // [B][(I-1)J]
+    const uint64_t* swap_seed;     // [B]
+    void* rec;                     // TgRecordDev [B][rec_cap]
+    int64_t* rec_acc;              // [B][rec_cap][np+nb]
+    int8_t* rec_states;            // snapshots, or null
+    const int32_t* perm;           // internal -> caller index, per instance (offset h_off)
+};
+
 // ---------------------------------------------------------------- swaps
 
 // Reference round schedule (engine.cpp:121-146,216): parity alternates every

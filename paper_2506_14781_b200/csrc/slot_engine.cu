@@ -1,0 +1,291 @@
+// slot_engine.cu -- SLOT engine v2: replica-fastest int8 layout, batched
+// instances, cooperative persistent sweep kernel.
+//
+// Restates metropolis_sweep (/root/reference/proj/src/mc.cpp:21-35) with the
+// reference's per-slot RNG association (engine.cpp:98-107): the update of
+// spin i in sweep t of the replica at grid slot r draws output t*N+i of
+// stream(derive_seed(seed, replica, r)).  Layout spins[b][site][Rp] (Rp = I*J
+// rounded up to 32): a warp updates one site of one instance for 32
+// replicas, so the site's neighbour list is a warp-uniform broadcast load and
+// each neighbour gather is one coalesced 32-byte sector.  Any number of
+// independent instances (config 3's batch) share one launch; every instance
+// keeps its own structure, schedule, seed, labels, counters and records, so a
+// batch equals independent run_2dpt calls instance by instance.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "engine.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tg {
+
+__device__ __forceinline__ int find_instance(const int* pref, int B, int item) {
+    int lo = 0, hi = B;  // pref[lo] <= item < pref[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (pref[mid] <= item) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// FP64 decision (the semantics all fast paths must reproduce): local field
+// in the reference's merged-CSR order (constraints.cpp:122-140, ising.cpp:79-88).
+__device__ __forceinline__ int8_t s2_exact(const S2Args& a, const SInst& in, const int8_t* sp, int i,
+                                           int r, int8_t si8, uint64_t u53, double beta,
+                                           double two_p) {
+    double local = a.h[in.h_off + i];
+    const int e0 = a.off[in.csr_off + i], e1 = a.off[in.csr_off + i + 1];
+    for (int e = e0; e < e1; ++e) {
+        const int q = in.nbr_off + e;
+        const double wgt = a.w[q] + (double)a.cm[q] * two_p;
+        local += wgt * (double)sp[(size_t)a.nbr[q] * a.Rp + r];
+    }
+    const double si = (double)si8;
+    const double u = (double)u53 * 0x1.0p-53;
+    if (a.rule == 0) {
+        const double de = 2.0 * si * local;
+        return (de <= 0.0 || u < exp(-beta * de)) ? (int8_t)-si8 : si8;
+    }
+    const double p = 1.0 / (1.0 + exp(-2.0 * beta * local));
+    return u < p ? (int8_t)1 : (int8_t)-1;
+}
+
+template <int D>
+__device__ __forceinline__ void s2_update(const S2Args& a, const SInst& in, int8_t* sp, int i, int r,
+                                          uint64_t u53, double beta, double two_p, float beta32,
+                                          float two_p32) {
+    const int2* ep = a.entp + in.entp_off + (size_t)i * D;
+    float l32 = __ldg(a.h32 + in.h_off + i);
+#pragma unroll
+    for (int k = 0; k < D; k += 2) {
+        const int4 v = __ldg(reinterpret_cast<const int4*>(ep + k));
+        const float w0 = __int_as_float(v.y) + (float)((v.x >> 28) & 15) * two_p32;
+        const float w1 = __int_as_float(v.w) + (float)((v.z >> 28) & 15) * two_p32;
+        l32 = fmaf(w0, (float)sp[(size_t)(v.x & 0x07ffffff) * a.Rp + r], l32);
+        l32 = fmaf(w1, (float)sp[(size_t)(v.z & 0x07ffffff) * a.Rp + r], l32);
+    }
+    int8_t* cell = sp + (size_t)i * a.Rp + r;
+    const int8_t si8 = *cell;
+    const float si = (float)si8;
+    const float uf = (float)u53 * 0x1.0p-53f;
+    const float eb = 2.0f * in.beta_max * in.eps;
+    // certified FP32 decision (error bounds as in kernels.cu slot_update_fast)
+    if (a.rule == 0) {
+        const float de32 = 2.0f * si * l32;
+        const float tol = 2.0f * in.eps;
+        if (de32 < -tol) { *cell = (int8_t)-si8; return; }
+        if (de32 > tol) {
+            const float x = -beta32 * de32;
+            const float T = __expf(x);
+            const float band = T * (2.0f * eb + fabsf(x) * 0x1.0p-19f + 0x1.0p-18f) + uf * 0x1.0p-22f;
+            if (uf < T - band) { *cell = (int8_t)-si8; return; }
+            if (uf > T + band) return;
+        }
+    } else {
+        const float y = 2.0f * beta32 * l32;
+        const float p = __frcp_rn(1.0f + __expf(-y));
+        const float band = eb + fabsf(y) * 0x1.0p-19f + 0x1.0p-18f + uf * 0x1.0p-22f;
+        if (uf < p - band) { *cell = 1; return; }
+        if (uf > p + band) { *cell = -1; return; }
+    }
+    *cell = s2_exact(a, in, sp, i, r, si8, u53, beta, two_p);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kSlot2Threads, 1)
+slot2_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, int do_energy) {
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
+    const int nw = gridDim.x * wpb;
+    for (int sw = 0; sw < n_sweeps; ++sw) {
+        const uint64_t t = (uint64_t)(t0 + sw);
+        for (int c = 0; c < a.max_colors; ++c) {
+            const int* pref = a.item_pref + (size_t)c * (a.B + 1);
+            const int total = pref[a.B];
+            for (int item = gw; item < total; item += nw) {
+                const int b = find_instance(pref, a.B, item);
+                const SInst& in = a.inst[b];
+                if (c >= in.n_colors) continue;
+                const int local = item - pref[b];
+                const int gi = local % a.G, qi = local / a.G;
+                const int cs = a.color_start[in.color_off + c], ce = a.color_start[in.color_off + c + 1];
+                if (ce <= cs) continue;
+                const uint64_t base = t * (uint64_t)in.n;
+                const uint64_t q = ((base + cs) >> 1) + (uint64_t)qi;
+                if (q > ((base + ce - 1) >> 1)) continue;
+                const int r = gi * 32 + lane;
+                if (r >= a.R) continue;
+                const int label = a.state_slot[b * a.R + r];
+                const double beta = a.betas[b * a.I + label / a.J];
+                const double two_p = 2.0 * a.pens[b * a.J + label % a.J];
+                const uint64_t key = a.slot_key[b * a.R + label];
+                const u32x4 o = philox4x32_10(u32x4{(uint32_t)q, (uint32_t)(q >> 32), 0u, 0u},
+                                              (uint32_t)key, (uint32_t)(key >> 32));
+                int8_t* sp = a.spins + in.spin_off;
+                const int64_t i0 = (int64_t)(2 * q - base);
+                if (i0 >= cs && i0 < ce)
+                    s2_update<D>(a, in, sp, (int)i0, r, ((uint64_t)o.x | ((uint64_t)o.y << 32)) >> 11,
+                                 beta, two_p, (float)beta, (float)two_p);
+                if (i0 + 1 >= cs && i0 + 1 < ce)
+                    s2_update<D>(a, in, sp, (int)i0 + 1, r, ((uint64_t)o.z | ((uint64_t)o.w << 32)) >> 11,
+                                 beta, two_p, (float)beta, (float)two_p);
+            }
+            grid.sync();
+        }
+    }
+    if (!do_energy) return;
+    // (f, g) per replica: deterministic two-stage sums (per 32-site chunk, then
+    // chunks in order) -- f = -sum_{i<j} J s_i s_j - sum h s, g = sum cm (s_i - s_j)^2
+    {
+        const int total = a.energy_pref[a.B];
+        for (int item = gw; item < total; item += nw) {
+            const int b = find_instance(a.energy_pref, a.B, item);
+            const SInst& in = a.inst[b];
+            const int local = item - a.energy_pref[b];
+            const int gi = local % a.G, ch = local / a.G;
+            const int r = gi * 32 + lane;
+            if (r >= a.R) continue;
+            const int8_t* sp = a.spins + in.spin_off;
+            double fl = 0.0, gl = 0.0;
+            const int i1 = min(in.n, (ch + 1) * 32);
+            for (int i = ch * 32; i < i1; ++i) {
+                const double si = (double)sp[(size_t)i * a.Rp + r];
+                fl -= a.h[in.h_off + i] * si;
+                const int2* ep = a.entp + in.entp_off + (size_t)i * D;
+                const double* wp = a.wp + in.entp_off + (size_t)i * D;
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    const int2 v = __ldg(ep + k);
+                    if ((v.x >> 27) & 1) {
+                        const double sj = (double)sp[(size_t)(v.x & 0x07ffffff) * a.Rp + r];
+                        fl -= __ldg(wp + k) * si * sj;
+                        const double d = si - sj;
+                        gl += (double)((v.x >> 28) & 15) * d * d;
+                    }
+                }
+            }
+            a.part_f[(size_t)(in.chunk_off + ch) * a.Rp + r] = fl;
+            a.part_g[(size_t)(in.chunk_off + ch) * a.Rp + r] = gl;
+        }
+    }
+    grid.sync();
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < a.B * a.R;
+         idx += gridDim.x * blockDim.x) {
+        const int b = idx / a.R, r = idx % a.R;
+        const SInst& in = a.inst[b];
+        double F = 0.0, G = 0.0;
+        for (int ch = 0; ch < in.n_chunks; ++ch) {
+            F += a.part_f[(size_t)(in.chunk_off + ch) * a.Rp + r];
+            G += a.part_g[(size_t)(in.chunk_off + ch) * a.Rp + r];
+        }
+        a.f[idx] = F;
+        a.g[idx] = G;
+    }
+}
+
+template __global__ void slot2_sweep_kernel<4>(const __grid_constant__ S2Args, int64_t, int, int);
+template __global__ void slot2_sweep_kernel<8>(const __grid_constant__ S2Args, int64_t, int, int);
+template __global__ void slot2_sweep_kernel<16>(const __grid_constant__ S2Args, int64_t, int, int);
+
+void* slot2_sweep_fn(int D) {
+    return D <= 4 ? (void*)slot2_sweep_kernel<4>
+                  : (D <= 8 ? (void*)slot2_sweep_kernel<8> : (void*)slot2_sweep_kernel<16>);
+}
+
+// One block per instance: that instance's swap phase, record and counters.
+__global__ void __launch_bounds__(kSwapThreads)
+slot2_swap_kernel(const __grid_constant__ S2Swap s, int64_t round, uint64_t swap_base, int rec_idx,
+                  int rec_flags) {
+    const int b = blockIdx.x;
+    const int R = s.R, I = s.I, J = s.J;
+    const int np = I * (J > 1 ? J - 1 : 0), nb = (I > 1 ? I - 1 : 0) * J;
+    int32_t* slot_state = s.slot_state + b * R;
+    int32_t* state_slot = s.state_slot + b * R;
+    const double* f = s.f + b * R;
+    const double* g = s.g + b * R;
+    int64_t* acc_p = s.acc_p + (size_t)b * np;
+    int64_t* acc_b = s.acc_b + (size_t)b * nb;
+    const int64_t n_att = round_attempts(I, J, round);
+    for (int k = threadIdx.x; k < n_att; k += blockDim.x) {
+        int sa, sb, ctr, is_p;
+        if (swap_attempt(I, J, s.betas + b * I, s.pens + b * J, round, k, f, g, slot_state,
+                         s.swap_seed[b], swap_base, sa, sb, ctr, is_p)) {
+            const int xa = slot_state[sa], xb = slot_state[sb];
+            slot_state[sa] = xb;
+            slot_state[sb] = xa;
+            state_slot[xb] = sa;
+            state_slot[xa] = sb;
+            if (is_p) acc_p[ctr] += 1; else acc_b[ctr] += 1;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        TgRecordDev* rec = reinterpret_cast<TgRecordDev*>(s.rec) + (size_t)b * s.rec_cap + rec_idx;
+        const int tgt = slot_state[R - 1];
+        rec->round = round;
+        rec->f = f[tgt];
+        rec->g = g[tgt];
+        rec->feasible = g[tgt] == 0.0 ? 1 : 0;
+        rec->target_state = tgt;
+        rec->digest = 0ull;
+    }
+    if ((rec_flags & 8) && s.rec_acc) {
+        int64_t* dst = s.rec_acc + ((size_t)b * s.rec_cap + rec_idx) * (np + nb);
+        for (int k = threadIdx.x; k < np; k += blockDim.x) dst[k] = acc_p[k];
+        for (int k = threadIdx.x; k < nb; k += blockDim.x) dst[np + k] = acc_b[k];
+    }
+}
+
+// Target-state digest / snapshot (or every slot) per instance, caller order.
+__global__ void slot2_extract_kernel(const __grid_constant__ S2Args a, const __grid_constant__ S2Swap s,
+                                     int rec_idx, int all_slots) {
+    const int b = blockIdx.y;
+    const SInst& in = a.inst[b];
+    const int slots = all_slots ? a.R : 1;
+    const long long total = (long long)slots * in.n;
+    uint64_t dsum = 0;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+         q += (long long)gridDim.x * blockDim.x) {
+        const int sl = all_slots ? (int)(q / in.n) : a.R - 1;
+        const int i = (int)(q % in.n);
+        const int m = s.slot_state[b * a.R + sl];
+        const int8_t v = a.spins[in.spin_off + (size_t)i * a.Rp + m];
+        const int ci = s.perm[in.h_off + i];
+        if (s.rec_states) {
+            int8_t* dst = s.rec_states + (size_t)in.state_off * slots * s.rec_cap +
+                          (size_t)rec_idx * in.n * slots;
+            dst[(size_t)(all_slots ? sl : 0) * in.n + ci] = v;
+        }
+        if (!all_slots && v > 0) dsum += digest_term((uint64_t)ci);
+    }
+    if (s.rec && !all_slots) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+        if ((threadIdx.x & 31) == 0 && dsum) {
+            TgRecordDev* rec = reinterpret_cast<TgRecordDev*>(s.rec) + (size_t)b * s.rec_cap + rec_idx;
+            atomicAdd(reinterpret_cast<unsigned long long*>(&rec->digest), (unsigned long long)dsum);
+        }
+    }
+}
+
+__global__ void slot2_init_kernel(const __grid_constant__ S2Args a, const uint64_t* seeds) {
+    const int b = blockIdx.y;
+    const SInst& in = a.inst[b];
+    const long long total = (long long)in.n * a.Rp;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+         q += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(q / a.Rp), m = (int)(q % a.Rp);
+        int8_t v = 1;
+        if (m < a.R) {  // random_state with the init stream of replica m (engine.cpp:100-101)
+            const uint64_t key = derive_seed(seeds[b], kPurposeInit, (uint64_t)m);
+            v = (stream_bits(key, (uint64_t)i) >> 63) ? (int8_t)1 : (int8_t)-1;
+        }
+        a.spins[in.spin_off + q] = v;
+    }
+}
+
+}  // namespace tg
