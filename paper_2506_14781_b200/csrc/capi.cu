@@ -150,9 +150,11 @@ struct S2Prep {
 
 struct Slot2 {
     int B = 0, I = 0, J = 0, R = 0, Rp = 0, G = 0, D = 4, max_colors = 0, slots = 1;
-    int rec_cap = 0, grid = 0;
+    int rec_cap = 0, grid = 0, nsub = 1;
     tg_run_config cfg{};
     std::vector<S2Prep> prep;
+    DBuf<double> d_sbeta, d_stwop;
+    DBuf<uint64_t> d_skey;
     std::vector<int> state_off;
     DBuf<SInst> d_inst;
     DBuf<int2> d_entp;
@@ -1184,6 +1186,7 @@ S2Args s2_args(tg_ctx& c) {
     a.betas = S.d_betas.p; a.pens = S.d_pens.p; a.state_slot = S.d_state_slot.p;
     a.slot_key = S.d_keys.p; a.part_f = S.d_part_f.p; a.part_g = S.d_part_g.p;
     a.f = S.d_f.p; a.g = S.d_g.p;
+    a.sbeta = S.d_sbeta.p; a.stwop = S.d_stwop.p; a.skey = S.d_skey.p; a.nsub = S.nsub;
     return a;
 }
 
@@ -1196,6 +1199,8 @@ S2Swap s2_swap(tg_ctx& c) {
     s.acc_p = S.d_acc_p.p; s.acc_b = S.d_acc_b.p; s.swap_seed = S.d_swap_seed.p;
     s.rec = S.d_rec.p; s.rec_acc = S.d_rec_acc.p; s.rec_states = S.d_rec_states.p;
     s.perm = S.d_perm.p;
+    s.sbeta = S.d_sbeta.p; s.stwop = S.d_stwop.p; s.skey = S.d_skey.p;
+    s.slot_key = S.d_keys.p; s.Rp = S.Rp;
     return s;
 }
 
@@ -1282,7 +1287,7 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
             const S2Prep& P = S.prep[b];
             const int len = col < P.n_colors ? P.color_start[col + 1] - P.color_start[col] : 0;
             const int ub = len > 0 ? (len + 3) / 2 : 0;
-            item_pref[(size_t)col * (B + 1) + b + 1] = item_pref[(size_t)col * (B + 1) + b] + ub * S.G;
+            item_pref[(size_t)col * (B + 1) + b + 1] = item_pref[(size_t)col * (B + 1) + b] + ub;
         }
     for (int b = 0; b < B; ++b) energy_pref[b + 1] = energy_pref[b] + inst[b].n_chunks * S.G;
     S.d_inst.upload(inst, st);
@@ -1304,8 +1309,46 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
     S.d_seeds.upload(seeds, st);
     S.d_perm.upload(perm, st);
     S.d_spins.alloc((size_t)spin_off);
-    S.d_part_f.alloc((size_t)chunk_off * S.Rp);
-    S.d_part_g.alloc((size_t)chunk_off * S.Rp);
+    // cooperative grid: whole warps per replica group
+    {
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, slot2_sweep_fn(S.D), kSlot2Threads, 0));
+        if (per_sm < 1) fail(TG_ERR_RESOURCE, "slot engine: sweep kernel does not fit on an SM");
+        int blocks = per_sm * c.sms;
+        const int wpb = kSlot2Threads / 32;
+        // no more warps than the widest colour phase can use (small instances)
+        long long need = 0;
+        for (int col = 0; col < max_colors; ++col)
+            need = std::max<long long>(need, (long long)item_pref[(size_t)col * (B + 1) + B] * S.G);
+        need = std::max<long long>(need, (long long)B * S.R);  // energy reduction: one warp per replica
+        blocks = (int)std::min<long long>(blocks, (need + wpb - 1) / wpb);
+        blocks = std::max(blocks, 1);
+        while (blocks > 1 && (blocks * wpb) % S.G != 0) --blocks;
+        if ((blocks * wpb) % S.G != 0) {  // round up instead (still co-resident if under the limit)
+            blocks = (S.G + wpb - 1) / wpb * wpb / wpb;
+            while ((blocks * wpb) % S.G != 0) ++blocks;
+            if (blocks > per_sm * c.sms) fail(TG_ERR_RESOURCE, "slot engine: cannot tile %d replica groups", S.G);
+        }
+        S.grid = blocks;
+        S.nsub = blocks * wpb / S.G;
+    }
+    S.d_part_f.alloc((size_t)B * S.nsub * S.Rp);
+    S.d_part_g.alloc((size_t)B * S.nsub * S.Rp);
+    S.d_part_f.zero(st);
+    S.d_part_g.zero(st);
+    {
+        std::vector<double> sb((size_t)B * S.Rp, 0.0), stp((size_t)B * S.Rp, 0.0);
+        std::vector<uint64_t> sk((size_t)B * S.Rp, 0);
+        for (int b = 0; b < B; ++b)
+            for (int r = 0; r < S.R; ++r) {
+                sb[(size_t)b * S.Rp + r] = c.batch[b].betas[r / S.J];
+                stp[(size_t)b * S.Rp + r] = 2.0 * c.batch[b].pens[r % S.J];
+                sk[(size_t)b * S.Rp + r] = keys[(size_t)b * S.R + r];
+            }
+        S.d_sbeta.upload(sb, st);
+        S.d_stwop.upload(stp, st);
+        S.d_skey.upload(sk, st);
+    }
     S.d_f.alloc((size_t)B * S.R);
     S.d_g.alloc((size_t)B * S.R);
     std::vector<int32_t> ident((size_t)B * S.R);
@@ -1333,12 +1376,6 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
     S.h_rec.resize((size_t)B * cap);
     S.h_acc.resize((flags & TG_REC_COUNTERS) ? (size_t)B * cap * (np + nb + 1) : 0);
     S.h_states.resize(per_round_states * cap);
-    // cooperative grid
-    const void* fn = slot2_sweep_fn(S.D);
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSlot2Threads, 0));
-    if (per_sm < 1) fail(TG_ERR_RESOURCE, "slot engine: sweep kernel does not fit on an SM");
-    S.grid = per_sm * c.sms;
     // initial configurations (engine.cpp:98-106)
     S2Args a = s2_args(c);
     slot2_init_kernel<<<dim3(c.sms * 4, B), 256, 0, st>>>(a, S.d_seeds.p);

@@ -191,10 +191,14 @@ struct S2Args {
     const double* pens;            // [B][J]
     const int32_t* state_slot;     // [B][R]
     const uint64_t* slot_key;      // [B][R]
-    double* part_f;                // [sum chunks][Rp]
+    double* part_f;                // [B][nsub][Rp] per-warp energy partials (fixed order)
     double* part_g;
     double* f;                     // [B][R]
     double* g;
+    const double* sbeta;           // [B][Rp] beta of the slot each physical replica occupies
+    const double* stwop;           // [B][Rp] 2P of that slot
+    const uint64_t* skey;          // [B][Rp] Philox key of that slot's stream
+    int nsub;                      // warps per replica group
 };
 
 struct S2Swap {
@@ -212,6 +216,11 @@ struct S2Swap {
     int64_t* rec_acc;              // [B][rec_cap][np+nb]
     int8_t* rec_states;            // snapshots, or null
     const int32_t* perm;           // internal -> caller index, per instance (offset h_off)
+    double* sbeta;                 // per-state label tables refreshed after the swaps
+    double* stwop;
+    uint64_t* skey;
+    const uint64_t* slot_key;      // [B][R]
+    int Rp;
 };
 
 // ---------------------------------------------------------------- swaps

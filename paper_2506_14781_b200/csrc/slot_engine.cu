@@ -52,138 +52,166 @@ __device__ __forceinline__ int8_t s2_exact(const S2Args& a, const SInst& in, con
     return u < p ? (int8_t)1 : (int8_t)-1;
 }
 
+// One update of spin i for replica r: certified FP32 decision with FP64
+// fallback (error bounds as in kernels.cu slot_update_fast).  Returns the new
+// spin; on the counting sweep adds the bonds to lower-colour neighbours to
+// (fl, gl) (each edge once, at its higher-colour endpoint).
 template <int D>
 __device__ __forceinline__ void s2_update(const S2Args& a, const SInst& in, int8_t* sp, int i, int r,
                                           uint64_t u53, double beta, double two_p, float beta32,
-                                          float two_p32) {
-    const int2* ep = a.entp + in.entp_off + (size_t)i * D;
+                                          float two_p32, bool count, int lower, double& fl,
+                                          double& gl) {
+    const int2* ep = a.entp + in.entp_off + i * D;
+    const unsigned Rp = (unsigned)a.Rp;
+    int4 v[D / 2];
+#pragma unroll
+    for (int k = 0; k < D / 2; ++k) v[k] = __ldg(reinterpret_cast<const int4*>(ep) + k);
+    int8_t sn[D];
+#pragma unroll
+    for (int k = 0; k < D / 2; ++k) {
+        sn[2 * k] = sp[(unsigned)(v[k].x & 0x07ffffff) * Rp + r];
+        sn[2 * k + 1] = sp[(unsigned)(v[k].z & 0x07ffffff) * Rp + r];
+    }
     float l32 = __ldg(a.h32 + in.h_off + i);
 #pragma unroll
-    for (int k = 0; k < D; k += 2) {
-        const int4 v = __ldg(reinterpret_cast<const int4*>(ep + k));
-        const float w0 = __int_as_float(v.y) + (float)((v.x >> 28) & 15) * two_p32;
-        const float w1 = __int_as_float(v.w) + (float)((v.z >> 28) & 15) * two_p32;
-        l32 = fmaf(w0, (float)sp[(size_t)(v.x & 0x07ffffff) * a.Rp + r], l32);
-        l32 = fmaf(w1, (float)sp[(size_t)(v.z & 0x07ffffff) * a.Rp + r], l32);
+    for (int k = 0; k < D / 2; ++k) {
+        const float w0 = __int_as_float(v[k].y) + (float)((v[k].x >> 28) & 15) * two_p32;
+        const float w1 = __int_as_float(v[k].w) + (float)((v[k].z >> 28) & 15) * two_p32;
+        l32 = fmaf(w0, (float)sn[2 * k], l32);
+        l32 = fmaf(w1, (float)sn[2 * k + 1], l32);
     }
-    int8_t* cell = sp + (size_t)i * a.Rp + r;
+    int8_t* cell = sp + (unsigned)i * Rp + r;
     const int8_t si8 = *cell;
     const float si = (float)si8;
     const float uf = (float)u53 * 0x1.0p-53f;
     const float eb = 2.0f * in.beta_max * in.eps;
-    // certified FP32 decision (error bounds as in kernels.cu slot_update_fast)
+    int decided = 0;  // 1: take, -1: keep / set -1, 2: set +1 (heat bath)
+    int8_t nv = si8;
     if (a.rule == 0) {
         const float de32 = 2.0f * si * l32;
         const float tol = 2.0f * in.eps;
-        if (de32 < -tol) { *cell = (int8_t)-si8; return; }
-        if (de32 > tol) {
+        if (de32 < -tol) { nv = (int8_t)-si8; decided = 1; }
+        else if (de32 > tol) {
             const float x = -beta32 * de32;
             const float T = __expf(x);
             const float band = T * (2.0f * eb + fabsf(x) * 0x1.0p-19f + 0x1.0p-18f) + uf * 0x1.0p-22f;
-            if (uf < T - band) { *cell = (int8_t)-si8; return; }
-            if (uf > T + band) return;
+            if (uf < T - band) { nv = (int8_t)-si8; decided = 1; }
+            else if (uf > T + band) decided = 1;
         }
     } else {
         const float y = 2.0f * beta32 * l32;
         const float p = __frcp_rn(1.0f + __expf(-y));
         const float band = eb + fabsf(y) * 0x1.0p-19f + 0x1.0p-18f + uf * 0x1.0p-22f;
-        if (uf < p - band) { *cell = 1; return; }
-        if (uf > p + band) { *cell = -1; return; }
+        if (uf < p - band) { nv = 1; decided = 1; }
+        else if (uf > p + band) { nv = -1; decided = 1; }
     }
-    *cell = s2_exact(a, in, sp, i, r, si8, u53, beta, two_p);
+    if (!decided) nv = s2_exact(a, in, sp, i, r, si8, u53, beta, two_p);
+    if (nv != si8) *cell = nv;
+    if (count) {
+        const double sv = (double)nv;
+        fl -= a.h[in.h_off + i] * sv;
+        const double* wp = a.wp + in.entp_off + i * D;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const int x = (k & 1) ? v[k >> 1].z : v[k >> 1].x;
+            const int j = x & 0x07ffffff;
+            if (j < lower) {
+                const double sj = (double)sn[k];
+                fl -= __ldg(wp + k) * sv * sj;
+                const double d = sv - sj;
+                gl += (double)((x >> 28) & 15) * d * d;
+            }
+        }
+    }
 }
 
+// Persistent cooperative kernel: the sweeps of one round for every instance
+// of the batch.  Each warp keeps one replica group (its lanes = replicas
+// 32*gi .. 32*gi+31 of every instance), so a lane's slot label, beta, 2P and
+// stream key are loaded once per instance instead of per update.
 template <int D>
-__global__ void __launch_bounds__(kSlot2Threads, 1)
+__global__ void __launch_bounds__(kSlot2Threads, 2)
 slot2_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, int do_energy) {
     cg::grid_group grid = cg::this_grid();
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
-    const int nw = gridDim.x * wpb;
-    for (int sw = 0; sw < n_sweeps; ++sw) {
-        const uint64_t t = (uint64_t)(t0 + sw);
+    const int gi = gw % a.G;           // replica group of this warp (host: warps % G == 0)
+    const int sw = gw / a.G, nsub = a.nsub;
+    const int r = gi * 32 + lane;
+    const bool live = r < a.R;
+    for (int swp = 0; swp < n_sweeps; ++swp) {
+        const uint64_t t = (uint64_t)(t0 + swp);
+        const bool count = do_energy && swp == n_sweeps - 1;
+        int cur_b = -1;
+        double beta = 0.0, two_p = 0.0;
+        uint64_t key = 0;
+        double fl = 0.0, gl = 0.0;
         for (int c = 0; c < a.max_colors; ++c) {
             const int* pref = a.item_pref + (size_t)c * (a.B + 1);
             const int total = pref[a.B];
-            for (int item = gw; item < total; item += nw) {
+            for (int item = sw; item < total; item += nsub) {
                 const int b = find_instance(pref, a.B, item);
                 const SInst& in = a.inst[b];
+                if (b != cur_b) {
+                    if (count && cur_b >= 0) {  // flush the previous instance's partial sums
+                        a.part_f[((size_t)cur_b * nsub + sw) * a.Rp + r] += fl;
+                        a.part_g[((size_t)cur_b * nsub + sw) * a.Rp + r] += gl;
+                        fl = 0.0; gl = 0.0;
+                    }
+                    cur_b = b;
+                    beta = a.sbeta[(size_t)b * a.Rp + r];
+                    two_p = a.stwop[(size_t)b * a.Rp + r];
+                    key = a.skey[(size_t)b * a.Rp + r];
+                }
                 if (c >= in.n_colors) continue;
-                const int local = item - pref[b];
-                const int gi = local % a.G, qi = local / a.G;
                 const int cs = a.color_start[in.color_off + c], ce = a.color_start[in.color_off + c + 1];
                 if (ce <= cs) continue;
                 const uint64_t base = t * (uint64_t)in.n;
-                const uint64_t q = ((base + cs) >> 1) + (uint64_t)qi;
-                if (q > ((base + ce - 1) >> 1)) continue;
-                const int r = gi * 32 + lane;
-                if (r >= a.R) continue;
-                const int label = a.state_slot[b * a.R + r];
-                const double beta = a.betas[b * a.I + label / a.J];
-                const double two_p = 2.0 * a.pens[b * a.J + label % a.J];
-                const uint64_t key = a.slot_key[b * a.R + label];
+                const uint64_t q = ((base + cs) >> 1) + (uint64_t)(item - pref[b]);
+                if (q > ((base + ce - 1) >> 1) || !live) continue;
                 const u32x4 o = philox4x32_10(u32x4{(uint32_t)q, (uint32_t)(q >> 32), 0u, 0u},
                                               (uint32_t)key, (uint32_t)(key >> 32));
                 int8_t* sp = a.spins + in.spin_off;
                 const int64_t i0 = (int64_t)(2 * q - base);
                 if (i0 >= cs && i0 < ce)
                     s2_update<D>(a, in, sp, (int)i0, r, ((uint64_t)o.x | ((uint64_t)o.y << 32)) >> 11,
-                                 beta, two_p, (float)beta, (float)two_p);
+                                 beta, two_p, (float)beta, (float)two_p, count, cs, fl, gl);
                 if (i0 + 1 >= cs && i0 + 1 < ce)
                     s2_update<D>(a, in, sp, (int)i0 + 1, r, ((uint64_t)o.z | ((uint64_t)o.w << 32)) >> 11,
-                                 beta, two_p, (float)beta, (float)two_p);
+                                 beta, two_p, (float)beta, (float)two_p, count, cs, fl, gl);
             }
             grid.sync();
         }
+        if (count && cur_b >= 0) {
+            a.part_f[((size_t)cur_b * nsub + sw) * a.Rp + r] += fl;
+            a.part_g[((size_t)cur_b * nsub + sw) * a.Rp + r] += gl;
+        }
     }
     if (!do_energy) return;
-    // (f, g) per replica: deterministic two-stage sums (per 32-site chunk, then
-    // chunks in order) -- f = -sum_{i<j} J s_i s_j - sum h s, g = sum cm (s_i - s_j)^2
-    {
-        const int total = a.energy_pref[a.B];
-        for (int item = gw; item < total; item += nw) {
-            const int b = find_instance(a.energy_pref, a.B, item);
-            const SInst& in = a.inst[b];
-            const int local = item - a.energy_pref[b];
-            const int gi = local % a.G, ch = local / a.G;
-            const int r = gi * 32 + lane;
-            if (r >= a.R) continue;
-            const int8_t* sp = a.spins + in.spin_off;
-            double fl = 0.0, gl = 0.0;
-            const int i1 = min(in.n, (ch + 1) * 32);
-            for (int i = ch * 32; i < i1; ++i) {
-                const double si = (double)sp[(size_t)i * a.Rp + r];
-                fl -= a.h[in.h_off + i] * si;
-                const int2* ep = a.entp + in.entp_off + (size_t)i * D;
-                const double* wp = a.wp + in.entp_off + (size_t)i * D;
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    const int2 v = __ldg(ep + k);
-                    if ((v.x >> 27) & 1) {
-                        const double sj = (double)sp[(size_t)(v.x & 0x07ffffff) * a.Rp + r];
-                        fl -= __ldg(wp + k) * si * sj;
-                        const double d = si - sj;
-                        gl += (double)((v.x >> 28) & 15) * d * d;
-                    }
-                }
-            }
-            a.part_f[(size_t)(in.chunk_off + ch) * a.Rp + r] = fl;
-            a.part_g[(size_t)(in.chunk_off + ch) * a.Rp + r] = gl;
-        }
-    }
     grid.sync();
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < a.B * a.R;
-         idx += gridDim.x * blockDim.x) {
-        const int b = idx / a.R, r = idx % a.R;
-        const SInst& in = a.inst[b];
+    // fixed-order reduction of the per-warp partials (one warp per replica,
+    // lanes take strided partials, then a fixed shuffle tree); clears them
+    for (int idx = gw; idx < a.B * a.R; idx += gridDim.x * (blockDim.x >> 5)) {
+        const int b = idx / a.R, rr = idx % a.R;
         double F = 0.0, G = 0.0;
-        for (int ch = 0; ch < in.n_chunks; ++ch) {
-            F += a.part_f[(size_t)(in.chunk_off + ch) * a.Rp + r];
-            G += a.part_g[(size_t)(in.chunk_off + ch) * a.Rp + r];
+        for (int q = lane; q < nsub; q += 32) {
+            double* pf = a.part_f + ((size_t)b * nsub + q) * a.Rp + rr;
+            double* pg = a.part_g + ((size_t)b * nsub + q) * a.Rp + rr;
+            F += *pf;
+            G += *pg;
+            *pf = 0.0;
+            *pg = 0.0;
         }
-        a.f[idx] = F;
-        a.g[idx] = G;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            F += __shfl_xor_sync(0xffffffffu, F, o);
+            G += __shfl_xor_sync(0xffffffffu, G, o);
+        }
+        if (lane == 0) {
+            a.f[idx] = F;
+            a.g[idx] = G;
+        }
     }
 }
 
@@ -223,6 +251,12 @@ slot2_swap_kernel(const __grid_constant__ S2Swap s, int64_t round, uint64_t swap
         }
     }
     __syncthreads();
+    for (int m = threadIdx.x; m < R; m += blockDim.x) {  // label tables of each physical replica
+        const int sl = state_slot[m];
+        s.sbeta[(size_t)b * s.Rp + m] = s.betas[b * I + sl / J];
+        s.stwop[(size_t)b * s.Rp + m] = 2.0 * s.pens[b * J + sl % J];
+        s.skey[(size_t)b * s.Rp + m] = s.slot_key[(size_t)b * R + sl];
+    }
     if (threadIdx.x == 0) {
         TgRecordDev* rec = reinterpret_cast<TgRecordDev*>(s.rec) + (size_t)b * s.rec_cap + rec_idx;
         const int tgt = slot_state[R - 1];
