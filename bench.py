@@ -50,7 +50,7 @@ def parse():
                     help="c5: config 5 (the metric's config, default); c2/c4: Wishart float32 "
                          "configs on the slot engine")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sweeps", type=int, default=2, help="marginal sweeps of the CPU sample")
+    ap.add_argument("--cpu-sweeps", type=int, default=16, help="marginal sweeps of the CPU sample")
     return ap.parse_args()
 
 
@@ -294,6 +294,8 @@ def run_ours(args, rank, world, local):
     smem_peak_gbs = 148 * 128 * sm_max * 1e6 / 1e9  # SURVEY.md §8d official smem roofline
     achieved_gbs = bytes_per_launch / mean_sweep_s / 1e9
     clocks = clk.summary()
+    kname = dominant_kernel(args, world)
+    traffic = ncu_traffic(kname, args, pr, R, sweeps / max(n_sweep_launches, 1))
     eng.close()
 
     # e2e: the public API with host buffers -- H2D of the instance, init, the
@@ -327,7 +329,7 @@ def run_ours(args, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         rate, kind, dt = cpu_reference_rate(pr, betas, pens, args.cpu_sweeps, threads)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
+        cpu = {"value": rate, "unit": UNIT, "cores": threads if kind == "reference" else 1, "kind": kind,
                "sample": f"unmodified reference run_2dpt (mt19937_64, Metropolis, FP64) on the "
                          f"same N={pr.n} instance and 16x16 grid; marginal rate of "
                          f"{1 + args.cpu_sweeps} vs 1 sweeps ({dt:.1f} s of sweeping)"}
@@ -344,8 +346,10 @@ def run_ours(args, rank, world, local):
                        "engine": args.engine, "parallelism": f"replica-split x{world}",
                        "l2": "flushed between timed steps (256 MB write)"},
             "roofline": {"bound": "smem", "achieved": achieved_gbs, "peak": smem_peak_gbs,
-                         "unit": "GB/s", "frac": achieved_gbs / smem_peak_gbs, "traffic": None,
-                         "kernel": "plane_sweep_kernel",
+                         "unit": "GB/s", "frac": achieved_gbs / smem_peak_gbs,
+                         "traffic": traffic["bytes_per_launch"] if traffic else None,
+                         "traffic_source": traffic["source"] if traffic else None,
+                         "kernel": kname,
                          "bytes_per_update": bal,
                          "mean_launch_ms": mean_sweep_s * 1e3,
                          "peak_note": "148 SM x 128 B/clk x sm_max_mhz (MEASURED_PEAKS.json), "
@@ -356,6 +360,32 @@ def run_ours(args, rank, world, local):
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
+
+
+def dominant_kernel(args, world):
+    if args.engine == "slot":
+        return "slot2_sweep_kernel" if world == 1 else "slot_sweep_kernel"
+    return "plane_rounds_kernel" if world == 1 else "plane_sweep_kernel"
+
+
+def ncu_traffic(kname, args, pr, R, sweeps_per_launch):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel from the
+    committed `ncu --set full` capture (profiles/traffic.json), rescaled from the
+    captured launch to this run's launch size (the kernel's DRAM traffic is per
+    sweep of the same instance); None when no capture matches this workload."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            caps = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    for c in caps:
+        if c.get("kernel") == kname and c.get("workload") == args.workload and \
+                c.get("n_spins") == pr.n and c.get("replicas") == R and c.get("rule") == args.rule:
+            per_sweep = c["dram_bytes"] / c["sweeps_per_launch"]
+            return {"bytes_per_launch": per_sweep * sweeps_per_launch,
+                    "source": f"profiles/traffic.json: {c['source']}"}
+    return None
 
 
 def main():
