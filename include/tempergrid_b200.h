@@ -168,6 +168,29 @@ int tg_batch_get_state(tg_ctx* ctx, int instance, int slot, int8_t* out);
 int tg_batch_get_counters(tg_ctx* ctx, int instance, int64_t* attempts_p, int64_t* accepts_p,
                           int64_t* attempts_b, int64_t* accepts_b);
 
+/* ---- Resource-matched J-column baseline (run_jcolumn_pt, engine.cpp:221-270) ----
+ * j_repeats independent single-column runs of the context's problem
+ * (tg_set_problem) with schedule (betas, {p_fixed}) and seeds
+ * derive_seed(cfg->seed, repeat = 5, rep) (rng.hpp:28, engine.cpp:238),
+ * executed as ONE batch on the device (SLOT engine) and merged per round:
+ * out[k] for rounds k+1 = 1..total_sweeps/sweeps_per_swap (out_cap must hold
+ * them).  best_f is NaN where no repeat was feasible.  cfg->engine must be
+ * AUTO or SLOT; record_flags / record_every are ignored.  Errors as the
+ * reference: p_fixed <= 0 or j_repeats < 1 -> TG_ERR_CONFIG. */
+typedef struct {
+    int64_t round;
+    int64_t sweep_count;
+    double best_f;
+    int32_t any_feasible;
+    int32_t n_feasible;
+    int32_t n_total;
+    int32_t reserved;
+} tg_baseline_record;
+
+int tg_run_jcolumn(tg_ctx* ctx, int n_betas, const double* betas, double p_fixed, int j_repeats,
+                   const tg_run_config* cfg, tg_baseline_record* out, int64_t out_cap,
+                   double* feasible_fraction);
+
 /* Host-only helper (no device needed): greedy colouring of cost+chain edges
  * and the canonical sweep order (stable sort by colour, chain degree, cost
  * degree); order[k] = caller spin at internal position k. */

@@ -6,6 +6,9 @@
 //
 //     Trace tempergrid::run_2dpt_b200(const ConstrainedProblem&, const Schedule&,
 //                                     const RunConfig&, const B200Options& = {});
+//     BaselineTrace tempergrid::run_jcolumn_pt_b200(const ConstrainedProblem&,
+//                                     const std::vector<double>& betas, double p_fixed,
+//                                     int j_repeats, const RunConfig&, const B200Options& = {});
 //
 // with the exact signature, validation, exceptions and Trace contents of
 // tempergrid::run_2dpt (include/tempergrid/engine.hpp:62-63, src/engine.cpp:83-219),
@@ -18,7 +21,9 @@
 // oracle/Makefile (target `shim`) and exercised by tests/test_integration.py,
 // which checks that run_2dpt_b200 and the reference's run_2dpt produce
 // byte-identical trace_to_jsonl output when both consume Philox draws.
+#include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -102,6 +107,25 @@ int sink(void* user, const tg_record* recs, std::int64_t n_recs, const std::int8
     return 0;
 }
 
+void set_problem(tg_ctx* ctx, const ConstrainedProblem& problem) {
+    const IsingModel& cost = problem.cost;
+    std::vector<std::int32_t> ci, cj, pa, pb;
+    std::vector<double> w;
+    for (const Coupling& c : cost.couplings()) {
+        ci.push_back(c.i);
+        cj.push_back(c.j);
+        w.push_back(c.weight);
+    }
+    for (const auto& [a, b] : problem.constraints.pairs()) {
+        pa.push_back(a);
+        pb.push_back(b);
+    }
+    const int rc = tg_set_problem(ctx, cost.n_spins(), static_cast<int>(ci.size()), ci.data(),
+                                  cj.data(), w.data(), cost.fields().data(),
+                                  static_cast<int>(pa.size()), pa.data(), pb.data());
+    if (rc != TG_OK) raise(ctx, rc);
+}
+
 }  // namespace
 
 Trace run_2dpt_b200(const ConstrainedProblem& problem, const Schedule& schedule,
@@ -115,21 +139,7 @@ Trace run_2dpt_b200(const ConstrainedProblem& problem, const Schedule& schedule,
     } guard{ctx};
 
     const IsingModel& cost = problem.cost;
-    std::vector<std::int32_t> ci, cj, pa, pb;
-    std::vector<double> w;
-    for (const Coupling& c : cost.couplings()) {
-        ci.push_back(c.i);
-        cj.push_back(c.j);
-        w.push_back(c.weight);
-    }
-    for (const auto& [a, b] : problem.constraints.pairs()) {
-        pa.push_back(a);
-        pb.push_back(b);
-    }
-    rc = tg_set_problem(ctx, cost.n_spins(), static_cast<int>(ci.size()), ci.data(), cj.data(),
-                        w.data(), cost.fields().data(), static_cast<int>(pa.size()), pa.data(),
-                        pb.data());
-    if (rc != TG_OK) raise(ctx, rc);
+    set_problem(ctx, problem);
     rc = tg_set_schedule(ctx, static_cast<int>(schedule.betas.size()), schedule.betas.data(),
                          static_cast<int>(schedule.penalties.size()), schedule.penalties.data());
     if (rc != TG_OK) raise(ctx, rc);
@@ -162,7 +172,111 @@ Trace run_2dpt_b200(const ConstrainedProblem& problem, const Schedule& schedule,
     return trace;
 }
 
+// run_jcolumn_pt (engine.cpp:221-270): all j_repeats columns run as one device
+// batch (tg_run_jcolumn), merged per round into the reference's BaselineTrace.
+BaselineTrace run_jcolumn_pt_b200(const ConstrainedProblem& problem,
+                                  const std::vector<double>& betas, double p_fixed,
+                                  int j_repeats, const RunConfig& cfg,
+                                  const B200Options& opt = {}) {
+    if (p_fixed <= 0.0) throw config_error("baseline: P must be positive");
+    if (j_repeats < 1) throw config_error("baseline: repeats must be >= 1");
+    tg_ctx* ctx = nullptr;
+    int rc = tg_create(opt.device, &ctx);
+    if (rc != TG_OK) raise(nullptr, rc);
+    struct Guard {
+        tg_ctx* c;
+        ~Guard() { tg_destroy(c); }
+    } guard{ctx};
+    set_problem(ctx, problem);
+    if (cfg.threads < 1) throw config_error("run: threads must be >= 1");
+    tg_run_config rc_cfg{};
+    rc_cfg.total_sweeps = cfg.total_sweeps;
+    rc_cfg.sweeps_per_swap = cfg.sweeps_per_swap;
+    rc_cfg.seed = cfg.seed;
+    rc_cfg.rule = opt.rule;
+    rc_cfg.engine = TG_ENGINE_SLOT;
+    rc_cfg.record_every = 1;
+    const std::int64_t rounds =
+        cfg.sweeps_per_swap >= 1 ? cfg.total_sweeps / cfg.sweeps_per_swap : 0;
+    std::vector<tg_baseline_record> recs(static_cast<std::size_t>(std::max<std::int64_t>(rounds, 1)));
+    double ff = 0.0;
+    rc = tg_run_jcolumn(ctx, static_cast<int>(betas.size()), betas.data(), p_fixed, j_repeats,
+                        &rc_cfg, recs.data(), rounds, &ff);
+    if (rc != TG_OK) raise(ctx, rc);
+    BaselineTrace out;
+    out.betas = betas;
+    out.penalty = p_fixed;
+    out.sweeps_per_swap = cfg.sweeps_per_swap;
+    for (std::int64_t k = 0; k < rounds; ++k) {
+        BaselineRecord r;
+        r.round = recs[k].round;
+        r.sweep_count = recs[k].sweep_count;
+        r.best_f = recs[k].best_f;
+        r.any_feasible = recs[k].any_feasible != 0;
+        r.n_feasible = recs[k].n_feasible;
+        r.n_total = recs[k].n_total;
+        out.records.push_back(r);
+    }
+    out.feasible_fraction = ff;
+    return out;
+}
+
 }  // namespace tempergrid
+
+namespace {
+std::string baseline_text(const tempergrid::BaselineTrace& t) {
+    std::string s;
+    char buf[160];
+    for (const auto& r : t.records) {
+        std::snprintf(buf, sizeof buf, "%lld %lld %.17g %d %d %d\n", (long long)r.round,
+                      (long long)r.sweep_count, r.best_f, r.any_feasible ? 1 : 0, r.n_feasible,
+                      r.n_total);
+        s += buf;
+    }
+    std::snprintf(buf, sizeof buf, "fraction %.17g\n", t.feasible_fraction);
+    return s + buf;
+}
+}  // namespace
+
+// C entry for tests: the reference run_jcolumn_pt and run_jcolumn_pt_b200 on
+// the same inputs, each serialised record by record (%.17g doubles).
+extern "C" int tg_shim_compare_jcolumn(int n, int nc, const int* ci, const int* cj, const double* w,
+                                       const double* h, int np, const int* pa, const int* pb,
+                                       int I, const double* betas, double p_fixed, int repeats,
+                                       std::int64_t total, std::int64_t sps, std::uint64_t seed,
+                                       char* ref_out, std::size_t ref_cap, char* gpu_out,
+                                       std::size_t gpu_cap, char* err, int errlen) {
+    using namespace tempergrid;
+    try {
+        std::vector<Coupling> cs;
+        for (int k = 0; k < nc; ++k) cs.push_back({ci[k], cj[k], w[k]});
+        std::vector<std::pair<int, int>> pairs;
+        for (int k = 0; k < np; ++k) pairs.emplace_back(pa[k], pb[k]);
+        ConstrainedProblem problem{IsingModel(n, cs, std::vector<double>(h, h + n)),
+                                   ConstraintSet(n, pairs)};
+        std::vector<double> b(betas, betas + I);
+        RunConfig cfg;
+        cfg.total_sweeps = total;
+        cfg.sweeps_per_swap = sps;
+        cfg.seed = seed;
+        const std::string a = baseline_text(run_jcolumn_pt(problem, b, p_fixed, repeats, cfg));
+        const std::string g = baseline_text(run_jcolumn_pt_b200(problem, b, p_fixed, repeats, cfg));
+        if (a.size() + 1 > ref_cap || g.size() + 1 > gpu_cap) return -3;
+        std::copy(a.begin(), a.end(), ref_out);
+        ref_out[a.size()] = '\0';
+        std::copy(g.begin(), g.end(), gpu_out);
+        gpu_out[g.size()] = '\0';
+        return 0;
+    } catch (const std::exception& e) {
+        std::string m = e.what();
+        if (errlen > 0) {
+            const std::size_t k = std::min<std::size_t>(m.size(), errlen - 1);
+            std::copy(m.begin(), m.begin() + k, err);
+            err[k] = '\0';
+        }
+        return -1;
+    }
+}
 
 // C entry for tests: run both the reference run_2dpt and run_2dpt_b200 on the
 // same inputs and return their trace_to_jsonl texts.

@@ -174,6 +174,47 @@ def run(pr, betas, penalties, total_sweeps, sps=1, seed=1, rule="metropolis", rn
                         o["round_acc_p"], o["round_acc_b"], o["final_grid"], o["grid_states"])
 
 
+class _BaselineOut(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in (
+        "round", "sweep_count", "best_f", "any_feasible", "n_feasible", "n_total",
+        "feasible_fraction")]
+
+
+@dataclass
+class BaselineResult:
+    round: np.ndarray
+    sweep_count: np.ndarray
+    best_f: np.ndarray
+    any_feasible: np.ndarray
+    n_feasible: np.ndarray
+    n_total: np.ndarray
+    feasible_fraction: float
+
+
+def run_jcolumn(pr, betas, p_fixed, j_repeats, total_sweeps, sps=1, seed=1, rule="metropolis",
+                impl="port", threads=1) -> BaselineResult:
+    """run_jcolumn_pt (engine.cpp:221-270) on the C port or a reference build."""
+    p, c, keep = _marshal(pr, betas, [max(float(p_fixed), 0.0)], total_sweeps, sps, seed, rule, "slot")
+    rounds = int(total_sweeps) // max(int(sps), 1)
+    o = dict(round=np.zeros(rounds, np.int64), sweep_count=np.zeros(rounds, np.int64),
+             best_f=np.zeros(rounds), any_feasible=np.zeros(rounds, np.uint8),
+             n_feasible=np.zeros(rounds, np.int32), n_total=np.zeros(rounds, np.int32),
+             feasible_fraction=np.zeros(1))
+    out = _BaselineOut(*[_ptr(o[k]) for k, _ in _BaselineOut._fields_])
+    err = C.create_string_buffer(512)
+    if impl == "port":
+        rc = port_lib().tgo_run_jcolumn(C.byref(p), C.byref(c), C.c_double(p_fixed), int(j_repeats),
+                                        C.byref(out), err, 512)
+    else:
+        rc = ref_lib(impl.split(":", 1)[1]).tgr_run_jcolumn(
+            C.byref(p), C.byref(c), C.c_double(p_fixed), int(j_repeats), int(threads), C.byref(out),
+            err, 512)
+    if rc != 0:
+        raise OracleError(rc, err.value.decode())
+    return BaselineResult(o["round"], o["sweep_count"], o["best_f"], o["any_feasible"].astype(bool),
+                          o["n_feasible"], o["n_total"], float(o["feasible_fraction"][0]))
+
+
 def ref_timed(variant, pr, betas, penalties, total_sweeps, sps=1, seed=1, threads=1) -> float:
     """Run the reference build once; returns the last target f (for timing legs)."""
     p, c, keep = _marshal(pr, betas, penalties, total_sweeps, sps, seed, "metropolis", "slot")

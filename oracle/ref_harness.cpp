@@ -186,6 +186,52 @@ extern "C" int tgr_run_2dpt_timed(const tgo_problem* p, const tgo_run_cfg* cfg, 
     }
 }
 
+// tempergrid::run_jcolumn_pt (engine.cpp:221-270) on the same plain arrays;
+// cfg's penalties are ignored (the column runs at p_fixed).
+extern "C" int tgr_run_jcolumn(const tgo_problem* p, const tgo_run_cfg* cfg, double p_fixed,
+                               int j_repeats, int threads, tgo_baseline_out* out, char* err,
+                               int errlen) {
+    using namespace tempergrid;
+    try {
+        std::vector<Coupling> cs;
+        for (int k = 0; k < p->n_couplings; ++k) cs.push_back({p->ci[k], p->cj[k], p->cw[k]});
+        std::vector<double> h(p->fields, p->fields + p->n);
+        IsingModel cost(p->n, std::move(cs), std::move(h));
+        std::vector<std::pair<int, int>> pairs;
+        for (int k = 0; k < p->n_pairs; ++k) pairs.emplace_back(p->pa[k], p->pb[k]);
+        ConstrainedProblem problem{std::move(cost), ConstraintSet(p->n, std::move(pairs))};
+        std::vector<double> betas(cfg->betas, cfg->betas + cfg->n_betas);
+        RunConfig rc;
+        rc.total_sweeps = cfg->total_sweeps;
+        rc.sweeps_per_swap = cfg->sweeps_per_swap;
+        rc.seed = cfg->seed;
+        rc.threads = threads;
+        tgref_ctx::master = cfg->seed;
+        tgref_ctx::n_replicas = cfg->n_betas;
+        const BaselineTrace t = run_jcolumn_pt(problem, betas, p_fixed, j_repeats, rc);
+        for (std::size_t k = 0; k < t.records.size(); ++k) {
+            const BaselineRecord& r = t.records[k];
+            if (out->round) out->round[k] = r.round;
+            if (out->sweep_count) out->sweep_count[k] = r.sweep_count;
+            if (out->best_f) out->best_f[k] = r.best_f;
+            if (out->any_feasible) out->any_feasible[k] = r.any_feasible ? 1 : 0;
+            if (out->n_feasible) out->n_feasible[k] = r.n_feasible;
+            if (out->n_total) out->n_total[k] = r.n_total;
+        }
+        if (out->feasible_fraction) *out->feasible_fraction = t.feasible_fraction;
+        return 0;
+    } catch (const tempergrid::config_error& e) {
+        put_err(err, errlen, e.what());
+        return 2;
+    } catch (const tempergrid::resource_error& e) {
+        put_err(err, errlen, e.what());
+        return 3;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
 // tempergrid::sparsify (constraints.cpp:50-120) on a logical model; writes the
 // physical couplings (canonical order) and chain pairs.  Returns the number
 // of physical spins, or -code on error.  Capacities are the caller's.

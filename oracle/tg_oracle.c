@@ -579,3 +579,55 @@ int tgo_run_2dpt(const tgo_problem* prob, const tgo_run_cfg* cfg, tgo_outputs* o
     model_free(&cost);
     return TGO_OK;
 }
+
+/* run_jcolumn_pt, engine.cpp:221-270: standard PT (beta swaps only) at a fixed
+ * penalty, repeated with independent seeds (StreamPurpose::repeat = 5,
+ * rng.hpp:28) and merged per round. */
+int tgo_run_jcolumn(const tgo_problem* prob, const tgo_run_cfg* cfg, double p_fixed,
+                    int j_repeats, tgo_baseline_out* out, char* err, int errlen) {
+    if (p_fixed <= 0.0) { set_err(err, errlen, "baseline: P must be positive"); return TGO_CONFIG_ERROR; }
+    if (j_repeats < 1) { set_err(err, errlen, "baseline: repeats must be >= 1"); return TGO_CONFIG_ERROR; }
+    const int64_t rounds = cfg->sweeps_per_swap >= 1 ? cfg->total_sweeps / cfg->sweeps_per_swap : 0;
+    double* f = (double*)calloc((size_t)(rounds > 0 ? rounds : 1), sizeof(double));
+    double* g = (double*)calloc((size_t)(rounds > 0 ? rounds : 1), sizeof(double));
+    uint8_t* fe = (uint8_t*)calloc((size_t)(rounds > 0 ? rounds : 1), 1);
+    int64_t feasible_total = 0, sample_total = 0;
+    int rc = TGO_OK;
+    for (int rep = 0; rep < j_repeats; ++rep) {
+        tgo_run_cfg c = *cfg;
+        c.n_penalties = 1;
+        c.penalties = &p_fixed;
+        c.seed = tgo_derive(cfg->seed, 5, (uint64_t)rep);
+        tgo_outputs o;
+        memset(&o, 0, sizeof o);
+        o.f = f;
+        o.g = g;
+        o.feasible = fe;
+        rc = tgo_run_2dpt(prob, &c, &o, err, errlen);
+        if (rc != TGO_OK) break;
+        for (int64_t k = 0; k < rounds; ++k) {
+            if (rep == 0) {
+                if (out->round) out->round[k] = k + 1;
+                if (out->sweep_count) out->sweep_count[k] = (k + 1) * cfg->sweeps_per_swap;
+                if (out->best_f) out->best_f[k] = NAN;
+                if (out->any_feasible) out->any_feasible[k] = 0;
+                if (out->n_feasible) out->n_feasible[k] = 0;
+                if (out->n_total) out->n_total[k] = 0;
+            }
+            if (out->n_total) ++out->n_total[k];
+            ++sample_total;
+            if (fe[k]) {
+                if (out->n_feasible) ++out->n_feasible[k];
+                ++feasible_total;
+                if (out->best_f && (!out->any_feasible[k] || f[k] < out->best_f[k])) out->best_f[k] = f[k];
+                if (out->any_feasible) out->any_feasible[k] = 1;
+            }
+        }
+    }
+    if (rc == TGO_OK && out->feasible_fraction)
+        *out->feasible_fraction = sample_total == 0 ? 0.0 : (double)feasible_total / (double)sample_total;
+    free(f);
+    free(g);
+    free(fe);
+    return rc;
+}

@@ -74,6 +74,24 @@ typedef struct {
 int tgo_run_2dpt(const tgo_problem* prob, const tgo_run_cfg* cfg, tgo_outputs* out,
                  char* err, int errlen);
 
+/* Resource-matched J-column baseline, run_jcolumn_pt (engine.cpp:221-270):
+ * j_repeats single-column runs (betas, {p_fixed}) with seeds
+ * derive_seed(cfg->seed, repeat=5, rep), merged round by round.  cfg's
+ * n_penalties/penalties are ignored.  Outputs are [rounds]; best_f is NaN
+ * where no repeat was feasible. */
+typedef struct {
+    int64_t* round;
+    int64_t* sweep_count;
+    double* best_f;
+    uint8_t* any_feasible;
+    int32_t* n_feasible;
+    int32_t* n_total;
+    double* feasible_fraction; /* scalar */
+} tgo_baseline_out;
+
+int tgo_run_jcolumn(const tgo_problem* prob, const tgo_run_cfg* cfg, double p_fixed,
+                    int j_repeats, tgo_baseline_out* out, char* err, int errlen);
+
 /* engine.cpp:18-32 */
 double tgo_p_swap_probability(double beta, double d_penalty, double dg);
 double tgo_beta_swap_probability(double d_beta, double d_energy);

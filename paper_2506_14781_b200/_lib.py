@@ -24,6 +24,12 @@ class RunConfigC(C.Structure):
                 ("record_every", C.c_int32)]
 
 
+class BaselineRecordC(C.Structure):
+    _fields_ = [("round", C.c_int64), ("sweep_count", C.c_int64), ("best_f", C.c_double),
+                ("any_feasible", C.c_int32), ("n_feasible", C.c_int32), ("n_total", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
 class RecordC(C.Structure):
     _fields_ = [("round", C.c_int64), ("sweep_count", C.c_int64), ("f", C.c_double),
                 ("g", C.c_double), ("feasible", C.c_int32), ("target_state", C.c_int32),
@@ -88,6 +94,7 @@ def lib() -> C.CDLL:
     L.tg_batch_run.argtypes = [vp, C.POINTER(RunConfigC), BATCH_SINK, C.c_void_p]
     L.tg_batch_get_state.argtypes = [vp, C.c_int, C.c_int, vp]
     L.tg_batch_get_counters.argtypes = [vp, C.c_int, vp, vp, vp, vp]
+    L.tg_run_jcolumn.argtypes = [vp, C.c_int, vp, C.c_double, C.c_int, vp, vp, C.c_int64, vp]
     L.tg_partition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]
     L.tg_swap_phase_host.argtypes = [C.c_int, vp, C.c_int, vp, C.c_int64, C.c_int, C.c_uint64,
                                      C.c_uint64, vp, vp, vp, vp, vp]
@@ -102,4 +109,5 @@ EXPORTED = [
     "tg_set_profiling", "tg_canonical_order", "tg_p_swap_probability", "tg_beta_swap_probability",
     "tg_general_swap_probability", "tg_swap_phase_host", "tg_partition", "tg_batch_clear",
     "tg_batch_add", "tg_batch_run", "tg_batch_get_state", "tg_batch_get_counters",
+    "tg_run_jcolumn",
 ]

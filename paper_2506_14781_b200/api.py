@@ -403,6 +403,57 @@ def run_2dpt_batch(problems: Sequence[Problem], schedules: Sequence[Schedule], c
             eng.close()
 
 
+@dataclass
+class BaselineRecord:
+    """``tempergrid::BaselineRecord`` (engine.hpp:67-74)."""
+    round: int
+    sweep_count: int
+    best_f: float
+    any_feasible: bool
+    n_feasible: int
+    n_total: int
+
+
+@dataclass
+class BaselineTrace:
+    """``tempergrid::BaselineTrace`` (engine.hpp:76-82)."""
+    betas: List[float]
+    penalty: float
+    sweeps_per_swap: int
+    records: List[BaselineRecord] = field(default_factory=list)
+    feasible_fraction: float = 0.0
+
+
+def run_jcolumn_pt(problem: Problem, betas, p_fixed: float, j_repeats: int, cfg: RunConfig,
+                   device: int = 0, engine: Optional[Engine] = None) -> BaselineTrace:
+    """Drop-in for ``tempergrid::run_jcolumn_pt`` (engine.cpp:221-270): the
+    resource-matched baseline of J independent standard-PT columns at a fixed
+    penalty, run as one device batch (``tg_run_jcolumn``) and merged per round."""
+    if not p_fixed > 0.0:  # engine.cpp:224-225, checked before anything else
+        raise ConfigError("baseline: P must be positive")
+    if j_repeats < 1:
+        raise ConfigError("baseline: repeats must be >= 1")
+    b = _arr(betas, np.float64)
+    eng = engine or Engine(device)
+    try:
+        eng.set_problem(problem)
+        rounds = int(cfg.total_sweeps) // max(int(cfg.sweeps_per_swap), 1)
+        recs = (_lib.BaselineRecordC * max(rounds, 1))()
+        ff = C.c_double(0.0)
+        c = eng._cfg(cfg)
+        eng._check(eng._L.tg_run_jcolumn(eng._h, len(b), _p(b), float(p_fixed), int(j_repeats),
+                                         C.byref(c), recs, rounds, C.byref(ff)))
+        out = BaselineTrace(list(map(float, b)), float(p_fixed), int(cfg.sweeps_per_swap))
+        out.records = [BaselineRecord(int(r.round), int(r.sweep_count), float(r.best_f),
+                                      bool(r.any_feasible), int(r.n_feasible), int(r.n_total))
+                       for r in recs[:rounds]]
+        out.feasible_fraction = float(ff.value)
+        return out
+    finally:
+        if engine is None:
+            eng.close()
+
+
 def batch_state(engine: Engine, instance: int, slot: int, n: int) -> np.ndarray:
     out = np.zeros(n, np.int8)
     engine._check(engine._L.tg_batch_get_state(engine._h, int(instance), int(slot), _p(out)))

@@ -21,6 +21,7 @@
 #include <string>
 #include <utility>
 #include <vector>
+#include <limits>
 
 #include "../../include/tempergrid_b200.h"
 #include "engine.cuh"
@@ -1222,7 +1223,15 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
     if (S.cfg.record_every < 1) S.cfg.record_every = 1;
     S.prep.assign(B, S2Prep{});
     S.state_off.clear();
-    for (int b = 0; b < B; ++b) s2_prepare(S.prep[b], c.batch[b]);
+    for (int b = 0; b < B; ++b) {
+        const BatchInst& x = c.batch[b];
+        const BatchInst* y = b ? &c.batch[b - 1] : nullptr;
+        if (y && x.n == y->n && x.ci == y->ci && x.cj == y->cj && x.cw == y->cw && x.h == y->h &&
+            x.pa == y->pa && x.pb == y->pb)
+            S.prep[b] = S.prep[b - 1];  // repeats of one instance (J-column baseline)
+        else
+            s2_prepare(S.prep[b], x);
+    }
     int D = 4;
     for (const auto& P : S.prep) D = std::max(D, P.D);
     S.D = D;
@@ -1841,6 +1850,89 @@ int tg_batch_get_counters(tg_ctx* ctx, int instance, int64_t* attempts_p, int64_
                           int64_t* attempts_b, int64_t* accepts_b) {
     if (!ctx) return TG_ERR_CONFIG;
     return guard(ctx, [&] { s2_counters(*ctx, instance, attempts_p, accepts_p, attempts_b, accepts_b); });
+}
+
+namespace {
+struct JColumnMerge {
+    tg_baseline_record* out;
+    int64_t rounds;
+    int64_t feasible_total, sample_total;
+};
+
+int jcolumn_sink(void* user, int32_t, const tg_record* recs, int64_t n, const int8_t*, const int64_t*,
+                 const int64_t*) {
+    auto* m = static_cast<JColumnMerge*>(user);
+    for (int64_t k = 0; k < n; ++k) {
+        const tg_record& r = recs[k];
+        if (r.round < 1 || r.round > m->rounds) return 1;
+        tg_baseline_record& b = m->out[r.round - 1];
+        ++b.n_total;
+        ++m->sample_total;
+        if (r.feasible) {
+            ++b.n_feasible;
+            ++m->feasible_total;
+            if (!b.any_feasible || r.f < b.best_f) b.best_f = r.f;
+            b.any_feasible = 1;
+        }
+    }
+    return 0;
+}
+}  // namespace
+
+int tg_run_jcolumn(tg_ctx* ctx, int n_betas, const double* betas, double p_fixed, int j_repeats,
+                   const tg_run_config* cfg, tg_baseline_record* out, int64_t out_cap,
+                   double* feasible_fraction) {
+    if (!ctx || !cfg) return TG_ERR_CONFIG;
+    return guard(ctx, [&] {
+        // engine.cpp:224-225
+        if (!(p_fixed > 0.0)) fail(TG_ERR_CONFIG, "baseline: P must be positive");
+        if (j_repeats < 1) fail(TG_ERR_CONFIG, "baseline: repeats must be >= 1");
+        if (!ctx->have_problem) fail(TG_ERR_CONFIG, "baseline: no problem set (tg_set_problem)");
+        if (cfg->sweeps_per_swap < 1) fail(TG_ERR_CONFIG, "run: sweeps_per_swap must be >= 1");
+        if (cfg->total_sweeps < cfg->sweeps_per_swap)
+            fail(TG_ERR_CONFIG, "run: total_sweeps must be >= sweeps_per_swap");
+        const int64_t rounds = cfg->total_sweeps / cfg->sweeps_per_swap;
+        if (!out || out_cap < rounds) fail(TG_ERR_CONFIG, "baseline: output holds %lld of %lld rounds",
+                                           (long long)out_cap, (long long)rounds);
+        BatchInst proto;
+        proto.n = ctx->n;
+        proto.ci = ctx->ci;
+        proto.cj = ctx->cj;
+        proto.cw = ctx->cw;
+        proto.h = ctx->h;
+        proto.pa = ctx->pa;
+        proto.pb = ctx->pb;
+        proto.betas.assign(betas, betas + std::max(n_betas, 0));
+        proto.pens.assign(1, p_fixed);
+        check_vec(proto.betas, "beta");
+        ctx->batch.clear();
+        for (int rep = 0; rep < j_repeats; ++rep) {
+            ctx->batch.push_back(proto);
+            ctx->batch.back().seed = derive_seed(cfg->seed, 5, (uint64_t)rep);  // StreamPurpose::repeat
+        }
+        for (int64_t k = 0; k < rounds; ++k) {
+            tg_baseline_record& b = out[k];
+            b.round = k + 1;
+            b.sweep_count = (k + 1) * cfg->sweeps_per_swap;
+            b.best_f = std::numeric_limits<double>::quiet_NaN();
+            b.any_feasible = b.n_feasible = b.n_total = b.reserved = 0;
+        }
+        tg_run_config c2 = *cfg;
+        c2.record_flags = 0;  // f, g, feasible only (store_target_only, engine.cpp:239)
+        c2.record_every = 1;
+        c2.engine = TG_ENGINE_SLOT;
+        if (cfg->engine != TG_ENGINE_AUTO && cfg->engine != TG_ENGINE_SLOT)
+            fail(TG_ERR_CONFIG, "baseline: only the SLOT engine runs batches");
+        if (ctx->world != 1) fail(TG_ERR_CONFIG, "baseline: single-GPU contexts only");
+        JColumnMerge m{out, rounds, 0, 0};
+        ctx->use_s2 = false;
+        ctx->initialised = false;
+        s2_build(*ctx, &c2);
+        s2_advance(*ctx, rounds, BatchSinkCtx{&jcolumn_sink, &m});
+        ctx->batch.clear();
+        if (feasible_fraction)
+            *feasible_fraction = m.sample_total == 0 ? 0.0 : (double)m.feasible_total / (double)m.sample_total;
+    });
 }
 
 int tg_canonical_order(int n, int n_couplings, const int32_t* ci, const int32_t* cj, int n_pairs,

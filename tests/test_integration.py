@@ -61,3 +61,31 @@ def test_grid_records_identical():
 def test_errors_map_to_reference_exceptions():
     with pytest.raises(AssertionError, match="strictly increasing"):
         compare(I.k10_pm1(1), [1.0, 0.5], [0.0], 10, 1, 1)
+
+
+def compare_jcolumn(pr, betas, p_fixed, repeats, total, sps, seed):
+    L = C.CDLL(SHIM)
+    P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    a = [np.ascontiguousarray(x, dtype=t) for x, t in (
+        (pr.ci, np.int32), (pr.cj, np.int32), (pr.cw, np.float64), (pr.fields, np.float64),
+        (pr.pa, np.int32), (pr.pb, np.int32), (betas, np.float64))]
+    cap = 16 << 20
+    ref = C.create_string_buffer(cap)
+    gpu = C.create_string_buffer(cap)
+    err = C.create_string_buffer(512)
+    L.tg_shim_compare_jcolumn.restype = C.c_int
+    rc = L.tg_shim_compare_jcolumn(pr.n, len(a[0]), P(a[0]), P(a[1]), P(a[2]), P(a[3]), len(a[4]),
+                                   P(a[4]), P(a[5]), len(a[6]), P(a[6]), C.c_double(p_fixed),
+                                   int(repeats), C.c_int64(total), C.c_int64(sps), C.c_uint64(seed),
+                                   ref, cap, gpu, cap, err, 512)
+    assert rc == 0, err.value
+    return ref.value.decode(), gpu.value.decode()
+
+
+def test_jcolumn_baseline_identical():
+    # run_jcolumn_pt (engine.cpp:221-270) vs run_jcolumn_pt_b200, as acceptance.cpp:385-393
+    # calls it: the grid schedule's betas, mean penalty, J repeats
+    b, p = I.config_schedule("c1")
+    ref, gpu = compare_jcolumn(I.k10_pm1(2), b, float(np.mean(p)), len(p), 2000, 2, 7000)
+    assert ref.count("\n") == 1001
+    assert gpu == ref
