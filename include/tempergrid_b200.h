@@ -191,6 +191,40 @@ int tg_run_jcolumn(tg_ctx* ctx, int n_betas, const double* betas, double p_fixed
                    const tg_run_config* cfg, tg_baseline_record* out, int64_t out_cap,
                    double* feasible_fraction);
 
+/* ---- Schedule probes and the adaptive ladder (schedule.cpp:18-163) ----
+ * tg_probe_population = probe_population (schedule.hpp:44-48) over the
+ * context's problem: n_chains independent chains at (beta, penalty), chain c
+ * on the Philox stream derive_seed(seed, probe = 4, c) (initial state from
+ * draw 0, then one draw per spin per sweep), all chains in one device launch;
+ * the second half of the sweeps is pooled on the device.  rule selects the
+ * sweep (the reference probes with metropolis_sweep).
+ * tg_build_schedule = build_schedule (schedule.hpp:57-58) with every probe on
+ * the device; the ladder logic runs on the host between probes. */
+typedef struct {
+    int32_t row, column;
+    double beta, penalty, sigma_e, sigma_g, mean_g;
+} tg_probe_stats;
+
+typedef struct {               /* ScheduleConfig, schedule.hpp:10-22 (+ rule) */
+    double beta0;              /* 0.3 */
+    double p0;                 /* 0.5 */
+    int32_t i_max, j_max;      /* 20, 20 */
+    double sigma_min;          /* <= 0: 0.5 sqrt(n) */
+    double alpha_beta;         /* 1.0 */
+    double alpha_p;            /* 1.2 */
+    int32_t n_chains;          /* 32 */
+    int32_t sweeps_per_probe;  /* 1000 */
+    int32_t replica_budget;    /* 400 */
+    int32_t rule;              /* TG_RULE_METROPOLIS */
+    uint64_t seed;             /* 1 */
+} tg_schedule_config;
+
+int tg_probe_population(tg_ctx* ctx, double beta, double penalty, int n_chains, int sweeps,
+                        uint64_t seed, int rule, tg_probe_stats* out);
+int tg_build_schedule(tg_ctx* ctx, const tg_schedule_config* cfg, double* betas, int betas_cap,
+                      int* n_betas, double* penalties, int penalties_cap, int* n_penalties,
+                      tg_probe_stats* stats, int stats_cap, int* n_stats, int* budget_exhausted);
+
 /* Host-only helper (no device needed): greedy colouring of cost+chain edges
  * and the canonical sweep order (stable sort by colour, chain degree, cost
  * degree); order[k] = caller spin at internal position k. */

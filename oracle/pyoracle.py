@@ -215,6 +215,73 @@ def run_jcolumn(pr, betas, p_fixed, j_repeats, total_sweeps, sps=1, seed=1, rule
                           o["n_feasible"], o["n_total"], float(o["feasible_fraction"][0]))
 
 
+class _ProbeStats(C.Structure):
+    _fields_ = [("row", C.c_int), ("column", C.c_int), ("beta", C.c_double),
+                ("penalty", C.c_double), ("sigma_e", C.c_double), ("sigma_g", C.c_double),
+                ("mean_g", C.c_double)]
+
+
+class _ScheduleCfg(C.Structure):
+    _fields_ = [("beta0", C.c_double), ("p0", C.c_double), ("i_max", C.c_int), ("j_max", C.c_int),
+                ("sigma_min", C.c_double), ("alpha_beta", C.c_double), ("alpha_p", C.c_double),
+                ("n_chains", C.c_int), ("sweeps_per_probe", C.c_int), ("replica_budget", C.c_int),
+                ("seed", C.c_uint64)]
+
+
+SCHEDULE_DEFAULTS = dict(beta0=0.3, p0=0.5, i_max=20, j_max=20, sigma_min=0.0, alpha_beta=1.0,
+                         alpha_p=1.2, n_chains=32, sweeps_per_probe=1000, replica_budget=400,
+                         seed=1)  # schedule.hpp:10-22
+
+
+def _stats_dict(s):
+    return {k: getattr(s, k) for k, _ in _ProbeStats._fields_}
+
+
+def probe_population(pr, beta, penalty, n_chains, sweeps, seed, rule="metropolis", impl="port"):
+    """probe_population (schedule.cpp:18-52) on the C port or a reference build
+    ('ref:philox' / 'ref:philox_hb'); returns the ProbeStats fields as a dict."""
+    p, _, keep = _marshal(pr, [1.0], [0.0], 1, 1, 1, rule, "slot")
+    out = _ProbeStats()
+    err = C.create_string_buffer(512)
+    if impl == "port":
+        rc = port_lib().tgo_probe_population(C.byref(p), C.c_double(beta), C.c_double(penalty),
+                                             int(n_chains), int(sweeps), C.c_uint64(seed),
+                                             RULE[rule], C.byref(out), err, 512)
+    else:
+        rc = ref_lib(impl.split(":", 1)[1]).tgr_probe_population(
+            C.byref(p), C.c_double(beta), C.c_double(penalty), int(n_chains), int(sweeps),
+            C.c_uint64(seed), C.byref(out), err, 512)
+    if rc != 0:
+        raise OracleError(rc, err.value.decode())
+    return _stats_dict(out)
+
+
+def build_schedule(pr, rule="metropolis", impl="port", **cfg):
+    """build_schedule (schedule.cpp:77-163); returns (betas, penalties, probe_stats,
+    budget_exhausted)."""
+    c = dict(SCHEDULE_DEFAULTS)
+    c.update(cfg)
+    sc = _ScheduleCfg(**c)
+    p, _, keep = _marshal(pr, [1.0], [0.0], 1, 1, 1, rule, "slot")
+    im, jm = max(int(c["i_max"]), 1), max(int(c["j_max"]), 1)
+    betas, pens = np.zeros(im), np.zeros(jm + 1)
+    cap = im * (jm + 1) + 1
+    stats = (_ProbeStats * cap)()
+    nb, npn, ns, be = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    err = C.create_string_buffer(512)
+    args = (C.byref(p), C.byref(sc))
+    tail = (_ptr(betas), C.byref(nb), _ptr(pens), C.byref(npn), stats, cap, C.byref(ns), C.byref(be),
+            err, 512)
+    if impl == "port":
+        rc = port_lib().tgo_build_schedule(*args, RULE[rule], *tail)
+    else:
+        rc = ref_lib(impl.split(":", 1)[1]).tgr_build_schedule(*args, *tail)
+    if rc != 0:
+        raise OracleError(rc, err.value.decode())
+    return (betas[:nb.value].copy(), pens[:npn.value].copy(),
+            [_stats_dict(stats[k]) for k in range(min(ns.value, cap))], bool(be.value))
+
+
 def ref_timed(variant, pr, betas, penalties, total_sweeps, sps=1, seed=1, threads=1) -> float:
     """Run the reference build once; returns the last target f (for timing legs)."""
     p, c, keep = _marshal(pr, betas, penalties, total_sweeps, sps, seed, "metropolis", "slot")

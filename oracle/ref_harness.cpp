@@ -232,6 +232,85 @@ extern "C" int tgr_run_jcolumn(const tgo_problem* p, const tgo_run_cfg* cfg, dou
     }
 }
 
+#ifndef TGREF_NO_SCHEDULE
+namespace {
+tempergrid::ConstrainedProblem make_problem(const tgo_problem* p) {
+    using namespace tempergrid;
+    std::vector<Coupling> cs;
+    for (int k = 0; k < p->n_couplings; ++k) cs.push_back({p->ci[k], p->cj[k], p->cw[k]});
+    std::vector<double> h(p->fields, p->fields + p->n);
+    IsingModel cost(p->n, std::move(cs), std::move(h));
+    std::vector<std::pair<int, int>> pairs;
+    for (int k = 0; k < p->n_pairs; ++k) pairs.emplace_back(p->pa[k], p->pb[k]);
+    return ConstrainedProblem{std::move(cost), ConstraintSet(p->n, std::move(pairs))};
+}
+
+void put_stats(const tempergrid::ProbeStats& s, tgo_probe_stats* o) {
+    o->row = s.row;
+    o->column = s.column;
+    o->beta = s.beta;
+    o->penalty = s.penalty;
+    o->sigma_e = s.sigma_e;
+    o->sigma_g = s.sigma_g;
+    o->mean_g = s.mean_g;
+}
+}  // namespace
+
+// tempergrid::probe_population (schedule.cpp:18-52).
+extern "C" int tgr_probe_population(const tgo_problem* p, double beta, double penalty,
+                                    int n_chains, int sweeps, std::uint64_t seed,
+                                    tgo_probe_stats* out, char* err, int errlen) {
+    try {
+        put_stats(tempergrid::probe_population(make_problem(p), beta, penalty, n_chains, sweeps,
+                                               seed),
+                  out);
+        return 0;
+    } catch (const tempergrid::config_error& e) {
+        put_err(err, errlen, e.what());
+        return 2;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
+// tempergrid::build_schedule (schedule.cpp:77-163).
+extern "C" int tgr_build_schedule(const tgo_problem* p, const tgo_schedule_cfg* c, double* betas,
+                                  int* n_betas, double* penalties, int* n_penalties,
+                                  tgo_probe_stats* stats, int stats_cap, int* n_stats,
+                                  int* budget_exhausted, char* err, int errlen) {
+    try {
+        tempergrid::ScheduleConfig cfg;
+        cfg.beta0 = c->beta0;
+        cfg.p0 = c->p0;
+        cfg.i_max = c->i_max;
+        cfg.j_max = c->j_max;
+        cfg.sigma_min = c->sigma_min;
+        cfg.alpha_beta = c->alpha_beta;
+        cfg.alpha_p = c->alpha_p;
+        cfg.n_chains = c->n_chains;
+        cfg.sweeps_per_probe = c->sweeps_per_probe;
+        cfg.replica_budget = c->replica_budget;
+        cfg.seed = c->seed;
+        const tempergrid::Schedule s = tempergrid::build_schedule(make_problem(p), cfg);
+        *n_betas = static_cast<int>(s.betas.size());
+        *n_penalties = static_cast<int>(s.penalties.size());
+        std::copy(s.betas.begin(), s.betas.end(), betas);
+        std::copy(s.penalties.begin(), s.penalties.end(), penalties);
+        *n_stats = static_cast<int>(s.probe_stats.size());
+        for (int k = 0; k < *n_stats && k < stats_cap; ++k) put_stats(s.probe_stats[k], stats + k);
+        *budget_exhausted = s.budget_exhausted ? 1 : 0;
+        return 0;
+    } catch (const tempergrid::config_error& e) {
+        put_err(err, errlen, e.what());
+        return 2;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return 1;
+    }
+}
+#endif
+
 // tempergrid::sparsify (constraints.cpp:50-120) on a logical model; writes the
 // physical couplings (canonical order) and chain pairs.  Returns the number
 // of physical spins, or -code on error.  Capacities are the caller's.

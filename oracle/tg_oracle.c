@@ -631,3 +631,187 @@ int tgo_run_jcolumn(const tgo_problem* prob, const tgo_run_cfg* cfg, double p_fi
     free(fe);
     return rc;
 }
+
+/* probe_population, schedule.cpp:18-52: n_chains independent chains at
+ * (beta, P), each on ONE stream derive_seed(seed, probe = 4, c) that first
+ * draws the random initial state (ising.cpp:15-19) and then one uniform per
+ * spin per sweep; the second half of every chain's per-sweep (E = f + P g, g)
+ * is pooled in chain-major order. */
+int tgo_probe_population(const tgo_problem* prob, double beta, double penalty, int n_chains,
+                         int sweeps, uint64_t seed, int rule, tgo_probe_stats* out, char* err,
+                         int errlen) {
+    if (n_chains < 2) { set_err(err, errlen, "probe: need at least 2 chains"); return TGO_CONFIG_ERROR; }
+    if (sweeps < 2) { set_err(err, errlen, "probe: need at least 2 sweeps"); return TGO_CONFIG_ERROR; }
+    model_t cost;
+    cset_t cs;
+    view_t v;
+    int rc = model_build(&cost, prob->n, prob->n_couplings, prob->ci, prob->cj, prob->cw,
+                         prob->fields, err, errlen);
+    if (rc) return rc;
+    rc = cset_build(&cs, prob->n, prob->n_pairs, prob->pa, prob->pb, err, errlen);
+    if (rc) { model_free(&cost); return rc; }
+    rc = view_build(&v, &cost, &cs, penalty, err, errlen);
+    if (rc) { cset_free(&cs); model_free(&cost); return rc; }
+    const int n = prob->n, burn_in = sweeps / 2;
+    double sum_e = 0.0, sum_e2 = 0.0, sum_g = 0.0, sum_g2 = 0.0;
+    int64_t kept = 0;
+    rstate_t st;
+    st.spins = (int8_t*)malloc((size_t)n);
+    st.local = (double*)malloc(sizeof(double) * (size_t)n);
+    st.id = 0;
+    for (int c = 0; c < n_chains; ++c) {
+        const uint64_t key = tgo_derive_seed(seed, 4, (uint64_t)c);
+        uint64_t ctr = 0;
+        for (int i = 0; i < n; ++i) st.spins[i] = (tgo_stream_bits(key, ctr++) >> 63) ? (int8_t)1 : (int8_t)-1;
+        refresh(&v, &st);
+        for (int s = 0; s < sweeps; ++s) {
+            draw_ctx_t d;
+            d.mode = TGO_RNG_SLOT;
+            d.slot_seed = key;
+            d.slot_ctr = &ctr;
+            d.pkey = 0;
+            d.t = 0;
+            sweep(&v, beta, &st, &d, rule);
+            if (s < burn_in) continue;
+            const double e = st.f + penalty * st.g;
+            sum_e += e;
+            sum_e2 += e * e;
+            sum_g += st.g;
+            sum_g2 += st.g * st.g;
+            ++kept;
+        }
+    }
+    const double inv = 1.0 / (double)kept;
+    out->row = out->column = 0;
+    out->beta = beta;
+    out->penalty = penalty;
+    out->mean_g = sum_g * inv;
+    const double mean_e = sum_e * inv;
+    const double ve = sum_e2 * inv - mean_e * mean_e;
+    out->sigma_e = sqrt(ve > 0.0 ? ve : 0.0);
+    const double vg = sum_g2 * inv - out->mean_g * out->mean_g;
+    out->sigma_g = sqrt(vg > 0.0 ? vg : 0.0);
+    free(st.spins);
+    free(st.local);
+    model_free(&v.merged);
+    cset_free(&cs);
+    model_free(&cost);
+    return TGO_OK;
+}
+
+static int cmp_double(const void* a, const void* b) {
+    const double x = *(const double*)a, y = *(const double*)b;
+    return x < y ? -1 : (x > y);
+}
+
+/* std::min / std::max semantics (NaN-order identical to <algorithm>) */
+static inline double std_min(double a, double b) { return (b < a) ? b : a; }
+static inline double std_max(double a, double b) { return (a < b) ? b : a; }
+
+/* lower median, schedule.cpp:57-60 */
+static double median_of(double* v, int n) {
+    qsort(v, (size_t)n, sizeof(double), cmp_double);
+    return v[(n - 1) / 2];
+}
+
+/* build_schedule, schedule.cpp:77-163.  The reference's std::map of
+ * proposals keyed (row, column) is a dense [i_max][j_max + 2] table here;
+ * collecting column j in row order equals the map's ordered iteration. */
+int tgo_build_schedule(const tgo_problem* prob, const tgo_schedule_cfg* cfg, int rule,
+                       double* betas, int* n_betas, double* penalties, int* n_penalties,
+                       tgo_probe_stats* stats, int stats_cap, int* n_stats, int* budget_exhausted,
+                       char* err, int errlen) {
+    /* check_config, schedule.cpp:62-73 */
+    if (cfg->beta0 <= 0.0) { set_err(err, errlen, "schedule: beta0 must be > 0"); return TGO_CONFIG_ERROR; }
+    if (cfg->p0 < 0.0) { set_err(err, errlen, "schedule: P0 must be >= 0"); return TGO_CONFIG_ERROR; }
+    if (cfg->i_max < 1 || cfg->j_max < 1) { set_err(err, errlen, "schedule: I_max and J_max must be >= 1"); return TGO_CONFIG_ERROR; }
+    if (cfg->alpha_beta <= 0.0 || cfg->alpha_p <= 0.0) { set_err(err, errlen, "schedule: learning rates must be > 0"); return TGO_CONFIG_ERROR; }
+    if (cfg->replica_budget < 1) { set_err(err, errlen, "schedule: replica budget must be >= 1"); return TGO_CONFIG_ERROR; }
+    if ((long long)cfg->i_max * cfg->j_max > cfg->replica_budget) { set_err(err, errlen, "schedule: I_max * J_max exceeds replica budget"); return TGO_CONFIG_ERROR; }
+    const double sigma_min = cfg->sigma_min > 0.0 ? cfg->sigma_min : 0.5 * sqrt((double)prob->n);
+    const double p_cap = 2.0 * cfg->p0 + 1.0;
+    const int IM = cfg->i_max, JC = cfg->j_max + 2;
+    double* prop = (double*)calloc((size_t)IM * JC, sizeof(double));
+    uint8_t* has = (uint8_t*)calloc((size_t)IM * JC, 1);
+    double* cols = (double*)malloc(sizeof(double) * (size_t)IM * (cfg->j_max + 1));
+    double* column = (double*)malloc(sizeof(double) * (size_t)IM);
+    double* tmp = (double*)malloc(sizeof(double) * (size_t)(IM > cfg->j_max + 1 ? IM : cfg->j_max + 1));
+    uint64_t probe_counter = 0;
+    int ns = 0, np = 0, ncols = 0, rc = TGO_OK;
+    *budget_exhausted = 0;
+    penalties[np++] = cfg->p0;
+#define PINC(beta, sg) std_min(cfg->alpha_p / ((beta) * std_max((sg), 1e-300)), p_cap)
+#define PROBE(BETA_, PEN_, ROW_, COL_)                                                               \
+    do {                                                                                        \
+        rc = tgo_probe_population(prob, (BETA_), (PEN_), cfg->n_chains, cfg->sweeps_per_probe,    \
+                                  tgo_derive_seed(cfg->seed, 4, probe_counter++), rule, &last,  \
+                                  err, errlen);                                                 \
+        if (rc) goto done;                                                                      \
+        last.row = (ROW_);                                                                      \
+        last.column = (COL_);                                                                   \
+        if (ns < stats_cap) stats[ns] = last;                                                   \
+        ++ns;                                                                                   \
+    } while (0)
+    tgo_probe_stats last;
+    memset(&last, 0, sizeof last);
+    int clen = 0;
+    column[clen++] = cfg->beta0;
+    for (int i = 0;; ++i) {
+        PROBE(column[i], cfg->p0, i, 0);
+        if (last.sigma_e <= sigma_min) break;
+        prop[i * JC + 1] = cfg->p0 + PINC(column[i], last.sigma_g);
+        has[i * JC + 1] = 1;
+        if (i + 1 >= cfg->i_max) break;
+        column[clen++] = column[i] + cfg->alpha_beta / last.sigma_e;
+    }
+    for (int i = 0; i < clen; ++i) cols[(size_t)ncols * IM + i] = column[i];
+    ++ncols;
+    const int n_rows = clen;
+    if (last.mean_g >= 0.5) {
+        int any = 0;
+        for (int q = 0; q < IM * JC; ++q) any |= has[q];
+        if (!any) { prop[0 * JC + 1] = cfg->p0 + PINC(cfg->beta0, last.sigma_g); has[1] = 1; }
+        for (int j = 1;; ++j) {
+            int nn = 0;
+            for (int i = 0; i < IM; ++i)
+                if (j < JC && has[i * JC + j]) tmp[nn++] = prop[i * JC + j];
+            if ((long long)(j + 1) * n_rows > cfg->replica_budget || j >= cfg->j_max) {
+                *budget_exhausted = 1;
+                break;
+            }
+            const double prev = penalties[np - 1];
+            const double med = median_of(tmp, nn);
+            const double floor_ = prev + 1e-9 * (1.0 + fabs(prev));
+            penalties[np++] = std_max(med, floor_);
+            clen = 0;
+            column[clen++] = cfg->beta0;
+            for (int i = 0; i < n_rows; ++i) {
+                PROBE(column[i], penalties[j], i, j);
+                const double base = has[i * JC + j] ? prop[i * JC + j] : penalties[j];
+                prop[i * JC + j + 1] = base + PINC(column[i], last.sigma_g);
+                has[i * JC + j + 1] = 1;
+                if (i + 1 < n_rows)
+                    column[clen++] = column[i] + cfg->alpha_beta / std_max(last.sigma_e, sigma_min);
+            }
+            for (int i = 0; i < clen; ++i) cols[(size_t)ncols * IM + i] = column[i];
+            ++ncols;
+            if (last.mean_g < 0.5) break;
+        }
+    }
+    for (int i = 0; i < n_rows; ++i) {
+        for (int q = 0; q < ncols; ++q) tmp[q] = cols[(size_t)q * IM + i];
+        betas[i] = median_of(tmp, ncols);
+    }
+    *n_betas = n_rows;
+    *n_penalties = np;
+    *n_stats = ns;
+#undef PROBE
+#undef PINC
+done:
+    free(prop);
+    free(has);
+    free(cols);
+    free(column);
+    free(tmp);
+    return rc;
+}

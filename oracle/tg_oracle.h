@@ -92,6 +92,31 @@ typedef struct {
 int tgo_run_jcolumn(const tgo_problem* prob, const tgo_run_cfg* cfg, double p_fixed,
                     int j_repeats, tgo_baseline_out* out, char* err, int errlen);
 
+/* Schedule probes and the adaptive ladder (schedule.cpp:18-163,
+ * schedule.hpp:10-60).  rule selects the sweep the probes run (the reference
+ * calls metropolis_sweep; the heat-bath build links the alt sweep). */
+typedef struct {
+    int row, column;
+    double beta, penalty, sigma_e, sigma_g, mean_g;
+} tgo_probe_stats;
+
+typedef struct {
+    double beta0, p0;
+    int i_max, j_max;
+    double sigma_min, alpha_beta, alpha_p;
+    int n_chains, sweeps_per_probe, replica_budget;
+    uint64_t seed;
+} tgo_schedule_cfg;
+
+int tgo_probe_population(const tgo_problem* prob, double beta, double penalty, int n_chains,
+                         int sweeps, uint64_t seed, int rule, tgo_probe_stats* out, char* err,
+                         int errlen);
+/* betas[cap i_max], penalties[cap j_max], stats[cap stats_cap]; counts out. */
+int tgo_build_schedule(const tgo_problem* prob, const tgo_schedule_cfg* cfg, int rule,
+                       double* betas, int* n_betas, double* penalties, int* n_penalties,
+                       tgo_probe_stats* stats, int stats_cap, int* n_stats, int* budget_exhausted,
+                       char* err, int errlen);
+
 /* engine.cpp:18-32 */
 double tgo_p_swap_probability(double beta, double d_penalty, double dg);
 double tgo_beta_swap_probability(double d_beta, double d_energy);

@@ -30,6 +30,19 @@ class BaselineRecordC(C.Structure):
                 ("reserved", C.c_int32)]
 
 
+class ProbeStatsC(C.Structure):
+    _fields_ = [("row", C.c_int32), ("column", C.c_int32), ("beta", C.c_double),
+                ("penalty", C.c_double), ("sigma_e", C.c_double), ("sigma_g", C.c_double),
+                ("mean_g", C.c_double)]
+
+
+class ScheduleConfigC(C.Structure):
+    _fields_ = [("beta0", C.c_double), ("p0", C.c_double), ("i_max", C.c_int32),
+                ("j_max", C.c_int32), ("sigma_min", C.c_double), ("alpha_beta", C.c_double),
+                ("alpha_p", C.c_double), ("n_chains", C.c_int32), ("sweeps_per_probe", C.c_int32),
+                ("replica_budget", C.c_int32), ("rule", C.c_int32), ("seed", C.c_uint64)]
+
+
 class RecordC(C.Structure):
     _fields_ = [("round", C.c_int64), ("sweep_count", C.c_int64), ("f", C.c_double),
                 ("g", C.c_double), ("feasible", C.c_int32), ("target_state", C.c_int32),
@@ -95,6 +108,9 @@ def lib() -> C.CDLL:
     L.tg_batch_get_state.argtypes = [vp, C.c_int, C.c_int, vp]
     L.tg_batch_get_counters.argtypes = [vp, C.c_int, vp, vp, vp, vp]
     L.tg_run_jcolumn.argtypes = [vp, C.c_int, vp, C.c_double, C.c_int, vp, vp, C.c_int64, vp]
+    L.tg_probe_population.argtypes = [vp, C.c_double, C.c_double, C.c_int, C.c_int, C.c_uint64,
+                                      C.c_int, vp]
+    L.tg_build_schedule.argtypes = [vp, vp, vp, C.c_int, vp, vp, C.c_int, vp, vp, C.c_int, vp, vp]
     L.tg_partition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]
     L.tg_swap_phase_host.argtypes = [C.c_int, vp, C.c_int, vp, C.c_int64, C.c_int, C.c_uint64,
                                      C.c_uint64, vp, vp, vp, vp, vp]
@@ -109,5 +125,5 @@ EXPORTED = [
     "tg_set_profiling", "tg_canonical_order", "tg_p_swap_probability", "tg_beta_swap_probability",
     "tg_general_swap_probability", "tg_swap_phase_host", "tg_partition", "tg_batch_clear",
     "tg_batch_add", "tg_batch_run", "tg_batch_get_state", "tg_batch_get_counters",
-    "tg_run_jcolumn",
+    "tg_run_jcolumn", "tg_probe_population", "tg_build_schedule",
 ]

@@ -454,6 +454,94 @@ def run_jcolumn_pt(problem: Problem, betas, p_fixed: float, j_repeats: int, cfg:
             eng.close()
 
 
+@dataclass
+class ProbeStats:
+    """``tempergrid::ProbeStats`` (schedule.hpp:24-32)."""
+    row: int = 0
+    column: int = 0
+    beta: float = 0.0
+    penalty: float = 0.0
+    sigma_e: float = 0.0
+    sigma_g: float = 0.0
+    mean_g: float = 0.0
+
+
+@dataclass
+class ScheduleConfig:
+    """``tempergrid::ScheduleConfig`` (schedule.hpp:10-22) plus the probe sweep rule."""
+    beta0: float = 0.3
+    p0: float = 0.5
+    i_max: int = 20
+    j_max: int = 20
+    sigma_min: float = 0.0
+    alpha_beta: float = 1.0
+    alpha_p: float = 1.2
+    n_chains: int = 32
+    sweeps_per_probe: int = 1000
+    replica_budget: int = 400
+    seed: int = 1
+    rule: str = "metropolis"
+
+
+@dataclass
+class BuiltSchedule(Schedule):
+    """``tempergrid::Schedule`` as build_schedule returns it (schedule.hpp:34-42)."""
+    probe_stats: List[ProbeStats] = field(default_factory=list)
+    budget_exhausted: bool = False
+
+
+def _stats(s) -> ProbeStats:
+    return ProbeStats(int(s.row), int(s.column), float(s.beta), float(s.penalty), float(s.sigma_e),
+                      float(s.sigma_g), float(s.mean_g))
+
+
+def probe_population(problem: Problem, beta: float, penalty: float, n_chains: int, sweeps: int,
+                     seed: int, rule: str = "metropolis", device: int = 0,
+                     engine: Optional[Engine] = None) -> ProbeStats:
+    """Drop-in for ``tempergrid::probe_population`` (schedule.cpp:18-52): all
+    chains in one device launch (``tg_probe_population``)."""
+    eng = engine or Engine(device)
+    try:
+        eng.set_problem(problem)
+        out = _lib.ProbeStatsC()
+        eng._check(eng._L.tg_probe_population(eng._h, float(beta), float(penalty), int(n_chains),
+                                              int(sweeps), int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                              _lib.RULES[rule], C.byref(out)))
+        return _stats(out)
+    finally:
+        if engine is None:
+            eng.close()
+
+
+def build_schedule(problem: Problem, cfg: Optional[ScheduleConfig] = None, device: int = 0,
+                   engine: Optional[Engine] = None) -> BuiltSchedule:
+    """Drop-in for ``tempergrid::build_schedule`` (schedule.cpp:77-163): the
+    adaptive (beta, P) ladder, every probe on the device (``tg_build_schedule``)."""
+    cfg = cfg or ScheduleConfig()
+    c = _lib.ScheduleConfigC(float(cfg.beta0), float(cfg.p0), int(cfg.i_max), int(cfg.j_max),
+                             float(cfg.sigma_min), float(cfg.alpha_beta), float(cfg.alpha_p),
+                             int(cfg.n_chains), int(cfg.sweeps_per_probe), int(cfg.replica_budget),
+                             _lib.RULES[cfg.rule], int(cfg.seed) & 0xFFFFFFFFFFFFFFFF)
+    im, jm = max(int(cfg.i_max), 1), max(int(cfg.j_max), 1)
+    betas, pens = np.zeros(im), np.zeros(jm + 1)
+    cap = im * (jm + 1) + 1
+    stats = (_lib.ProbeStatsC * cap)()
+    nb, npn, ns, ex = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    eng = engine or Engine(device)
+    try:
+        eng.set_problem(problem)
+        eng._check(eng._L.tg_build_schedule(eng._h, C.byref(c), _p(betas), im, C.byref(nb), _p(pens),
+                                            jm + 1, C.byref(npn), stats, cap, C.byref(ns),
+                                            C.byref(ex)))
+    finally:
+        if engine is None:
+            eng.close()
+    out = BuiltSchedule(list(map(float, betas[:nb.value])), list(map(float, pens[:npn.value])))
+    out.probe_stats = [_stats(stats[k]) for k in range(min(ns.value, cap))]
+    out.budget_exhausted = bool(ex.value)
+    return out
+
+
 def batch_state(engine: Engine, instance: int, slot: int, n: int) -> np.ndarray:
     out = np.zeros(n, np.int8)
     engine._check(engine._L.tg_batch_get_state(engine._h, int(instance), int(slot), _p(out)))

@@ -173,6 +173,14 @@ struct Slot2 {
     int64_t rounds_done = 0;
     uint64_t swap_base = 0;
     bool ready = false;
+    // schedule probes (schedule.cpp:18-52): independent chains, no swaps,
+    // one stream per chain for the initial state and the sweeps
+    bool probe = false;
+    DBuf<uint64_t> d_init_keys;
+    DBuf<double> d_hist_f, d_hist_g, d_moments;
+    std::vector<SInst> h_inst;
+    uint64_t probe_gen = 0;
+    int probe_chains = 0, probe_rule = -1;
 };
 
 }  // namespace
@@ -187,6 +195,7 @@ struct tg_ctx {
 
     // problem (caller order) + canonical relabel
     bool have_problem = false;
+    uint64_t problem_gen = 0;
     int n = 0;
     std::vector<int> ci, cj, pa, pb;
     std::vector<double> cw, h;
@@ -825,6 +834,7 @@ void do_init(tg_ctx& c, const tg_run_config* cfg) {
         bi.n = c.n; bi.ci = c.ci; bi.cj = c.cj; bi.pa = c.pa; bi.pb = c.pb;
         bi.cw = c.cw; bi.h = c.h; bi.betas = c.betas; bi.pens = c.pens; bi.seed = cfg->seed;
         c.batch.assign(1, bi);
+        c.s2.probe = false;
         s2_build(c, &c.cfg);
         c.use_s2 = true;
         c.rounds_done = 0;
@@ -1105,6 +1115,21 @@ void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
 // One instance prepared for the device: canonical order, merged CSR (FP64
 // fallback), padded degree-D entries (FP32 fast path + forward-edge flags),
 // and the FP32 error bound (see kernels.cu slot_update_fast).
+// Error bands of the certified FP32 decision path (slot_engine.cu s2_update)
+// for fields bounded by |h| + sum |w| + 2 pmax * chain multiplicity at
+// inverse temperatures up to bmax.
+void s2_bands(S2Prep& P, double bmax, double pmax) {
+    double eps = 0.0;
+    for (int i = 0; i < P.n; ++i) {
+        double S = std::fabs(P.h[i]);
+        for (int e = P.off[i]; e < P.off[i + 1]; ++e)
+            S += std::fabs(P.w[e]) + (double)P.cm[e] * 2.0 * pmax;
+        eps = std::max(eps, (double)(P.off[i + 1] - P.off[i] + 3) * S * 0x1.0p-22);
+    }
+    P.eps = (float)(eps * 1.0001 + 1e-30);
+    P.beta_max = (float)(bmax * 1.0001);
+}
+
 void s2_prepare(S2Prep& P, const BatchInst& bi) {
     const int n = bi.n;
     P.n = n;
@@ -1147,7 +1172,7 @@ void s2_prepare(S2Prep& P, const BatchInst& bi) {
     if (maxdeg > 16) fail(TG_ERR_RESOURCE, "slot engine: merged degree %d > 16", maxdeg);
     if (n >= (1 << 27)) fail(TG_ERR_RESOURCE, "slot engine: %d spins exceed the packed index", n);
     P.D = maxdeg <= 4 ? 4 : (maxdeg <= 8 ? 8 : 16);
-    double pmax = 0.0, bmax = 0.0, eps = 0.0;
+    double pmax = 0.0, bmax = 0.0;
     for (double p : bi.pens) pmax = std::max(pmax, p);
     for (double b : bi.betas) bmax = std::max(bmax, std::fabs(b));
     P.h.resize(n);
@@ -1157,7 +1182,6 @@ void s2_prepare(S2Prep& P, const BatchInst& bi) {
     for (int i = 0; i < n; ++i) {
         P.h[i] = bi.h[P.order[i]];
         P.h32[i] = (float)P.h[i];
-        double S = std::fabs(P.h[i]);
         for (int k = 0; k < P.D; ++k) P.entp[(size_t)i * P.D + k] = make_int2(i, 0);  // pad: weight 0
         for (int e = P.off[i]; e < P.off[i + 1]; ++e) {
             const float wf = (float)P.w[e];
@@ -1167,12 +1191,9 @@ void s2_prepare(S2Prep& P, const BatchInst& bi) {
             if (P.nbr[e] > i) x |= 1 << 27;
             P.entp[(size_t)i * P.D + (e - P.off[i])] = make_int2(x, bits);
             P.wp[(size_t)i * P.D + (e - P.off[i])] = P.w[e];
-            S += std::fabs(P.w[e]) + (double)P.cm[e] * 2.0 * pmax;
         }
-        eps = std::max(eps, (double)(P.off[i + 1] - P.off[i] + 3) * S * 0x1.0p-22);
     }
-    P.eps = (float)(eps * 1.0001 + 1e-30);
-    P.beta_max = (float)(bmax * 1.0001);
+    s2_bands(P, bmax, pmax);
 }
 
 S2Args s2_args(tg_ctx& c) {
@@ -1285,7 +1306,8 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
         pens.insert(pens.end(), c.batch[b].pens.begin(), c.batch[b].pens.end());
         seeds[b] = c.batch[b].seed;
         for (int r = 0; r < S.R; ++r)
-            keys[(size_t)b * S.R + r] = derive_seed(c.batch[b].seed, kPurposeReplica, (uint64_t)r);
+            keys[(size_t)b * S.R + r] = S.probe ? derive_seed(c.batch[b].seed, kPurposeProbe, (uint64_t)r)
+                                                : derive_seed(c.batch[b].seed, kPurposeReplica, (uint64_t)r);
         swap_seed[b] = derive_seed(c.batch[b].seed, kPurposeSwap, 0);
     }
     S.max_colors = max_colors;
@@ -1300,6 +1322,7 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
         }
     for (int b = 0; b < B; ++b) energy_pref[b + 1] = energy_pref[b] + inst[b].n_chunks * S.G;
     S.d_inst.upload(inst, st);
+    S.h_inst = inst;
     S.d_entp.upload(entp, st);
     S.d_wp.upload(wp, st);
     S.d_off.upload(off, st);
@@ -1316,6 +1339,15 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
     S.d_keys.upload(keys, st);
     S.d_swap_seed.upload(swap_seed, st);
     S.d_seeds.upload(seeds, st);
+    {   // init streams: engine.cpp:100-101 (purpose init, per replica), or for a
+        // probe the chain's own stream from draw 0 (schedule.cpp:30-31)
+        std::vector<uint64_t> ik((size_t)B * S.R);
+        for (int b = 0; b < B; ++b)
+            for (int r = 0; r < S.R; ++r)
+                ik[(size_t)b * S.R + r] = S.probe ? keys[(size_t)b * S.R + r]
+                                                  : derive_seed(c.batch[b].seed, kPurposeInit, (uint64_t)r);
+        S.d_init_keys.upload(ik, st);
+    }
     S.d_perm.upload(perm, st);
     S.d_spins.alloc((size_t)spin_off);
     // cooperative grid: whole warps per replica group
@@ -1387,7 +1419,7 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
     S.h_states.resize(per_round_states * cap);
     // initial configurations (engine.cpp:98-106)
     S2Args a = s2_args(c);
-    slot2_init_kernel<<<dim3(c.sms * 4, B), 256, 0, st>>>(a, S.d_seeds.p);
+    slot2_init_kernel<<<dim3(c.sms * 4, B), 256, 0, st>>>(a, S.d_init_keys.p);
     CK(cudaGetLastError());
     S.rounds_done = 0;
     S.swap_base = 0;
@@ -1564,6 +1596,190 @@ void s2_energies(tg_ctx& c, int b, double* f, double* g) {
 
 // ================================================================ C ABI
 
+namespace {
+
+// ---------------------------------------------------------------- probes
+// probe_population (schedule.cpp:18-52) on the device: the chains are the
+// replicas of a one-instance SLOT-engine batch that never swaps.  The batch is
+// built once per (problem, n_chains, rule); every probe re-keys the chains'
+// streams (derive_seed(seed, probe, c), drawing the initial state from draw 0
+// and the sweeps from draw n on), re-initialises them, and runs all its sweeps
+// in ONE cooperative launch that writes each kept sweep's (f, g) of every chain
+// into a history; probe_moments_kernel pools the history in the reference's
+// order.  The host only evaluates the closing formulas.
+void probe_run(tg_ctx& c, double beta, double penalty, int n_chains, int sweeps, uint64_t seed,
+               int rule, tg_probe_stats* out) {
+    if (n_chains < 2) fail(TG_ERR_CONFIG, "probe: need at least 2 chains");
+    if (sweeps < 2) fail(TG_ERR_CONFIG, "probe: need at least 2 sweeps");
+    if (!c.have_problem) fail(TG_ERR_CONFIG, "probe: no problem set (tg_set_problem)");
+    if (!(penalty >= 0.0)) fail(TG_ERR_CONFIG, "build_effective: penalty must be >= 0");
+    if (rule != TG_RULE_METROPOLIS && rule != TG_RULE_HEAT_BATH)
+        fail(TG_ERR_CONFIG, "probe: unknown update rule %d", rule);
+    if (c.world != 1) fail(TG_ERR_CONFIG, "probe: single-GPU contexts only");
+    Slot2& S = c.s2;
+    cudaStream_t st = c.stream;
+    if (!S.ready || !S.probe || S.probe_gen != c.problem_gen || S.probe_chains != n_chains ||
+        S.probe_rule != rule) {
+        BatchInst bi;
+        bi.n = c.n;
+        bi.ci = c.ci; bi.cj = c.cj; bi.cw = c.cw; bi.h = c.h; bi.pa = c.pa; bi.pb = c.pb;
+        bi.betas.assign(n_chains, beta);
+        bi.pens.assign(1, penalty);
+        bi.seed = seed;
+        c.batch.assign(1, std::move(bi));
+        tg_run_config cfg{};
+        cfg.total_sweeps = 1;
+        cfg.sweeps_per_swap = 1;
+        cfg.rule = rule;
+        cfg.engine = TG_ENGINE_SLOT;
+        cfg.record_every = 1;
+        c.use_s2 = false;
+        c.initialised = false;
+        S.probe = true;
+        s2_build(c, &cfg);
+        c.batch.clear();
+        S.probe_gen = c.problem_gen;
+        S.probe_chains = n_chains;
+        S.probe_rule = rule;
+    }
+    const int R = S.R, Rp = S.Rp, n = S.prep[0].n;
+    // per-probe labels: beta, 2P, stream keys; error bands for this (beta, P)
+    s2_bands(S.prep[0], std::fabs(beta), penalty);
+    S.h_inst[0].eps = S.prep[0].eps;
+    S.h_inst[0].beta_max = S.prep[0].beta_max;
+    S.d_inst.upload(S.h_inst, st);
+    std::vector<double> sb(Rp, 0.0), stp(Rp, 0.0);
+    std::vector<uint64_t> sk(Rp, 0), keys(R);
+    for (int r = 0; r < R; ++r) {
+        keys[r] = derive_seed(seed, kPurposeProbe, (uint64_t)r);
+        sb[r] = beta;
+        stp[r] = 2.0 * penalty;
+        sk[r] = keys[r];
+    }
+    S.d_sbeta.upload(sb, st);
+    S.d_stwop.upload(stp, st);
+    S.d_skey.upload(sk, st);
+    S.d_keys.upload(keys, st);
+    S.d_init_keys.upload(keys, st);
+    const int burn_in = sweeps / 2, kept = sweeps - burn_in;
+    S.d_hist_f.alloc((size_t)kept * R);
+    S.d_hist_g.alloc((size_t)kept * R);
+    S.d_moments.alloc(4);
+    S2Args a = s2_args(c);
+    slot2_init_kernel<<<dim3(c.sms * 4, 1), 256, 0, st>>>(a, S.d_init_keys.p);
+    CK(cudaGetLastError());
+    a.hist_f = S.d_hist_f.p;
+    a.hist_g = S.d_hist_g.p;
+    a.hist_t0 = 1 + burn_in;      // sweep s uses draws (s+1)*n + i: t = s + 1
+    int64_t t0 = 1;
+    int nsw = sweeps, de = 0;
+    void* args[] = {&a, &t0, &nsw, &de};
+    CK(cudaLaunchCooperativeKernel(slot2_sweep_fn(S.D, true), dim3(S.grid), dim3(kSlot2Threads), args, 0, st));
+    probe_moments_kernel<<<1, 32, 0, st>>>(S.d_hist_f.p, S.d_hist_g.p, R, kept, penalty, S.d_moments.p);
+    CK(cudaGetLastError());
+    c.sweep_launches += 1;
+    c.other_launches += 2;
+    double sum[4];
+    CK(cudaMemcpyAsync(sum, S.d_moments.p, sizeof sum, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    (void)n;
+    // schedule.cpp:43-51
+    const double inv = 1.0 / static_cast<double>((int64_t)kept * n_chains);
+    out->row = out->column = 0;
+    out->beta = beta;
+    out->penalty = penalty;
+    out->mean_g = sum[2] * inv;
+    const double mean_e = sum[0] * inv;
+    out->sigma_e = std::sqrt(std::max(0.0, sum[1] * inv - mean_e * mean_e));
+    out->sigma_g = std::sqrt(std::max(0.0, sum[3] * inv - out->mean_g * out->mean_g));
+}
+
+double median_of(std::vector<double> v) {  // schedule.cpp:57-60 (lower median)
+    std::sort(v.begin(), v.end());
+    return v[(v.size() - 1) / 2];
+}
+
+// build_schedule (schedule.cpp:77-163) with every probe on the device.
+void build_schedule(tg_ctx& c, const tg_schedule_config& cfg, std::vector<double>& betas,
+                    std::vector<double>& pens, std::vector<tg_probe_stats>& stats, bool& exhausted) {
+    // check_config, schedule.cpp:62-73
+    if (cfg.beta0 <= 0.0) fail(TG_ERR_CONFIG, "schedule: beta0 must be > 0");
+    if (cfg.p0 < 0.0) fail(TG_ERR_CONFIG, "schedule: P0 must be >= 0");
+    if (cfg.i_max < 1 || cfg.j_max < 1) fail(TG_ERR_CONFIG, "schedule: I_max and J_max must be >= 1");
+    if (cfg.alpha_beta <= 0.0 || cfg.alpha_p <= 0.0) fail(TG_ERR_CONFIG, "schedule: learning rates must be > 0");
+    if (cfg.replica_budget < 1) fail(TG_ERR_CONFIG, "schedule: replica budget must be >= 1");
+    if ((long long)cfg.i_max * cfg.j_max > cfg.replica_budget)
+        fail(TG_ERR_CONFIG, "schedule: I_max * J_max exceeds replica budget");
+    if (!c.have_problem) fail(TG_ERR_CONFIG, "schedule: no problem set (tg_set_problem)");
+    const double sigma_min = cfg.sigma_min > 0.0 ? cfg.sigma_min : 0.5 * std::sqrt((double)c.n);
+    const double p_cap = 2.0 * cfg.p0 + 1.0;
+    uint64_t probe_counter = 0;
+    auto run_probe = [&](double beta, double penalty) {
+        tg_probe_stats s;
+        probe_run(c, beta, penalty, cfg.n_chains, cfg.sweeps_per_probe,
+                  derive_seed(cfg.seed, kPurposeProbe, probe_counter++), cfg.rule, &s);
+        return s;
+    };
+    auto p_increment = [&](double beta, double sigma_g) {
+        return std::min(cfg.alpha_p / (beta * std::max(sigma_g, 1e-300)), p_cap);
+    };
+    pens.assign(1, cfg.p0);
+    stats.clear();
+    exhausted = false;
+    std::vector<std::vector<double>> beta_columns;
+    std::map<std::pair<int, int>, double> proposals;
+    std::vector<double> column = {cfg.beta0};
+    tg_probe_stats last{};
+    for (int i = 0;; ++i) {
+        last = run_probe(column[i], cfg.p0);
+        last.row = i;
+        last.column = 0;
+        stats.push_back(last);
+        if (last.sigma_e <= sigma_min) break;
+        proposals[{i, 1}] = cfg.p0 + p_increment(column[i], last.sigma_g);
+        if (i + 1 >= cfg.i_max) break;
+        column.push_back(column[i] + cfg.alpha_beta / last.sigma_e);
+    }
+    beta_columns.push_back(column);
+    const int n_rows = (int)column.size();
+    if (last.mean_g >= 0.5) {
+        if (proposals.empty()) proposals[{0, 1}] = cfg.p0 + p_increment(cfg.beta0, last.sigma_g);
+        for (int j = 1;; ++j) {
+            std::vector<double> next_p;
+            for (const auto& kv : proposals)
+                if (kv.first.second == j) next_p.push_back(kv.second);
+            if ((long long)(j + 1) * n_rows > cfg.replica_budget || j >= cfg.j_max) {
+                exhausted = true;
+                break;
+            }
+            const double prev = pens.back();
+            pens.push_back(std::max(median_of(next_p), prev + 1e-9 * (1.0 + std::fabs(prev))));
+            column.assign(1, cfg.beta0);
+            for (int i = 0; i < n_rows; ++i) {
+                last = run_probe(column[i], pens[j]);
+                last.row = i;
+                last.column = j;
+                stats.push_back(last);
+                const auto base = proposals.find({i, j});
+                proposals[{i, j + 1}] = (base != proposals.end() ? base->second : pens[j]) +
+                                        p_increment(column[i], last.sigma_g);
+                if (i + 1 < n_rows)
+                    column.push_back(column[i] + cfg.alpha_beta / std::max(last.sigma_e, sigma_min));
+            }
+            beta_columns.push_back(column);
+            if (last.mean_g < 0.5) break;
+        }
+    }
+    betas.resize(n_rows);
+    for (int i = 0; i < n_rows; ++i) {
+        std::vector<double> row;
+        for (const auto& col : beta_columns) row.push_back(col[i]);
+        betas[i] = median_of(row);
+    }
+}
+
+}  // namespace
+
 extern "C" {
 
 int tg_abi_version(void) { return TG_ABI_VERSION; }
@@ -1652,6 +1868,7 @@ int tg_set_problem(tg_ctx* ctx, int n, int n_couplings, const int32_t* ci, const
         for (int k = 0; k < n; ++k) ctx->color_start[ctx->color[ctx->order[k]] + 1]++;
         for (int q = 0; q < ctx->n_colors; ++q) ctx->color_start[q + 1] += ctx->color_start[q];
         ctx->have_problem = true;
+        ++ctx->problem_gen;
         ctx->initialised = false;
     });
 }
@@ -1836,6 +2053,7 @@ int tg_batch_run(tg_ctx* ctx, const tg_run_config* cfg, tg_batch_sink_fn sink, v
         if (ctx->world != 1) fail(TG_ERR_CONFIG, "batch: single-GPU contexts only");
         ctx->use_s2 = false;
         ctx->initialised = false;
+        ctx->s2.probe = false;
         s2_build(*ctx, cfg);
         s2_advance(*ctx, cfg->total_sweeps / cfg->sweeps_per_swap, BatchSinkCtx{sink, user});
     });
@@ -1908,7 +2126,7 @@ int tg_run_jcolumn(tg_ctx* ctx, int n_betas, const double* betas, double p_fixed
         ctx->batch.clear();
         for (int rep = 0; rep < j_repeats; ++rep) {
             ctx->batch.push_back(proto);
-            ctx->batch.back().seed = derive_seed(cfg->seed, 5, (uint64_t)rep);  // StreamPurpose::repeat
+            ctx->batch.back().seed = derive_seed(cfg->seed, kPurposeRepeat, (uint64_t)rep);
         }
         for (int64_t k = 0; k < rounds; ++k) {
             tg_baseline_record& b = out[k];
@@ -1927,11 +2145,40 @@ int tg_run_jcolumn(tg_ctx* ctx, int n_betas, const double* betas, double p_fixed
         JColumnMerge m{out, rounds, 0, 0};
         ctx->use_s2 = false;
         ctx->initialised = false;
+        ctx->s2.probe = false;
         s2_build(*ctx, &c2);
         s2_advance(*ctx, rounds, BatchSinkCtx{&jcolumn_sink, &m});
         ctx->batch.clear();
         if (feasible_fraction)
             *feasible_fraction = m.sample_total == 0 ? 0.0 : (double)m.feasible_total / (double)m.sample_total;
+    });
+}
+
+int tg_probe_population(tg_ctx* ctx, double beta, double penalty, int n_chains, int sweeps,
+                        uint64_t seed, int rule, tg_probe_stats* out) {
+    if (!ctx || !out) return TG_ERR_CONFIG;
+    return guard(ctx, [&] { probe_run(*ctx, beta, penalty, n_chains, sweeps, seed, rule, out); });
+}
+
+int tg_build_schedule(tg_ctx* ctx, const tg_schedule_config* cfg, double* betas, int betas_cap,
+                      int* n_betas, double* penalties, int penalties_cap, int* n_penalties,
+                      tg_probe_stats* stats, int stats_cap, int* n_stats, int* budget_exhausted) {
+    if (!ctx || !cfg) return TG_ERR_CONFIG;
+    return guard(ctx, [&] {
+        std::vector<double> b, p;
+        std::vector<tg_probe_stats> st;
+        bool ex = false;
+        build_schedule(*ctx, *cfg, b, p, st, ex);
+        if ((int)b.size() > betas_cap || (int)p.size() > penalties_cap)
+            fail(TG_ERR_CONFIG, "schedule: output arrays hold %d betas / %d penalties, need %d / %d",
+                 betas_cap, penalties_cap, (int)b.size(), (int)p.size());
+        std::copy(b.begin(), b.end(), betas);
+        std::copy(p.begin(), p.end(), penalties);
+        if (n_betas) *n_betas = (int)b.size();
+        if (n_penalties) *n_penalties = (int)p.size();
+        if (stats) std::copy_n(st.begin(), std::min<size_t>(st.size(), (size_t)std::max(stats_cap, 0)), stats);
+        if (n_stats) *n_stats = (int)st.size();
+        if (budget_exhausted) *budget_exhausted = ex ? 1 : 0;
     });
 }
 

@@ -199,6 +199,9 @@ struct S2Args {
     const double* stwop;           // [B][Rp] 2P of that slot
     const uint64_t* skey;          // [B][Rp] Philox key of that slot's stream
     int nsub;                      // warps per replica group
+    double* hist_f;                // probes: per-sweep (f, g) of every replica,
+    double* hist_g;                //   [t - hist_t0][B*R], for sweeps t >= hist_t0
+    int64_t hist_t0;
 };
 
 struct S2Swap {

@@ -44,12 +44,14 @@ void* slot_sweep_fn();
 void* slot_sweep_fn_d(int D);  // padded-degree variant, D in {4, 8}
 
 constexpr int kSlot2Threads = 512;
-void* slot2_sweep_fn(int D);
+void* slot2_sweep_fn(int D, bool hist = false);
 __global__ void slot2_swap_kernel(const __grid_constant__ S2Swap s, int64_t round, uint64_t swap_base,
                                   int rec_idx, int rec_flags);
 __global__ void slot2_extract_kernel(const __grid_constant__ S2Args a, const __grid_constant__ S2Swap s,
                                      int rec_idx, int all_slots);
-__global__ void slot2_init_kernel(const __grid_constant__ S2Args a, const uint64_t* seeds);
+__global__ void slot2_init_kernel(const __grid_constant__ S2Args a, const uint64_t* init_keys);
+__global__ void probe_moments_kernel(const double* hist_f, const double* hist_g, int R, int kept,
+                                     double penalty, double* out);
 
 __global__ void swap_kernel(SwapArgs a, int64_t round, uint64_t swap_base, int rec_idx,
                             int rec_flags);

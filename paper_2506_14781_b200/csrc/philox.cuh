@@ -23,6 +23,8 @@ enum : uint64_t {
     kPurposeReplica = 1,
     kPurposeSwap = 2,
     kPurposeInit = 3,
+    kPurposeProbe = 4,   // schedule probe chains (rng.hpp:27)
+    kPurposeRepeat = 5,  // J-column baseline repeats (rng.hpp:28)
     kPurposePlane = 8,
 };
 

@@ -125,11 +125,39 @@ __device__ __forceinline__ void s2_update(const S2Args& a, const SInst& in, int8
     }
 }
 
+// Fixed-order reduction of the per-warp energy partials into out_f/out_g
+// [B*R] (one warp per replica, lanes take strided partials, then a fixed
+// shuffle tree); clears the partials for the next sweep.
+__device__ __forceinline__ void s2_reduce(const S2Args& a, int gw, int lane, int nsub, double* out_f,
+                                          double* out_g) {
+    for (int idx = gw; idx < a.B * a.R; idx += gridDim.x * (blockDim.x >> 5)) {
+        const int b = idx / a.R, rr = idx % a.R;
+        double F = 0.0, G = 0.0;
+        for (int q = lane; q < nsub; q += 32) {
+            double* pf = a.part_f + ((size_t)b * nsub + q) * a.Rp + rr;
+            double* pg = a.part_g + ((size_t)b * nsub + q) * a.Rp + rr;
+            F += *pf;
+            G += *pg;
+            *pf = 0.0;
+            *pg = 0.0;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            F += __shfl_xor_sync(0xffffffffu, F, o);
+            G += __shfl_xor_sync(0xffffffffu, G, o);
+        }
+        if (lane == 0) {
+            out_f[idx] = F;
+            out_g[idx] = G;
+        }
+    }
+}
+
 // Persistent cooperative kernel: the sweeps of one round for every instance
 // of the batch.  Each warp keeps one replica group (its lanes = replicas
 // 32*gi .. 32*gi+31 of every instance), so a lane's slot label, beta, 2P and
 // stream key are loaded once per instance instead of per update.
-template <int D>
+template <int D, bool HIST>
 __global__ void __launch_bounds__(kSlot2Threads, 2)
 slot2_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, int do_energy) {
     cg::grid_group grid = cg::this_grid();
@@ -142,7 +170,8 @@ slot2_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
     const bool live = r < a.R;
     for (int swp = 0; swp < n_sweeps; ++swp) {
         const uint64_t t = (uint64_t)(t0 + swp);
-        const bool count = do_energy && swp == n_sweeps - 1;
+        const bool hist = HIST && (int64_t)t >= a.hist_t0;
+        const bool count = (do_energy && swp == n_sweeps - 1) || hist;
         int cur_b = -1;
         double beta = 0.0, two_p = 0.0;
         uint64_t key = 0;
@@ -187,41 +216,32 @@ slot2_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
             a.part_f[((size_t)cur_b * nsub + sw) * a.Rp + r] += fl;
             a.part_g[((size_t)cur_b * nsub + sw) * a.Rp + r] += gl;
         }
+        if (HIST && hist) {  // probe: this sweep's (f, g) of every replica into the history
+            grid.sync();
+            const size_t row = (size_t)((int64_t)t - a.hist_t0) * a.B * a.R;
+            s2_reduce(a, gw, lane, nsub, a.hist_f + row, a.hist_g + row);
+            grid.sync();
+        }
     }
     if (!do_energy) return;
     grid.sync();
-    // fixed-order reduction of the per-warp partials (one warp per replica,
-    // lanes take strided partials, then a fixed shuffle tree); clears them
-    for (int idx = gw; idx < a.B * a.R; idx += gridDim.x * (blockDim.x >> 5)) {
-        const int b = idx / a.R, rr = idx % a.R;
-        double F = 0.0, G = 0.0;
-        for (int q = lane; q < nsub; q += 32) {
-            double* pf = a.part_f + ((size_t)b * nsub + q) * a.Rp + rr;
-            double* pg = a.part_g + ((size_t)b * nsub + q) * a.Rp + rr;
-            F += *pf;
-            G += *pg;
-            *pf = 0.0;
-            *pg = 0.0;
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            F += __shfl_xor_sync(0xffffffffu, F, o);
-            G += __shfl_xor_sync(0xffffffffu, G, o);
-        }
-        if (lane == 0) {
-            a.f[idx] = F;
-            a.g[idx] = G;
-        }
-    }
+    s2_reduce(a, gw, lane, nsub, a.f, a.g);
 }
 
-template __global__ void slot2_sweep_kernel<4>(const __grid_constant__ S2Args, int64_t, int, int);
-template __global__ void slot2_sweep_kernel<8>(const __grid_constant__ S2Args, int64_t, int, int);
-template __global__ void slot2_sweep_kernel<16>(const __grid_constant__ S2Args, int64_t, int, int);
+template __global__ void slot2_sweep_kernel<4, false>(const __grid_constant__ S2Args, int64_t, int, int);
+template __global__ void slot2_sweep_kernel<8, false>(const __grid_constant__ S2Args, int64_t, int, int);
+template __global__ void slot2_sweep_kernel<16, false>(const __grid_constant__ S2Args, int64_t, int, int);
+template __global__ void slot2_sweep_kernel<4, true>(const __grid_constant__ S2Args, int64_t, int, int);
+template __global__ void slot2_sweep_kernel<8, true>(const __grid_constant__ S2Args, int64_t, int, int);
+template __global__ void slot2_sweep_kernel<16, true>(const __grid_constant__ S2Args, int64_t, int, int);
 
-void* slot2_sweep_fn(int D) {
-    return D <= 4 ? (void*)slot2_sweep_kernel<4>
-                  : (D <= 8 ? (void*)slot2_sweep_kernel<8> : (void*)slot2_sweep_kernel<16>);
+// hist = the probe variant (per-sweep energies into a history)
+void* slot2_sweep_fn(int D, bool hist) {
+    if (hist)
+        return D <= 4 ? (void*)slot2_sweep_kernel<4, true>
+                      : (D <= 8 ? (void*)slot2_sweep_kernel<8, true> : (void*)slot2_sweep_kernel<16, true>);
+    return D <= 4 ? (void*)slot2_sweep_kernel<4, false>
+                  : (D <= 8 ? (void*)slot2_sweep_kernel<8, false> : (void*)slot2_sweep_kernel<16, false>);
 }
 
 // One block per instance: that instance's swap phase, record and counters.
@@ -306,7 +326,7 @@ __global__ void slot2_extract_kernel(const __grid_constant__ S2Args a, const __g
     }
 }
 
-__global__ void slot2_init_kernel(const __grid_constant__ S2Args a, const uint64_t* seeds) {
+__global__ void slot2_init_kernel(const __grid_constant__ S2Args a, const uint64_t* init_keys) {
     const int b = blockIdx.y;
     const SInst& in = a.inst[b];
     const long long total = (long long)in.n * a.Rp;
@@ -314,12 +334,35 @@ __global__ void slot2_init_kernel(const __grid_constant__ S2Args a, const uint64
          q += (long long)gridDim.x * blockDim.x) {
         const int i = (int)(q / a.Rp), m = (int)(q % a.Rp);
         int8_t v = 1;
-        if (m < a.R) {  // random_state with the init stream of replica m (engine.cpp:100-101)
-            const uint64_t key = derive_seed(seeds[b], kPurposeInit, (uint64_t)m);
+        if (m < a.R) {  // random_state with replica m's init stream (engine.cpp:100-101,
+                        // schedule.cpp:30-31 for probes), draw i
+            const uint64_t key = init_keys[(size_t)b * a.R + m];
             v = (stream_bits(key, (uint64_t)i) >> 63) ? (int8_t)1 : (int8_t)-1;
         }
         a.spins[in.spin_off + q] = v;
     }
+}
+
+}  // namespace tg
+
+namespace tg {
+
+// Probe moments (schedule.cpp:34-51): the four pooled sums over the history in
+// the reference's order (chain-major, then sweep), one thread per sum, with
+// unfused FP64 arithmetic as on the host.
+__global__ void probe_moments_kernel(const double* hist_f, const double* hist_g, int R, int kept,
+                                     double penalty, double* out) {
+    const int k = threadIdx.x;
+    if (k >= 4) return;
+    double acc = 0.0;
+    for (int c = 0; c < R; ++c)
+        for (int s = 0; s < kept; ++s) {
+            const double f = hist_f[(size_t)s * R + c], g = hist_g[(size_t)s * R + c];
+            const double e = __dadd_rn(f, __dmul_rn(penalty, g));
+            const double x = k == 0 ? e : (k == 1 ? __dmul_rn(e, e) : (k == 2 ? g : __dmul_rn(g, g)));
+            acc = __dadd_rn(acc, x);
+        }
+    out[k] = acc;
 }
 
 }  // namespace tg
