@@ -191,6 +191,28 @@ int tg_run_jcolumn(tg_ctx* ctx, int n_betas, const double* betas, double p_fixed
                    const tg_run_config* cfg, tg_baseline_record* out, int64_t out_cap,
                    double* feasible_fraction);
 
+/* ---- Decoded-sample KL curve on the device (kl_curve, analysis.cpp:215-241) ----
+ * Attach a decoder to the context's following SLOT-engine runs on one GPU
+ * (tg_run, tg_init + tg_advance, tg_batch_run -- one curve per instance; AUTO
+ * picks SLOT while a decoder is set): after every round the target replica of
+ * each instance is decoded on the device
+ * through the copy map (decode, constraints.cpp:149-162: majority vote over the
+ * logical spin's copies, ties to the first copy; infeasible when chain-adjacent
+ * copies differ), added to a device histogram (skipped when infeasible and
+ * discard_infeasible), and the KL divergence of the accumulated histogram
+ * against the exact Boltzmann distribution of the logical model at beta
+ * (enumerate_boltzmann, oracle.cpp:154-165, computed once on the host) is
+ * evaluated (kl_divergence, oracle.cpp:178-195).  copy_offsets[n_logical+1],
+ * copies[]: physical spins (caller order) of logical spin u in chain order.
+ * Read the curve with tg_get_kl_curve (rounds are 1-based; kl is NaN while the
+ * histogram is empty).  n_logical <= 20. */
+int tg_set_kl_decoder(tg_ctx* ctx, int n_logical, int n_couplings, const int32_t* li,
+                      const int32_t* lj, const double* lw, const double* lh, double beta,
+                      const int32_t* copy_offsets, const int32_t* copies, int discard_infeasible);
+int tg_clear_kl_decoder(tg_ctx* ctx);
+int tg_get_kl_curve(tg_ctx* ctx, int instance, int64_t first_round, int64_t n, double* kl,
+                    int64_t* samples);
+
 /* ---- Schedule probes and the adaptive ladder (schedule.cpp:18-163) ----
  * tg_probe_population = probe_population (schedule.hpp:44-48) over the
  * context's problem: n_chains independent chains at (beta, penalty), chain c

@@ -282,6 +282,50 @@ def build_schedule(pr, rule="metropolis", impl="port", **cfg):
             [_stats_dict(stats[k]) for k in range(min(ns.value, cap))], bool(be.value))
 
 
+class _Decoder(C.Structure):
+    _fields_ = [("logical", C.c_void_p), ("copy_off", C.c_void_p), ("copies", C.c_void_p)]
+
+
+def _decoder(logical_pr, copies):
+    lp, _, keep = _marshal(logical_pr, [1.0], [0.0], 1, 1, 1, "metropolis", "slot")
+    off = np.zeros(len(copies) + 1, np.int32)
+    off[1:] = np.cumsum([len(c) for c in copies])
+    flat = np.ascontiguousarray(np.concatenate([np.asarray(c, np.int32) for c in copies]), np.int32)
+    keep.update(lp=lp, off=off, flat=flat)
+    return _Decoder(C.cast(C.pointer(lp), C.c_void_p), _ptr(off), _ptr(flat)), keep
+
+
+def enumerate_boltzmann(logical_pr, beta):
+    p, _, keep = _marshal(logical_pr, [1.0], [0.0], 1, 1, 1, "metropolis", "slot")
+    probs = np.zeros(1 << logical_pr.n)
+    err = C.create_string_buffer(512)
+    rc = port_lib().tgo_enumerate_boltzmann(C.byref(p), C.c_double(beta), _ptr(probs), None, err, 512)
+    if rc != 0:
+        raise OracleError(rc, err.value.decode())
+    return probs
+
+
+def kl_curve(pr, betas, penalties, total_sweeps, sps, seed, logical_pr, copies, beta,
+             discard_infeasible=False, rule="metropolis", impl="port", threads=1):
+    """run_2dpt + kl_curve (analysis.cpp:215-241) on the port or a reference build;
+    returns (t, samples, kl) per round."""
+    p, c, keep = _marshal(pr, betas, penalties, total_sweeps, sps, seed, rule, "slot")
+    dec, keep2 = _decoder(logical_pr, copies)
+    rounds = int(total_sweeps) // max(int(sps), 1)
+    t, smp, kl = np.zeros(rounds, np.int64), np.zeros(rounds, np.int64), np.zeros(rounds)
+    err = C.create_string_buffer(512)
+    if impl == "port":
+        rc = port_lib().tgo_kl_curve(C.byref(p), C.byref(c), C.byref(dec), C.c_double(beta),
+                                     int(discard_infeasible), _ptr(t), _ptr(smp), _ptr(kl), err, 512)
+    else:
+        rc = ref_lib(impl.split(":", 1)[1]).tgr_kl_curve(
+            C.byref(p), C.byref(c), C.byref(dec), C.c_double(beta), int(discard_infeasible),
+            int(threads), _ptr(t), _ptr(smp), _ptr(kl), err, 512)
+    if rc != 0:
+        raise OracleError(rc, err.value.decode())
+    return t, smp, kl
+
+
 def ref_timed(variant, pr, betas, penalties, total_sweeps, sps=1, seed=1, threads=1) -> float:
     """Run the reference build once; returns the last target f (for timing legs)."""
     p, c, keep = _marshal(pr, betas, penalties, total_sweeps, sps, seed, "metropolis", "slot")

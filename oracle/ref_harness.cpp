@@ -19,6 +19,10 @@
 #include "tempergrid/errors.hpp"
 #include "tempergrid/ising.hpp"
 #include "tempergrid/schedule.hpp"
+#ifndef TGREF_NO_SCHEDULE
+#include "tempergrid/analysis.hpp"
+#include "tempergrid/oracle.hpp"
+#endif
 
 #include "philox_ref.h"
 #include "tg_oracle.h"
@@ -304,6 +308,47 @@ extern "C" int tgr_build_schedule(const tgo_problem* p, const tgo_schedule_cfg* 
     } catch (const tempergrid::config_error& e) {
         put_err(err, errlen, e.what());
         return 2;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return 1;
+    }
+}
+// run_2dpt + tempergrid::kl_curve (analysis.cpp:215-241) with the reference's
+// own decode (constraints.cpp:149-162) and enumerate_boltzmann (oracle.cpp).
+extern "C" int tgr_kl_curve(const tgo_problem* p, const tgo_run_cfg* cfg, const tgo_decoder* dec,
+                            double beta, int discard, int threads, std::int64_t* t,
+                            std::int64_t* samples, double* kl, char* err, int errlen) {
+    using namespace tempergrid;
+    try {
+        const ConstrainedProblem problem = make_problem(p);
+        Schedule schedule;
+        schedule.betas.assign(cfg->betas, cfg->betas + cfg->n_betas);
+        schedule.penalties.assign(cfg->penalties, cfg->penalties + cfg->n_penalties);
+        RunConfig rc;
+        rc.total_sweeps = cfg->total_sweeps;
+        rc.sweeps_per_swap = cfg->sweeps_per_swap;
+        rc.seed = cfg->seed;
+        rc.threads = threads;
+        const Trace trace = run_2dpt(problem, schedule, rc);
+        const ConstrainedProblem lp = make_problem(dec->logical);
+        SparsificationMap map;
+        map.n_logical = dec->logical->n;
+        map.n_physical = p->n;
+        for (int u = 0; u < map.n_logical; ++u)
+            map.copies.emplace_back(dec->copies + dec->copy_off[u], dec->copies + dec->copy_off[u + 1]);
+        const auto pts = kl_curve(trace, map, lp.cost, beta, discard != 0);
+        for (std::size_t k = 0; k < pts.size(); ++k) {
+            t[k] = pts[k].t;
+            samples[k] = pts[k].samples;
+            kl[k] = pts[k].kl;
+        }
+        return 0;
+    } catch (const tempergrid::config_error& e) {
+        put_err(err, errlen, e.what());
+        return 2;
+    } catch (const tempergrid::resource_error& e) {
+        put_err(err, errlen, e.what());
+        return 3;
     } catch (const std::exception& e) {
         put_err(err, errlen, e.what());
         return 1;

@@ -815,3 +815,87 @@ done:
     free(tmp);
     return rc;
 }
+
+/* enumerate_boltzmann (oracle.cpp:86-165): energies by encoding (bit i of the
+ * encoding = spin i is +1, oracle.cpp:17-29), max-shifted exponentials summed
+ * in encoding order, then normalised. */
+int tgo_enumerate_boltzmann(const tgo_problem* lp, double beta, double* probs,
+                            double* log_partition, char* err, int errlen) {
+    if (lp->n > 24) {
+        set_err(err, errlen, "exact enumeration refused for %d spins (limit 24)", lp->n);
+        return TGO_RESOURCE_ERROR;
+    }
+    model_t m;
+    int rc = model_build(&m, lp->n, lp->n_couplings, lp->ci, lp->cj, lp->cw, lp->fields, err, errlen);
+    if (rc) return rc;
+    const uint64_t K = (uint64_t)1 << lp->n;
+    int8_t* st = (int8_t*)malloc((size_t)lp->n);
+    double max_log = -INFINITY;
+    for (uint64_t enc = 0; enc < K; ++enc) {
+        for (int i = 0; i < lp->n; ++i) st[i] = ((enc >> i) & 1) ? (int8_t)1 : (int8_t)-1;
+        probs[enc] = model_energy(&m, st);
+        const double x = -beta * probs[enc];
+        if (max_log < x) max_log = x;
+    }
+    double sum = 0.0;
+    for (uint64_t enc = 0; enc < K; ++enc) {
+        probs[enc] = exp(-beta * probs[enc] - max_log);
+        sum += probs[enc];
+    }
+    if (log_partition) *log_partition = max_log + log(sum);
+    for (uint64_t enc = 0; enc < K; ++enc) probs[enc] /= sum;
+    free(st);
+    model_free(&m);
+    return TGO_OK;
+}
+
+int tgo_kl_curve(const tgo_problem* prob, const tgo_run_cfg* cfg, const tgo_decoder* dec,
+                 double beta, int discard_infeasible, int64_t* t, int64_t* samples, double* kl,
+                 char* err, int errlen) {
+    const int nl = dec->logical->n, n = prob->n;
+    const uint64_t K = (uint64_t)1 << (nl > 24 ? 0 : nl);
+    double* probs = (double*)malloc(sizeof(double) * (size_t)K);
+    int rc = tgo_enumerate_boltzmann(dec->logical, beta, probs, NULL, err, errlen);
+    if (rc) { free(probs); return rc; }
+    const int64_t rounds = cfg->sweeps_per_swap >= 1 ? cfg->total_sweeps / cfg->sweeps_per_swap : 0;
+    int8_t* states = (int8_t*)malloc((size_t)(rounds > 0 ? rounds : 1) * (size_t)n);
+    tgo_outputs o;
+    memset(&o, 0, sizeof o);
+    o.states = states;
+    rc = tgo_run_2dpt(prob, cfg, &o, err, errlen);
+    uint64_t* cnt = (uint64_t*)calloc((size_t)K, sizeof(uint64_t));
+    uint64_t total = 0;
+    for (int64_t k = 0; rc == TGO_OK && k < rounds; ++k) {
+        const int8_t* ph = states + (size_t)k * n;
+        uint64_t enc = 0;
+        int feasible = 1;
+        for (int u = 0; u < nl; ++u) { /* decode, constraints.cpp:149-160 */
+            int sum = 0;
+            for (int q = dec->copy_off[u]; q < dec->copy_off[u + 1]; ++q) sum += ph[dec->copies[q]];
+            const int8_t v = sum != 0 ? (sum > 0 ? 1 : -1) : ph[dec->copies[dec->copy_off[u]]];
+            if (v > 0) enc |= (uint64_t)1 << u;
+            for (int q = dec->copy_off[u]; q + 1 < dec->copy_off[u + 1]; ++q)
+                if (ph[dec->copies[q]] != ph[dec->copies[q + 1]]) feasible = 0;
+        }
+        if (feasible || !discard_infeasible) { ++cnt[enc]; ++total; }
+        t[k] = (k + 1) * cfg->sweeps_per_swap;
+        samples[k] = (int64_t)total;
+        if (total == 0) { kl[k] = NAN; continue; }
+        double acc = 0.0; /* kl_divergence, oracle.cpp:178-195 (std::map order = ascending) */
+        for (uint64_t e = 0; e < K; ++e) {
+            if (!cnt[e]) continue;
+            const double ph_ = (double)cnt[e] / (double)total;
+            if (probs[e] <= 0.0) {
+                set_err(err, errlen, "kl: target has zero mass on an observed state");
+                rc = TGO_CONFIG_ERROR;
+                break;
+            }
+            acc += ph_ * log(ph_ / probs[e]);
+        }
+        kl[k] = acc;
+    }
+    free(cnt);
+    free(states);
+    free(probs);
+    return rc;
+}

@@ -117,6 +117,24 @@ int tgo_build_schedule(const tgo_problem* prob, const tgo_schedule_cfg* cfg, int
                        tgo_probe_stats* stats, int stats_cap, int* n_stats, int* budget_exhausted,
                        char* err, int errlen);
 
+/* Decoded-sample KL (analysis.cpp:215-241, decode constraints.cpp:149-162,
+ * enumerate_boltzmann oracle.cpp:105-165, kl_divergence oracle.cpp:178-195).
+ * logical: the logical model; copy_off[n_logical+1] / copies: physical spins
+ * of each logical spin in chain order. */
+typedef struct {
+    const tgo_problem* logical; /* only n, couplings, fields are used */
+    const int* copy_off;
+    const int* copies;
+} tgo_decoder;
+
+/* probs[2^n] (guard: n <= 24, resource error beyond); log_partition optional */
+int tgo_enumerate_boltzmann(const tgo_problem* logical, double beta, double* probs,
+                            double* log_partition, char* err, int errlen);
+/* run_2dpt (cfg) + kl_curve: t/samples/kl per round (kl NaN while empty). */
+int tgo_kl_curve(const tgo_problem* prob, const tgo_run_cfg* cfg, const tgo_decoder* dec,
+                 double beta, int discard_infeasible, int64_t* t, int64_t* samples, double* kl,
+                 char* err, int errlen);
+
 /* engine.cpp:18-32 */
 double tgo_p_swap_probability(double beta, double d_penalty, double dg);
 double tgo_beta_swap_probability(double d_beta, double d_energy);

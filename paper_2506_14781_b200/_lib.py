@@ -108,6 +108,9 @@ def lib() -> C.CDLL:
     L.tg_batch_get_state.argtypes = [vp, C.c_int, C.c_int, vp]
     L.tg_batch_get_counters.argtypes = [vp, C.c_int, vp, vp, vp, vp]
     L.tg_run_jcolumn.argtypes = [vp, C.c_int, vp, C.c_double, C.c_int, vp, vp, C.c_int64, vp]
+    L.tg_set_kl_decoder.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, vp, C.c_double, vp, vp, C.c_int]
+    L.tg_clear_kl_decoder.argtypes = [vp]
+    L.tg_get_kl_curve.argtypes = [vp, C.c_int, C.c_int64, C.c_int64, vp, vp]
     L.tg_probe_population.argtypes = [vp, C.c_double, C.c_double, C.c_int, C.c_int, C.c_uint64,
                                       C.c_int, vp]
     L.tg_build_schedule.argtypes = [vp, vp, vp, C.c_int, vp, vp, C.c_int, vp, vp, C.c_int, vp, vp]
@@ -125,5 +128,6 @@ EXPORTED = [
     "tg_set_profiling", "tg_canonical_order", "tg_p_swap_probability", "tg_beta_swap_probability",
     "tg_general_swap_probability", "tg_swap_phase_host", "tg_partition", "tg_batch_clear",
     "tg_batch_add", "tg_batch_run", "tg_batch_get_state", "tg_batch_get_counters",
-    "tg_run_jcolumn", "tg_probe_population", "tg_build_schedule",
+    "tg_run_jcolumn", "tg_probe_population", "tg_build_schedule", "tg_set_kl_decoder",
+    "tg_clear_kl_decoder", "tg_get_kl_curve",
 ]

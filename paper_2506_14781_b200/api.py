@@ -255,6 +255,36 @@ class Engine:
     def stream_ptr(self) -> int:
         return int(self._L.tg_stream(self._h) or 0)
 
+    def set_kl_decoder(self, logical: Problem, copies, beta: float, discard_infeasible: bool = False):
+        """Decoded-sample KL observer for the following SLOT-engine runs
+        (``tg_set_kl_decoder``; kl_curve, analysis.cpp:215-241)."""
+        li, lj = _arr(logical.ci, np.int32), _arr(logical.cj, np.int32)
+        lw, lh = _arr(logical.cw, np.float64), _arr(logical.fields, np.float64)
+        off = np.zeros(len(copies) + 1, np.int32)
+        off[1:] = np.cumsum([len(c) for c in copies])
+        flat = _arr(np.concatenate([np.asarray(c, np.int64) for c in copies]) if len(copies) else
+                    np.zeros(0), np.int32)
+        self._check(self._L.tg_set_kl_decoder(self._h, logical.n, len(li), _p(li), _p(lj), _p(lw),
+                                              _p(lh), float(beta), _p(off), _p(flat),
+                                              1 if discard_infeasible else 0))
+        self._kl_k = 1 << logical.n
+
+    def clear_kl_decoder(self):
+        self._check(self._L.tg_clear_kl_decoder(self._h))
+
+    def kl_curve(self, instance: int = 0, rounds: Optional[int] = None,
+                 sweeps_per_swap: int = 1) -> List["KlPoint"]:
+        """The device KL curve of the last decoded run (KlPoint, analysis.hpp:74-79)."""
+        if rounds is None:
+            rounds = int(self.info()["rounds_done"])
+        kl = np.zeros(rounds)
+        smp = np.zeros(rounds, np.int64)
+        self._check(self._L.tg_get_kl_curve(self._h, int(instance), 1, int(rounds), _p(kl), _p(smp)))
+        k = self._kl_k
+        return [KlPoint(int((r + 1) * sweeps_per_swap), int(smp[r]), float(kl[r]),
+                        (k - 1) / (2.0 * smp[r]) if smp[r] > 0 else float("nan"))
+                for r in range(rounds)]
+
     def set_profiling(self, on: bool):
         self._check(self._L.tg_set_profiling(self._h, 1 if on else 0))
 
@@ -398,6 +428,34 @@ def run_2dpt_batch(problems: Sequence[Problem], schedules: Sequence[Schedule], c
         eng._check(L.tg_batch_run(eng._h, C.byref(c), cb, None))
         eng._batch_problems = problems
         return traces
+    finally:
+        if engine is None:
+            eng.close()
+
+
+@dataclass
+class KlPoint:
+    """``tempergrid::KlPoint`` (analysis.hpp:74-79)."""
+    t: int
+    samples: int
+    kl: float
+    iid_reference: float
+
+
+def run_2dpt_kl(problem: Problem, schedule: Schedule, cfg: RunConfig, logical: Problem, copies,
+                beta: float, discard_infeasible: bool = False, device: int = 0,
+                engine: Optional[Engine] = None) -> List[KlPoint]:
+    """``kl_curve(run_2dpt(...), map, logical, beta, discard)`` (analysis.cpp:215-241)
+    with the decode, histogram and KL evaluated on the device every round."""
+    eng = engine or Engine(device)
+    try:
+        eng.set_kl_decoder(logical, copies, beta, discard_infeasible)
+        eng.set_problem(problem)
+        eng.set_schedule(schedule.betas, schedule.penalties)
+        c = RunConfig(**{**cfg.__dict__, "engine": "slot", "store_states": False, "digest": False})
+        eng.run(c, None, flags=0)
+        rounds = int(cfg.total_sweeps) // max(int(cfg.sweeps_per_swap), 1)
+        return eng.kl_curve(0, rounds, int(cfg.sweeps_per_swap))
     finally:
         if engine is None:
             eng.close()

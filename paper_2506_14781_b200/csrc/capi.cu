@@ -179,6 +179,14 @@ struct Slot2 {
     DBuf<uint64_t> d_init_keys;
     DBuf<double> d_hist_f, d_hist_g, d_moments;
     std::vector<SInst> h_inst;
+    // KL observer buffers
+    bool kl_on = false;
+    int64_t kl_cap = 0;
+    DBuf<int> d_kl_off, d_kl_map, d_kl_err;
+    DBuf<double> d_kl_p, d_kl;
+    DBuf<uint32_t> d_kl_hist;
+    DBuf<unsigned long long> d_kl_total;
+    DBuf<int64_t> d_kl_samples;
     uint64_t probe_gen = 0;
     int probe_chains = 0, probe_rule = -1;
 };
@@ -247,6 +255,14 @@ struct tg_ctx {
     DBuf<float> d_h32;
     float slot_eps = 0.0f, slot_beta_max = 0.0f;
     DBuf<uint64_t> d_slot_key;
+
+    // decoded-sample KL observer (analysis.cpp:215-241), SLOT engine v2
+    struct {
+        bool on = false;
+        int n_logical = 0, discard = 0;
+        std::vector<int> copy_off, copies;   // caller physical indices, chain order
+        std::vector<double> probs;           // exact logical Boltzmann, 2^n_logical
+    } kl;
 
     // SLOT engine v2 (single instance and batches)
     std::vector<BatchInst> batch;
@@ -812,7 +828,10 @@ void do_init(tg_ctx& c, const tg_run_config* cfg) {
     c.R = c.I * c.J;
     std::string why;
     int eng = cfg->engine;
-    if (eng == TG_ENGINE_AUTO) eng = plane_eligible(c, nullptr) ? TG_ENGINE_PLANE : TG_ENGINE_SLOT;
+    if (eng == TG_ENGINE_AUTO)
+        eng = (!c.kl.on && plane_eligible(c, nullptr)) ? TG_ENGINE_PLANE : TG_ENGINE_SLOT;
+    if (c.kl.on && (eng != TG_ENGINE_SLOT || c.world != 1 || std::getenv("TG_SLOT_V1")))
+        fail(TG_ERR_CONFIG, "kl decoder: needs the single-GPU SLOT engine");
     if (eng == TG_ENGINE_PLANE && !plane_eligible(c, &why))
         fail(TG_ERR_CONFIG, "plane engine: instance not eligible (%s)", why.c_str());
     if (eng != TG_ENGINE_PLANE && eng != TG_ENGINE_SLOT) fail(TG_ERR_CONFIG, "unknown engine %d", eng);
@@ -1212,6 +1231,25 @@ S2Args s2_args(tg_ctx& c) {
     return a;
 }
 
+KLArgs kl_args(tg_ctx& c) {
+    Slot2& S = c.s2;
+    KLArgs k{};
+    k.n_logical = c.kl.n_logical;
+    k.K = 1 << c.kl.n_logical;
+    k.discard = c.kl.discard;
+    k.ncopies = (int)c.kl.copies.size();
+    k.map_off = S.d_kl_off.p;
+    k.map = S.d_kl_map.p;
+    k.p = S.d_kl_p.p;
+    k.hist = S.d_kl_hist.p;
+    k.total = S.d_kl_total.p;
+    k.kl = S.d_kl.p;
+    k.samples = S.d_kl_samples.p;
+    k.cap = S.kl_cap;
+    k.error = S.d_kl_err.p;
+    return k;
+}
+
 S2Swap s2_swap(tg_ctx& c) {
     Slot2& S = c.s2;
     S2Swap s{};
@@ -1417,6 +1455,30 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
     S.h_rec.resize((size_t)B * cap);
     S.h_acc.resize((flags & TG_REC_COUNTERS) ? (size_t)B * cap * (np + nb + 1) : 0);
     S.h_states.resize(per_round_states * cap);
+    // decoded-sample KL observer
+    S.kl_on = c.kl.on && !S.probe;
+    if (S.kl_on) {
+        const int nc = (int)c.kl.copies.size(), K = 1 << c.kl.n_logical;
+        std::vector<int> map((size_t)B * nc);
+        for (int b = 0; b < B; ++b)
+            for (int q = 0; q < nc; ++q) {
+                const int x = c.kl.copies[q];
+                if (x < 0 || x >= S.prep[b].n) fail(TG_ERR_CONFIG, "kl decoder: copy %d out of range", x);
+                map[(size_t)b * nc + q] = S.prep[b].inv[x];
+            }
+        S.d_kl_off.upload(c.kl.copy_off, st);
+        S.d_kl_map.upload(map, st);
+        S.d_kl_p.upload(c.kl.probs, st);
+        S.d_kl_hist.alloc((size_t)B * K);
+        S.d_kl_hist.zero(st);
+        S.d_kl_total.alloc(B);
+        S.d_kl_total.zero(st);
+        S.kl_cap = std::max<int64_t>(1, cfg->total_sweeps / std::max<int64_t>(1, cfg->sweeps_per_swap));
+        S.d_kl.alloc((size_t)B * S.kl_cap);
+        S.d_kl_samples.alloc((size_t)B * S.kl_cap);
+        S.d_kl_err.alloc(1);
+        S.d_kl_err.zero(st);
+    }
     // initial configurations (engine.cpp:98-106)
     S2Args a = s2_args(c);
     slot2_init_kernel<<<dim3(c.sms * 4, B), 256, 0, st>>>(a, S.d_init_keys.p);
@@ -1507,6 +1569,11 @@ void s2_advance(tg_ctx& c, int64_t n_rounds, const BatchSinkCtx& sink) {
         slot2_swap_kernel<<<S.B, kSwapThreads, 0, st>>>(s, round, S.swap_base, filled, flags);
         CK(cudaGetLastError());
         c.other_launches++;
+        if (S.kl_on) {
+            slot2_kl_kernel<<<S.B, 1024, 0, st>>>(a, S.d_slot_state.p, kl_args(c), round);
+            CK(cudaGetLastError());
+            c.other_launches++;
+        }
         if (flags & (TG_REC_DIGEST | TG_REC_STATE | TG_REC_GRID)) {
             slot2_extract_kernel<<<dim3(std::max(1, c.sms / 2), S.B), 256, 0, st>>>(
                 a, s, filled, (flags & TG_REC_GRID) ? 1 : 0);
@@ -1532,6 +1599,11 @@ void s2_advance(tg_ctx& c, int64_t n_rounds, const BatchSinkCtx& sink) {
     s2_drain(c, filled, first, sink);
     CK(cudaStreamSynchronize(st));
     c.last_sweep_ms = sweep_ms;
+    if (S.kl_on) {
+        int e = 0;
+        CK(cudaMemcpy(&e, S.d_kl_err.p, sizeof e, cudaMemcpyDeviceToHost));
+        if (e) fail(TG_ERR_CONFIG, "kl: target has zero mass on an observed state");
+    }
 }
 
 
@@ -2056,6 +2128,7 @@ int tg_batch_run(tg_ctx* ctx, const tg_run_config* cfg, tg_batch_sink_fn sink, v
         ctx->s2.probe = false;
         s2_build(*ctx, cfg);
         s2_advance(*ctx, cfg->total_sweeps / cfg->sweeps_per_swap, BatchSinkCtx{sink, user});
+        ctx->rounds_done = ctx->s2.rounds_done;
     });
 }
 
@@ -2151,6 +2224,82 @@ int tg_run_jcolumn(tg_ctx* ctx, int n_betas, const double* betas, double p_fixed
         ctx->batch.clear();
         if (feasible_fraction)
             *feasible_fraction = m.sample_total == 0 ? 0.0 : (double)m.feasible_total / (double)m.sample_total;
+    });
+}
+
+int tg_set_kl_decoder(tg_ctx* ctx, int n_logical, int n_couplings, const int32_t* li,
+                      const int32_t* lj, const double* lw, const double* lh, double beta,
+                      const int32_t* copy_offsets, const int32_t* copies, int discard_infeasible) {
+    if (!ctx) return TG_ERR_CONFIG;
+    return guard(ctx, [&] {
+        // IsingModel validation (ising.cpp:21-46) of the logical model
+        BatchInst lm;
+        load_problem(lm, n_logical, n_couplings, li, lj, lw, lh, 0, nullptr, nullptr);
+        if (n_logical > 20)
+            fail(TG_ERR_RESOURCE, "kl decoder: %d logical spins (device histogram limit 20)", n_logical);
+        if (!copy_offsets || !copies) fail(TG_ERR_CONFIG, "kl decoder: missing copy map");
+        std::vector<int> off(copy_offsets, copy_offsets + n_logical + 1);
+        if (off[0] != 0) fail(TG_ERR_CONFIG, "kl decoder: copy offsets must start at 0");
+        for (int u = 0; u < n_logical; ++u)
+            if (off[u + 1] <= off[u]) fail(TG_ERR_CONFIG, "kl decoder: logical spin %d has no copies", u);
+        // enumerate_boltzmann (oracle.cpp:86-165): couplings sorted (i, j) as the
+        // IsingModel stores them, energy = -sum w s_i s_j - sum h s_i, max-shifted
+        // exponentials summed in encoding order
+        std::vector<int> idx(lm.ci.size());
+        for (size_t q = 0; q < idx.size(); ++q) idx[q] = (int)q;
+        std::sort(idx.begin(), idx.end(), [&](int x, int y) {
+            return lm.ci[x] != lm.ci[y] ? lm.ci[x] < lm.ci[y] : lm.cj[x] < lm.cj[y];
+        });
+        const size_t K = (size_t)1 << n_logical;
+        std::vector<double> pr(K);
+        double max_log = -std::numeric_limits<double>::infinity();
+        for (size_t enc = 0; enc < K; ++enc) {
+            double e = 0.0;
+            for (int q : idx) {
+                const double si = ((enc >> lm.ci[q]) & 1) ? 1.0 : -1.0;
+                const double sj = ((enc >> lm.cj[q]) & 1) ? 1.0 : -1.0;
+                e -= lm.cw[q] * si * sj;
+            }
+            for (int i = 0; i < n_logical; ++i) e -= lm.h[i] * (((enc >> i) & 1) ? 1.0 : -1.0);
+            pr[enc] = e;
+            max_log = std::max(max_log, -beta * e);
+        }
+        double sum = 0.0;
+        for (size_t enc = 0; enc < K; ++enc) {
+            pr[enc] = std::exp(-beta * pr[enc] - max_log);
+            sum += pr[enc];
+        }
+        for (auto& p : pr) p /= sum;
+        ctx->kl.on = true;
+        ctx->kl.n_logical = n_logical;
+        ctx->kl.discard = discard_infeasible ? 1 : 0;
+        ctx->kl.copy_off = off;
+        ctx->kl.copies.assign(copies, copies + off[n_logical]);
+        ctx->kl.probs = std::move(pr);
+        ctx->initialised = false;
+    });
+}
+
+int tg_clear_kl_decoder(tg_ctx* ctx) {
+    if (!ctx) return TG_ERR_CONFIG;
+    ctx->kl.on = false;
+    ctx->initialised = false;
+    return TG_OK;
+}
+
+int tg_get_kl_curve(tg_ctx* ctx, int instance, int64_t first_round, int64_t n, double* kl,
+                    int64_t* samples) {
+    if (!ctx) return TG_ERR_CONFIG;
+    return guard(ctx, [&] {
+        Slot2& S = ctx->s2;
+        if (!S.ready || !S.kl_on) fail(TG_ERR_CONFIG, "kl: no decoded run on this context");
+        if (instance < 0 || instance >= S.B) fail(TG_ERR_CONFIG, "instance %d out of range", instance);
+        if (first_round < 1 || n < 0 || first_round - 1 + n > std::min<int64_t>(S.kl_cap, S.rounds_done))
+            fail(TG_ERR_CONFIG, "kl: rounds [%lld, %lld) not recorded", (long long)first_round,
+                 (long long)(first_round + n));
+        const size_t off = (size_t)instance * S.kl_cap + (size_t)(first_round - 1);
+        if (kl) CK(cudaMemcpy(kl, S.d_kl.p + off, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        if (samples) CK(cudaMemcpy(samples, S.d_kl_samples.p + off, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
     });
 }
 

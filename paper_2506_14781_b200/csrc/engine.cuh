@@ -226,6 +226,20 @@ struct S2Swap {
     int Rp;
 };
 
+// Decoded-sample histogram + KL per round (analysis.cpp:215-241).
+struct KLArgs {
+    int n_logical, K, discard, ncopies;
+    const int* map_off;            // [n_logical + 1]
+    const int* map;                // [B][ncopies] internal spin index of each copy
+    const double* p;               // [K] exact logical Boltzmann probabilities
+    uint32_t* hist;                // [B][K]
+    unsigned long long* total;     // [B]
+    double* kl;                    // [B][cap]
+    int64_t* samples;              // [B][cap]
+    int64_t cap;
+    int* error;                    // set when an observed state has zero target mass
+};
+
 // ---------------------------------------------------------------- swaps
 
 // Reference round schedule (engine.cpp:121-146,216): parity alternates every

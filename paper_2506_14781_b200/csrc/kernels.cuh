@@ -50,6 +50,8 @@ __global__ void slot2_swap_kernel(const __grid_constant__ S2Swap s, int64_t roun
 __global__ void slot2_extract_kernel(const __grid_constant__ S2Args a, const __grid_constant__ S2Swap s,
                                      int rec_idx, int all_slots);
 __global__ void slot2_init_kernel(const __grid_constant__ S2Args a, const uint64_t* init_keys);
+__global__ void slot2_kl_kernel(const __grid_constant__ S2Args a, const int32_t* slot_state,
+                                const __grid_constant__ KLArgs k, int64_t round);
 __global__ void probe_moments_kernel(const double* hist_f, const double* hist_g, int R, int kept,
                                      double penalty, double* out);
 

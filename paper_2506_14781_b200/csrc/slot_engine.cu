@@ -347,6 +347,75 @@ __global__ void slot2_init_kernel(const __grid_constant__ S2Args a, const uint64
 
 namespace tg {
 
+// One block per instance, after the round's swaps: decode the target replica
+// (decode, constraints.cpp:149-160: majority over each logical spin's copies,
+// ties to the first copy, infeasible when chain-adjacent copies differ), add it
+// to the instance's histogram (kl_curve, analysis.cpp:224-226) and evaluate
+// kl_divergence (oracle.cpp:178-195) of the accumulated histogram -- every
+// histogram bin in parallel, combined in a fixed tree order.
+__global__ void __launch_bounds__(1024)
+slot2_kl_kernel(const __grid_constant__ S2Args a, const int32_t* slot_state,
+                const __grid_constant__ KLArgs k, int64_t round) {
+    __shared__ unsigned s_enc;
+    __shared__ int s_feas;
+    __shared__ double s_red[32];
+    const int b = blockIdx.x;
+    const SInst& in = a.inst[b];
+    const int tgt = slot_state[(size_t)b * a.R + a.R - 1];
+    const int8_t* sp = a.spins + in.spin_off;
+    if (threadIdx.x == 0) { s_enc = 0u; s_feas = 1; }
+    __syncthreads();
+    const int* map = k.map + (size_t)b * k.ncopies;
+    for (int u = threadIdx.x; u < k.n_logical; u += blockDim.x) {
+        const int q0 = k.map_off[u], q1 = k.map_off[u + 1];
+        int sum = 0, feas = 1;
+        int8_t prev = 0;
+        for (int q = q0; q < q1; ++q) {
+            const int8_t v = sp[(size_t)map[q] * a.Rp + tgt];
+            sum += v;
+            if (q > q0 && v != prev) feas = 0;
+            prev = v;
+        }
+        const int8_t first = sp[(size_t)map[q0] * a.Rp + tgt];
+        const int bit = sum != 0 ? (sum > 0) : (first > 0);
+        if (bit) atomicOr(&s_enc, 1u << u);
+        if (!feas) s_feas = 0;
+    }
+    __syncthreads();
+    uint32_t* hist = k.hist + (size_t)b * k.K;
+    if (threadIdx.x == 0 && (s_feas || !k.discard)) {
+        hist[s_enc] += 1u;
+        k.total[b] += 1ull;
+    }
+    __syncthreads();
+    const unsigned long long T = k.total[b];
+    double acc = 0.0;
+    if (T > 0) {
+        const double inv_t = (double)T;
+        for (int e = threadIdx.x; e < k.K; e += blockDim.x) {
+            const uint32_t c = hist[e];
+            if (!c) continue;
+            const double ph = (double)c / inv_t;
+            const double pe = k.p[e];
+            if (pe <= 0.0) { atomicExch(k.error, 1); continue; }
+            acc += ph * log(ph / pe);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? s_red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0 && round >= 1 && round <= k.cap) {
+            k.kl[(size_t)b * k.cap + round - 1] = T > 0 ? v : __longlong_as_double(0x7ff8000000000000ll);
+            k.samples[(size_t)b * k.cap + round - 1] = (int64_t)T;
+        }
+    }
+}
+
 // Probe moments (schedule.cpp:34-51): the four pooled sums over the history in
 // the reference's order (chain-major, then sweep), one thread per sum, with
 // unfused FP64 arithmetic as on the host.
