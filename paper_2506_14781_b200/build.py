@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtempergrid_b200.so")
 CPPLIB = os.path.join(PKG, "libtempergrid_cpp.so")
-SOURCES = ["kernels.cu", "capi.cu", "plane_sweep.cu", "slot_engine.cu"]
+SOURCES = ["kernels.cu", "capi.cu", "plane_sweep.cu", "slot_engine.cu", "prep.cu"]
 HEADERS = ["engine.cuh", "kernels.cuh", "philox.cuh", "plane_device.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -48,7 +48,7 @@ def build_engine(force: bool = False, verbose: bool = False) -> str:
     units = [("kernels.cu", "kernels.o", []), ("capi.cu", "capi.o", []),
              ("plane_sweep.cu", "plane_r0.o", ["-DTG_PLANE_RULE=0"]),
              ("plane_sweep.cu", "plane_r1.o", ["-DTG_PLANE_RULE=1"]),
-             ("slot_engine.cu", "slot_engine.o", [])]
+             ("slot_engine.cu", "slot_engine.o", []), ("prep.cu", "prep.o", [])]
     procs = []
     for src, obj, extra in units:
         cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v",

@@ -12,6 +12,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -20,6 +21,7 @@
 #include <map>
 #include <string>
 #include <utility>
+#include <thread>
 #include <vector>
 #include <limits>
 
@@ -98,28 +100,71 @@ struct TgFail {
         if (r_ != ncclSuccess) fail(TG_ERR_CUDA, "%s: %s", #x, nccl().GetErrorString(r_));      \
     } while (0)
 
+// Device buffers come from the device's stream-ordered memory pool on the
+// stream of the context being served (set by guard() / create_impl): freed
+// memory stays in the pool, so the next context's allocations -- e.g. the next
+// run_2dpt call -- cost microseconds instead of cudaMalloc / cudaFree.
+thread_local cudaStream_t t_alloc_stream = nullptr;
+
 template <class T>
 struct DBuf {
     T* p = nullptr;
     size_t n = 0;
+    cudaStream_t s_ = nullptr;
     void alloc(size_t count) {
         release();
         n = count;
-        if (count) CK(cudaMalloc(&p, sizeof(T) * count));
+        s_ = t_alloc_stream;
+        if (count) CK(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, s_));
     }
     void upload(const std::vector<T>& v, cudaStream_t s) {
         alloc(v.size());
         if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, s));
     }
+    void upload(const T* src, size_t count, cudaStream_t s) {
+        alloc(count);
+        if (count) CK(cudaMemcpyAsync(p, src, sizeof(T) * count, cudaMemcpyHostToDevice, s));
+    }
+    void copy_from(const DBuf<T>& o, cudaStream_t s) {
+        alloc(o.n);
+        if (o.n) CK(cudaMemcpyAsync(p, o.p, sizeof(T) * o.n, cudaMemcpyDeviceToDevice, s));
+    }
     void zero(cudaStream_t s) {
         if (n) CK(cudaMemsetAsync(p, 0, sizeof(T) * n, s));
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, s_);
         p = nullptr;
         n = 0;
     }
     ~DBuf() { release(); }
+};
+
+// Owns the context stream; declared before every DBuf member of tg_ctx, so it
+// is destroyed after them (their stream-ordered frees are queued on a live
+// stream) and drains the stream before destroying it.
+struct StreamOwner {
+    cudaStream_t s = nullptr;
+    ~StreamOwner() {
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    }
+};
+
+// TG_HOST_TIMING=1: host-side phase timings on stderr (e2e breakdown).
+struct HostTimer {
+    const char* what;
+    std::chrono::steady_clock::time_point t0;
+    bool on;
+    explicit HostTimer(const char* w) : what(w), t0(std::chrono::steady_clock::now()),
+                                        on(std::getenv("TG_HOST_TIMING") != nullptr) {}
+    ~HostTimer() {
+        if (on)
+            std::fprintf(stderr, "[tg host] %-28s %9.3f ms\n", what,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
 };
 
 int nbits(int d) {
@@ -197,6 +242,7 @@ struct tg_ctx {
     std::string err;
     int device = 0, rank = 0, world = 1;
     int sms = 0;
+    StreamOwner stream_owner;
     cudaStream_t stream = nullptr;
     ncclComm_t comm = nullptr;
     bool profiling = false;
@@ -210,6 +256,15 @@ struct tg_ctx {
     std::vector<int> order, inv, color;  // order[k] = caller index at internal k
     int n_colors = 0;
     std::vector<int> color_start;
+    // canonical order + internal CSR computed on the device at set_problem
+    // (prep.cu); the host copies of order / inv / color are materialised only
+    // when a host-side path needs them (ensure_host_canonical)
+    bool dev_prep = false, host_canonical = false, host_arrays = false;
+    int m = 0, np = 0;
+    PrepSummary prep;
+    DBuf<int> d_raw_ci, d_raw_cj, d_raw_pa, d_raw_pb;  // caller arrays as given
+    DBuf<double> d_raw_w, d_raw_h;
+    DBuf<int> d_order_dev, d_inv_dev, d_base_dev, d_nbr_dev;
 
     bool have_schedule = false;
     std::vector<double> betas, pens;
@@ -278,9 +333,10 @@ struct tg_ctx {
     int64_t sweep_launches = 0, other_launches = 0;
 
     ~tg_ctx() {
+        t_alloc_stream = stream;
         for (auto e : ev) cudaEventDestroy(e);
         if (comm) nccl().CommDestroy(comm);
-        if (stream) cudaStreamDestroy(stream);
+        // members free their buffers on `stream`; stream_owner destroys it last
     }
 };
 
@@ -291,6 +347,7 @@ namespace {
 
 template <class F>
 int guard(tg_ctx* ctx, F&& f) {
+    if (ctx) t_alloc_stream = ctx->stream;
     try {
         f();
         if (ctx) ctx->err.clear();
@@ -346,8 +403,8 @@ void load_problem(BatchInst& bi, int n, int n_couplings, const int32_t* ci, cons
                   const int32_t* pb) {
     if (n <= 0) fail(TG_ERR_CONFIG, "model: n_spins must be positive");
     if (n_couplings < 0 || n_pairs < 0) fail(TG_ERR_CONFIG, "model: negative counts");
-    std::vector<uint64_t> keys;
     std::vector<int> a(n_couplings), b(n_couplings), qa(n_pairs), qb(n_pairs);
+    std::vector<int> row(n + 1, 0);
     for (int k = 0; k < n_couplings; ++k) {
         int x = ci[k], y = cj[k];
         if (x == y) fail(TG_ERR_CONFIG, "model: self-loop on spin %d", x);
@@ -356,13 +413,23 @@ void load_problem(BatchInst& bi, int n, int n_couplings, const int32_t* ci, cons
         if (!std::isfinite(w[k])) fail(TG_ERR_CONFIG, "model: coupling weights must be finite");
         a[k] = x;
         b[k] = y;
-        keys.push_back((uint64_t)x << 32 | (uint64_t)y);
+        row[x + 1]++;
     }
-    std::sort(keys.begin(), keys.end());
-    for (size_t k = 1; k < keys.size(); ++k)
-        if (keys[k] == keys[k - 1])
-            fail(TG_ERR_CONFIG, "model: duplicate coupling (%d, %d)", (int)(keys[k] >> 32),
-                 (int)(keys[k] & 0xffffffffu));
+    {   // duplicate check in O(E): bucket the upper endpoints by lower endpoint
+        // (counting sort), then sort each short bucket; the reported pair is the
+        // smallest duplicate, as after the reference's full sort (ising.cpp:37-46)
+        for (int i = 0; i < n; ++i) row[i + 1] += row[i];
+        std::vector<int> cur(row.begin(), row.end() - 1), ys(n_couplings);
+        for (int k = 0; k < n_couplings; ++k) ys[cur[a[k]]++] = b[k];
+        for (int i = 0; i < n; ++i) {
+            int* p0 = ys.data() + row[i];
+            int* p1 = ys.data() + row[i + 1];
+            if (p1 - p0 < 2) continue;
+            std::sort(p0, p1);
+            for (int* q = p0 + 1; q < p1; ++q)
+                if (*q == q[-1]) fail(TG_ERR_CONFIG, "model: duplicate coupling (%d, %d)", i, *q);
+        }
+    }
     for (int k = 0; k < n_pairs; ++k) {
         int x = pa[k], y = pb[k];
         if (x == y) fail(TG_ERR_CONFIG, "constraint: pair on a single spin %d", x);
@@ -389,7 +456,16 @@ void check_vec(const std::vector<double>& v, const char* what) {  // engine.cpp:
         if (v[k] <= v[k - 1]) fail(TG_ERR_CONFIG, "%s vector must be strictly increasing", what);
 }
 
-bool plane_eligible(const tg_ctx& c, std::string* why) {
+void ensure_host_arrays(tg_ctx& c);
+
+bool plane_eligible(tg_ctx& c, std::string* why) {
+    if (c.dev_prep) {
+        if (c.prep.info & kPrepNotPM1) { if (why) *why = "couplings must be +-1"; return false; }
+        if (c.prep.info & kPrepNonzeroField) { if (why) *why = "fields must be 0"; return false; }
+        if (c.prep.max_dc > kMaxDC || c.prep.max_dq > kMaxDQ) { if (why) *why = "degree bound exceeded"; return false; }
+        return true;
+    }
+    ensure_host_arrays(c);
     for (double w : c.cw) if (!(w == 1.0 || w == -1.0)) { if (why) *why = "couplings must be +-1"; return false; }
     for (double x : c.h) if (x != 0.0) { if (why) *why = "fields must be 0"; return false; }
     std::vector<int> dc(c.n, 0), dq(c.n, 0);
@@ -413,9 +489,101 @@ uint64_t threshold_heat_bath(double beta, double local) {
     return (uint64_t)std::ceil(p * 0x1.0p53);
 }
 
+void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vector<int>& chunk_off);
+
+// Host copies of the instance (indices normalised i < j as IsingModel /
+// ConstraintSet store them), fetched from the device copy on first use by a
+// host-side path (SLOT engine, batches, probes, the J-column baseline).
+void ensure_host_arrays(tg_ctx& c) {
+    if (c.host_arrays) return;
+    cudaStream_t st = c.stream;
+    c.ci.resize(c.m); c.cj.resize(c.m); c.cw.resize(c.m); c.h.resize(c.n);
+    c.pa.resize(c.np); c.pb.resize(c.np);
+    if (c.m) {
+        CK(cudaMemcpyAsync(c.ci.data(), c.d_raw_ci.p, sizeof(int) * c.m, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(c.cj.data(), c.d_raw_cj.p, sizeof(int) * c.m, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(c.cw.data(), c.d_raw_w.p, sizeof(double) * c.m, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaMemcpyAsync(c.h.data(), c.d_raw_h.p, sizeof(double) * c.n, cudaMemcpyDeviceToHost, st));
+    if (c.np) {
+        CK(cudaMemcpyAsync(c.pa.data(), c.d_raw_pa.p, sizeof(int) * c.np, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(c.pb.data(), c.d_raw_pb.p, sizeof(int) * c.np, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    for (int k = 0; k < c.m; ++k)
+        if (c.ci[k] > c.cj[k]) std::swap(c.ci[k], c.cj[k]);
+    for (int k = 0; k < c.np; ++k)
+        if (c.pa[k] > c.pb[k]) std::swap(c.pa[k], c.pb[k]);
+    c.host_arrays = true;
+}
+
+// Host copies of the canonical order (order / inv / color) for host-side
+// paths, from the device prep when it ran.
+void ensure_host_canonical(tg_ctx& c) {
+    if (c.host_canonical) return;
+    const int n = c.n;
+    c.order.resize(n);
+    c.inv.resize(n);
+    CK(cudaMemcpyAsync(c.order.data(), c.d_order_dev.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(c.inv.data(), c.d_inv_dev.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    c.color.assign(n, 0);
+    for (int col = 0; col < c.n_colors; ++col)
+        for (int k = c.color_start[col]; k < c.color_start[col + 1]; ++k) c.color[c.order[k]] = col;
+    c.host_canonical = true;
+}
+
+// PLANE engine structure from the device prep: site types and 32-site chunks
+// from the (colour, chain degree, cost degree) run summary; rows stay on the
+// device.  Same types / chunks / rows as the host construction below.
+void build_plane_structure_device(tg_ctx& c, std::vector<PlaneType>& types, std::vector<Chunk>& chunks,
+                                  std::vector<int>& chunk_off) {
+    const PrepSummary& P = c.prep;
+    const int mq1 = P.max_dq + 1, mc1 = P.max_dc + 1;
+    std::vector<int> tid_of((kMaxDC + 1) * (kMaxDQ + 1), -1);
+    chunk_off.assign(c.n_colors + 1, 0);
+    int start = 0, cur_col = -1;
+    for (size_t q = 0; q < P.run_keys.size(); ++q) {
+        const unsigned key = P.run_keys[q];
+        const int cnt = P.run_counts[q];
+        const int dc = (int)(key % mc1), dq = (int)((key / mc1) % mq1), col = (int)(key / ((unsigned)mc1 * mq1));
+        while (cur_col < col) chunk_off[++cur_col] = (int)chunks.size();
+        const int tkey = dc * (kMaxDQ + 1) + dq;
+        if (tid_of[tkey] < 0) {
+            PlaneType t{};
+            t.dc = dc;
+            t.dq = dq;
+            t.ncb = nbits(dc);
+            t.nqb = nbits(dq);
+            t.ncl = std::max(4, 1 << (t.ncb + t.nqb));
+            tid_of[tkey] = (int)types.size();
+            types.push_back(t);
+        }
+        for (int s0 = start; s0 < start + cnt; s0 += 32)
+            chunks.push_back(Chunk{s0, std::min(32, start + cnt - s0), tid_of[tkey], 0});
+        start += cnt;
+    }
+    while (cur_col < c.n_colors) chunk_off[++cur_col] = (int)chunks.size();
+    chunk_off[c.n_colors] = (int)chunks.size();
+}
+
 void build_plane(tg_ctx& c) {
+    HostTimer tm_("build_plane");
     cudaStream_t st = c.stream;
     const int n = c.n;
+    if (c.dev_prep) {
+        std::vector<PlaneType> types;
+        std::vector<Chunk> chunks;
+        std::vector<int> chunk_off;
+        build_plane_structure_device(c, types, chunks, chunk_off);
+        c.d_nbr.copy_from(c.d_nbr_dev, st);
+        c.d_chunks.upload(chunks, st);
+        CK(plane_chunk_bases(c.d_chunks.p, (int)chunks.size(), c.d_base_dev.p, st, c.sms));
+        build_plane_rest(c, types, chunk_off);
+        return;
+    }
+    ensure_host_arrays(c);
+    ensure_host_canonical(c);
     // internal adjacency as flat CSR (cost entries carry the J<0 sign bit)
     std::vector<int> dcv(n, 0), dqv(n, 0);
     for (size_t k = 0; k < c.ci.size(); ++k) { dcv[c.inv[c.ci[k]]]++; dcv[c.inv[c.cj[k]]]++; }
@@ -456,17 +624,6 @@ void build_plane(tg_ctx& c) {
         }
         site_type[i] = tid_of[key];
     }
-    if ((int)types.size() > kMaxTypes) fail(TG_ERR_RESOURCE, "plane engine: too many site types");
-    int kpw = 0, krow = 0;
-    for (auto& t : types) {
-        t.kp_off = kpw;
-        t.ktab_off = krow;
-        kpw += kKWords * t.ncl;
-        krow += t.ncl;
-    }
-    c.kpw = kpw;
-    c.ktab_row = krow;
-    c.n_types = (int)types.size();
     // chunks (colour-major; the canonical order keeps types contiguous)
     std::vector<Chunk> chunks;
     std::vector<int> chunk_off(c.n_colors + 1, 0);
@@ -483,6 +640,27 @@ void build_plane(tg_ctx& c) {
         }
     }
     chunk_off[c.n_colors] = (int)chunks.size();
+    c.d_nbr.upload(nbr, st);
+    c.d_chunks.upload(chunks, st);
+    build_plane_rest(c, types, chunk_off);
+}
+
+// Everything after the site types and chunks: threshold tables, words, keys,
+// masks, buffers and the cooperative grids.
+void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vector<int>& chunk_off) {
+    cudaStream_t st = c.stream;
+    const int n = c.n;
+    if ((int)types.size() > kMaxTypes) fail(TG_ERR_RESOURCE, "plane engine: too many site types");
+    int kpw = 0, krow = 0;
+    for (auto& t : types) {
+        t.kp_off = kpw;
+        t.ktab_off = krow;
+        kpw += kKWords * t.ncl;
+        krow += t.ncl;
+    }
+    c.kpw = kpw;
+    c.ktab_row = krow;
+    c.n_types = (int)types.size();
     // words, keys, masks: rows padded to a whole number of WV-word passes
     const int w_log = (c.R_local + 31) / 32;
     c.WV = w_log > 2 ? 4 : w_log;
@@ -519,9 +697,7 @@ void build_plane(tg_ctx& c) {
             }
         }
     }
-    c.m_cost = (int)c.ci.size();
-    c.d_nbr.upload(nbr, st);
-    c.d_chunks.upload(chunks, st);
+    c.m_cost = c.m;
     c.d_chunk_off.upload(chunk_off, st);
     c.d_color_start.upload(c.color_start, st);
     c.d_types.upload(types, st);
@@ -583,6 +759,8 @@ void build_plane(tg_ctx& c) {
 }
 
 void build_slot(tg_ctx& c) {
+    ensure_host_arrays(c);
+    ensure_host_canonical(c);
     cudaStream_t st = c.stream;
     const int n = c.n;
     if (n > 200 * 1024) fail(TG_ERR_RESOURCE, "slot engine: %d spins exceed shared memory", n);
@@ -814,6 +992,7 @@ void rebuild_planes(tg_ctx& c) {
 void s2_build(tg_ctx& c, const tg_run_config* cfg);
 
 void do_init(tg_ctx& c, const tg_run_config* cfg) {
+    HostTimer tm_("init (total)");
     if (!c.have_problem) fail(TG_ERR_CONFIG, "run: no problem set");
     if (!c.have_schedule) fail(TG_ERR_CONFIG, "run: no schedule set");
     if (cfg->sweeps_per_swap < 1) fail(TG_ERR_CONFIG, "run: sweeps_per_swap must be >= 1");
@@ -850,6 +1029,7 @@ void do_init(tg_ctx& c, const tg_run_config* cfg) {
     if (eng == TG_ENGINE_SLOT && c.world == 1 && !std::getenv("TG_SLOT_V1")) {
         // single instance = batch of one on the replica-fastest SLOT engine
         BatchInst bi;
+        ensure_host_arrays(c);
         bi.n = c.n; bi.ci = c.ci; bi.cj = c.cj; bi.pa = c.pa; bi.pb = c.pb;
         bi.cw = c.cw; bi.h = c.h; bi.betas = c.betas; bi.pens = c.pens; bi.seed = cfg->seed;
         c.batch.assign(1, bi);
@@ -870,7 +1050,8 @@ void do_init(tg_ctx& c, const tg_run_config* cfg) {
     for (int r = 0; r < c.R; ++r) ident[r] = r;
     c.d_slot_state.upload(ident, st);
     c.d_state_slot.upload(ident, st);
-    c.d_perm.upload(c.order, st);
+    if (c.dev_prep) c.d_perm.copy_from(c.d_order_dev, st);
+    else c.d_perm.upload(c.order, st);
     const int np = c.I * std::max(0, c.J - 1), nb = std::max(0, c.I - 1) * c.J;
     c.d_acc_p.alloc(std::max(np, 1));
     c.d_acc_b.alloc(std::max(nb, 1));
@@ -1694,6 +1875,7 @@ void probe_run(tg_ctx& c, double beta, double penalty, int n_chains, int sweeps,
         S.probe_rule != rule) {
         BatchInst bi;
         bi.n = c.n;
+        ensure_host_arrays(c);
         bi.ci = c.ci; bi.cj = c.cj; bi.cw = c.cw; bi.h = c.h; bi.pa = c.pa; bi.pb = c.pb;
         bi.betas.assign(n_chains, beta);
         bi.pens.assign(1, penalty);
@@ -1857,6 +2039,7 @@ extern "C" {
 int tg_abi_version(void) { return TG_ABI_VERSION; }
 
 static int create_impl(int device, int rank, int world, const void* nccl_id, tg_ctx** out) {
+    HostTimer tm_("create");
     if (!out) return TG_ERR_CONFIG;
     *out = nullptr;
     tg_ctx* c = new tg_ctx();
@@ -1870,12 +2053,23 @@ static int create_impl(int device, int rank, int world, const void* nccl_id, tg_
         c->rank = rank;
         c->world = world;
         CK(cudaSetDevice(device));
-        cudaDeviceProp prop;
-        CK(cudaGetDeviceProperties(&prop, device));
-        if (prop.major < 10)
-            fail(TG_ERR_CUDA, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor);
-        c->sms = prop.multiProcessorCount;
+        int major = 0, minor = 0;  // attribute queries: microseconds, unlike cudaGetDeviceProperties
+        CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+        CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+        if (major < 10)
+            fail(TG_ERR_CUDA, "device %d is sm_%d%d; this build targets sm_100a", device, major, minor);
+        CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->stream_owner.s = c->stream;
+        t_alloc_stream = c->stream;
+        static bool pool_set[64] = {};
+        if (device < 64 && !pool_set[device]) {  // keep freed pool memory for the next context
+            cudaMemPool_t pool;
+            CK(cudaDeviceGetDefaultMemPool(&pool, device));
+            uint64_t keep = ~0ull;
+            CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+            pool_set[device] = true;
+        }
         if (world > 1) {
             ncclUniqueId id;
             std::memcpy(&id, nccl_id, sizeof(id));
@@ -1907,7 +2101,10 @@ int tg_nccl_unique_id(void* out128) {
     return TG_OK;
 }
 
-void tg_destroy(tg_ctx* ctx) { delete ctx; }
+void tg_destroy(tg_ctx* ctx) {
+    HostTimer tm_("destroy");
+    delete ctx;
+}
 
 size_t tg_last_error(const tg_ctx* ctx, char* buf, size_t len) {
     const std::string& s = ctx ? ctx->err : g_create_error;
@@ -1924,21 +2121,71 @@ int tg_set_problem(tg_ctx* ctx, int n, int n_couplings, const int32_t* ci, const
                    const int32_t* pb) {
     if (!ctx) return TG_ERR_CONFIG;
     return guard(ctx, [&] {
-        BatchInst bi;
-        load_problem(bi, n, n_couplings, ci, cj, w, fields, n_pairs, pa, pb);
-        ctx->n = bi.n;
-        ctx->ci = bi.ci;
-        ctx->cj = bi.cj;
-        ctx->cw = bi.cw;
-        ctx->h = bi.h;
-        ctx->pa = bi.pa;
-        ctx->pb = bi.pb;
-        canonical(n, ctx->ci, ctx->cj, ctx->pa, ctx->pb, ctx->order, ctx->color, ctx->n_colors);
-        ctx->inv.assign(n, 0);
-        for (int k = 0; k < n; ++k) ctx->inv[ctx->order[k]] = k;
-        ctx->color_start.assign(ctx->n_colors + 1, 0);
-        for (int k = 0; k < n; ++k) ctx->color_start[ctx->color[ctx->order[k]] + 1]++;
-        for (int q = 0; q < ctx->n_colors; ++q) ctx->color_start[q + 1] += ctx->color_start[q];
+        HostTimer tm_("set_problem (total)");
+        if (n <= 0) fail(TG_ERR_CONFIG, "model: n_spins must be positive");
+        if (n_couplings < 0 || n_pairs < 0) fail(TG_ERR_CONFIG, "model: negative counts");
+        tg_ctx& c = *ctx;
+        cudaStream_t st = c.stream;
+        CK(cudaSetDevice(c.device));
+        c.have_problem = false;
+        c.dev_prep = c.host_canonical = false;
+        // validation, colouring, canonical order and the internal CSR on the
+        // device (prep.cu); the raw caller arrays go up once
+        PrepSummary P;
+        {
+            HostTimer t2_("set_problem: device prep");
+            DBuf<int>& dci = c.d_raw_ci; DBuf<int>& dcj = c.d_raw_cj;
+            DBuf<int>& dpa = c.d_raw_pa; DBuf<int>& dpb = c.d_raw_pb;
+            DBuf<double>& dw = c.d_raw_w; DBuf<double>& dh = c.d_raw_h;
+            dci.upload(ci, n_couplings, st);
+            dcj.upload(cj, n_couplings, st);
+            dw.upload(w, n_couplings, st);
+            std::vector<double> hz;
+            if (!fields) hz.assign(n, 0.0);
+            dh.upload(fields ? fields : hz.data(), n, st);
+            dpa.upload(pa, n_pairs, st);
+            dpb.upload(pb, n_pairs, st);
+            c.d_order_dev.alloc(n);
+            c.d_inv_dev.alloc(n);
+            c.d_base_dev.alloc((size_t)n + 1);
+            c.d_nbr_dev.alloc((size_t)2 * ((size_t)n_couplings + n_pairs));
+            PrepIn in{n, n_couplings, n_pairs, dci.p, dcj.p, dw.p, dh.p, dpa.p, dpb.p};
+            PrepOut out{c.d_order_dev.p, c.d_inv_dev.p, c.d_base_dev.p, c.d_nbr_dev.p};
+            CK(plane_prep_device(in, out, P, st, c.sms));
+        }
+        HostTimer t3_("set_problem: finish");
+        if (P.bad) {  // the host validator produces the reference's message
+            BatchInst bi;
+            load_problem(bi, n, n_couplings, ci, cj, w, fields, n_pairs, pa, pb);
+            fail(TG_ERR_INTERNAL, "device validation rejected an instance the host accepts (flags %u)", P.bad);
+        }
+        c.n = n;
+        c.m = n_couplings;
+        c.np = n_pairs;
+        c.host_arrays = false;  // host copies are fetched from the device when a host path needs them
+        if (P.colour_incomplete) {  // dependency chains beyond the device round budget
+            ensure_host_arrays(c);
+            canonical(n, c.ci, c.cj, c.pa, c.pb, c.order, c.color, c.n_colors);
+            c.inv.assign(n, 0);
+            for (int k = 0; k < n; ++k) c.inv[c.order[k]] = k;
+            c.color_start.assign(c.n_colors + 1, 0);
+            for (int k = 0; k < n; ++k) c.color_start[c.color[c.order[k]] + 1]++;
+            for (int q = 0; q < c.n_colors; ++q) c.color_start[q + 1] += c.color_start[q];
+            c.host_canonical = true;
+            c.d_order_dev.release();
+            c.d_inv_dev.release();
+            c.d_base_dev.release();
+            c.d_nbr_dev.release();
+        } else {
+            c.n_colors = P.n_colors;
+            c.color_start.assign(c.n_colors + 1, 0);
+            const unsigned mq1 = P.max_dq + 1, mc1 = P.max_dc + 1;
+            for (size_t q = 0; q < P.run_keys.size(); ++q)
+                c.color_start[P.run_keys[q] / (mq1 * mc1) + 1] += P.run_counts[q];
+            for (int q = 0; q < c.n_colors; ++q) c.color_start[q + 1] += c.color_start[q];
+            c.prep = std::move(P);
+            c.dev_prep = true;
+        }
         ctx->have_problem = true;
         ++ctx->problem_gen;
         ctx->initialised = false;
@@ -1975,6 +2222,7 @@ int tg_run(tg_ctx* ctx, const tg_run_config* cfg, tg_sink_fn sink, void* user) {
     if (!ctx || !cfg) return TG_ERR_CONFIG;
     return guard(ctx, [&] {
         do_init(*ctx, cfg);
+        HostTimer tm_("advance (all rounds)");
         do_advance(*ctx, cfg->total_sweeps / cfg->sweeps_per_swap, SinkCtx{sink, user});
     });
 }
@@ -1982,6 +2230,7 @@ int tg_run(tg_ctx* ctx, const tg_run_config* cfg, tg_sink_fn sink, void* user) {
 int tg_get_state(tg_ctx* ctx, int slot, int8_t* out) {
     if (!ctx) return TG_ERR_CONFIG;
     return guard(ctx, [&] {
+        HostTimer tm_("get_state");
         tg_ctx& c = *ctx;
         if (c.use_s2) { s2_get_state(c, 0, slot, out); return; }
         if (!c.initialised) fail(TG_ERR_CONFIG, "get_state: context not initialised");
@@ -2187,6 +2436,7 @@ int tg_run_jcolumn(tg_ctx* ctx, int n_betas, const double* betas, double p_fixed
                                            (long long)out_cap, (long long)rounds);
         BatchInst proto;
         proto.n = ctx->n;
+        ensure_host_arrays(*ctx);
         proto.ci = ctx->ci;
         proto.cj = ctx->cj;
         proto.cw = ctx->cw;

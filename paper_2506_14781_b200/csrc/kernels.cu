@@ -394,20 +394,29 @@ __global__ void extract_kernel(ExtractArgs e) {
 
 // ------------------------------------------------------------- init kernels
 
+// random_state (ising.cpp:15-19) of every local replica, bit-packed: one warp
+// per (site pair, word); lane l is replica 32 w + l, whose init stream gives
+// the draws of sites 2p and 2p+1 from ONE Philox block (rng.hpp:79: the spin
+// is the top bit), and two ballots pack the 32 replicas into the words.
 __global__ void plane_init_kernel(uint32_t* spins, int n, int W, int local_states, int state0,
                                   uint64_t seed) {
-    const long long total = (long long)n * W;
-    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
-         q += (long long)gridDim.x * blockDim.x) {
-        const int i = (int)(q / W), w = (int)(q % W);
-        uint32_t word = 0;
-        for (int l = 0; l < 32; ++l) {
-            const int m = w * 32 + l;
-            if (m >= local_states) break;
-            const uint64_t key = derive_seed(seed, kPurposeInit, (uint64_t)(state0 + m));
-            if (stream_bits(key, (uint64_t)i) >> 63) word |= 1u << l;  // rng.hpp:79
+    const int lane = threadIdx.x & 31;
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    const long long items = (long long)((n + 1) >> 1) * W;
+    for (long long it = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); it < items; it += nw) {
+        const int w = (int)(it % W);
+        const long long p = it / W;
+        const int m = w * 32 + lane;
+        const uint64_t key = derive_seed(seed, kPurposeInit, (uint64_t)(state0 + m));
+        const u32x4 o = philox4x32_10(u32x4{(uint32_t)p, (uint32_t)((uint64_t)p >> 32), 0u, 0u},
+                                      (uint32_t)key, (uint32_t)(key >> 32));
+        const bool live = m < local_states;
+        const uint32_t w0 = __ballot_sync(0xffffffffu, live && (o.y >> 31));  // draw 2p
+        const uint32_t w1 = __ballot_sync(0xffffffffu, live && (o.w >> 31));  // draw 2p + 1
+        if (lane == 0) {
+            spins[(size_t)(2 * p) * W + w] = w0;
+            if (2 * p + 1 < n) spins[(size_t)(2 * p + 1) * W + w] = w1;
         }
-        spins[q] = word;
     }
 }
 

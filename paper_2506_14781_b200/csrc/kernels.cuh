@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "engine.cuh"
 
 namespace tg {
@@ -52,6 +54,40 @@ __global__ void slot2_extract_kernel(const __grid_constant__ S2Args a, const __g
 __global__ void slot2_init_kernel(const __grid_constant__ S2Args a, const uint64_t* init_keys);
 __global__ void slot2_kl_kernel(const __grid_constant__ S2Args a, const int32_t* slot_state,
                                 const __grid_constant__ KLArgs k, int64_t round);
+// ---- device instance preprocessing for the PLANE engine (prep.cu)
+enum : unsigned {
+    kPrepBadCoupling = 1u, kPrepBadPair = 2u, kPrepBadField = 4u, kPrepDuplicate = 8u,
+    kPrepErrors = 15u,
+    kPrepNotPM1 = 16u, kPrepNonzeroField = 32u  // plane-engine eligibility (not errors)
+};
+constexpr int kPrepColourRounds = 4096;
+struct PrepIn {             // device arrays, caller order
+    int n, m, np;
+    const int* ci;
+    const int* cj;
+    const double* w;
+    const double* h;
+    const int* pa;
+    const int* pb;
+};
+struct PrepOut {            // caller-allocated device outputs
+    int* order;             // [n] internal -> caller
+    int* inv;               // [n] caller -> internal
+    int* base;              // [n + 1] internal row offsets
+    int* nbr;               // [2 (m + np)] internal rows (cost | sign, then chain)
+};
+struct PrepSummary {        // host
+    unsigned bad = 0;       // kPrep* error flags: invalid instance (host re-validates for the message)
+    unsigned info = 0;      // kPrepNotPM1 / kPrepNonzeroField
+    bool colour_incomplete = false;
+    int colour_rounds = 0, n_colors = 0, max_dc = 0, max_dq = 0;
+    std::vector<unsigned> run_keys;   // sorted (colour, dq, dc) keys, one per run
+    std::vector<int> run_counts;
+};
+cudaError_t plane_prep_device(const PrepIn& in, const PrepOut& o, PrepSummary& r, cudaStream_t st,
+                              int sms);
+cudaError_t plane_chunk_bases(Chunk* chunks, int n_chunks, const int* base, cudaStream_t st, int sms);
+
 __global__ void probe_moments_kernel(const double* hist_f, const double* hist_g, int R, int kept,
                                      double penalty, double* out);
 
