@@ -741,10 +741,12 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
         if (const char* e = std::getenv("TG_PLANE_LOOP")) if (std::atoi(e)) c.fused_wv = 0;
         const void* fn = plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast);
         c.fused_block = c.fused_fast ? kPlaneThreadsFast : kPlaneThreads;
+        const size_t pf_words = c.fused_fast && (c.fused_wv == 4 || c.fused_wv == 2)
+                                    ? (size_t)2 * (5 * 32 * c.fused_wv + 4 * 32) : 0;
+        const size_t tail_words = c.fused_fast && (c.fused_wv == 4 || c.fused_wv == 2)
+                                      ? 0 : std::max<size_t>(kTailCap * 7, (size_t)2 * c.W * 32);
         c.fused_smem = (size_t)c.R * (2 * sizeof(double) + 2 * sizeof(int32_t)) + 8 +
-                       (size_t)(c.fused_block / 32) *
-                           std::max<size_t>(std::max<size_t>(kTailCap * 7, (size_t)2 * c.W * 32),
-                                            (size_t)2 * (5 * 32 * 4 + 4 * 32)) * sizeof(int32_t);
+                       (size_t)(c.fused_block / 32) * std::max(pf_words, tail_words) * sizeof(int32_t);
         if (c.fused_smem > 48 * 1024)
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.fused_smem));
         int fb = 0;

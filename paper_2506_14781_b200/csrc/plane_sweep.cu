@@ -552,12 +552,14 @@ __device__ __forceinline__ void plane_phase(const PlaneArgs& a, int c, uint64_t 
 // cp.async (LDGSTS) -- the L2 latency of the random neighbour gathers is
 // hidden behind a chunk of Philox/compare work instead of stalling the warp.
 constexpr int kPfRows = 5;                     // own row + up to 4 neighbours
-constexpr int kPfStageWords = kPfRows * 32 * 4 + 4 * 32;  // rows + neighbour entries
-template <int RULE>
+template <int WV>
+__host__ __device__ constexpr int pf_stage_words() { return kPfRows * 32 * WV + 4 * 32; }  // rows + neighbour entries
+constexpr int kPfStageWords = pf_stage_words<4>();
+template <int RULE, int WV>
 __device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64_t t, bool count,
                                                int gidx, int ngroups, int wb, int32_t* cnt_c,
                                                int32_t* cnt_q, uint32_t* pf, int* work) {
-    constexpr int WV = 4;
+    constexpr int kStage = pf_stage_words<WV>();
     int acc_c[WV], acc_q[WV];
 #pragma unroll
     for (int w = 0; w < WV; ++w) { acc_c[w] = 0; acc_q[w] = 0; }
@@ -573,16 +575,16 @@ __device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64
         const Chunk ch = a.chunks[c0 + item];
         const PlaneType& ty = a.ty[ch.type];
         const int deg = ty.dc + ty.dq;
-        uint32_t* rows = pf + stage * kPfStageWords;
-        int32_t* idx = reinterpret_cast<int32_t*>(rows + kPfRows * 32 * 4);
+        uint32_t* rows = pf + stage * kStage;
+        int32_t* idx = reinterpret_cast<int32_t*>(rows + kPfRows * 32 * WV);
         if (lane < ch.len) {
             const int site = ch.start + lane;
-            __pipeline_memcpy_async(rows + lane * 4, a.spins + (size_t)site * Wp + wb, 16);
+            __pipeline_memcpy_async(rows + lane * WV, a.spins + (size_t)site * Wp + wb, 4 * WV);
             for (int k = 0; k < deg; ++k) {
                 const int32_t e = __ldg(a.nbr + ch.nbr_base + lane * deg + k);
                 idx[k * 32 + lane] = e;
-                __pipeline_memcpy_async(rows + ((1 + k) * 32 + lane) * 4,
-                                        a.spins + (size_t)(e & 0x7fffffff) * Wp + wb, 16);
+                __pipeline_memcpy_async(rows + ((1 + k) * 32 + lane) * WV,
+                                        a.spins + (size_t)(e & 0x7fffffff) * Wp + wb, 4 * WV);
             }
         }
         __pipeline_commit();
@@ -606,8 +608,8 @@ __device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64
         else __pipeline_commit();
         __pipeline_wait_prior(1);
         __syncwarp();
-        const uint32_t* rows = pf + (k & 1) * kPfStageWords;
-        const int32_t* idx = reinterpret_cast<const int32_t*>(rows + kPfRows * 32 * 4);
+        const uint32_t* rows = pf + (k & 1) * kStage;
+        const int32_t* idx = reinterpret_cast<const int32_t*>(rows + kPfRows * 32 * WV);
         const PlaneType& ty = a.ty[cur.type];
         switch (ty.ncb * 4 + ty.nqb) {
             case 1 * 4 + 0: plane_site<1, 0, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
@@ -844,7 +846,8 @@ plane_sweep_kernel(const __grid_constant__ PlaneArgs a, int64_t t0, int n_sweeps
 // more grid barrier closes the round.
 template <int RULE, int WV, int FAST>
 __global__ void __launch_bounds__(FAST ? kPlaneThreadsFast : kPlaneThreads,
-                                  WV == 0 ? kPlaneMinBlocksLoop : (FAST ? kPlaneMinBlocksFast : 1))
+                                  WV == 0 ? kPlaneMinBlocksLoop
+                                          : (FAST ? (WV == 2 ? 2 : kPlaneMinBlocksFast) : 1))
 plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__ RoundArgs r) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double sm_d[];
@@ -855,7 +858,8 @@ plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__
     char* sm_tail = reinterpret_cast<char*>(s_state + r.R + (r.R & 1));
     TailQ tq = tail_view(sm_tail, threadIdx.x >> 5);
     int* sacc = reinterpret_cast<int*>(sm_tail) + (size_t)(threadIdx.x >> 5) * 2 * a.W * 32;
-    uint32_t* pfbuf = reinterpret_cast<uint32_t*>(sm_tail) + (size_t)(threadIdx.x >> 5) * 2 * kPfStageWords;
+    uint32_t* pfbuf = reinterpret_cast<uint32_t*>(sm_tail) +
+                      (size_t)(threadIdx.x >> 5) * 2 * pf_stage_words<WV == 2 ? 2 : 4>();
     const int tid = threadIdx.x;
     const int wpb = blockDim.x >> 5;
     const int warp = tid >> 5, lane = tid & 31;
@@ -882,8 +886,8 @@ plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__
             const bool count = (sw == r.sps - 1);
             for (int c = 0; c < a.n_colors; ++c) {
                 if constexpr (WV == 0) plane_phase_loop<RULE, FAST>(a, c, t, count, gidx, ngroups, cc, cq, sacc);
-                else if constexpr (FAST && WV == 4)
-                    plane_phase_pf<RULE>(a, c, t, count, gidx, ngroups, wb, cc, cq, pfbuf,
+                else if constexpr (FAST && (WV == 4 || WV == 2))
+                    plane_phase_pf<RULE, WV>(a, c, t, count, gidx, ngroups, wb, cc, cq, pfbuf,
                                          r.work ? r.work + ((size_t)(par * a.n_colors + c) * passes +
                                                             wb / WV) : nullptr);
                 else plane_phase<RULE, WV, FAST, kPlaneTail>(a, c, t, count, gidx, ngroups, wb, cc, cq, tq);
