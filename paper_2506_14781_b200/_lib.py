@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libtempergrid_b200.so")
+LIB_PATH = os.environ.get("TG_ENGINE_LIB") or os.path.join(PKG, "libtempergrid_b200.so")  # override: A/B builds
 
 TG_OK, TG_ERR_INTERNAL, TG_ERR_CONFIG, TG_ERR_RESOURCE, TG_ERR_CUDA, TG_ERR_SINK = range(6)
 RULES = {"metropolis": 0, "heat_bath": 1}
