@@ -46,9 +46,9 @@ def parse():
     ap.add_argument("--sps", type=int, default=1, help="sweeps per swap")
     ap.add_argument("--rule", default="metropolis")
     ap.add_argument("--engine", default="plane")
-    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c4"],
+    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c3", "c4"],
                     help="c5: config 5 (the metric's config, default); c2/c4: Wishart float32 "
-                         "configs on the slot engine")
+                         "configs on the slot engine; c3: the 64-instance Wishart batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sweeps", type=int, default=16, help="marginal sweeps of the CPU sample")
     return ap.parse_args()
@@ -60,6 +60,9 @@ def workload(n, kind="c5"):
         pr = I.wishart_planted(32, 0.5, seed=1)
         betas, pens = I.wishart_schedule(pr, 16, 8)
         return pr, betas, pens
+    if kind == "c3":   # one instance of the config-3 batch (the CPU legs time one instance)
+        prs, scheds = c3_instances()
+        return prs[0], scheds[0][0], scheds[0][1]
     if kind == "c4":   # N=256 logical, alpha=0.5 (64768 spins), 32x32 grid
         pr = I.wishart_planted(256, 0.5, seed=1)
         betas, pens = I.wishart_schedule(pr, 32, 32)
@@ -227,6 +230,142 @@ def run_reference_arm(args, rank, world):
 
 
 # ------------------------------------------------------------- GPU leg
+
+def c3_instances():
+    """Config 3: 64 Wishart instances, N=64 logical, alpha=0.75, float32 J, degree <= 3
+    chains (3904 physical spins each), each on its own 16x16 grid (schedule rule of C2)."""
+    from paper_2506_14781_b200 import instances as I
+    prs = [I.wishart_planted(64, 0.75, seed=s) for s in range(1, 65)]
+    scheds = [I.wishart_schedule(p, 16, 16) for p in prs]
+    return prs, scheds
+
+
+def run_ours_batch(args, rank, world, local):
+    """Config 3 through the batch engine (tg_batch_*): one launch sweeps every
+    instance's 256 replicas.  Under torchrun each rank takes instances
+    rank::world (no collective: the instances are independent)."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    from paper_2506_14781_b200 import _lib
+    from paper_2506_14781_b200.api import Engine, RunConfig, Schedule, run_2dpt_batch
+
+    torch.cuda.set_device(local)
+    prs_all, scheds_all = c3_instances()
+    mine = list(range(rank, len(prs_all), world))
+    prs = [prs_all[b] for b in mine]
+    scheds = [Schedule(*scheds_all[b]) for b in mine]
+    seeds = [1 + b for b in mine]
+    R = 256
+    eng = Engine(local)
+    L = eng._L
+    keep = []
+    L.tg_batch_clear(eng._h)
+    for pr, sc, sd in zip(prs, scheds, seeds):
+        arrs = [np.ascontiguousarray(x, dtype=t) for x, t in (
+            (pr.ci, np.int32), (pr.cj, np.int32), (pr.cw, np.float64), (pr.fields, np.float64),
+            (pr.pa, np.int32), (pr.pb, np.int32), (sc.betas, np.float64), (sc.penalties, np.float64))]
+        keep.append(arrs)
+        P = [a.ctypes.data_as(C.c_void_p) for a in arrs]
+        eng._check(L.tg_batch_add(eng._h, pr.n, len(arrs[0]), P[0], P[1], P[2], P[3], len(arrs[4]),
+                                  P[4], P[5], len(arrs[6]), P[6], len(arrs[7]), P[7], sd, None))
+    total = args.rounds * args.sps * (args.warmup + args.steps + 1)
+    cfg = RunConfig(total_sweeps=total, sweeps_per_swap=args.sps, seed=1, rule=args.rule,
+                    engine="slot", store_states=False, digest=False)
+    c = eng._cfg(cfg)
+    c.record_flags = 0
+    eng._check(L.tg_batch_init(eng._h, C.byref(c)))
+    eng.set_profiling(True)
+    stream = torch.cuda.ExternalStream(eng.stream_ptr())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    nosink = C.cast(None, _lib.BATCH_SINK)
+
+    def step():
+        eng._check(L.tg_batch_advance(eng._h, args.rounds, nosink, None))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    info0 = eng.info()
+    step_ms, sweep_ms = [], 0.0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            sweep_ms += eng.info()["last_sweep_ms"]
+    torch.cuda.synchronize()
+    barrier(world)
+    info1 = eng.info()
+    eng.close()
+    total_ms = reduce_max(sum(step_ms), world)
+    sweeps = args.steps * args.rounds * args.sps
+    n_spins = sum(p.n for p in prs_all)
+    value = float(n_spins) * R * sweeps / (total_ms / 1e3)
+    n_sweep = info1["sweep_launches"] - info0["sweep_launches"]
+    launches = n_sweep + info1["other_launches"] - info0["other_launches"]
+    mean_sweep_s = reduce_max(sweep_ms, world) / 1e3 / max(n_sweep, 1)
+    bal = b_alg(prs[0])
+    my_spins = sum(p.n for p in prs)
+    achieved = bal * my_spins * R * sweeps / max(n_sweep, 1) / mean_sweep_s / 1e9
+    peaks = load_peaks()
+    smem_peak = 148 * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e9
+    clocks = clk.summary()
+
+    # e2e: run_2dpt_batch from pinned host arrays (instances up, build, rounds, records down)
+    def pinned(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+
+    from paper_2506_14781_b200.instances import Problem
+    pprs = [Problem(p.n, pinned(p.ci), pinned(p.cj), pinned(p.cw), pinned(p.fields), pinned(p.pa),
+                    pinned(p.pb)) for p in prs]
+    cfg2 = RunConfig(total_sweeps=args.rounds * args.sps, sweeps_per_swap=args.sps, seed=2,
+                     rule=args.rule, engine="slot", store_states=False, digest=False)
+    times = []
+    for k in range(args.warmup + args.steps):
+        barrier(world)
+        t = time.perf_counter()
+        run_2dpt_batch(pprs, scheds, cfg2, seeds, device=local, sink=lambda *a: 0)
+        dt = time.perf_counter() - t
+        if k >= args.warmup:
+            times.append(dt)
+    t_e2e = reduce_max(statistics.median(times) * 1e3, world) / 1e3
+    h2d = sum(a.nbytes for p in pprs for a in (p.ci, p.cj, p.cw, p.fields, p.pa, p.pb))
+    e2e = {"value": float(n_spins) * R * args.rounds * args.sps / t_e2e, "unit": UNIT,
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(48 * args.rounds * len(prs)),
+           "ms_per_step": 1e3 * t_e2e, "inputs": "pinned host arrays"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, kind, dt = cpu_reference_rate(prs[0], *scheds_all[0], args.cpu_sweeps, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads if kind == "reference" else 1,
+               "kind": kind, "sample": f"unmodified reference run_2dpt on instance 1 of 64 "
+                                       f"(N={prs[0].n}, 16x16); marginal rate of "
+                                       f"{1 + args.cpu_sweeps} vs 1 sweeps ({dt:.1f} s)"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C3 batch: 64 Wishart N=64 logical (alpha 0.75) -> "
+                                   f"{prs_all[0].n} physical each, 16x16 grids, sps={args.sps} "
+                                   f"{args.rule}",
+                       "instances": len(prs_all), "n_spins_total": n_spins, "replicas": R,
+                       "rounds_per_step": args.rounds, "engine": "slot (batch)",
+                       "parallelism": f"instances x{world}",
+                       "l2": "flushed between timed steps (256 MB write)"},
+            "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
+                         "frac": achieved / smem_peak, "traffic": None, "kernel": "slot2_sweep_kernel",
+                         "bytes_per_update": bal, "mean_launch_ms": mean_sweep_s * 1e3},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks}),
+            flush=True)
+
 
 def run_ours(args, rank, world, local):
     import numpy as np
@@ -413,6 +552,8 @@ def main():
     rank, world, local = dist_setup(args.gpus)
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
+    elif args.workload == "c3":
+        run_ours_batch(args, rank, world, local)
     else:
         run_ours(args, rank, world, local)
     if world > 1:

@@ -164,6 +164,10 @@ int tg_batch_add(tg_ctx* ctx, int n, int n_couplings, const int32_t* ci, const i
                  const double* penalties, uint64_t seed, int32_t* index);
 /* cfg->seed is ignored (per-instance seeds); engine must be AUTO or SLOT. */
 int tg_batch_run(tg_ctx* ctx, const tg_run_config* cfg, tg_batch_sink_fn sink, void* user);
+/* tg_batch_run split in two (resume / timing): build + initial states, then
+ * n_rounds more rounds of every instance per call. */
+int tg_batch_init(tg_ctx* ctx, const tg_run_config* cfg);
+int tg_batch_advance(tg_ctx* ctx, int64_t n_rounds, tg_batch_sink_fn sink, void* user);
 int tg_batch_get_state(tg_ctx* ctx, int instance, int slot, int8_t* out);
 int tg_batch_get_counters(tg_ctx* ctx, int instance, int64_t* attempts_p, int64_t* accepts_p,
                           int64_t* attempts_b, int64_t* accepts_b);

@@ -107,6 +107,8 @@ def lib() -> C.CDLL:
     L.tg_batch_run.argtypes = [vp, C.POINTER(RunConfigC), BATCH_SINK, C.c_void_p]
     L.tg_batch_get_state.argtypes = [vp, C.c_int, C.c_int, vp]
     L.tg_batch_get_counters.argtypes = [vp, C.c_int, vp, vp, vp, vp]
+    L.tg_batch_init.argtypes = [vp, vp]
+    L.tg_batch_advance.argtypes = [vp, C.c_int64, BATCH_SINK, vp]
     L.tg_run_jcolumn.argtypes = [vp, C.c_int, vp, C.c_double, C.c_int, vp, vp, C.c_int64, vp]
     L.tg_set_kl_decoder.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, vp, C.c_double, vp, vp, C.c_int]
     L.tg_clear_kl_decoder.argtypes = [vp]
@@ -128,6 +130,6 @@ EXPORTED = [
     "tg_set_profiling", "tg_canonical_order", "tg_p_swap_probability", "tg_beta_swap_probability",
     "tg_general_swap_probability", "tg_swap_phase_host", "tg_partition", "tg_batch_clear",
     "tg_batch_add", "tg_batch_run", "tg_batch_get_state", "tg_batch_get_counters",
-    "tg_run_jcolumn", "tg_probe_population", "tg_build_schedule", "tg_set_kl_decoder",
+    "tg_batch_init", "tg_batch_advance", "tg_run_jcolumn", "tg_probe_population", "tg_build_schedule", "tg_set_kl_decoder",
     "tg_clear_kl_decoder", "tg_get_kl_curve",
 ]

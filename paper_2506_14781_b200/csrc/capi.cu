@@ -224,6 +224,10 @@ struct Slot2 {
     DBuf<uint64_t> d_init_keys;
     DBuf<double> d_hist_f, d_hist_g, d_moments;
     std::vector<SInst> h_inst;
+    // separate energy pass (large batches): slices per instance, partials
+    bool sep_energy = false;
+    int e_slices = 1;
+    DBuf<double> d_epart;
     // KL observer buffers
     bool kl_on = false;
     int64_t kl_cap = 0;
@@ -1594,8 +1598,15 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
         S.grid = blocks;
         S.nsub = blocks * wpb / S.G;
     }
-    S.d_part_f.alloc((size_t)B * S.nsub * S.Rp);
-    S.d_part_g.alloc((size_t)B * S.nsub * S.Rp);
+    // fused per-warp energy partials cost B x nsub x Rp doubles of traffic per
+    // round; past a few MB a separate pass over the spins is cheaper
+    S.sep_energy = (size_t)B * S.nsub * S.Rp * 16 > ((size_t)8 << 20) || std::getenv("TG_SLOT_SEP_ENERGY");
+    if (S.sep_energy) {
+        S.e_slices = std::max(1, (c.sms * 8) / std::max(1, B * S.G));
+        S.d_epart.alloc((size_t)2 * B * S.e_slices * S.R);
+    }
+    S.d_part_f.alloc(S.sep_energy ? 0 : (size_t)B * S.nsub * S.Rp);
+    S.d_part_g.alloc(S.sep_energy ? 0 : (size_t)B * S.nsub * S.Rp);
     S.d_part_f.zero(st);
     S.d_part_g.zero(st);
     {
@@ -1743,12 +1754,18 @@ void s2_advance(tg_ctx& c, int64_t n_rounds, const BatchSinkCtx& sink) {
     for (int64_t k = 0; k < n_rounds; ++k) {
         const int64_t round = S.rounds_done + 1;
         int64_t t0 = (round - 1) * sps;
-        int nsw = sps, de = 1;
+        int nsw = sps, de = S.sep_energy ? 0 : 1;
         void* args[] = {&a, &t0, &nsw, &de};
         if (c.profiling) CK(cudaEventRecord(c.ev[0], st));
         CK(cudaLaunchCooperativeKernel(slot2_sweep_fn(S.D), dim3(S.grid), dim3(kSlot2Threads), args, 0, st));
         if (c.profiling) CK(cudaEventRecord(c.ev[1], st));
         c.sweep_launches++;
+        if (S.sep_energy) {
+            slot2_energy_kernel<<<dim3(S.e_slices, S.G, S.B), 256, 0, st>>>(a, S.e_slices, S.d_epart.p);
+            slot2_energy_sum_kernel<<<(S.B * S.R + 255) / 256, 256, 0, st>>>(a, S.e_slices, S.d_epart.p);
+            CK(cudaGetLastError());
+            c.other_launches += 2;
+        }
         slot2_swap_kernel<<<S.B, kSwapThreads, 0, st>>>(s, round, S.swap_base, filled, flags);
         CK(cudaGetLastError());
         c.other_launches++;
@@ -2363,7 +2380,7 @@ int tg_batch_add(tg_ctx* ctx, int n, int n_couplings, const int32_t* ci, const i
     });
 }
 
-int tg_batch_run(tg_ctx* ctx, const tg_run_config* cfg, tg_batch_sink_fn sink, void* user) {
+int tg_batch_init(tg_ctx* ctx, const tg_run_config* cfg) {
     if (!ctx || !cfg) return TG_ERR_CONFIG;
     return guard(ctx, [&] {
         if (cfg->sweeps_per_swap < 1) fail(TG_ERR_CONFIG, "run: sweeps_per_swap must be >= 1");
@@ -2378,9 +2395,23 @@ int tg_batch_run(tg_ctx* ctx, const tg_run_config* cfg, tg_batch_sink_fn sink, v
         ctx->initialised = false;
         ctx->s2.probe = false;
         s2_build(*ctx, cfg);
-        s2_advance(*ctx, cfg->total_sweeps / cfg->sweeps_per_swap, BatchSinkCtx{sink, user});
+        ctx->rounds_done = 0;
+    });
+}
+
+int tg_batch_advance(tg_ctx* ctx, int64_t n_rounds, tg_batch_sink_fn sink, void* user) {
+    if (!ctx) return TG_ERR_CONFIG;
+    return guard(ctx, [&] {
+        if (!ctx->s2.ready || ctx->s2.probe) fail(TG_ERR_CONFIG, "batch: not initialised (tg_batch_init)");
+        s2_advance(*ctx, n_rounds, BatchSinkCtx{sink, user});
         ctx->rounds_done = ctx->s2.rounds_done;
     });
+}
+
+int tg_batch_run(tg_ctx* ctx, const tg_run_config* cfg, tg_batch_sink_fn sink, void* user) {
+    const int rc = tg_batch_init(ctx, cfg);
+    if (rc != TG_OK) return rc;
+    return tg_batch_advance(ctx, cfg->total_sweeps / cfg->sweeps_per_swap, sink, user);
 }
 
 int tg_batch_get_state(tg_ctx* ctx, int instance, int slot, int8_t* out) {

@@ -52,6 +52,8 @@ __global__ void slot2_swap_kernel(const __grid_constant__ S2Swap s, int64_t roun
 __global__ void slot2_extract_kernel(const __grid_constant__ S2Args a, const __grid_constant__ S2Swap s,
                                      int rec_idx, int all_slots);
 __global__ void slot2_init_kernel(const __grid_constant__ S2Args a, const uint64_t* init_keys);
+__global__ void slot2_energy_kernel(const __grid_constant__ S2Args a, int n_slices, double* part);
+__global__ void slot2_energy_sum_kernel(const __grid_constant__ S2Args a, int n_slices, const double* part);
 __global__ void slot2_kl_kernel(const __grid_constant__ S2Args a, const int32_t* slot_state,
                                 const __grid_constant__ KLArgs k, int64_t round);
 // ---- device instance preprocessing for the PLANE engine (prep.cu)

@@ -179,8 +179,11 @@ slot2_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
         for (int c = 0; c < a.max_colors; ++c) {
             const int* pref = a.item_pref + (size_t)c * (a.B + 1);
             const int total = pref[a.B];
+            // items rise monotonically: advance the instance instead of searching
+            int b = sw < total ? find_instance(pref, a.B, sw) : 0;
+            int b_end = pref[b + 1];
             for (int item = sw; item < total; item += nsub) {
-                const int b = find_instance(pref, a.B, item);
+                while (item >= b_end) b_end = pref[++b + 1];
                 const SInst& in = a.inst[b];
                 if (b != cur_b) {
                     if (count && cur_b >= 0) {  // flush the previous instance's partial sums
@@ -414,6 +417,69 @@ slot2_kl_kernel(const __grid_constant__ S2Args a, const int32_t* slot_state,
             k.samples[(size_t)b * k.cap + round - 1] = (int64_t)T;
         }
     }
+}
+
+// Per-replica (f, g) after a round's sweeps, as a separate deterministic pass
+// (used when the fused per-warp partials of the sweep kernel would not fit:
+// large batches).  Stage 1: block (slice s, replica group g, instance b), 8
+// warps; warp w sums sites s_lo + w, s_lo + w + 8, ... of the slice in order
+// (field term, and every edge at its higher-index endpoint), the 8 warp sums
+// are combined in warp order.  Stage 2 adds the slices in order.
+__global__ void __launch_bounds__(256)
+slot2_energy_kernel(const __grid_constant__ S2Args a, int n_slices, double* part) {
+    __shared__ double sf[8][32], sg[8][32];
+    const int b = blockIdx.z, g = blockIdx.y, sl = blockIdx.x;
+    const SInst& in = a.inst[b];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r = g * 32 + lane;
+    const int per = (in.n + n_slices - 1) / n_slices;
+    const int lo = sl * per, hi = min(in.n, lo + per);
+    const int8_t* sp = a.spins + in.spin_off;
+    const int D = in.D;
+    double fl = 0.0, gl = 0.0;
+    if (r < a.R) {
+        for (int i = lo + warp; i < hi; i += 8) {
+            const double sv = (double)sp[(size_t)i * a.Rp + r];
+            fl -= a.h[in.h_off + i] * sv;
+            const int2* ep = a.entp + in.entp_off + (size_t)i * D;
+            const double* wp = a.wp + in.entp_off + (size_t)i * D;
+            for (int k = 0; k < D; ++k) {
+                const int x = __ldg(&ep[k].x);
+                const int j = x & 0x07ffffff;
+                if (j < i) {
+                    const double sj = (double)sp[(size_t)j * a.Rp + r];
+                    fl -= __ldg(wp + k) * sv * sj;
+                    const double d = sv - sj;
+                    gl += (double)((x >> 28) & 15) * d * d;
+                }
+            }
+        }
+    }
+    sf[warp][lane] = fl;
+    sg[warp][lane] = gl;
+    __syncthreads();
+    if (warp == 0 && r < a.R) {
+        double F = 0.0, G = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) { F += sf[w][lane]; G += sg[w][lane]; }
+        const size_t o = ((size_t)b * n_slices + sl) * a.R + r;
+        part[2 * o] = F;
+        part[2 * o + 1] = G;
+    }
+}
+
+__global__ void slot2_energy_sum_kernel(const __grid_constant__ S2Args a, int n_slices, const double* part) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= a.B * a.R) return;
+    const int b = idx / a.R, r = idx % a.R;
+    double F = 0.0, G = 0.0;
+    for (int sl = 0; sl < n_slices; ++sl) {
+        const size_t o = ((size_t)b * n_slices + sl) * a.R + r;
+        F += part[2 * o];
+        G += part[2 * o + 1];
+    }
+    a.f[idx] = F;
+    a.g[idx] = G;
 }
 
 // Probe moments (schedule.cpp:34-51): the four pooled sums over the history in
