@@ -321,7 +321,7 @@ cudaError_t plane_prep_device(const PrepIn& in, const PrepOut& o, PrepSummary& r
     PK(cudaStreamSynchronize(st));
     r.bad = h_bad & kPrepErrors;
     r.colour_rounds = h_status[1];
-    if (h_bad) return cudaSuccess;
+    if (r.bad) return cudaSuccess;
     if ((h_status[0] & 2) || h_status[1] >= max_rounds) {
         r.colour_incomplete = true;
         return cudaSuccess;

@@ -1,0 +1,107 @@
+"""GPU coverage of the less-travelled paths: the device instance preprocessing
+(prep.cu) on inputs that force its host fallbacks, the reference's validation
+messages raised through it, and the SLOT v1 engine (the multi-GPU slot path)
+on one GPU.  Every run is checked against the oracle."""
+import numpy as np
+import pytest
+
+import pyoracle as O
+from paper_2506_14781_b200 import instances as I
+from paper_2506_14781_b200.api import Engine, RunConfig
+from paper_2506_14781_b200.instances import ConfigError, Problem
+
+pytestmark = pytest.mark.gpu
+
+
+def run(pr, betas, pens, total, seed, engine, rule="metropolis"):
+    with Engine(0) as eng:
+        eng.set_problem(pr)
+        eng.set_schedule(betas, pens)
+        recs = []
+        eng.run(RunConfig(total_sweeps=total, seed=seed, engine=engine, rule=rule, store_states=False,
+                          digest=False),
+                lambda r, n, s, a, b: [recs.append((r[k].f, r[k].g)) for k in range(n)] and 0, flags=0)
+        grid = eng.grid()
+        _, cp, _, cb = eng.counters()
+    return np.array(recs), grid, cp, cb
+
+
+def check(pr, betas, pens, total, seed, engine, rule="metropolis"):
+    """Engine on `pr` (caller order) vs the oracle on the canonical relabel of `pr`
+    (the engine equals the reference run on the relabelled instance)."""
+    order, _, _ = I.canonical_order(pr)
+    o = O.run(pr.permuted(order), betas, pens, total, 1, seed=seed, rule=rule,
+              rng="plane" if engine == "plane" else "slot")
+    recs, grid, cp, cb = run(pr, betas, pens, total, seed, engine, rule)
+    np.testing.assert_array_equal(recs[:, 0], o.f)
+    np.testing.assert_array_equal(recs[:, 1], o.g)
+    np.testing.assert_array_equal(grid[:, np.asarray(order)], o.final_grid)
+    np.testing.assert_array_equal(cp, o.accepts_p)
+    np.testing.assert_array_equal(cb, o.accepts_b)
+
+
+def path_graph(n, seed):
+    rng = np.random.default_rng(seed)
+    w = rng.choice([-1.0, 1.0], size=n - 1)
+    return Problem.make(n, [(i, i + 1, float(w[i])) for i in range(n - 1)], [0.0] * n,
+                        [(i, i + 3) for i in range(0, n - 3, 97)])
+
+
+def test_long_dependency_chain_falls_back_to_host_colouring():
+    # a path in index order: the colouring fixpoint needs ~n rounds (> the 4096
+    # device budget), so set_problem finishes the canonical order on the host
+    pr = path_graph(6000, 3)
+    check(pr, [0.3, 1.0, 3.0], [0.0, 0.25, 0.5, 1.0] + [1.5, 2.0, 2.5, 3.0], 30, 5, "plane")
+
+
+def test_short_chain_path_on_device():
+    pr = path_graph(600, 4)   # within the device round budget, non-identity relabel
+    check(pr, [0.3, 1.0, 3.0], [0.0, 0.5], 40, 6, "plane")
+    check(pr, [0.3, 1.0, 3.0], [0.0, 0.5], 20, 6, "slot")
+
+
+def test_many_colours_fall_back_to_host(monkeypatch):
+    # K_70: 70 colours exceed the device colouring's 63-colour word; degree 69
+    # is beyond SLOT v2's padded rows, so the CSR kernels of SLOT v1 run it
+    monkeypatch.setenv("TG_SLOT_V1", "1")
+    rng = np.random.default_rng(7)
+    cpl = [(i, j, float(rng.choice([-1.0, 1.0]))) for i in range(70) for j in range(i + 1, 70)]
+    pr = Problem.make(70, cpl, [0.0] * 70)
+    check(pr, [0.05, 0.1], [0.0], 10, 3, "slot")
+
+
+@pytest.mark.parametrize("rule", ["metropolis", "heat_bath"])
+def test_slot_v1_engine_on_one_gpu(monkeypatch, rule):
+    monkeypatch.setenv("TG_SLOT_V1", "1")   # the multi-GPU SLOT kernels, single rank
+    pr = I.k10_pm1(2)
+    check(pr, *I.config_schedule("c1"), 60, 9, "slot", rule)
+    f = I.five_node_complete()
+    five = I.to_canonical(I.sparsify(5, list(zip(f.ci.tolist(), f.cj.tolist(), f.cw.tolist())),
+                                     f.fields.tolist(), 2, 3))
+    check(five, [0.5, 1.0, 1.5], [2.0, 4.0, 6.0], 60, 3, "slot", rule)
+
+
+BAD = [
+    ("self loop", Problem.make(4, [(0, 1, 1.0), (2, 2, 1.0)], [0.0] * 4)),
+    ("index out of range", Problem.make(4, [(0, 1, 1.0), (1, 7, 1.0)], [0.0] * 4)),
+    ("duplicate", Problem.make(4, [(0, 1, 1.0), (2, 3, 1.0), (1, 0, -1.0)], [0.0] * 4)),
+    ("non-finite weight", Problem.make(4, [(0, 1, float("nan"))], [0.0] * 4)),
+    ("non-finite field", Problem.make(4, [(0, 1, 1.0)], [0.0, float("inf"), 0.0, 0.0])),
+    ("pair on one spin", Problem.make(4, [(0, 1, 1.0)], [0.0] * 4, [(2, 2)])),
+    ("pair out of range", Problem.make(4, [(0, 1, 1.0)], [0.0] * 4, [(0, 9)])),
+]
+
+
+@pytest.mark.parametrize("name,pr", BAD, ids=[b[0] for b in BAD])
+def test_device_validation_raises_reference_messages(name, pr):
+    with Engine(0) as eng:
+        with pytest.raises(ConfigError) as got:
+            eng.set_problem(pr)
+    if "non-finite" in name:
+        # the reference accepts NaN/inf and runs into NaN energies; the engine
+        # refuses them up front (its FP32 certificate needs finite fields)
+        assert "must be finite" in str(got.value)
+        return
+    with pytest.raises(O.OracleError) as want:
+        O.run(pr, [1.0], [0.5], 2, 1)
+    assert str(got.value) == want.value.msg
