@@ -498,11 +498,13 @@ __device__ __forceinline__ void plane_dispatch(const PlaneArgs& a, const Chunk& 
     case (C) * 4 + (Q): plane_site<C, Q, RULE, WV, TAIL>(a, ch, ty, wb, t, count, lower, acc_c, acc_q, tq, qn); break;
     if constexpr (FAST) {
         switch (ty.ncb * 4 + ty.nqb) {
+            TG_CASE(0, 0) TG_CASE(0, 1)
             TG_CASE(1, 0) TG_CASE(1, 1) TG_CASE(2, 0) TG_CASE(2, 1)
             default: break;
         }
     } else {
         switch (ty.ncb * 4 + ty.nqb) {
+            TG_CASE(0, 0) TG_CASE(0, 1) TG_CASE(0, 2)
             TG_CASE(1, 0) TG_CASE(1, 1) TG_CASE(1, 2)
             TG_CASE(2, 0) TG_CASE(2, 1) TG_CASE(2, 2)
             TG_CASE(3, 0) TG_CASE(3, 1) TG_CASE(3, 2)
@@ -554,7 +556,6 @@ __device__ __forceinline__ void plane_phase(const PlaneArgs& a, int c, uint64_t 
 constexpr int kPfRows = 5;                     // own row + up to 4 neighbours
 template <int WV>
 __host__ __device__ constexpr int pf_stage_words() { return kPfRows * 32 * WV + 4 * 32; }  // rows + neighbour entries
-constexpr int kPfStageWords = pf_stage_words<4>();
 template <int RULE, int WV>
 __device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64_t t, bool count,
                                                int gidx, int ngroups, int wb, int32_t* cnt_c,
@@ -612,6 +613,8 @@ __device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64
         const int32_t* idx = reinterpret_cast<const int32_t*>(rows + kPfRows * 32 * WV);
         const PlaneType& ty = a.ty[cur.type];
         switch (ty.ncb * 4 + ty.nqb) {
+            case 0 * 4 + 0: plane_site<0, 0, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
+            case 0 * 4 + 1: plane_site<0, 1, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
             case 1 * 4 + 0: plane_site<1, 0, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
             case 1 * 4 + 1: plane_site<1, 1, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
             case 2 * 4 + 0: plane_site<2, 0, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
@@ -777,11 +780,13 @@ __device__ __forceinline__ void plane_phase_loop(const PlaneArgs& a, int c, uint
         case (C) * 4 + (Q): plane_site_loop<C, Q, RULE>(a, ch, ty, t, count, lower, sacc_c, sacc_q); break;
         if constexpr (FAST) {
             switch (ty.ncb * 4 + ty.nqb) {
+                TG_LCASE(0, 0) TG_LCASE(0, 1)
                 TG_LCASE(1, 0) TG_LCASE(1, 1) TG_LCASE(2, 0) TG_LCASE(2, 1)
                 default: break;
             }
         } else {
             switch (ty.ncb * 4 + ty.nqb) {
+                TG_LCASE(0, 0) TG_LCASE(0, 1) TG_LCASE(0, 2)
                 TG_LCASE(1, 0) TG_LCASE(1, 1) TG_LCASE(1, 2)
                 TG_LCASE(2, 0) TG_LCASE(2, 1) TG_LCASE(2, 2)
                 TG_LCASE(3, 0) TG_LCASE(3, 1) TG_LCASE(3, 2)

@@ -105,3 +105,13 @@ def test_device_validation_raises_reference_messages(name, pr):
     with pytest.raises(O.OracleError) as want:
         O.run(pr, [1.0], [0.5], 2, 1)
     assert str(got.value) == want.value.msg
+
+
+@pytest.mark.parametrize("engine", ["slot", "plane"])
+def test_degenerate_instances(engine):
+    # a free spin (test_engine.cpp:23-25), isolated spins, and chains without couplings
+    free = Problem.make(1, [], [0.0])
+    lone = Problem.make(5, [], [0.0] * 5)
+    pairs_only = Problem.make(6, [], [0.0] * 6, [(0, 3), (1, 4), (2, 5)])
+    for pr in (free, lone, pairs_only):
+        check(pr, [0.5, 1.0], [1.0, 2.0], 12, 4, engine)
