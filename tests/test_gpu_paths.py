@@ -115,3 +115,50 @@ def test_degenerate_instances(engine):
     pairs_only = Problem.make(6, [], [0.0] * 6, [(0, 3), (1, 4), (2, 5)])
     for pr in (free, lone, pairs_only):
         check(pr, [0.5, 1.0], [1.0, 2.0], 12, 4, engine)
+
+
+def test_plane_full_word_budget_32x32():
+    # 1024 replicas = 32 words per site row (the PLANE engine's maximum)
+    pr = I.bipartite_3regular(256, seed=5)
+    betas = list(np.geomspace(0.2, 5.0, 32))
+    pens = [k / 64.0 for k in range(32)]
+    check(pr, betas, pens, 12, 7, "plane")
+
+
+def test_slot_32x32_grid():
+    pr = I.wishart_planted(8, 0.5, seed=2)
+    betas, pens = I.wishart_schedule(pr, 32, 32)
+    order, _, _ = I.canonical_order(pr)
+    o = O.run(pr.permuted(order), betas, pens, 8, 1, seed=3)
+    recs, grid, cp, cb = run(pr, betas, pens, 8, 3, "slot")
+    np.testing.assert_allclose(recs[:, 0], o.f, rtol=1e-9, atol=1e-9)
+    np.testing.assert_array_equal(recs[:, 1], o.g)
+    np.testing.assert_array_equal(grid[:, np.asarray(order)], o.final_grid)
+    np.testing.assert_array_equal(cp, o.accepts_p)
+    np.testing.assert_array_equal(cb, o.accepts_b)
+
+
+@pytest.mark.parametrize("engine", ["slot", "plane"])
+def test_record_every_decimates(engine):
+    pr = I.k10_pm1(3)
+    betas, pens = I.config_schedule("c1")
+    o = O.run(pr, betas, pens, 30, 1, seed=4, states=True)
+    if engine == "plane":
+        o = O.run(pr, betas, pens, 30, 1, seed=4, states=True, rng="plane")
+    with Engine(0) as eng:
+        eng.set_problem(pr)
+        eng.set_schedule(betas, pens)
+        got = []
+
+        def sink(r, n, states, ap, ab):
+            st = np.ctypeslib.as_array(states, shape=(n * pr.n,)).reshape(n, pr.n)
+            for k in range(n):
+                got.append((r[k].round, r[k].f, r[k].g, st[k].copy()))
+            return 0
+
+        eng.run(RunConfig(total_sweeps=30, seed=4, engine=engine, record_every=3, store_states=True,
+                          digest=False), sink)
+    assert [g[0] for g in got] == list(range(3, 31, 3))
+    for rnd, f, g, st in got:
+        assert f == o.f[rnd - 1] and g == o.g[rnd - 1]
+        np.testing.assert_array_equal(st, o.states[rnd - 1])
