@@ -162,3 +162,28 @@ def test_record_every_decimates(engine):
     for rnd, f, g, st in got:
         assert f == o.f[rnd - 1] and g == o.g[rnd - 1]
         np.testing.assert_array_equal(st, o.states[rnd - 1])
+
+
+@pytest.mark.parametrize("engine", ["slot", "plane"])
+def test_context_reuse_equals_fresh_contexts(engine):
+    # one context: problem A, run, problem B, run, schedule change, run -- each
+    # result must equal a fresh context's (buffers are pooled and re-sized)
+    a, b = I.k10_pm1(1), I.bipartite_3regular(64, seed=2)
+    sa, sb = I.config_schedule("c1"), ([0.3, 1.0, 2.0], [0.0, 0.25])
+    runs = [(a, sa, 20, 1), (b, sb, 16, 2), (b, ([0.5, 1.5], [0.0, 0.5, 1.0]), 10, 3), (a, sa, 20, 1)]
+
+    def once(eng, pr, sc, total, seed):
+        eng.set_problem(pr)
+        eng.set_schedule(*sc)
+        recs = []
+        eng.run(RunConfig(total_sweeps=total, seed=seed, engine=engine, store_states=False, digest=True),
+                lambda r, n, s, x, y: [recs.append((r[k].f, r[k].g, r[k].digest)) for k in range(n)] and 0)
+        return recs, eng.grid()
+
+    with Engine(0) as eng:
+        shared = [once(eng, *r) for r in runs]
+    for r, (recs, grid) in zip(runs, shared):
+        with Engine(0) as eng:
+            fresh_recs, fresh_grid = once(eng, *r)
+        assert recs == fresh_recs
+        np.testing.assert_array_equal(grid, fresh_grid)
