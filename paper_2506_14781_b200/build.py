@@ -18,8 +18,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtempergrid_b200.so")
 CPPLIB = os.path.join(PKG, "libtempergrid_cpp.so")
-SOURCES = ["kernels.cu", "capi.cu", "plane_sweep.cu", "slot_engine.cu", "prep.cu"]
-HEADERS = ["engine.cuh", "kernels.cuh", "philox.cuh", "plane_device.cuh"]
+SOURCES = ["kernels.cu", "capi.cu", "host_common.cu", "host_plane.cu", "host_slot.cu",
+           "host_run.cu", "host_extras.cu", "plane_sweep.cu", "slot_engine.cu", "prep.cu"]
+HEADERS = ["engine.cuh", "kernels.cuh", "philox.cuh", "plane_device.cuh", "host.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -46,6 +47,9 @@ def build_engine(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
     units = [("kernels.cu", "kernels.o", []), ("capi.cu", "capi.o", []),
+             ("host_common.cu", "host_common.o", []), ("host_plane.cu", "host_plane.o", []),
+             ("host_slot.cu", "host_slot.o", []), ("host_run.cu", "host_run.o", []),
+             ("host_extras.cu", "host_extras.o", []),
              ("plane_sweep.cu", "plane_r0.o", ["-DTG_PLANE_RULE=0"]),
              ("plane_sweep.cu", "plane_r1.o", ["-DTG_PLANE_RULE=1"]),
              ("slot_engine.cu", "slot_engine.o", []), ("prep.cu", "prep.o", [])]

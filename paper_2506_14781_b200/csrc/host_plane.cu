@@ -1,0 +1,346 @@
+// host_plane.cu -- PLANE engine host driver: eligibility, structure from the device prep (or the host), threshold tables, launch arguments, the fused round loop.
+#include "host.cuh"
+
+namespace tgh {
+
+bool plane_eligible(tg_ctx& c, std::string* why) {
+    if (c.dev_prep) {
+        if (c.prep.info & kPrepNotPM1) { if (why) *why = "couplings must be +-1"; return false; }
+        if (c.prep.info & kPrepNonzeroField) { if (why) *why = "fields must be 0"; return false; }
+        if (c.prep.max_dc > kMaxDC || c.prep.max_dq > kMaxDQ) { if (why) *why = "degree bound exceeded"; return false; }
+        return true;
+    }
+    ensure_host_arrays(c);
+    for (double w : c.cw) if (!(w == 1.0 || w == -1.0)) { if (why) *why = "couplings must be +-1"; return false; }
+    for (double x : c.h) if (x != 0.0) { if (why) *why = "fields must be 0"; return false; }
+    std::vector<int> dc(c.n, 0), dq(c.n, 0);
+    for (size_t k = 0; k < c.ci.size(); ++k) { dc[c.ci[k]]++; dc[c.cj[k]]++; }
+    for (size_t k = 0; k < c.pa.size(); ++k) { dq[c.pa[k]]++; dq[c.pb[k]]++; }
+    for (int i = 0; i < c.n; ++i)
+        if (dc[i] > kMaxDC || dq[i] > kMaxDQ) { if (why) *why = "degree bound exceeded"; return false; }
+    return true;
+}
+
+void build_plane_structure_device(tg_ctx& c, std::vector<PlaneType>& types, std::vector<Chunk>& chunks,
+                                  std::vector<int>& chunk_off) {
+    const PrepSummary& P = c.prep;
+    const int mq1 = P.max_dq + 1, mc1 = P.max_dc + 1;
+    std::vector<int> tid_of((kMaxDC + 1) * (kMaxDQ + 1), -1);
+    chunk_off.assign(c.n_colors + 1, 0);
+    int start = 0, cur_col = -1;
+    for (size_t q = 0; q < P.run_keys.size(); ++q) {
+        const unsigned key = P.run_keys[q];
+        const int cnt = P.run_counts[q];
+        const int dc = (int)(key % mc1), dq = (int)((key / mc1) % mq1), col = (int)(key / ((unsigned)mc1 * mq1));
+        while (cur_col < col) chunk_off[++cur_col] = (int)chunks.size();
+        const int tkey = dc * (kMaxDQ + 1) + dq;
+        if (tid_of[tkey] < 0) {
+            PlaneType t{};
+            t.dc = dc;
+            t.dq = dq;
+            t.ncb = nbits(dc);
+            t.nqb = nbits(dq);
+            t.ncl = std::max(4, 1 << (t.ncb + t.nqb));
+            tid_of[tkey] = (int)types.size();
+            types.push_back(t);
+        }
+        for (int s0 = start; s0 < start + cnt; s0 += 32)
+            chunks.push_back(Chunk{s0, std::min(32, start + cnt - s0), tid_of[tkey], 0});
+        start += cnt;
+    }
+    while (cur_col < c.n_colors) chunk_off[++cur_col] = (int)chunks.size();
+    chunk_off[c.n_colors] = (int)chunks.size();
+}
+
+void build_plane(tg_ctx& c) {
+    HostTimer tm_("build_plane");
+    cudaStream_t st = c.stream;
+    const int n = c.n;
+    if (c.dev_prep) {
+        std::vector<PlaneType> types;
+        std::vector<Chunk> chunks;
+        std::vector<int> chunk_off;
+        build_plane_structure_device(c, types, chunks, chunk_off);
+        c.d_nbr.copy_from(c.d_nbr_dev, st);
+        c.d_chunks.upload(chunks, st);
+        CK(plane_chunk_bases(c.d_chunks.p, (int)chunks.size(), c.d_base_dev.p, st, c.sms));
+        build_plane_rest(c, types, chunk_off);
+        return;
+    }
+    ensure_host_arrays(c);
+    ensure_host_canonical(c);
+    // internal adjacency as flat CSR (cost entries carry the J<0 sign bit)
+    std::vector<int> dcv(n, 0), dqv(n, 0);
+    for (size_t k = 0; k < c.ci.size(); ++k) { dcv[c.inv[c.ci[k]]]++; dcv[c.inv[c.cj[k]]]++; }
+    for (size_t k = 0; k < c.pa.size(); ++k) { dqv[c.inv[c.pa[k]]]++; dqv[c.inv[c.pb[k]]]++; }
+    std::vector<int> base(n + 1, 0);
+    for (int i = 0; i < n; ++i) base[i + 1] = base[i] + dcv[i] + dqv[i];
+    std::vector<int32_t> nbr(base[n]);
+    {
+        std::vector<int> cc(n), cq(n);
+        for (int i = 0; i < n; ++i) { cc[i] = base[i]; cq[i] = base[i] + dcv[i]; }
+        for (size_t k = 0; k < c.ci.size(); ++k) {
+            const int x = c.inv[c.ci[k]], y = c.inv[c.cj[k]];
+            const int32_t sgn = c.cw[k] < 0 ? (int32_t)0x80000000u : 0;
+            nbr[cc[x]++] = y | sgn;
+            nbr[cc[y]++] = x | sgn;
+        }
+        for (size_t k = 0; k < c.pa.size(); ++k) {
+            const int x = c.inv[c.pa[k]], y = c.inv[c.pb[k]];
+            nbr[cq[x]++] = y;
+            nbr[cq[y]++] = x;
+        }
+    }
+    // site types (cost degree, chain degree)
+    std::vector<int> tid_of((kMaxDC + 1) * (kMaxDQ + 1), -1);
+    std::vector<int> site_type(n);
+    std::vector<PlaneType> types;
+    for (int i = 0; i < n; ++i) {
+        const int key = dcv[i] * (kMaxDQ + 1) + dqv[i];
+        if (tid_of[key] < 0) {
+            PlaneType t{};
+            t.dc = dcv[i];
+            t.dq = dqv[i];
+            t.ncb = nbits(t.dc);
+            t.nqb = nbits(t.dq);
+            t.ncl = std::max(4, 1 << (t.ncb + t.nqb));
+            tid_of[key] = (int)types.size();
+            types.push_back(t);
+        }
+        site_type[i] = tid_of[key];
+    }
+    // chunks (colour-major; the canonical order keeps types contiguous)
+    std::vector<Chunk> chunks;
+    std::vector<int> chunk_off(c.n_colors + 1, 0);
+    for (int col = 0; col < c.n_colors; ++col) {
+        chunk_off[col] = (int)chunks.size();
+        int i = c.color_start[col];
+        const int end = c.color_start[col + 1];
+        while (i < end) {
+            const int ty = site_type[i];
+            int j = i;
+            while (j < end && j - i < 32 && site_type[j] == ty) ++j;
+            chunks.push_back(Chunk{i, j - i, ty, base[i]});
+            i = j;
+        }
+    }
+    chunk_off[c.n_colors] = (int)chunks.size();
+    c.d_nbr.upload(nbr, st);
+    c.d_chunks.upload(chunks, st);
+    build_plane_rest(c, types, chunk_off);
+}
+
+// Everything after the site types and chunks: threshold tables, words, keys,
+// masks, buffers and the cooperative grids.
+void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vector<int>& chunk_off) {
+    cudaStream_t st = c.stream;
+    const int n = c.n;
+    if ((int)types.size() > kMaxTypes) fail(TG_ERR_RESOURCE, "plane engine: too many site types");
+    int kpw = 0, krow = 0;
+    for (auto& t : types) {
+        t.kp_off = kpw;
+        t.ktab_off = krow;
+        kpw += kKWords * t.ncl;
+        krow += t.ncl;
+    }
+    c.kpw = kpw;
+    c.ktab_row = krow;
+    c.n_types = (int)types.size();
+    // words, keys, masks: rows padded to a whole number of WV-word passes
+    const int w_log = (c.R_local + 31) / 32;
+    c.WV = w_log > 2 ? 4 : w_log;
+    if (const char* e = std::getenv("TG_PLANE_WV")) {  // tuning override: 1, 2 or 4
+        const int v = std::atoi(e);
+        if (v == 1 || v == 2 || v == 4) c.WV = std::min(v, w_log > 2 ? 4 : (w_log > 1 ? 2 : 1));
+    }
+    c.W = (w_log + c.WV - 1) / c.WV * c.WV;
+    if (c.W > kMaxWordsArg) fail(TG_ERR_RESOURCE, "plane engine: %d replicas per rank exceed %d", c.R_local, 32 * kMaxWordsArg);
+    std::vector<uint32_t> active(c.W, 0u);
+    std::vector<uint2> wkey(c.W);
+    for (int w = 0; w < c.W; ++w) {
+        for (int l = 0; l < 32; ++l) if (w * 32 + l < c.R_local) active[w] |= 1u << l;
+        const uint64_t k = derive_seed(c.cfg.seed, kPurposePlane, (uint64_t)(c.state0 / 32 + w));
+        wkey[w] = make_uint2((uint32_t)k, (uint32_t)(k >> 32));
+    }
+    // thresholds per (slot, type, class)
+    std::vector<uint64_t> ktab((size_t)c.R * krow, 0ull);
+    for (int slot = 0; slot < c.R; ++slot) {
+        const double beta = c.betas[slot / c.J], P = c.pens[slot % c.J];
+        for (const auto& t : types) {
+            for (int cl = 0; cl < t.ncl; ++cl) {
+                const int ncnt = cl & ((1 << t.ncb) - 1);
+                const int qcnt = cl >> t.ncb;
+                uint64_t K = 0;
+                if (ncnt <= t.dc && qcnt <= t.dq) {
+                    // s_i * local_i (Metropolis, counts of satisfied bonds) or
+                    // local_i (heat bath, counts of +1 contributions)
+                    const double v = (double)(2 * ncnt - t.dc) + 2.0 * P * (double)(2 * qcnt - t.dq);
+                    K = c.cfg.rule == TG_RULE_METROPOLIS ? threshold_metropolis(beta, 2.0 * v)
+                                                         : threshold_heat_bath(beta, v);
+                }
+                ktab[(size_t)slot * krow + t.ktab_off + cl] = K;
+            }
+        }
+    }
+    c.m_cost = c.m;
+    c.d_chunk_off.upload(chunk_off, st);
+    c.d_color_start.upload(c.color_start, st);
+    c.d_types.upload(types, st);
+    c.h_types = types;
+    c.h_active = active;
+    c.h_wkey = wkey;
+    c.d_ktab.upload(ktab, st);
+    c.d_kp.alloc((size_t)c.W * kpw);
+    c.d_kp.zero(st);
+    c.d_kpc.alloc((size_t)c.W * c.n_types * 128);
+    c.d_kpc.zero(st);
+    c.d_spins32.alloc((size_t)n * c.W);
+    c.d_cnt_c.alloc((size_t)c.W * 32);
+    c.d_cnt_q.alloc((size_t)c.W * 32);
+    c.d_cnt_c.zero(st);
+    c.d_cnt_q.zero(st);
+    c.d_cnt2.alloc((size_t)4 * c.W * 32);
+    c.d_cnt2.zero(st);
+    c.d_work.alloc((size_t)2 * c.n_colors * std::max(1, c.W));
+    c.d_work.zero(st);
+    // cooperative grid: a multiple of W warps, all blocks co-resident
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)plane_sweep_fn(c.cfg.rule, c.WV),
+                                                     kPlaneThreads, 0));
+    if (per_sm < 1) fail(TG_ERR_RESOURCE, "plane engine: kernel does not fit on an SM");
+    int blocks = per_sm * c.sms;
+    const int wpb = kPlaneThreads / 32;
+    const int passes = c.W / c.WV;
+    blocks -= blocks % passes;  // each block owns one pass of WV words
+    if (blocks < passes) fail(TG_ERR_RESOURCE, "plane engine: cannot tile %d words", c.W);
+    c.plane_grid = blocks;
+    // fused round-loop kernel (single GPU)
+    c.fused_fast = 1;
+    for (const auto& t : types) if (t.ncb > 2 || t.nqb > 1) c.fused_fast = 0;
+    // FAST: specialised kernel for site types with cost degree <= 3 and chain
+    // degree <= 1 (config 5), cp.async row prefetch; TG_PLANE_FAST=0 disables.
+    if (const char* e = std::getenv("TG_PLANE_FAST")) c.fused_fast = c.fused_fast && std::atoi(e) != 0;
+    c.fused_grid = 0;
+    if (c.world == 1 && c.R <= 2048) {
+        c.fused_wv = c.WV;
+        if (const char* e = std::getenv("TG_PLANE_LOOP")) if (std::atoi(e)) c.fused_wv = 0;
+        const void* fn = plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast);
+        c.fused_block = c.fused_fast ? kPlaneThreadsFast : kPlaneThreads;
+        const size_t pf_words = c.fused_fast && (c.fused_wv == 4 || c.fused_wv == 2)
+                                    ? (size_t)2 * (5 * 32 * c.fused_wv + 4 * 32) : 0;
+        const size_t tail_words = c.fused_fast && (c.fused_wv == 4 || c.fused_wv == 2)
+                                      ? 0 : std::max<size_t>(kTailCap * 7, (size_t)2 * c.W * 32);
+        c.fused_smem = (size_t)c.R * (2 * sizeof(double) + 2 * sizeof(int32_t)) + 8 +
+                       (size_t)(c.fused_block / 32) * std::max(pf_words, tail_words) * sizeof(int32_t);
+        if (c.fused_smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.fused_smem));
+        int fb = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fb, fn, c.fused_block, c.fused_smem));
+        if (fb >= 1) {
+            int g = fb * c.sms;
+            const int fp = c.fused_wv ? passes : 1;
+            g -= g % fp;
+            if (g >= fp) c.fused_grid = g;
+        }
+    }
+}
+
+PlaneArgs plane_args(tg_ctx& c) {
+    PlaneArgs a{};
+    a.n = c.n;
+    a.W = c.W;
+    a.n_colors = c.n_colors;
+    a.local_states = c.R_local;
+    a.rule = c.cfg.rule;
+    a.n_types = c.n_types;
+    a.kpw = c.kpw;
+    a.m_cost = c.m_cost;
+    a.spins = c.d_spins32.p;
+    a.nbr = c.d_nbr.p;
+    a.chunks = c.d_chunks.p;
+    a.chunk_off = c.d_chunk_off.p;
+    a.color_start = c.d_color_start.p;
+    for (int q = 0; q < c.n_types && q < kMaxTypes; ++q) a.ty[q] = c.h_types[q];
+    for (int w = 0; w < c.W && w < kMaxWordsArg; ++w) a.active[w] = c.h_active[w];
+    philox_key_schedule(derive_seed(c.cfg.seed, kPurposePlane, 0), a.pks);
+    a.state_slot = c.d_state_slot.p;
+    a.ktab = c.d_ktab.p;
+    a.ktab_row = c.ktab_row;
+    a.w_global0 = c.state0 / 32;
+    a.kp = c.d_kp.p;
+    a.kpc = c.d_kpc.p;
+    a.cnt_c = c.d_cnt_c.p;
+    a.cnt_q = c.d_cnt_q.p;
+    a.f_loc = c.d_f.p + c.state0;
+    a.g_loc = c.d_g.p + c.state0;
+    return a;
+}
+
+void rebuild_planes(tg_ctx& c) {
+    if (c.engine != TG_ENGINE_PLANE) return;
+    SwapArgs a = swap_args(c);
+    // round 1 of a 1x1-like schedule attempts nothing: fake I=J=1 for the swap part
+    a.I = 1;
+    a.J = 1;
+    swap_kernel<<<1, kSwapThreads, 0, c.stream>>>(a, 1, 0, c.rec_cap, 0);
+    CK(cudaGetLastError());
+}
+
+void s2_build(tg_ctx& c, const tg_run_config* cfg);
+
+void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
+    cudaStream_t st = c.stream;
+    const int flags = c.cfg.record_flags;
+    if (c.profiling && c.ev.size() < 2) {
+        for (auto e : c.ev) cudaEventDestroy(e);
+        c.ev.assign(2, nullptr);
+        for (auto& e : c.ev) CK(cudaEventCreate(&e));
+    }
+    double sweep_ms = 0;
+    int64_t left = n_rounds;
+    while (left > 0) {
+        const int n = (int)std::min<int64_t>(left, c.rec_cap);
+        CK(cudaMemsetAsync(c.d_rec.p, 0, sizeof(TgRecordDev) * n, st));
+        PlaneArgs a = plane_args(c);
+        RoundArgs r{};
+        r.I = c.I; r.J = c.J; r.R = c.R; r.sps = (int)c.cfg.sweeps_per_swap;
+        r.round0 = c.rounds_done + 1;
+        r.n_rounds = n;
+        r.rec_flags = flags & (TG_REC_DIGEST | TG_REC_STATE | TG_REC_COUNTERS);
+        r.swap_base0 = c.swap_base;
+        r.swap_seed = derive_seed(c.cfg.seed, kPurposeSwap, 0);
+        r.betas = c.d_betas.p; r.pens = c.d_pens.p;
+        r.slot_state = c.d_slot_state.p; r.state_slot = c.d_state_slot.p;
+        r.acc_p = c.d_acc_p.p; r.acc_b = c.d_acc_b.p;
+        r.f_all = c.d_f.p; r.g_all = c.d_g.p;
+        r.cnt = c.d_cnt2.p; r.cnt_stride = c.W * 32;
+        // dynamic chunk grabbing measured 3% slower than the static split (r1); opt in
+        r.work = (std::getenv("TG_PLANE_DYNAMIC") ? c.d_work.p : nullptr);
+        r.ktab = c.d_ktab.p; r.ktab_row = c.ktab_row; r.kp = c.d_kp.p; r.kpc = c.d_kpc.p;
+        r.rec = c.d_rec.p; r.rec_acc = c.d_rec_acc.p;
+        r.rec_states = (flags & TG_REC_STATE) ? c.d_rec_states.p : nullptr;
+        r.perm = c.d_perm.p;
+        void* args[] = {&a, &r};
+        if (c.profiling) CK(cudaEventRecord(c.ev[0], st));
+        CK(cudaLaunchCooperativeKernel(plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast),
+                                       dim3(c.fused_grid), dim3(c.fused_block), args, c.fused_smem, st));
+        if (c.profiling) CK(cudaEventRecord(c.ev[1], st));
+        c.sweep_launches++;
+        const int64_t first = c.rounds_done + 1;
+        for (int k = 0; k < n; ++k) c.swap_base += (uint64_t)round_attempts(c.I, c.J, first + k);
+        c.rounds_done += n;
+        left -= n;
+        drain(c, n, first, sink);
+        if (c.profiling) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));
+            sweep_ms += ms;
+        }
+    }
+    CK(cudaStreamSynchronize(st));
+    c.last_sweep_ms = sweep_ms;
+    c.last_swap_ms = 0;
+}
+
+
+}  // namespace tgh
