@@ -139,7 +139,7 @@ void do_init(tg_ctx& c, const tg_run_config* cfg) {
     if (eng == TG_ENGINE_PLANE) build_plane(c); else build_slot(c);
     // initial configurations (engine.cpp:98-106)
     if (eng == TG_ENGINE_PLANE) {
-        plane_init_kernel<<<c.sms * 4, 256, 0, st>>>(c.d_spins32.p, c.n, c.W, c.R_local, c.state0, c.cfg.seed);
+        plane_init_kernel<<<c.sms * 16, 256, 0, st>>>(c.d_spins32.p, c.n, c.W, c.R_local, c.state0, c.cfg.seed);
     } else {
         slot_init_kernel<<<c.sms * 4, 256, 0, st>>>(c.d_spins8.p, c.n, c.R_local, c.state0, c.cfg.seed);
     }

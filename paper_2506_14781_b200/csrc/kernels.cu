@@ -402,15 +402,22 @@ __global__ void plane_init_kernel(uint32_t* spins, int n, int W, int local_state
                                   uint64_t seed) {
     const int lane = threadIdx.x & 31;
     const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-    const long long items = (long long)((n + 1) >> 1) * W;
-    for (long long it = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); it < items; it += nw) {
-        const int w = (int)(it % W);
+    const long long gw = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+    const long long npairs = (n + 1) >> 1;
+    // a warp keeps one word (its lanes' init keys) when the warp count allows
+    const bool fixed_w = nw % W == 0;
+    const long long items = npairs * W;
+    int w = (int)(gw % W);
+    uint64_t key = derive_seed(seed, kPurposeInit, (uint64_t)(state0 + w * 32 + lane));
+    for (long long it = gw; it < items; it += nw) {
+        if (!fixed_w) {
+            w = (int)(it % W);
+            key = derive_seed(seed, kPurposeInit, (uint64_t)(state0 + w * 32 + lane));
+        }
         const long long p = it / W;
-        const int m = w * 32 + lane;
-        const uint64_t key = derive_seed(seed, kPurposeInit, (uint64_t)(state0 + m));
         const u32x4 o = philox4x32_10(u32x4{(uint32_t)p, (uint32_t)((uint64_t)p >> 32), 0u, 0u},
                                       (uint32_t)key, (uint32_t)(key >> 32));
-        const bool live = m < local_states;
+        const bool live = w * 32 + lane < local_states;
         const uint32_t w0 = __ballot_sync(0xffffffffu, live && (o.y >> 31));  // draw 2p
         const uint32_t w1 = __ballot_sync(0xffffffffu, live && (o.w >> 31));  // draw 2p + 1
         if (lane == 0) {

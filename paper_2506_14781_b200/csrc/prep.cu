@@ -46,7 +46,8 @@ __global__ void k_check_couplings(int n, int m, const int* ci, const int* cj, co
             atomicOr(bad, kPrepBadCoupling);
             continue;
         }
-        if (!(w[k] == 1.0 || w[k] == -1.0)) atomicOr(bad, kPrepNotPM1);
+        if (!(w[k] == 1.0 || w[k] == -1.0) && !(*(volatile unsigned*)bad & kPrepNotPM1))
+            atomicOr(bad, kPrepNotPM1);  // set once; later threads see it and skip the atomic
         atomicAdd(&degc[x], 1);
         atomicAdd(&degc[y], 1);
     }
@@ -70,13 +71,17 @@ __global__ void k_degrees(int n, const double* h, const int* degc, const int* de
     int mc = 0, mq = 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         if (!isfinite(h[i])) atomicOr(bad, kPrepBadField);
-        if (h[i] != 0.0) atomicOr(bad, kPrepNonzeroField);
+        if (h[i] != 0.0 && !(*(volatile unsigned*)bad & kPrepNonzeroField)) atomicOr(bad, kPrepNonzeroField);
         deg[i] = degc[i] + degq[i];
         mc = max(mc, degc[i]);
         mq = max(mq, degq[i]);
     }
-    atomicMax(&maxd[0], mc);
-    atomicMax(&maxd[1], mq);
+    mc = __reduce_max_sync(0xffffffffu, mc);
+    mq = __reduce_max_sync(0xffffffffu, mq);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&maxd[0], mc);
+        atomicMax(&maxd[1], mq);
+    }
 }
 
 // rows: [off[i], off[i] + degc[i]) cost entries (neighbour | J<0 sign bit),
@@ -175,7 +180,7 @@ __global__ void k_colour(int n, const int* off, const int* adj, int* color, int*
 }
 
 __global__ void k_keys(int n, const int* color, const int* degc, const int* degq, const int* maxd,
-                       unsigned* key, int* idx, int* ncol, int* color_count) {
+                       unsigned* key, int* idx, int* ncol) {
     const int mc = maxd[0], mq = maxd[1];
     int mx = 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -183,9 +188,9 @@ __global__ void k_keys(int n, const int* color, const int* degc, const int* degq
         key[i] = (unsigned)((c * (mq + 1) + degq[i]) * (mc + 1) + degc[i]);
         idx[i] = i;
         mx = max(mx, c);
-        atomicAdd(&color_count[c], 1);
     }
-    atomicMax(ncol, mx + 1);
+    mx = __reduce_max_sync(0xffffffffu, mx);  // one atomic per warp, not per thread
+    if ((threadIdx.x & 31) == 0) atomicMax(ncol, mx + 1);
 }
 
 __global__ void k_inverse(int n, const int* order, const int* deg, int* inv, int* deg_int) {
@@ -331,10 +336,8 @@ cudaError_t plane_prep_device(const PrepIn& in, const PrepOut& o, PrepSummary& r
     unsigned* key = T.get<unsigned>(n);
     unsigned* key_sorted = T.get<unsigned>(n);
     int* idx = T.get<int>(n);
-    int* ccount = T.get<int>(65);
-    PA(key); PA(key_sorted); PA(idx); PA(ccount);
-    PK(cudaMemsetAsync(ccount, 0, sizeof(int) * 65, st));
-    k_keys<<<gb, 256, 0, st>>>(n, color, degc, degq, maxd, key, idx, ncol, ccount);
+    PA(key); PA(key_sorted); PA(idx);
+    k_keys<<<gb, 256, 0, st>>>(n, color, degc, degq, maxd, key, idx, ncol);
     PK(cudaGetLastError());
     const unsigned long long kmax = 64ull * (h_maxd[1] + 1) * (h_maxd[0] + 1);
     int end_bit = 1;
