@@ -19,8 +19,8 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtempergrid_b200.so")
 CPPLIB = os.path.join(PKG, "libtempergrid_cpp.so")
 SOURCES = ["kernels.cu", "capi.cu", "host_common.cu", "host_plane.cu", "host_slot.cu",
-           "host_run.cu", "host_extras.cu", "plane_sweep.cu", "slot_engine.cu", "prep.cu"]
-HEADERS = ["engine.cuh", "kernels.cuh", "philox.cuh", "plane_device.cuh", "host.cuh"]
+           "host_run.cu", "host_extras.cu", "plane_sweep.cu", "plane_tpw.cu", "slot_engine.cu", "prep.cu"]
+HEADERS = ["engine.cuh", "kernels.cuh", "philox.cuh", "plane_device.cuh", "plane_round.cuh", "host.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -52,6 +52,8 @@ def build_engine(force: bool = False, verbose: bool = False) -> str:
              ("host_extras.cu", "host_extras.o", []),
              ("plane_sweep.cu", "plane_r0.o", ["-DTG_PLANE_RULE=0"]),
              ("plane_sweep.cu", "plane_r1.o", ["-DTG_PLANE_RULE=1"]),
+             ("plane_tpw.cu", "tpw_r0.o", ["-DTG_PLANE_RULE=0"]),
+             ("plane_tpw.cu", "tpw_r1.o", ["-DTG_PLANE_RULE=1"]),
              ("slot_engine.cu", "slot_engine.o", []), ("prep.cu", "prep.o", [])]
     procs = []
     for src, obj, extra in units:

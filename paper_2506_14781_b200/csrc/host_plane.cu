@@ -1,5 +1,6 @@
 // host_plane.cu -- PLANE engine host driver: eligibility, structure from the device prep (or the host), threshold tables, launch arguments, the fused round loop.
 #include "host.cuh"
+#include "plane_round.cuh"
 
 namespace tgh {
 
@@ -182,6 +183,18 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
             }
         }
     }
+    // Metropolis, cost degree 3, no chain partner: flag bit 0 = classes 2 and
+    // 3 (de > 0) are never "always" under any label, so a lane is undecided
+    // iff its class is 2 or 3 (plane_tpw.cu's single-select compare)
+    for (auto& t : types) {
+        t.pad = 0;
+        if (c.cfg.rule != TG_RULE_METROPOLIS || t.dc != 3 || t.dq != 0 || t.ncb != 2) continue;
+        bool ok = true;
+        for (int slot = 0; slot < c.R && ok; ++slot)
+            for (int cl = 2; cl < 4; ++cl)
+                if (ktab[(size_t)slot * krow + t.ktab_off + cl] >= (1ull << 53)) ok = false;
+        t.pad = ok ? 1 : 0;
+    }
     c.m_cost = c.m;
     c.d_chunk_off.upload(chunk_off, st);
     c.d_color_start.upload(c.color_start, st);
@@ -221,7 +234,32 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
     // degree <= 1 (config 5), cp.async row prefetch; TG_PLANE_FAST=0 disables.
     if (const char* e = std::getenv("TG_PLANE_FAST")) c.fused_fast = c.fused_fast && std::atoi(e) != 0;
     c.fused_grid = 0;
-    if (c.world == 1 && c.R <= 2048) {
+    c.fused_tpw = 0;
+    // thread-per-(site, word) kernel: rows of a power-of-two number of words
+    if (c.world == 1 && c.R <= 2048 && (c.W & (c.W - 1)) == 0 && c.W <= 32) {
+        c.fused_tpw = 1;
+        if (const char* e = std::getenv("TG_PLANE_TPW")) c.fused_tpw = std::atoi(e) != 0;
+    }
+    // tpw FAST variant (c5_site): Metropolis, every site of cost degree 3
+    // and chain degree 0 / 1, chain-free types with flag bit 0
+    c.tpw_fast = c.cfg.rule == TG_RULE_METROPOLIS;
+    for (const auto& t : types)
+        if (!(t.dc == 3 && (t.dq == 1 || (t.dq == 0 && (t.pad & 1))))) c.tpw_fast = 0;
+    if (const char* e = std::getenv("TG_PLANE_FAST")) c.tpw_fast = c.tpw_fast && std::atoi(e) != 0;
+    if (c.fused_tpw) {
+        const void* fn = plane_tpw_fn(c.cfg.rule, c.tpw_fast);
+        cudaFuncAttributes fa{};
+        CK(cudaFuncGetAttributes(&fa, fn));
+        c.fused_block = fa.maxThreadsPerBlock;  // the kernel's launch bound
+        c.fused_smem = tpw_smem_bytes(c.R, c.W, c.fused_block);
+        if (c.fused_smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.fused_smem));
+        int fb = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fb, fn, c.fused_block, c.fused_smem));
+        if (fb >= 1) c.fused_grid = fb * c.sms;
+        else c.fused_tpw = 0;
+    }
+    if (!c.fused_tpw && c.world == 1 && c.R <= 2048) {
         c.fused_wv = c.WV;
         if (const char* e = std::getenv("TG_PLANE_LOOP")) if (std::atoi(e)) c.fused_wv = 0;
         const void* fn = plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast);
@@ -322,7 +360,8 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         r.perm = c.d_perm.p;
         void* args[] = {&a, &r};
         if (c.profiling) CK(cudaEventRecord(c.ev[0], st));
-        CK(cudaLaunchCooperativeKernel(plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast),
+        CK(cudaLaunchCooperativeKernel(c.fused_tpw ? plane_tpw_fn(c.cfg.rule, c.tpw_fast)
+                                                   : plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast),
                                        dim3(c.fused_grid), dim3(c.fused_block), args, c.fused_smem, st));
         if (c.profiling) CK(cudaEventRecord(c.ev[1], st));
         c.sweep_launches++;

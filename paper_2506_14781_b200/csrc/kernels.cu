@@ -24,6 +24,9 @@ void* plane_sweep_fn_r1(int wv);
 void* plane_sweep_fn(int rule, int wv) { return rule == 0 ? plane_sweep_fn_r0(wv) : plane_sweep_fn_r1(wv); }
 void* plane_rounds_fn_r0(int wv, int fast);
 void* plane_rounds_fn_r1(int wv, int fast);
+void* plane_tpw_fn_r0(int fast);
+void* plane_tpw_fn_r1(int fast);
+void* plane_tpw_fn(int rule, int fast) { return rule == 0 ? plane_tpw_fn_r0(fast) : plane_tpw_fn_r1(fast); }
 void* plane_rounds_fn(int rule, int wv, int fast) {
     return rule == 0 ? plane_rounds_fn_r0(wv, fast) : plane_rounds_fn_r1(wv, fast);
 }

@@ -14,6 +14,23 @@ constexpr int kPlaneThreads = 512;
 constexpr int kPlaneThreadsFast = 512;
 constexpr int kPlaneMinBlocksFast = 1;
 constexpr int kPlaneMinBlocksLoop = 2;   // looped-row variant: 2 x 512 threads per SM
+#ifndef TG_TPW_THREADS
+#define TG_TPW_THREADS 512
+#endif
+constexpr int kTpwThreads = TG_TPW_THREADS;  // thread-per-(site, word) fused kernel (plane_tpw.cu)
+#ifndef TG_TPW_MINB
+#define TG_TPW_MINB 1
+#endif
+constexpr int kTpwMinBlocks = TG_TPW_MINB;
+constexpr int kTpwVB = 8;               // planes of its vertical bond counters
+constexpr int kTpwQCap = 64;            // per-warp deferred-tail queue entries (>= 31 + 32)
+// Dynamic shared memory of plane_tpw_rounds_kernel: tail queues
+// [warps][6][kTpwQCap], chain vertical counters [kTpwVB][threads],
+// per-replica counters [2][32W], labels and energies (plane_round.cuh).
+inline size_t tpw_smem_bytes(int R, int W, int threads) {
+    return (size_t)R * (2 * sizeof(double) + 2 * sizeof(int32_t)) + 8 + (size_t)2 * W * 32 * sizeof(int) +
+           (size_t)kTpwVB * threads * sizeof(int) + (size_t)(threads / 32) * kTpwQCap * 6 * sizeof(int);
+}
 constexpr int kSlotThreads = 256;
 constexpr int kSwapThreads = 1024;
 constexpr int kTailCap = 160;   // per-warp deferred-tail queue entries (plane_sweep.cu)
@@ -41,6 +58,7 @@ struct ExtractArgs {
 
 void* plane_sweep_fn(int rule, int wv);
 void* plane_rounds_fn(int rule, int wv, int fast);
+void* plane_tpw_fn(int rule, int fast);
 int plane_words_per_pass(int W);
 void* slot_sweep_fn();
 void* slot_sweep_fn_d(int D);  // padded-degree variant, D in {4, 8}

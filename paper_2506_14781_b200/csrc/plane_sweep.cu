@@ -13,6 +13,7 @@
 #include "engine.cuh"
 #include "kernels.cuh"
 #include "plane_device.cuh"
+#include "plane_round.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -867,15 +868,11 @@ plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__
                       (size_t)(threadIdx.x >> 5) * 2 * pf_stage_words<WV == 2 ? 2 : 4>();
     const int tid = threadIdx.x;
     const int wpb = blockDim.x >> 5;
-    const int warp = tid >> 5, lane = tid & 31;
-    const int gw = blockIdx.x * wpb + warp;
-    const int nw = gridDim.x * wpb;
+    const int warp = tid >> 5;
     const int passes = WV ? a.W / WV : 1;
     const int wb = WV ? (int)(blockIdx.x % passes) * WV : 0;
     const int gidx = (int)(blockIdx.x / passes) * wpb + warp;
     const int ngroups = (int)(gridDim.x / passes) * wpb;
-    const int np = r.I * (r.J > 1 ? r.J - 1 : 0);
-    const int nb = (r.I > 1 ? r.I - 1 : 0) * r.J;
     for (int m = tid; m < r.R; m += blockDim.x) {
         s_slot[m] = r.slot_state[m];
         s_state[m] = r.state_slot[m];
@@ -899,108 +896,8 @@ plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__
                 grid.sync();
             }
         }
-        // (f, g) of every replica, reference units: f = -(m - 2 u_c), g = 4 u_q
-        for (int m = tid; m < r.R; m += blockDim.x) {
-            s_f[m] = -((double)a.m_cost - 2.0 * (double)cc[m]);
-            s_g[m] = 4.0 * (double)cq[m];
-        }
-        __syncthreads();
-        // swap phase (engine.cpp:148-187), replayed identically by every block
-        const int64_t n_att = round_attempts(r.I, r.J, round);
-        for (int q = tid; q < n_att; q += blockDim.x) {
-            int sa, sb, ctr, is_p;
-            if (swap_attempt(r.I, r.J, r.betas, r.pens, round, q, s_f, s_g, s_slot, r.swap_seed,
-                             swap_base, sa, sb, ctr, is_p)) {
-                const int xa = s_slot[sa], xb = s_slot[sb];
-                s_slot[sa] = xb;
-                s_slot[sb] = xa;
-                s_state[xb] = sa;
-                s_state[xa] = sb;
-                if (blockIdx.x == 0) {
-                    if (is_p) r.acc_p[ctr] += 1; else r.acc_b[ctr] += 1;
-                }
-            }
-        }
-        swap_base += (uint64_t)n_att;
-        __syncthreads();
-        if (blockIdx.x == 0) {
-            // counters of the other parity are free again: zero them
-            int32_t* other = r.cnt + (size_t)(par ^ 1) * 2 * r.cnt_stride;
-            for (int m = tid; m < 2 * r.cnt_stride; m += blockDim.x) other[m] = 0;
-            if (r.work) {
-                int* ow = r.work + (size_t)(par ^ 1) * a.n_colors * passes;
-                for (int m = tid; m < a.n_colors * passes; m += blockDim.x) ow[m] = 0;
-            }
-            for (int m = tid; m < r.R; m += blockDim.x) {
-                r.slot_state[m] = s_slot[m];
-                r.state_slot[m] = s_state[m];
-                r.f_all[m] = s_f[m];
-                r.g_all[m] = s_g[m];
-            }
-            if (tid == 0) {  // record, engine.cpp:189-208
-                TgRecordDev* rec = reinterpret_cast<TgRecordDev*>(r.rec) + k;
-                const int tg = s_slot[r.R - 1];
-                rec->round = round;
-                rec->sweep_count = round * r.sps;
-                rec->f = s_f[tg];
-                rec->g = s_g[tg];
-                rec->feasible = s_g[tg] == 0.0 ? 1 : 0;
-                rec->target_state = tg;
-            }
-            if ((r.rec_flags & 8) && r.rec_acc) {
-                int64_t* dst = r.rec_acc + (size_t)k * (np + nb);
-                for (int q = tid; q < np; q += blockDim.x) dst[q] = r.acc_p[q];
-                for (int q = tid; q < nb; q += blockDim.x) dst[np + q] = r.acc_b[q];
-            }
-        }
-        // threshold planes for the new labels: warp job = (word, type, class)
-        {
-            int combos = 0;
-            for (int ty = 0; ty < a.n_types; ++ty) combos += a.ty[ty].ncl;
-            const int total = a.W * combos;
-            for (int job = gw; job < total; job += nw) {
-                const int w = job / combos;
-                int c = job % combos, ty = 0;
-                while (c >= a.ty[ty].ncl) { c -= a.ty[ty].ncl; ++ty; }
-                const PlaneType& pt = a.ty[ty];
-                const int m = w * 32 + lane;
-                uint64_t K = 0;
-                const bool live = m < a.local_states;
-                if (live) K = r.ktab[(size_t)s_state[m] * r.ktab_row + pt.ktab_off + c];
-                uint32_t* dst = r.kp + (size_t)w * a.kpw + pt.kp_off + c;
-                uint32_t* dstc = (c == 2 || c == 3)
-                    ? r.kpc + ((size_t)w * a.n_types + ty) * 128 + (c - 2) * 64 : nullptr;
-                for (int b = 0; b < kKPlanes; ++b) {
-                    const uint32_t word = __ballot_sync(0xffffffffu, live && ((K >> (52 - b)) & 1ull));
-                    if (lane == (b & 31)) {
-                        dst[b * pt.ncl] = word;
-                        if (dstc) dstc[b] = word;
-                    }
-                }
-                const uint32_t alw = __ballot_sync(0xffffffffu, live && K >= (1ull << 53));
-                if (lane == (kKPlanes & 31)) dst[kKPlanes * pt.ncl] = alw;
-            }
-        }
-        // target-state digest / snapshot for the trace (optional)
-        if (r.rec_flags & 3) {
-            const int tg = s_slot[r.R - 1];
-            uint64_t dsum = 0;
-            for (int i = blockIdx.x * blockDim.x + tid; i < a.n; i += gridDim.x * blockDim.x) {
-                const bool up = (a.spins[(size_t)i * a.W + (tg >> 5)] >> (tg & 31)) & 1u;
-                const int ci = r.perm[i];
-                if (r.rec_flags & 2) r.rec_states[(size_t)k * a.n + ci] = up ? 1 : -1;
-                if (up) dsum += digest_term((uint64_t)ci);
-            }
-            if (r.rec_flags & 1) {
-#pragma unroll
-                for (int o = 16; o; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
-                if (lane == 0 && dsum)
-                    atomicAdd(reinterpret_cast<unsigned long long*>(
-                                  &(reinterpret_cast<TgRecordDev*>(r.rec) + k)->digest),
-                              (unsigned long long)dsum);
-            }
-        }
-        grid.sync();
+        round_epilogue(a, r, RoundSmem{s_f, s_g, s_slot, s_state}, k, round, cc, cq, swap_base,
+                       a.n_colors * passes);
     }
 }
 
