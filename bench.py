@@ -433,7 +433,7 @@ def run_ours(args, rank, world, local):
     smem_peak_gbs = 148 * 128 * sm_max * 1e6 / 1e9  # SURVEY.md §8d official smem roofline
     achieved_gbs = bytes_per_launch / mean_sweep_s / 1e9
     clocks = clk.summary()
-    kname = dominant_kernel(args, world)
+    kname = info1.get("sweep_kernel") or dominant_kernel(args, world)  # the kernel the engine launched
     traffic = ncu_traffic(kname, args, pr, R, sweeps / max(n_sweep_launches, 1))
     eng.close()
 
@@ -522,7 +522,7 @@ def run_ours(args, rank, world, local):
 def dominant_kernel(args, world):
     if args.engine == "slot":
         return "slot2_sweep_kernel" if world == 1 else "slot_sweep_kernel"
-    return "plane_rounds_kernel" if world == 1 else "plane_sweep_kernel"
+    return "plane_tpw_rounds_kernel" if world == 1 else "plane_sweep_kernel"
 
 
 def ncu_traffic(kname, args, pr, R, sweeps_per_launch):

@@ -140,6 +140,7 @@ typedef struct {
     double last_swap_ms;   /* device time of the swap/record kernels of the last tg_advance */
     int64_t sweep_launches;
     int64_t other_launches;
+    char sweep_kernel[48]; /* name of the sweep kernel the last tg_advance launched ("" before) */
 } tg_info;
 int tg_get_info(tg_ctx* ctx, tg_info* info);
 /* cudaStream_t the context launches on (for external CUDA-event timing). */

@@ -54,7 +54,7 @@ class InfoC(C.Structure):
                 ("local_replicas", C.c_int32), ("words", C.c_int32), ("device_sms", C.c_int32),
                 ("rounds_done", C.c_int64), ("last_sweep_ms", C.c_double),
                 ("last_swap_ms", C.c_double), ("sweep_launches", C.c_int64),
-                ("other_launches", C.c_int64)]
+                ("other_launches", C.c_int64), ("sweep_kernel", C.c_char * 48)]
 
 
 BATCH_SINK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.POINTER(RecordC), C.c_int64,

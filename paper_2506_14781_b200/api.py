@@ -250,7 +250,9 @@ class Engine:
     def info(self) -> dict:
         i = _lib.InfoC()
         self._check(self._L.tg_get_info(self._h, C.byref(i)))
-        return {k: getattr(i, k) for k, _ in _lib.InfoC._fields_}
+        d = {k: getattr(i, k) for k, _ in _lib.InfoC._fields_}
+        d["sweep_kernel"] = d["sweep_kernel"].decode()
+        return d
 
     def stream_ptr(self) -> int:
         return int(self._L.tg_stream(self._h) or 0)

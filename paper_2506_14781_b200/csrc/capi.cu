@@ -300,6 +300,7 @@ int tg_get_info(tg_ctx* ctx, tg_info* info) {
     info->last_swap_ms = ctx->last_swap_ms;
     info->sweep_launches = ctx->sweep_launches;
     info->other_launches = ctx->other_launches;
+    std::snprintf(info->sweep_kernel, sizeof(info->sweep_kernel), "%s", ctx->sweep_kernel);
     return TG_OK;
 }
 

@@ -259,7 +259,8 @@ struct tg_ctx {
     std::vector<uint2> h_wkey;
     int plane_grid = 0, plane_block = kPlaneThreads;
     int fused_grid = 0, fused_fast = 0, fused_block = kPlaneThreads, fused_wv = 4;
-    int fused_tpw = 0, tpw_fast = 0;     // thread-per-(site, word) kernel (plane_tpw.cu) instead of plane_rounds_kernel
+    int fused_tpw = 0, tpw_fast = 0;
+    const char* sweep_kernel = "";   // dominant sweep kernel of the last advance (tg_info)     // thread-per-(site, word) kernel (plane_tpw.cu) instead of plane_rounds_kernel
     size_t fused_smem = 0;
     size_t slot_smem = 0;
 

@@ -222,7 +222,6 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
                                                      kPlaneThreads, 0));
     if (per_sm < 1) fail(TG_ERR_RESOURCE, "plane engine: kernel does not fit on an SM");
     int blocks = per_sm * c.sms;
-    const int wpb = kPlaneThreads / 32;
     const int passes = c.W / c.WV;
     blocks -= blocks % passes;  // each block owns one pass of WV words
     if (blocks < passes) fail(TG_ERR_RESOURCE, "plane engine: cannot tile %d words", c.W);
@@ -360,6 +359,7 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         r.perm = c.d_perm.p;
         void* args[] = {&a, &r};
         if (c.profiling) CK(cudaEventRecord(c.ev[0], st));
+        c.sweep_kernel = c.fused_tpw ? "plane_tpw_rounds_kernel" : "plane_rounds_kernel";
         CK(cudaLaunchCooperativeKernel(c.fused_tpw ? plane_tpw_fn(c.cfg.rule, c.tpw_fast)
                                                    : plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast),
                                        dim3(c.fused_grid), dim3(c.fused_block), args, c.fused_smem, st));

@@ -41,6 +41,7 @@ void launch_sweep(tg_ctx& c, int64_t t0) {
         int64_t t = t0;
         int nsw = sps;
         void* args[] = {&a, &t, &nsw};
+        c.sweep_kernel = "plane_sweep_kernel";
         CK(cudaLaunchCooperativeKernel(plane_sweep_fn(c.cfg.rule, c.WV), dim3(c.plane_grid),
                                        dim3(kPlaneThreads), args, 0, c.stream));
     } else {
@@ -48,6 +49,7 @@ void launch_sweep(tg_ctx& c, int64_t t0) {
         int64_t t = t0;
         int nsw = sps;
         void* args[] = {&a, &t, &nsw};
+        c.sweep_kernel = "slot_sweep_kernel";
         CK(cudaLaunchKernel(c.slot_D ? slot_sweep_fn_d(c.slot_D) : slot_sweep_fn(), dim3(c.R_local),
                             dim3(kSlotThreads), args, c.slot_smem, c.stream));
     }

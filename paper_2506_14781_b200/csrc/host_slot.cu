@@ -581,6 +581,7 @@ void s2_advance(tg_ctx& c, int64_t n_rounds, const BatchSinkCtx& sink) {
         int nsw = sps, de = S.sep_energy ? 0 : 1;
         void* args[] = {&a, &t0, &nsw, &de};
         if (c.profiling) CK(cudaEventRecord(c.ev[0], st));
+        c.sweep_kernel = "slot2_sweep_kernel";
         CK(cudaLaunchCooperativeKernel(slot2_sweep_fn(S.D), dim3(S.grid), dim3(kSlot2Threads), args, 0, st));
         if (c.profiling) CK(cudaEventRecord(c.ev[1], st));
         c.sweep_launches++;

@@ -59,6 +59,7 @@ __device__ __forceinline__ void vadd(uint32_t (&V)[kVB], const uint32_t* m) {
     }
 }
 
+static_assert(kTpwVB == 8, "vflush_v passes 8 counter planes");
 // Per-replica totals of the warp's vertical counters, added into
 // s_cnt[w * 32 + l]; V is cleared.  Lanes sharing a word (lane = p * W + w)
 // are summed by a butterfly; the sum's planes are then packed S per 32x32
@@ -114,7 +115,10 @@ __device__ __forceinline__ void vflush_w(uint32_t (&V)[kVB], int* s_cnt) {
     }
 }
 
-static __device__ __noinline__ void vflush(uint32_t (&V)[kVB], int logW, int* s_cnt) {
+// Counters passed by value (registers through the call, no local-memory
+// copy of the caller's array); the caller clears its counters.
+static __device__ __noinline__ void vflush_v(uint4 lo, uint4 hi, int logW, int* s_cnt) {
+    uint32_t V[kVB] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
     switch (logW) {
         case 0: vflush_w<0>(V, s_cnt); break;
         case 1: vflush_w<1>(V, s_cnt); break;
@@ -123,6 +127,83 @@ static __device__ __noinline__ void vflush(uint32_t (&V)[kVB], int logW, int* s_
         case 4: vflush_w<4>(V, s_cnt); break;
         default: vflush_w<5>(V, s_cnt); break;
     }
+}
+
+__device__ __forceinline__ void vflush(uint32_t (&V)[kVB], int logW, int* s_cnt) {
+    vflush_v(make_uint4(V[0], V[1], V[2], V[3]), make_uint4(V[4], V[5], V[6], V[7]), logW, s_cnt);
+#pragma unroll
+    for (int b = 0; b < kVB; ++b) V[b] = 0u;
+}
+
+// Philox4x32-10 for the plane counters {site, t_lo, t_hi, group << 4 | blk}
+// with t and the key fixed for a colour phase: the products of round 1 on
+// (t_hi) and of round 2 on the resulting constant are per-phase constants
+// (PhiloxT), and the two unconditional blocks of a site share round 1's
+// product on `site` and round 3's on the site-only word.  Output identical
+// to philox4x32_10_ks (tests compare every plane draw with the oracle).
+struct PhiloxT {
+    uint32_t c0, c1x;  // round-1 words 0, 1 (c1x = word 1 ^ round-2 key 0)
+    uint32_t h0x, l0;  // round-2 hi(M0 * c0) ^ round-2 key 1, lo(M0 * c0)
+};
+
+__device__ __forceinline__ PhiloxT philox_t(uint32_t tlo, uint32_t thi, const uint32_t* ks) {
+    PhiloxT P;
+    const uint32_t hi1 = __umulhi(kPhiloxM1, thi), lo1 = kPhiloxM1 * thi;
+    P.c0 = hi1 ^ tlo ^ ks[0];
+    P.c1x = lo1 ^ ks[2];
+    P.h0x = __umulhi(kPhiloxM0, P.c0) ^ ks[3];
+    P.l0 = kPhiloxM0 * P.c0;
+    return P;
+}
+
+// Rounds 3..10 from the round-2 output.
+__device__ __forceinline__ u32x4 philox_rounds_3_10(u32x4 c, const uint32_t* ks) {
+#pragma unroll
+    for (int r = 2; r < 10; ++r) {
+        uint32_t hi0, lo0, hi1, lo1;
+        mulhilo(kPhiloxM0, c.x, hi0, lo0);
+        mulhilo(kPhiloxM1, c.z, hi1, lo1);
+        c = u32x4{hi1 ^ c.y ^ ks[2 * r], lo1, hi0 ^ c.w ^ ks[2 * r + 1], lo0};
+    }
+    return c;
+}
+
+// One block: counter word 3 = g.
+__device__ __forceinline__ u32x4 philox_plane(uint32_t site, uint32_t g, const PhiloxT& P,
+                                              const uint32_t* ks) {
+    const uint32_t hs = __umulhi(kPhiloxM0, site), ls = kPhiloxM0 * site;
+    const uint32_t y2 = hs ^ g ^ ks[1];                  // round 1 (words 0, 1 are P.c0, lo1)
+    const uint32_t hq = __umulhi(kPhiloxM1, y2), lq = kPhiloxM1 * y2;
+    return philox_rounds_3_10(u32x4{hq ^ P.c1x, lq, P.h0x ^ ls, P.l0}, ks);  // round 2
+}
+
+// The two blocks g0, g0 | 1 of one site.
+__device__ __forceinline__ void philox_plane2(uint32_t site, uint32_t g0, const PhiloxT& P,
+                                              const uint32_t* ks, u32x4& r0, u32x4& r1) {
+    const uint32_t hs = __umulhi(kPhiloxM0, site), ls = kPhiloxM0 * site;
+    const uint32_t z2 = P.h0x ^ ls;                      // round-2 word 2, shared
+    const uint32_t ya = hs ^ g0 ^ ks[1], yb = hs ^ (g0 | 1u) ^ ks[1];
+    const uint32_t hqa = __umulhi(kPhiloxM1, ya), lqa = kPhiloxM1 * ya;
+    const uint32_t hqb = __umulhi(kPhiloxM1, yb), lqb = kPhiloxM1 * yb;
+    // round 3: M1 * z2 shared
+    const uint32_t h3 = __umulhi(kPhiloxM1, z2), l3 = kPhiloxM1 * z2;
+    const uint32_t xa = hqa ^ P.c1x, xb = hqb ^ P.c1x;
+    const uint32_t h0a = __umulhi(kPhiloxM0, xa), l0a = kPhiloxM0 * xa;
+    const uint32_t h0b = __umulhi(kPhiloxM0, xb), l0b = kPhiloxM0 * xb;
+    u32x4 a{h3 ^ lqa ^ ks[4], l3, h0a ^ P.l0 ^ ks[5], l0a};
+    u32x4 b{h3 ^ lqb ^ ks[4], l3, h0b ^ P.l0 ^ ks[5], l0b};
+#pragma unroll
+    for (int r = 3; r < 10; ++r) {
+        uint32_t p0, q0, p1, q1, s0, t0, s1, t1;
+        mulhilo(kPhiloxM0, a.x, p0, q0);
+        mulhilo(kPhiloxM1, a.z, p1, q1);
+        mulhilo(kPhiloxM0, b.x, s0, t0);
+        mulhilo(kPhiloxM1, b.z, s1, t1);
+        a = u32x4{p1 ^ a.y ^ ks[2 * r], q1, p0 ^ a.w ^ ks[2 * r + 1], q0};
+        b = u32x4{s1 ^ b.y ^ ks[2 * r], t1, s0 ^ b.w ^ ks[2 * r + 1], t0};
+    }
+    r0 = a;
+    r1 = b;
 }
 
 // Deferred tail of the lazy comparison (Metropolis, cost degree 3, no chain:
@@ -168,10 +249,11 @@ static __device__ __noinline__ void tpw_drain(const PlaneArgs& a, int base, int 
     const uint32_t grp4 = (uint32_t)(a.w_global0 + w) << 4;
     const uint4* kc2 = reinterpret_cast<const uint4*>(a.kpc + ((size_t)w * a.n_types + type) * 128);
     uint32_t lt = 0u;
+    const PhiloxT P = philox_t(tlo, thi, a.pks);
 #pragma unroll 1
     for (int blk = 2; blk < 14; ++blk) {
         if (!__any_sync(0xffffffffu, und)) break;
-        const u32x4 r = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | (uint32_t)blk}, a.pks);
+        const u32x4 r = philox_plane((uint32_t)site, grp4 | (uint32_t)blk, P, a.pks);
         compare4_sel(c0, __ldg(kc2 + blk), __ldg(kc2 + 16 + blk), r, und, lt);
     }
     if (lt) {
@@ -346,35 +428,42 @@ struct C5K {
     uint32_t kc2;          // word offset of word w's class-2/3 planes in kpc (w * n_types * 128)
     uint32_t kpw;          // word offset of word w's block in kp (w * kpw)
     uint32_t act_w, grp4, tlo, thi;
+    PhiloxT P;
     int w, logW, lower;
 };
 
-// An item's rows, gathered one item ahead: own word, the three cost
-// neighbours' words (J sign not yet applied), the chain partner's word,
-// bits = J<0 signs | lowx << 3 | lowy << 6.
-struct C5Row {
-    uint32_t s, x0, x1, x2, y0, bits;
+// An item's row words (own, cost neighbours, chain partner), gathered at the
+// top of the item loop before the next item's prefetches are issued.
+struct C5Rows {
+    uint32_t s, x0, x1, x2, y0;
 };
 
 template <int DQ, bool ALLLOW>
 __device__ __forceinline__ void c5_site(const PlaneArgs& a, const C5K& K, const Chunk& ch,
                                         const PlaneType& ty, int pos, bool count,
-                                        uint32_t (&Vc)[kVB], int& qn, const C5Row& R) {
+                                        uint32_t (&Vc)[kVB], int& qn, int32_t e0, int32_t e1,
+                                        int32_t e2, int32_t e3, const C5Rows& R) {
     const bool valid = pos < ch.len;
     const uint32_t site = (uint32_t)(ch.start + pos);
-    const u32x4 r0 = philox4x32_10_ks(u32x4{site, K.tlo, K.thi, K.grp4 | 0u}, a.pks);
-    const u32x4 r1 = philox4x32_10_ks(u32x4{site, K.tlo, K.thi, K.grp4 | 1u}, a.pks);
-    const uint32_t s = R.s, y0 = R.y0;
-    const uint32_t x0 = R.x0 ^ (0u - (R.bits & 1u));  // bit: J_ij s_j = +1
-    const uint32_t x1 = R.x1 ^ (0u - ((R.bits >> 1) & 1u));
-    const uint32_t x2 = R.x2 ^ (0u - ((R.bits >> 2) & 1u));
-    const uint32_t lowx = (R.bits >> 3) & 7u, lowy = (R.bits >> 6) & 1u;
+    const uint32_t j0 = (uint32_t)e0 & 0x7fffffffu, j1 = (uint32_t)e1 & 0x7fffffffu,
+                   j2 = (uint32_t)e2 & 0x7fffffffu, jq = (uint32_t)e3;
+    uint32_t s = R.s, x0 = R.x0, x1 = R.x1, x2 = R.x2, y0 = R.y0;
+    u32x4 r0, r1;
+    philox_plane2(site, K.grp4, K.P, a.pks, r0, r1);
+    x0 ^= (uint32_t)(e0 >> 31);  // bit: J_ij s_j = +1
+    x1 ^= (uint32_t)(e1 >> 31);
+    x2 ^= (uint32_t)(e2 >> 31);
+    uint32_t lowx = 7u, lowy = 1u;
+    if (!ALLLOW) {
+        lowx = (uint32_t)((int)j0 < K.lower) | ((uint32_t)((int)j1 < K.lower) << 1) |
+               ((uint32_t)((int)j2 < K.lower) << 2);
+        lowy = (uint32_t)((int)jq < K.lower);
+    }
     const uint32_t a0 = ~(s ^ x0), a1 = ~(s ^ x1), a2 = ~(s ^ x2);  // satisfied bonds
     const uint32_t c0 = a0 ^ a1 ^ a2;
     const uint32_t c1 = (a0 & a1) | (a2 & (a0 ^ a1));
     const uint32_t act = valid ? K.act_w : 0u;
     uint32_t always, und, lt = 0u;
-    const uint4* kc2 = reinterpret_cast<const uint4*>(a.kpc + K.kc2) + ch.type * 32;
     const uint32_t* kpb = a.kp + K.kpw + ty.kp_off;
     uint32_t cb[3] = {c0, c1, DQ ? ~(s ^ y0) : 0u};
     if (DQ == 0) {
@@ -400,7 +489,7 @@ __device__ __forceinline__ void c5_site(const PlaneArgs& a, const C5K& K, const 
 #pragma unroll 1
         for (int blk = 2; blk < 14; ++blk) {
             if (!__any_sync(0xffffffffu, und)) break;
-            const u32x4 r = philox4x32_10_ks(u32x4{site, K.tlo, K.thi, K.grp4 | (uint32_t)blk}, a.pks);
+            const u32x4 r = philox_plane(site, K.grp4 | (uint32_t)blk, K.P, a.pks);
             compare_block<3>(cb, kpb, 8, blk, r, und, lt);
         }
     }
@@ -480,10 +569,14 @@ __device__ __forceinline__ void tpw_phase_c5(const PlaneArgs& a, int c, uint64_t
     K.grp4 = (uint32_t)(a.w_global0 + w) << 4;
     K.tlo = (uint32_t)t;
     K.thi = (uint32_t)(t >> 32);
+    K.P = philox_t(K.tlo, K.thi, a.pks);
     K.w = w;
     K.logW = logW;
     K.lower = lower;
     int since = 0, qn = 0;
+    // items strided over the warps (the chain-site items, costlier, sit
+    // together in the canonical order: a contiguous split unbalances the
+    // grid barrier); chunk descriptors two items ahead, entries one
     auto chunk_of = [&](int it) {
         Chunk ch{0, 0, 0, 0};
         if (it < n_items) ch = a.chunks[c0 + (it >> logW)];
@@ -501,46 +594,33 @@ __device__ __forceinline__ void tpw_phase_c5(const PlaneArgs& a, int c, uint64_t
             if (deg == 4) e[3] = __ldg(nb + 3);
         }
     };
-    const uint32_t* sp = a.spins + w;
-    auto rows = [&](int it, const Chunk& ch, const int32_t (&e)[4], C5Row& R) {
-        const int pos = (it & (W - 1)) * S + sl;
-        R = C5Row{0u, 0u, 0u, 0u, 0u, 0u};
-        if (it < n_items && pos < ch.len) {
-            const uint32_t site = (uint32_t)(ch.start + pos);
-            const uint32_t j0 = (uint32_t)e[0] & 0x7fffffffu, j1 = (uint32_t)e[1] & 0x7fffffffu,
-                           j2 = (uint32_t)e[2] & 0x7fffffffu, jq = (uint32_t)e[3];
-            R.s = sp[site << logW];
-            R.x0 = sp[j0 << logW];
-            R.x1 = sp[j1 << logW];
-            R.x2 = sp[j2 << logW];
-            const bool dq = a.ty[ch.type].dq != 0;
-            if (dq) R.y0 = sp[jq << logW];
-            R.bits = ((uint32_t)e[0] >> 31) | (((uint32_t)e[1] >> 31) << 1) | (((uint32_t)e[2] >> 31) << 2) |
-                     ((uint32_t)((int)j0 < lower) << 3) | ((uint32_t)((int)j1 < lower) << 4) |
-                     ((uint32_t)((int)j2 < lower) << 5) | ((uint32_t)(dq && (int)jq < lower) << 6);
-        }
-    };
-    // pipeline: chunk descriptors two items ahead, neighbour entries one
     int item = gw;
-    Chunk ch0 = chunk_of(item), ch1 = chunk_of(item + nw);
-    int32_t e0[4];
-    entries(item, ch0, e0);
-    while (item < n_items) {
-        const Chunk ch = ch0;
-        C5Row R;
-        rows(item, ch, e0, R);  // gathers in flight during the next prefetches and the Philox blocks
+    Chunk ch_c = chunk_of(item), ch_n = chunk_of(item + nw);
+    int32_t en[4];
+    entries(item, ch_c, en);
+    for (; item < n_items; item += nw) {
+        const Chunk ch = ch_c;
+        const int32_t e0 = en[0], e1 = en[1], e2 = en[2], e3 = en[3];
         const int p0 = (item & (W - 1)) * S;
-        item += nw;
-        ch0 = ch1;
-        ch1 = chunk_of(item + nw);
-        entries(item, ch0, e0);
+        C5Rows R{0u, 0u, 0u, 0u, 0u};
+        if (p0 + sl < ch.len) {  // gathers first: in flight during the prefetches and the Philox blocks
+            const uint32_t* sp = a.spins + w;
+            R.s = sp[(uint32_t)(ch.start + p0 + sl) << logW];
+            R.x0 = sp[((uint32_t)e0 & 0x7fffffffu) << logW];
+            R.x1 = sp[((uint32_t)e1 & 0x7fffffffu) << logW];
+            R.x2 = sp[((uint32_t)e2 & 0x7fffffffu) << logW];
+            if (a.ty[ch.type].dq) R.y0 = sp[(uint32_t)e3 << logW];
+        }
+        ch_c = ch_n;
+        ch_n = chunk_of(item + 2 * nw);
+        entries(item + nw, ch_c, en);
         if (p0 >= ch.len) continue;
         const PlaneType& ty = a.ty[ch.type];
         if (ty.nqb == 0) {
-            if (alllow) c5_site<0, true>(a, K, ch, ty, p0 + sl, count, Vc, qn, R);
-            else c5_site<0, false>(a, K, ch, ty, p0 + sl, count, Vc, qn, R);
+            if (alllow) c5_site<0, true>(a, K, ch, ty, p0 + sl, count, Vc, qn, e0, e1, e2, e3, R);
+            else c5_site<0, false>(a, K, ch, ty, p0 + sl, count, Vc, qn, e0, e1, e2, e3, R);
         } else {
-            c5_site<1, false>(a, K, ch, ty, p0 + sl, count, Vc, qn, R);
+            c5_site<1, false>(a, K, ch, ty, p0 + sl, count, Vc, qn, e0, e1, e2, e3, R);
         }
         if (qn >= 32) {
             qn -= 32;
@@ -594,17 +674,6 @@ __device__ __forceinline__ void tpw_phase(const PlaneArgs& a, int c, uint64_t t,
     const int n_items = (a.chunk_off[c + 1] - c0) << logW;
     const int lower = a.color_start[c];
     count = count && lower > 0;  // colour 0 has no lower-colour neighbours
-    const bool alllow = a.n_colors == 2 && c == 1;  // proper 2-colouring: every neighbour is colour 0
-    C5K K;
-    K.kc2 = (uint32_t)(w * a.n_types * 128);
-    K.kpw = (uint32_t)(w * a.kpw);
-    K.act_w = act_w;
-    K.grp4 = grp4;
-    K.tlo = tlo;
-    K.thi = thi;
-    K.w = w;
-    K.logW = logW;
-    K.lower = lower;
     int since = 0, qn = 0;
     int item = gw;
     Chunk nxt{};
