@@ -122,6 +122,7 @@ struct RoundArgs {
     int32_t* cnt;          // [2 parities][2 (cost, chain)][cnt_stride]
     int* work;             // [2 parities][n_colors][passes] chunk counters (dynamic distribution)
     int cnt_stride;
+    int flush_every;       // tpw kernel: items between vertical-counter flushes (0: the overflow bound)
     const uint64_t* ktab;
     int ktab_row;
     uint32_t* kp;

@@ -141,6 +141,7 @@ void ensure_host_arrays(tg_ctx& c);
 uint64_t threshold_metropolis(double beta, double de) {
     if (de <= 0.0) return 1ull << 53;
     const double T = std::exp(-beta * de);
+    if (!(T < 1.0)) return 1ull << 53;  // beta <= 0: accepted for every uniform (no overflowing cast)
     return (uint64_t)std::ceil(T * 0x1.0p53);
 }
 uint64_t threshold_heat_bath(double beta, double local) {

@@ -351,6 +351,8 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         r.acc_p = c.d_acc_p.p; r.acc_b = c.d_acc_b.p;
         r.f_all = c.d_f.p; r.g_all = c.d_g.p;
         r.cnt = c.d_cnt2.p; r.cnt_stride = c.W * 32;
+        // testing knob: flush the tpw kernel's vertical counters more often
+        if (const char* e = std::getenv("TG_TPW_FLUSH_EVERY")) r.flush_every = std::atoi(e);
         // dynamic chunk grabbing measured 3% slower than the static split (r1); opt in
         r.work = (std::getenv("TG_PLANE_DYNAMIC") ? c.d_work.p : nullptr);
         r.ktab = c.d_ktab.p; r.ktab_row = c.ktab_row; r.kp = c.d_kp.p; r.kpc = c.d_kpc.p;

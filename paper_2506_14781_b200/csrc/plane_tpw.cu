@@ -751,7 +751,8 @@ plane_tpw_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_consta
     const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int nw = gridDim.x * (blockDim.x >> 5);
     // max bonds added per item: 2^ncb - 1 <= 7; 8-bit counters
-    const int flush_every = FAST ? 255 / 3 : 255 / 7;
+    int flush_every = FAST ? 255 / 3 : 255 / 7;
+    if (r.flush_every > 0 && r.flush_every < flush_every) flush_every = r.flush_every;
     for (int m = threadIdx.x; m < 2 * nrep; m += blockDim.x) s_cc[m] = 0;
 #pragma unroll
     for (int b = 0; b < kVB; ++b) vq[b * kTpwThreads] = 0u;
