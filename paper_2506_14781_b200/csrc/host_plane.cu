@@ -245,6 +245,21 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
     for (const auto& t : types)
         if (!(t.dc == 3 && (t.dq == 1 || (t.dq == 0 && (t.pad & 1))))) c.tpw_fast = 0;
     if (const char* e = std::getenv("TG_PLANE_FAST")) c.tpw_fast = c.tpw_fast && std::atoi(e) != 0;
+    // sweep-only tpw kernel (multi-GPU rounds, full-grid records)
+    c.tpw_sweep_grid = 0;
+    if ((c.W & (c.W - 1)) == 0 && c.W <= 32) {
+        bool on = true;
+        if (const char* e = std::getenv("TG_PLANE_TPW")) on = std::atoi(e) != 0;
+        const void* fn = plane_tpw_sweep_fn(c.cfg.rule, c.tpw_fast);
+        cudaFuncAttributes fa{};
+        CK(cudaFuncGetAttributes(&fa, fn));
+        c.tpw_sweep_smem = tpw_smem_bytes(0, c.W, fa.maxThreadsPerBlock);
+        if (c.tpw_sweep_smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.tpw_sweep_smem));
+        int fb = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fb, fn, fa.maxThreadsPerBlock, c.tpw_sweep_smem));
+        if (on && fb >= 1) c.tpw_sweep_grid = fb * c.sms;
+    }
     if (c.fused_tpw) {
         const void* fn = plane_tpw_fn(c.cfg.rule, c.tpw_fast);
         cudaFuncAttributes fa{};

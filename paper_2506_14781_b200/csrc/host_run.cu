@@ -41,9 +41,15 @@ void launch_sweep(tg_ctx& c, int64_t t0) {
         int64_t t = t0;
         int nsw = sps;
         void* args[] = {&a, &t, &nsw};
-        c.sweep_kernel = "plane_sweep_kernel";
-        CK(cudaLaunchCooperativeKernel(plane_sweep_fn(c.cfg.rule, c.WV), dim3(c.plane_grid),
-                                       dim3(kPlaneThreads), args, 0, c.stream));
+        if (c.tpw_sweep_grid > 0) {
+            c.sweep_kernel = "plane_tpw_sweep_kernel";
+            CK(cudaLaunchCooperativeKernel(plane_tpw_sweep_fn(c.cfg.rule, c.tpw_fast), dim3(c.tpw_sweep_grid),
+                                           dim3(kTpwThreads), args, c.tpw_sweep_smem, c.stream));
+        } else {
+            c.sweep_kernel = "plane_sweep_kernel";
+            CK(cudaLaunchCooperativeKernel(plane_sweep_fn(c.cfg.rule, c.WV), dim3(c.plane_grid),
+                                           dim3(kPlaneThreads), args, 0, c.stream));
+        }
     } else {
         SlotArgs a = slot_args(c);
         int64_t t = t0;

@@ -27,6 +27,11 @@ void* plane_rounds_fn_r1(int wv, int fast);
 void* plane_tpw_fn_r0(int fast);
 void* plane_tpw_fn_r1(int fast);
 void* plane_tpw_fn(int rule, int fast) { return rule == 0 ? plane_tpw_fn_r0(fast) : plane_tpw_fn_r1(fast); }
+void* plane_tpw_sweep_fn_r0(int fast);
+void* plane_tpw_sweep_fn_r1(int fast);
+void* plane_tpw_sweep_fn(int rule, int fast) {
+    return rule == 0 ? plane_tpw_sweep_fn_r0(fast) : plane_tpw_sweep_fn_r1(fast);
+}
 void* plane_rounds_fn(int rule, int wv, int fast) {
     return rule == 0 ? plane_rounds_fn_r0(wv, fast) : plane_rounds_fn_r1(wv, fast);
 }
@@ -385,7 +390,7 @@ __global__ void extract_kernel(ExtractArgs e) {
         }
         const int ci = e.perm[i];  // caller index
         if (e.states) e.states[(size_t)(e.all_slots ? sl : 0) * e.n + ci] = v;
-        if (!e.all_slots && v > 0) dsum += digest_term((uint64_t)ci);
+        if (sl == e.R - 1 && v > 0) dsum += digest_term((uint64_t)ci);  // the target slot's digest
     }
     if (e.digest) {
 #pragma unroll

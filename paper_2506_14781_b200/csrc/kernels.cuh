@@ -59,6 +59,7 @@ struct ExtractArgs {
 void* plane_sweep_fn(int rule, int wv);
 void* plane_rounds_fn(int rule, int wv, int fast);
 void* plane_tpw_fn(int rule, int fast);
+void* plane_tpw_sweep_fn(int rule, int fast);
 int plane_words_per_pass(int W);
 void* slot_sweep_fn();
 void* slot_sweep_fn_d(int D);  // padded-degree variant, D in {4, 8}

@@ -788,6 +788,63 @@ plane_tpw_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_consta
     }
 }
 
+// Sweep-only variant (multi-GPU, full-grid records): n_sweeps sweeps, then
+// every replica's (f, g) in reference units from the bond counts (which it
+// zeroes); the (f, g) exchange and the swap phase run after it.
+template <int RULE, int FAST>
+__global__ void __launch_bounds__(kTpwThreads, kTpwMinBlocks)
+plane_tpw_sweep_kernel(const __grid_constant__ PlaneArgs a, int64_t t0, int n_sweeps) {
+    cg::grid_group grid = cg::this_grid();
+    const int nrep = a.W * 32;
+    int* s_cc = tpw_sm + kTpwSmCnt;
+    int* s_cq = s_cc + nrep;
+    uint32_t* vq = reinterpret_cast<uint32_t*>(tpw_sm + kTpwSmVq) + threadIdx.x;
+    const int logW = __ffs(a.W) - 1;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int nw = gridDim.x * (blockDim.x >> 5);
+    const int flush_every = FAST ? 255 / 3 : 255 / 7;
+    for (int m = threadIdx.x; m < 2 * nrep; m += blockDim.x) s_cc[m] = 0;
+#pragma unroll
+    for (int b = 0; b < kVB; ++b) vq[b * kTpwThreads] = 0u;
+    __syncthreads();
+    uint32_t Vc[kVB];
+#pragma unroll
+    for (int b = 0; b < kVB; ++b) Vc[b] = 0u;
+    for (int sw = 0; sw < n_sweeps; ++sw) {
+        const uint64_t t = (uint64_t)(t0 + sw);
+        const bool count = (sw == n_sweeps - 1);
+        for (int c = 0; c < a.n_colors; ++c) {
+            if constexpr (FAST) tpw_phase_c5<RULE>(a, c, t, count, gw, nw, logW, Vc, flush_every);
+            else tpw_phase<RULE, FAST>(a, c, t, count, gw, nw, logW, Vc, flush_every);
+            if (count && a.color_start[c] > 0) {
+                __syncthreads();
+                for (int m = threadIdx.x; m < nrep; m += blockDim.x) {
+                    const int vc = s_cc[m], vqv = s_cq[m];
+                    if (vc) { atomicAdd(a.cnt_c + m, vc); s_cc[m] = 0; }
+                    if (vqv) { atomicAdd(a.cnt_q + m, vqv); s_cq[m] = 0; }
+                }
+            }
+            grid.sync();
+        }
+    }
+    // f = -(m - 2 u_c) for J = +-1, h = 0; g = sum (s_a - s_b)^2 = 4 u_q
+    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < a.local_states; m += gridDim.x * blockDim.x) {
+        const int uc = a.cnt_c[m], uq = a.cnt_q[m];
+        a.f_loc[m] = -((double)a.m_cost - 2.0 * (double)uc);
+        a.g_loc[m] = 4.0 * (double)uq;
+        a.cnt_c[m] = 0;
+        a.cnt_q[m] = 0;
+    }
+}
+
+template __global__ void plane_tpw_sweep_kernel<TG_PLANE_RULE, 0>(const __grid_constant__ PlaneArgs, int64_t, int);
+template __global__ void plane_tpw_sweep_kernel<TG_PLANE_RULE, 1>(const __grid_constant__ PlaneArgs, int64_t, int);
+
+void* TG_CAT(plane_tpw_sweep_fn_r, TG_PLANE_RULE)(int fast) {
+    return fast ? (void*)plane_tpw_sweep_kernel<TG_PLANE_RULE, 1>
+                : (void*)plane_tpw_sweep_kernel<TG_PLANE_RULE, 0>;
+}
+
 template __global__ void plane_tpw_rounds_kernel<TG_PLANE_RULE, 0>(const __grid_constant__ PlaneArgs,
                                                                    const __grid_constant__ RoundArgs);
 template __global__ void plane_tpw_rounds_kernel<TG_PLANE_RULE, 1>(const __grid_constant__ PlaneArgs,

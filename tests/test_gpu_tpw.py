@@ -100,3 +100,45 @@ def test_vertical_counter_flush_mid_phase(monkeypatch, every):
     b, p = sched(16, 16)
     run_and_kernel(pr, b, p, 6, "metropolis", seed=2)
     run_and_kernel(K10, *sched(8, 8, 0.1, 3.0), 20, "heat_bath")
+
+
+def run_grid_records(pr, b, p, rounds, rule, seed):
+    """Full-grid records force the unfused round loop (sweep kernel, swap
+    kernel, extract): the multi-GPU path's kernels on one GPU."""
+    import pyoracle as O
+    from paper_2506_14781_b200.api import Engine, RunConfig
+    o = O.run(pr, b, p, rounds, 1, seed=seed, rule=rule, rng="plane")
+    eng = Engine(0)
+    eng.set_problem(pr)
+    eng.set_schedule(b, p)
+    recs = []
+
+    def sink(r, n, states, ap, ab):
+        for k in range(n):
+            recs.append((r[k].f, r[k].g, r[k].digest))
+        return 0
+
+    eng.run(RunConfig(total_sweeps=rounds, sweeps_per_swap=1, seed=seed, rule=rule, engine="plane",
+                      store_states=False, store_target_only=False), sink)
+    grid = eng.grid()
+    kern = eng.info()["sweep_kernel"]
+    eng.close()
+    np.testing.assert_array_equal(np.array([x[0] for x in recs]), o.f)
+    np.testing.assert_array_equal(np.array([x[1] for x in recs]), o.g)
+    np.testing.assert_array_equal(np.array([x[2] for x in recs], dtype=np.uint64), o.digest)
+    np.testing.assert_array_equal(grid, o.final_grid)
+    return kern
+
+
+@pytest.mark.parametrize("rule", ["metropolis", "heat_bath"])
+def test_unfused_round_loop_uses_the_tpw_sweep_kernel(rule):
+    b, p = sched(16, 16)
+    assert run_grid_records(C5S, b, p, 10, rule, 4) == "plane_tpw_sweep_kernel"
+    b, p = sched(8, 8, 0.1, 3.0)
+    assert run_grid_records(K10, b, p, 20, rule, 6) == "plane_tpw_sweep_kernel"
+
+
+def test_unfused_round_loop_thread_per_site_kernel(monkeypatch):
+    monkeypatch.setenv("TG_PLANE_TPW", "0")
+    b, p = sched(16, 16)
+    assert run_grid_records(C5S, b, p, 10, "metropolis", 4) == "plane_sweep_kernel"
