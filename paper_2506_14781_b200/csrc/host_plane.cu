@@ -234,22 +234,25 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
     if (const char* e = std::getenv("TG_PLANE_FAST")) c.fused_fast = c.fused_fast && std::atoi(e) != 0;
     c.fused_grid = 0;
     c.fused_tpw = 0;
-    // thread-per-(site, word) kernel: rows of a power-of-two number of words
-    if (c.world == 1 && c.R <= 2048 && (c.W & (c.W - 1)) == 0 && c.W <= 32) {
-        c.fused_tpw = 1;
-        if (const char* e = std::getenv("TG_PLANE_TPW")) c.fused_tpw = std::atoi(e) != 0;
-    }
     // tpw FAST variant (c5_site): Metropolis, every site of cost degree 3
     // and chain degree 0 / 1, chain-free types with flag bit 0
     c.tpw_fast = c.cfg.rule == TG_RULE_METROPOLIS;
     for (const auto& t : types)
         if (!(t.dc == 3 && (t.dq == 1 || (t.dq == 0 && (t.pad & 1))))) c.tpw_fast = 0;
     if (const char* e = std::getenv("TG_PLANE_FAST")) c.tpw_fast = c.tpw_fast && std::atoi(e) != 0;
+    // thread-per-(site, word) kernels (rows of a power-of-two number of
+    // words): by default only on their config-5 path, where they are faster
+    // (r1: 1.60e12 vs 1.39e12 flips/s); on generic site types and heat bath
+    // the thread-per-site kernels measured faster (1.34e12 vs 1.08e12).
+    // TG_PLANE_TPW = 0 never, 2 always (generic path included), else auto.
+    int tpw_mode = 1;
+    if (const char* e = std::getenv("TG_PLANE_TPW")) tpw_mode = std::atoi(e);
+    const bool tpw_ok = (c.W & (c.W - 1)) == 0 && c.W <= 32 &&
+                        (tpw_mode == 2 || (tpw_mode == 1 && c.tpw_fast));
+    if (c.world == 1 && c.R <= 2048 && tpw_ok) c.fused_tpw = 1;
     // sweep-only tpw kernel (multi-GPU rounds, full-grid records)
     c.tpw_sweep_grid = 0;
-    if ((c.W & (c.W - 1)) == 0 && c.W <= 32) {
-        bool on = true;
-        if (const char* e = std::getenv("TG_PLANE_TPW")) on = std::atoi(e) != 0;
+    if (tpw_ok) {
         const void* fn = plane_tpw_sweep_fn(c.cfg.rule, c.tpw_fast);
         cudaFuncAttributes fa{};
         CK(cudaFuncGetAttributes(&fa, fn));
@@ -258,7 +261,7 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.tpw_sweep_smem));
         int fb = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fb, fn, fa.maxThreadsPerBlock, c.tpw_sweep_smem));
-        if (on && fb >= 1) c.tpw_sweep_grid = fb * c.sms;
+        if (fb >= 1) c.tpw_sweep_grid = fb * c.sms;
     }
     if (c.fused_tpw) {
         const void* fn = plane_tpw_fn(c.cfg.rule, c.tpw_fast);

@@ -2,9 +2,9 @@
 
 The single-GPU fused round loop has three device paths with one contract
 (plane_tpw.cu, plane_sweep.cu): the thread-per-(site, word) kernel's config-5
-path (Metropolis, cost degree 3, chain degree 0/1), its generic path (any
-site type, both rules) and the older thread-per-site kernel (rows whose word
-count is not a power of two, or TG_PLANE_TPW=0).  Every case is compared bit
+path (Metropolis, cost degree 3, chain degree 0/1; the default where it
+applies), its generic path (any site type, both rules; TG_PLANE_TPW=2) and
+the thread-per-site kernel (everything else by default, TG_PLANE_TPW=0).  Every case is compared bit
 for bit with the oracle (f, g, feasibility, digests, final grid, counters)
 and the test checks which kernel the engine reports it launched.
 """
@@ -53,22 +53,35 @@ def test_tpw_config5_path_word_counts(grid):
 
 
 @pytest.mark.parametrize("grid", [(4, 8), (16, 16), (32, 32)])
-def test_tpw_generic_path_heat_bath(grid):
+def test_tpw_generic_path_heat_bath(monkeypatch, grid):
+    monkeypatch.setenv("TG_PLANE_TPW", "2")
     b, p = sched(*grid)
     run_and_kernel(C5S, b, p, 12, "heat_bath")
+    assert kernel_of(C5S, b, p, "heat_bath") == "plane_tpw_rounds_kernel"
 
 
 @pytest.mark.parametrize("rule", ["metropolis", "heat_bath"])
-def test_tpw_generic_path_non_bipartite(rule):
+def test_tpw_generic_path_non_bipartite(monkeypatch, rule):
+    monkeypatch.setenv("TG_PLANE_TPW", "2")
     b, p = sched(8, 8, 0.1, 3.0)
     run_and_kernel(K10, b, p, 40, rule)
 
 
-def test_tpw_negative_betas_disable_the_class_shortcut():
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_tpw_negative_betas_disable_the_class_shortcut(monkeypatch, mode):
     # beta < 0 makes classes 2 and 3 "always" for some labels: the config-5
     # path's single-select compare must not be taken (flag bit 0 off)
+    monkeypatch.setenv("TG_PLANE_TPW", mode)
     b, p = sched(16, 16, -1.0, 2.0)
     run_and_kernel(C5S, b, p, 12, "metropolis")
+
+
+@pytest.mark.parametrize("rule", ["metropolis", "heat_bath"])
+def test_default_dispatch_outside_the_config5_path(rule):
+    b, p = sched(8, 8, 0.1, 3.0)
+    assert kernel_of(K10, b, p, rule) == "plane_rounds_kernel"
+    b, p = sched(16, 16)
+    assert kernel_of(C5S, b, p, "heat_bath") == "plane_rounds_kernel"
 
 
 def test_non_power_of_two_rows_use_the_thread_per_site_kernel():
@@ -96,6 +109,7 @@ def test_large_instance_many_items_per_warp():
 def test_vertical_counter_flush_mid_phase(monkeypatch, every):
     # flushing after every item / every second item must give the same energies
     monkeypatch.setenv("TG_TPW_FLUSH_EVERY", str(every))
+    monkeypatch.setenv("TG_PLANE_TPW", "2")
     pr = I.bipartite_3regular(1 << 14, seed=9)
     b, p = sched(16, 16)
     run_and_kernel(pr, b, p, 6, "metropolis", seed=2)
@@ -130,8 +144,14 @@ def run_grid_records(pr, b, p, rounds, rule, seed):
     return kern
 
 
+def test_unfused_round_loop_uses_the_tpw_sweep_kernel():
+    b, p = sched(16, 16)
+    assert run_grid_records(C5S, b, p, 10, "metropolis", 4) == "plane_tpw_sweep_kernel"
+
+
 @pytest.mark.parametrize("rule", ["metropolis", "heat_bath"])
-def test_unfused_round_loop_uses_the_tpw_sweep_kernel(rule):
+def test_unfused_round_loop_tpw_generic(monkeypatch, rule):
+    monkeypatch.setenv("TG_PLANE_TPW", "2")
     b, p = sched(16, 16)
     assert run_grid_records(C5S, b, p, 10, rule, 4) == "plane_tpw_sweep_kernel"
     b, p = sched(8, 8, 0.1, 3.0)
