@@ -409,22 +409,25 @@ __global__ void extract_kernel(ExtractArgs e) {
 __global__ void plane_init_kernel(uint32_t* spins, int n, int W, int local_states, int state0,
                                   uint64_t seed) {
     const int lane = threadIdx.x & 31;
-    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-    const long long gw = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
-    const long long npairs = (n + 1) >> 1;
-    // a warp keeps one word (its lanes' init keys) when the warp count allows
+    const int nw = gridDim.x * (blockDim.x >> 5);
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int npairs = (n + 1) >> 1;
+    // a warp keeps one word (its lanes' init keys, key schedule in registers)
+    // when the warp count allows: then p advances by nw / W with no division
     const bool fixed_w = nw % W == 0;
-    const long long items = npairs * W;
-    int w = (int)(gw % W);
-    uint64_t key = derive_seed(seed, kPurposeInit, (uint64_t)(state0 + w * 32 + lane));
-    for (long long it = gw; it < items; it += nw) {
+    const int items = npairs * W;  // <= 2^19 * 32
+    int w = gw % W;
+    uint32_t ks[20];
+    philox_key_schedule(derive_seed(seed, kPurposeInit, (uint64_t)(state0 + w * 32 + lane)), ks);
+    const int dp = nw / W;
+    int p = gw / W;
+    for (int it = gw; it < items; it += nw) {
         if (!fixed_w) {
-            w = (int)(it % W);
-            key = derive_seed(seed, kPurposeInit, (uint64_t)(state0 + w * 32 + lane));
+            w = it % W;
+            p = it / W;
+            philox_key_schedule(derive_seed(seed, kPurposeInit, (uint64_t)(state0 + w * 32 + lane)), ks);
         }
-        const long long p = it / W;
-        const u32x4 o = philox4x32_10(u32x4{(uint32_t)p, (uint32_t)((uint64_t)p >> 32), 0u, 0u},
-                                      (uint32_t)key, (uint32_t)(key >> 32));
+        const u32x4 o = philox4x32_10_ks(u32x4{(uint32_t)p, 0u, 0u, 0u}, ks);
         const bool live = w * 32 + lane < local_states;
         const uint32_t w0 = __ballot_sync(0xffffffffu, live && (o.y >> 31));  // draw 2p
         const uint32_t w1 = __ballot_sync(0xffffffffu, live && (o.w >> 31));  // draw 2p + 1
@@ -432,6 +435,7 @@ __global__ void plane_init_kernel(uint32_t* spins, int n, int W, int local_state
             spins[(size_t)(2 * p) * W + w] = w0;
             if (2 * p + 1 < n) spins[(size_t)(2 * p + 1) * W + w] = w1;
         }
+        p += dp;
     }
 }
 

@@ -90,7 +90,7 @@ TG_HD u32x4 philox4x32_10_ks(u32x4 c, const uint32_t* ks) {
     return c;
 }
 
-inline void philox_key_schedule(uint64_t key, uint32_t ks[20]) {
+TG_HD void philox_key_schedule(uint64_t key, uint32_t ks[20]) {
     uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
     for (int r = 0; r < 10; ++r) {
         ks[2 * r] = k0;
