@@ -274,6 +274,7 @@ struct tg_ctx {
     // plane
     DBuf<uint32_t> d_spins32, d_kp, d_kpc, d_active;
     DBuf<int32_t> d_nbr, d_cnt_c, d_cnt_q, d_cnt2;
+    DBuf<int4> d_nbr4;
     DBuf<int> d_work;
     DBuf<Chunk> d_chunks;
     DBuf<int> d_chunk_off, d_color_start;

@@ -240,6 +240,16 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
     for (const auto& t : types)
         if (!(t.dc == 3 && (t.dq == 1 || (t.dq == 0 && (t.pad & 1))))) c.tpw_fast = 0;
     if (const char* e = std::getenv("TG_PLANE_FAST")) c.tpw_fast = c.tpw_fast && std::atoi(e) != 0;
+    // the config-5 path's per-site padded neighbour table (row offsets)
+    c.d_nbr4.release();
+    if (c.tpw_fast && (c.W & (c.W - 1)) == 0 && c.W <= 32) {
+        TypeDq tdq{};
+        for (int q = 0; q < c.n_types; ++q) tdq.dq[q] = types[q].dq;
+        int logW = 0;
+        while ((1 << logW) < c.W) ++logW;
+        c.d_nbr4.alloc((size_t)n);
+        CK(tpw_build_nbr4(c.d_chunks.p, (int)c.d_chunks.n, tdq, c.d_nbr.p, logW, c.d_nbr4.p, st));
+    }
     // thread-per-(site, word) kernels (rows of a power-of-two number of
     // words): by default only on their config-5 path, where they are faster
     // (r1: 1.60e12 vs 1.39e12 flips/s); on generic site types and heat bath
@@ -312,6 +322,7 @@ PlaneArgs plane_args(tg_ctx& c) {
     a.m_cost = c.m_cost;
     a.spins = c.d_spins32.p;
     a.nbr = c.d_nbr.p;
+    a.nbr4 = c.d_nbr4.p;
     a.chunks = c.d_chunks.p;
     a.chunk_off = c.d_chunk_off.p;
     a.color_start = c.d_color_start.p;

@@ -27,6 +27,29 @@ void* plane_rounds_fn_r1(int wv, int fast);
 void* plane_tpw_fn_r0(int fast);
 void* plane_tpw_fn_r1(int fast);
 void* plane_tpw_fn(int rule, int fast) { return rule == 0 ? plane_tpw_fn_r0(fast) : plane_tpw_fn_r1(fast); }
+// Per-site padded neighbour table of the tpw config-5 path (one warp per chunk).
+__global__ void k_tpw_nbr4(const Chunk* chunks, int n_chunks, TypeDq tdq, const int32_t* nbr, int logW,
+                           int4* out) {
+    const int lane = threadIdx.x & 31;
+    for (int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < n_chunks;
+         q += gridDim.x * (blockDim.x >> 5)) {
+        const Chunk ch = chunks[q];
+        if (lane >= ch.len) continue;
+        const int dq = tdq.dq[ch.type];
+        const int32_t* e = nbr + ch.nbr_base + lane * (3 + dq);
+        auto sh = [&](int32_t v) {
+            return (int)((((uint32_t)v & 0x7fffffffu) << logW) | ((uint32_t)v & 0x80000000u));
+        };
+        out[ch.start + lane] = make_int4(sh(e[0]), sh(e[1]), sh(e[2]), dq ? sh(e[3]) : 0);
+    }
+}
+
+cudaError_t tpw_build_nbr4(const Chunk* chunks, int n_chunks, TypeDq tdq, const int32_t* nbr, int logW,
+                           int4* out, cudaStream_t st) {
+    if (n_chunks > 0) k_tpw_nbr4<<<(n_chunks + 7) / 8, 256, 0, st>>>(chunks, n_chunks, tdq, nbr, logW, out);
+    return cudaGetLastError();
+}
+
 void* plane_tpw_sweep_fn_r0(int fast);
 void* plane_tpw_sweep_fn_r1(int fast);
 void* plane_tpw_sweep_fn(int rule, int fast) {

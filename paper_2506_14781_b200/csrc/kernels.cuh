@@ -60,6 +60,9 @@ void* plane_sweep_fn(int rule, int wv);
 void* plane_rounds_fn(int rule, int wv, int fast);
 void* plane_tpw_fn(int rule, int fast);
 void* plane_tpw_sweep_fn(int rule, int fast);
+struct TypeDq { int dq[kMaxTypes]; };
+cudaError_t tpw_build_nbr4(const Chunk* chunks, int n_chunks, TypeDq tdq, const int32_t* nbr, int logW,
+                           int4* out, cudaStream_t st);
 int plane_words_per_pass(int W);
 void* slot_sweep_fn();
 void* slot_sweep_fn_d(int D);  // padded-degree variant, D in {4, 8}

@@ -454,10 +454,10 @@ __device__ __forceinline__ void c5_site(const PlaneArgs& a, const C5K& K, const 
     x1 ^= (uint32_t)(e1 >> 31);
     x2 ^= (uint32_t)(e2 >> 31);
     uint32_t lowx = 7u, lowy = 1u;
-    if (!ALLLOW) {
-        lowx = (uint32_t)((int)j0 < K.lower) | ((uint32_t)((int)j1 < K.lower) << 1) |
-               ((uint32_t)((int)j2 < K.lower) << 2);
-        lowy = (uint32_t)((int)jq < K.lower);
+    if (!ALLLOW) {  // j are row offsets (index << log2 W)
+        const int lw = K.lower << K.logW;
+        lowx = (uint32_t)((int)j0 < lw) | ((uint32_t)((int)j1 < lw) << 1) | ((uint32_t)((int)j2 < lw) << 2);
+        lowy = (uint32_t)((int)jq < lw);
     }
     const uint32_t a0 = ~(s ^ x0), a1 = ~(s ^ x1), a2 = ~(s ^ x2);  // satisfied bonds
     const uint32_t c0 = a0 ^ a1 ^ a2;
@@ -584,15 +584,9 @@ __device__ __forceinline__ void tpw_phase_c5(const PlaneArgs& a, int c, uint64_t
     };
     auto entries = [&](int it, const Chunk& ch, int32_t (&e)[4]) {
         const int pos = (it & (W - 1)) * S + sl;
-        e[0] = e[1] = e[2] = e[3] = 0;
-        if (it < n_items && pos < ch.len) {
-            const int deg = 3 + a.ty[ch.type].dq;
-            const int32_t* nb = a.nbr + (uint32_t)(ch.nbr_base + pos * deg);
-            e[0] = __ldg(nb);
-            e[1] = __ldg(nb + 1);
-            e[2] = __ldg(nb + 2);
-            if (deg == 4) e[3] = __ldg(nb + 3);
-        }
+        int4 v = make_int4(0, 0, 0, 0);
+        if (it < n_items && pos < ch.len) v = __ldg(a.nbr4 + (ch.start + pos));  // one 16-byte load
+        e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
     };
     int item = gw;
     Chunk ch_c = chunk_of(item), ch_n = chunk_of(item + nw);
@@ -606,10 +600,10 @@ __device__ __forceinline__ void tpw_phase_c5(const PlaneArgs& a, int c, uint64_t
         if (p0 + sl < ch.len) {  // gathers first: in flight during the prefetches and the Philox blocks
             const uint32_t* sp = a.spins + w;
             R.s = sp[(uint32_t)(ch.start + p0 + sl) << logW];
-            R.x0 = sp[((uint32_t)e0 & 0x7fffffffu) << logW];
-            R.x1 = sp[((uint32_t)e1 & 0x7fffffffu) << logW];
-            R.x2 = sp[((uint32_t)e2 & 0x7fffffffu) << logW];
-            if (a.ty[ch.type].dq) R.y0 = sp[(uint32_t)e3 << logW];
+            R.x0 = sp[(uint32_t)e0 & 0x7fffffffu];  // nbr4 entries are row offsets
+            R.x1 = sp[(uint32_t)e1 & 0x7fffffffu];
+            R.x2 = sp[(uint32_t)e2 & 0x7fffffffu];
+            if (a.ty[ch.type].dq) R.y0 = sp[(uint32_t)e3];
         }
         ch_c = ch_n;
         ch_n = chunk_of(item + 2 * nw);
