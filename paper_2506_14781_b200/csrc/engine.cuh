@@ -57,7 +57,7 @@ struct PlaneArgs {
     uint32_t* spins;      // [n][W]
     const int32_t* nbr;   // per site: dc cost neighbours (bit31 = J<0), dq chain partners
     const int4* nbr4;     // tpw config-5 path: per site {3 cost neighbours, chain partner} as
-                          // row offsets (index << log2 W) with bit 31 = J<0; 0 without a partner
+                          // row offsets (index << log2 W), bit 31 = J<0 (cost) / no partner (4th)
     const Chunk* chunks;  // all colours, concatenated
     const int* chunk_off; // [n_colors+1]
     const int* color_start; // [n_colors+1] internal site ranges

@@ -40,7 +40,8 @@ __global__ void k_tpw_nbr4(const Chunk* chunks, int n_chunks, TypeDq tdq, const 
         auto sh = [&](int32_t v) {
             return (int)((((uint32_t)v & 0x7fffffffu) << logW) | ((uint32_t)v & 0x80000000u));
         };
-        out[ch.start + lane] = make_int4(sh(e[0]), sh(e[1]), sh(e[2]), dq ? sh(e[3]) : 0);
+        // bit 31 of the 4th entry: no chain partner
+        out[ch.start + lane] = make_int4(sh(e[0]), sh(e[1]), sh(e[2]), dq ? sh(e[3]) : (int)0x80000000u);
     }
 }
 

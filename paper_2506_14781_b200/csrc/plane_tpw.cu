@@ -430,6 +430,7 @@ struct C5K {
     uint32_t act_w, grp4, tlo, thi;
     PhiloxT P;
     int w, logW, lower;
+    int t30, t31;          // type ids of the chain-free and the chain sites
 };
 
 // An item's row words (own, cost neighbours, chain partner), gathered at the
@@ -439,12 +440,10 @@ struct C5Rows {
 };
 
 template <int DQ, bool ALLLOW>
-__device__ __forceinline__ void c5_site(const PlaneArgs& a, const C5K& K, const Chunk& ch,
-                                        const PlaneType& ty, int pos, bool count,
+__device__ __forceinline__ void c5_site(const PlaneArgs& a, const C5K& K, int tyi,
+                                        const PlaneType& ty, uint32_t site, bool valid, bool count,
                                         uint32_t (&Vc)[kVB], int& qn, int32_t e0, int32_t e1,
                                         int32_t e2, int32_t e3, const C5Rows& R) {
-    const bool valid = pos < ch.len;
-    const uint32_t site = (uint32_t)(ch.start + pos);
     const uint32_t j0 = (uint32_t)e0 & 0x7fffffffu, j1 = (uint32_t)e1 & 0x7fffffffu,
                    j2 = (uint32_t)e2 & 0x7fffffffu, jq = (uint32_t)e3;
     uint32_t s = R.s, x0 = R.x0, x1 = R.x1, x2 = R.x2, y0 = R.y0;
@@ -523,7 +522,7 @@ __device__ __forceinline__ void c5_site(const PlaneArgs& a, const C5K& K, const 
             const int e = qn + __popc(pend & ((1u << (threadIdx.x & 31)) - 1u));
             const int warp = threadIdx.x >> 5;
             tq(warp, kQSite)[e] = (int)site;
-            tq(warp, kQMeta)[e] = K.w | (ch.type << 5) | ((int)count << 10) |
+            tq(warp, kQMeta)[e] = K.w | (tyi << 5) | ((int)count << 10) |
                                   ((ALLLOW ? 3 : __popc(lowx)) << 11);
             tq(warp, kQUnd)[e] = (int)und;
             tq(warp, kQC0)[e] = (int)c0;
@@ -547,19 +546,19 @@ __device__ __forceinline__ void tpw_phase_c5(const PlaneArgs& a, int c, uint64_t
     const int lane = threadIdx.x & 31;
     const int W = 1 << logW, S = 32 >> logW;
     const int w = lane & (W - 1), sl = lane >> logW;
-    const int c0 = a.chunk_off[c];
-    const int n_items = (a.chunk_off[c + 1] - c0) << logW;
     const int lower = a.color_start[c];
     count = count && lower > 0;  // colour 0 has no lower-colour neighbours
     const bool alllow = a.n_colors == 2 && c == 1;  // proper 2-colouring: every neighbour is colour 0
     C5K K;
     K.kc2 = (uint32_t)(w * a.n_types * 128);
     K.kpw = (uint32_t)(w * a.kpw);
+    K.t30 = K.t31 = 0;  // FAST kernels: at most one type of each
+    for (int ty = 0; ty < a.n_types; ++ty) {
+        if (a.ty[ty].dq == 0) K.t30 = ty;
+        else K.t31 = ty;
+    }
     {
-        int t30 = 0;  // the cost-3 chain-free type (FAST kernels have at most one)
-        for (int ty = 0; ty < a.n_types; ++ty)
-            if (a.ty[ty].dq == 0) t30 = ty;
-        const uint4* kc = reinterpret_cast<const uint4*>(a.kpc + K.kc2) + t30 * 32;
+        const uint4* kc = reinterpret_cast<const uint4*>(a.kpc + K.kc2) + K.t30 * 32;
         K.k2a = kc[0];
         K.k2b = kc[1];
         K.k3a = kc[16];
@@ -574,48 +573,48 @@ __device__ __forceinline__ void tpw_phase_c5(const PlaneArgs& a, int c, uint64_t
     K.logW = logW;
     K.lower = lower;
     int since = 0, qn = 0;
-    // items strided over the warps (the chain-site items, costlier, sit
-    // together in the canonical order: a contiguous split unbalances the
-    // grid barrier); chunk descriptors two items ahead, entries one
-    auto chunk_of = [&](int it) {
-        Chunk ch{0, 0, 0, 0};
-        if (it < n_items) ch = a.chunks[c0 + (it >> logW)];
-        return ch;
-    };
-    auto entries = [&](int it, const Chunk& ch, int32_t (&e)[4]) {
-        const int pos = (it & (W - 1)) * S + sl;
-        int4 v = make_int4(0, 0, 0, 0);
-        if (it < n_items && pos < ch.len) v = __ldg(a.nbr4 + (ch.start + pos));  // one 16-byte load
-        e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
+    // items: S consecutive sites of the colour x the W words of their rows,
+    // strided over the warps (chain sites, costlier, sit together in the
+    // canonical order).  The padded neighbour table is indexed by site and
+    // flags chain-free sites (bit 31 of the 4th entry), so no chunk table is
+    // read; an item straddling the chain-free / chain boundary runs both
+    // paths with complementary lane masks.  Entries are loaded one item ahead.
+    const int cs = a.color_start[c], ce = a.color_start[c + 1];
+    const int n_it = (ce - cs + S - 1) / S;
+    const PlaneType& ty0 = a.ty[K.t30];
+    const PlaneType& ty1 = a.ty[K.t31];
+    auto entries = [&](int it, int4& e) {
+        const int site = cs + it * S + sl;
+        e = make_int4(0, 0, 0, (int)0x80000000u);
+        if (it < n_it && site < ce) e = __ldg(a.nbr4 + site);  // one 16-byte load
     };
     int item = gw;
-    Chunk ch_c = chunk_of(item), ch_n = chunk_of(item + nw);
-    int32_t en[4];
-    entries(item, ch_c, en);
-    for (; item < n_items; item += nw) {
-        const Chunk ch = ch_c;
-        const int32_t e0 = en[0], e1 = en[1], e2 = en[2], e3 = en[3];
-        const int p0 = (item & (W - 1)) * S;
+    int4 en;
+    entries(item, en);
+    for (; item < n_it; item += nw) {
+        const int4 e = en;
+        const uint32_t site = (uint32_t)(cs + item * S + sl);
+        const bool valid = (int)site < ce;
+        const bool hasq = valid && !((uint32_t)e.w & 0x80000000u);
         C5Rows R{0u, 0u, 0u, 0u, 0u};
-        if (p0 + sl < ch.len) {  // gathers first: in flight during the prefetches and the Philox blocks
+        if (valid) {  // gathers first: in flight during the prefetch and the Philox blocks
             const uint32_t* sp = a.spins + w;
-            R.s = sp[(uint32_t)(ch.start + p0 + sl) << logW];
-            R.x0 = sp[(uint32_t)e0 & 0x7fffffffu];  // nbr4 entries are row offsets
-            R.x1 = sp[(uint32_t)e1 & 0x7fffffffu];
-            R.x2 = sp[(uint32_t)e2 & 0x7fffffffu];
-            if (a.ty[ch.type].dq) R.y0 = sp[(uint32_t)e3];
+            R.s = sp[site << logW];
+            R.x0 = sp[(uint32_t)e.x & 0x7fffffffu];  // nbr4 entries are row offsets
+            R.x1 = sp[(uint32_t)e.y & 0x7fffffffu];
+            R.x2 = sp[(uint32_t)e.z & 0x7fffffffu];
+            if (hasq) R.y0 = sp[(uint32_t)e.w];
         }
-        ch_c = ch_n;
-        ch_n = chunk_of(item + 2 * nw);
-        entries(item + nw, ch_c, en);
-        if (p0 >= ch.len) continue;
-        const PlaneType& ty = a.ty[ch.type];
-        if (ty.nqb == 0) {
-            if (alllow) c5_site<0, true>(a, K, ch, ty, p0 + sl, count, Vc, qn, e0, e1, e2, e3, R);
-            else c5_site<0, false>(a, K, ch, ty, p0 + sl, count, Vc, qn, e0, e1, e2, e3, R);
-        } else {
-            c5_site<1, false>(a, K, ch, ty, p0 + sl, count, Vc, qn, e0, e1, e2, e3, R);
+        entries(item + nw, en);
+        // one call site per path; both run (complementary lanes) only when
+        // the item straddles the chain-free / chain boundary
+        const bool v0 = valid && !hasq;
+        if (__any_sync(0xffffffffu, v0)) {
+            if (alllow) c5_site<0, true>(a, K, K.t30, ty0, site, v0, count, Vc, qn, e.x, e.y, e.z, e.w, R);
+            else c5_site<0, false>(a, K, K.t30, ty0, site, v0, count, Vc, qn, e.x, e.y, e.z, e.w, R);
         }
+        if (__any_sync(0xffffffffu, hasq))
+            c5_site<1, false>(a, K, K.t31, ty1, site, hasq, count, Vc, qn, e.x, e.y, e.z, e.w, R);
         if (qn >= 32) {
             qn -= 32;
             tpw_drain(a, qn, 32, K.tlo, K.thi);
