@@ -234,11 +234,14 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
     if (const char* e = std::getenv("TG_PLANE_FAST")) c.fused_fast = c.fused_fast && std::atoi(e) != 0;
     c.fused_grid = 0;
     c.fused_tpw = 0;
-    // tpw FAST variant (c5_site): Metropolis, every site of cost degree 3
-    // and chain degree 0 / 1, chain-free types with flag bit 0
-    c.tpw_fast = c.cfg.rule == TG_RULE_METROPOLIS;
-    for (const auto& t : types)
-        if (!(t.dc == 3 && (t.dq == 1 || (t.dq == 0 && (t.pad & 1))))) c.tpw_fast = 0;
+    // tpw FAST variant (c5_site): every site of cost degree 3 and chain
+    // degree 0 / 1; Metropolis: chain-free types with flag bit 0
+    // (heat bath: any labels, its chain-free classes staged per phase)
+    c.tpw_fast = 1;
+    for (const auto& t : types) {
+        const bool metro_ok = t.dq == 1 || (t.dq == 0 && (t.pad & 1));
+        if (!(t.dc == 3 && t.dq <= 1 && (c.cfg.rule != TG_RULE_METROPOLIS || metro_ok))) c.tpw_fast = 0;
+    }
     if (const char* e = std::getenv("TG_PLANE_FAST")) c.tpw_fast = c.tpw_fast && std::atoi(e) != 0;
     // the config-5 path's per-site padded neighbour table (row offsets)
     c.d_nbr4.release();

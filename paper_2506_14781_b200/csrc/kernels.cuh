@@ -24,12 +24,16 @@ constexpr int kTpwThreads = TG_TPW_THREADS;  // thread-per-(site, word) fused ke
 constexpr int kTpwMinBlocks = TG_TPW_MINB;
 constexpr int kTpwVB = 8;               // planes of its vertical bond counters
 constexpr int kTpwQCap = 64;            // per-warp deferred-tail queue entries (>= 31 + 32)
+constexpr int kTpwQFields = 7;          // words per queue entry
+constexpr int kTpwHbWords = 9 * 32 * 4; // heat-bath threshold stage: [9 planes][<= 32 words] uint4
 // Dynamic shared memory of plane_tpw_rounds_kernel: tail queues
-// [warps][6][kTpwQCap], chain vertical counters [kTpwVB][threads],
-// per-replica counters [2][32W], labels and energies (plane_round.cuh).
+// [warps][kTpwQFields][kTpwQCap], chain vertical counters [kTpwVB][threads],
+// the heat-bath threshold stage, per-replica counters [2][32W], labels and
+// energies (plane_round.cuh).
 inline size_t tpw_smem_bytes(int R, int W, int threads) {
     return (size_t)R * (2 * sizeof(double) + 2 * sizeof(int32_t)) + 8 + (size_t)2 * W * 32 * sizeof(int) +
-           (size_t)kTpwVB * threads * sizeof(int) + (size_t)(threads / 32) * kTpwQCap * 6 * sizeof(int);
+           (size_t)kTpwVB * threads * sizeof(int) + (size_t)kTpwHbWords * sizeof(int) +
+           (size_t)(threads / 32) * kTpwQCap * kTpwQFields * sizeof(int);
 }
 constexpr int kSlotThreads = 256;
 constexpr int kSwapThreads = 1024;

@@ -222,14 +222,19 @@ __device__ __forceinline__ void philox_plane2(uint32_t site, uint32_t g0, const 
 // 2-bit unsatisfied lower bonds m0/m1), chain vertical counters
 // [kVB][threads], per-replica counters [2][32W], then the round block.
 extern __shared__ __align__(16) int tpw_sm[];
-enum { kQSite, kQMeta, kQUnd, kQC0, kQM0, kQM1 };
+enum { kQSite, kQMeta, kQUnd, kQC0, kQM0, kQM1, kQC1, kQFields };
 __device__ __forceinline__ int* tq(int warp, int field) {
-    return tpw_sm + (warp * 6 + field) * kTpwQCap;
+    return tpw_sm + (warp * kQFields + field) * kTpwQCap;
 }
-constexpr int kTpwSmVq = (kTpwThreads / 32) * 6 * kTpwQCap;
-constexpr int kTpwSmCnt = kTpwSmVq + kVB * kTpwThreads;
+static_assert(kQFields == kTpwQFields, "queue layout");
+constexpr int kTpwSmVq = (kTpwThreads / 32) * kQFields * kTpwQCap;
+// heat bath, config-5 path: planes 0-7 and the "always" word of the 4
+// classes of the chain-free type, [9][W] uint4, staged once per colour phase
+constexpr int kTpwSmHb = kTpwSmVq + kVB * kTpwThreads;
+constexpr int kTpwSmCnt = kTpwSmHb + kTpwHbWords;
 
 // Resolve entries [base, base + n) of the warp's queue (n <= 32).
+template <int RULE>
 static __device__ __noinline__ void tpw_drain(const PlaneArgs& a, int base, int n, uint32_t tlo,
                                               uint32_t thi) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -238,12 +243,13 @@ static __device__ __noinline__ void tpw_drain(const PlaneArgs& a, int base, int 
     const bool mine = lane < n;
     const int e = base + lane;
     int site = 0, meta = 0;
-    uint32_t und = 0u, c0 = 0u;
+    uint32_t und = 0u, c0 = 0u, c1 = 0u;
     if (mine) {
         site = tq(warp, kQSite)[e];
         meta = tq(warp, kQMeta)[e];
         und = (uint32_t)tq(warp, kQUnd)[e];
         c0 = (uint32_t)tq(warp, kQC0)[e];
+        if (RULE == 1) c1 = (uint32_t)tq(warp, kQC1)[e];
     }
     const int w = meta & 31, type = (meta >> 5) & 31;
     const uint32_t grp4 = (uint32_t)(a.w_global0 + w) << 4;
@@ -254,10 +260,17 @@ static __device__ __noinline__ void tpw_drain(const PlaneArgs& a, int base, int 
     for (int blk = 2; blk < 14; ++blk) {
         if (!__any_sync(0xffffffffu, und)) break;
         const u32x4 r = philox_plane((uint32_t)site, grp4 | (uint32_t)blk, P, a.pks);
-        compare4_sel(c0, __ldg(kc2 + blk), __ldg(kc2 + 16 + blk), r, und, lt);
+        if (RULE == 0) {
+            compare4_sel(c0, __ldg(kc2 + blk), __ldg(kc2 + 16 + blk), r, und, lt);
+        } else {  // 4 classes, plane-major leaves of kp
+            const uint32_t cb[2] = {c0, c1};
+            compare_block<2>(cb, a.kp + (size_t)w * a.kpw + a.ty[type].kp_off, 4, blk, r, und, lt);
+        }
     }
     if (lt) {
-        a.spins[(size_t)site * a.W + w] ^= lt;
+        // Metropolis: late flips; heat bath: late "up" (the provisional word has them down)
+        if (RULE == 0) a.spins[(size_t)site * a.W + w] ^= lt;
+        else a.spins[(size_t)site * a.W + w] |= lt;
         if ((meta >> 10) & 1) {
             const uint32_t m0 = (uint32_t)tq(warp, kQM0)[e], m1 = (uint32_t)tq(warp, kQM1)[e];
             const int nlow = (meta >> 11) & 7;
@@ -439,7 +452,7 @@ struct C5Rows {
     uint32_t s, x0, x1, x2, y0;
 };
 
-template <int DQ, bool ALLLOW>
+template <int RULE, int DQ, bool ALLLOW>
 __device__ __forceinline__ void c5_site(const PlaneArgs& a, const C5K& K, int tyi,
                                         const PlaneType& ty, uint32_t site, bool valid, bool count,
                                         uint32_t (&Vc)[kVB], int& qn, int32_t e0, int32_t e1,
@@ -458,24 +471,47 @@ __device__ __forceinline__ void c5_site(const PlaneArgs& a, const C5K& K, int ty
         lowx = (uint32_t)((int)j0 < lw) | ((uint32_t)((int)j1 < lw) << 1) | ((uint32_t)((int)j2 < lw) << 2);
         lowy = (uint32_t)((int)jq < lw);
     }
-    const uint32_t a0 = ~(s ^ x0), a1 = ~(s ^ x1), a2 = ~(s ^ x2);  // satisfied bonds
+    // class counters: satisfied bonds (Metropolis) / +1 contributions (heat bath)
+    const uint32_t a0 = RULE == 0 ? ~(s ^ x0) : x0, a1 = RULE == 0 ? ~(s ^ x1) : x1,
+                   a2 = RULE == 0 ? ~(s ^ x2) : x2;
     const uint32_t c0 = a0 ^ a1 ^ a2;
     const uint32_t c1 = (a0 & a1) | (a2 & (a0 ^ a1));
     const uint32_t act = valid ? K.act_w : 0u;
     uint32_t always, und, lt = 0u;
     const uint32_t* kpb = a.kp + K.kpw + ty.kp_off;
-    uint32_t cb[3] = {c0, c1, DQ ? ~(s ^ y0) : 0u};
+    uint32_t cb[3] = {c0, c1, DQ ? (RULE == 0 ? ~(s ^ y0) : y0) : 0u};
+    // heat bath, chain-free sites: planes 0-7 and "always" of the 4 classes
+    // from the per-phase shared-memory stage [9][W] (uint4 = classes 0..3)
+    const uint4* hb = reinterpret_cast<const uint4*>(tpw_sm + kTpwSmHb) + K.w;
     if (DQ == 0) {
-        always = ~c1 & act;
-        und = c1 & act;
+        if (RULE == 0) {
+            always = ~c1 & act;
+            und = c1 & act;
+        } else {
+            const uint4 L = hb[8 << K.logW];
+            always = sel(c1, sel(c0, L.w, L.z), sel(c0, L.y, L.x)) & act;
+            und = act & ~always;
+        }
     } else {
         always = mux_tree<3>(cb, kpb + kKPlanes * 8) & act;
         und = act & ~always;
     }
     {
         if (DQ == 0) {
-            compare4_sel(c0, K.k2a, K.k3a, r0, und, lt);
-            compare4_sel(c0, K.k2b, K.k3b, r1, und, lt);
+            if (RULE == 0) {
+                compare4_sel(c0, K.k2a, K.k3a, r0, und, lt);
+                compare4_sel(c0, K.k2b, K.k3b, r1, und, lt);
+            } else {
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    const uint4 L = hb[b << K.logW];
+                    const uint32_t tb = sel(c1, sel(c0, L.w, L.z), sel(c0, L.y, L.x));
+                    const uint32_t rb = b == 0 ? r0.x : b == 1 ? r0.y : b == 2 ? r0.z : b == 3 ? r0.w
+                                      : b == 4 ? r1.x : b == 5 ? r1.y : b == 6 ? r1.z : r1.w;
+                    lt |= und & tb & ~rb;
+                    und &= ~(tb ^ rb);
+                }
+            }
         } else {
             compare_block<3>(cb, kpb, 8, 0, r0, und, lt);
             compare_block<3>(cb, kpb, 8, 1, r1, und, lt);
@@ -493,11 +529,13 @@ __device__ __forceinline__ void c5_site(const PlaneArgs& a, const C5K& K, int ty
         }
     }
     const uint32_t take = (always | lt) & act;
-    const uint32_t ns = s ^ take;
+    // Metropolis: taken lanes flip; heat bath: taken lanes +1, the others -1
+    // (undecided lanes provisionally -1, raised by the drain when taken)
+    const uint32_t ns = RULE == 0 ? (s ^ take) : ((s & ~act) | take);
     if (valid) a.spins[K.w + (site << K.logW)] = ns;
     uint32_t m[2] = {0u, 0u};
     if (count) {
-        if (ALLLOW) {
+        if (RULE == 0 && ALLLOW) {
             m[0] = ~(c0 ^ take) & act;
             m[1] = ~(c1 ^ take) & act;
         } else {
@@ -528,6 +566,7 @@ __device__ __forceinline__ void c5_site(const PlaneArgs& a, const C5K& K, int ty
             tq(warp, kQC0)[e] = (int)c0;
             tq(warp, kQM0)[e] = (int)m[0];
             tq(warp, kQM1)[e] = (int)m[1];
+            if (RULE == 1) tq(warp, kQC1)[e] = (int)c1;
         }
         qn += __popc(pend);
     }
@@ -557,12 +596,23 @@ __device__ __forceinline__ void tpw_phase_c5(const PlaneArgs& a, int c, uint64_t
         if (a.ty[ty].dq == 0) K.t30 = ty;
         else K.t31 = ty;
     }
-    {
+    if (RULE == 0) {
         const uint4* kc = reinterpret_cast<const uint4*>(a.kpc + K.kc2) + K.t30 * 32;
         K.k2a = kc[0];
         K.k2b = kc[1];
         K.k3a = kc[16];
         K.k3b = kc[17];
+    } else {
+        // heat bath: stage planes 0-7 and "always" of the chain-free type's 4
+        // classes for every word: [9][W] uint4 (the previous phase's readers
+        // are past the grid barrier that preceded this phase)
+        uint4* hb = reinterpret_cast<uint4*>(tpw_sm + kTpwSmHb);
+        const int kp0 = a.ty[K.t30].kp_off;
+        for (int q = threadIdx.x; q < 9 * W; q += blockDim.x) {
+            const int b = q / W, ww = q % W;
+            hb[q] = *reinterpret_cast<const uint4*>(a.kp + (size_t)ww * a.kpw + kp0 + (b < 8 ? b : kKPlanes) * 4);
+        }
+        __syncthreads();
     }
     K.act_w = a.active[w];
     K.grp4 = (uint32_t)(a.w_global0 + w) << 4;
@@ -610,14 +660,14 @@ __device__ __forceinline__ void tpw_phase_c5(const PlaneArgs& a, int c, uint64_t
         // the item straddles the chain-free / chain boundary
         const bool v0 = valid && !hasq;
         if (__any_sync(0xffffffffu, v0)) {
-            if (alllow) c5_site<0, true>(a, K, K.t30, ty0, site, v0, count, Vc, qn, e.x, e.y, e.z, e.w, R);
-            else c5_site<0, false>(a, K, K.t30, ty0, site, v0, count, Vc, qn, e.x, e.y, e.z, e.w, R);
+            if (alllow) c5_site<RULE, 0, true>(a, K, K.t30, ty0, site, v0, count, Vc, qn, e.x, e.y, e.z, e.w, R);
+            else c5_site<RULE, 0, false>(a, K, K.t30, ty0, site, v0, count, Vc, qn, e.x, e.y, e.z, e.w, R);
         }
         if (__any_sync(0xffffffffu, hasq))
-            c5_site<1, false>(a, K, K.t31, ty1, site, hasq, count, Vc, qn, e.x, e.y, e.z, e.w, R);
+            c5_site<RULE, 1, false>(a, K, K.t31, ty1, site, hasq, count, Vc, qn, e.x, e.y, e.z, e.w, R);
         if (qn >= 32) {
             qn -= 32;
-            tpw_drain(a, qn, 32, K.tlo, K.thi);
+            tpw_drain<RULE>(a, qn, 32, K.tlo, K.thi);
         }
         if (count && ++since >= flush_every) {  // keep the 8-bit vertical counters from overflowing
             vflush(Vc, logW, s_cc);
@@ -635,7 +685,7 @@ __device__ __forceinline__ void tpw_phase_c5(const PlaneArgs& a, int c, uint64_t
     while (qn > 0) {
         const int n = qn < 32 ? qn : 32;
         qn -= n;
-        tpw_drain(a, qn, n, K.tlo, K.thi);
+        tpw_drain<RULE>(a, qn, n, K.tlo, K.thi);
     }
     if (count) {
         vflush(Vc, logW, s_cc);
@@ -694,7 +744,7 @@ __device__ __forceinline__ void tpw_phase(const PlaneArgs& a, int c, uint64_t t,
 #undef TG_TCASE
         if (qn >= 32) {
             qn -= 32;
-            tpw_drain(a, qn, 32, tlo, thi);
+            tpw_drain<RULE>(a, qn, 32, tlo, thi);
         }
         if (count && ++since >= flush_every) {  // keep the 8-bit vertical counters from overflowing
             vflush(Vc, logW, s_cc);
@@ -712,7 +762,7 @@ __device__ __forceinline__ void tpw_phase(const PlaneArgs& a, int c, uint64_t t,
     while (qn > 0) {
         const int n = qn < 32 ? qn : 32;
         qn -= n;
-        tpw_drain(a, qn, n, tlo, thi);
+        tpw_drain<RULE>(a, qn, n, tlo, thi);
     }
     if (count) {
         vflush(Vc, logW, s_cc);

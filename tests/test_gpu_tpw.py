@@ -2,9 +2,10 @@
 
 The single-GPU fused round loop has three device paths with one contract
 (plane_tpw.cu, plane_sweep.cu): the thread-per-(site, word) kernel's config-5
-path (Metropolis, cost degree 3, chain degree 0/1; the default where it
-applies), its generic path (any site type, both rules; TG_PLANE_TPW=2) and
-the thread-per-site kernel (everything else by default, TG_PLANE_TPW=0).  Every case is compared bit
+path (cost degree 3, chain degree 0/1; the default where it applies), its generic path (any site type, both rules; TG_PLANE_TPW=2) and
+the thread-per-site kernel (everything else by default, TG_PLANE_TPW=0).
+The config-5 path serves both rules (heat bath: four classes per chain-free
+site, staged per colour phase in shared memory).  Every case is compared bit
 for bit with the oracle (f, g, feasibility, digests, final grid, counters)
 and the test checks which kernel the engine reports it launched.
 """
@@ -77,11 +78,19 @@ def test_tpw_negative_betas_disable_the_class_shortcut(monkeypatch, mode):
 
 
 @pytest.mark.parametrize("rule", ["metropolis", "heat_bath"])
-def test_default_dispatch_outside_the_config5_path(rule):
+def test_default_dispatch(rule):
+    # config-5 site types: the tpw kernel for both rules; other types: thread per site
     b, p = sched(8, 8, 0.1, 3.0)
     assert kernel_of(K10, b, p, rule) == "plane_rounds_kernel"
     b, p = sched(16, 16)
-    assert kernel_of(C5S, b, p, "heat_bath") == "plane_rounds_kernel"
+    assert kernel_of(C5S, b, p, rule) == "plane_tpw_rounds_kernel"
+
+
+@pytest.mark.parametrize("grid", [(4, 8), (16, 16), (32, 32)])
+def test_tpw_config5_path_heat_bath(grid):
+    b, p = sched(*grid)
+    run_and_kernel(C5S, b, p, 12, "heat_bath")
+    run_and_kernel(C5S, *sched(grid[0], grid[1], 0.05, 2.0), 12, "heat_bath", seed=9)
 
 
 def test_non_power_of_two_rows_use_the_thread_per_site_kernel():
@@ -144,9 +153,10 @@ def run_grid_records(pr, b, p, rounds, rule, seed):
     return kern
 
 
-def test_unfused_round_loop_uses_the_tpw_sweep_kernel():
+@pytest.mark.parametrize("rule", ["metropolis", "heat_bath"])
+def test_unfused_round_loop_uses_the_tpw_sweep_kernel(rule):
     b, p = sched(16, 16)
-    assert run_grid_records(C5S, b, p, 10, "metropolis", 4) == "plane_tpw_sweep_kernel"
+    assert run_grid_records(C5S, b, p, 10, rule, 4) == "plane_tpw_sweep_kernel"
 
 
 @pytest.mark.parametrize("rule", ["metropolis", "heat_bath"])
