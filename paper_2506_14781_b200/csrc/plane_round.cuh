@@ -10,6 +10,7 @@
 
 #include "engine.cuh"
 #include "kernels.cuh"
+#include "plane_device.cuh"
 
 namespace tg {
 
@@ -81,6 +82,9 @@ __device__ __forceinline__ void round_epilogue(const PlaneArgs& a, const RoundAr
     }
     swap_base += (uint64_t)n_att;
     __syncthreads();
+#ifdef TPW_EPI_STAMP
+    TPW_EPI_STAMP(k, 8);
+#endif
     if (blockIdx.x == 0) {
         // counters of the other parity are free again: zero them
         int32_t* other = r.cnt + (size_t)(par ^ 1) * 2 * r.cnt_stride;
@@ -111,7 +115,11 @@ __device__ __forceinline__ void round_epilogue(const PlaneArgs& a, const RoundAr
             for (int q = tid; q < nb; q += blockDim.x) dst[np + q] = r.acc_b[q];
         }
     }
-    // threshold planes for the new labels: warp job = (word, type, class)
+    // threshold planes for the new labels: warp job = (word, type, class).
+    // Plane b (b = 0..52) holds bit 52-b of the lanes' 53-bit thresholds:
+    // the 32x32 transpose of the words K >> 21 gives lane j plane 31-j, that
+    // of K << 11 gives lane j >= 11 plane 63-j (two transposes instead of 53
+    // ballots).
     {
         int combos = 0;
         for (int ty = 0; ty < a.n_types; ++ty) combos += a.ty[ty].ncl;
@@ -128,26 +136,46 @@ __device__ __forceinline__ void round_epilogue(const PlaneArgs& a, const RoundAr
             uint32_t* dst = r.kp + (size_t)w * a.kpw + pt.kp_off + c;
             uint32_t* dstc = (c == 2 || c == 3)
                 ? r.kpc + ((size_t)w * a.n_types + ty) * 128 + (c - 2) * 64 : nullptr;
-            for (int b = 0; b < kKPlanes; ++b) {
-                const uint32_t word = __ballot_sync(0xffffffffu, live && ((K >> (52 - b)) & 1ull));
-                if (lane == (b & 31)) {
-                    dst[b * pt.ncl] = word;
-                    if (dstc) dstc[b] = word;
-                }
+            const uint32_t th = warp_transpose32((uint32_t)(K >> 21));
+            const uint32_t tl = warp_transpose32((uint32_t)(K << 11));
+            const int bh = 31 - lane, bl = 63 - lane;
+            dst[bh * pt.ncl] = th;
+            if (dstc) dstc[bh] = th;
+            if (lane >= 11) {
+                dst[bl * pt.ncl] = tl;
+                if (dstc) dstc[bl] = tl;
             }
             const uint32_t alw = __ballot_sync(0xffffffffu, live && K >= (1ull << 53));
-            if (lane == (kKPlanes & 31)) dst[kKPlanes * pt.ncl] = alw;
+            if (lane == 0) dst[kKPlanes * pt.ncl] = alw;
         }
     }
+#ifdef TPW_EPI_STAMP
+    TPW_EPI_STAMP(k, 9);
+#endif
     // target-state digest / snapshot for the trace (optional)
     if (r.rec_flags & 3) {
         const int tg = s.slot[r.R - 1];
         uint64_t dsum = 0;
-        for (int i = blockIdx.x * blockDim.x + tid; i < a.n; i += gridDim.x * blockDim.x) {
-            const bool up = (a.spins[(size_t)i * a.W + (tg >> 5)] >> (tg & 31)) & 1u;
-            const int ci = r.perm[i];
-            if (r.rec_flags & 2) r.rec_states[(size_t)k * a.n + ci] = up ? 1 : -1;
-            if (up) dsum += digest_term((uint64_t)ci);
+        // four independent row loads in flight per thread (the pass is a
+        // latency-bound gather of one word per site)
+        const int stride = gridDim.x * blockDim.x;
+        for (int i0 = blockIdx.x * blockDim.x + tid; i0 < a.n; i0 += 4 * stride) {
+            uint32_t wv[4];
+            int ci[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * stride;
+                wv[u] = i < a.n ? a.spins[(size_t)i * a.W + (tg >> 5)] : 0u;
+                ci[u] = i < a.n ? r.perm[i] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * stride;
+                if (i >= a.n) break;
+                const bool up = (wv[u] >> (tg & 31)) & 1u;
+                if (r.rec_flags & 2) r.rec_states[(size_t)k * a.n + ci[u]] = up ? 1 : -1;
+                if (up) dsum += digest_term((uint64_t)ci[u]);
+            }
         }
         if (r.rec_flags & 1) {
 #pragma unroll
@@ -158,6 +186,9 @@ __device__ __forceinline__ void round_epilogue(const PlaneArgs& a, const RoundAr
                           (unsigned long long)dsum);
         }
     }
+#ifdef TPW_EPI_STAMP
+    TPW_EPI_STAMP(k, 10);
+#endif
     cg::this_grid().sync();
 }
 

@@ -27,7 +27,6 @@
 #include "engine.cuh"
 #include "kernels.cuh"
 #include "plane_device.cuh"
-#include "plane_round.cuh"
 
 #ifndef TG_PLANE_RULE
 #define TG_PLANE_RULE 0
@@ -37,6 +36,30 @@
 
 namespace cg = cooperative_groups;
 
+namespace tg {
+
+// Stage timer (variant builds only, -DTG_TPW_PROF=1): block 0 records
+// %globaltimer at the stages of the first 64 rounds of a launch; every block
+// records the latest "all items of this phase done" time (atomicMax).
+#ifndef TG_TPW_PROF
+#define TG_TPW_PROF 0
+#endif
+#if TG_TPW_PROF
+__device__ unsigned long long g_tpw_prof[64][16];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TPW_STAMP(k, s) do { if ((k) < 64 && blockIdx.x == 0 && threadIdx.x == 0) g_tpw_prof[k][s] = gtimer(); } while (0)
+#define TPW_MAXSTAMP(k, s) do { __syncthreads(); if ((k) < 64 && threadIdx.x == 0) atomicMax(&g_tpw_prof[k][s], gtimer()); } while (0)
+#define TPW_EPI_STAMP(k, s) TPW_STAMP(k, s)
+#else
+#define TPW_STAMP(k, s) do {} while (0)
+#define TPW_MAXSTAMP(k, s) do {} while (0)
+#endif
+}  // namespace tg
+#include "plane_round.cuh"
 namespace tg {
 
 constexpr int kVB = kTpwVB;  // planes of the per-thread vertical bond counters (max 255)
@@ -810,12 +833,15 @@ plane_tpw_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_consta
         const int par = (int)(round & 1);
         int32_t* cc = r.cnt + (size_t)par * 2 * r.cnt_stride;
         int32_t* cq = cc + r.cnt_stride;
+        TPW_STAMP(k, 0);
         for (int sw = 0; sw < r.sps; ++sw) {
             const uint64_t t = (uint64_t)((round - 1) * r.sps + sw);
             const bool count = (sw == r.sps - 1);
             for (int c = 0; c < a.n_colors; ++c) {
                 if constexpr (FAST) tpw_phase_c5<RULE>(a, c, t, count, gw, nw, logW, Vc, flush_every);
                 else tpw_phase<RULE, FAST>(a, c, t, count, gw, nw, logW, Vc, flush_every);
+                TPW_STAMP(k, 1 + 3 * (c & 1));
+                TPW_MAXSTAMP(k, 2 + 3 * (c & 1));
                 if (count && a.color_start[c] > 0) {
                     __syncthreads();
                     for (int m = threadIdx.x; m < nrep; m += blockDim.x) {
@@ -825,9 +851,11 @@ plane_tpw_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_consta
                     }
                 }
                 grid.sync();
+                TPW_STAMP(k, 3 + 3 * (c & 1));
             }
         }
         round_epilogue(a, r, s, k, round, cc, cq, swap_base, 0);
+        TPW_STAMP(k, 7);
     }
 }
 
@@ -892,6 +920,16 @@ template __global__ void plane_tpw_rounds_kernel<TG_PLANE_RULE, 0>(const __grid_
                                                                    const __grid_constant__ RoundArgs);
 template __global__ void plane_tpw_rounds_kernel<TG_PLANE_RULE, 1>(const __grid_constant__ PlaneArgs,
                                                                    const __grid_constant__ RoundArgs);
+
+#if TG_TPW_PROF && TG_PLANE_RULE == 0
+extern "C" int tg_debug_tpw_prof(unsigned long long* dst) {
+    return (int)cudaMemcpyFromSymbol(dst, g_tpw_prof, sizeof(g_tpw_prof));
+}
+extern "C" int tg_debug_tpw_prof_reset() {
+    static unsigned long long z[64][16] = {};
+    return (int)cudaMemcpyToSymbol(g_tpw_prof, z, sizeof(z));
+}
+#endif
 
 void* TG_CAT(plane_tpw_fn_r, TG_PLANE_RULE)(int fast) {
     return fast ? (void*)plane_tpw_rounds_kernel<TG_PLANE_RULE, 1>
