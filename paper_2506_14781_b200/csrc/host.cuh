@@ -15,6 +15,8 @@
 #include <cstring>
 #include <limits>
 #include <map>
+#include <mutex>
+#include <tuple>
 #include <string>
 #include <utility>
 #include <vector>

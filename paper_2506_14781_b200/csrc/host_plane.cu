@@ -4,6 +4,38 @@
 
 namespace tgh {
 
+// Launch bound and co-resident blocks per SM of a kernel at `smem` dynamic
+// bytes (raising its dynamic shared-memory limit when needed), cached per
+// (device, kernel, threads, smem): the queries cost tens of microseconds and
+// set_problem runs once per e2e step.
+struct KernelFit {
+    int max_threads = 0, blocks_per_sm = 0;
+};
+static KernelFit kernel_fit(const void* fn, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, int, size_t>, KernelFit> cache;
+    static std::map<std::pair<int, const void*>, size_t> smem_set;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(dev, fn, threads, smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    KernelFit f;
+    cudaFuncAttributes fa{};
+    CK(cudaFuncGetAttributes(&fa, fn));
+    f.max_threads = fa.maxThreadsPerBlock;
+    if (threads <= 0) threads = f.max_threads;
+    size_t& have = smem_set[std::make_pair(dev, fn)];
+    if (smem > 48 * 1024 && smem > have) {
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        have = smem;
+    }
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f.blocks_per_sm, fn, threads, smem));
+    cache[key] = f;
+    return f;
+}
+
 bool plane_eligible(tg_ctx& c, std::string* why) {
     if (c.dev_prep) {
         if (c.prep.info & kPrepNotPM1) { if (why) *why = "couplings must be +-1"; return false; }
@@ -217,9 +249,7 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
     c.d_work.alloc((size_t)2 * c.n_colors * std::max(1, c.W));
     c.d_work.zero(st);
     // cooperative grid: a multiple of W warps, all blocks co-resident
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)plane_sweep_fn(c.cfg.rule, c.WV),
-                                                     kPlaneThreads, 0));
+    const int per_sm = kernel_fit((const void*)plane_sweep_fn(c.cfg.rule, c.WV), kPlaneThreads, 0).blocks_per_sm;
     if (per_sm < 1) fail(TG_ERR_RESOURCE, "plane engine: kernel does not fit on an SM");
     int blocks = per_sm * c.sms;
     const int passes = c.W / c.WV;
@@ -267,25 +297,15 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
     c.tpw_sweep_grid = 0;
     if (tpw_ok) {
         const void* fn = plane_tpw_sweep_fn(c.cfg.rule, c.tpw_fast);
-        cudaFuncAttributes fa{};
-        CK(cudaFuncGetAttributes(&fa, fn));
-        c.tpw_sweep_smem = tpw_smem_bytes(0, c.W, fa.maxThreadsPerBlock);
-        if (c.tpw_sweep_smem > 48 * 1024)
-            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.tpw_sweep_smem));
-        int fb = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fb, fn, fa.maxThreadsPerBlock, c.tpw_sweep_smem));
+        c.tpw_sweep_smem = tpw_smem_bytes(0, c.W, kernel_fit(fn, 0, 0).max_threads);
+        const int fb = kernel_fit(fn, 0, c.tpw_sweep_smem).blocks_per_sm;
         if (fb >= 1) c.tpw_sweep_grid = fb * c.sms;
     }
     if (c.fused_tpw) {
         const void* fn = plane_tpw_fn(c.cfg.rule, c.tpw_fast);
-        cudaFuncAttributes fa{};
-        CK(cudaFuncGetAttributes(&fa, fn));
-        c.fused_block = fa.maxThreadsPerBlock;  // the kernel's launch bound
+        c.fused_block = kernel_fit(fn, 0, 0).max_threads;  // the kernel's launch bound
         c.fused_smem = tpw_smem_bytes(c.R, c.W, c.fused_block);
-        if (c.fused_smem > 48 * 1024)
-            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.fused_smem));
-        int fb = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fb, fn, c.fused_block, c.fused_smem));
+        const int fb = kernel_fit(fn, c.fused_block, c.fused_smem).blocks_per_sm;
         if (fb >= 1) c.fused_grid = fb * c.sms;
         else c.fused_tpw = 0;
     }
@@ -300,10 +320,7 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
                                       ? 0 : std::max<size_t>(kTailCap * 7, (size_t)2 * c.W * 32);
         c.fused_smem = (size_t)c.R * (2 * sizeof(double) + 2 * sizeof(int32_t)) + 8 +
                        (size_t)(c.fused_block / 32) * std::max(pf_words, tail_words) * sizeof(int32_t);
-        if (c.fused_smem > 48 * 1024)
-            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.fused_smem));
-        int fb = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fb, fn, c.fused_block, c.fused_smem));
+        const int fb = kernel_fit(fn, c.fused_block, c.fused_smem).blocks_per_sm;
         if (fb >= 1) {
             int g = fb * c.sms;
             const int fp = c.fused_wv ? passes : 1;

@@ -12,9 +12,13 @@ import torch  # noqa: E402,F401  (NCCL / CUDA runtime first, as bench.py)
 from paper_2506_14781_b200 import instances as I  # noqa: E402
 from paper_2506_14781_b200.api import Engine, RunConfig  # noqa: E402
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20
+n = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 1 << 20
 t = time.perf_counter()
 pr = I.bipartite_3regular(n, seed=1)
+if "--pinned" in sys.argv:  # as bench.py's e2e leg
+    import numpy as np
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    pr = I.Problem(pr.n, pin(pr.ci), pin(pr.cj), pin(pr.cw), pin(pr.fields), pin(pr.pa), pin(pr.pb))
 betas, pens = I.config_schedule("c5")
 print(f"generate {1e3 * (time.perf_counter() - t):.1f} ms", flush=True)
 for rep in range(3):
