@@ -392,3 +392,72 @@ extern "C" int tgr_sparsify(int n, int n_couplings, const int* ci, const int* cj
         return -1;
     }
 }
+
+#ifndef TGREF_NO_SCHEDULE
+// ---- trace reports (analysis.cpp), pinned for paper_2506_14781_b200/reports.py
+
+// time_to_residual (analysis.cpp:260-270) over a flat (t, f, feasible) series;
+// *out = -1 when the threshold is never reached.
+extern "C" int tgr_time_to_residual(int n, const std::int64_t* t, const double* f, const int* feasible,
+                                    double e_gs, int n_logical, double rho_max, std::int64_t* out) {
+    try {
+        std::vector<tempergrid::EnergySample> s(n);
+        for (int i = 0; i < n; ++i) s[i] = tempergrid::EnergySample{t[i], f[i], feasible[i] != 0};
+        const auto r = tempergrid::time_to_residual(s, e_gs, n_logical, rho_max);
+        *out = r ? *r : -1;
+        return 0;
+    } catch (const tempergrid::config_error&) {
+        return 2;
+    } catch (...) {
+        return 4;
+    }
+}
+
+// residual_curve (analysis.cpp:38-96): runs x rounds target records (f,
+// feasible, state), the sparsification map (copy chains) and the logical
+// model; outputs t, rho_E and ci95 per round.
+extern "C" int tgr_residual_curve(int n_runs, int n_rounds, int n_phys, const std::int64_t* t,
+                                  const double* f, const int* feasible, const std::int8_t* states,
+                                  const double* e_gs, const int* instance_id, int n_logical,
+                                  const int* chain_off, const int* chain, int n_lc, const int* lci,
+                                  const int* lcj, const double* lw, const double* lh, int strict,
+                                  int resamples, std::uint64_t seed, std::int64_t* out_t,
+                                  double* out_rho, double* out_ci) {
+    try {
+        std::vector<tempergrid::Trace> traces(n_runs);
+        for (int r = 0; r < n_runs; ++r) {
+            traces[r].records.resize(n_rounds);
+            for (int k = 0; k < n_rounds; ++k) {
+                auto& rec = traces[r].records[k];
+                const size_t q = (size_t)r * n_rounds + k;
+                rec.sweep_count = t[k];
+                rec.f = f[q];
+                rec.feasible = feasible[q] != 0;
+                rec.state.assign(states + q * n_phys, states + (q + 1) * n_phys);
+            }
+        }
+        std::vector<tempergrid::ResidualInput> runs(n_runs);
+        for (int r = 0; r < n_runs; ++r) runs[r] = {&traces[r], e_gs[r], instance_id[r]};
+        tempergrid::SparsificationMap map;
+        map.n_logical = n_logical;
+        map.n_physical = n_phys;
+        map.copies.resize(n_logical);
+        for (int u = 0; u < n_logical; ++u) map.copies[u].assign(chain + chain_off[u], chain + chain_off[u + 1]);
+        std::vector<tempergrid::Coupling> cpl(n_lc);
+        for (int e = 0; e < n_lc; ++e) cpl[e] = {lci[e], lcj[e], lw[e]};
+        tempergrid::IsingModel logical(n_logical, cpl, std::vector<double>(lh, lh + n_logical));
+        const auto curve = tempergrid::residual_curve(runs, map, logical, n_logical, strict != 0,
+                                                      resamples, seed);
+        for (int k = 0; k < n_rounds; ++k) {
+            out_t[k] = curve.points[k].t;
+            out_rho[k] = curve.points[k].rho_e;
+            out_ci[k] = curve.points[k].ci95;
+        }
+        return 0;
+    } catch (const tempergrid::config_error&) {
+        return 2;
+    } catch (...) {
+        return 4;
+    }
+}
+#endif
