@@ -402,8 +402,15 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         r.cnt = c.d_cnt2.p; r.cnt_stride = c.W * 32;
         // testing knob: flush the tpw kernel's vertical counters more often
         if (const char* e = std::getenv("TG_TPW_FLUSH_EVERY")) r.flush_every = std::atoi(e);
-        // dynamic chunk grabbing measured 3% slower than the static split (r1); opt in
+        // old kernel: dynamic chunk grabbing measured 3% slower than the static
+        // split (r1), opt in; tpw kernel: the last ~item per warp is handed
+        // out dynamically ([2 parities][colours][sps] counters)
         r.work = (std::getenv("TG_PLANE_DYNAMIC") ? c.d_work.p : nullptr);
+        if (c.fused_tpw && c.tpw_fast) {
+            const size_t need = (size_t)2 * c.n_colors * c.cfg.sweeps_per_swap;
+            if (c.d_work.n < need) { c.d_work.alloc(need); c.d_work.zero(st); }
+            r.work = std::getenv("TG_TPW_STATIC") ? nullptr : c.d_work.p;
+        }
         r.ktab = c.d_ktab.p; r.ktab_row = c.ktab_row; r.kp = c.d_kp.p; r.kpc = c.d_kpc.p;
         r.rec = c.d_rec.p; r.rec_acc = c.d_rec_acc.p;
         r.rec_states = (flags & TG_REC_STATE) ? c.d_rec_states.p : nullptr;

@@ -601,7 +601,7 @@ __device__ __forceinline__ void c5_site(const PlaneArgs& a, const C5K& K, int ty
 template <int RULE>
 __device__ __forceinline__ void tpw_phase_c5(const PlaneArgs& a, int c, uint64_t t, bool count,
                                              int gw, int nw, int logW, uint32_t (&Vc)[kVB],
-                                             int flush_every) {
+                                             int flush_every, int* work = nullptr) {
     int* s_cc = tpw_sm + kTpwSmCnt;
     int* s_cq = s_cc + 32 * a.W;
     uint32_t* vq = reinterpret_cast<uint32_t*>(tpw_sm + kTpwSmVq) + threadIdx.x;
@@ -661,10 +661,23 @@ __device__ __forceinline__ void tpw_phase_c5(const PlaneArgs& a, int c, uint64_t
         e = make_int4(0, 0, 0, (int)0x80000000u);
         if (it < n_it && site < ce) e = __ldg(a.nbr4 + site);  // one 16-byte load
     };
-    int item = gw;
+    // Static strided items for all but about one item per warp; the tail is
+    // handed out by a per-phase counter (work != nullptr), so warps that
+    // finish early take the remaining items instead of idling at the barrier.
+    const int n_static = work ? (n_it / nw - 1 > 0 ? (n_it / nw - 1) * nw : 0) : n_it;
+    const int lane_ = threadIdx.x & 31;
+    auto next_of = [&](int it) {
+        const int nx = it + nw;
+        if (nx < n_static || !work) return nx;
+        int v = 0;
+        if (lane_ == 0) v = n_static + atomicAdd(work, 1);
+        return __shfl_sync(0xffffffffu, v, 0);
+    };
+    int item = gw < n_static ? gw : next_of(gw - nw);
     int4 en;
     entries(item, en);
-    for (; item < n_it; item += nw) {
+    for (int nxt; item < n_it; item = nxt) {
+        nxt = next_of(item);
         const int4 e = en;
         const uint32_t site = (uint32_t)(cs + item * S + sl);
         const bool valid = (int)site < ce;
@@ -678,7 +691,7 @@ __device__ __forceinline__ void tpw_phase_c5(const PlaneArgs& a, int c, uint64_t
             R.x2 = sp[(uint32_t)e.z & 0x7fffffffu];
             if (hasq) R.y0 = sp[(uint32_t)e.w];
         }
-        entries(item + nw, en);
+        entries(nxt, en);
         // one call site per path; both run (complementary lanes) only when
         // the item straddles the chain-free / chain boundary
         const bool v0 = valid && !hasq;
@@ -838,7 +851,9 @@ plane_tpw_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_consta
             const uint64_t t = (uint64_t)((round - 1) * r.sps + sw);
             const bool count = (sw == r.sps - 1);
             for (int c = 0; c < a.n_colors; ++c) {
-                if constexpr (FAST) tpw_phase_c5<RULE>(a, c, t, count, gw, nw, logW, Vc, flush_every);
+                if constexpr (FAST)
+                    tpw_phase_c5<RULE>(a, c, t, count, gw, nw, logW, Vc, flush_every,
+                                       r.work ? r.work + (size_t)(par * a.n_colors + c) * r.sps + sw : nullptr);
                 else tpw_phase<RULE, FAST>(a, c, t, count, gw, nw, logW, Vc, flush_every);
                 TPW_STAMP(k, 1 + 3 * (c & 1));
                 TPW_MAXSTAMP(k, 2 + 3 * (c & 1));
@@ -854,7 +869,7 @@ plane_tpw_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_consta
                 TPW_STAMP(k, 3 + 3 * (c & 1));
             }
         }
-        round_epilogue(a, r, s, k, round, cc, cq, swap_base, 0);
+        round_epilogue(a, r, s, k, round, cc, cq, swap_base, a.n_colors * r.sps);
         TPW_STAMP(k, 7);
     }
 }
