@@ -62,6 +62,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #include "plane_round.cuh"
 namespace tg {
 
+#ifndef TG_TPW_DYN_K
+#define TG_TPW_DYN_K 1
+#endif
+constexpr int kTpwDynK = TG_TPW_DYN_K;  // items per warp left to the dynamic tail
 constexpr int kVB = kTpwVB;  // planes of the per-thread vertical bond counters (max 255)
 
 // V += m (NB-bit bit-sliced value) in kVB-bit vertical arithmetic.
@@ -664,7 +668,7 @@ __device__ __forceinline__ void tpw_phase_c5(const PlaneArgs& a, int c, uint64_t
     // Static strided items for all but about one item per warp; the tail is
     // handed out by a per-phase counter (work != nullptr), so warps that
     // finish early take the remaining items instead of idling at the barrier.
-    const int n_static = work ? (n_it / nw - 1 > 0 ? (n_it / nw - 1) * nw : 0) : n_it;
+    const int n_static = work ? (n_it / nw - kTpwDynK > 0 ? (n_it / nw - kTpwDynK) * nw : 0) : n_it;
     const int lane_ = threadIdx.x & 31;
     auto next_of = [&](int it) {
         const int nx = it + nw;
