@@ -172,3 +172,12 @@ def test_unfused_round_loop_thread_per_site_kernel(monkeypatch):
     monkeypatch.setenv("TG_PLANE_TPW", "0")
     b, p = sched(16, 16)
     assert run_grid_records(C5S, b, p, 10, "metropolis", 4) == "plane_sweep_kernel"
+
+
+@pytest.mark.parametrize("rule", ["metropolis", "heat_bath"])
+def test_config5_path_several_sweeps_per_round(rule):
+    # the dynamic-tail counters are per (parity, colour, sweep of the round)
+    pr = I.bipartite_3regular(1 << 14, seed=12)
+    b, p = sched(16, 16)
+    compare(pr, b, p, 3 * 8, 3, seed=5, rule=rule, engine="plane")
+    assert kernel_of(pr, b, p, rule) == "plane_tpw_rounds_kernel"
