@@ -311,15 +311,12 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
     }
     if (!c.fused_tpw && c.world == 1 && c.R <= 2048) {
         c.fused_wv = c.WV;
-        if (const char* e = std::getenv("TG_PLANE_LOOP")) if (std::atoi(e)) c.fused_wv = 0;
         const void* fn = plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast);
         c.fused_block = c.fused_fast ? kPlaneThreadsFast : kPlaneThreads;
         const size_t pf_words = c.fused_fast && (c.fused_wv == 4 || c.fused_wv == 2)
                                     ? (size_t)2 * (5 * 32 * c.fused_wv + 4 * 32) : 0;
-        const size_t tail_words = c.fused_fast && (c.fused_wv == 4 || c.fused_wv == 2)
-                                      ? 0 : std::max<size_t>(kTailCap * 7, (size_t)2 * c.W * 32);
         c.fused_smem = (size_t)c.R * (2 * sizeof(double) + 2 * sizeof(int32_t)) + 8 +
-                       (size_t)(c.fused_block / 32) * std::max(pf_words, tail_words) * sizeof(int32_t);
+                       (size_t)(c.fused_block / 32) * pf_words * sizeof(int32_t);
         const int fb = kernel_fit(fn, c.fused_block, c.fused_smem).blocks_per_sm;
         if (fb >= 1) {
             int g = fb * c.sms;
@@ -402,10 +399,9 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         r.cnt = c.d_cnt2.p; r.cnt_stride = c.W * 32;
         // testing knob: flush the tpw kernel's vertical counters more often
         if (const char* e = std::getenv("TG_TPW_FLUSH_EVERY")) r.flush_every = std::atoi(e);
-        // old kernel: dynamic chunk grabbing measured 3% slower than the static
-        // split (r1), opt in; tpw kernel: the last ~item per warp is handed
+        // tpw kernel: the last ~item per warp of each colour phase is handed
         // out dynamically ([2 parities][colours][sps] counters)
-        r.work = (std::getenv("TG_PLANE_DYNAMIC") ? c.d_work.p : nullptr);
+        r.work = nullptr;
         if (c.fused_tpw && c.tpw_fast) {
             const size_t need = (size_t)2 * c.n_colors * c.cfg.sweeps_per_swap;
             if (c.d_work.n < need) { c.d_work.alloc(need); c.d_work.zero(st); }

@@ -13,7 +13,6 @@ namespace tg {
 constexpr int kPlaneThreads = 512;
 constexpr int kPlaneThreadsFast = 512;
 constexpr int kPlaneMinBlocksFast = 1;
-constexpr int kPlaneMinBlocksLoop = 2;   // looped-row variant: 2 x 512 threads per SM
 #ifndef TG_TPW_THREADS
 #define TG_TPW_THREADS 512
 #endif
@@ -37,7 +36,6 @@ inline size_t tpw_smem_bytes(int R, int W, int threads) {
 }
 constexpr int kSlotThreads = 256;
 constexpr int kSwapThreads = 1024;
-constexpr int kTailCap = 160;   // per-warp deferred-tail queue entries (plane_sweep.cu)
 
 // Device image of tg_record (same layout as the C-ABI struct).
 struct TgRecordDev {

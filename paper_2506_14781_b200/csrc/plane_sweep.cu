@@ -25,169 +25,16 @@ namespace cg = cooperative_groups;
 
 namespace tg {
 
-// Deferred tail of the lazy threshold comparison.  After the two
-// unconditional Philox blocks (8 planes) a (site, word) still has undecided
-// lanes with probability ~2^-8 per lane; instead of running the whole warp
-// through further blocks for the few that need them, such words are queued
-// per warp (shared memory) and resolved 32 at a time, one per thread.
-// kTailCap (kernels.cuh) = 160 > 31 queued before a site + 4 words x 32 lanes.
-// Measured r1: the deferred tail saves ~1.1 Philox blocks per word but its
-// drains (re-loads, per-lane threshold look-ups, call spills) cost more on
-// B200 than they save (1.10e12 vs 1.29e12 flips/s); kept behind kPlaneTail.
-#ifndef TG_PLANE_TAIL
-#define TG_PLANE_TAIL 0
-#endif
-constexpr int kPlaneTail = TG_PLANE_TAIL;
-// In-warp compaction of undecided (site, word) pairs in the FAST/prefetch path.
-#ifndef TG_PF_TAIL
-#define TG_PF_TAIL 2
-#endif
-constexpr int kPfTail = TG_PF_TAIL;
-struct TailQ {
-    int* site;
-    int* word;       // local word index
-    int* type;
-    int* nbr_off;    // offset of the site's neighbour list in a.nbr
-    uint32_t* und;   // lanes still undecided after 8 planes
-    uint32_t* s;     // configuration word before the update
-    uint32_t* nsp;   // provisional new word (undecided lanes not taken)
-};
-
-__device__ __forceinline__ TailQ tail_view(char* base, int warp) {
-    char* p = base + (size_t)warp * kTailCap * 7 * sizeof(int);
-    TailQ q;
-    q.site = reinterpret_cast<int*>(p);
-    q.word = q.site + kTailCap;
-    q.type = q.word + kTailCap;
-    q.nbr_off = q.type + kTailCap;
-    q.und = reinterpret_cast<uint32_t*>(q.nbr_off + kTailCap);
-    q.s = q.und + kTailCap;
-    q.nsp = q.s + kTailCap;
-    return q;
-}
-
-// Resolve queued words (all of them when flush, else while >= 32 remain).
-// Decisions are identical to running the lazy loop in place: same planes,
-// same thresholds (ktab, host-computed), same order of planes per lane.
-template <int RULE>
-__device__ __noinline__ int tail_drain(const PlaneArgs& a, TailQ q, int qn, uint64_t t, bool count,
-                                       int lower, int32_t* cnt_c, int32_t* cnt_q, bool flush) {
-    const int lane = threadIdx.x & 31;
-    __syncwarp();
-    while (qn >= 32 || (flush && qn > 0)) {
-        const int n = qn < 32 ? qn : 32;
-        const int e = qn - n + lane;
-        const bool mine = lane < n;
-        int site = 0, w = 0, nbo = 0;
-        uint32_t und = 0, s = 0, nsp = 0;
-        PlaneType ty = a.ty[0];
-        if (mine) {
-            site = q.site[e]; w = q.word[e]; nbo = q.nbr_off[e];
-            und = q.und[e]; s = q.s[e]; nsp = q.nsp[e];
-            ty = a.ty[q.type[e]];
-        }
-        // neighbour words (unchanged during this colour phase) and class bits
-        uint32_t x[kMaxDC], y[kMaxDQ];
-        uint32_t c3[3] = {0u, 0u, 0u}, q2[2] = {0u, 0u};
-        uint32_t lowx = 0, lowy = 0;
-#pragma unroll
-        for (int k = 0; k < kMaxDC; ++k) {
-            x[k] = 0u;
-            if (mine && k < ty.dc) {
-                const int32_t ev = __ldg(a.nbr + nbo + k);
-                const int j = ev & 0x7fffffff;
-                x[k] = a.spins[(size_t)j * a.W + w] ^ (ev < 0 ? 0xffffffffu : 0u);
-                lowx |= (uint32_t)(j < lower) << k;
-                bs_add<3>(c3, RULE == 0 ? ~(s ^ x[k]) : x[k]);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < kMaxDQ; ++k) {
-            y[k] = 0u;
-            if (mine && k < ty.dq) {
-                const int j = __ldg(a.nbr + nbo + ty.dc + k);
-                y[k] = a.spins[(size_t)j * a.W + w];
-                lowy |= (uint32_t)(j < lower) << k;
-                bs_add<2>(q2, RULE == 0 ? ~(s ^ y[k]) : y[k]);
-            }
-        }
-        const uint32_t grp4 = (uint32_t)(a.w_global0 + w) << 4;
-        const uint32_t thi = (uint32_t)(t >> 32), tlo = (uint32_t)t;
-        uint32_t rest = und, extra = 0;
-        // up to 4 undecided lanes per pass, each with its 53-bit threshold
-        while (__any_sync(0xffffffffu, rest)) {
-            uint64_t K[4] = {0ull, 0ull, 0ull, 0ull};
-            uint32_t bit[4] = {0u, 0u, 0u, 0u};
-            uint32_t pu = 0;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (rest) {
-                    const int l = __ffs(rest) - 1;
-                    rest &= rest - 1;
-                    const uint32_t cls =
-                        (((c3[0] >> l) & 1u) | (((c3[1] >> l) & 1u) << 1) | (((c3[2] >> l) & 1u) << 2)) |
-                        ((((q2[0] >> l) & 1u) | (((q2[1] >> l) & 1u) << 1)) << ty.ncb);
-                    const int slot = a.state_slot[a.w_global0 * 32 + w * 32 + l];
-                    K[j] = __ldg(a.ktab + (size_t)slot * a.ktab_row + ty.ktab_off + cls);
-                    bit[j] = 1u << l;
-                    pu |= bit[j];
-                }
-            }
-            uint32_t lt = 0;
-#pragma unroll 1
-            for (int blk = 2; blk < 14; ++blk) {
-                if (!__any_sync(0xffffffffu, pu)) break;
-                const u32x4 r = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | (uint32_t)blk},
-                                                 a.pks);
-                const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-                for (int qq = 0; qq < 4; ++qq) {
-                    const int b = blk * 4 + qq;
-                    if (b < kKPlanes) {
-                        uint32_t tb = 0;
-#pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            if ((K[j] >> (52 - b)) & 1ull) tb |= bit[j];
-                        lt |= pu & tb & ~rr[qq];
-                        pu &= ~(tb ^ rr[qq]);
-                    }
-                }
-            }
-            extra |= lt;
-        }
-        if (mine && extra) {
-            uint32_t* word = a.spins + (size_t)site * a.W + w;
-            *word = RULE == 0 ? (*word ^ extra) : (*word | extra);
-            if (count) {
-                // bonds to lower-colour neighbours toggle satisfaction for taken lanes
-                uint32_t ex = extra;
-                while (ex) {
-                    const int l = __ffs(ex) - 1;
-                    ex &= ex - 1;
-                    int dcnt = 0, dqnt = 0;
-#pragma unroll
-                    for (int k = 0; k < kMaxDC; ++k)
-                        if (k < ty.dc && ((lowx >> k) & 1u)) dcnt += 1 - 2 * (int)(((nsp ^ x[k]) >> l) & 1u);
-#pragma unroll
-                    for (int k = 0; k < kMaxDQ; ++k)
-                        if (k < ty.dq && ((lowy >> k) & 1u)) dqnt += 1 - 2 * (int)(((nsp ^ y[k]) >> l) & 1u);
-                    if (dcnt) atomicAdd(cnt_c + w * 32 + l, dcnt);
-                    if (dqnt) atomicAdd(cnt_q + w * 32 + l, dqnt);
-                }
-            }
-        }
-        qn -= n;
-        __syncwarp();
-    }
-    return qn;
-}
+// In-warp compaction of undecided (site, word) pairs in the FAST/prefetch path
+// (TAIL = 2 below; TAIL = 0: each word runs its own lazy loop).
+constexpr int kPfTail = 2;
 
 // One thread = one site of the chunk; all WV words (32 replicas each) of the
 // site row [wb, wb+WV) are loaded as one vector, updated, stored back.
 template <int NCB, int NQB, int RULE, int WV, int TAIL, int PF = 0>
 __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, const PlaneType& ty,
                                            int wb, uint64_t t, bool count, int lower,
-                                           int (&acc_c)[WV], int (&acc_q)[WV], TailQ& tq, int& qn,
+                                           int (&acc_c)[WV], int (&acc_q)[WV],
                                            const uint32_t* pfrow = nullptr,
                                            const int32_t* pfidx = nullptr) {
     constexpr int DCM = (1 << NCB) - 1;
@@ -425,7 +272,7 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
             compare_block<B>(cb, kpb, ncl, 0, r0, und, lt);
             compare_block<B>(cb, kpb, ncl, 1, r1, und, lt);
         }
-        if constexpr (!TAIL) {
+        {
 #pragma unroll 1
             for (int blk = 2; blk < 14; ++blk) {
                 if (!__any_sync(0xffffffffu, und)) break;
@@ -436,23 +283,6 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
         }
         const uint32_t take = (always | lt) & act;
         ns[w] = RULE == 0 ? (s[w] ^ take) : ((s[w] & ~act) | take);
-        if constexpr (TAIL) {
-            // queue words with undecided lanes; their provisional word does not take them
-            const uint32_t need = __ballot_sync(0xffffffffu, und != 0u);
-            if (need) {
-                if (und) {
-                    const int pos = qn + __popc(need & ((1u << lane) - 1u));
-                    tq.site[pos] = site;
-                    tq.word[pos] = wb + w;
-                    tq.type[pos] = ch.type;
-                    tq.nbr_off[pos] = ch.nbr_base + lane * deg;
-                    tq.und[pos] = und;
-                    tq.s[pos] = s[w];
-                    tq.nsp[pos] = ns[w];
-                }
-                qn += __popc(need);
-            }
-        }
         if (count) {
             // unsatisfied bonds to lower-colour neighbours, counted once per
             // edge at its higher-colour endpoint, summed per replica lane.
@@ -493,10 +323,10 @@ __device__ __forceinline__ void plane_site(const PlaneArgs& a, const Chunk& ch, 
 template <int RULE, int WV, int FAST, int TAIL>
 __device__ __forceinline__ void plane_dispatch(const PlaneArgs& a, const Chunk& ch, int wb,
                                                uint64_t t, bool count, int lower,
-                                               int (&acc_c)[WV], int (&acc_q)[WV], TailQ& tq, int& qn) {
+                                               int (&acc_c)[WV], int (&acc_q)[WV]) {
     const PlaneType& ty = a.ty[ch.type];
 #define TG_CASE(C, Q) \
-    case (C) * 4 + (Q): plane_site<C, Q, RULE, WV, TAIL>(a, ch, ty, wb, t, count, lower, acc_c, acc_q, tq, qn); break;
+    case (C) * 4 + (Q): plane_site<C, Q, RULE, WV, TAIL>(a, ch, ty, wb, t, count, lower, acc_c, acc_q); break;
     if constexpr (FAST) {
         switch (ty.ncb * 4 + ty.nqb) {
             TG_CASE(0, 0) TG_CASE(0, 1)
@@ -517,10 +347,10 @@ __device__ __forceinline__ void plane_dispatch(const PlaneArgs& a, const Chunk& 
 
 // One colour phase of one sweep over this warp's items; unsatisfied-bond
 // counts (last sweep of a round) go to cnt_c/cnt_q.
-template <int RULE, int WV, int FAST, int TAIL>
+template <int RULE, int WV, int FAST>
 __device__ __forceinline__ void plane_phase(const PlaneArgs& a, int c, uint64_t t, bool count,
                                             int gidx, int ngroups, int wb,
-                                            int32_t* cnt_c, int32_t* cnt_q, TailQ& tq) {
+                                            int32_t* cnt_c, int32_t* cnt_q) {
     int acc_c[WV], acc_q[WV];
 #pragma unroll
     for (int w = 0; w < WV; ++w) { acc_c[w] = 0; acc_q[w] = 0; }
@@ -528,13 +358,10 @@ __device__ __forceinline__ void plane_phase(const PlaneArgs& a, int c, uint64_t 
     const int n_chunks = a.chunk_off[c + 1] - c0;
     const int lower = a.color_start[c];
     count = count && lower > 0;  // colour 0 has no lower-colour neighbours: nothing to count
-    int qn = 0;
     for (int item = gidx; item < n_chunks; item += ngroups) {
         const Chunk ch = a.chunks[c0 + item];
-        plane_dispatch<RULE, WV, FAST, TAIL>(a, ch, wb, t, count, lower, acc_c, acc_q, tq, qn);
-        if (TAIL && qn >= 32) qn = tail_drain<RULE>(a, tq, qn, t, count, lower, cnt_c, cnt_q, false);
+        plane_dispatch<RULE, WV, FAST, 0>(a, ch, wb, t, count, lower, acc_c, acc_q);
     }
-    if (TAIL && qn > 0) tail_drain<RULE>(a, tq, qn, t, count, lower, cnt_c, cnt_q, true);
     if (count) {
         const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -560,7 +387,7 @@ __host__ __device__ constexpr int pf_stage_words() { return kPfRows * 32 * WV + 
 template <int RULE, int WV>
 __device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64_t t, bool count,
                                                int gidx, int ngroups, int wb, int32_t* cnt_c,
-                                               int32_t* cnt_q, uint32_t* pf, int* work) {
+                                               int32_t* cnt_q, uint32_t* pf) {
     constexpr int kStage = pf_stage_words<WV>();
     int acc_c[WV], acc_q[WV];
 #pragma unroll
@@ -571,8 +398,6 @@ __device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64
     count = count && lower > 0;
     const int lane = threadIdx.x & 31;
     const int Wp = a.W;
-    TailQ tq{};
-    int qn = 0;
     auto issue = [&](int item, int stage) {
         const Chunk ch = a.chunks[c0 + item];
         const PlaneType& ty = a.ty[ch.type];
@@ -592,19 +417,12 @@ __device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64
         __pipeline_commit();
         return ch;
     };
-    // dynamic chunk distribution: warps of this pass grab chunks from a
-    // global counter (balances the colour phase before the grid barrier)
-    auto grab = [&]() {
-        int v = 0;
-        if (lane == 0) v = work ? atomicAdd(work, 1) : 0;
-        return work ? __shfl_sync(0xffffffffu, v, 0) : 0;
-    };
-    int item = work ? grab() : gidx;
+    int item = gidx;
     Chunk cur{};
     if (item < n_chunks) cur = issue(item, 0);
     int k = 0;
     while (item < n_chunks) {
-        const int nxt = work ? grab() : item + ngroups;
+        const int nxt = item + ngroups;
         Chunk next{};
         if (nxt < n_chunks) next = issue(nxt, (k + 1) & 1);
         else __pipeline_commit();
@@ -614,12 +432,12 @@ __device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64
         const int32_t* idx = reinterpret_cast<const int32_t*>(rows + kPfRows * 32 * WV);
         const PlaneType& ty = a.ty[cur.type];
         switch (ty.ncb * 4 + ty.nqb) {
-            case 0 * 4 + 0: plane_site<0, 0, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
-            case 0 * 4 + 1: plane_site<0, 1, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
-            case 1 * 4 + 0: plane_site<1, 0, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
-            case 1 * 4 + 1: plane_site<1, 1, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
-            case 2 * 4 + 0: plane_site<2, 0, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
-            case 2 * 4 + 1: plane_site<2, 1, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, tq, qn, rows, idx); break;
+            case 0 * 4 + 0: plane_site<0, 0, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, rows, idx); break;
+            case 0 * 4 + 1: plane_site<0, 1, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, rows, idx); break;
+            case 1 * 4 + 0: plane_site<1, 0, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, rows, idx); break;
+            case 1 * 4 + 1: plane_site<1, 1, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, rows, idx); break;
+            case 2 * 4 + 0: plane_site<2, 0, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, rows, idx); break;
+            case 2 * 4 + 1: plane_site<2, 1, RULE, WV, kPfTail, 1>(a, cur, ty, wb, t, count, lower, acc_c, acc_q, rows, idx); break;
             default: break;
         }
         __syncwarp();
@@ -635,174 +453,6 @@ __device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64
             if (m < a.local_states) {
                 if (acc_c[w]) atomicAdd(cnt_c + m, acc_c[w]);
                 if (acc_q[w]) atomicAdd(cnt_q + m, acc_q[w]);
-            }
-        }
-    }
-}
-
-// Looped variant (WV == 0): one thread = one site for ALL words of its row,
-// words processed one at a time (#pragma unroll 1).  Neighbour indices are
-// loaded once per site; per-word row words are 4-byte loads that hit L1 after
-// the first word touches the row's sector.  Far fewer live registers than the
-// vector-row variant; energy counts go to a per-warp shared-memory accumulator.
-template <int NCB, int NQB, int RULE>
-__device__ __forceinline__ void plane_site_loop(const PlaneArgs& a, const Chunk& ch,
-                                                const PlaneType& ty, uint64_t t, bool count,
-                                                int lower, int* sacc_c, int* sacc_q) {
-    constexpr int DCM = (1 << NCB) - 1;
-    constexpr int DQM = (1 << NQB) - 1;
-    constexpr int B = NCB + NQB;
-    const int lane = threadIdx.x & 31;
-    const int dc = ty.dc, dq = ty.dq, deg = dc + dq;
-    const bool valid = lane < ch.len;
-    const int site = ch.start + lane;
-    const int Wp = a.W;
-    int jx[DCM > 0 ? DCM : 1], jy[DQM > 0 ? DQM : 1];
-    uint32_t negx = 0, lowx = 0, lowy = 0;
-#pragma unroll
-    for (int k = 0; k < DCM; ++k) {
-        jx[k] = site;
-        if (valid && k < dc) {
-            const int32_t e = __ldg(a.nbr + ch.nbr_base + lane * deg + k);
-            jx[k] = e & 0x7fffffff;
-            negx |= (uint32_t)(e < 0) << k;
-            lowx |= (uint32_t)(jx[k] < lower) << k;
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < DQM; ++k) {
-        jy[k] = site;
-        if (valid && k < dq) {
-            jy[k] = __ldg(a.nbr + ch.nbr_base + lane * deg + dc + k);
-            lowy |= (uint32_t)(jy[k] < lower) << k;
-        }
-    }
-    const int ncl = ty.ncl;
-    const bool pruned = (RULE == 0 && NQB == 0 && NCB == 2 && dc == 3);
-    const uint32_t thi = (uint32_t)(t >> 32), tlo = (uint32_t)t;
-    const uint32_t* srow = a.spins + (size_t)site * Wp;
-#pragma unroll 1
-    for (int w = 0; w < Wp; ++w) {
-        const uint32_t act = valid ? a.active[w] : 0u;
-        if (!__any_sync(0xffffffffu, act)) break;  // padding words
-        uint32_t s = 0u, x[DCM > 0 ? DCM : 1], y[DQM > 0 ? DQM : 1];
-        uint32_t cb[B > 0 ? B : 1];
-#pragma unroll
-        for (int b = 0; b < (B > 0 ? B : 1); ++b) cb[b] = 0u;
-        if (valid) s = srow[w];
-#pragma unroll
-        for (int k = 0; k < DCM; ++k) {
-            x[k] = 0u;
-            if (valid && k < dc) {
-                x[k] = a.spins[(size_t)jx[k] * Wp + w] ^ (((negx >> k) & 1u) ? 0xffffffffu : 0u);
-                bs_add<NCB>(cb, RULE == 0 ? ~(s ^ x[k]) : x[k]);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < DQM; ++k) {
-            y[k] = 0u;
-            if (valid && k < dq) {
-                y[k] = a.spins[(size_t)jy[k] * Wp + w];
-                bs_add<NQB>(cb + NCB, RULE == 0 ? ~(s ^ y[k]) : y[k]);
-            }
-        }
-        const uint32_t* kpb = a.kp + (size_t)w * a.kpw + ty.kp_off;
-        const uint32_t always = mux_tree<B>(cb, kpb + kKPlanes * ncl) & act;
-        uint32_t und = act & ~always;
-        uint32_t lt = 0;
-        const uint32_t grp4 = (uint32_t)(a.w_global0 + w) << 4;
-        const u32x4 r0 = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | 0u}, a.pks);
-        const u32x4 r1 = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | 1u}, a.pks);
-        if (pruned) {
-            compare_block_sel(cb[0], kpb + 2, ncl, 0, r0, und, lt);
-            compare_block_sel(cb[0], kpb + 2, ncl, 1, r1, und, lt);
-        } else {
-            compare_block<B>(cb, kpb, ncl, 0, r0, und, lt);
-            compare_block<B>(cb, kpb, ncl, 1, r1, und, lt);
-        }
-#pragma unroll 1
-        for (int blk = 2; blk < 14; ++blk) {
-            if (!__any_sync(0xffffffffu, und)) break;
-            const u32x4 r = philox4x32_10_ks(u32x4{(uint32_t)site, tlo, thi, grp4 | (uint32_t)blk}, a.pks);
-            if (pruned) compare_block_sel(cb[0], kpb + 2, ncl, blk, r, und, lt);
-            else compare_block<B>(cb, kpb, ncl, blk, r, und, lt);
-        }
-        const uint32_t take = (always | lt) & act;
-        const uint32_t ns = RULE == 0 ? (s ^ take) : ((s & ~act) | take);
-        if (valid) a.spins[(size_t)site * Wp + w] = ns;
-        if (count) {
-            if constexpr (NCB > 0) {
-                uint32_t m[NCB];
-#pragma unroll
-                for (int b = 0; b < NCB; ++b) m[b] = 0u;
-#pragma unroll
-                for (int k = 0; k < DCM; ++k)
-                    if (k < dc && ((lowx >> k) & 1u)) bs_add<NCB>(m, (ns ^ x[k]) & act);
-                int tot = 0;
-#pragma unroll
-                for (int b = 0; b < NCB; ++b)
-                    if (__any_sync(0xffffffffu, m[b])) tot += __popc(warp_transpose32(m[b])) << b;
-                if (tot) sacc_c[w * 32 + lane] += tot;
-            }
-            if constexpr (NQB > 0) {
-                uint32_t m[NQB];
-#pragma unroll
-                for (int b = 0; b < NQB; ++b) m[b] = 0u;
-#pragma unroll
-                for (int k = 0; k < DQM; ++k)
-                    if (k < dq && ((lowy >> k) & 1u)) bs_add<NQB>(m, (ns ^ y[k]) & act);
-                int tot = 0;
-#pragma unroll
-                for (int b = 0; b < NQB; ++b)
-                    if (__any_sync(0xffffffffu, m[b])) tot += __popc(warp_transpose32(m[b])) << b;
-                if (tot) sacc_q[w * 32 + lane] += tot;
-            }
-        }
-    }
-}
-
-template <int RULE, int FAST>
-__device__ __forceinline__ void plane_phase_loop(const PlaneArgs& a, int c, uint64_t t, bool count,
-                                                 int gidx, int ngroups, int32_t* cnt_c,
-                                                 int32_t* cnt_q, int* sacc) {
-    const int c0 = a.chunk_off[c];
-    const int n_chunks = a.chunk_off[c + 1] - c0;
-    const int lower = a.color_start[c];
-    count = count && lower > 0;
-    const int lane = threadIdx.x & 31;
-    int* sacc_c = sacc;
-    int* sacc_q = sacc + a.W * 32;
-    if (count)
-        for (int w = 0; w < a.W; ++w) { sacc_c[w * 32 + lane] = 0; sacc_q[w * 32 + lane] = 0; }
-    for (int item = gidx; item < n_chunks; item += ngroups) {
-        const Chunk ch = a.chunks[c0 + item];
-        const PlaneType& ty = a.ty[ch.type];
-#define TG_LCASE(C, Q) \
-        case (C) * 4 + (Q): plane_site_loop<C, Q, RULE>(a, ch, ty, t, count, lower, sacc_c, sacc_q); break;
-        if constexpr (FAST) {
-            switch (ty.ncb * 4 + ty.nqb) {
-                TG_LCASE(0, 0) TG_LCASE(0, 1)
-                TG_LCASE(1, 0) TG_LCASE(1, 1) TG_LCASE(2, 0) TG_LCASE(2, 1)
-                default: break;
-            }
-        } else {
-            switch (ty.ncb * 4 + ty.nqb) {
-                TG_LCASE(0, 0) TG_LCASE(0, 1) TG_LCASE(0, 2)
-                TG_LCASE(1, 0) TG_LCASE(1, 1) TG_LCASE(1, 2)
-                TG_LCASE(2, 0) TG_LCASE(2, 1) TG_LCASE(2, 2)
-                TG_LCASE(3, 0) TG_LCASE(3, 1) TG_LCASE(3, 2)
-                default: break;
-            }
-        }
-#undef TG_LCASE
-    }
-    if (count) {
-        __syncwarp();
-        for (int w = 0; w < a.W; ++w) {
-            const int m = w * 32 + lane;
-            if (m < a.local_states) {
-                if (sacc_c[m]) atomicAdd(cnt_c + m, sacc_c[m]);
-                if (sacc_q[m]) atomicAdd(cnt_q + m, sacc_q[m]);
             }
         }
     }
@@ -826,8 +476,7 @@ plane_sweep_kernel(const __grid_constant__ PlaneArgs a, int64_t t0, int n_sweeps
         const uint64_t t = (uint64_t)(t0 + sw);
         const bool count = (sw == n_sweeps - 1);
         for (int c = 0; c < a.n_colors; ++c) {
-            TailQ tq{};
-            plane_phase<RULE, WV, 0, 0>(a, c, t, count, gidx, ngroups, wb, a.cnt_c, a.cnt_q, tq);
+            plane_phase<RULE, WV, 0>(a, c, t, count, gidx, ngroups, wb, a.cnt_c, a.cnt_q);
             grid.sync();
         }
     }
@@ -852,8 +501,7 @@ plane_sweep_kernel(const __grid_constant__ PlaneArgs a, int64_t t0, int n_sweeps
 // more grid barrier closes the round.
 template <int RULE, int WV, int FAST>
 __global__ void __launch_bounds__(FAST ? kPlaneThreadsFast : kPlaneThreads,
-                                  WV == 0 ? kPlaneMinBlocksLoop
-                                          : (FAST ? (WV == 2 ? 2 : kPlaneMinBlocksFast) : 1))
+                                  FAST ? (WV == 2 ? 2 : kPlaneMinBlocksFast) : 1)
 plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__ RoundArgs r) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double sm_d[];
@@ -861,16 +509,14 @@ plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__
     double* s_g = sm_d + r.R;
     int32_t* s_slot = reinterpret_cast<int32_t*>(sm_d + 2 * r.R);
     int32_t* s_state = s_slot + r.R;
-    char* sm_tail = reinterpret_cast<char*>(s_state + r.R + (r.R & 1));
-    TailQ tq = tail_view(sm_tail, threadIdx.x >> 5);
-    int* sacc = reinterpret_cast<int*>(sm_tail) + (size_t)(threadIdx.x >> 5) * 2 * a.W * 32;
-    uint32_t* pfbuf = reinterpret_cast<uint32_t*>(sm_tail) +
+    char* sm_pf = reinterpret_cast<char*>(s_state + r.R + (r.R & 1));  // cp.async row stages
+    uint32_t* pfbuf = reinterpret_cast<uint32_t*>(sm_pf) +
                       (size_t)(threadIdx.x >> 5) * 2 * pf_stage_words<WV == 2 ? 2 : 4>();
     const int tid = threadIdx.x;
     const int wpb = blockDim.x >> 5;
     const int warp = tid >> 5;
-    const int passes = WV ? a.W / WV : 1;
-    const int wb = WV ? (int)(blockIdx.x % passes) * WV : 0;
+    const int passes = a.W / WV;
+    const int wb = (int)(blockIdx.x % passes) * WV;
     const int gidx = (int)(blockIdx.x / passes) * wpb + warp;
     const int ngroups = (int)(gridDim.x / passes) * wpb;
     for (int m = tid; m < r.R; m += blockDim.x) {
@@ -887,17 +533,13 @@ plane_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__
             const uint64_t t = (uint64_t)((round - 1) * r.sps + sw);
             const bool count = (sw == r.sps - 1);
             for (int c = 0; c < a.n_colors; ++c) {
-                if constexpr (WV == 0) plane_phase_loop<RULE, FAST>(a, c, t, count, gidx, ngroups, cc, cq, sacc);
-                else if constexpr (FAST && (WV == 4 || WV == 2))
-                    plane_phase_pf<RULE, WV>(a, c, t, count, gidx, ngroups, wb, cc, cq, pfbuf,
-                                         r.work ? r.work + ((size_t)(par * a.n_colors + c) * passes +
-                                                            wb / WV) : nullptr);
-                else plane_phase<RULE, WV, FAST, kPlaneTail>(a, c, t, count, gidx, ngroups, wb, cc, cq, tq);
+                if constexpr (FAST && (WV == 4 || WV == 2))
+                    plane_phase_pf<RULE, WV>(a, c, t, count, gidx, ngroups, wb, cc, cq, pfbuf);
+                else plane_phase<RULE, WV, FAST>(a, c, t, count, gidx, ngroups, wb, cc, cq);
                 grid.sync();
             }
         }
-        round_epilogue(a, r, RoundSmem{s_f, s_g, s_slot, s_state}, k, round, cc, cq, swap_base,
-                       a.n_colors * passes);
+        round_epilogue(a, r, RoundSmem{s_f, s_g, s_slot, s_state}, k, round, cc, cq, swap_base, 0);
     }
 }
 
@@ -910,14 +552,10 @@ template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 4, 0>(const __grid_c
 template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 4, 1>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
 template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 2, 1>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
 template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 1, 1>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
-template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 0, 1>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
-template __global__ void plane_rounds_kernel<TG_PLANE_RULE, 0, 0>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
 
 
 
 void* TG_CAT(plane_rounds_fn_r, TG_PLANE_RULE)(int wv, int fast) {
-    if (wv == 0) return fast ? (void*)plane_rounds_kernel<TG_PLANE_RULE, 0, 1>
-                             : (void*)plane_rounds_kernel<TG_PLANE_RULE, 0, 0>;
     if (wv >= 4) return fast ? (void*)plane_rounds_kernel<TG_PLANE_RULE, 4, 1>
                              : (void*)plane_rounds_kernel<TG_PLANE_RULE, 4, 0>;
     if (wv >= 2) return fast ? (void*)plane_rounds_kernel<TG_PLANE_RULE, 2, 1>
