@@ -124,7 +124,9 @@ struct RoundArgs {
     int32_t* cnt;          // [2 parities][2 (cost, chain)][cnt_stride]
     int* work;             // [2 parities][n_colors][passes] chunk counters (dynamic distribution)
     int cnt_stride;
-    int flush_every;       // tpw kernel: items between vertical-counter flushes (0: the overflow bound)
+    int flush_every;       // tpw kernel: items between vertical-counter flushes (host: <= 255 / max bonds)
+    int n_warps;           // tpw kernel: warps of the launch
+    int log_w;             // tpw kernel: log2 of the words per site
     const uint64_t* ktab;
     int ktab_row;
     uint32_t* kp;

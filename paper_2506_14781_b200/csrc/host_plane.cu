@@ -397,8 +397,17 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         r.acc_p = c.d_acc_p.p; r.acc_b = c.d_acc_b.p;
         r.f_all = c.d_f.p; r.g_all = c.d_g.p;
         r.cnt = c.d_cnt2.p; r.cnt_stride = c.W * 32;
-        // testing knob: flush the tpw kernel's vertical counters more often
-        if (const char* e = std::getenv("TG_TPW_FLUSH_EVERY")) r.flush_every = std::atoi(e);
+        // tpw kernel: 8-bit vertical counters take <= 255 / (max bonds per item)
+        // items between flushes (config-5 path: 3, generic: 7); testing knob
+        // TG_TPW_FLUSH_EVERY flushes more often
+        r.flush_every = c.tpw_fast ? 255 / 3 : 255 / 7;
+        if (const char* e = std::getenv("TG_TPW_FLUSH_EVERY")) {
+            const int v = std::atoi(e);
+            if (v > 0 && v < r.flush_every) r.flush_every = v;
+        }
+        r.n_warps = c.fused_grid * (c.fused_block / 32);
+        r.log_w = 0;
+        while ((1 << r.log_w) < c.W) ++r.log_w;
         // tpw kernel: the last ~item per warp of each colour phase is handed
         // out dynamically ([2 parities][colours][sps] counters)
         r.work = nullptr;

@@ -830,12 +830,13 @@ plane_tpw_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_consta
     int* s_cq = s_cc + nrep;
     const RoundSmem s = round_smem(s_cq + nrep, r.R);
     uint32_t* vq = reinterpret_cast<uint32_t*>(tpw_sm + kTpwSmVq) + threadIdx.x;
-    const int logW = __ffs(a.W) - 1;
-    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int nw = gridDim.x * (blockDim.x >> 5);
-    // max bonds added per item: 2^ncb - 1 <= 7; 8-bit counters
-    int flush_every = FAST ? 255 / 3 : 255 / 7;
-    if (r.flush_every > 0 && r.flush_every < flush_every) flush_every = r.flush_every;
+    // launch constants as kernel parameters (host-computed): when register
+    // pressure makes the compiler rematerialise them inside the item loop a
+    // constant-bank load is all it costs
+    const int logW = r.log_w;
+    const int gw = blockIdx.x * (kTpwThreads >> 5) + (threadIdx.x >> 5);
+    const int nw = r.n_warps;
+    const int flush_every = r.flush_every;  // <= 255 / (max bonds per item): 8-bit counters
     for (int m = threadIdx.x; m < 2 * nrep; m += blockDim.x) s_cc[m] = 0;
 #pragma unroll
     for (int b = 0; b < kVB; ++b) vq[b * kTpwThreads] = 0u;
