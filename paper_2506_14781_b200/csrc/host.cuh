@@ -372,6 +372,8 @@ void ensure_host_canonical(tg_ctx& c);
 void build_plane_structure_device(tg_ctx& c, std::vector<PlaneType>& types, std::vector<Chunk>& chunks,
                                   std::vector<int>& chunk_off);
 void build_plane(tg_ctx& c);
+void build_plane_types_device(tg_ctx& c, std::vector<PlaneType>& types, std::vector<int>& chunk_off,
+                              RunTable& rt);
 void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vector<int>& chunk_off);
 void build_slot(tg_ctx& c);
 PlaneArgs plane_args(tg_ctx& c);

@@ -85,6 +85,44 @@ void build_plane_structure_device(tg_ctx& c, std::vector<PlaneType>& types, std:
     chunk_off[c.n_colors] = (int)chunks.size();
 }
 
+// Site types, per-colour chunk offsets and the run table of the device prep's
+// runs (same chunk order as build_plane_structure_device).
+void build_plane_types_device(tg_ctx& c, std::vector<PlaneType>& types, std::vector<int>& chunk_off,
+                              RunTable& rt) {
+    const PrepSummary& P = c.prep;
+    const int mq1 = P.max_dq + 1, mc1 = P.max_dc + 1;
+    std::vector<int> tid_of((kMaxDC + 1) * (kMaxDQ + 1), -1);
+    chunk_off.assign(c.n_colors + 1, 0);
+    int start = 0, cur_col = -1, nch = 0;
+    rt.n = (int)P.run_keys.size();
+    for (int q = 0; q < rt.n; ++q) {
+        const unsigned key = P.run_keys[q];
+        const int cnt = P.run_counts[q];
+        const int dc = (int)(key % mc1), dq = (int)((key / mc1) % mq1), col = (int)(key / ((unsigned)mc1 * mq1));
+        while (cur_col < col) chunk_off[++cur_col] = nch;
+        const int tkey = dc * (kMaxDQ + 1) + dq;
+        if (tid_of[tkey] < 0) {
+            PlaneType t{};
+            t.dc = dc;
+            t.dq = dq;
+            t.ncb = nbits(dc);
+            t.nqb = nbits(dq);
+            t.ncl = std::max(4, 1 << (t.ncb + t.nqb));
+            tid_of[tkey] = (int)types.size();
+            types.push_back(t);
+        }
+        rt.start[q] = start;
+        rt.cnt[q] = cnt;
+        rt.type[q] = tid_of[tkey];
+        rt.cpref[q] = nch;
+        nch += (cnt + 31) / 32;
+        start += cnt;
+    }
+    rt.cpref[rt.n] = nch;
+    while (cur_col < c.n_colors) chunk_off[++cur_col] = nch;
+    chunk_off[c.n_colors] = nch;
+}
+
 void build_plane(tg_ctx& c) {
     HostTimer tm_("build_plane");
     cudaStream_t st = c.stream;
@@ -93,10 +131,21 @@ void build_plane(tg_ctx& c) {
         std::vector<PlaneType> types;
         std::vector<Chunk> chunks;
         std::vector<int> chunk_off;
-        build_plane_structure_device(c, types, chunks, chunk_off);
         c.d_nbr.copy_from(c.d_nbr_dev, st);
-        c.d_chunks.upload(chunks, st);
-        CK(plane_chunk_bases(c.d_chunks.p, (int)chunks.size(), c.d_base_dev.p, st, c.sms));
+        if (c.prep.run_keys.size() <= (size_t)kMaxRuns) {
+            // the chunk list is a function of the few (colour, type) runs:
+            // generate it on the device (a host list of ~n/32 chunks costs
+            // first-touch page faults on every set_problem)
+            RunTable rt{};
+            build_plane_types_device(c, types, chunk_off, rt);
+            c.d_chunks.alloc((size_t)rt.cpref[rt.n]);
+            CK(plane_gen_chunks(rt, c.d_chunks.p, st));
+            CK(plane_chunk_bases(c.d_chunks.p, rt.cpref[rt.n], c.d_base_dev.p, st, c.sms));
+        } else {
+            build_plane_structure_device(c, types, chunks, chunk_off);
+            c.d_chunks.upload(chunks, st);
+            CK(plane_chunk_bases(c.d_chunks.p, (int)chunks.size(), c.d_base_dev.p, st, c.sms));
+        }
         build_plane_rest(c, types, chunk_off);
         return;
     }

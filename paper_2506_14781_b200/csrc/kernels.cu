@@ -27,6 +27,22 @@ void* plane_rounds_fn_r1(int wv, int fast);
 void* plane_tpw_fn_r0(int fast);
 void* plane_tpw_fn_r1(int fast);
 void* plane_tpw_fn(int rule, int fast) { return rule == 0 ? plane_tpw_fn_r0(fast) : plane_tpw_fn_r1(fast); }
+__global__ void k_gen_chunks(const __grid_constant__ RunTable rt, Chunk* chunks) {
+    const int total = rt.cpref[rt.n];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+        int q = 0;
+        while (rt.cpref[q + 1] <= k) ++q;  // runs are few
+        const int s0 = rt.start[q] + 32 * (k - rt.cpref[q]);
+        chunks[k] = Chunk{s0, min(32, rt.start[q] + rt.cnt[q] - s0), rt.type[q], 0};
+    }
+}
+
+cudaError_t plane_gen_chunks(const RunTable& rt, Chunk* chunks, cudaStream_t st) {
+    const int total = rt.cpref[rt.n];
+    if (total > 0) k_gen_chunks<<<(total + 255) / 256, 256, 0, st>>>(rt, chunks);
+    return cudaGetLastError();
+}
+
 // Per-site padded neighbour table of the tpw config-5 path (one warp per chunk).
 __global__ void k_tpw_nbr4(const Chunk* chunks, int n_chunks, TypeDq tdq, const int32_t* nbr, int logW,
                            int4* out) {

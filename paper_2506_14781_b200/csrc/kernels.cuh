@@ -113,6 +113,15 @@ struct PrepSummary {        // host
 cudaError_t plane_prep_device(const PrepIn& in, const PrepOut& o, PrepSummary& r, cudaStream_t st,
                               int sms);
 cudaError_t plane_chunk_bases(Chunk* chunks, int n_chunks, const int* base, cudaStream_t st, int sms);
+// Chunks of <= 32 sites per run of one (colour, site type), generated on the
+// device from the run table (kernels.cu); nbr_base is filled by plane_chunk_bases.
+constexpr int kMaxRuns = 64;
+struct RunTable {
+    int n;
+    int start[kMaxRuns], cnt[kMaxRuns], type[kMaxRuns];
+    int cpref[kMaxRuns + 1];  // first chunk of each run
+};
+cudaError_t plane_gen_chunks(const RunTable& rt, Chunk* chunks, cudaStream_t st);
 
 __global__ void probe_moments_kernel(const double* hist_f, const double* hist_g, int R, int kept,
                                      double penalty, double* out);
