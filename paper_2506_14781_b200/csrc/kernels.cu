@@ -461,12 +461,33 @@ __global__ void plane_init_kernel(uint32_t* spins, int n, int W, int local_state
     philox_key_schedule(derive_seed(seed, kPurposeInit, (uint64_t)(state0 + w * 32 + lane)), ks);
     const int dp = nw / W;
     int p = gw / W;
-    for (int it = gw; it < items; it += nw) {
-        if (!fixed_w) {
-            w = it % W;
-            p = it / W;
-            philox_key_schedule(derive_seed(seed, kPurposeInit, (uint64_t)(state0 + w * 32 + lane)), ks);
+    if (fixed_w) {
+        // two independent site pairs per iteration (two Philox blocks in flight)
+        const bool live = w * 32 + lane < local_states;
+        for (int it = gw; it < items; it += 2 * nw, p += 2 * dp) {
+            const bool two = it + nw < items;
+            const u32x4 o = philox4x32_10_ks(u32x4{(uint32_t)p, 0u, 0u, 0u}, ks);
+            const u32x4 o2 = philox4x32_10_ks(u32x4{(uint32_t)(p + dp), 0u, 0u, 0u}, ks);
+            const uint32_t w0 = __ballot_sync(0xffffffffu, live && (o.y >> 31));   // draw 2p
+            const uint32_t w1 = __ballot_sync(0xffffffffu, live && (o.w >> 31));   // draw 2p + 1
+            const uint32_t w2 = __ballot_sync(0xffffffffu, live && (o2.y >> 31));
+            const uint32_t w3 = __ballot_sync(0xffffffffu, live && (o2.w >> 31));
+            if (lane == 0) {
+                spins[(size_t)(2 * p) * W + w] = w0;
+                if (2 * p + 1 < n) spins[(size_t)(2 * p + 1) * W + w] = w1;
+                if (two) {
+                    const int q = p + dp;
+                    spins[(size_t)(2 * q) * W + w] = w2;
+                    if (2 * q + 1 < n) spins[(size_t)(2 * q + 1) * W + w] = w3;
+                }
+            }
         }
+        return;
+    }
+    for (int it = gw; it < items; it += nw) {
+        w = it % W;
+        p = it / W;
+        philox_key_schedule(derive_seed(seed, kPurposeInit, (uint64_t)(state0 + w * 32 + lane)), ks);
         const u32x4 o = philox4x32_10_ks(u32x4{(uint32_t)p, 0u, 0u, 0u}, ks);
         const bool live = w * 32 + lane < local_states;
         const uint32_t w0 = __ballot_sync(0xffffffffu, live && (o.y >> 31));  // draw 2p
@@ -475,7 +496,6 @@ __global__ void plane_init_kernel(uint32_t* spins, int n, int W, int local_state
             spins[(size_t)(2 * p) * W + w] = w0;
             if (2 * p + 1 < n) spins[(size_t)(2 * p + 1) * W + w] = w1;
         }
-        p += dp;
     }
 }
 
