@@ -506,6 +506,7 @@ def run_ours(args, rank, world, local):
                          "unit": "GB/s", "frac": achieved_gbs / smem_peak_gbs,
                          "traffic": traffic["bytes_per_launch"] if traffic else None,
                          "traffic_source": traffic["source"] if traffic else None,
+                         "issue": issue_roofline(traffic, value / world, sm_max),
                          "kernel": kname,
                          "bytes_per_update": bal,
                          "mean_launch_ms": mean_sweep_s * 1e3,
@@ -525,6 +526,20 @@ def dominant_kernel(args, world):
     return "plane_tpw_rounds_kernel" if world == 1 else "plane_sweep_kernel"
 
 
+def issue_roofline(traffic, updates_per_s_per_gpu, sm_max_mhz):
+    """The bound the integer-issue kernels actually meet: lane-instructions per
+    spin update (committed ncu capture, smsp__inst_executed x 32 / updates)
+    against the SM issue peak (148 SMs x 4 schedulers x 32 lanes x clock)."""
+    ipu = traffic.get("lane_instr_per_update") if traffic else None
+    if not ipu:
+        return None
+    peak = 148 * 4 * 32 * sm_max_mhz * 1e6
+    bound = peak / ipu
+    return {"lane_instr_per_update": ipu, "peak_lane_instr_per_s": peak,
+            "issue_bound_updates_per_s": bound, "frac": updates_per_s_per_gpu / bound,
+            "note": "issue-slot roofline of the dominant kernel; instructions/update from profiles/traffic.json"}
+
+
 def ncu_traffic(kname, args, pr, R, sweeps_per_launch):
     """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel from the
     committed `ncu --set full` capture (profiles/traffic.json), rescaled from the
@@ -541,7 +556,8 @@ def ncu_traffic(kname, args, pr, R, sweeps_per_launch):
                 c.get("n_spins") == pr.n and c.get("replicas") == R and c.get("rule") == args.rule:
             per_sweep = c["dram_bytes"] / c["sweeps_per_launch"]
             return {"bytes_per_launch": per_sweep * sweeps_per_launch,
-                    "source": f"profiles/traffic.json: {c['source']}"}
+                    "source": f"profiles/traffic.json: {c['source']}",
+                    "lane_instr_per_update": c.get("lane_instr_per_update")}
     return None
 
 
