@@ -181,3 +181,14 @@ def test_config5_path_several_sweeps_per_round(rule):
     b, p = sched(16, 16)
     compare(pr, b, p, 3 * 8, 3, seed=5, rule=rule, engine="plane")
     assert kernel_of(pr, b, p, rule) == "plane_tpw_rounds_kernel"
+
+
+@pytest.mark.parametrize("n,chain_frac", [(1002, 0.1), (30, 0.1), (4096, 0.0), (4096, 0.5)])
+@pytest.mark.parametrize("rule", ["metropolis", "heat_bath"])
+def test_config5_path_shapes(n, chain_frac, rule):
+    # partial last items (colour sizes not a multiple of the item's sites),
+    # no chain sites at all, and many chain sites
+    pr = I.bipartite_3regular(n, seed=21, chain_frac=chain_frac)
+    b, p = sched(16, 16)
+    compare(pr, b, p, 10, 1, seed=8, rule=rule, engine="plane")
+    assert kernel_of(pr, b, p, rule) == "plane_tpw_rounds_kernel"
