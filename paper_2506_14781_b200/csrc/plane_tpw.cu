@@ -599,6 +599,22 @@ __device__ __forceinline__ void c5_site(const PlaneArgs& a, const C5K& K, int ty
     }
 }
 
+// Heat bath, config-5 path: stage planes 0-7 and "always" of the chain-free
+// type's 4 classes for every word, [9][W] uint4, once per round (thresholds
+// change only in the round epilogue; the caller's grid barrier precedes this).
+__device__ __forceinline__ void tpw_stage_hb(const PlaneArgs& a) {
+    int t30 = 0;
+    for (int ty = 0; ty < a.n_types; ++ty)
+        if (a.ty[ty].dq == 0) t30 = ty;
+    uint4* hb = reinterpret_cast<uint4*>(tpw_sm + kTpwSmHb);
+    const int kp0 = a.ty[t30].kp_off, W = a.W;
+    for (int q = threadIdx.x; q < 9 * W; q += blockDim.x) {
+        const int b = q / W, ww = q % W;
+        hb[q] = *reinterpret_cast<const uint4*>(a.kp + (size_t)ww * a.kpw + kp0 + (b < 8 ? b : kKPlanes) * 4);
+    }
+    __syncthreads();
+}
+
 // FAST colour phase (config-5 types): chunk descriptors two items ahead,
 // neighbour entries one item ahead, so an item's gathers depend only on
 // registers when it starts.
@@ -629,18 +645,7 @@ __device__ __forceinline__ void tpw_phase_c5(const PlaneArgs& a, int c, uint64_t
         K.k2b = kc[1];
         K.k3a = kc[16];
         K.k3b = kc[17];
-    } else {
-        // heat bath: stage planes 0-7 and "always" of the chain-free type's 4
-        // classes for every word: [9][W] uint4 (the previous phase's readers
-        // are past the grid barrier that preceded this phase)
-        uint4* hb = reinterpret_cast<uint4*>(tpw_sm + kTpwSmHb);
-        const int kp0 = a.ty[K.t30].kp_off;
-        for (int q = threadIdx.x; q < 9 * W; q += blockDim.x) {
-            const int b = q / W, ww = q % W;
-            hb[q] = *reinterpret_cast<const uint4*>(a.kp + (size_t)ww * a.kpw + kp0 + (b < 8 ? b : kKPlanes) * 4);
-        }
-        __syncthreads();
-    }
+    }  // heat bath: planes 0-7 of the chain-free type's classes were staged at round start
     K.act_w = a.active[w];
     K.grp4 = (uint32_t)(a.w_global0 + w) << 4;
     K.tlo = (uint32_t)t;
@@ -852,6 +857,7 @@ plane_tpw_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_consta
         int32_t* cc = r.cnt + (size_t)par * 2 * r.cnt_stride;
         int32_t* cq = cc + r.cnt_stride;
         TPW_STAMP(k, 0);
+        if (FAST && RULE == 1) tpw_stage_hb(a);
         for (int sw = 0; sw < r.sps; ++sw) {
             const uint64_t t = (uint64_t)((round - 1) * r.sps + sw);
             const bool count = (sw == r.sps - 1);
@@ -901,6 +907,7 @@ plane_tpw_sweep_kernel(const __grid_constant__ PlaneArgs a, int64_t t0, int n_sw
     uint32_t Vc[kVB];
 #pragma unroll
     for (int b = 0; b < kVB; ++b) Vc[b] = 0u;
+    if (FAST && RULE == 1) tpw_stage_hb(a);  // labels are fixed for the whole launch
     for (int sw = 0; sw < n_sweeps; ++sw) {
         const uint64_t t = (uint64_t)(t0 + sw);
         const bool count = (sw == n_sweeps - 1);
