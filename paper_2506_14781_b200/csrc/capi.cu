@@ -325,6 +325,7 @@ int tg_batch_add(tg_ctx* ctx, int n, int n_couplings, const int32_t* ci, const i
                  const int32_t* pb, int n_betas, const double* betas, int n_penalties,
                  const double* penalties, uint64_t seed, int32_t* index) {
     if (!ctx) return TG_ERR_CONFIG;
+    HostTimer tm_("batch: add");
     return guard(ctx, [&] {
         BatchInst bi;
         load_problem(bi, n, n_couplings, ci, cj, w, fields, n_pairs, pa, pb);

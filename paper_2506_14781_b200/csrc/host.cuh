@@ -15,7 +15,11 @@
 #include <cstring>
 #include <limits>
 #include <map>
+#include <atomic>
+#include <exception>
+#include <memory>
 #include <mutex>
+#include <thread>
 #include <tuple>
 #include <string>
 #include <utility>
@@ -125,6 +129,28 @@ struct StreamOwner {
 };
 
 // TG_HOST_TIMING=1: host-side phase timings on stderr (e2e breakdown).
+// Uninitialised host staging buffer for device-to-host record copies: a
+// std::vector's zero-fill of a large ring (e.g. 64 instances x 1024 rounds of
+// acceptance counters, 250 MB) cost ~80 ms per run before any data arrived.
+template <class T>
+struct HostVec {
+    std::unique_ptr<T[]> p;
+    size_t n = 0;
+    void resize(size_t m) {
+        if (m != n) {
+            p.reset(m ? new T[m] : nullptr);
+            n = m;
+        }
+    }
+    T* data() { return p.get(); }
+    const T* data() const { return p.get(); }
+    size_t size() const { return n; }
+    T& operator[](size_t i) { return p[i]; }
+    const T& operator[](size_t i) const { return p[i]; }
+    T* begin() { return p.get(); }
+    T* end() { return p.get() + n; }
+};
+
 struct HostTimer {
     const char* what;
     std::chrono::steady_clock::time_point t0;
@@ -183,9 +209,9 @@ struct Slot2 {
     DBuf<uint64_t> d_keys, d_swap_seed, d_seeds;
     DBuf<int64_t> d_acc_p, d_acc_b, d_rec_acc;
     DBuf<TgRecordDev> d_rec;
-    std::vector<TgRecordDev> h_rec;
-    std::vector<int64_t> h_acc;
-    std::vector<int8_t> h_states;
+    HostVec<TgRecordDev> h_rec;
+    HostVec<int64_t> h_acc;
+    HostVec<int8_t> h_states;
     int64_t rounds_done = 0;
     uint64_t swap_base = 0;
     bool ready = false;
@@ -309,9 +335,9 @@ struct tg_ctx {
     bool use_s2 = false;
 
     int rec_cap = 0;
-    std::vector<TgRecordDev> h_rec;
-    std::vector<int8_t> h_states;
-    std::vector<int64_t> h_acc;
+    HostVec<TgRecordDev> h_rec;
+    HostVec<int8_t> h_states;
+    HostVec<int64_t> h_acc;
     std::vector<cudaEvent_t> ev;
     double last_sweep_ms = 0, last_swap_ms = 0;
     int64_t sweep_launches = 0, other_launches = 0;

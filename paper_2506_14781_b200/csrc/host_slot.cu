@@ -276,6 +276,7 @@ S2Swap s2_swap(tg_ctx& c) {
 }
 
 void s2_build(tg_ctx& c, const tg_run_config* cfg) {
+    HostTimer tm_("batch: s2_build");
     Slot2& S = c.s2;
     cudaStream_t st = c.stream;
     const int B = (int)c.batch.size();
@@ -293,18 +294,47 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
     if (S.cfg.record_every < 1) S.cfg.record_every = 1;
     S.prep.assign(B, S2Prep{});
     S.state_off.clear();
+    std::unique_ptr<HostTimer> tsec(new HostTimer("batch: s2_build prepare"));
+    // per-instance host preprocessing (canonical order, merged CSR, padded
+    // entries): independent instances run on host threads; repeats of one
+    // instance (J-column baseline) copy the previous instance's result
+    std::vector<char> dup(B, 0);
+    std::vector<int> todo;
     for (int b = 0; b < B; ++b) {
         const BatchInst& x = c.batch[b];
         const BatchInst* y = b ? &c.batch[b - 1] : nullptr;
-        if (y && x.n == y->n && x.ci == y->ci && x.cj == y->cj && x.cw == y->cw && x.h == y->h &&
-            x.pa == y->pa && x.pb == y->pb)
-            S.prep[b] = S.prep[b - 1];  // repeats of one instance (J-column baseline)
-        else
-            s2_prepare(S.prep[b], x);
+        dup[b] = y && x.n == y->n && x.ci == y->ci && x.cj == y->cj && x.cw == y->cw && x.h == y->h &&
+                 x.pa == y->pa && x.pb == y->pb;
+        if (!dup[b]) todo.push_back(b);
     }
+    {
+        const int nt = (int)std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(),
+                                                            std::min<size_t>(todo.size(), 32)));
+        std::vector<std::exception_ptr> err(B);
+        std::atomic<int> next{0};
+        auto work = [&] {
+            for (int k; (k = next.fetch_add(1)) < (int)todo.size();) {
+                const int b = todo[k];
+                try {
+                    s2_prepare(S.prep[b], c.batch[b]);
+                } catch (...) {
+                    err[b] = std::current_exception();
+                }
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+        work();
+        for (auto& th : pool) th.join();
+        for (int b = 0; b < B; ++b)  // the first failing instance's error, as a sequential loop would
+            if (err[b]) std::rethrow_exception(err[b]);
+    }
+    for (int b = 1; b < B; ++b)
+        if (dup[b]) S.prep[b] = S.prep[b - 1];
     int D = 4;
     for (const auto& P : S.prep) D = std::max(D, P.D);
     S.D = D;
+    tsec.reset(new HostTimer("batch: s2_build concatenate"));
     // concatenate
     std::vector<SInst> inst(B);
     std::vector<int2> entp;
@@ -370,6 +400,7 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
             item_pref[(size_t)col * (B + 1) + b + 1] = item_pref[(size_t)col * (B + 1) + b] + ub;
         }
     for (int b = 0; b < B; ++b) energy_pref[b + 1] = energy_pref[b] + inst[b].n_chunks * S.G;
+    tsec.reset(new HostTimer("batch: s2_build uploads"));
     S.d_inst.upload(inst, st);
     S.h_inst = inst;
     S.d_entp.upload(entp, st);
@@ -399,6 +430,7 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
     }
     S.d_perm.upload(perm, st);
     S.d_spins.alloc((size_t)spin_off);
+    tsec.reset(new HostTimer("batch: s2_build grid/rest"));
     // cooperative grid: whole warps per replica group
     {
         int per_sm = 0;
@@ -560,6 +592,7 @@ void s2_drain(tg_ctx& c, int filled, int64_t first_round, const BatchSinkCtx& si
 }
 
 void s2_advance(tg_ctx& c, int64_t n_rounds, const BatchSinkCtx& sink) {
+    HostTimer tm_("batch: s2_advance");
     Slot2& S = c.s2;
     if (!S.ready) fail(TG_ERR_CONFIG, "advance: batch not initialised");
     cudaStream_t st = c.stream;
