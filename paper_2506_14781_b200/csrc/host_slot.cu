@@ -24,7 +24,24 @@ void build_slot(tg_ctx& c) {
         ent.push_back({x << 32 | y, 0.0, 1});
         ent.push_back({y << 32 | x, 0.0, 1});
     }
-    std::stable_sort(ent.begin(), ent.end(), [](const E& p, const E& q) { return p.key < q.key; });
+    {
+        // = std::stable_sort by key (row x, then column y): a stable counting
+        // sort by row, then a stable insertion sort inside each (short) row
+        std::vector<int> pos(n + 1, 0);
+        for (const E& e : ent) pos[(e.key >> 32) + 1]++;
+        for (int i = 0; i < n; ++i) pos[i + 1] += pos[i];
+        std::vector<E> srt(ent.size());
+        std::vector<int> fill(pos.begin(), pos.end() - 1);
+        for (const E& e : ent) srt[fill[e.key >> 32]++] = e;
+        for (int i = 0; i < n; ++i)
+            for (int a = pos[i] + 1; a < pos[i + 1]; ++a) {
+                const E v = srt[a];
+                int b = a - 1;
+                while (b >= pos[i] && srt[b].key > v.key) { srt[b + 1] = srt[b]; --b; }
+                srt[b + 1] = v;
+            }
+        ent.swap(srt);
+    }
     std::vector<int> off(n + 1, 0);
     std::vector<int32_t> nbr;
     std::vector<double> w;
@@ -182,7 +199,24 @@ void s2_prepare(S2Prep& P, const BatchInst& bi) {
         ent.push_back({x << 32 | y, 0.0, 1});
         ent.push_back({y << 32 | x, 0.0, 1});
     }
-    std::stable_sort(ent.begin(), ent.end(), [](const E& p, const E& q) { return p.key < q.key; });
+    {
+        // = std::stable_sort by key (row x, then column y): a stable counting
+        // sort by row, then a stable insertion sort inside each (short) row
+        std::vector<int> pos(n + 1, 0);
+        for (const E& e : ent) pos[(e.key >> 32) + 1]++;
+        for (int i = 0; i < n; ++i) pos[i + 1] += pos[i];
+        std::vector<E> srt(ent.size());
+        std::vector<int> fill(pos.begin(), pos.end() - 1);
+        for (const E& e : ent) srt[fill[e.key >> 32]++] = e;
+        for (int i = 0; i < n; ++i)
+            for (int a = pos[i] + 1; a < pos[i + 1]; ++a) {
+                const E v = srt[a];
+                int b = a - 1;
+                while (b >= pos[i] && srt[b].key > v.key) { srt[b + 1] = srt[b]; --b; }
+                srt[b + 1] = v;
+            }
+        ent.swap(srt);
+    }
     P.off.assign(n + 1, 0);
     P.nbr.clear(); P.w.clear(); P.cm.clear();
     for (size_t k = 0; k < ent.size();) {
