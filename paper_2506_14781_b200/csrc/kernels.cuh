@@ -87,6 +87,8 @@ enum : unsigned {
     kPrepNotPM1 = 16u, kPrepNonzeroField = 32u  // plane-engine eligibility (not errors)
 };
 constexpr int kPrepColourRounds = 4096;
+// largest (colour, dq, dc) run list read back together with the run count
+constexpr size_t kPrepEagerRuns = 1 << 16;
 struct PrepIn {             // device arrays, caller order
     int n, m, np;
     const int* ci;

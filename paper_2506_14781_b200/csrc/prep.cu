@@ -370,10 +370,25 @@ cudaError_t plane_prep_device(const PrepIn& in, const PrepOut& o, PrepSummary& r
     PA(tmp);
     PK(cub::DeviceRunLengthEncode::Encode(tmp, tb, key_sorted, rk, rc, nruns, n, st));
     int h_runs = 0, h_ncol = 0;
+    // the run count is bounded by the key range: when that bound is small, the
+    // runs come back with the counts in the same synchronisation
+    const size_t bound = (size_t)std::min<unsigned long long>((unsigned long long)n, kmax);
+    const bool eager = bound <= kPrepEagerRuns;
+    if (eager) {
+        r.run_keys.resize(bound);
+        r.run_counts.resize(bound);
+        PK(cudaMemcpyAsync(r.run_keys.data(), rk, sizeof(unsigned) * bound, cudaMemcpyDeviceToHost, st));
+        PK(cudaMemcpyAsync(r.run_counts.data(), rc, sizeof(int) * bound, cudaMemcpyDeviceToHost, st));
+    }
     PK(cudaMemcpyAsync(&h_runs, nruns, sizeof(int), cudaMemcpyDeviceToHost, st));
     PK(cudaMemcpyAsync(&h_ncol, ncol, sizeof(int), cudaMemcpyDeviceToHost, st));
     PK(cudaStreamSynchronize(st));
     r.n_colors = h_ncol;
+    if (eager) {
+        r.run_keys.resize(h_runs);
+        r.run_counts.resize(h_runs);
+        return cudaSuccess;
+    }
     r.run_keys.resize(h_runs);
     r.run_counts.resize(h_runs);
     PK(cudaMemcpyAsync(r.run_keys.data(), rk, sizeof(unsigned) * h_runs, cudaMemcpyDeviceToHost, st));
