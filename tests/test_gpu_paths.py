@@ -187,3 +187,24 @@ def test_context_reuse_equals_fresh_contexts(engine):
             fresh_recs, fresh_grid = once(eng, *r)
         assert recs == fresh_recs
         np.testing.assert_array_equal(grid, fresh_grid)
+
+
+def test_large_key_range_run_list_read_back_in_two_steps(monkeypatch):
+    # a hub of cost degree 34 and chain degree 31 on n = 70000 sites: the
+    # (colour, dq, dc) key range 64*32*35 and n both exceed kPrepEagerRuns, so
+    # device prep reads the run count before the run list (prep.cu); the
+    # merged degree needs the CSR kernels of SLOT v1
+    monkeypatch.setenv("TG_SLOT_V1", "1")
+    n = 70000
+    rng = np.random.default_rng(12)
+    perm = rng.permutation(n)
+    w = rng.choice([-1.0, 1.0], size=n + 32)
+    cpl = [(int(perm[k]), int(perm[k + 1]), float(w[k])) for k in range(n - 1)]
+    hub = int(perm[n // 2])
+    others = [int(v) for v in rng.choice(n, size=200, replace=False) if int(v) != hub]
+    path_nb = {int(perm[n // 2 - 1]), int(perm[n // 2 + 1])}
+    others = [v for v in others if v not in path_nb]
+    cpl += [(hub, v, float(w[n + k])) for k, v in enumerate(others[:32])]
+    pairs = [(hub, v) for v in others[32:63]]
+    pr = Problem.make(n, cpl, [0.0] * n, pairs)
+    check(pr, [0.3, 2.0], [0.0, 0.5], 4, 9, "slot")
