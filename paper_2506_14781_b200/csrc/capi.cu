@@ -213,24 +213,19 @@ int tg_get_state(tg_ctx* ctx, int slot, int8_t* out) {
         if (c.use_s2) { s2_get_state(c, 0, slot, out); return; }
         if (!c.initialised) fail(TG_ERR_CONFIG, "get_state: context not initialised");
         if (slot < 0 || slot >= c.R) fail(TG_ERR_CONFIG, "get_state: slot %d out of range", slot);
-        // reuse the extract kernel on a one-slot view: temporarily point slot R-1 at `slot`
-        std::vector<int32_t> ss(c.R);
-        CK(cudaMemcpyAsync(ss.data(), c.d_slot_state.p, sizeof(int32_t) * c.R, cudaMemcpyDeviceToHost, c.stream));
-        CK(cudaStreamSynchronize(c.stream));
-        DBuf<int32_t> view;
-        std::vector<int32_t> v(c.R, ss[slot]);
-        view.upload(v, c.stream);
+        // the extract kernel's one-slot mode reads slot R-1: a grid truncated
+        // after `slot` makes that the slot asked for (state looked up on device)
         DBuf<int8_t> dst;
         dst.alloc(c.n);
         ExtractArgs e{};
         e.n = c.n;
-        e.R = c.R;
+        e.R = slot + 1;
         e.W = c.W;
         e.plane = c.engine == TG_ENGINE_PLANE;
         e.all_slots = 0;
         e.local_states = c.R_local;
         e.state0 = c.state0;
-        e.slot_state = view.p;
+        e.slot_state = c.d_slot_state.p;
         e.spins32 = c.d_spins32.p;
         e.spins8 = c.d_spins8.p;
         e.perm = c.d_perm.p;
