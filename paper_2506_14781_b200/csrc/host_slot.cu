@@ -380,32 +380,40 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
     std::vector<uint64_t> keys((size_t)B * S.R), swap_seed(B), seeds(B);
     long long spin_off = 0;
     int chunk_off = 0, state_off = 0, max_colors = 0;
+    // offsets of every instance in each concatenated array, then the copies
+    // on host threads (instances are independent)
+    struct Cat { size_t cst, ent, off, nbr, w, cm, h, h32, perm; };
+    std::vector<Cat> at(B + 1, Cat{0, 0, 0, 0, 0, 0, 0, 0, 0});
+    for (int b = 0; b < B; ++b) {
+        const S2Prep& P = S.prep[b];
+        const Cat& a = at[b];
+        at[b + 1] = Cat{a.cst + P.color_start.size(), a.ent + (size_t)P.n * D, a.off + P.off.size(),
+                        a.nbr + P.nbr.size(), a.w + P.w.size(), a.cm + P.cm.size(), a.h + P.h.size(),
+                        a.h32 + P.h32.size(), a.perm + P.order.size()};
+    }
+    cstart.resize(at[B].cst);
+    entp.resize(at[B].ent);
+    wp.resize(at[B].ent);
+    off.resize(at[B].off);
+    nbr.resize(at[B].nbr);
+    w.resize(at[B].w);
+    cm.resize(at[B].cm);
+    h.resize(at[B].h);
+    h32.resize(at[B].h32);
+    perm.resize(at[B].perm);
     for (int b = 0; b < B; ++b) {
         S2Prep& P = S.prep[b];
         SInst& in = inst[b];
         in.n = P.n;
         in.D = D;
         in.n_colors = P.n_colors;
-        in.color_off = (int)cstart.size();
-        cstart.insert(cstart.end(), P.color_start.begin(), P.color_start.end());
+        in.color_off = (int)at[b].cst;
         in.spin_off = spin_off;
         spin_off += (long long)P.n * S.Rp;
-        in.entp_off = (int)entp.size();
-        for (int i = 0; i < P.n; ++i)
-            for (int k = 0; k < D; ++k) {
-                entp.push_back(k < P.D ? P.entp[(size_t)i * P.D + k] : make_int2(i, 0));
-                wp.push_back(k < P.D ? P.wp[(size_t)i * P.D + k] : 0.0);
-            }
-        in.csr_off = (int)off.size();
-        off.insert(off.end(), P.off.begin(), P.off.end());
-        in.nbr_off = (int)nbr.size();
-        nbr.insert(nbr.end(), P.nbr.begin(), P.nbr.end());
-        w.insert(w.end(), P.w.begin(), P.w.end());
-        cm.insert(cm.end(), P.cm.begin(), P.cm.end());
-        in.h_off = (int)h.size();
-        h.insert(h.end(), P.h.begin(), P.h.end());
-        h32.insert(h32.end(), P.h32.begin(), P.h32.end());
-        perm.insert(perm.end(), P.order.begin(), P.order.end());
+        in.entp_off = (int)at[b].ent;
+        in.csr_off = (int)at[b].off;
+        in.nbr_off = (int)at[b].nbr;
+        in.h_off = (int)at[b].h;
         in.n_chunks = (P.n + 31) / 32;
         in.chunk_off = chunk_off;
         chunk_off += in.n_chunks;
@@ -422,6 +430,37 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
             keys[(size_t)b * S.R + r] = S.probe ? derive_seed(c.batch[b].seed, kPurposeProbe, (uint64_t)r)
                                                 : derive_seed(c.batch[b].seed, kPurposeReplica, (uint64_t)r);
         swap_seed[b] = derive_seed(c.batch[b].seed, kPurposeSwap, 0);
+    }
+    {
+        auto fill = [&](int b) {
+            const S2Prep& P = S.prep[b];
+            const Cat& a = at[b];
+            std::copy(P.color_start.begin(), P.color_start.end(), cstart.begin() + a.cst);
+            int2* ep = entp.data() + a.ent;
+            double* wq = wp.data() + a.ent;
+            for (int i = 0; i < P.n; ++i)
+                for (int k = 0; k < D; ++k) {
+                    *ep++ = k < P.D ? P.entp[(size_t)i * P.D + k] : make_int2(i, 0);
+                    *wq++ = k < P.D ? P.wp[(size_t)i * P.D + k] : 0.0;
+                }
+            std::copy(P.off.begin(), P.off.end(), off.begin() + a.off);
+            std::copy(P.nbr.begin(), P.nbr.end(), nbr.begin() + a.nbr);
+            std::copy(P.w.begin(), P.w.end(), w.begin() + a.w);
+            std::copy(P.cm.begin(), P.cm.end(), cm.begin() + a.cm);
+            std::copy(P.h.begin(), P.h.end(), h.begin() + a.h);
+            std::copy(P.h32.begin(), P.h32.end(), h32.begin() + a.h32);
+            std::copy(P.order.begin(), P.order.end(), perm.begin() + a.perm);
+        };
+        const int nt = (int)std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(),
+                                                            (unsigned)std::min(B, 16)));
+        std::atomic<int> next{0};
+        auto work = [&] {
+            for (int b; (b = next.fetch_add(1)) < B;) fill(b);
+        };
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+        work();
+        for (auto& th : pool) th.join();
     }
     S.max_colors = max_colors;
     // item prefix tables: per colour, per instance, upper bound of Philox pairs x groups
