@@ -371,8 +371,11 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
     tsec.reset(new HostTimer("batch: s2_build concatenate"));
     // concatenate
     std::vector<SInst> inst(B);
-    std::vector<int2> entp;
-    std::vector<double> wp, w, h, betas, pens;
+    // the padded entry arrays are the largest: allocated without value-init so
+    // their pages are first touched by the filling threads below
+    std::unique_ptr<int2[]> entp;
+    std::unique_ptr<double[]> wp;
+    std::vector<double> w, h, betas, pens;
     std::vector<int> off, cstart, perm;
     std::vector<int32_t> nbr;
     std::vector<int8_t> cm;
@@ -392,8 +395,8 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
                         a.h32 + P.h32.size(), a.perm + P.order.size()};
     }
     cstart.resize(at[B].cst);
-    entp.resize(at[B].ent);
-    wp.resize(at[B].ent);
+    entp.reset(new int2[std::max<size_t>(at[B].ent, 1)]);
+    wp.reset(new double[std::max<size_t>(at[B].ent, 1)]);
     off.resize(at[B].off);
     nbr.resize(at[B].nbr);
     w.resize(at[B].w);
@@ -436,8 +439,8 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
             const S2Prep& P = S.prep[b];
             const Cat& a = at[b];
             std::copy(P.color_start.begin(), P.color_start.end(), cstart.begin() + a.cst);
-            int2* ep = entp.data() + a.ent;
-            double* wq = wp.data() + a.ent;
+            int2* ep = entp.get() + a.ent;
+            double* wq = wp.get() + a.ent;
             for (int i = 0; i < P.n; ++i)
                 for (int k = 0; k < D; ++k) {
                     *ep++ = k < P.D ? P.entp[(size_t)i * P.D + k] : make_int2(i, 0);
@@ -476,8 +479,8 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
     tsec.reset(new HostTimer("batch: s2_build uploads"));
     S.d_inst.upload(inst, st);
     S.h_inst = inst;
-    S.d_entp.upload(entp, st);
-    S.d_wp.upload(wp, st);
+    S.d_entp.upload(entp.get(), at[B].ent, st);
+    S.d_wp.upload(wp.get(), at[B].ent, st);
     S.d_off.upload(off, st);
     S.d_nbr.upload(nbr, st);
     S.d_w.upload(w, st);
