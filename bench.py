@@ -50,6 +50,7 @@ def parse():
                     help="c5: config 5 (the metric's config, default); c2/c4: Wishart float32 "
                          "configs on the slot engine; c3: the 64-instance Wishart batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-heat-bath", action="store_true", help="skip the heat-bath sub-record")
     ap.add_argument("--cpu-sweeps", type=int, default=16, help="marginal sweeps of the CPU sample")
     return ap.parse_args()
 
@@ -198,33 +199,88 @@ def cpu_reference_rate(pr, betas, pens, sweeps, threads):
     return rate, kind, dt
 
 
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:  # noqa: BLE001
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_baseline_record(pr, betas, pens, sweeps, what):
+    """The reference on the host cores: all threads (the reported value) and
+    one thread, with the CPU model (BASELINE.md CPU-baseline plan)."""
+    nproc = os.cpu_count() or 1
+    rate_n, kind, dt_n = cpu_reference_rate(pr, betas, pens, sweeps, nproc)
+    s1 = max(1, sweeps // 8)
+    rate_1, _, dt_1 = cpu_reference_rate(pr, betas, pens, s1, 1)
+    return {"value": rate_n, "unit": UNIT, "cores": nproc if kind == "reference" else 1,
+            "kind": kind, "cpu_model": cpu_model(), "nproc": nproc,
+            "value_1thread": rate_1,
+            "sample": f"{what}; marginal rate of {1 + sweeps} vs 1 sweeps at RunConfig.threads="
+                      f"{nproc} ({dt_n:.1f} s of sweeping) and {1 + s1} vs 1 sweeps at threads=1 "
+                      f"({dt_1:.1f} s)"}
+
+
+def repo_libraries():
+    """Shared objects of this repo mapped into the process (/proc/self/maps)."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as fh:
+            for line in fh:
+                path = line.split()[-1]
+                if path.startswith(ROOT) and ".so" in path:
+                    libs.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
+def bench_config(args, pr, R, world):
+    """The workload description both arms print (identical dicts)."""
+    return {"workload": workload_name(args, pr, R, args.rule), "n_spins": int(pr.n),
+            "replicas": R, "sweeps_per_swap": args.sps, "rule": args.rule,
+            "rounds_per_step": args.rounds, "parallelism": f"replica-split x{world}",
+            "l2": "flushed between timed GPU steps (256 MB write)"}
+
+
 def run_reference_arm(args, rank, world):
+    """The unmodified reference run_2dpt (oracle/_ref/libtgref_mt.so: the
+    reference's own engine/mc/ising/constraints sources, mt19937_64,
+    Metropolis, FP64) on all host threads.  Rank 0 only; the engine library
+    is never loaded in this process."""
     if rank != 0:
         return
+    if args.rule != "metropolis":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference implements Metropolis only"}))
+        return
     pr, betas, pens = workload(args.n, args.workload)
+    R = len(betas) * len(pens)
     threads = os.cpu_count() or 1
-    vals = []
+    vals, dts = [], []
     kind = "reference"
-    dts = []
     for k in range(args.warmup + args.steps):
         rate, kind, dt = cpu_reference_rate(pr, betas, pens, args.cpu_sweeps, threads)
         if k >= args.warmup:
             vals.append(rate)
             dts.append(dt)
     value = statistics.median(vals)
-    sample = (f"run_2dpt on the full workload (N={pr.n}, 16x16 grid), marginal rate of "
-              f"{1 + args.cpu_sweeps} vs 1 sweeps, RunConfig.threads={threads}")
+    sample = (f"reference run_2dpt on the full workload (N={pr.n}, {R} replicas), marginal rate of "
+              f"{1 + args.cpu_sweeps} vs 1 sweeps per step, RunConfig.threads={threads}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * statistics.median(dts), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args, pr, 256, "Metropolis") +
-                               " (CPU reference, mt19937_64)",
-                   "n_spins": pr.n, "replicas": 256, "sweeps_per_step": args.cpu_sweeps},
+        "config": bench_config(args, pr, R, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "libraries_mapped": repo_libraries(),
     }
     print(json.dumps(line), flush=True)
 
@@ -367,13 +423,15 @@ def run_ours_batch(args, rank, world, local):
             flush=True)
 
 
-def run_ours(args, rank, world, local):
-    import numpy as np
+def device_leg(args, pr, betas, pens, rank, world, local, rule):
+    """Device-timed throughput: inputs resident in HBM, K steps of
+    args.rounds rounds (sweeps + swap phase + per-round digest record), L2
+    flushed between steps, CUDA events on the engine's stream, max over
+    ranks.  Returns the numbers of the line (and of the heat-bath record)."""
     import torch
+    from paper_2506_14781_b200 import _lib
     from paper_2506_14781_b200.api import Engine, RunConfig
 
-    torch.cuda.set_device(local)
-    pr, betas, pens = workload(args.n, args.workload)
     R = len(betas) * len(pens)
     nccl_id = None
     if world > 1:
@@ -385,15 +443,20 @@ def run_ours(args, rank, world, local):
     eng.set_problem(pr)
     eng.set_schedule(betas, pens)
     total = args.rounds * args.sps * (args.warmup + args.steps + 1)
-    cfg = RunConfig(total_sweeps=total, sweeps_per_swap=args.sps, seed=1, rule=args.rule,
-                    engine=args.engine, store_states=False, digest=False)
-    eng.init(cfg, flags=0)
+    cfg = RunConfig(total_sweeps=total, sweeps_per_swap=args.sps, seed=1, rule=rule,
+                    engine=args.engine, store_states=False, digest=True)
+    eng.init(cfg, flags=_lib.REC_DIGEST)  # per-round (f, g, feasible, target digest) records
     eng.set_profiling(True)
     stream = torch.cuda.ExternalStream(eng.stream_ptr())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    nrec = [0]
+
+    def sink(r, n, s, a, b):
+        nrec[0] += n
+        return 0
 
     def step():
-        eng.advance(args.rounds)
+        eng.advance(args.rounds, sink)
 
     for _ in range(args.warmup):
         step()
@@ -416,32 +479,52 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     barrier(world)
     info1 = eng.info()
+    eng.close()
     total_ms = reduce_max(sum(step_ms), world)
     sweeps = args.steps * args.rounds * args.sps
-    updates = float(pr.n) * R * sweeps  # all ranks together
-    value = updates / (total_ms / 1e3)
+    value = float(pr.n) * R * sweeps / (total_ms / 1e3)  # all ranks together
     launches = (info1["sweep_launches"] - info0["sweep_launches"]) + \
                (info1["other_launches"] - info0["other_launches"])
-    # roofline of the dominant kernel (the sweep): algorithmic bytes per launch / mean launch time
     n_sweep_launches = info1["sweep_launches"] - info0["sweep_launches"]
     mean_sweep_s = reduce_max(sweep_ms, world) / 1e3 / max(n_sweep_launches, 1)
     bal = b_alg(pr)
-    # updates of this rank per launch of the dominant kernel
+    # algorithmic bytes of this rank per launch of the dominant kernel
     bytes_per_launch = bal * pr.n * (R / world) * sweeps / max(n_sweep_launches, 1)
     peaks = load_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     smem_peak_gbs = 148 * 128 * sm_max * 1e6 / 1e9  # SURVEY.md §8d official smem roofline
     achieved_gbs = bytes_per_launch / mean_sweep_s / 1e9
-    clocks = clk.summary()
-    kname = info1.get("sweep_kernel") or dominant_kernel(args, world)  # the kernel the engine launched
-    traffic = ncu_traffic(kname, args, pr, R, sweeps / max(n_sweep_launches, 1))
-    eng.close()
+    kname = info1.get("sweep_kernel") or dominant_kernel(args, world)
+    return {"value": value, "total_ms": total_ms, "launches": launches, "bal": bal,
+            "mean_sweep_s": mean_sweep_s, "achieved_gbs": achieved_gbs, "peak_gbs": smem_peak_gbs,
+            "sm_max": sm_max, "kernel": kname, "clocks": clk.summary(), "sweeps": sweeps,
+            "sweeps_per_launch": sweeps / max(n_sweep_launches, 1), "records": nrec[0]}
+
+
+def run_ours(args, rank, world, local):
+    import numpy as np
+    import torch
+    from paper_2506_14781_b200 import _lib
+    from paper_2506_14781_b200.api import Engine, RunConfig
+
+    torch.cuda.set_device(local)
+    pr, betas, pens = workload(args.n, args.workload)
+    R = len(betas) * len(pens)
+    d = device_leg(args, pr, betas, pens, rank, world, local, args.rule)
+    traffic = ncu_traffic(d["kernel"], args, pr, R, d["sweeps_per_launch"])
+    hb = None
+    if args.workload == "c5" and args.rule == "metropolis" and not args.no_heat_bath:
+        # the north star's p-bit rule s = sign(tanh(beta h) - u) on the same workload
+        h = device_leg(args, pr, betas, pens, rank, world, local, "heat_bath")
+        hb = {"value": h["value"], "unit": UNIT, "ms_per_step": h["total_ms"] / args.steps,
+              "kernel": h["kernel"], "roofline_frac": h["achieved_gbs"] / h["peak_gbs"],
+              "achieved_gbs": h["achieved_gbs"], "clocks": h["clocks"], "gpu_launches": h["launches"]}
 
     # e2e: the public API with host buffers -- H2D of the instance (from pinned
-    # host memory), device preprocessing, init, the same rounds, records to a
-    # host sink, D2H of the target configuration.  N = 1: a fresh Engine per
-    # step (run_2dpt as a user calls it); N > 1: the Engine (its NCCL
-    # communicator) is the session, each step re-sends the instance.
+    # host memory), device preprocessing, init, the same rounds, per-round
+    # digest records to a host sink, D2H of the target configuration.  N = 1:
+    # a fresh Engine per step (run_2dpt as a user calls it); N > 1: the Engine
+    # (its NCCL communicator) is the session, each step re-sends the instance.
     def pinned(a):
         return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
 
@@ -449,7 +532,7 @@ def run_ours(args, rank, world, local):
     prp = Problem(pr.n, pinned(pr.ci), pinned(pr.cj), pinned(pr.cw), pinned(pr.fields),
                   pinned(pr.pa), pinned(pr.pb))
     cfg2 = RunConfig(total_sweeps=args.rounds * args.sps, sweeps_per_swap=args.sps, seed=2,
-                     rule=args.rule, engine=args.engine, store_states=False, digest=False)
+                     rule=args.rule, engine=args.engine, store_states=False, digest=True)
     h2d = sum(a.nbytes for a in (prp.ci, prp.cj, prp.cw, prp.fields, prp.pa, prp.pb)) + 8 * (
         len(betas) + len(pens))
     sess = None
@@ -467,7 +550,7 @@ def run_ours(args, rank, world, local):
         e.set_problem(prp)
         e.set_schedule(betas, pens)
         recs = []
-        e.run(cfg2, lambda r, n, s, a, b: recs.append(n) or 0, flags=0)
+        e.run(cfg2, lambda r, n, s, a, b: recs.append(n) or 0, flags=_lib.REC_DIGEST)
         tgt = e.state(R - 1)
         if sess is None:
             e.close()
@@ -484,38 +567,35 @@ def run_ours(args, rank, world, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        rate, kind, dt = cpu_reference_rate(pr, betas, pens, args.cpu_sweeps, threads)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads if kind == "reference" else 1, "kind": kind,
-               "sample": f"unmodified reference run_2dpt (mt19937_64, Metropolis, FP64) on the "
-                         f"same N={pr.n} instance and 16x16 grid; marginal rate of "
-                         f"{1 + args.cpu_sweeps} vs 1 sweeps ({dt:.1f} s of sweeping)"}
+        cpu = cpu_baseline_record(pr, betas, pens, args.cpu_sweeps,
+                                  f"unmodified reference run_2dpt (mt19937_64, Metropolis, FP64) on "
+                                  f"the same N={pr.n} instance and {R}-replica grid")
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": METRIC, "value": d["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "ms_per_step": d["total_ms"] / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic",
-            "config": {"workload": workload_name(args, pr, R, args.rule),
-                       "n_spins": pr.n, "replicas": R, "rounds_per_step": args.rounds,
-                       "engine": args.engine, "parallelism": f"replica-split x{world}",
-                       "l2": "flushed between timed steps (256 MB write)"},
-            "roofline": {"bound": "smem", "achieved": achieved_gbs, "peak": smem_peak_gbs,
-                         "unit": "GB/s", "frac": achieved_gbs / smem_peak_gbs,
+            "config": bench_config(args, pr, R, world),
+            "engine": args.engine,
+            "roofline": {"bound": "smem", "achieved": d["achieved_gbs"], "peak": d["peak_gbs"],
+                         "unit": "GB/s", "frac": d["achieved_gbs"] / d["peak_gbs"],
                          "traffic": traffic["bytes_per_launch"] if traffic else None,
                          "traffic_source": traffic["source"] if traffic else None,
-                         "issue": issue_roofline(traffic, value / world, sm_max),
-                         "kernel": kname,
-                         "bytes_per_update": bal,
-                         "mean_launch_ms": mean_sweep_s * 1e3,
+                         "issue": issue_roofline(traffic, d["value"] / world, d["sm_max"]),
+                         "kernel": d["kernel"],
+                         "bytes_per_update": d["bal"],
+                         "mean_launch_ms": d["mean_sweep_s"] * 1e3,
                          "peak_note": "148 SM x 128 B/clk x sm_max_mhz (MEASURED_PEAKS.json), "
                                       "SURVEY.md §8d"},
+            "heat_bath": hb,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": int(launches),
-            "clocks": clocks,
+            "gpu_launches": int(d["launches"]),
+            "records_per_step": d["records"] // max(args.steps + args.warmup, 1),
+            "clocks": d["clocks"],
         }
         print(json.dumps(line), flush=True)
 
@@ -561,14 +641,41 @@ def ncu_traffic(kname, args, pr, R, sweeps_per_launch):
     return None
 
 
+def spawn_or_check(args):
+    """--gpus N > 1 without torchrun: re-launch this command as N ranks (one
+    process per GPU over NCCL); under torchrun WORLD_SIZE must equal N."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is None:
+        if args.gpus > 1:
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                   f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                   "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+            sys.exit(subprocess.call(cmd))
+        return
+    if int(world) != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
+
+
 def main():
     args = parse()
+    spawn_or_check(args)
     if args.workload != "c5":
         args.engine = "slot"  # float32 Wishart couplings: the FP64 slot engine
-    rank, world, local = dist_setup(args.gpus)
     if args.impl == "reference":
-        run_reference_arm(args, rank, world)
-    elif args.workload == "c3":
+        # the reference arm never maps the engine library: instances are built
+        # with the pure-Python host helpers, the timed code is oracle/_ref
+        from paper_2506_14781_b200 import instances as I
+        I.use_native_helpers(False)
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference_arm(args, rank, int(os.environ.get("WORLD_SIZE", "1")))
+        return
+    rank, world, local = dist_setup(args.gpus)
+    if args.workload == "c3":
         run_ours_batch(args, rank, world, local)
     else:
         run_ours(args, rank, world, local)

@@ -162,7 +162,13 @@ def run(pr, betas, penalties, total_sweeps, sps=1, seed=1, rule="metropolis", rn
     out = _Outputs(*[_ptr(o.get(k)) for k, _ in _Outputs._fields_])
     err = C.create_string_buffer(512)
     if impl == "port":
-        rc = port_lib().tgo_run_2dpt(C.byref(p), C.byref(c), C.byref(out), err, 512)
+        if threads > 1:  # sweep threads of the port (result independent of the count)
+            os.environ["TGO_THREADS"] = str(int(threads))
+        try:
+            rc = port_lib().tgo_run_2dpt(C.byref(p), C.byref(c), C.byref(out), err, 512)
+        finally:
+            if threads > 1:
+                os.environ.pop("TGO_THREADS", None)
     else:
         variant = impl.split(":", 1)[1]
         rc = ref_lib(variant).tgr_run_2dpt(C.byref(p), C.byref(c), C.byref(out), int(threads),

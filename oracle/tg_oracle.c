@@ -15,6 +15,7 @@
 #include "tg_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -296,18 +297,57 @@ static inline uint64_t next_u53(draw_ctx_t* d, const rstate_t* st, int site) {
     return tgo_plane_u53(d->pkey, (uint32_t)(st->id >> 5), d->t, (uint32_t)site, st->id & 31);
 }
 
+/* u < T for the bit-plane uniform u = U53 * 2^-53 of (state, site, sweep),
+ * decided exactly with the bits of U53 drawn MSB first (philox_ref.h
+ * tgo_plane_u53 word layout: plane b = bit `lane` of word b & 3 of block
+ * b >> 2), stopping as soon as the comparison is decided.  Same result as
+ * tgo_u53_to_unit(tgo_plane_u53(...)) < T (tests/test_oracle_lazy.py). */
+static int plane_less(const draw_ctx_t* d, const rstate_t* st, int site, double T) {
+    if (!(T > 0.0)) return 0;
+    if (T >= 1.0) return 1; /* U53 <= 2^53 - 1 */
+    /* U53 < T * 2^53  <=>  U53 < K = ceil(T * 2^53) (exact: power-of-two scaling) */
+    const uint64_t K = (uint64_t)ceil(ldexp(T, 53));
+    const uint32_t grp = (uint32_t)(st->id >> 5);
+    const int lane = st->id & 31;
+    const uint32_t key[2] = {(uint32_t)d->pkey, (uint32_t)(d->pkey >> 32)};
+    for (int blk = 0; blk < 14; ++blk) {
+        const uint32_t ctr[4] = {(uint32_t)site, (uint32_t)d->t, (uint32_t)(d->t >> 32),
+                                 (uint32_t)blk | (grp << 4)};
+        uint32_t o[4];
+        tgo_philox4x32_10(ctr, key, o);
+        for (int w = 0; w < 4; ++w) {
+            const int b = blk * 4 + w;
+            if (b >= 53) return 0; /* U53 == K */
+            const uint32_t ub = (o[w] >> lane) & 1u;
+            const uint32_t kb = (uint32_t)(K >> (52 - b)) & 1u;
+            if (ub != kb) return ub < kb;
+        }
+    }
+    return 0;
+}
+
 /* metropolis_sweep, mc.cpp:21-35 (rule 0); heat-bath variant (rule 1) with
  * the same one-draw-per-spin contract and the same f/g bookkeeping. */
 static void sweep(const view_t* v, double beta, rstate_t* st, draw_ctx_t* d, int rule) {
     const int n = v->merged.n;
+    const int lazy = d->mode != TGO_RNG_SLOT;
     for (int i = 0; i < n; ++i) {
         const double local_i = st->local[i];
         const double de = 2.0 * (double)st->spins[i] * local_i;
-        const double u = tgo_u53_to_unit(next_u53(d, st, i));
         int flip;
-        if (rule == TGO_RULE_METROPOLIS) {
+        if (lazy) { /* bit-plane draws: the same u < T decided bit by bit */
+            if (rule == TGO_RULE_METROPOLIS) {
+                flip = (de <= 0.0 || plane_less(d, st, i, exp(-beta * de)));
+            } else {
+                const double p = 1.0 / (1.0 + exp(-2.0 * beta * local_i));
+                const int8_t nv = plane_less(d, st, i, p) ? (int8_t)1 : (int8_t)-1;
+                flip = nv != st->spins[i];
+            }
+        } else if (rule == TGO_RULE_METROPOLIS) {
+            const double u = tgo_u53_to_unit(next_u53(d, st, i));
             flip = (de <= 0.0 || u < exp(-beta * de));
         } else {
+            const double u = tgo_u53_to_unit(next_u53(d, st, i));
             const double p = 1.0 / (1.0 + exp(-2.0 * beta * local_i));
             const int8_t nv = (u < p) ? (int8_t)1 : (int8_t)-1;
             flip = nv != st->spins[i];
@@ -359,6 +399,17 @@ uint64_t tgo_derive(uint64_t master, uint64_t purpose, uint64_t index) {
 uint64_t tgo_bits(uint64_t seed, uint64_t n) { return tgo_stream_bits(seed, n); }
 uint64_t tgo_plane(uint64_t pkey, uint32_t grp, uint64_t t, uint32_t site, int lane) {
     return tgo_plane_u53(pkey, grp, t, site, lane);
+}
+int tgo_plane_less(uint64_t pkey, uint32_t grp, uint64_t t, uint32_t site, int lane, double T) {
+    draw_ctx_t d;
+    memset(&d, 0, sizeof d);
+    d.mode = TGO_RNG_PLANE;
+    d.pkey = pkey;
+    d.t = t;
+    rstate_t st;
+    memset(&st, 0, sizeof st);
+    st.id = (int)(grp << 5) | lane;
+    return plane_less(&d, &st, (int)site, T);
 }
 
 int tgo_energy_breakdown(const tgo_problem* p, double penalty, const int8_t* s, double* f,
@@ -434,6 +485,76 @@ static int check_monotone(const double* v, int len, const char* what, char* err,
     return TGO_OK;
 }
 
+/* One round's sweeps of every replica (engine.cpp:125-132, for_each_replica
+ * :61-77): replicas are independent between swap phases, so a strided
+ * partition over threads (r = w mod T, as the reference) gives the same
+ * result for any thread count. */
+typedef struct {
+    const view_t* views;
+    const tgo_run_cfg* cfg;
+    rstate_t* rep;
+    const uint64_t* slot_seed;
+    uint64_t* slot_ctr;
+    uint64_t pkey;
+    int64_t rn;
+    int R, J;
+    int64_t sps;
+    int w, T;
+} sweep_job_t;
+
+static void* sweep_worker(void* arg) {
+    const sweep_job_t* jb = (const sweep_job_t*)arg;
+    for (int r = jb->w; r < jb->R; r += jb->T) {
+        const view_t* v = &jb->views[r % jb->J];
+        const double beta = jb->cfg->betas[r / jb->J];
+        for (int64_t s = 0; s < jb->sps; ++s) {
+            draw_ctx_t d;
+            d.mode = jb->cfg->rng_mode;
+            d.slot_seed = jb->slot_seed[r];
+            d.slot_ctr = &jb->slot_ctr[r];
+            d.pkey = jb->pkey;
+            d.t = (uint64_t)((jb->rn - 1) * jb->sps + s);
+            sweep(v, beta, &jb->rep[r], &d, jb->cfg->rule);
+        }
+        if (jb->rn % REFRESH_INTERVAL == 0) refresh(v, &jb->rep[r]);
+    }
+    return NULL;
+}
+
+static void run_sweeps(const sweep_job_t* job, int T) {
+    if (T <= 1) {
+        sweep_worker((void*)job);
+        return;
+    }
+    pthread_t th[256];
+    sweep_job_t jobs[256];
+    int started = 0;
+    for (int w = 0; w < T; ++w) {
+        jobs[w] = *job;
+        jobs[w].w = w;
+        jobs[w].T = T;
+    }
+    for (int w = 1; w < T; ++w) {
+        if (pthread_create(&th[w], NULL, sweep_worker, &jobs[w]) != 0) break;
+        started = w;
+    }
+    /* threads that could not start: their share runs here */
+    for (int w = started + 1; w < T; ++w) sweep_worker(&jobs[w]);
+    sweep_worker(&jobs[0]);
+    for (int w = 1; w <= started; ++w) pthread_join(th[w], NULL);
+}
+
+/* TGO_THREADS (environment, default 1): sweep threads of tgo_run_2dpt; the
+ * result does not depend on it. */
+static int oracle_threads(int R, int n) {
+    const char* e = getenv("TGO_THREADS");
+    int t = e ? atoi(e) : 1;
+    if (t > 256) t = 256;
+    if (t > R) t = R;
+    if ((int64_t)R * n < 65536) t = 1;
+    return t < 1 ? 1 : t;
+}
+
 int tgo_run_2dpt(const tgo_problem* prob, const tgo_run_cfg* cfg, tgo_outputs* out, char* err,
                  int errlen) {
     model_t cost;
@@ -489,23 +610,12 @@ int tgo_run_2dpt(const tgo_problem* prob, const tgo_run_cfg* cfg, tgo_outputs* o
 
     const int64_t sps = cfg->sweeps_per_swap;
     const int64_t n_swap = cfg->total_sweeps / sps;
+    const int n_threads = oracle_threads(R, n);
     int direction = 1;
     for (int64_t rn = 1; rn <= n_swap; ++rn) { /* engine.cpp:121-217 */
         const int even_swap = (rn % 2 == 0) ? 1 : 0;
-        for (int r = 0; r < R; ++r) {
-            const view_t* v = &views[r % J];
-            const double beta = cfg->betas[r / J];
-            for (int64_t s = 0; s < sps; ++s) {
-                draw_ctx_t d;
-                d.mode = cfg->rng_mode;
-                d.slot_seed = slot_seed[r];
-                d.slot_ctr = &slot_ctr[r];
-                d.pkey = pkey;
-                d.t = (uint64_t)((rn - 1) * sps + s);
-                sweep(v, beta, &rep[r], &d, cfg->rule);
-            }
-            if (rn % REFRESH_INTERVAL == 0) refresh(v, &rep[r]);
-        }
+        sweep_job_t job = {views, cfg, rep, slot_seed, slot_ctr, pkey, rn, R, J, sps, 0, 1};
+        run_sweeps(&job, n_threads);
         int do_p, do_b;
         if (I == 1 && J == 1) { do_p = do_b = 0; }
         else if (I == 1) { do_p = 1; do_b = 0; }

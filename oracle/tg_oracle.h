@@ -157,6 +157,8 @@ void tgo_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 uint64_t tgo_derive(uint64_t master, uint64_t purpose, uint64_t index);
 uint64_t tgo_bits(uint64_t seed, uint64_t n);
 uint64_t tgo_plane(uint64_t pkey, uint32_t grp, uint64_t t, uint32_t site, int lane);
+/* lazy MSB-first decision u < T on the bit-plane uniform (tests only) */
+int tgo_plane_less(uint64_t pkey, uint32_t grp, uint64_t t, uint32_t site, int lane, double T);
 
 #ifdef __cplusplus
 }

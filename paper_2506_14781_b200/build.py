@@ -17,7 +17,6 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtempergrid_b200.so")
-CPPLIB = os.path.join(PKG, "libtempergrid_cpp.so")
 SOURCES = ["kernels.cu", "capi.cu", "host_common.cu", "host_plane.cu", "host_slot.cu",
            "host_run.cu", "host_extras.cu", "plane_sweep.cu", "plane_tpw.cu", "slot_engine.cu", "prep.cu"]
 HEADERS = ["engine.cuh", "kernels.cuh", "philox.cuh", "plane_device.cuh", "plane_round.cuh", "host.cuh"]
@@ -81,20 +80,6 @@ def build_engine(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
-def build_cpp(force: bool = False) -> str:
-    """C++ mirror of the reference API (tempergrid::run_2dpt over the C ABI)."""
-    src = os.path.join(CSRC, "tempergrid_api.cpp")
-    hdr = os.path.join(CSRC, "tempergrid", "tempergrid.hpp")
-    if not os.path.exists(src):
-        return ""
-    if not force and not _stale(CPPLIB, [src, hdr, LIB]):
-        return CPPLIB
-    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", CSRC, "-I", os.path.join(ROOT, "include"),
-           "-o", CPPLIB, src, "-L", PKG, "-ltempergrid_b200", "-Wl,-rpath,$ORIGIN"]
-    subprocess.run(cmd, check=True)
-    return CPPLIB
-
-
 def build_oracle() -> None:
     targets = ["port"]
     if os.path.isdir("/root/reference/proj"):
@@ -106,7 +91,6 @@ def main(argv=None) -> int:
     argv = sys.argv[1:] if argv is None else argv
     force = "--force" in argv
     build_engine(force=force, verbose="-v" in argv)
-    build_cpp(force=force)
     if "--all" in argv:
         build_oracle()
     print(LIB)

@@ -62,6 +62,27 @@ struct TgFail {
 
 [[noreturn]] void fail(int code, const char* fmt, ...);
 
+// Run `work` on the calling thread and up to nt - 1 helper threads.  Helper
+// creation may fail (pids / cgroup limits): the threads already started are
+// always joined and the caller's own run of `work` covers the rest (`work`
+// pulls its items from a shared counter).
+template <class F>
+void run_pool(int nt, F& work) {
+    std::vector<std::thread> pool;
+    struct Joiner {
+        std::vector<std::thread>& p;
+        ~Joiner() { for (auto& th : p) if (th.joinable()) th.join(); }
+    } joiner{pool};
+    for (int t = 1; t < nt; ++t) {
+        try {
+            pool.emplace_back(work);
+        } catch (...) {
+            break;
+        }
+    }
+    work();
+}
+
 #define CK(x)                                                                                  \
     do {                                                                                       \
         cudaError_t e_ = (x);                                                                  \

@@ -356,15 +356,20 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
                 }
             }
         };
-        std::vector<std::thread> pool;
-        for (int t = 1; t < nt; ++t) pool.emplace_back(work);
-        work();
-        for (auto& th : pool) th.join();
+        run_pool(nt, work);
         for (int b = 0; b < B; ++b)  // the first failing instance's error, as a sequential loop would
             if (err[b]) std::rethrow_exception(err[b]);
     }
     for (int b = 1; b < B; ++b)
-        if (dup[b]) S.prep[b] = S.prep[b - 1];
+        if (dup[b]) {
+            // same graph, possibly another schedule: the FP32 error bands
+            // depend on this instance's own max |beta| and max P
+            S.prep[b] = S.prep[b - 1];
+            double pmax = 0.0, bmax = 0.0;
+            for (double p : c.batch[b].pens) pmax = std::max(pmax, p);
+            for (double be : c.batch[b].betas) bmax = std::max(bmax, std::fabs(be));
+            s2_bands(S.prep[b], bmax, pmax);
+        }
     int D = 4;
     for (const auto& P : S.prep) D = std::max(D, P.D);
     S.D = D;
@@ -394,6 +399,10 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
                         a.nbr + P.nbr.size(), a.w + P.w.size(), a.cm + P.cm.size(), a.h + P.h.size(),
                         a.h32 + P.h32.size(), a.perm + P.order.size()};
     }
+    // the device table keeps 32-bit offsets (entp_off, csr_off, nbr_off, h_off)
+    if (at[B].ent > (size_t)INT_MAX || at[B].off > (size_t)INT_MAX || at[B].nbr > (size_t)INT_MAX ||
+        at[B].h > (size_t)INT_MAX)
+        fail(TG_ERR_RESOURCE, "batch: concatenated instance arrays exceed 2^31 entries");
     cstart.resize(at[B].cst);
     entp.reset(new int2[std::max<size_t>(at[B].ent, 1)]);
     wp.reset(new double[std::max<size_t>(at[B].ent, 1)]);
@@ -460,10 +469,7 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
         auto work = [&] {
             for (int b; (b = next.fetch_add(1)) < B;) fill(b);
         };
-        std::vector<std::thread> pool;
-        for (int t = 1; t < nt; ++t) pool.emplace_back(work);
-        work();
-        for (auto& th : pool) th.join();
+        run_pool(nt, work);
     }
     S.max_colors = max_colors;
     // item prefix tables: per colour, per instance, upper bound of Philox pairs x groups
@@ -627,8 +633,18 @@ void s2_drain(tg_ctx& c, int filled, int64_t first_round, const BatchSinkCtx& si
         CK(cudaMemcpy2DAsync(S.h_acc.data(), sizeof(int64_t) * cap * (np + nb), S.d_rec_acc.p,
                              sizeof(int64_t) * cap * (np + nb), sizeof(int64_t) * filled * (np + nb), B,
                              cudaMemcpyDeviceToHost, st));
-    if (S.d_rec_states.p) CK(cudaMemcpyAsync(S.h_states.data(), S.d_rec_states.p, S.h_states.size(),
-                                             cudaMemcpyDeviceToHost, st));
+    if (S.d_rec_states.p) {
+        if (filled == cap) {
+            CK(cudaMemcpyAsync(S.h_states.data(), S.d_rec_states.p, S.h_states.size(),
+                               cudaMemcpyDeviceToHost, st));
+        } else {  // only the filled rows of each instance's block
+            for (int b = 0; b < B; ++b) {
+                const size_t o = (size_t)S.state_off[b] * S.slots * cap;
+                CK(cudaMemcpyAsync(S.h_states.data() + o, S.d_rec_states.p + o,
+                                   (size_t)filled * S.prep[b].n * S.slots, cudaMemcpyDeviceToHost, st));
+            }
+        }
+    }
     CK(cudaStreamSynchronize(st));
     if (!sink.fn) return;
     for (int b = 0; b < B; ++b) {

@@ -20,6 +20,7 @@ the canonical colour order the engine sweeps in.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, Tuple
 
@@ -143,15 +144,29 @@ def min_copies(n_logical_degree: int, max_degree: int) -> int:
 
 # ----------------------------------------------------------- colour order
 
+# False: never load the engine library for instance construction (bench.py's
+# reference arm must not map libtempergrid_b200.so; set TG_INSTANCES_PY=1 or
+# call use_native_helpers(False)).
+_NATIVE_HELPERS = os.environ.get("TG_INSTANCES_PY", "0") in ("", "0")
+
+
+def use_native_helpers(on: bool) -> None:
+    global _NATIVE_HELPERS
+    _NATIVE_HELPERS = bool(on)
+
+
 def canonical_order(pr: Problem) -> Tuple[np.ndarray, np.ndarray, int]:
     """Greedy index-order colouring of cost+chain edges, then a stable sort by
     (colour, chain degree, cost degree).  Returns (order, colour, n_colours).
     Uses the engine library's host helper (tg_canonical_order) when it is
-    built, else the pure-Python restatement below; tests check they agree."""
-    try:
-        return canonical_order_native(pr)
-    except Exception:  # noqa: BLE001 - library not built: host-only fallback
-        return canonical_order_py(pr)
+    built and allowed, else the pure-Python restatement below; tests check
+    they agree."""
+    if _NATIVE_HELPERS:
+        try:
+            return canonical_order_native(pr)
+        except Exception:  # noqa: BLE001 - library not built: host-only path
+            pass
+    return canonical_order_py(pr)
 
 
 def canonical_order_native(pr: Problem) -> Tuple[np.ndarray, np.ndarray, int]:
