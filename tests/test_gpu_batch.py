@@ -64,3 +64,19 @@ def test_config3_shape_batch_runs():
     run_2dpt_batch(prs, scheds, RunConfig(total_sweeps=20, store_states=False, digest=False),
                    list(range(8)), sink=sink)
     assert counts == {b: 20 for b in range(8)}
+
+
+def test_batch_duplicate_graph_other_schedule():
+    """Two consecutive instances with the same graph but different schedules
+    (the second with larger beta and P): the duplicate's preparation is
+    reused, its FP32 error bands must follow its own schedule."""
+    pr = I.wishart_planted(12, 0.5, seed=9)
+    scheds = [Schedule([0.2, 0.5, 1.0], [0.0, 0.1, 0.2]), Schedule([0.5, 3.0, 9.0], [0.5, 2.0, 6.0])]
+    seeds = [3, 4]
+    traces = run_2dpt_batch([pr, pr], scheds, RunConfig(total_sweeps=150, sweeps_per_swap=1,
+                                                        store_states=True), seeds)
+    for b in range(2):
+        o = O.run(pr, scheds[b].betas, scheds[b].penalties, 150, 1, seed=seeds[b], rng="slot",
+                  states=True)
+        np.testing.assert_allclose([r.f for r in traces[b].records], o.f, rtol=1e-9, atol=1e-9)
+        np.testing.assert_array_equal(np.stack([r.state for r in traces[b].records]), o.states)
