@@ -127,6 +127,7 @@ struct RoundArgs {
     int flush_every;       // tpw kernel: items between vertical-counter flushes (host: <= 255 / max bonds)
     int n_warps;           // tpw kernel: warps of the launch
     int log_w;             // tpw kernel: log2 of the words per site
+    int c5_nfree[2];       // c5 kernel: chain-free sites of colours 0, 1 (they precede the chain sites)
     const uint64_t* ktab;
     int ktab_row;
     uint32_t* kp;

@@ -309,6 +309,8 @@ struct tg_ctx {
     int plane_grid = 0, plane_block = kPlaneThreads;
     int fused_grid = 0, fused_fast = 0, fused_block = kPlaneThreads, fused_wv = 4;
     int fused_tpw = 0, tpw_fast = 0;
+    int fused_c5 = 0;                // config-5 kernel (plane_c5.cu) for the fused round loop
+    int c5_nfree[2] = {0, 0};        // chain-free sites of colours 0, 1
     int tpw_sweep_grid = 0;          // sweep-only tpw kernel grid (0: plane_sweep_kernel)
     size_t tpw_sweep_smem = 0;
     const char* sweep_kernel = "";   // dominant sweep kernel of the last advance (tg_info)     // thread-per-(site, word) kernel (plane_tpw.cu) instead of plane_rounds_kernel

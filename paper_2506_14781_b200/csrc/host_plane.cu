@@ -94,6 +94,7 @@ void build_plane_types_device(tg_ctx& c, std::vector<PlaneType>& types, std::vec
     std::vector<int> tid_of((kMaxDC + 1) * (kMaxDQ + 1), -1);
     chunk_off.assign(c.n_colors + 1, 0);
     int start = 0, cur_col = -1, nch = 0;
+    c.c5_nfree[0] = c.c5_nfree[1] = 0;
     rt.n = (int)P.run_keys.size();
     for (int q = 0; q < rt.n; ++q) {
         const unsigned key = P.run_keys[q];
@@ -111,6 +112,7 @@ void build_plane_types_device(tg_ctx& c, std::vector<PlaneType>& types, std::vec
             tid_of[tkey] = (int)types.size();
             types.push_back(t);
         }
+        if (dq == 0 && col < 2) c.c5_nfree[col] += cnt;
         rt.start[q] = start;
         rt.cnt[q] = cnt;
         rt.type[q] = tid_of[tkey];
@@ -143,6 +145,10 @@ void build_plane(tg_ctx& c) {
             CK(plane_chunk_bases(c.d_chunks.p, rt.cpref[rt.n], c.d_base_dev.p, st, c.sms));
         } else {
             build_plane_structure_device(c, types, chunks, chunk_off);
+            c.c5_nfree[0] = c.c5_nfree[1] = 0;
+            for (int col = 0; col < std::min(2, c.n_colors); ++col)
+                for (int q = chunk_off[col]; q < chunk_off[col + 1]; ++q)
+                    if (types[chunks[q].type].dq == 0) c.c5_nfree[col] += chunks[q].len;
             c.d_chunks.upload(chunks, st);
             CK(plane_chunk_bases(c.d_chunks.p, (int)chunks.size(), c.d_base_dev.p, st, c.sms));
         }
@@ -207,6 +213,10 @@ void build_plane(tg_ctx& c) {
         }
     }
     chunk_off[c.n_colors] = (int)chunks.size();
+    c.c5_nfree[0] = c.c5_nfree[1] = 0;
+    for (int col = 0; col < std::min(2, c.n_colors); ++col)
+        for (int q = chunk_off[col]; q < chunk_off[col + 1]; ++q)
+            if (types[chunks[q].type].dq == 0) c.c5_nfree[col] += chunks[q].len;
     c.d_nbr.upload(nbr, st);
     c.d_chunks.upload(chunks, st);
     build_plane_rest(c, types, chunk_off);
@@ -350,7 +360,28 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
         const int fb = kernel_fit(fn, 0, c.tpw_sweep_smem).blocks_per_sm;
         if (fb >= 1) c.tpw_sweep_grid = fb * c.sms;
     }
-    if (c.fused_tpw) {
+    // config-5 kernel (plane_c5.cu): Metropolis on the tpw config-5 path with
+    // a 2-colouring, at least two words per site row; TG_PLANE_C5=0 disables
+    c.fused_c5 = 0;
+    {
+        bool ok = c.fused_tpw && c.tpw_fast && c.cfg.rule == TG_RULE_METROPOLIS && c.n_colors == 2 &&
+                  c.W >= 2 && c.n_types <= 2 && c.d_nbr4.p != nullptr;
+        int nfree_type = 0;
+        for (const auto& t : types) nfree_type += t.dq == 0;
+        ok = ok && nfree_type <= 1;
+        if (const char* e = std::getenv("TG_PLANE_C5")) ok = ok && std::atoi(e) != 0;
+        if (ok) {
+            const size_t smem = c5_smem_bytes(c.R, c.W);
+            const int fb = kernel_fit(plane_c5_fn(), kC5Threads, smem).blocks_per_sm;
+            if (fb >= 1) {
+                c.fused_c5 = 1;
+                c.fused_grid = fb * c.sms;
+                c.fused_block = kC5Threads;
+                c.fused_smem = smem;
+            }
+        }
+    }
+    if (c.fused_tpw && !c.fused_c5) {
         const void* fn = plane_tpw_fn(c.cfg.rule, c.tpw_fast);
         c.fused_block = kernel_fit(fn, 0, 0).max_threads;  // the kernel's launch bound
         c.fused_smem = tpw_smem_bytes(c.R, c.W, c.fused_block);
@@ -460,7 +491,9 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         // tpw kernel: the last ~item per warp of each colour phase is handed
         // out dynamically ([2 parities][colours][sps] counters)
         r.work = nullptr;
-        if (c.fused_tpw && c.tpw_fast) {
+        r.c5_nfree[0] = c.c5_nfree[0];
+        r.c5_nfree[1] = c.c5_nfree[1];
+        if (c.fused_tpw && c.tpw_fast && !c.fused_c5) {
             const size_t need = (size_t)2 * c.n_colors * c.cfg.sweeps_per_swap;
             if (c.d_work.n < need) { c.d_work.alloc(need); c.d_work.zero(st); }
             r.work = std::getenv("TG_TPW_STATIC") ? nullptr : c.d_work.p;
@@ -471,10 +504,12 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         r.perm = c.d_perm.p;
         void* args[] = {&a, &r};
         if (c.profiling) CK(cudaEventRecord(c.ev[0], st));
-        c.sweep_kernel = c.fused_tpw ? "plane_tpw_rounds_kernel" : "plane_rounds_kernel";
-        CK(cudaLaunchCooperativeKernel(c.fused_tpw ? plane_tpw_fn(c.cfg.rule, c.tpw_fast)
-                                                   : plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast),
-                                       dim3(c.fused_grid), dim3(c.fused_block), args, c.fused_smem, st));
+        c.sweep_kernel = c.fused_c5 ? "plane_c5_rounds_kernel"
+                                    : c.fused_tpw ? "plane_tpw_rounds_kernel" : "plane_rounds_kernel";
+        const void* fn = c.fused_c5 ? plane_c5_fn()
+                                    : c.fused_tpw ? plane_tpw_fn(c.cfg.rule, c.tpw_fast)
+                                                  : plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast);
+        CK(cudaLaunchCooperativeKernel(fn, dim3(c.fused_grid), dim3(c.fused_block), args, c.fused_smem, st));
         if (c.profiling) CK(cudaEventRecord(c.ev[1], st));
         c.sweep_launches++;
         const int64_t first = c.rounds_done + 1;

@@ -1,0 +1,422 @@
+// plane_c5.cu -- the config-5 fused round kernel of the PLANE engine
+// (Metropolis): two 32-replica words per thread, chain-free and chain sites
+// in separate item loops.
+//
+// Same contract, and therefore the same trajectories bit for bit, as
+// plane_tpw_rounds_kernel / plane_rounds_kernel: the reference sweep
+// (mc.cpp:21-35) over the canonical colour order, thresholds
+// K = ceil(T * 2^53) compared MSB-first against bit planes of Philox4x32-10
+// draws with counter {site, t_lo, t_hi, group << 4 | block}, labels permuted
+// by the swap phase (plane_round.cuh).  It applies to instances whose sites
+// all have cost degree 3 (J = +-1, h = 0) and chain degree 0 or 1 with a
+// proper 2-colouring (BASELINE config 5): every neighbour of a colour-1 site
+// is colour 0, so the unsatisfied bonds a colour-1 site leaves behind are c if
+// it flips and 3 - c otherwise (c = satisfied bonds before the update).
+//
+// Work layout: thread = (site, word pair); a warp item is S = 64 / W
+// consecutive sites x the W / 2 word pairs of their rows (lane = site * W/2 +
+// pair), so each row load is one 8-byte access per lane and W/2 lanes cover a
+// whole 32-byte row.  Per colour phase the chain-free sites and the chain
+// sites (contiguous in the canonical order) are walked by two loops, so every
+// item is of one kind and no per-item type test or straddling exists.  Per
+// thread and phase: the class-2/3 threshold planes 0-7 of both words in
+// registers, 4 Philox blocks per chain-free item (the two unconditional blocks
+// of each word, sharing the site's round-1/2/3 products).  Chain-free pairs
+// still undecided after 8 planes go to a per-warp shared-memory queue (one
+// 16-byte record) resolved 32 at a time, one per lane.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "engine.cuh"
+#include "kernels.cuh"
+#include "philox_plane.cuh"
+#include "plane_device.cuh"
+#include "plane_round.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tg {
+
+constexpr int kC5VB = 8;  // vertical counter planes (<= 255 per lane between flushes)
+
+extern __shared__ __align__(16) int c5_sm[];
+
+// Dynamic shared memory: queues [warps][kC5QCap] int4 | s_cc[32W] | s_cq[32W]
+// | the round block (labels, energies) of plane_round.cuh.
+__device__ __forceinline__ int4* c5_queue(int warp) {
+    return reinterpret_cast<int4*>(c5_sm) + warp * kC5QCap;
+}
+__device__ __forceinline__ int* c5_cnt() { return c5_sm + (kC5Threads / 32) * kC5QCap * 4; }
+
+// V += m (2-bit bit-sliced value) in kC5VB-bit vertical arithmetic.
+template <int NB>
+__device__ __forceinline__ void c5_vadd(uint32_t (&V)[kC5VB], uint32_t m0, uint32_t m1) {
+    uint32_t carry = 0u;
+#pragma unroll
+    for (int b = 0; b < kC5VB; ++b) {
+        const uint32_t x = V[b];
+        if (b < NB) {
+            const uint32_t y = b == 0 ? m0 : m1;
+            V[b] = x ^ y ^ carry;
+            carry = (x & y) | (carry & (x ^ y));
+        } else {
+            V[b] = x ^ carry;
+            carry = x & carry;
+        }
+    }
+}
+
+// Per-replica totals of the warp's vertical counters of word `j` of each
+// lane's pair, added into s_cnt[(2 * pair + j) * 32 + replica]; V is
+// cleared.  Lanes holding the same pair (lane = p * WP + pair) are summed by
+// a butterfly; the sums' planes are packed S per 32x32 transpose, after which
+// lane l reads replica l's bits of every pair.
+template <int LOGWP>
+__device__ __noinline__ void c5_vflush(uint4 lo, uint4 hi, int j, int* s_cnt) {
+    constexpr int WP = 1 << LOGWP, LOGS = 5 - LOGWP, S = 1 << LOGS;
+    constexpr int NB = kC5VB + LOGS;
+    constexpr int NQ = (NB + S - 1) / S;
+    const int lane = threadIdx.x & 31;
+    uint32_t E[NB];
+    const uint32_t V[kC5VB] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+    for (int b = 0; b < NB; ++b) E[b] = b < kC5VB ? V[b] : 0u;
+#pragma unroll
+    for (int lv = 0; lv < LOGS; ++lv) {
+        uint32_t carry = 0u;
+#pragma unroll
+        for (int b = 0; b <= kC5VB + lv && b < NB; ++b) {
+            const uint32_t x = E[b];
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, x, WP << lv);
+            E[b] = x ^ o ^ carry;
+            carry = (x & o) | (carry & (x ^ o));
+        }
+    }
+    const int p_me = lane >> LOGWP;
+    uint32_t T[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        uint32_t v = 0u;
+#pragma unroll
+        for (int p = 0; p < S; ++p)
+            if (q * S + p < NB) v = (p == p_me) ? E[q * S + p] : v;
+        T[q] = warp_transpose32(v);
+    }
+#pragma unroll
+    for (int w = 0; w < WP; ++w) {
+        int val = 0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+            for (int p = 0; p < S; ++p)
+                if (q * S + p < NB) val += (int)((T[q] >> (p * WP + w)) & 1u) << (q * S + p);
+        }
+        if (val) atomicAdd(s_cnt + (2 * w + j) * 32 + lane, val);
+    }
+}
+
+__device__ __forceinline__ void c5_flush(uint32_t (&V)[kC5VB], int logWP, int j, int* s_cnt) {
+    const uint4 lo = make_uint4(V[0], V[1], V[2], V[3]), hi = make_uint4(V[4], V[5], V[6], V[7]);
+    switch (logWP) {
+        case 0: c5_vflush<0>(lo, hi, j, s_cnt); break;
+        case 1: c5_vflush<1>(lo, hi, j, s_cnt); break;
+        case 2: c5_vflush<2>(lo, hi, j, s_cnt); break;
+        case 3: c5_vflush<3>(lo, hi, j, s_cnt); break;
+        default: c5_vflush<4>(lo, hi, j, s_cnt); break;
+    }
+#pragma unroll
+    for (int b = 0; b < kC5VB; ++b) V[b] = 0u;
+}
+
+// Resolve queue entries [base, base + n) (n <= 32) of the calling warp, one
+// per lane: Philox blocks 2.. of the entry's (site, word), class-2/3 planes
+// 8.. of its word (kpc), late flips XORed into the stored word (same warp,
+// after __syncwarp) and, when counting, the unsatisfied-bond correction of a
+// late flip: 2c - 3 = 1 + 2 c0 (undecided lanes have c = 2 + c0).
+__device__ __noinline__ void c5_drain(const PlaneArgs& a, int base, int n, uint32_t tlo, uint32_t thi,
+                                      int t30, bool count, int* s_cc) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    const bool mine = lane < n;
+    int4 e = make_int4(0, 0, 0, 0);
+    if (mine) e = c5_queue(threadIdx.x >> 5)[base + lane];
+    const uint32_t site = (uint32_t)e.x;
+    const int w = e.y;
+    uint32_t und = (uint32_t)e.z;
+    const uint32_t c0 = (uint32_t)e.w;
+    const uint32_t grp4 = (uint32_t)(a.w_global0 + w) << 4;
+    const uint4* kc2 = reinterpret_cast<const uint4*>(a.kpc + ((size_t)w * a.n_types + t30) * 128);
+    uint32_t lt = 0u;
+    const PhiloxT P = philox_t(tlo, thi, a.pks);
+#pragma unroll 1
+    for (int blk = 2; blk < 14; ++blk) {
+        if (!__any_sync(0xffffffffu, und)) break;
+        const u32x4 r = philox_plane(site, grp4 | (uint32_t)blk, P, a.pks);
+        compare4_sel(c0, __ldg(kc2 + blk), __ldg(kc2 + 16 + blk), r, und, lt);
+    }
+    if (lt) {
+        a.spins[(size_t)site * a.W + w] ^= lt;
+        if (count) {
+            uint32_t ex = lt;
+            while (ex) {
+                const int l = __ffs(ex) - 1;
+                ex &= ex - 1;
+                atomicAdd(s_cc + w * 32 + l, 1 + 2 * (int)((c0 >> l) & 1u));
+            }
+        }
+    }
+    __syncwarp();
+}
+
+// Per-thread constants of a colour phase.
+struct C5Ctx {
+    uint4 k2a[2], k2b[2], k3a[2], k3b[2];  // planes 0-7 of classes 2, 3 of the two words
+    uint32_t act[2];
+    uint32_t g[4];                         // Philox word 3 of the 4 unconditional blocks
+    uint32_t tlo, thi;
+    PhiloxT P;
+};
+
+// One colour phase: chain-free items, then chain items.
+__device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, bool count, int gw,
+                                         int nw, int logW, uint32_t (&V0)[kC5VB], uint32_t (&V1)[kC5VB],
+                                         int t30, int t31, int nfree) {
+    int* s_cc = c5_cnt();
+    int* s_cq = s_cc + 32 * a.W;
+    const int lane = threadIdx.x & 31;
+    const int logWP = logW - 1;
+    const int WP = 1 << logWP;
+    const int S = 32 >> logWP;               // sites per item
+    const int wp = lane & (WP - 1), sl = lane >> logWP;
+    const int w0 = 2 * wp;
+    const int cs = a.color_start[c], ce = a.color_start[c + 1];
+    const int cf = cs + nfree;               // first chain site of the colour
+    count = count && c == 1;
+    C5Ctx K;
+    {
+        const uint4* kc0 = reinterpret_cast<const uint4*>(a.kpc + ((size_t)w0 * a.n_types + t30) * 128);
+        const uint4* kc1 = reinterpret_cast<const uint4*>(a.kpc + ((size_t)(w0 + 1) * a.n_types + t30) * 128);
+        K.k2a[0] = kc0[0]; K.k2b[0] = kc0[1]; K.k3a[0] = kc0[16]; K.k3b[0] = kc0[17];
+        K.k2a[1] = kc1[0]; K.k2b[1] = kc1[1]; K.k3a[1] = kc1[16]; K.k3b[1] = kc1[17];
+    }
+    K.act[0] = a.active[w0];
+    K.act[1] = a.active[w0 + 1];
+    const uint32_t g0 = (uint32_t)(a.w_global0 + w0) << 4;
+    K.g[0] = g0; K.g[1] = g0 | 1u; K.g[2] = g0 + 16u; K.g[3] = (g0 + 16u) | 1u;
+    K.tlo = (uint32_t)t;
+    K.thi = (uint32_t)(t >> 32);
+    K.P = philox_t(K.tlo, K.thi, a.pks);
+    const char* base = reinterpret_cast<const char*>(a.spins + w0);
+    auto row = [&](uint32_t off) -> uint2 {   // off: word offset of a row (index << logW)
+        return *reinterpret_cast<const uint2*>(base + (size_t)off * 4u);
+    };
+    int qn = 0;
+    // ---------------------------------------------------------- chain-free
+    {
+        const int n_it = (nfree + S - 1) / S;
+        int it = gw;
+        int4 en = make_int4(0, 0, 0, 0);
+        if (it < n_it) {
+            const int site = cs + it * S + sl;
+            if (site < cf) en = __ldg(a.nbr4 + site);
+        }
+        for (; it < n_it; it += nw) {
+            const int4 e = en;
+            const uint32_t site = (uint32_t)(cs + it * S + sl);
+            const bool valid = (int)site < cf;
+            uint2 s = make_uint2(0u, 0u), x0 = s, x1 = s, x2 = s;
+            if (valid) {
+                s = row(site << logW);
+                x0 = row((uint32_t)e.x & 0x7fffffffu);
+                x1 = row((uint32_t)e.y & 0x7fffffffu);
+                x2 = row((uint32_t)e.z & 0x7fffffffu);
+            }
+            {
+                const int nx = it + nw;
+                en = make_int4(0, 0, 0, 0);
+                if (nx < n_it) {
+                    const int ns = cs + nx * S + sl;
+                    if (ns < cf) en = __ldg(a.nbr4 + ns);
+                }
+            }
+            u32x4 r[4];
+            philox_planeN<4>(site, K.g, K.P, a.pks, r);
+            const uint32_t m0s = (uint32_t)(e.x >> 31), m1s = (uint32_t)(e.y >> 31), m2s = (uint32_t)(e.z >> 31);
+            uint32_t und[2], ns[2], cl0[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const uint32_t sj = j ? s.y : s.x;
+                // satisfied bond k: J_ik s_i s_k = +1
+                const uint32_t a0 = ~(sj ^ (j ? x0.y : x0.x) ^ m0s);
+                const uint32_t a1 = ~(sj ^ (j ? x1.y : x1.x) ^ m1s);
+                const uint32_t a2 = ~(sj ^ (j ? x2.y : x2.x) ^ m2s);
+                const uint32_t c0 = a0 ^ a1 ^ a2;
+                const uint32_t c1 = (a0 & a1) | (a2 & (a0 ^ a1));
+                const uint32_t act = valid ? K.act[j] : 0u;
+                uint32_t u = c1 & act, lt = 0u;   // classes 0, 1 (de < 0): always taken
+                compare4_sel(c0, K.k2a[j], K.k3a[j], r[2 * j], u, lt);
+                compare4_sel(c0, K.k2b[j], K.k3b[j], r[2 * j + 1], u, lt);
+                const uint32_t take = (~c1 & act) | lt;
+                ns[j] = sj ^ take;
+                und[j] = u;
+                if (count) {
+                    if (j == 0) c5_vadd<2>(V0, ~(c0 ^ take) & act, ~(c1 ^ take) & act);
+                    else c5_vadd<2>(V1, ~(c0 ^ take) & act, ~(c1 ^ take) & act);
+                }
+                cl0[j] = c0;
+            }
+            if (valid)
+                *reinterpret_cast<uint2*>(const_cast<char*>(base) + (size_t)(site << logW) * 4u) =
+                    make_uint2(ns[0], ns[1]);
+            // deferred tail: pairs with lanes still undecided after 8 planes
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const uint32_t pend = __ballot_sync(0xffffffffu, und[j] != 0u);
+                if (pend) {
+                    if (und[j])
+                        c5_queue(threadIdx.x >> 5)[qn + __popc(pend & ((1u << lane) - 1u))] =
+                            make_int4((int)site, w0 + j, (int)und[j], (int)cl0[j]);
+                    qn += __popc(pend);
+                }
+            }
+            if (qn >= 32) {
+                qn -= 32;
+                c5_drain(a, qn, 32, K.tlo, K.thi, t30, count, s_cc);
+            }
+        }
+    }
+    while (qn > 0) {
+        const int n = qn < 32 ? qn : 32;
+        qn -= n;
+        c5_drain(a, qn, n, K.tlo, K.thi, t30, count, s_cc);
+    }
+    if (count) {
+        c5_flush(V0, logWP, 0, s_cc);
+        c5_flush(V1, logWP, 1, s_cc);
+    }
+    // ---------------------------------------------------------- chain sites
+    const int nq = ce - cf;
+    if (nq > 0) {
+        const int n_it = (nq + S - 1) / S;
+        const uint32_t* kpb0 = a.kp + (size_t)w0 * a.kpw + a.ty[t31].kp_off;
+        const uint32_t* kpb1 = kpb0 + a.kpw;
+        uint32_t Q0[kC5VB], Q1[kC5VB];
+#pragma unroll
+        for (int b = 0; b < kC5VB; ++b) { Q0[b] = 0u; Q1[b] = 0u; }
+        for (int it = gw; it < n_it; it += nw) {
+            const uint32_t site = (uint32_t)(cf + it * S + sl);
+            const bool valid = (int)site < ce;
+            int4 e = make_int4(0, 0, 0, 0);
+            uint2 s = make_uint2(0u, 0u), x0 = s, x1 = s, x2 = s, y = s;
+            if (valid) {
+                e = __ldg(a.nbr4 + site);
+                s = row(site << logW);
+                x0 = row((uint32_t)e.x & 0x7fffffffu);
+                x1 = row((uint32_t)e.y & 0x7fffffffu);
+                x2 = row((uint32_t)e.z & 0x7fffffffu);
+                y = row((uint32_t)e.w);
+            }
+            u32x4 r[4];
+            philox_planeN<4>(site, K.g, K.P, a.pks, r);
+            const uint32_t m0s = (uint32_t)(e.x >> 31), m1s = (uint32_t)(e.y >> 31), m2s = (uint32_t)(e.z >> 31);
+            uint32_t ns[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const uint32_t sj = j ? s.y : s.x;
+                const uint32_t a0 = ~(sj ^ (j ? x0.y : x0.x) ^ m0s);
+                const uint32_t a1 = ~(sj ^ (j ? x1.y : x1.x) ^ m1s);
+                const uint32_t a2 = ~(sj ^ (j ? x2.y : x2.x) ^ m2s);
+                const uint32_t yj = j ? y.y : y.x;
+                const uint32_t cb[3] = {a0 ^ a1 ^ a2, (a0 & a1) | (a2 & (a0 ^ a1)), ~(sj ^ yj)};
+                const uint32_t act = valid ? K.act[j] : 0u;
+                const uint32_t* kpb = j ? kpb1 : kpb0;
+                const uint32_t always = mux_tree<3>(cb, kpb + kKPlanes * 8) & act;
+                uint32_t u = act & ~always, lt = 0u;
+                compare_block<3>(cb, kpb, 8, 0, r[2 * j], u, lt);
+                compare_block<3>(cb, kpb, 8, 1, r[2 * j + 1], u, lt);
+#pragma unroll 1
+                for (int blk = 2; blk < 14; ++blk) {
+                    if (!__any_sync(0xffffffffu, u)) break;
+                    const u32x4 rb = philox_plane(site, K.g[2 * j] | (uint32_t)blk, K.P, a.pks);
+                    compare_block<3>(cb, kpb, 8, blk, rb, u, lt);
+                }
+                const uint32_t take = (always | lt) & act;
+                ns[j] = sj ^ take;
+                if (count) {
+                    const uint32_t mq = (ns[j] ^ yj) & act;  // chain bond unsatisfied after the update
+                    if (j == 0) {
+                        c5_vadd<2>(V0, ~(cb[0] ^ take) & act, ~(cb[1] ^ take) & act);
+                        c5_vadd<1>(Q0, mq, 0u);
+                    } else {
+                        c5_vadd<2>(V1, ~(cb[0] ^ take) & act, ~(cb[1] ^ take) & act);
+                        c5_vadd<1>(Q1, mq, 0u);
+                    }
+                }
+            }
+            if (valid)
+                *reinterpret_cast<uint2*>(const_cast<char*>(base) + (size_t)(site << logW) * 4u) =
+                    make_uint2(ns[0], ns[1]);
+        }
+        if (count) {
+            c5_flush(V0, logWP, 0, s_cc);
+            c5_flush(V1, logWP, 1, s_cc);
+            c5_flush(Q0, logWP, 0, s_cq);
+            c5_flush(Q1, logWP, 1, s_cq);
+        }
+    }
+}
+
+// Persistent single-GPU kernel: n_rounds whole rounds of run_2dpt
+// (engine.cpp:121-216); one grid barrier per colour phase, the round epilogue
+// (plane_round.cuh) closes each round.
+__global__ void __launch_bounds__(kC5Threads, 1)
+plane_c5_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__ RoundArgs r) {
+    cg::grid_group grid = cg::this_grid();
+    const int nrep = a.W * 32;
+    int* s_cc = c5_cnt();
+    int* s_cq = s_cc + nrep;
+    const RoundSmem s = round_smem(s_cq + nrep, r.R);
+    const int logW = r.log_w;
+    const int gw = blockIdx.x * (kC5Threads >> 5) + (threadIdx.x >> 5);
+    const int nw = r.n_warps;
+    // site types: t30 = cost 3 / no chain, t31 = cost 3 / one chain partner
+    int t30 = 0, t31 = 0;
+    for (int ty = 0; ty < a.n_types; ++ty) {
+        if (a.ty[ty].dq == 0) t30 = ty;
+        else t31 = ty;
+    }
+    for (int m = threadIdx.x; m < 2 * nrep; m += blockDim.x) s_cc[m] = 0;
+    round_load_labels(r, s);
+    __syncthreads();
+    uint32_t V0[kC5VB], V1[kC5VB];
+#pragma unroll
+    for (int b = 0; b < kC5VB; ++b) { V0[b] = 0u; V1[b] = 0u; }
+    uint64_t swap_base = r.swap_base0;
+    for (int k = 0; k < r.n_rounds; ++k) {
+        const int64_t round = r.round0 + k;
+        const int par = (int)(round & 1);
+        int32_t* cc = r.cnt + (size_t)par * 2 * r.cnt_stride;
+        int32_t* cq = cc + r.cnt_stride;
+        for (int sw = 0; sw < r.sps; ++sw) {
+            const uint64_t t = (uint64_t)((round - 1) * r.sps + sw);
+            const bool count = (sw == r.sps - 1);
+            for (int c = 0; c < 2; ++c) {
+                c5_phase(a, c, t, count, gw, nw, logW, V0, V1, t30, t31, r.c5_nfree[c]);
+                if (count && c == 1) {
+                    __syncthreads();
+                    for (int m = threadIdx.x; m < nrep; m += blockDim.x) {
+                        const int vc = s_cc[m], vqv = s_cq[m];
+                        if (vc) { atomicAdd(cc + m, vc); s_cc[m] = 0; }
+                        if (vqv) { atomicAdd(cq + m, vqv); s_cq[m] = 0; }
+                    }
+                }
+                grid.sync();
+            }
+        }
+        round_epilogue(a, r, s, k, round, cc, cq, swap_base, 2 * r.sps);
+    }
+}
+
+void* plane_c5_fn() { return (void*)plane_c5_rounds_kernel; }
+
+}  // namespace tg

@@ -17,6 +17,13 @@ from test_gpu_parity import compare
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True)
+def _no_c5_kernel(monkeypatch):
+    # these cases pin the tpw / thread-per-site kernels: keep the config-5
+    # kernel (plane_c5.cu, tests/test_gpu_c5.py) out of the dispatch
+    monkeypatch.setenv("TG_PLANE_C5", "0")
+
 C5S = I.bipartite_3regular(512, seed=3)      # cost degree 3, chain degree 0/1, 2 colours
 K10 = I.k10_pm1(1)                           # non-bipartite, larger degrees: generic path
 
