@@ -48,8 +48,17 @@ struct u32x4 {
     uint32_t x, y, z, w;
 };
 
+#ifndef TG_MULWIDE
+#define TG_MULWIDE 0
+#endif
 TG_HD void mulhilo(uint32_t a, uint32_t b, uint32_t& hi, uint32_t& lo) {
-#if defined(__CUDA_ARCH__)
+#if defined(__CUDA_ARCH__) && TG_MULWIDE
+    // one 32x32->64 multiply (IMAD.WIDE.U32) for both halves
+    uint64_t p;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(b));
+    hi = (uint32_t)(p >> 32);
+    lo = (uint32_t)p;
+#elif defined(__CUDA_ARCH__)
     hi = __umulhi(a, b);
     lo = a * b;
 #else

@@ -38,6 +38,9 @@ namespace cg = cooperative_groups;
 namespace tg {
 
 constexpr int kC5VB = 8;  // vertical counter planes (<= 255 per lane between flushes)
+#ifndef TG_C5_THR_SMEM
+#define TG_C5_THR_SMEM 1  // class-2/3 thresholds from shared memory (0: registers)
+#endif
 
 extern __shared__ __align__(16) int c5_sm[];
 
@@ -46,7 +49,10 @@ extern __shared__ __align__(16) int c5_sm[];
 __device__ __forceinline__ int4* c5_queue(int warp) {
     return reinterpret_cast<int4*>(c5_sm) + warp * kC5QCap;
 }
-__device__ __forceinline__ int* c5_cnt() { return c5_sm + (kC5Threads / 32) * kC5QCap * 4; }
+__device__ __forceinline__ int* c5_cnt() { return c5_sm + (kC5Threads / 32) * kC5QCap * 4 + kMaxWordsArg * 16; }
+// class-2/3 threshold planes 0-7 of every word, [W][4] uint4 (k2 planes 0-3,
+// 4-7, k3 planes 0-3, 4-7), staged per round after the counters [2][32W]
+__device__ __forceinline__ uint4* c5_thr() { return reinterpret_cast<uint4*>(c5_sm + (kC5Threads / 32) * kC5QCap * 4); }
 
 // V += m (2-bit bit-sliced value) in kC5VB-bit vertical arithmetic.
 template <int NB>
@@ -193,12 +199,15 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
     const int cf = cs + nfree;               // first chain site of the colour
     count = count && c == 1;
     C5Ctx K;
+#if !TG_C5_THR_SMEM
     {
         const uint4* kc0 = reinterpret_cast<const uint4*>(a.kpc + ((size_t)w0 * a.n_types + t30) * 128);
         const uint4* kc1 = reinterpret_cast<const uint4*>(a.kpc + ((size_t)(w0 + 1) * a.n_types + t30) * 128);
         K.k2a[0] = kc0[0]; K.k2b[0] = kc0[1]; K.k3a[0] = kc0[16]; K.k3b[0] = kc0[17];
         K.k2a[1] = kc1[0]; K.k2b[1] = kc1[1]; K.k3a[1] = kc1[16]; K.k3b[1] = kc1[17];
     }
+#endif
+    const uint4* thr = c5_thr() + w0 * 4;  // staged per round: [word][k2a, k2b, k3a, k3b]
     K.act[0] = a.active[w0];
     K.act[1] = a.active[w0 + 1];
     const uint32_t g0 = (uint32_t)(a.w_global0 + w0) << 4;
@@ -214,31 +223,41 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
     // ---------------------------------------------------------- chain-free
     {
         const int n_it = (nfree + S - 1) / S;
+        auto entries = [&](int i) -> int4 {
+            int4 v = make_int4(0, 0, 0, 0);
+            if (i < n_it) {
+                const int st = cs + i * S + sl;
+                if (st < cf) v = __ldg(a.nbr4 + st);
+            }
+            return v;
+        };
+        struct Rows { uint2 s, x0, x1, x2; };
+        auto rows = [&](int i, const int4& e) -> Rows {
+            Rows q{make_uint2(0u, 0u), make_uint2(0u, 0u), make_uint2(0u, 0u), make_uint2(0u, 0u)};
+            const int st = cs + i * S + sl;
+            if (i < n_it && st < cf) {
+                q.s = row((uint32_t)st << logW);
+                q.x0 = row((uint32_t)e.x & 0x7fffffffu);
+                q.x1 = row((uint32_t)e.y & 0x7fffffffu);
+                q.x2 = row((uint32_t)e.z & 0x7fffffffu);
+            }
+            return q;
+        };
         int it = gw;
-        int4 en = make_int4(0, 0, 0, 0);
-        if (it < n_it) {
-            const int site = cs + it * S + sl;
-            if (site < cf) en = __ldg(a.nbr4 + site);
-        }
+        // software pipeline: the rows of the next item and the entries of the
+        // one after it are in flight while the current item computes
+        int4 en = entries(it);
+        Rows rn = rows(it, en);
+        int4 en2 = entries(it + nw);
         for (; it < n_it; it += nw) {
             const int4 e = en;
+            const Rows q = rn;
             const uint32_t site = (uint32_t)(cs + it * S + sl);
             const bool valid = (int)site < cf;
-            uint2 s = make_uint2(0u, 0u), x0 = s, x1 = s, x2 = s;
-            if (valid) {
-                s = row(site << logW);
-                x0 = row((uint32_t)e.x & 0x7fffffffu);
-                x1 = row((uint32_t)e.y & 0x7fffffffu);
-                x2 = row((uint32_t)e.z & 0x7fffffffu);
-            }
-            {
-                const int nx = it + nw;
-                en = make_int4(0, 0, 0, 0);
-                if (nx < n_it) {
-                    const int ns = cs + nx * S + sl;
-                    if (ns < cf) en = __ldg(a.nbr4 + ns);
-                }
-            }
+            en = en2;
+            rn = rows(it + nw, en);
+            en2 = entries(it + 2 * nw);
+            const uint2 s = q.s, x0 = q.x0, x1 = q.x1, x2 = q.x2;
             u32x4 r[4];
             philox_planeN<4>(site, K.g, K.P, a.pks, r);
             const uint32_t m0s = (uint32_t)(e.x >> 31), m1s = (uint32_t)(e.y >> 31), m2s = (uint32_t)(e.z >> 31);
@@ -254,8 +273,13 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
                 const uint32_t c1 = (a0 & a1) | (a2 & (a0 ^ a1));
                 const uint32_t act = valid ? K.act[j] : 0u;
                 uint32_t u = c1 & act, lt = 0u;   // classes 0, 1 (de < 0): always taken
+#if TG_C5_THR_SMEM
+                compare4_sel(c0, thr[4 * j], thr[4 * j + 2], r[2 * j], u, lt);
+                compare4_sel(c0, thr[4 * j + 1], thr[4 * j + 3], r[2 * j + 1], u, lt);
+#else
                 compare4_sel(c0, K.k2a[j], K.k3a[j], r[2 * j], u, lt);
                 compare4_sel(c0, K.k2b[j], K.k3b[j], r[2 * j + 1], u, lt);
+#endif
                 const uint32_t take = (~c1 & act) | lt;
                 ns[j] = sj ^ take;
                 und[j] = u;
@@ -397,6 +421,15 @@ plane_c5_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
         const int par = (int)(round & 1);
         int32_t* cc = r.cnt + (size_t)par * 2 * r.cnt_stride;
         int32_t* cq = cc + r.cnt_stride;
+        {   // this round's class-2/3 planes 0-7 (the epilogue's grid barrier precedes)
+            uint4* th = c5_thr();
+            for (int q = threadIdx.x; q < 4 * a.W; q += blockDim.x) {
+                const int w = q >> 2, part = q & 3;
+                th[q] = reinterpret_cast<const uint4*>(a.kpc + ((size_t)w * a.n_types + t30) * 128)
+                    [(part & 1) + 16 * (part >> 1)];
+            }
+            __syncthreads();
+        }
         for (int sw = 0; sw < r.sps; ++sw) {
             const uint64_t t = (uint64_t)((round - 1) * r.sps + sw);
             const bool count = (sw == r.sps - 1);

@@ -1,0 +1,7 @@
+# tools-like multi-variant A/B: A = default lib, others by name
+for rep in 1 2; do
+  for v in A "$@"; do
+    if [ $v = A ]; then unset TG_ENGINE_LIB; else export TG_ENGINE_LIB=$PWD/paper_2506_14781_b200/libtempergrid_b200_$v.so; fi
+    timeout 300 python bench.py --no-cpu-baseline --no-heat-bath --steps 5 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', '%.4e' % d['value'], round(d['ms_per_step'], 3), d['roofline']['kernel'])"
+  done
+done
