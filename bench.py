@@ -327,7 +327,7 @@ def run_ours_batch(args, rank, world, local):
                                   P[4], P[5], len(arrs[6]), P[6], len(arrs[7]), P[7], sd, None))
     total = args.rounds * args.sps * (args.warmup + args.steps + 1)
     cfg = RunConfig(total_sweeps=total, sweeps_per_swap=args.sps, seed=1, rule=args.rule,
-                    engine="slot", store_states=False, digest=False)
+                    engine=args.engine, store_states=False, digest=False)
     c = eng._cfg(cfg)
     c.record_flags = 0
     eng._check(L.tg_batch_init(eng._h, C.byref(c)))
@@ -382,7 +382,7 @@ def run_ours_batch(args, rank, world, local):
     pprs = [Problem(p.n, pinned(p.ci), pinned(p.cj), pinned(p.cw), pinned(p.fields), pinned(p.pa),
                     pinned(p.pb)) for p in prs]
     cfg2 = RunConfig(total_sweeps=args.rounds * args.sps, sweeps_per_swap=args.sps, seed=2,
-                     rule=args.rule, engine="slot", store_states=False, digest=False)
+                     rule=args.rule, engine=args.engine, store_states=False, digest=False)
     times = []
     for k in range(args.warmup + args.steps):
         barrier(world)
@@ -413,11 +413,12 @@ def run_ours_batch(args, rank, world, local):
                                    f"{prs_all[0].n} physical each, 16x16 grids, sps={args.sps} "
                                    f"{args.rule}",
                        "instances": len(prs_all), "n_spins_total": n_spins, "replicas": R,
-                       "rounds_per_step": args.rounds, "engine": "slot (batch)",
+                       "rounds_per_step": args.rounds, "engine": f"{args.engine} (batch)",
                        "parallelism": f"instances x{world}",
                        "l2": "flushed between timed steps (256 MB write)"},
             "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
-                         "frac": achieved / smem_peak, "traffic": None, "kernel": "slot2_sweep_kernel",
+                         "frac": achieved / smem_peak, "traffic": None,
+                         "kernel": info1.get("sweep_kernel") or "slot2_sweep_kernel",
                          "bytes_per_update": bal, "mean_launch_ms": mean_sweep_s * 1e3},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks}),
             flush=True)
@@ -664,8 +665,8 @@ def spawn_or_check(args):
 def main():
     args = parse()
     spawn_or_check(args)
-    if args.workload != "c5":
-        args.engine = "slot"  # float32 Wishart couplings: the FP64 slot engine
+    if args.workload != "c5" and args.engine == "plane":
+        args.engine = "float"  # float32 Wishart couplings: the FLOAT engine (--engine slot: SLOT v2)
     if args.impl == "reference":
         # the reference arm never maps the engine library: instances are built
         # with the pure-Python host helpers, the timed code is oracle/_ref

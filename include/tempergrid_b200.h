@@ -51,7 +51,7 @@ enum tg_rule { TG_RULE_METROPOLIS = 0, TG_RULE_HEAT_BATH = 1 };
  * PLANE: multi-spin-coded bit planes (32 replicas per word), threshold tables,
  * lazily consumed bit-plane draws keyed by physical replica; requires J = +-1,
  * h = 0 (the integer-coupling instances).  AUTO picks PLANE when eligible. */
-enum tg_engine { TG_ENGINE_AUTO = 0, TG_ENGINE_SLOT = 1, TG_ENGINE_PLANE = 2 };
+enum tg_engine { TG_ENGINE_AUTO = 0, TG_ENGINE_SLOT = 1, TG_ENGINE_PLANE = 2, TG_ENGINE_FLOAT = 3 };
 
 /* What each round record carries beyond (f, g, feasible). */
 enum tg_record_flags {

@@ -6,8 +6,10 @@
 //                with the reference's one-draw-per-spin contract and f/g bookkeeping
 //                (mc.cpp:21-35, test_mc.cpp:52-61);
 //   ALT_PLANE=1  bit-plane draws keyed by physical state (philox_ref.h), the RNG
-//                association of the B200 "msc" engine.  Needs the shadow SweepState
+//                association of the B200 PLANE engine.  Needs the shadow SweepState
 //                of oracle/shadow_plane/tempergrid/mc.hpp.
+//   ALT_PLANE=2  packed draws keyed by physical state (philox_ref.h tgo_pack_u53),
+//                the RNG association of the B200 FLOAT engine (same shadow).
 // make_sweep_state / refresh_sweep_state restate mc.cpp:7-19 unchanged.
 #include <cmath>
 #include <cstdint>
@@ -65,7 +67,8 @@ void metropolis_sweep(const EffectiveModel& view, double beta, SweepState& state
     // Every configuration sweeps first in the slot it was created in, so the
     // slot stream seen at its first sweep names the physical state.
     if (state.plane_id < 0) state.plane_id = slot_of_seed(rng.seed());
-    const std::uint64_t pkey = tgo_derive_seed(tgref_ctx::master, TGO_PURPOSE_PLANE, 0);
+    const std::uint64_t pkey = tgo_derive_seed(tgref_ctx::master,
+                                               ALT_PLANE == 2 ? TGO_PURPOSE_PACK : TGO_PURPOSE_PLANE, 0);
     const std::uint32_t grp = (std::uint32_t)(state.plane_id >> 5);
     const int lane = state.plane_id & 31;
     const std::uint64_t t = state.plane_t++;
@@ -73,7 +76,10 @@ void metropolis_sweep(const EffectiveModel& view, double beta, SweepState& state
     for (int i = 0; i < n; ++i) {
         const double local_i = state.local[i];
         const double de = 2.0 * static_cast<double>(state.spins[i]) * local_i;
-#if ALT_PLANE
+#if ALT_PLANE == 2
+        const double u = tgo_u53_to_unit(tgo_pack_u53(pkey, (std::uint32_t)state.plane_id, t, (std::uint32_t)i));
+        (void)grp; (void)lane;
+#elif ALT_PLANE
         const double u = tgo_u53_to_unit(tgo_plane_u53(pkey, grp, t, (std::uint32_t)i, lane));
 #else
         const double u = rng.uniform01();

@@ -27,6 +27,15 @@
  *   u   = U53 * 2^-53.
  * One key per run (the stream identity of a 32-replica group lives in the
  * counter), so the device key schedule is a compile-time-addressed constant.
+ *
+ * Packed draws (engine "float"): the 53-bit uniform of physical state m at
+ * sweep t, site i is U53 = hi16 << 37 | lo37 with
+ *   hi16 = halfword (m & 7) of philox(ctr={i, lo32(t), hi32(t), (m>>3) | 1<<30}, key)
+ *          (halfword h = bits 16*(h&1) .. +15 of word h>>1): one block serves
+ *          8 consecutive states, whose decisions are nearly always settled
+ *          by these 16 bits;
+ *   lo37 = low 37 bits of (c0 | c1<<32) of philox(ctr={i, lo32(t), hi32(t), m | 2<<30}, key),
+ * key = derive_seed(seed, PACK, 0).
  */
 #ifndef TG_PHILOX_REF_H
 #define TG_PHILOX_REF_H
@@ -45,7 +54,8 @@ enum {
     TGO_PURPOSE_REPEAT = 5,
     TGO_PURPOSE_SAMPLING = 6,
     TGO_PURPOSE_BOOTSTRAP = 7,
-    TGO_PURPOSE_PLANE = 8
+    TGO_PURPOSE_PLANE = 8,
+    TGO_PURPOSE_PACK = 9
 };
 
 static inline uint64_t tgo_mix64(uint64_t z) {
@@ -109,6 +119,21 @@ static inline uint64_t tgo_plane_u53(uint64_t pkey, uint32_t grp, uint64_t t, ui
         }
     }
     return u;
+}
+
+/* Packed-draw 53-bit uniform of physical state m at sweep t, site i under run
+ * key `pkey` = derive_seed(seed, PACK, 0) (see header comment). */
+static inline uint64_t tgo_pack_u53(uint64_t pkey, uint32_t m, uint64_t t, uint32_t site) {
+    const uint32_t key[2] = {(uint32_t)pkey, (uint32_t)(pkey >> 32)};
+    uint32_t o[4];
+    const uint32_t c1[4] = {site, (uint32_t)t, (uint32_t)(t >> 32), (m >> 3) | (1u << 30)};
+    tgo_philox4x32_10(c1, key, o);
+    const uint32_t h = m & 7u;
+    const uint64_t hi16 = (o[h >> 1] >> (16u * (h & 1u))) & 0xFFFFu;
+    const uint32_t c2[4] = {site, (uint32_t)t, (uint32_t)(t >> 32), m | (2u << 30)};
+    tgo_philox4x32_10(c2, key, o);
+    const uint64_t lo37 = ((uint64_t)o[0] | ((uint64_t)o[1] << 32)) & ((1ull << 37) - 1ull);
+    return (hi16 << 37) | lo37;
 }
 
 /* Order-independent, position-keyed digest of a spin configuration:

@@ -22,10 +22,12 @@ REF_LIBS = {
     "philox_hb": "libtgref_philox_hb.so",
     "plane": "libtgref_plane.so",
     "plane_hb": "libtgref_plane_hb.so",
+    "pack": "libtgref_pack.so",        # O2: reference + packed draws (FLOAT engine)
+    "pack_hb": "libtgref_pack_hb.so",
 }
 
 RULE = {"metropolis": 0, "heat_bath": 1}
-RNG = {"slot": 0, "plane": 1}
+RNG = {"slot": 0, "plane": 1, "float": 2}
 
 
 class _Problem(C.Structure):

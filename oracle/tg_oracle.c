@@ -6,8 +6,9 @@
  * /root/reference/proj).  The only departures from the reference are the ones
  * the parity contract names: the mt19937_64 engine is replaced by the Philox
  * stream of philox_ref.h, a heat-bath update rule is offered next to
- * Metropolis, and an alternative RNG association (bit-plane draws keyed by the
- * physical state) is offered next to the reference's per-slot streams.
+ * Metropolis, and two alternative RNG associations (bit-plane draws and packed
+ * draws keyed by the physical state) are offered next to the reference's
+ * per-slot streams.
  * Floating-point expressions are written in the reference's evaluation order
  * so that the port is bit-identical to the reference objects (checked against
  * oracle/_ref in tests/test_oracle_ref.py).
@@ -294,6 +295,7 @@ static inline uint64_t next_u53(draw_ctx_t* d, const rstate_t* st, int site) {
         const uint64_t b = tgo_stream_bits(d->slot_seed, (*d->slot_ctr)++);
         return b >> 11; /* rng.hpp:53-55 */
     }
+    if (d->mode == TGO_RNG_PACK) return tgo_pack_u53(d->pkey, (uint32_t)st->id, d->t, (uint32_t)site);
     return tgo_plane_u53(d->pkey, (uint32_t)(st->id >> 5), d->t, (uint32_t)site, st->id & 31);
 }
 
@@ -330,7 +332,7 @@ static int plane_less(const draw_ctx_t* d, const rstate_t* st, int site, double 
  * the same one-draw-per-spin contract and the same f/g bookkeeping. */
 static void sweep(const view_t* v, double beta, rstate_t* st, draw_ctx_t* d, int rule) {
     const int n = v->merged.n;
-    const int lazy = d->mode != TGO_RNG_SLOT;
+    const int lazy = d->mode == TGO_RNG_PLANE;
     for (int i = 0; i < n; ++i) {
         const double local_i = st->local[i];
         const double de = 2.0 * (double)st->spins[i] * local_i;
@@ -399,6 +401,9 @@ uint64_t tgo_derive(uint64_t master, uint64_t purpose, uint64_t index) {
 uint64_t tgo_bits(uint64_t seed, uint64_t n) { return tgo_stream_bits(seed, n); }
 uint64_t tgo_plane(uint64_t pkey, uint32_t grp, uint64_t t, uint32_t site, int lane) {
     return tgo_plane_u53(pkey, grp, t, site, lane);
+}
+uint64_t tgo_pack(uint64_t pkey, uint32_t m, uint64_t t, uint32_t site) {
+    return tgo_pack_u53(pkey, m, t, site);
 }
 int tgo_plane_less(uint64_t pkey, uint32_t grp, uint64_t t, uint32_t site, int lane, double T) {
     draw_ctx_t d;
@@ -587,7 +592,8 @@ int tgo_run_2dpt(const tgo_problem* prob, const tgo_run_cfg* cfg, tgo_outputs* o
     rstate_t* rep = (rstate_t*)calloc((size_t)R, sizeof(rstate_t));
     uint64_t* slot_seed = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)R);
     uint64_t* slot_ctr = (uint64_t*)calloc((size_t)R, sizeof(uint64_t));
-    const uint64_t pkey = tgo_derive_seed(cfg->seed, TGO_PURPOSE_PLANE, 0);
+    const uint64_t pkey = tgo_derive_seed(cfg->seed,
+                                          cfg->rng_mode == TGO_RNG_PACK ? TGO_PURPOSE_PACK : TGO_PURPOSE_PLANE, 0);
     for (int r = 0; r < R; ++r) { /* engine.cpp:98-106 */
         rep[r].spins = (int8_t*)malloc((size_t)n);
         rep[r].local = (double*)malloc(sizeof(double) * (size_t)n);

@@ -25,7 +25,7 @@ enum { TGO_OK = 0, TGO_CONFIG_ERROR = 2, TGO_RESOURCE_ERROR = 3 };
 enum { TGO_RULE_METROPOLIS = 0, TGO_RULE_HEAT_BATH = 1 };
 /* RNG association: SLOT = reference (stream stays with the grid slot,
  * engine.cpp:36-39,160,182); PLANE = bit-plane draws keyed by physical state. */
-enum { TGO_RNG_SLOT = 0, TGO_RNG_PLANE = 1 };
+enum { TGO_RNG_SLOT = 0, TGO_RNG_PLANE = 1, TGO_RNG_PACK = 2 };
 
 typedef struct {
     int n;
@@ -159,6 +159,8 @@ uint64_t tgo_bits(uint64_t seed, uint64_t n);
 uint64_t tgo_plane(uint64_t pkey, uint32_t grp, uint64_t t, uint32_t site, int lane);
 /* lazy MSB-first decision u < T on the bit-plane uniform (tests only) */
 int tgo_plane_less(uint64_t pkey, uint32_t grp, uint64_t t, uint32_t site, int lane, double T);
+/* packed-draw 53-bit uniform (engine "float"; philox_ref.h tgo_pack_u53) */
+uint64_t tgo_pack(uint64_t pkey, uint32_t m, uint64_t t, uint32_t site);
 
 #ifdef __cplusplus
 }

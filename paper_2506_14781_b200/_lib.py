@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("TG_ENGINE_LIB") or os.path.join(PKG, "libtempergrid_b
 
 TG_OK, TG_ERR_INTERNAL, TG_ERR_CONFIG, TG_ERR_RESOURCE, TG_ERR_CUDA, TG_ERR_SINK = range(6)
 RULES = {"metropolis": 0, "heat_bath": 1}
-ENGINES = {"auto": 0, "slot": 1, "plane": 2}
+ENGINES = {"auto": 0, "slot": 1, "plane": 2, "float": 3}
 REC_DIGEST, REC_STATE, REC_GRID, REC_COUNTERS = 1, 2, 4, 8
 
 

@@ -47,7 +47,7 @@ class RunConfig:
     store_target_only: bool = True
     threads: int = 1                 # accepted for API parity; results never depend on it
     rule: str = "metropolis"         # or "heat_bath"
-    engine: str = "auto"             # "slot" | "plane" | "auto"
+    engine: str = "auto"             # "slot" | "plane" | "float" | "auto"
     record_every: int = 1
     store_states: bool = True        # TraceRecord.state for every record
     digest: bool = True

@@ -344,8 +344,8 @@ int tg_batch_init(tg_ctx* ctx, const tg_run_config* cfg) {
             fail(TG_ERR_CONFIG, "run: total_sweeps must be >= sweeps_per_swap");
         if (cfg->rule != TG_RULE_METROPOLIS && cfg->rule != TG_RULE_HEAT_BATH)
             fail(TG_ERR_CONFIG, "run: unknown update rule %d", cfg->rule);
-        if (cfg->engine != TG_ENGINE_AUTO && cfg->engine != TG_ENGINE_SLOT)
-            fail(TG_ERR_CONFIG, "batch: only the SLOT engine runs batches");
+        if (cfg->engine != TG_ENGINE_AUTO && cfg->engine != TG_ENGINE_SLOT && cfg->engine != TG_ENGINE_FLOAT)
+            fail(TG_ERR_CONFIG, "batch: only the SLOT and FLOAT engines run batches");
         if (ctx->world != 1) fail(TG_ERR_CONFIG, "batch: single-GPU contexts only");
         ctx->use_s2 = false;
         ctx->initialised = false;

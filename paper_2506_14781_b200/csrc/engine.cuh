@@ -176,6 +176,7 @@ struct SInst {              // one instance of a batch (device table)
     int n_chunks;
     int state_off;          // sum of n over earlier instances (record snapshots)
     float eps, beta_max;    // FP32 fast-path error bound, max |beta|
+    unsigned long long pkey; // FLOAT engine: packed-draw key derive_seed(seed, PACK, 0)
 };
 
 struct S2Args {
@@ -205,6 +206,12 @@ struct S2Args {
     const double* stwop;           // [B][Rp] 2P of that slot
     const uint64_t* skey;          // [B][Rp] Philox key of that slot's stream
     int nsub;                      // warps per replica group
+    // FLOAT engine (slot_fast.cu)
+    const float2* lab;             // [B][Rp] (beta, 2P) of the slot each physical replica occupies
+    long long* fx;                 // [B][Rp] cost energy, 2^-40 fixed point (zeroed after use)
+    int* gx;                       // [B][Rp] unsatisfied chain bonds x multiplicity
+    const int* fitem_pref;         // [max_colors][B+1] prefix sums of warp items
+    int flps, fspw, fngs;          // lanes per site, sites per warp item, 256-replica group sets
     double* hist_f;                // probes: per-sweep (f, g) of every replica,
     double* hist_g;                //   [t - hist_t0][B*R], for sweeps t >= hist_t0
     int64_t hist_t0;
@@ -230,6 +237,7 @@ struct S2Swap {
     uint64_t* skey;
     const uint64_t* slot_key;      // [B][R]
     int Rp;
+    float2* lab;                   // FLOAT engine label table (or null)
 };
 
 // Decoded-sample histogram + KL per round (analysis.cpp:215-241).

@@ -239,6 +239,12 @@ struct Slot2 {
     // schedule probes (schedule.cpp:18-52): independent chains, no swaps,
     // one stream per chain for the initial state and the sweeps
     bool probe = false;
+    // FLOAT engine (slot_fast.cu): packed draws, certified FP32 decisions
+    bool fast = false;
+    int fdeg = 4, flps = 32, fspw = 1, fngs = 1;
+    DBuf<float2> d_lab;
+    DBuf<long long> d_fx;
+    DBuf<int> d_gx, d_fitem_pref;
     DBuf<uint64_t> d_init_keys;
     DBuf<double> d_hist_f, d_hist_g, d_moments;
     std::vector<SInst> h_inst;

@@ -82,15 +82,17 @@ void do_init(tg_ctx& c, const tg_run_config* cfg) {
     int eng = cfg->engine;
     if (eng == TG_ENGINE_AUTO)
         eng = (!c.kl.on && plane_eligible(c, nullptr)) ? TG_ENGINE_PLANE : TG_ENGINE_SLOT;
-    if (c.kl.on && (eng != TG_ENGINE_SLOT || c.world != 1 || std::getenv("TG_SLOT_V1")))
-        fail(TG_ERR_CONFIG, "kl decoder: needs the single-GPU SLOT engine");
+    if (c.kl.on && ((eng != TG_ENGINE_SLOT && eng != TG_ENGINE_FLOAT) || c.world != 1 || std::getenv("TG_SLOT_V1")))
+        fail(TG_ERR_CONFIG, "kl decoder: needs the single-GPU SLOT or FLOAT engine");
     if (eng == TG_ENGINE_PLANE && !plane_eligible(c, &why))
         fail(TG_ERR_CONFIG, "plane engine: instance not eligible (%s)", why.c_str());
-    if (eng != TG_ENGINE_PLANE && eng != TG_ENGINE_SLOT) fail(TG_ERR_CONFIG, "unknown engine %d", eng);
+    if (eng == TG_ENGINE_FLOAT && c.world != 1) fail(TG_ERR_CONFIG, "float engine: single-GPU contexts only");
+    if (eng != TG_ENGINE_PLANE && eng != TG_ENGINE_SLOT && eng != TG_ENGINE_FLOAT)
+        fail(TG_ERR_CONFIG, "unknown engine %d", eng);
     c.engine = eng;
     {
         int32_t s0 = 0, cnt = 0;
-        if (tg_partition(c.R, c.rank, c.world, eng, &s0, &cnt) != TG_OK)
+        if (tg_partition(c.R, c.rank, c.world, eng == TG_ENGINE_FLOAT ? TG_ENGINE_SLOT : eng, &s0, &cnt) != TG_OK)
             fail(TG_ERR_CONFIG, "grid of %d replicas does not split over %d ranks%s", c.R, c.world,
                  eng == TG_ENGINE_PLANE ? " in 32-replica words" : "");
         c.state0 = s0;
@@ -99,7 +101,7 @@ void do_init(tg_ctx& c, const tg_run_config* cfg) {
     cudaStream_t st = c.stream;
     CK(cudaSetDevice(c.device));
     c.use_s2 = false;
-    if (eng == TG_ENGINE_SLOT && c.world == 1 && !std::getenv("TG_SLOT_V1")) {
+    if ((eng == TG_ENGINE_SLOT && c.world == 1 && !std::getenv("TG_SLOT_V1")) || eng == TG_ENGINE_FLOAT) {
         // single instance = batch of one on the replica-fastest SLOT engine
         BatchInst bi;
         ensure_host_arrays(c);

@@ -273,6 +273,8 @@ S2Args s2_args(tg_ctx& c) {
     a.slot_key = S.d_keys.p; a.part_f = S.d_part_f.p; a.part_g = S.d_part_g.p;
     a.f = S.d_f.p; a.g = S.d_g.p;
     a.sbeta = S.d_sbeta.p; a.stwop = S.d_stwop.p; a.skey = S.d_skey.p; a.nsub = S.nsub;
+    a.lab = S.d_lab.p; a.fx = S.d_fx.p; a.gx = S.d_gx.p; a.fitem_pref = S.d_fitem_pref.p;
+    a.flps = S.flps; a.fspw = S.fspw; a.fngs = S.fngs;
     return a;
 }
 
@@ -306,6 +308,7 @@ S2Swap s2_swap(tg_ctx& c) {
     s.perm = S.d_perm.p;
     s.sbeta = S.d_sbeta.p; s.stwop = S.d_stwop.p; s.skey = S.d_skey.p;
     s.slot_key = S.d_keys.p; s.Rp = S.Rp;
+    s.lab = S.fast ? S.d_lab.p : nullptr;
     return s;
 }
 
@@ -326,6 +329,7 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
     S.G = S.Rp / 32;
     S.cfg = *cfg;
     if (S.cfg.record_every < 1) S.cfg.record_every = 1;
+    S.fast = cfg->engine == TG_ENGINE_FLOAT && !S.probe;
     S.prep.assign(B, S2Prep{});
     S.state_off.clear();
     std::unique_ptr<HostTimer> tsec(new HostTimer("batch: s2_build prepare"));
@@ -434,6 +438,7 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
         state_off += P.n;
         in.eps = P.eps;
         in.beta_max = P.beta_max;
+        in.pkey = derive_seed(c.batch[b].seed, kPurposePack, 0);
         max_colors = std::max(max_colors, P.n_colors);
         betas.insert(betas.end(), c.batch[b].betas.begin(), c.batch[b].betas.end());
         pens.insert(pens.end(), c.batch[b].pens.begin(), c.batch[b].pens.end());
@@ -536,15 +541,64 @@ void s2_build(tg_ctx& c, const tg_run_config* cfg) {
         S.grid = blocks;
         S.nsub = blocks * wpb / S.G;
     }
+    if (S.fast) {
+        // FLOAT engine: lanes per site, sites per warp item, 256-replica group
+        // sets; warp items per colour and instance (prefix sums)
+        int maxdeg = 0;
+        for (const auto& P : S.prep)
+            for (int i = 0; i < P.n; ++i) maxdeg = std::max(maxdeg, P.off[i + 1] - P.off[i]);
+        if (maxdeg > 8) fail(TG_ERR_RESOURCE, "float engine: merged degree %d > 8", maxdeg);
+        S.fdeg = maxdeg <= 3 && D == 4 ? 3 : (maxdeg <= 4 && D == 4 ? 4 : 8);
+        if (S.fdeg == 8 && D != 8) fail(TG_ERR_RESOURCE, "float engine: padded degree %d", D);
+        const int g8 = S.Rp / 8;
+        S.flps = std::min(32, g8);
+        S.fspw = 32 / S.flps;
+        S.fngs = (g8 + 31) / 32;
+        std::vector<int> fpref((size_t)max_colors * (B + 1), 0);
+        for (int col = 0; col < max_colors; ++col)
+            for (int b = 0; b < B; ++b) {
+                const S2Prep& P = S.prep[b];
+                const int len = col < P.n_colors ? P.color_start[col + 1] - P.color_start[col] : 0;
+                fpref[(size_t)col * (B + 1) + b + 1] = fpref[(size_t)col * (B + 1) + b] + (len + S.fspw - 1) / S.fspw;
+            }
+        S.d_fitem_pref.upload(fpref, st);
+        const void* fn = slotf_sweep_fn(S.cfg.rule, S.fdeg);
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSlotFThreads, 0));
+        if (per_sm < 1) fail(TG_ERR_RESOURCE, "float engine: sweep kernel does not fit on an SM");
+        const int wpb = kSlotFThreads / 32;
+        long long need = 0;  // no more warps than the widest colour phase can use
+        for (int col = 0; col < max_colors; ++col)
+            need = std::max<long long>(need, (long long)fpref[(size_t)col * (B + 1) + B] * S.fngs);
+        int blocks = (int)std::min<long long>((long long)per_sm * c.sms, (need + wpb - 1) / wpb);
+        blocks = std::max(blocks, 1);
+        while (blocks > 1 && (blocks * wpb) % S.fngs != 0) --blocks;
+        if ((blocks * wpb) % S.fngs != 0) fail(TG_ERR_RESOURCE, "float engine: cannot tile %d group sets", S.fngs);
+        S.grid = blocks;
+        S.d_fx.alloc((size_t)B * S.Rp);
+        S.d_gx.alloc((size_t)B * S.Rp);
+        S.d_fx.zero(st);
+        S.d_gx.zero(st);
+        std::vector<float2> lab((size_t)B * S.Rp, make_float2(0.f, 0.f));
+        for (int b = 0; b < B; ++b)
+            for (int r = 0; r < S.R; ++r)
+                lab[(size_t)b * S.Rp + r] = make_float2((float)c.batch[b].betas[r / S.J],
+                                                        (float)(2.0 * c.batch[b].pens[r % S.J]));
+        S.d_lab.upload(lab, st);
+    } else {
+        S.d_lab.release();
+        S.d_fx.release();
+        S.d_gx.release();
+    }
     // fused per-warp energy partials cost B x nsub x Rp doubles of traffic per
     // round; past a few MB a separate pass over the spins is cheaper
-    S.sep_energy = (size_t)B * S.nsub * S.Rp * 16 > ((size_t)8 << 20) || std::getenv("TG_SLOT_SEP_ENERGY");
+    S.sep_energy = !S.fast && ((size_t)B * S.nsub * S.Rp * 16 > ((size_t)8 << 20) || std::getenv("TG_SLOT_SEP_ENERGY"));
     if (S.sep_energy) {
         S.e_slices = std::max(1, (c.sms * 8) / std::max(1, B * S.G));
         S.d_epart.alloc((size_t)2 * B * S.e_slices * S.R);
     }
-    S.d_part_f.alloc(S.sep_energy ? 0 : (size_t)B * S.nsub * S.Rp);
-    S.d_part_g.alloc(S.sep_energy ? 0 : (size_t)B * S.nsub * S.Rp);
+    S.d_part_f.alloc(S.sep_energy || S.fast ? 0 : (size_t)B * S.nsub * S.Rp);
+    S.d_part_g.alloc(S.sep_energy || S.fast ? 0 : (size_t)B * S.nsub * S.Rp);
     S.d_part_f.zero(st);
     S.d_part_g.zero(st);
     {
@@ -706,8 +760,14 @@ void s2_advance(tg_ctx& c, int64_t n_rounds, const BatchSinkCtx& sink) {
         int nsw = sps, de = S.sep_energy ? 0 : 1;
         void* args[] = {&a, &t0, &nsw, &de};
         if (c.profiling) CK(cudaEventRecord(c.ev[0], st));
-        c.sweep_kernel = "slot2_sweep_kernel";
-        CK(cudaLaunchCooperativeKernel(slot2_sweep_fn(S.D), dim3(S.grid), dim3(kSlot2Threads), args, 0, st));
+        if (S.fast) {
+            c.sweep_kernel = "slotf_sweep_kernel";
+            CK(cudaLaunchCooperativeKernel(slotf_sweep_fn(S.cfg.rule, S.fdeg), dim3(S.grid), dim3(kSlotFThreads),
+                                           args, 0, st));
+        } else {
+            c.sweep_kernel = "slot2_sweep_kernel";
+            CK(cudaLaunchCooperativeKernel(slot2_sweep_fn(S.D), dim3(S.grid), dim3(kSlot2Threads), args, 0, st));
+        }
         if (c.profiling) CK(cudaEventRecord(c.ev[1], st));
         c.sweep_launches++;
         if (S.sep_energy) {

@@ -82,6 +82,8 @@ void* slot_sweep_fn();
 void* slot_sweep_fn_d(int D);  // padded-degree variant, D in {4, 8}
 
 constexpr int kSlot2Threads = 512;
+constexpr int kSlotFThreads = 512;   // FLOAT engine sweep kernel (slot_fast.cu)
+void* slotf_sweep_fn(int rule, int deg);
 void* slot2_sweep_fn(int D, bool hist = false);
 __global__ void slot2_swap_kernel(const __grid_constant__ S2Swap s, int64_t round, uint64_t swap_base,
                                   int rec_idx, int rec_flags);

@@ -26,6 +26,7 @@ enum : uint64_t {
     kPurposeProbe = 4,   // schedule probe chains (rng.hpp:27)
     kPurposeRepeat = 5,  // J-column baseline repeats (rng.hpp:28)
     kPurposePlane = 8,
+    kPurposePack = 9,    // FLOAT engine packed draws (oracle/philox_ref.h tgo_pack_u53)
 };
 
 constexpr uint32_t kPhiloxM0 = 0xD2511F53u;

@@ -279,6 +279,9 @@ slot2_swap_kernel(const __grid_constant__ S2Swap s, int64_t round, uint64_t swap
         s.sbeta[(size_t)b * s.Rp + m] = s.betas[b * I + sl / J];
         s.stwop[(size_t)b * s.Rp + m] = 2.0 * s.pens[b * J + sl % J];
         s.skey[(size_t)b * s.Rp + m] = s.slot_key[(size_t)b * R + sl];
+        if (s.lab)  // FLOAT engine: FP32 (beta, 2P) of the slot
+            s.lab[(size_t)b * s.Rp + m] = make_float2((float)s.betas[b * I + sl / J],
+                                                      (float)(2.0 * s.pens[b * J + sl % J]));
     }
     if (threadIdx.x == 0) {
         TgRecordDev* rec = reinterpret_cast<TgRecordDev*>(s.rec) + (size_t)b * s.rec_cap + rec_idx;

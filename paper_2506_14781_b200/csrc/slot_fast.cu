@@ -1,0 +1,277 @@
+// slot_fast.cu -- FLOAT engine: the float-coupling sweep (configs 2-4) with
+// packed draws keyed by physical replica.
+//
+// Same update as the reference sweep (mc.cpp:21-35: u < exp(-beta de) /
+// heat bath u < sigma(2 beta h), one uniform per spin) over the canonical
+// colour order, in the SLOT v2 batch layout (spins int8 [instance][site][Rp],
+// labels permuted by slot2_swap_kernel).  Differences from SLOT v2:
+//
+// * RNG association: the 53-bit uniform of physical replica m at sweep t,
+//   site i is hi16 << 37 | lo37 (oracle/philox_ref.h tgo_pack_u53): hi16 is
+//   halfword m & 7 of one Philox4x32-10 block per (site, sweep, 8 replicas),
+//   lo37 comes from a per-replica block that is only generated when the 16
+//   leading bits cannot settle the decision.  One block serves 8 updates.
+// * Thread = (site, 8 consecutive replicas): one 8-byte load per row, the
+//   site's entries, field and couplings shared by its 8 replicas.
+// * Certified FP32 decisions: FP32 field and exp with the error band of
+//   slot_engine.cu s2_update; u lies in [hi16 2^-16, (hi16 + 1) 2^-16), so the
+//   decision is taken from the 16 bits when that interval clears the band and
+//   falls back to the reference's FP64 expression with all 53 bits otherwise
+//   (probability ~1e-4): decisions equal the FP64 ones.
+// * Energies: per-thread FP64 partials of the lower-colour bonds, flushed as
+//   2^-40 fixed-point integers with integer atomics (order-independent, so
+//   runs are bit-reproducible), converted to (f, g) after the last sweep.
+//
+// Work layout: lanes per site LPS = min(32, Rp / 8); a warp item is
+// SPW = 32 / LPS sites (Rp < 256) or one site and one of NGS = Rp / 256
+// 256-replica group sets; every warp keeps one group set for the launch and
+// walks a contiguous range of its colour's items, so a lane's instance (its
+// labels and accumulators) changes rarely.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "engine.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tg {
+
+__device__ __forceinline__ int sf_find_instance(const int* pref, int B, int item) {
+    int lo = 0, hi = B;  // pref[lo] <= item < pref[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (pref[mid] <= item) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// w with its sign flipped where byte `k` (0..3) of `word` is negative (spin -1)
+__device__ __forceinline__ float sf_signed(float w, uint32_t word, int k) {
+    return __int_as_float(__float_as_int(w) ^ ((word << (24 - 8 * k)) & 0x80000000u));
+}
+
+// FP64 decision of one replica with all 53 bits (the semantics the FP32 path
+// certifies): local field in the reference's merged-CSR order
+// (constraints.cpp:122-140, ising.cpp:79-88), then mc.cpp:27-29 / heat bath.
+__device__ __noinline__ int sf_exact(const S2Args& a, const SInst& in, const int8_t* sp, int i, int r,
+                                     int si8, uint64_t u53, double beta, double two_p, int rule) {
+    double local = a.h[in.h_off + i];
+    const int e0 = a.off[in.csr_off + i], e1 = a.off[in.csr_off + i + 1];
+    for (int e = e0; e < e1; ++e) {
+        const int q = in.nbr_off + e;
+        const double wgt = a.w[q] + (double)a.cm[q] * two_p;
+        local += wgt * (double)sp[(size_t)a.nbr[q] * a.Rp + r];
+    }
+    const double u = (double)u53 * 0x1.0p-53;
+    if (rule == 0) {
+        const double de = 2.0 * (double)si8 * local;
+        return (de <= 0.0 || u < exp(-beta * de)) ? -si8 : si8;
+    }
+    const double p = 1.0 / (1.0 + exp(-2.0 * beta * local));
+    return u < p ? 1 : -1;
+}
+
+// Per-thread accumulators of one instance: FP64 cost energy and chain-bond
+// counts of the thread's 8 replicas, flushed as fixed point.
+__device__ __forceinline__ void sf_flush(const S2Args& a, int b, int m0, double (&fl)[8], int (&gl)[8]) {
+    long long* fx = a.fx + (size_t)b * a.Rp + m0;
+    int* gx = a.gx + (size_t)b * a.Rp + m0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        if (fl[j] != 0.0) atomicAdd(reinterpret_cast<unsigned long long*>(fx + j),
+                                    (unsigned long long)__double2ll_rn(fl[j] * 0x1.0p40));
+        if (gl[j]) atomicAdd(gx + j, gl[j]);
+        fl[j] = 0.0;
+        gl[j] = 0;
+    }
+}
+
+template <int RULE, int DEG, int D>
+__global__ void __launch_bounds__(kSlotFThreads, 1)
+slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, int do_energy) {
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
+    const int nw = gridDim.x * wpb;
+    const int ngs = a.fngs, lps = a.flps, spw = a.fspw;
+    const int gs = gw % ngs, wi = gw / ngs, nwi = nw / ngs;  // host: nw % ngs == 0
+    const int sub = lane / lps;
+    const int grp = gs * 32 + lane % lps;                   // replicas 8 grp .. 8 grp + 7
+    const bool lane_on = sub < spw && grp * 8 < a.Rp;
+    const int m0 = grp * 8;
+    const unsigned Rp = (unsigned)a.Rp;
+    for (int swp = 0; swp < n_sweeps; ++swp) {
+        const uint64_t t = (uint64_t)(t0 + swp);
+        const uint32_t tlo = (uint32_t)t, thi = (uint32_t)(t >> 32);
+        const bool count = do_energy && swp == n_sweeps - 1;
+        double fl[8];
+        int gl[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { fl[j] = 0.0; gl[j] = 0; }
+        for (int c = 0; c < a.max_colors; ++c) {
+            const int* pref = a.fitem_pref + (size_t)c * (a.B + 1);
+            const int total = pref[a.B];
+            const int lo = (int)((long long)wi * total / nwi), hi = (int)((long long)(wi + 1) * total / nwi);
+            int b = -1, b_end = 0;
+            int cs = 0, ce = 0, p0 = 0;
+            float bt[8], tp[8];       // beta, 2P of the lanes' replicas (current instance)
+            uint32_t k0 = 0, k1 = 0;  // the instance's pack key
+            float eps = 0.f, eb = 0.f;
+            const SInst* in = nullptr;
+            for (int item = lo; item < hi; ++item) {
+                if (item >= b_end) {  // next instance (flush the previous one's energies)
+                    if (count && b >= 0 && lane_on) sf_flush(a, b, m0, fl, gl);
+                    b = (b < 0) ? sf_find_instance(pref, a.B, item) : b + 1;
+                    while (pref[b + 1] <= item) ++b;
+                    b_end = pref[b + 1];
+                    p0 = pref[b];
+                    in = a.inst + b;
+                    cs = a.color_start[in->color_off + c];
+                    ce = a.color_start[in->color_off + c + 1];
+                    k0 = (uint32_t)in->pkey;
+                    k1 = (uint32_t)(in->pkey >> 32);
+                    eps = in->eps;
+                    eb = 2.0f * in->beta_max * in->eps;
+                    if (lane_on) {
+                        const float4* lp = reinterpret_cast<const float4*>(a.lab + (size_t)b * a.Rp + m0);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const float4 v = lp[q];
+                            bt[2 * q] = v.x; tp[2 * q] = v.y; bt[2 * q + 1] = v.z; tp[2 * q + 1] = v.w;
+                        }
+                    }
+                }
+                const int i = cs + (item - p0) * spw + sub;
+                if (!lane_on || i >= ce) continue;
+                int8_t* sp = a.spins + in->spin_off;
+                // the site's entries {j | cm << 28 | fwd << 27, float J}
+                const int2* ep = a.entp + in->entp_off + (size_t)i * D;
+                int2 e[D];
+#pragma unroll
+                for (int q = 0; q < D / 2; ++q) {
+                    const int4 v = __ldg(reinterpret_cast<const int4*>(ep) + q);
+                    e[2 * q] = make_int2(v.x, v.y);
+                    e[2 * q + 1] = make_int2(v.z, v.w);
+                }
+                uint2 rk[DEG];
+#pragma unroll
+                for (int k = 0; k < DEG; ++k)
+                    rk[k] = *reinterpret_cast<const uint2*>(sp + (size_t)(unsigned)(e[k].x & 0x07ffffff) * Rp + m0);
+                uint2* own = reinterpret_cast<uint2*>(sp + (size_t)(unsigned)i * Rp + m0);
+                const uint2 s0 = *own;
+                const float h32 = __ldg(a.h32 + in->h_off + i);
+                const u32x4 o = philox4x32_10(u32x4{(uint32_t)i, tlo, thi, (uint32_t)grp | (1u << 30)}, k0, k1);
+                float cmf[DEG], jw[DEG];
+#pragma unroll
+                for (int k = 0; k < DEG; ++k) {
+                    cmf[k] = (float)((e[k].x >> 28) & 15);
+                    jw[k] = __int_as_float(e[k].y);
+                }
+                uint32_t fm0 = 0u, fm1 = 0u;  // bytes to flip (0xFE: +1 <-> -1)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t ow = j < 4 ? s0.x : s0.y;
+                    const int bj = j & 3;
+                    float l = h32;
+#pragma unroll
+                    for (int k = 0; k < DEG; ++k)
+                        l += sf_signed(fmaf(cmf[k], tp[j], jw[k]), j < 4 ? rk[k].x : rk[k].y, bj);
+                    const uint32_t hw = ((j < 2 ? o.x : j < 4 ? o.y : j < 6 ? o.z : o.w) >> (16 * (j & 1))) & 0xFFFFu;
+                    const float uf = (float)hw * 0x1.0p-16f;
+                    const float sl = sf_signed(l, ow, bj);  // s_i * l
+                    int dec = 0;                            // 1 flip, -1 keep, 0 undecided
+                    if (RULE == 0) {
+                        const float de = 2.0f * sl;
+                        const float tol = 2.0f * eps;
+                        if (de < -tol) dec = 1;
+                        else if (de > tol) {
+                            const float x = -bt[j] * de;
+                            const float T = __expf(x);
+                            const float band = T * (2.0f * eb + fabsf(x) * 0x1.0p-19f + 0x1.0p-18f);
+                            if (uf + 0x1.0p-16f <= T - band) dec = 1;
+                            else if (uf >= T + band) dec = -1;
+                        }
+                    } else {  // heat bath: new spin +1 iff u < sigma(2 beta l); dec on the flip
+                        const float y = 2.0f * bt[j] * l;
+                        const float p = __frcp_rn(1.0f + __expf(-y));
+                        const float band = eb + fabsf(y) * 0x1.0p-19f + 0x1.0p-18f;
+                        const bool up = ((ow >> (8 * bj + 7)) & 1u) == 0u;  // current spin +1
+                        if (uf + 0x1.0p-16f <= p - band) dec = up ? -1 : 1;   // new +1
+                        else if (uf >= p + band) dec = up ? 1 : -1;           // new -1
+                    }
+                    if (dec == 0) {  // FP64 with all 53 bits
+                        const int m = m0 + j;
+                        const u32x4 q2 = philox4x32_10(u32x4{(uint32_t)i, tlo, thi, (uint32_t)m | (2u << 30)}, k0, k1);
+                        const uint64_t u53 = ((uint64_t)hw << 37) |
+                                             (((uint64_t)q2.x | ((uint64_t)q2.y << 32)) & ((1ull << 37) - 1ull));
+                        const int si8 = ((ow >> (8 * bj + 7)) & 1u) ? -1 : 1;
+                        const int nv = sf_exact(a, *in, sp, i, m, si8, u53, a.sbeta[(size_t)b * a.Rp + m],
+                                                a.stwop[(size_t)b * a.Rp + m], RULE);
+                        dec = nv != si8 ? 1 : -1;
+                    }
+                    if (dec > 0) {
+                        if (j < 4) fm0 |= 0xFEu << (8 * bj);
+                        else fm1 |= 0xFEu << (8 * bj);
+                    }
+                }
+                const uint2 s1 = make_uint2(s0.x ^ fm0, s0.y ^ fm1);
+                if (fm0 | fm1) *own = s1;
+                if (count) {  // bonds to lower-colour neighbours (each bond once) and the field
+                    const double* wp = a.wp + in->entp_off + (size_t)i * D;
+                    const double h64 = a.h[in->h_off + i];
+#pragma unroll
+                    for (int k = 0; k < DEG; ++k) {
+                        const int jn = e[k].x & 0x07ffffff;
+                        if (jn >= cs) continue;
+                        const double wk = wp[k];
+                        const int cmk = (e[k].x >> 28) & 15;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const uint32_t a8 = ((j < 4 ? s1.x : s1.y) ^ (j < 4 ? rk[k].x : rk[k].y)) >> (8 * (j & 3) + 7);
+                            const bool diff = (a8 & 1u) != 0u;  // s_i != s_k
+                            fl[j] += diff ? wk : -wk;           // -J s_i s_k
+                            if (diff) gl[j] += cmk;
+                        }
+                    }
+                    if (h64 != 0.0) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const bool neg = (((j < 4 ? s1.x : s1.y) >> (8 * (j & 3) + 7)) & 1u) != 0u;
+                            fl[j] += neg ? h64 : -h64;          // -h_i s_i
+                        }
+                    }
+                }
+            }
+            if (count && b >= 0 && lane_on) sf_flush(a, b, m0, fl, gl);
+            grid.sync();
+        }
+    }
+    if (!do_energy) return;
+    // (f, g) of every replica: f = cost energy, g = 4 x unsatisfied chain bonds
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < a.B * a.R; q += gridDim.x * blockDim.x) {
+        const int b = q / a.R, r = q % a.R;
+        const size_t x = (size_t)b * a.Rp + r;
+        a.f[q] = (double)a.fx[x] * 0x1.0p-40;
+        a.g[q] = 4.0 * (double)a.gx[x];
+        a.fx[x] = 0;
+        a.gx[x] = 0;
+    }
+}
+
+template __global__ void slotf_sweep_kernel<0, 3, 4>(const __grid_constant__ S2Args, int64_t, int, int);
+template __global__ void slotf_sweep_kernel<1, 3, 4>(const __grid_constant__ S2Args, int64_t, int, int);
+template __global__ void slotf_sweep_kernel<0, 4, 4>(const __grid_constant__ S2Args, int64_t, int, int);
+template __global__ void slotf_sweep_kernel<1, 4, 4>(const __grid_constant__ S2Args, int64_t, int, int);
+template __global__ void slotf_sweep_kernel<0, 8, 8>(const __grid_constant__ S2Args, int64_t, int, int);
+template __global__ void slotf_sweep_kernel<1, 8, 8>(const __grid_constant__ S2Args, int64_t, int, int);
+
+// deg: the batch's largest merged degree (<= 8)
+void* slotf_sweep_fn(int rule, int deg) {
+    if (deg <= 3) return rule ? (void*)slotf_sweep_kernel<1, 3, 4> : (void*)slotf_sweep_kernel<0, 3, 4>;
+    if (deg <= 4) return rule ? (void*)slotf_sweep_kernel<1, 4, 4> : (void*)slotf_sweep_kernel<0, 4, 4>;
+    return rule ? (void*)slotf_sweep_kernel<1, 8, 8> : (void*)slotf_sweep_kernel<0, 8, 8>;
+}
+
+}  // namespace tg

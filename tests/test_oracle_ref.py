@@ -40,7 +40,8 @@ CASES = [
     ("one_by_one", lambda: I.k10_pm1(2), [1.0], [2.0], 40, 4),
 ]
 VARIANTS = [("metropolis", "slot", "philox"), ("heat_bath", "slot", "philox_hb"),
-            ("metropolis", "plane", "plane"), ("heat_bath", "plane", "plane_hb")]
+            ("metropolis", "plane", "plane"), ("heat_bath", "plane", "plane_hb"),
+            ("metropolis", "float", "pack"), ("heat_bath", "float", "pack_hb")]
 
 
 @needs_ref
