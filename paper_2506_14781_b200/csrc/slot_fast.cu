@@ -54,7 +54,7 @@ __device__ __forceinline__ float sf_signed(float w, uint32_t word, int k) {
 // FP64 decision of one replica with all 53 bits (the semantics the FP32 path
 // certifies): local field in the reference's merged-CSR order
 // (constraints.cpp:122-140, ising.cpp:79-88), then mc.cpp:27-29 / heat bath.
-__device__ __noinline__ int sf_exact(const S2Args& a, const SInst& in, const int8_t* sp, int i, int r,
+__device__ __forceinline__ int sf_exact(const S2Args& a, const SInst& in, const int8_t* sp, int i, int r,
                                      int si8, uint64_t u53, double beta, double two_p, int rule) {
     double local = a.h[in.h_off + i];
     const int e0 = a.off[in.csr_off + i], e1 = a.off[in.csr_off + i + 1];
@@ -74,17 +74,19 @@ __device__ __noinline__ int sf_exact(const S2Args& a, const SInst& in, const int
 
 // Per-thread accumulators of one instance: FP64 cost energy and chain-bond
 // counts of the thread's 8 replicas, flushed as fixed point.
-__device__ __forceinline__ void sf_flush(const S2Args& a, int b, int m0, double (&fl)[8], int (&gl)[8]) {
+__device__ __forceinline__ void sf_flush(const S2Args& a, int b, int m0, double (&fl)[8], uint32_t (&g16)[4]) {
     long long* fx = a.fx + (size_t)b * a.Rp + m0;
     int* gx = a.gx + (size_t)b * a.Rp + m0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
+        const int gj = (int)((g16[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
         if (fl[j] != 0.0) atomicAdd(reinterpret_cast<unsigned long long*>(fx + j),
                                     (unsigned long long)__double2ll_rn(fl[j] * 0x1.0p40));
-        if (gl[j]) atomicAdd(gx + j, gl[j]);
+        if (gj) atomicAdd(gx + j, gj);
         fl[j] = 0.0;
-        gl[j] = 0;
     }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) g16[j] = 0u;
 }
 
 template <int RULE, int DEG, int D>
@@ -107,9 +109,12 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
         const uint32_t tlo = (uint32_t)t, thi = (uint32_t)(t >> 32);
         const bool count = do_energy && swp == n_sweeps - 1;
         double fl[8];
-        int gl[8];
+        uint32_t g16[4];  // chain counters, two replicas per word (16-bit lanes)
+        int since = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) { fl[j] = 0.0; gl[j] = 0; }
+        for (int j = 0; j < 8; ++j) fl[j] = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) g16[j] = 0u;
         for (int c = 0; c < a.max_colors; ++c) {
             const int* pref = a.fitem_pref + (size_t)c * (a.B + 1);
             const int total = pref[a.B];
@@ -118,11 +123,12 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
             int cs = 0, ce = 0, p0 = 0;
             float bt[8], tp[8];       // beta, 2P of the lanes' replicas (current instance)
             uint32_t k0 = 0, k1 = 0;  // the instance's pack key
-            float eps = 0.f, eb = 0.f;
+            float tol = 0.f, c1 = 0.f;  // de dead band; band coefficient of T (p)
             const SInst* in = nullptr;
             for (int item = lo; item < hi; ++item) {
                 if (item >= b_end) {  // next instance (flush the previous one's energies)
-                    if (count && b >= 0 && lane_on) sf_flush(a, b, m0, fl, gl);
+                    if (count && b >= 0 && lane_on) sf_flush(a, b, m0, fl, g16);
+                    since = 0;
                     b = (b < 0) ? sf_find_instance(pref, a.B, item) : b + 1;
                     while (pref[b + 1] <= item) ++b;
                     b_end = pref[b + 1];
@@ -132,8 +138,12 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                     ce = a.color_start[in->color_off + c + 1];
                     k0 = (uint32_t)in->pkey;
                     k1 = (uint32_t)(in->pkey >> 32);
-                    eps = in->eps;
-                    eb = 2.0f * in->beta_max * in->eps;
+                    {   // error band of slot_engine.cu s2_update: T (2 eb + |x| 2^-19 + 2^-18),
+                        // heat bath eb + |y| 2^-19 + 2^-18, eb = 2 beta_max eps
+                        const float eb = 2.0f * in->beta_max * in->eps;
+                        tol = 2.0f * in->eps;
+                        c1 = RULE == 0 ? 2.0f * eb + 0x1.0p-18f : eb + 0x1.0p-18f;
+                    }
                     if (lane_on) {
                         const float4* lp = reinterpret_cast<const float4*>(a.lab + (size_t)b * a.Rp + m0);
 #pragma unroll
@@ -163,55 +173,79 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                 const uint2 s0 = *own;
                 const float h32 = __ldg(a.h32 + in->h_off + i);
                 const u32x4 o = philox4x32_10(u32x4{(uint32_t)i, tlo, thi, (uint32_t)grp | (1u << 30)}, k0, k1);
-                float cmf[DEG], jw[DEG];
+                // field of the 8 replicas: cost couplings (item-uniform J) and
+                // chain multiplicities times the replica's 2P
+                float l[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) l[j] = h32;
 #pragma unroll
                 for (int k = 0; k < DEG; ++k) {
-                    cmf[k] = (float)((e[k].x >> 28) & 15);
-                    jw[k] = __int_as_float(e[k].y);
+                    const float jk = __int_as_float(e[k].y);
+                    const int cmk = (e[k].x >> 28) & 15;
+                    if (jk != 0.0f) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) l[j] += sf_signed(jk, j < 4 ? rk[k].x : rk[k].y, j & 3);
+                    }
+                    if (cmk) {
+                        const float cf = (float)cmk;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            l[j] = fmaf(sf_signed(cf, j < 4 ? rk[k].x : rk[k].y, j & 3), tp[j], l[j]);
+                    }
                 }
+                // certified decisions from the 16-bit prefix; undecided replicas
+                // (|u - T| inside the error band) take the FP64 path below
                 uint32_t fm0 = 0u, fm1 = 0u;  // bytes to flip (0xFE: +1 <-> -1)
+                uint32_t und = 0u;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const uint32_t ow = j < 4 ? s0.x : s0.y;
                     const int bj = j & 3;
-                    float l = h32;
-#pragma unroll
-                    for (int k = 0; k < DEG; ++k)
-                        l += sf_signed(fmaf(cmf[k], tp[j], jw[k]), j < 4 ? rk[k].x : rk[k].y, bj);
+                    const float lj = l[j];
                     const uint32_t hw = ((j < 2 ? o.x : j < 4 ? o.y : j < 6 ? o.z : o.w) >> (16 * (j & 1))) & 0xFFFFu;
-                    const float uf = (float)hw * 0x1.0p-16f;
-                    const float sl = sf_signed(l, ow, bj);  // s_i * l
-                    int dec = 0;                            // 1 flip, -1 keep, 0 undecided
+                    const float uf0 = __uint2float_rn(hw) * 0x1.0p-16f;
+                    const float uf1 = uf0 + 0x1.0p-16f;
+                    bool flip, undec;
                     if (RULE == 0) {
-                        const float de = 2.0f * sl;
-                        const float tol = 2.0f * eps;
-                        if (de < -tol) dec = 1;
-                        else if (de > tol) {
-                            const float x = -bt[j] * de;
-                            const float T = __expf(x);
-                            const float band = T * (2.0f * eb + fabsf(x) * 0x1.0p-19f + 0x1.0p-18f);
-                            if (uf + 0x1.0p-16f <= T - band) dec = 1;
-                            else if (uf >= T + band) dec = -1;
-                        }
-                    } else {  // heat bath: new spin +1 iff u < sigma(2 beta l); dec on the flip
-                        const float y = 2.0f * bt[j] * l;
+                        const float de = 2.0f * sf_signed(lj, ow, bj);  // 2 s_i l
+                        const float x = -bt[j] * de;
+                        const float T = __expf(x);
+                        const float band = T * fmaf(fabsf(x), 0x1.0p-19f, c1);
+                        const bool pos = de > tol;
+                        const bool acc = de < -tol || (pos && uf1 + band <= T);
+                        const bool rej = pos && uf0 >= T + band;
+                        flip = acc;
+                        undec = !(acc || rej);
+                    } else {  // heat bath: new spin +1 iff u < sigma(2 beta l)
+                        const float y = 2.0f * bt[j] * lj;
                         const float p = __frcp_rn(1.0f + __expf(-y));
-                        const float band = eb + fabsf(y) * 0x1.0p-19f + 0x1.0p-18f;
+                        const float band = fmaf(fabsf(y), 0x1.0p-19f, c1);
                         const bool up = ((ow >> (8 * bj + 7)) & 1u) == 0u;  // current spin +1
-                        if (uf + 0x1.0p-16f <= p - band) dec = up ? -1 : 1;   // new +1
-                        else if (uf >= p + band) dec = up ? 1 : -1;           // new -1
+                        const bool nup = uf1 + band <= p, ndown = uf0 >= p + band;
+                        flip = up ? ndown : nup;
+                        undec = !(nup || ndown);
                     }
-                    if (dec == 0) {  // FP64 with all 53 bits
-                        const int m = m0 + j;
-                        const u32x4 q2 = philox4x32_10(u32x4{(uint32_t)i, tlo, thi, (uint32_t)m | (2u << 30)}, k0, k1);
-                        const uint64_t u53 = ((uint64_t)hw << 37) |
-                                             (((uint64_t)q2.x | ((uint64_t)q2.y << 32)) & ((1ull << 37) - 1ull));
-                        const int si8 = ((ow >> (8 * bj + 7)) & 1u) ? -1 : 1;
-                        const int nv = sf_exact(a, *in, sp, i, m, si8, u53, a.sbeta[(size_t)b * a.Rp + m],
-                                                a.stwop[(size_t)b * a.Rp + m], RULE);
-                        dec = nv != si8 ? 1 : -1;
+                    if (flip) {
+                        if (j < 4) fm0 |= 0xFEu << (8 * bj);
+                        else fm1 |= 0xFEu << (8 * bj);
                     }
-                    if (dec > 0) {
+                    und |= (uint32_t)undec << j;
+                }
+                while (und) {  // FP64 with all 53 bits (rare)
+                    const int j = __ffs(und) - 1;
+                    und &= und - 1;
+                    const int m = m0 + j;
+                    const uint32_t ow = j < 4 ? s0.x : s0.y;
+                    const int bj = j & 3;
+                    const uint32_t ox = j < 2 ? o.x : j < 4 ? o.y : j < 6 ? o.z : o.w;
+                    const uint32_t hw = (ox >> (16 * (j & 1))) & 0xFFFFu;
+                    const u32x4 q2 = philox4x32_10(u32x4{(uint32_t)i, tlo, thi, (uint32_t)m | (2u << 30)}, k0, k1);
+                    const uint64_t u53 = ((uint64_t)hw << 37) |
+                                         (((uint64_t)q2.x | ((uint64_t)q2.y << 32)) & ((1ull << 37) - 1ull));
+                    const int si8 = ((ow >> (8 * bj + 7)) & 1u) ? -1 : 1;
+                    const int nv = sf_exact(a, *in, sp, i, m, si8, u53, a.sbeta[(size_t)b * a.Rp + m],
+                                            a.stwop[(size_t)b * a.Rp + m], RULE);
+                    if (nv != si8) {
                         if (j < 4) fm0 |= 0xFEu << (8 * bj);
                         else fm1 |= 0xFEu << (8 * bj);
                     }
@@ -219,32 +253,47 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                 const uint2 s1 = make_uint2(s0.x ^ fm0, s0.y ^ fm1);
                 if (fm0 | fm1) *own = s1;
                 if (count) {  // bonds to lower-colour neighbours (each bond once) and the field
-                    const double* wp = a.wp + in->entp_off + (size_t)i * D;
-                    const double h64 = a.h[in->h_off + i];
+                    uint2 gb = make_uint2(0u, 0u);  // unsatisfied chain bonds x multiplicity, per byte
 #pragma unroll
                     for (int k = 0; k < DEG; ++k) {
                         const int jn = e[k].x & 0x07ffffff;
                         if (jn >= cs) continue;
-                        const double wk = wp[k];
                         const int cmk = (e[k].x >> 28) & 15;
+                        const uint32_t dx = s1.x ^ rk[k].x, dy = s1.y ^ rk[k].y;  // bytes 0xFE where s_i != s_k
+                        if (__int_as_float(e[k].y) != 0.0f) {
+                            const double nwk = -a.wp[in->entp_off + (size_t)i * D + k];  // -J s_i s_k, s_i = s_k
+                            const int hi = __double2hiint(nwk), lo = __double2loint(nwk);
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const uint32_t a8 = ((j < 4 ? s1.x : s1.y) ^ (j < 4 ? rk[k].x : rk[k].y)) >> (8 * (j & 3) + 7);
-                            const bool diff = (a8 & 1u) != 0u;  // s_i != s_k
-                            fl[j] += diff ? wk : -wk;           // -J s_i s_k
-                            if (diff) gl[j] += cmk;
+                            for (int j = 0; j < 8; ++j) {
+                                const uint32_t d = j < 4 ? dx : dy;
+                                fl[j] += __hiloint2double(hi ^ (int)((d << (24 - 8 * (j & 3))) & 0x80000000u), lo);
+                            }
+                        }
+                        if (cmk) {
+                            gb.x += ((dx >> 7) & 0x01010101u) * (uint32_t)cmk;
+                            gb.y += ((dy >> 7) & 0x01010101u) * (uint32_t)cmk;
                         }
                     }
+                    g16[0] += __byte_perm(gb.x, 0u, 0x4140);
+                    g16[1] += __byte_perm(gb.x, 0u, 0x4342);
+                    g16[2] += __byte_perm(gb.y, 0u, 0x4140);
+                    g16[3] += __byte_perm(gb.y, 0u, 0x4342);
+                    const double h64 = a.h[in->h_off + i];
                     if (h64 != 0.0) {
+                        const int hi = __double2hiint(-h64), lo = __double2loint(-h64);  // -h_i s_i
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
-                            const bool neg = (((j < 4 ? s1.x : s1.y) >> (8 * (j & 3) + 7)) & 1u) != 0u;
-                            fl[j] += neg ? h64 : -h64;          // -h_i s_i
+                            const uint32_t w = j < 4 ? s1.x : s1.y;
+                            fl[j] += __hiloint2double(hi ^ (int)((w << (24 - 8 * (j & 3))) & 0x80000000u), lo);
                         }
+                    }
+                    if (++since >= 1024) {  // 16-bit chain counters: flush well before overflow
+                        sf_flush(a, b, m0, fl, g16);
+                        since = 0;
                     }
                 }
             }
-            if (count && b >= 0 && lane_on) sf_flush(a, b, m0, fl, gl);
+            if (count && b >= 0 && lane_on) sf_flush(a, b, m0, fl, g16);
             grid.sync();
         }
     }
