@@ -93,7 +93,6 @@ template <int RULE, int DEG, int D>
 __global__ void __launch_bounds__(kSlotFThreads, 1)
 slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, int do_energy) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ float2 s_lab[8][kSlotFThreads];  // (beta, 2P) of each thread's 8 replicas
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
@@ -122,37 +121,10 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
             const int lo = (int)((long long)wi * total / nwi), hi = (int)((long long)(wi + 1) * total / nwi);
             int b = -1, b_end = 0;
             int cs = 0, ce = 0, p0 = 0;
+            float bt[8], tp[8];       // beta, 2P of the lanes' replicas (current instance)
             uint32_t k0 = 0, k1 = 0;  // the instance's pack key
             float tol = 0.f, c1 = 0.f;  // de dead band; band coefficient of T (p)
             const SInst* in = nullptr;
-            struct Item {
-                int i;
-                bool ok;
-                int2 e[DEG];    // entries {j | cm << 28 | fwd << 27, float J}
-                uint2 rk[DEG];  // the neighbours' rows (8 replicas)
-                uint2 s0;       // own row
-                float h32;
-            };
-            Item cur, nxt;
-            bool have_nxt = false;
-            auto fetch = [&](int it, Item& x) {
-                x.i = cs + (it - p0) * spw + sub;
-                x.ok = lane_on && x.i < ce;
-                if (!x.ok) return;
-                const int8_t* sp = a.spins + in->spin_off;
-                const int4* ep = reinterpret_cast<const int4*>(a.entp + in->entp_off + (size_t)x.i * D);
-#pragma unroll
-                for (int q = 0; q < (DEG + 1) / 2; ++q) {
-                    const int4 v = __ldg(ep + q);
-                    x.e[2 * q] = make_int2(v.x, v.y);
-                    if (2 * q + 1 < DEG) x.e[2 * q + 1] = make_int2(v.z, v.w);
-                }
-#pragma unroll
-                for (int k = 0; k < DEG; ++k)
-                    x.rk[k] = *reinterpret_cast<const uint2*>(sp + (size_t)(unsigned)(x.e[k].x & 0x07ffffff) * Rp + m0);
-                x.s0 = *reinterpret_cast<const uint2*>(sp + (size_t)(unsigned)x.i * Rp + m0);
-                x.h32 = __ldg(a.h32 + in->h_off + x.i);
-            };
             for (int item = lo; item < hi; ++item) {
                 if (item >= b_end) {  // next instance (flush the previous one's energies)
                     if (count && b >= 0 && lane_on) sf_flush(a, b, m0, fl, g16);
@@ -172,31 +144,34 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                         tol = 2.0f * in->eps;
                         c1 = RULE == 0 ? 2.0f * eb + 0x1.0p-18f : eb + 0x1.0p-18f;
                     }
-                    if (lane_on) {  // the thread's (beta, 2P) pairs into its shared-memory column
+                    if (lane_on) {
                         const float4* lp = reinterpret_cast<const float4*>(a.lab + (size_t)b * a.Rp + m0);
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
                             const float4 v = lp[q];
-                            s_lab[2 * q][threadIdx.x] = make_float2(v.x, v.y);
-                            s_lab[2 * q + 1][threadIdx.x] = make_float2(v.z, v.w);
+                            bt[2 * q] = v.x; tp[2 * q] = v.y; bt[2 * q + 1] = v.z; tp[2 * q + 1] = v.w;
                         }
                     }
-                    have_nxt = false;
                 }
-                // this item's data (prefetched during the previous item when it
-                // belongs to the same instance), then the next item's loads
-                if (have_nxt) cur = nxt;
-                else fetch(item, cur);
-                have_nxt = item + 1 < hi && item + 1 < b_end;
-                if (have_nxt) fetch(item + 1, nxt);
-                if (!cur.ok) continue;
-                const int i = cur.i;
+                const int i = cs + (item - p0) * spw + sub;
+                if (!lane_on || i >= ce) continue;
                 int8_t* sp = a.spins + in->spin_off;
-                const int2* e = cur.e;
-                const uint2* rk = cur.rk;
+                // the site's entries {j | cm << 28 | fwd << 27, float J}
+                const int2* ep = a.entp + in->entp_off + (size_t)i * D;
+                int2 e[D];
+#pragma unroll
+                for (int q = 0; q < D / 2; ++q) {
+                    const int4 v = __ldg(reinterpret_cast<const int4*>(ep) + q);
+                    e[2 * q] = make_int2(v.x, v.y);
+                    e[2 * q + 1] = make_int2(v.z, v.w);
+                }
+                uint2 rk[DEG];
+#pragma unroll
+                for (int k = 0; k < DEG; ++k)
+                    rk[k] = *reinterpret_cast<const uint2*>(sp + (size_t)(unsigned)(e[k].x & 0x07ffffff) * Rp + m0);
                 uint2* own = reinterpret_cast<uint2*>(sp + (size_t)(unsigned)i * Rp + m0);
-                const uint2 s0 = cur.s0;
-                const float h32 = cur.h32;
+                const uint2 s0 = *own;
+                const float h32 = __ldg(a.h32 + in->h_off + i);
                 const u32x4 o = philox4x32_10(u32x4{(uint32_t)i, tlo, thi, (uint32_t)grp | (1u << 30)}, k0, k1);
                 // field of the 8 replicas: cost couplings (item-uniform J) and
                 // chain multiplicities times the replica's 2P
@@ -215,7 +190,7 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                         const float cf = (float)cmk;
 #pragma unroll
                         for (int j = 0; j < 8; ++j)
-                            l[j] = fmaf(sf_signed(cf, j < 4 ? rk[k].x : rk[k].y, j & 3), s_lab[j][threadIdx.x].y, l[j]);
+                            l[j] = fmaf(sf_signed(cf, j < 4 ? rk[k].x : rk[k].y, j & 3), tp[j], l[j]);
                     }
                 }
                 // certified decisions from the 16-bit prefix; undecided replicas
@@ -233,7 +208,7 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                     bool flip, undec;
                     if (RULE == 0) {
                         const float de = 2.0f * sf_signed(lj, ow, bj);  // 2 s_i l
-                        const float x = -s_lab[j][threadIdx.x].x * de;
+                        const float x = -bt[j] * de;
                         const float T = __expf(x);
                         const float band = T * fmaf(fabsf(x), 0x1.0p-19f, c1);
                         const bool pos = de > tol;
@@ -242,7 +217,7 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                         flip = acc;
                         undec = !(acc || rej);
                     } else {  // heat bath: new spin +1 iff u < sigma(2 beta l)
-                        const float y = 2.0f * s_lab[j][threadIdx.x].x * lj;
+                        const float y = 2.0f * bt[j] * lj;
                         const float p = __frcp_rn(1.0f + __expf(-y));
                         const float band = fmaf(fabsf(y), 0x1.0p-19f, c1);
                         const bool up = ((ow >> (8 * bj + 7)) & 1u) == 0u;  // current spin +1
