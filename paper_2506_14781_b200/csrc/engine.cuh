@@ -27,6 +27,16 @@ constexpr int kVPlanes = 8;               // vertical counter planes
 constexpr int kMaxTypes = 16;
 constexpr int kMaxWordsArg = 32;       // plane engine: <= 1024 replicas per rank
 
+// Round counters of the unfused round loop, kept on the device so that a
+// captured CUDA graph of rounds can be replayed unchanged: the sweep, swap
+// and extract kernels read them, round_tick_kernel advances them.
+struct RoundState {
+    int64_t round;       // rounds completed
+    uint64_t swap_base;  // swap-stream draws consumed
+    int32_t filled;      // records in the current chunk
+    int32_t pad;
+};
+
 // One (cost degree, chain degree) class of sites in the plane engine.
 struct PlaneType {
     int dc, dq;      // cost / chain degree of every site of this type
@@ -74,6 +84,7 @@ struct PlaneArgs {
     int32_t* cnt_q;       // [32W] unsatisfied chain bonds
     double* f_loc;        // [local_states]
     double* g_loc;
+    const RoundState* rs; // unfused loop: sweep index t0 = rs->round * n_sweeps (else the argument)
 };
 
 struct SlotArgs {
@@ -103,6 +114,7 @@ struct SlotArgs {
     const uint64_t* slot_key;  // [R] derive_seed(seed, replica, slot)
     double* f_loc;
     double* g_loc;
+    const RoundState* rs;      // unfused loop: t0 = rs->round * n_sweeps (else the argument)
 };
 
 // Fused single-GPU round loop (plane engine).
@@ -161,6 +173,7 @@ struct SwapArgs {
     int ktab_row;
     uint32_t* kp;
     uint32_t* kpc;
+    const RoundState* rs;  // round = rs->round + 1, swap_base, record index from it (else arguments)
 };
 
 // ------------------------------------------------- SLOT engine v2 (batched)

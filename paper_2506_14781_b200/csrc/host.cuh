@@ -25,6 +25,8 @@
 #include <utility>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/tempergrid_b200.h"
 #include "engine.cuh"
 #include "kernels.cuh"
@@ -170,6 +172,15 @@ struct HostVec {
     const T& operator[](size_t i) const { return p[i]; }
     T* begin() { return p.get(); }
     T* end() { return p.get() + n; }
+};
+
+// NVTX range for the host-side phases (sweep launches, swap / exchange,
+// record drains): visible in Nsight timelines, free when no tool is attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 struct HostTimer {
@@ -370,9 +381,23 @@ struct tg_ctx {
     std::vector<cudaEvent_t> ev;
     double last_sweep_ms = 0, last_swap_ms = 0;
     int64_t sweep_launches = 0, other_launches = 0;
+    // unfused round loop (multi-GPU, full-grid records): device round state,
+    // per-chunk target digests, CUDA graphs of whole chunks keyed by length
+    DBuf<RoundState> d_rstate;
+    DBuf<uint64_t> d_dig;
+    HostVec<uint64_t> h_dig;
+    RoundState h_rstate{};
+    std::map<int, cudaGraphExec_t> graphs;
+    bool graphs_ok = true;
+    int64_t graph_launches = 0;
+    void clear_graphs() {
+        for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+        graphs.clear();
+    }
 
     ~tg_ctx() {
         t_alloc_stream = stream;
+        clear_graphs();
         for (auto e : ev) cudaEventDestroy(e);
         if (comm) nccl().CommDestroy(comm);
         // members free their buffers on `stream`; stream_owner destroys it last
@@ -434,10 +459,10 @@ void build_slot(tg_ctx& c);
 PlaneArgs plane_args(tg_ctx& c);
 SlotArgs slot_args(tg_ctx& c);
 SwapArgs swap_args(tg_ctx& c);
-void launch_sweep(tg_ctx& c, int64_t t0);
+void launch_sweep(tg_ctx& c, int64_t t0, const RoundState* rs = nullptr);
 void rebuild_planes(tg_ctx& c);
 void do_init(tg_ctx& c, const tg_run_config* cfg);
-void drain(tg_ctx& c, int filled, int64_t first_round, const SinkCtx& sink);
+void drain(tg_ctx& c, int filled, int64_t first_round, const SinkCtx& sink, bool dig_array = false);
 void profile_chunk(tg_ctx& c, int filled, double& sweep_ms, double& other_ms);
 void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink);
 int single_sink_adapter(void* user, int32_t, const tg_record* recs, int64_t n, const int8_t* st,

@@ -452,6 +452,7 @@ void rebuild_planes(tg_ctx& c) {
 void s2_build(tg_ctx& c, const tg_run_config* cfg);
 
 void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
+    NvtxRange nv_("tg: fused rounds (sweeps + swaps + records)");
     cudaStream_t st = c.stream;
     const int flags = c.cfg.record_flags;
     if (c.profiling && c.ev.size() < 2) {
@@ -516,7 +517,10 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         for (int k = 0; k < n; ++k) c.swap_base += (uint64_t)round_attempts(c.I, c.J, first + k);
         c.rounds_done += n;
         left -= n;
-        drain(c, n, first, sink);
+        {
+            NvtxRange nr_("tg: drain records");
+            drain(c, n, first, sink);
+        }
         if (c.profiling) {
             float ms = 0;
             CK(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));

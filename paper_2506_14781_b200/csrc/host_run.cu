@@ -34,10 +34,11 @@ SwapArgs swap_args(tg_ctx& c) {
     return a;
 }
 
-void launch_sweep(tg_ctx& c, int64_t t0) {
+void launch_sweep(tg_ctx& c, int64_t t0, const RoundState* rs) {
     const int sps = (int)c.cfg.sweeps_per_swap;
     if (c.engine == TG_ENGINE_PLANE) {
         PlaneArgs a = plane_args(c);
+        a.rs = rs;
         int64_t t = t0;
         int nsw = sps;
         void* args[] = {&a, &t, &nsw};
@@ -52,6 +53,7 @@ void launch_sweep(tg_ctx& c, int64_t t0) {
         }
     } else {
         SlotArgs a = slot_args(c);
+        a.rs = rs;
         int64_t t = t0;
         int nsw = sps;
         void* args[] = {&a, &t, &nsw};
@@ -66,6 +68,8 @@ void launch_sweep(tg_ctx& c, int64_t t0) {
 // kernel's plane-rebuild with a round that attempts nothing.
 void do_init(tg_ctx& c, const tg_run_config* cfg) {
     HostTimer tm_("init (total)");
+    c.clear_graphs();  // captured kernel arguments point at the previous buffers
+    c.graphs_ok = true;
     if (!c.have_problem) fail(TG_ERR_CONFIG, "run: no problem set");
     if (!c.have_schedule) fail(TG_ERR_CONFIG, "run: no schedule set");
     if (cfg->sweeps_per_swap < 1) fail(TG_ERR_CONFIG, "run: sweeps_per_swap must be >= 1");
@@ -161,10 +165,14 @@ void do_init(tg_ctx& c, const tg_run_config* cfg) {
     CK(cudaStreamSynchronize(st));
 }
 
-void drain(tg_ctx& c, int filled, int64_t first_round, const SinkCtx& sink) {
+void drain(tg_ctx& c, int filled, int64_t first_round, const SinkCtx& sink, bool dig_array) {
     if (filled <= 0) return;
     cudaStream_t st = c.stream;
     CK(cudaMemcpyAsync(c.h_rec.data(), c.d_rec.p, sizeof(TgRecordDev) * filled, cudaMemcpyDeviceToHost, st));
+    if (dig_array) {  // unfused loop: digests gathered (and all-reduced) in d_dig
+        c.h_dig.resize(c.rec_cap);
+        CK(cudaMemcpyAsync(c.h_dig.data(), c.d_dig.p, sizeof(uint64_t) * filled, cudaMemcpyDeviceToHost, st));
+    }
     const int flags = c.cfg.record_flags;
     const size_t per_state = (flags & TG_REC_GRID) ? (size_t)c.R * c.n : ((flags & TG_REC_STATE) ? (size_t)c.n : 0);
     if (per_state)
@@ -196,7 +204,7 @@ void drain(tg_ctx& c, int filled, int64_t first_round, const SinkCtx& sink) {
         r.g = d.g;
         r.feasible = d.feasible;
         r.target_state = d.target_state;
-        r.digest = d.digest;
+        r.digest = dig_array ? c.h_dig[k] : d.digest;
         out.push_back(r);
         if (per_state) outs.insert(outs.end(), c.h_states.begin() + (size_t)k * per_state,
                                    c.h_states.begin() + (size_t)(k + 1) * per_state);
@@ -251,68 +259,123 @@ void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
     const int flags = c.cfg.record_flags;
     const bool need_extract = (flags & (TG_REC_DIGEST | TG_REC_STATE | TG_REC_GRID)) != 0;
     const size_t per_state = (flags & TG_REC_GRID) ? (size_t)c.R * c.n : ((flags & TG_REC_STATE) ? (size_t)c.n : 0);
-    SwapArgs sa = swap_args(c);
-    const int sps = (int)c.cfg.sweeps_per_swap;
     if (c.profiling && (int)c.ev.size() < 2 * c.rec_cap + 1) {
+        c.clear_graphs();  // graphs record the events they were captured with
         for (auto e : c.ev) cudaEventDestroy(e);
         c.ev.assign(2 * c.rec_cap + 1, nullptr);
         for (auto& e : c.ev) CK(cudaEventCreate(&e));
     }
-    double sweep_ms = 0, swap_ms = 0;
-    int filled = 0;
-    int64_t first_round = c.rounds_done + 1;
-    for (int64_t k = 0; k < n_rounds; ++k) {
-        const int64_t round = c.rounds_done + 1;
-        if (c.profiling) CK(cudaEventRecord(c.ev[2 * filled], st));
-        launch_sweep(c, (round - 1) * sps);
-        if (c.profiling) CK(cudaEventRecord(c.ev[2 * filled + 1], st));
+    if (c.d_rstate.n < 1) c.d_rstate.alloc(1);
+    if (c.d_dig.n < (size_t)c.rec_cap) c.d_dig.alloc(c.rec_cap);
+    // every kernel of a round reads the device round state (round, swap-stream
+    // position, record slot); round_tick_kernel advances it, so the launch
+    // sequence of a chunk is the same every time and is replayed as a graph
+    SwapArgs sa = swap_args(c);
+    sa.rs = c.d_rstate.p;
+    ExtractArgs e{};
+    if (need_extract) {
+        e.n = c.n;
+        e.R = c.R;
+        e.W = c.W;
+        e.plane = c.engine == TG_ENGINE_PLANE;
+        e.all_slots = (flags & TG_REC_GRID) ? 1 : 0;
+        e.local_states = c.R_local;
+        e.state0 = c.state0;
+        e.slot_state = c.d_slot_state.p;
+        e.spins32 = c.d_spins32.p;
+        e.spins8 = c.d_spins8.p;
+        e.perm = c.d_perm.p;
+        e.states = per_state ? c.d_rec_states.p : nullptr;
+        e.digest = (flags & TG_REC_DIGEST) ? c.d_dig.p : nullptr;
+        e.rs = c.d_rstate.p;
+        e.per_state = per_state;
+    }
+    const long long ex_total = (long long)(e.all_slots ? c.R : 1) * c.n;
+    const int ex_blocks = std::max(1, (int)std::min<long long>((ex_total + 255) / 256, (long long)c.sms * 8));
+    NvtxRange nv_("tg: unfused rounds");
+    auto one_round = [&](int k, bool capturing) {
+        if (c.profiling)
+            CK(capturing ? cudaEventRecordWithFlags(c.ev[2 * k], st, cudaEventRecordExternal)
+                         : cudaEventRecord(c.ev[2 * k], st));
+        launch_sweep(c, 0, c.d_rstate.p);
+        if (c.profiling)
+            CK(capturing ? cudaEventRecordWithFlags(c.ev[2 * k + 1], st, cudaEventRecordExternal)
+                         : cudaEventRecord(c.ev[2 * k + 1], st));
         if (c.world > 1) {
+            NvtxRange nx_("tg: (f, g) all-gather");
             NK(nccl().GroupStart());
             NK(nccl().AllGather(c.d_f.p + c.state0, c.d_f.p, c.R_local, ncclDouble, c.comm, st));
             NK(nccl().AllGather(c.d_g.p + c.state0, c.d_g.p, c.R_local, ncclDouble, c.comm, st));
             NK(nccl().GroupEnd());
         }
-        swap_kernel<<<1, kSwapThreads, 0, st>>>(sa, round, c.swap_base, filled, flags);
+        swap_kernel<<<1, kSwapThreads, 0, st>>>(sa, 0, 0, 0, flags);
         CK(cudaGetLastError());
-        c.other_launches++;
         if (need_extract) {
-            ExtractArgs e{};
-            e.n = c.n;
-            e.R = c.R;
-            e.W = c.W;
-            e.plane = c.engine == TG_ENGINE_PLANE;
-            e.all_slots = (flags & TG_REC_GRID) ? 1 : 0;
-            e.local_states = c.R_local;
-            e.state0 = c.state0;
-            e.slot_state = c.d_slot_state.p;
-            e.spins32 = c.d_spins32.p;
-            e.spins8 = c.d_spins8.p;
-            e.perm = c.d_perm.p;
-            e.states = per_state ? c.d_rec_states.p + (size_t)filled * per_state : nullptr;
-            uint64_t* dg = (flags & TG_REC_DIGEST) ? &c.d_rec.p[filled].digest : nullptr;
-            e.digest = dg;
-            const long long total = (long long)(e.all_slots ? c.R : 1) * c.n;
-            const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)c.sms * 8);
-            extract_kernel<<<std::max(blocks, 1), 256, 0, st>>>(e);
+            extract_kernel<<<ex_blocks, 256, 0, st>>>(e);
             CK(cudaGetLastError());
-            c.other_launches++;
-            if (c.world > 1) {
-                if (dg) NK(nccl().AllReduce(dg, dg, 1, ncclUint64, ncclSum, c.comm, st));
-                if (e.states) NK(nccl().AllReduce(e.states, e.states, per_state, ncclInt8, ncclSum, c.comm, st));
+        }
+        round_tick_kernel<<<1, 32, 0, st>>>(c.d_rstate.p, c.I, c.J);
+        CK(cudaGetLastError());
+    };
+    const int per_round_other = 2 + (need_extract ? 1 : 0);
+    // a graph of n rounds (captured once per chunk length); none if capture fails
+    auto graph_for = [&](int n) -> cudaGraphExec_t {
+        if (!c.graphs_ok || std::getenv("TG_NO_GRAPHS")) return nullptr;
+        auto it = c.graphs.find(n);
+        if (it != c.graphs.end()) return it->second;
+        const int64_t sl0 = c.sweep_launches;
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ex = nullptr;
+        bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            try {
+                for (int k = 0; k < n; ++k) one_round(k, true);
+            } catch (const TgFail&) {
+                ok = false;
             }
+            ok = (cudaStreamEndCapture(st, &g) == cudaSuccess) && ok && g != nullptr;
         }
-        c.swap_base += (uint64_t)round_attempts(c.I, c.J, round);
-        c.rounds_done = round;
-        ++filled;
-        if (filled == c.rec_cap) {
-            if (c.profiling) profile_chunk(c, filled, sweep_ms, swap_ms);
-            drain(c, filled, first_round, sink);
-            filled = 0;
-            first_round = c.rounds_done + 1;
+        if (ok) ok = cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();  // a failed capture leaves no sticky error
+        c.sweep_launches = sl0;
+        if (!ok) {
+            c.graphs_ok = false;
+            return nullptr;
         }
+        c.graphs[n] = ex;
+        return ex;
+    };
+    double sweep_ms = 0, swap_ms = 0;
+    int64_t left = n_rounds;
+    while (left > 0) {
+        const int n = (int)std::min<int64_t>(left, c.rec_cap);
+        const int64_t first_round = c.rounds_done + 1;
+        c.h_rstate = RoundState{c.rounds_done, c.swap_base, 0, 0};
+        CK(cudaMemcpyAsync(c.d_rstate.p, &c.h_rstate, sizeof(RoundState), cudaMemcpyHostToDevice, st));
+        if (flags & TG_REC_DIGEST) CK(cudaMemsetAsync(c.d_dig.p, 0, sizeof(uint64_t) * n, st));
+        if (cudaGraphExec_t gx = graph_for(n)) {
+            CK(cudaGraphLaunch(gx, st));
+            c.graph_launches++;
+            c.sweep_launches += n;
+        } else {
+            for (int k = 0; k < n; ++k) one_round(k, false);
+        }
+        c.other_launches += (int64_t)n * per_round_other;
+        for (int k = 0; k < n; ++k) c.swap_base += (uint64_t)round_attempts(c.I, c.J, first_round + k);
+        c.rounds_done += n;
+        left -= n;
+        if (c.world > 1) {
+            // target digests and snapshots: every rank wrote zeros for states it
+            // does not hold, one all-reduce per chunk instead of one per round
+            if (flags & TG_REC_DIGEST) NK(nccl().AllReduce(c.d_dig.p, c.d_dig.p, n, ncclUint64, ncclSum, c.comm, st));
+            if (per_state)
+                NK(nccl().AllReduce(c.d_rec_states.p, c.d_rec_states.p, per_state * n, ncclInt8, ncclSum, c.comm, st));
+        }
+        if (c.profiling) profile_chunk(c, n, sweep_ms, swap_ms);
+        NvtxRange nr_("tg: drain records");
+        drain(c, n, first_round, sink, (flags & TG_REC_DIGEST) != 0);
     }
-    if (c.profiling && filled) profile_chunk(c, filled, sweep_ms, swap_ms);
-    drain(c, filled, first_round, sink);
     CK(cudaStreamSynchronize(st));
     c.last_sweep_ms = sweep_ms;
     c.last_swap_ms = swap_ms;

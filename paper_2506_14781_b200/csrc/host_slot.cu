@@ -738,6 +738,7 @@ void s2_drain(tg_ctx& c, int filled, int64_t first_round, const BatchSinkCtx& si
 }
 
 void s2_advance(tg_ctx& c, int64_t n_rounds, const BatchSinkCtx& sink) {
+    NvtxRange nv_("tg: slot/float rounds");
     HostTimer tm_("batch: s2_advance");
     Slot2& S = c.s2;
     if (!S.ready) fail(TG_ERR_CONFIG, "advance: batch not initialised");

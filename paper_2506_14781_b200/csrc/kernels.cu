@@ -139,6 +139,7 @@ __device__ __forceinline__ void slot_update_fast(const SlotArgs& a, int8_t* s, i
 
 __global__ void __launch_bounds__(kSlotThreads)
 slot_sweep_kernel(SlotArgs a, int64_t t0, int n_sweeps) {
+    if (a.rs) t0 = a.rs->round * n_sweeps;
     extern __shared__ int8_t sm[];
     const int m = blockIdx.x;  // local state
     const int n = a.n;
@@ -253,6 +254,7 @@ __device__ __forceinline__ void slot_update_d(const SlotArgs& a, int8_t* s, int 
 template <int D>
 __global__ void __launch_bounds__(kSlotThreads)
 slot_sweep_kernel_d(SlotArgs a, int64_t t0, int n_sweeps) {
+    if (a.rs) t0 = a.rs->round * n_sweeps;
     extern __shared__ int8_t sm[];
     const int m = blockIdx.x;
     const int n = a.n;
@@ -342,6 +344,11 @@ void* slot_sweep_fn_d(int D) {
 __global__ void __launch_bounds__(kSwapThreads) swap_kernel(SwapArgs a, int64_t round,
                                                             uint64_t swap_base, int rec_idx,
                                                             int rec_flags) {
+    if (a.rs) {
+        round = a.rs->round + 1;
+        swap_base = a.rs->swap_base;
+        rec_idx = a.rs->filled;
+    }
     const int64_t n_att = round_attempts(a.I, a.J, round);
     for (int k = threadIdx.x; k < n_att; k += blockDim.x) {
         int sa, sb, ctr, is_p;
@@ -414,7 +421,22 @@ __global__ void __launch_bounds__(kSwapThreads) swap_kernel(SwapArgs a, int64_t 
 
 // -------------------------------------------------------- extract kernel
 
+// Advance the device round counters after a round of the unfused loop.
+__global__ void round_tick_kernel(RoundState* rs, int I, int J) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const int64_t round = rs->round + 1;
+        rs->swap_base += (uint64_t)round_attempts(I, J, round);
+        rs->round = round;
+        rs->filled += 1;
+    }
+}
+
 __global__ void extract_kernel(ExtractArgs e) {
+    if (e.rs) {  // this round's slot of the chunk's state ring and digest array
+        const int k = e.rs->filled;
+        if (e.states) e.states += (size_t)k * e.per_state;
+        if (e.digest) e.digest += k;
+    }
     const int tgt_slot_count = e.all_slots ? e.R : 1;
     const long long total = (long long)tgt_slot_count * e.n;
     uint64_t dsum = 0;

@@ -68,7 +68,11 @@ struct ExtractArgs {
     const int32_t* perm;  // internal -> caller index
     int8_t* states;       // [1 or R][n] caller order, or null
     uint64_t* digest;     // record digest slot, or null
+    // unfused loop: the chunk's state ring / digest array, indexed by rs->filled
+    const RoundState* rs;
+    size_t per_state;
 };
+__global__ void round_tick_kernel(RoundState* rs, int I, int J);
 
 void* plane_sweep_fn(int rule, int wv);
 void* plane_rounds_fn(int rule, int wv, int fast);

@@ -464,6 +464,7 @@ __device__ __forceinline__ void plane_phase_pf(const PlaneArgs& a, int c, uint64
 template <int RULE, int WV>
 __global__ void __launch_bounds__(kPlaneThreads, 1)
 plane_sweep_kernel(const __grid_constant__ PlaneArgs a, int64_t t0, int n_sweeps) {
+    if (a.rs) t0 = a.rs->round * n_sweeps;
     cg::grid_group grid = cg::this_grid();
     const int wpb = blockDim.x >> 5;
     // each block owns one pass of WV words (block-uniform Philox keys); the

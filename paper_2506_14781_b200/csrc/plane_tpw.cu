@@ -821,6 +821,7 @@ plane_tpw_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_consta
 template <int RULE, int FAST>
 __global__ void __launch_bounds__(kTpwThreads, kTpwMinBlocks)
 plane_tpw_sweep_kernel(const __grid_constant__ PlaneArgs a, int64_t t0, int n_sweeps) {
+    if (a.rs) t0 = a.rs->round * n_sweeps;
     cg::grid_group grid = cg::this_grid();
     const int nrep = a.W * 32;
     int* s_cc = tpw_sm + kTpwSmCnt;

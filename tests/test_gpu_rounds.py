@@ -1,0 +1,79 @@
+"""The unfused round loop (full-grid records on one GPU; every multi-GPU run)
+keeps its round counters on the device and replays each chunk of rounds as a
+captured CUDA graph.  It must give the oracle's trajectories, and the same
+records with graphs disabled (TG_NO_GRAPHS=1, direct launches), including
+across record-ring drains (chunks) and for the slot engine's multi-GPU
+kernel path (TG_SLOT_V1)."""
+import numpy as np
+import pytest
+
+import pyoracle as O
+from paper_2506_14781_b200 import instances as I
+from paper_2506_14781_b200.api import Engine, RunConfig
+
+pytestmark = pytest.mark.gpu
+
+
+def unfused(pr, b, p, rounds, rule, seed, engine, grid=True):
+    eng = Engine(0)
+    eng.set_problem(pr)
+    eng.set_schedule(b, p)
+    recs, states = [], []
+    R = len(b) * len(p)
+
+    def sink(r, n, st, ap, ab):
+        for k in range(n):
+            recs.append((r[k].round, r[k].f, r[k].g, r[k].digest, r[k].target_state))
+        if st:
+            per = R * pr.n if grid else pr.n
+            states.append(np.ctypeslib.as_array(st, shape=(n * per,)).copy())
+        return 0
+
+    eng.run(RunConfig(total_sweeps=rounds, sweeps_per_swap=1, seed=seed, rule=rule, engine=engine,
+                      store_states=not grid, store_target_only=not grid, digest=True), sink)
+    fin = eng.grid()
+    kern = eng.info()["sweep_kernel"]
+    eng.close()
+    return recs, np.concatenate(states) if states else None, fin, kern
+
+
+@pytest.mark.parametrize("rule", ["metropolis", "heat_bath"])
+def test_graph_rounds_match_oracle_and_direct_launches(monkeypatch, rule):
+    pr = I.bipartite_3regular(512, seed=3)
+    b, p = I.config_schedule("c5")
+    o = O.run(pr, b, p, 30, 1, seed=4, rule=rule, rng="plane")
+    g = unfused(pr, b, p, 30, rule, 4, "plane")
+    assert g[3] == "plane_tpw_sweep_kernel"
+    np.testing.assert_array_equal([r[1] for r in g[0]], o.f)
+    np.testing.assert_array_equal(np.array([r[3] for r in g[0]], dtype=np.uint64), o.digest)
+    np.testing.assert_array_equal(g[2], o.final_grid)
+    monkeypatch.setenv("TG_NO_GRAPHS", "1")
+    d = unfused(pr, b, p, 30, rule, 4, "plane")
+    assert g[0] == d[0]
+    np.testing.assert_array_equal(g[1], d[1])
+    np.testing.assert_array_equal(g[2], d[2])
+
+
+def test_graph_rounds_across_ring_drains():
+    # full-grid records of 16 x 16 x 512 int8 = 128 KB per round: the ring holds
+    # 1024 rounds, so 1100 rounds span two chunks (two graph lengths)
+    pr = I.bipartite_3regular(512, seed=5)
+    b, p = I.config_schedule("c5")
+    o = O.run(pr, b, p, 1100, 1, seed=9, rng="plane", final_grid=True)
+    g = unfused(pr, b, p, 1100, "metropolis", 9, "plane")
+    assert len(g[0]) == 1100
+    np.testing.assert_array_equal([r[1] for r in g[0]], o.f)
+    np.testing.assert_array_equal(np.array([r[3] for r in g[0]], dtype=np.uint64), o.digest)
+    np.testing.assert_array_equal(g[2], o.final_grid)
+
+
+def test_graph_rounds_slot_v1_kernels(monkeypatch):
+    monkeypatch.setenv("TG_SLOT_V1", "1")
+    pr = I.k10_pm1(1)
+    b, p = I.config_schedule("c1")
+    o = O.run(pr, b, p, 60, 1, seed=2, rng="slot")
+    g = unfused(pr, b, p, 60, "metropolis", 2, "slot", grid=False)
+    assert g[3].startswith("slot_sweep_kernel")
+    np.testing.assert_array_equal([r[1] for r in g[0]], o.f)
+    np.testing.assert_array_equal(np.array([r[3] for r in g[0]], dtype=np.uint64), o.digest)
+    np.testing.assert_array_equal(g[2], o.final_grid)
