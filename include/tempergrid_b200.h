@@ -128,6 +128,29 @@ int tg_get_counters(tg_ctx* ctx, int64_t* attempts_p, int64_t* accepts_p, int64_
 /* Per-slot f and g after the last completed round. */
 int tg_get_energies(tg_ctx* ctx, double* f, double* g);
 
+/* ---- Checkpoint / resume (single-GPU contexts, not batches) ----
+ * The reference keeps a run only in RAM (engine.hpp:39-56, engine.cpp:119,214)
+ * and has no resume; a checkpoint here is everything a run's continuation
+ * depends on: every physical state's spins (caller order), the slot labels,
+ * the cumulative accept counters, the round counter and the swap-stream
+ * position.  The Philox draws are pure functions of (seed, counters), so no
+ * RNG state is saved.  tg_restore needs a context initialised (tg_init) with
+ * the same problem, schedule and config; the resumed run then continues bit
+ * for bit as if it had never stopped.  Layout: tg_checkpoint_header, int8
+ * states [R][n], int32 slot_state [R], int64 accepts_p [I(J-1)], int64
+ * accepts_b [(I-1)J]. */
+typedef struct {
+    uint32_t magic;        /* 'TGCP' */
+    uint32_t version;      /* 1 */
+    int32_t engine, rule, n, I, J, pad;
+    int64_t rounds_done;
+    uint64_t swap_base;    /* swap-stream draws consumed */
+    uint64_t seed;
+} tg_checkpoint_header;
+int tg_checkpoint_size(tg_ctx* ctx, size_t* bytes);
+int tg_checkpoint(tg_ctx* ctx, void* buf, size_t bytes);
+int tg_restore(tg_ctx* ctx, const void* buf, size_t bytes);
+
 typedef struct {
     int32_t engine;        /* engine actually selected */
     int32_t n_colors;      /* colour classes of the canonical order */

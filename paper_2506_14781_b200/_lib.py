@@ -84,6 +84,9 @@ def lib() -> C.CDLL:
     L.tg_destroy.restype = None
     L.tg_last_error.argtypes = [vp, C.c_char_p, C.c_size_t]
     L.tg_last_error.restype = C.c_size_t
+    L.tg_checkpoint_size.argtypes = [vp, C.POINTER(C.c_size_t)]
+    L.tg_checkpoint.argtypes = [vp, C.c_void_p, C.c_size_t]
+    L.tg_restore.argtypes = [vp, C.c_void_p, C.c_size_t]
     L.tg_set_problem.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int, vp, vp]
     L.tg_set_schedule.argtypes = [vp, C.c_int, vp, C.c_int, vp]
     L.tg_run.argtypes = [vp, C.POINTER(RunConfigC), SINK, C.c_void_p]
@@ -131,5 +134,5 @@ EXPORTED = [
     "tg_general_swap_probability", "tg_swap_phase_host", "tg_partition", "tg_batch_clear",
     "tg_batch_add", "tg_batch_run", "tg_batch_get_state", "tg_batch_get_counters",
     "tg_batch_init", "tg_batch_advance", "tg_run_jcolumn", "tg_probe_population", "tg_build_schedule", "tg_set_kl_decoder",
-    "tg_clear_kl_decoder", "tg_get_kl_curve",
+    "tg_clear_kl_decoder", "tg_get_kl_curve", "tg_checkpoint_size", "tg_checkpoint", "tg_restore",
 ]

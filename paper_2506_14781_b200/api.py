@@ -287,6 +287,22 @@ class Engine:
                         (k - 1) / (2.0 * smp[r]) if smp[r] > 0 else float("nan"))
                 for r in range(rounds)]
 
+    def checkpoint(self) -> bytes:
+        """Snapshot of the run (``tg_checkpoint``): spins of every physical
+        state, slot labels, accept counters, round counter, swap-stream
+        position.  The reference has no resume (engine.hpp:39-56)."""
+        n = C.c_size_t()
+        self._check(self._L.tg_checkpoint_size(self._h, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        self._check(self._L.tg_checkpoint(self._h, buf, n.value))
+        return buf.raw
+
+    def restore(self, blob: bytes):
+        """Continue from a checkpoint (``tg_restore``) on a context initialised
+        with the same problem, schedule and config."""
+        buf = C.create_string_buffer(bytes(blob), len(blob))
+        self._check(self._L.tg_restore(self._h, buf, len(blob)))
+
     def set_profiling(self, on: bool):
         self._check(self._L.tg_set_profiling(self._h, 1 if on else 0))
 

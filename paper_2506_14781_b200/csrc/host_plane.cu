@@ -360,11 +360,11 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
         const int fb = kernel_fit(fn, 0, c.tpw_sweep_smem).blocks_per_sm;
         if (fb >= 1) c.tpw_sweep_grid = fb * c.sms;
     }
-    // config-5 kernel (plane_c5.cu): Metropolis on the tpw config-5 path with
+    // config-5 kernel (plane_c5.cu): either rule on the tpw config-5 path with
     // a 2-colouring, at least two words per site row; TG_PLANE_C5=0 disables
     c.fused_c5 = 0;
     {
-        bool ok = c.fused_tpw && c.tpw_fast && c.cfg.rule == TG_RULE_METROPOLIS && c.n_colors == 2 &&
+        bool ok = c.fused_tpw && c.tpw_fast && c.n_colors == 2 &&
                   c.W >= 2 && c.n_types <= 2 && c.d_nbr4.p != nullptr;
         int nfree_type = 0;
         for (const auto& t : types) nfree_type += t.dq == 0;
@@ -372,7 +372,7 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
         if (const char* e = std::getenv("TG_PLANE_C5")) ok = ok && std::atoi(e) != 0;
         if (ok) {
             const size_t smem = c5_smem_bytes(c.R, c.W);
-            const int fb = kernel_fit(plane_c5_fn(), kC5Threads, smem).blocks_per_sm;
+            const int fb = kernel_fit(plane_c5_fn(c.cfg.rule), kC5Threads, smem).blocks_per_sm;
             if (fb >= 1) {
                 c.fused_c5 = 1;
                 c.fused_grid = fb * c.sms;
@@ -507,7 +507,7 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         if (c.profiling) CK(cudaEventRecord(c.ev[0], st));
         c.sweep_kernel = c.fused_c5 ? "plane_c5_rounds_kernel"
                                     : c.fused_tpw ? "plane_tpw_rounds_kernel" : "plane_rounds_kernel";
-        const void* fn = c.fused_c5 ? plane_c5_fn()
+        const void* fn = c.fused_c5 ? plane_c5_fn(c.cfg.rule)
                                     : c.fused_tpw ? plane_tpw_fn(c.cfg.rule, c.tpw_fast)
                                                   : plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast);
         CK(cudaLaunchCooperativeKernel(fn, dim3(c.fused_grid), dim3(c.fused_block), args, c.fused_smem, st));

@@ -36,16 +36,23 @@ inline size_t tpw_smem_bytes(int R, int W, int threads) {
 }
 // config-5 fused round kernel (plane_c5.cu): threads per CTA, per-warp tail
 // queue entries (>= 31 + 2 words x 32 lanes), dynamic shared memory = queues
-// [warps][kC5QCap] int4, staged thresholds [32 words][16], per-replica
+// [warps][kC5QCap] int4, staged thresholds [32 words][36], per-replica
 // counters [2][32W], labels and energies.
-constexpr int kC5Threads = 512;
+#ifndef TG_C5_THREADS
+#define TG_C5_THREADS 512
+#endif
+#ifndef TG_C5_MINB
+#define TG_C5_MINB 1
+#endif
+constexpr int kC5Threads = TG_C5_THREADS;
+constexpr int kC5MinBlocks = TG_C5_MINB;
 constexpr int kC5QCap = 96;
 inline size_t c5_smem_bytes(int R, int W) {
-    return (size_t)(kC5Threads / 32) * kC5QCap * 16 + (size_t)kMaxWordsArg * 16 * sizeof(int) +
+    return (size_t)(kC5Threads / 32) * kC5QCap * 16 + (size_t)kMaxWordsArg * 36 * sizeof(int) +
            (size_t)2 * W * 32 * sizeof(int) +
            (size_t)R * (2 * sizeof(double) + 2 * sizeof(int32_t)) + 8;
 }
-void* plane_c5_fn();
+void* plane_c5_fn(int rule);
 constexpr int kSlotThreads = 256;
 constexpr int kSwapThreads = 1024;
 

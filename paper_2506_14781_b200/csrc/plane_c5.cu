@@ -2,6 +2,7 @@
 // (Metropolis): two 32-replica words per thread, chain-free and chain sites
 // in separate item loops.
 //
+// Both update rules (Metropolis; heat bath, the north star's p-bit rule).
 // Same contract, and therefore the same trajectories bit for bit, as
 // plane_tpw_rounds_kernel / plane_rounds_kernel: the reference sweep
 // (mc.cpp:21-35) over the canonical colour order, thresholds
@@ -38,9 +39,6 @@ namespace cg = cooperative_groups;
 namespace tg {
 
 constexpr int kC5VB = 8;  // vertical counter planes (<= 255 per lane between flushes)
-#ifndef TG_C5_THR_SMEM
-#define TG_C5_THR_SMEM 1  // class-2/3 thresholds from shared memory (0: registers)
-#endif
 
 extern __shared__ __align__(16) int c5_sm[];
 
@@ -49,9 +47,11 @@ extern __shared__ __align__(16) int c5_sm[];
 __device__ __forceinline__ int4* c5_queue(int warp) {
     return reinterpret_cast<int4*>(c5_sm) + warp * kC5QCap;
 }
-__device__ __forceinline__ int* c5_cnt() { return c5_sm + (kC5Threads / 32) * kC5QCap * 4 + kMaxWordsArg * 16; }
-// class-2/3 threshold planes 0-7 of every word, [W][4] uint4 (k2 planes 0-3,
-// 4-7, k3 planes 0-3, 4-7), staged per round after the counters [2][32W]
+__device__ __forceinline__ int* c5_cnt() { return c5_sm + (kC5Threads / 32) * kC5QCap * 4 + kMaxWordsArg * 36; }
+// threshold planes staged per round for the chain-free type: Metropolis,
+// class-2/3 planes 0-7 of every word, [W][4] uint4 (k2 planes 0-3, 4-7, k3
+// planes 0-3, 4-7); heat bath, planes 0-7 and the "always" word of its 4
+// classes, [W][9] uint4 (x..w = classes 0..3)
 __device__ __forceinline__ uint4* c5_thr() { return reinterpret_cast<uint4*>(c5_sm + (kC5Threads / 32) * kC5QCap * 4); }
 
 // V += m (2-bit bit-sliced value) in kC5VB-bit vertical arithmetic.
@@ -135,10 +135,14 @@ __device__ __forceinline__ void c5_flush(uint32_t (&V)[kC5VB], int logWP, int j,
 }
 
 // Resolve queue entries [base, base + n) (n <= 32) of the calling warp, one
-// per lane: Philox blocks 2.. of the entry's (site, word), class-2/3 planes
-// 8.. of its word (kpc), late flips XORed into the stored word (same warp,
-// after __syncwarp) and, when counting, the unsatisfied-bond correction of a
-// late flip: 2c - 3 = 1 + 2 c0 (undecided lanes have c = 2 + c0).
+// per lane: Philox blocks 2.. of the entry's (site, word), threshold planes
+// 8.. of its word, late decisions applied to the stored word (same warp, after
+// __syncwarp) and, when counting, the unsatisfied-bond correction.
+// Metropolis: undecided lanes are class 2 | 3 (c = 2 + c0), planes from kpc,
+// a late flip changes the lane's unsatisfied bonds by 2c - 3 = 1 + 2 c0.
+// Heat bath: 4 classes (c = c0 + 2 c1 +1 contributions), planes from kp, a
+// late +1 (provisionally -1) changes them by 3 - 2c.
+template <int RULE>
 __device__ __noinline__ void c5_drain(const PlaneArgs& a, int base, int n, uint32_t tlo, uint32_t thi,
                                       int t30, bool count, int* s_cc) {
     const int lane = threadIdx.x & 31;
@@ -146,28 +150,45 @@ __device__ __noinline__ void c5_drain(const PlaneArgs& a, int base, int n, uint3
     const bool mine = lane < n;
     int4 e = make_int4(0, 0, 0, 0);
     if (mine) e = c5_queue(threadIdx.x >> 5)[base + lane];
-    const uint32_t site = (uint32_t)e.x;
-    const int w = e.y;
-    uint32_t und = (uint32_t)e.z;
-    const uint32_t c0 = (uint32_t)e.w;
+    const uint32_t site = (uint32_t)e.x & 0x07ffffffu;
+    const int w = (int)((uint32_t)e.x >> 27);
+    uint32_t und = (uint32_t)e.y;
+    const uint32_t c0 = (uint32_t)e.z, c1 = (uint32_t)e.w;
     const uint32_t grp4 = (uint32_t)(a.w_global0 + w) << 4;
     const uint4* kc2 = reinterpret_cast<const uint4*>(a.kpc + ((size_t)w * a.n_types + t30) * 128);
+    const uint4* kh = reinterpret_cast<const uint4*>(a.kp + (size_t)w * a.kpw + a.ty[t30].kp_off);
     uint32_t lt = 0u;
     const PhiloxT P = philox_t(tlo, thi, a.pks);
 #pragma unroll 1
     for (int blk = 2; blk < 14; ++blk) {
         if (!__any_sync(0xffffffffu, und)) break;
         const u32x4 r = philox_plane(site, grp4 | (uint32_t)blk, P, a.pks);
-        compare4_sel(c0, __ldg(kc2 + blk), __ldg(kc2 + 16 + blk), r, und, lt);
+        if (RULE == 0) {
+            compare4_sel(c0, __ldg(kc2 + blk), __ldg(kc2 + 16 + blk), r, und, lt);
+        } else {
+            const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int b = blk * 4 + q;
+                if (b < kKPlanes) {
+                    const uint4 T = __ldg(kh + b);  // the 4 classes of plane b
+                    const uint32_t tb = sel(c1, sel(c0, T.w, T.z), sel(c0, T.y, T.x));
+                    lt |= und & tb & ~rr[q];
+                    und &= ~(tb ^ rr[q]);
+                }
+            }
+        }
     }
     if (lt) {
-        a.spins[(size_t)site * a.W + w] ^= lt;
+        if (RULE == 0) a.spins[(size_t)site * a.W + w] ^= lt;
+        else a.spins[(size_t)site * a.W + w] |= lt;
         if (count) {
             uint32_t ex = lt;
             while (ex) {
                 const int l = __ffs(ex) - 1;
                 ex &= ex - 1;
-                atomicAdd(s_cc + w * 32 + l, 1 + 2 * (int)((c0 >> l) & 1u));
+                const int cl = (int)((c0 >> l) & 1u) + 2 * (int)((c1 >> l) & 1u);
+                atomicAdd(s_cc + w * 32 + l, RULE == 0 ? 1 + 2 * (int)((c0 >> l) & 1u) : 3 - 2 * cl);
             }
         }
     }
@@ -176,7 +197,6 @@ __device__ __noinline__ void c5_drain(const PlaneArgs& a, int base, int n, uint3
 
 // Per-thread constants of a colour phase.
 struct C5Ctx {
-    uint4 k2a[2], k2b[2], k3a[2], k3b[2];  // planes 0-7 of classes 2, 3 of the two words
     uint32_t act[2];
     uint32_t g[4];                         // Philox word 3 of the 4 unconditional blocks
     uint32_t tlo, thi;
@@ -184,6 +204,7 @@ struct C5Ctx {
 };
 
 // One colour phase: chain-free items, then chain items.
+template <int RULE>
 __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, bool count, int gw,
                                          int nw, int logW, uint32_t (&V0)[kC5VB], uint32_t (&V1)[kC5VB],
                                          int t30, int t31, int nfree) {
@@ -199,15 +220,8 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
     const int cf = cs + nfree;               // first chain site of the colour
     count = count && c == 1;
     C5Ctx K;
-#if !TG_C5_THR_SMEM
-    {
-        const uint4* kc0 = reinterpret_cast<const uint4*>(a.kpc + ((size_t)w0 * a.n_types + t30) * 128);
-        const uint4* kc1 = reinterpret_cast<const uint4*>(a.kpc + ((size_t)(w0 + 1) * a.n_types + t30) * 128);
-        K.k2a[0] = kc0[0]; K.k2b[0] = kc0[1]; K.k3a[0] = kc0[16]; K.k3b[0] = kc0[17];
-        K.k2a[1] = kc1[0]; K.k2b[1] = kc1[1]; K.k3a[1] = kc1[16]; K.k3b[1] = kc1[17];
-    }
-#endif
-    const uint4* thr = c5_thr() + w0 * 4;  // staged per round: [word][k2a, k2b, k3a, k3b]
+    // staged per round: Metropolis [word][k2a, k2b, k3a, k3b]; heat bath [word][9]
+    const uint4* thr = c5_thr() + w0 * (RULE == 0 ? 4 : 9);
     K.act[0] = a.active[w0];
     K.act[1] = a.active[w0 + 1];
     const uint32_t g0 = (uint32_t)(a.w_global0 + w0) << 4;
@@ -261,33 +275,59 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
             u32x4 r[4];
             philox_planeN<4>(site, K.g, K.P, a.pks, r);
             const uint32_t m0s = (uint32_t)(e.x >> 31), m1s = (uint32_t)(e.y >> 31), m2s = (uint32_t)(e.z >> 31);
-            uint32_t und[2], ns[2], cl0[2];
+            uint32_t und[2], ns[2], cl0[2], cl1[2];
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const uint32_t sj = j ? s.y : s.x;
-                // satisfied bond k: J_ik s_i s_k = +1
-                const uint32_t a0 = ~(sj ^ (j ? x0.y : x0.x) ^ m0s);
-                const uint32_t a1 = ~(sj ^ (j ? x1.y : x1.x) ^ m1s);
-                const uint32_t a2 = ~(sj ^ (j ? x2.y : x2.x) ^ m2s);
+                // Metropolis: satisfied bonds (J_ik s_i s_k = +1); heat bath:
+                // +1 contributions (J_ik s_k = +1)
+                const uint32_t b0 = (j ? x0.y : x0.x) ^ m0s, b1 = (j ? x1.y : x1.x) ^ m1s,
+                               b2 = (j ? x2.y : x2.x) ^ m2s;
+                const uint32_t a0 = RULE == 0 ? ~(sj ^ b0) : b0, a1 = RULE == 0 ? ~(sj ^ b1) : b1,
+                               a2 = RULE == 0 ? ~(sj ^ b2) : b2;
                 const uint32_t c0 = a0 ^ a1 ^ a2;
                 const uint32_t c1 = (a0 & a1) | (a2 & (a0 ^ a1));
                 const uint32_t act = valid ? K.act[j] : 0u;
-                uint32_t u = c1 & act, lt = 0u;   // classes 0, 1 (de < 0): always taken
-#if TG_C5_THR_SMEM
-                compare4_sel(c0, thr[4 * j], thr[4 * j + 2], r[2 * j], u, lt);
-                compare4_sel(c0, thr[4 * j + 1], thr[4 * j + 3], r[2 * j + 1], u, lt);
-#else
-                compare4_sel(c0, K.k2a[j], K.k3a[j], r[2 * j], u, lt);
-                compare4_sel(c0, K.k2b[j], K.k3b[j], r[2 * j + 1], u, lt);
-#endif
-                const uint32_t take = (~c1 & act) | lt;
-                ns[j] = sj ^ take;
+                uint32_t u, lt = 0u, take;
+                if (RULE == 0) {
+                    u = c1 & act;  // classes 0, 1 (de < 0): always taken
+                    compare4_sel(c0, thr[4 * j], thr[4 * j + 2], r[2 * j], u, lt);
+                    compare4_sel(c0, thr[4 * j + 1], thr[4 * j + 3], r[2 * j + 1], u, lt);
+                    take = (~c1 & act) | lt;
+                    ns[j] = sj ^ take;
+                } else {
+                    const uint4* tj = thr + 9 * j;
+                    const uint4 L = tj[8];
+                    const uint32_t always = sel(c1, sel(c0, L.w, L.z), sel(c0, L.y, L.x)) & act;
+                    u = act & ~always;
+                    const uint32_t rr[8] = {r[2 * j].x, r[2 * j].y, r[2 * j].z, r[2 * j].w,
+                                            r[2 * j + 1].x, r[2 * j + 1].y, r[2 * j + 1].z, r[2 * j + 1].w};
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        const uint4 T = tj[b];
+                        const uint32_t tb = sel(c1, sel(c0, T.w, T.z), sel(c0, T.y, T.x));
+                        lt |= u & tb & ~rr[b];
+                        u &= ~(tb ^ rr[b]);
+                    }
+                    take = (always | lt) & act;  // new spin +1 (undecided lanes provisionally -1)
+                    ns[j] = (sj & ~act) | take;
+                }
                 und[j] = u;
-                if (count) {
-                    if (j == 0) c5_vadd<2>(V0, ~(c0 ^ take) & act, ~(c1 ^ take) & act);
-                    else c5_vadd<2>(V1, ~(c0 ^ take) & act, ~(c1 ^ take) & act);
+                if (count) {  // unsatisfied bonds after the update (all neighbours lower)
+                    uint32_t m0, m1;
+                    if (RULE == 0) {
+                        m0 = ~(c0 ^ take) & act;
+                        m1 = ~(c1 ^ take) & act;
+                    } else {
+                        const uint32_t u0 = ns[j] ^ b0, u1 = ns[j] ^ b1, u2 = ns[j] ^ b2;
+                        m0 = (u0 ^ u1 ^ u2) & act;
+                        m1 = ((u0 & u1) | (u2 & (u0 ^ u1))) & act;
+                    }
+                    if (j == 0) c5_vadd<2>(V0, m0, m1);
+                    else c5_vadd<2>(V1, m0, m1);
                 }
                 cl0[j] = c0;
+                cl1[j] = c1;
             }
             if (valid)
                 *reinterpret_cast<uint2*>(const_cast<char*>(base) + (size_t)(site << logW) * 4u) =
@@ -297,22 +337,23 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
             for (int j = 0; j < 2; ++j) {
                 const uint32_t pend = __ballot_sync(0xffffffffu, und[j] != 0u);
                 if (pend) {
-                    if (und[j])
+                    if (und[j])  // {site | word << 27, undecided lanes, class bits}
                         c5_queue(threadIdx.x >> 5)[qn + __popc(pend & ((1u << lane) - 1u))] =
-                            make_int4((int)site, w0 + j, (int)und[j], (int)cl0[j]);
+                            make_int4((int)(site | ((uint32_t)(w0 + j) << 27)), (int)und[j], (int)cl0[j],
+                                      (int)cl1[j]);
                     qn += __popc(pend);
                 }
             }
             if (qn >= 32) {
                 qn -= 32;
-                c5_drain(a, qn, 32, K.tlo, K.thi, t30, count, s_cc);
+                c5_drain<RULE>(a, qn, 32, K.tlo, K.thi, t30, count, s_cc);
             }
         }
     }
     while (qn > 0) {
         const int n = qn < 32 ? qn : 32;
         qn -= n;
-        c5_drain(a, qn, n, K.tlo, K.thi, t30, count, s_cc);
+        c5_drain<RULE>(a, qn, n, K.tlo, K.thi, t30, count, s_cc);
     }
     if (count) {
         c5_flush(V0, logWP, 0, s_cc);
@@ -347,11 +388,12 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const uint32_t sj = j ? s.y : s.x;
-                const uint32_t a0 = ~(sj ^ (j ? x0.y : x0.x) ^ m0s);
-                const uint32_t a1 = ~(sj ^ (j ? x1.y : x1.x) ^ m1s);
-                const uint32_t a2 = ~(sj ^ (j ? x2.y : x2.x) ^ m2s);
+                const uint32_t b0 = (j ? x0.y : x0.x) ^ m0s, b1 = (j ? x1.y : x1.x) ^ m1s,
+                               b2 = (j ? x2.y : x2.x) ^ m2s;
+                const uint32_t a0 = RULE == 0 ? ~(sj ^ b0) : b0, a1 = RULE == 0 ? ~(sj ^ b1) : b1,
+                               a2 = RULE == 0 ? ~(sj ^ b2) : b2;
                 const uint32_t yj = j ? y.y : y.x;
-                const uint32_t cb[3] = {a0 ^ a1 ^ a2, (a0 & a1) | (a2 & (a0 ^ a1)), ~(sj ^ yj)};
+                const uint32_t cb[3] = {a0 ^ a1 ^ a2, (a0 & a1) | (a2 & (a0 ^ a1)), RULE == 0 ? ~(sj ^ yj) : yj};
                 const uint32_t act = valid ? K.act[j] : 0u;
                 const uint32_t* kpb = j ? kpb1 : kpb0;
                 const uint32_t always = mux_tree<3>(cb, kpb + kKPlanes * 8) & act;
@@ -365,14 +407,23 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
                     compare_block<3>(cb, kpb, 8, blk, rb, u, lt);
                 }
                 const uint32_t take = (always | lt) & act;
-                ns[j] = sj ^ take;
+                ns[j] = RULE == 0 ? sj ^ take : (sj & ~act) | take;
                 if (count) {
                     const uint32_t mq = (ns[j] ^ yj) & act;  // chain bond unsatisfied after the update
+                    uint32_t m0, m1;
+                    if (RULE == 0) {
+                        m0 = ~(cb[0] ^ take) & act;
+                        m1 = ~(cb[1] ^ take) & act;
+                    } else {
+                        const uint32_t u0 = ns[j] ^ b0, u1 = ns[j] ^ b1, u2 = ns[j] ^ b2;
+                        m0 = (u0 ^ u1 ^ u2) & act;
+                        m1 = ((u0 & u1) | (u2 & (u0 ^ u1))) & act;
+                    }
                     if (j == 0) {
-                        c5_vadd<2>(V0, ~(cb[0] ^ take) & act, ~(cb[1] ^ take) & act);
+                        c5_vadd<2>(V0, m0, m1);
                         c5_vadd<1>(Q0, mq, 0u);
                     } else {
-                        c5_vadd<2>(V1, ~(cb[0] ^ take) & act, ~(cb[1] ^ take) & act);
+                        c5_vadd<2>(V1, m0, m1);
                         c5_vadd<1>(Q1, mq, 0u);
                     }
                 }
@@ -393,7 +444,8 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
 // Persistent single-GPU kernel: n_rounds whole rounds of run_2dpt
 // (engine.cpp:121-216); one grid barrier per colour phase, the round epilogue
 // (plane_round.cuh) closes each round.
-__global__ void __launch_bounds__(kC5Threads, 1)
+template <int RULE>
+__global__ void __launch_bounds__(kC5Threads, kC5MinBlocks)
 plane_c5_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__ RoundArgs r) {
     cg::grid_group grid = cg::this_grid();
     const int nrep = a.W * 32;
@@ -421,12 +473,20 @@ plane_c5_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
         const int par = (int)(round & 1);
         int32_t* cc = r.cnt + (size_t)par * 2 * r.cnt_stride;
         int32_t* cq = cc + r.cnt_stride;
-        {   // this round's class-2/3 planes 0-7 (the epilogue's grid barrier precedes)
+        {   // this round's thresholds of the chain-free type (the epilogue's grid barrier precedes)
             uint4* th = c5_thr();
-            for (int q = threadIdx.x; q < 4 * a.W; q += blockDim.x) {
-                const int w = q >> 2, part = q & 3;
-                th[q] = reinterpret_cast<const uint4*>(a.kpc + ((size_t)w * a.n_types + t30) * 128)
-                    [(part & 1) + 16 * (part >> 1)];
+            if (RULE == 0) {  // class-2/3 planes 0-7
+                for (int q = threadIdx.x; q < 4 * a.W; q += blockDim.x) {
+                    const int w = q >> 2, part = q & 3;
+                    th[q] = reinterpret_cast<const uint4*>(a.kpc + ((size_t)w * a.n_types + t30) * 128)
+                        [(part & 1) + 16 * (part >> 1)];
+                }
+            } else {          // 4 classes: planes 0-7 and "always"
+                const int kp0 = a.ty[t30].kp_off;
+                for (int q = threadIdx.x; q < 9 * a.W; q += blockDim.x) {
+                    const int w = q / 9, b = q % 9;
+                    th[q] = *reinterpret_cast<const uint4*>(a.kp + (size_t)w * a.kpw + kp0 + (b < 8 ? b : kKPlanes) * 4);
+                }
             }
             __syncthreads();
         }
@@ -434,7 +494,7 @@ plane_c5_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
             const uint64_t t = (uint64_t)((round - 1) * r.sps + sw);
             const bool count = (sw == r.sps - 1);
             for (int c = 0; c < 2; ++c) {
-                c5_phase(a, c, t, count, gw, nw, logW, V0, V1, t30, t31, r.c5_nfree[c]);
+                c5_phase<RULE>(a, c, t, count, gw, nw, logW, V0, V1, t30, t31, r.c5_nfree[c]);
                 if (count && c == 1) {
                     __syncthreads();
                     for (int m = threadIdx.x; m < nrep; m += blockDim.x) {
@@ -450,6 +510,11 @@ plane_c5_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
     }
 }
 
-void* plane_c5_fn() { return (void*)plane_c5_rounds_kernel; }
+template __global__ void plane_c5_rounds_kernel<0>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
+template __global__ void plane_c5_rounds_kernel<1>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
+
+void* plane_c5_fn(int rule) {
+    return rule ? (void*)plane_c5_rounds_kernel<1> : (void*)plane_c5_rounds_kernel<0>;
+}
 
 }  // namespace tg

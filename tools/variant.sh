@@ -9,6 +9,6 @@ for r in 0 1; do $NV -DTG_PLANE_RULE=$r $2 -c csrc/plane_tpw.cu -o build/tpw_r${
 $NV $2 -c csrc/plane_c5.cu -o build/plane_c5_$1.o &
 $NV $2 -c csrc/host_plane.cu -o build/host_plane_$1.o &
 wait
-objs="build/kernels.o build/capi.o build/host_common.o build/host_slot.o build/host_run.o build/host_extras.o build/plane_r0.o build/plane_r1.o build/slot_engine.o build/slot_fast.o build/prep.o"
+objs="build/kernels.o build/capi.o build/host_common.o build/host_slot.o build/host_run.o build/host_extras.o build/host_ckpt.o build/plane_r0.o build/plane_r1.o build/slot_engine.o build/slot_fast.o build/prep.o"
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o libtempergrid_b200_$1.so $objs build/tpw_r0_$1.o build/tpw_r1_$1.o build/plane_c5_$1.o build/host_plane_$1.o -ldl
 echo libtempergrid_b200_$1.so
