@@ -49,9 +49,10 @@ __device__ __forceinline__ int4* c5_queue(int warp) {
 }
 __device__ __forceinline__ int* c5_cnt() { return c5_sm + (kC5Threads / 32) * kC5QCap * 4 + kMaxWordsArg * 36; }
 // threshold planes staged per round for the chain-free type: Metropolis,
-// class-2/3 planes 0-7 of every word, [W][4] uint4 (k2 planes 0-3, 4-7, k3
+// class-2/3 planes 0-7 of every word, [4][W] uint4 (k2 planes 0-3, 4-7, k3
 // planes 0-3, 4-7); heat bath, planes 0-7 and the "always" word of its 4
-// classes, [W][9] uint4 (x..w = classes 0..3)
+// classes, [9][W] uint4 (x..w = classes 0..3) -- part-major: the words of one
+// warp's pairs are 32 bytes apart, so an LDS.128 is conflict-free
 __device__ __forceinline__ uint4* c5_thr() { return reinterpret_cast<uint4*>(c5_sm + (kC5Threads / 32) * kC5QCap * 4); }
 
 // V += m (2-bit bit-sliced value) in kC5VB-bit vertical arithmetic.
@@ -220,8 +221,10 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
     const int cf = cs + nfree;               // first chain site of the colour
     count = count && c == 1;
     C5Ctx K;
-    // staged per round: Metropolis [word][k2a, k2b, k3a, k3b]; heat bath [word][9]
-    const uint4* thr = c5_thr() + w0 * (RULE == 0 ? 4 : 9);
+    // staged per round, part-major so the word pairs of a warp hit distinct
+    // banks: Metropolis [k2a, k2b, k3a, k3b][word]; heat bath [9][word]
+    const uint4* thr = c5_thr() + w0;
+    const int W = 1 << logW;
     K.act[0] = a.active[w0];
     K.act[1] = a.active[w0 + 1];
     const uint32_t g0 = (uint32_t)(a.w_global0 + w0) << 4;
@@ -291,20 +294,20 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
                 uint32_t u, lt = 0u, take;
                 if (RULE == 0) {
                     u = c1 & act;  // classes 0, 1 (de < 0): always taken
-                    compare4_sel(c0, thr[4 * j], thr[4 * j + 2], r[2 * j], u, lt);
-                    compare4_sel(c0, thr[4 * j + 1], thr[4 * j + 3], r[2 * j + 1], u, lt);
+                    compare4_sel(c0, thr[j], thr[2 * W + j], r[2 * j], u, lt);
+                    compare4_sel(c0, thr[W + j], thr[3 * W + j], r[2 * j + 1], u, lt);
                     take = (~c1 & act) | lt;
                     ns[j] = sj ^ take;
                 } else {
-                    const uint4* tj = thr + 9 * j;
-                    const uint4 L = tj[8];
+                    const uint4* tj = thr + j;
+                    const uint4 L = tj[8 * W];
                     const uint32_t always = sel(c1, sel(c0, L.w, L.z), sel(c0, L.y, L.x)) & act;
                     u = act & ~always;
                     const uint32_t rr[8] = {r[2 * j].x, r[2 * j].y, r[2 * j].z, r[2 * j].w,
                                             r[2 * j + 1].x, r[2 * j + 1].y, r[2 * j + 1].z, r[2 * j + 1].w};
 #pragma unroll
                     for (int b = 0; b < 8; ++b) {
-                        const uint4 T = tj[b];
+                        const uint4 T = tj[b * W];
                         const uint32_t tb = sel(c1, sel(c0, T.w, T.z), sel(c0, T.y, T.x));
                         lt |= u & tb & ~rr[b];
                         u &= ~(tb ^ rr[b]);
@@ -477,14 +480,14 @@ plane_c5_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
             uint4* th = c5_thr();
             if (RULE == 0) {  // class-2/3 planes 0-7
                 for (int q = threadIdx.x; q < 4 * a.W; q += blockDim.x) {
-                    const int w = q >> 2, part = q & 3;
+                    const int part = q / a.W, w = q % a.W;
                     th[q] = reinterpret_cast<const uint4*>(a.kpc + ((size_t)w * a.n_types + t30) * 128)
                         [(part & 1) + 16 * (part >> 1)];
                 }
             } else {          // 4 classes: planes 0-7 and "always"
                 const int kp0 = a.ty[t30].kp_off;
                 for (int q = threadIdx.x; q < 9 * a.W; q += blockDim.x) {
-                    const int w = q / 9, b = q % 9;
+                    const int b = q / a.W, w = q % a.W;
                     th[q] = *reinterpret_cast<const uint4*>(a.kp + (size_t)w * a.kpw + kp0 + (b < 8 ? b : kKPlanes) * 4);
                 }
             }
