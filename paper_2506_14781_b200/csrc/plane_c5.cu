@@ -371,41 +371,19 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
         uint32_t Q0[kC5VB], Q1[kC5VB];
 #pragma unroll
         for (int b = 0; b < kC5VB; ++b) { Q0[b] = 0u; Q1[b] = 0u; }
-        struct QRows { uint2 s, x0, x1, x2, y; };
-        auto qentries = [&](int i) -> int4 {
-            int4 v = make_int4(0, 0, 0, 0);
-            if (i < n_it) {
-                const int st = cf + i * S + sl;
-                if (st < ce) v = __ldg(a.nbr4 + st);
-            }
-            return v;
-        };
-        auto qrows = [&](int i, const int4& e) -> QRows {
-            const uint2 z = make_uint2(0u, 0u);
-            QRows q{z, z, z, z, z};
-            const int st = cf + i * S + sl;
-            if (i < n_it && st < ce) {
-                q.s = row((uint32_t)st << logW);
-                q.x0 = row((uint32_t)e.x & 0x7fffffffu);
-                q.x1 = row((uint32_t)e.y & 0x7fffffffu);
-                q.x2 = row((uint32_t)e.z & 0x7fffffffu);
-                q.y = row((uint32_t)e.w);
-            }
-            return q;
-        };
-        // software pipeline as in the chain-free loop
-        int4 qen = qentries(gw);
-        QRows qrn = qrows(gw, qen);
-        int4 qen2 = qentries(gw + nw);
         for (int it = gw; it < n_it; it += nw) {
             const uint32_t site = (uint32_t)(cf + it * S + sl);
             const bool valid = (int)site < ce;
-            const int4 e = qen;
-            const QRows qr = qrn;
-            qen = qen2;
-            qrn = qrows(it + nw, qen);
-            qen2 = qentries(it + 2 * nw);
-            const uint2 s = qr.s, x0 = qr.x0, x1 = qr.x1, x2 = qr.x2, y = qr.y;
+            int4 e = make_int4(0, 0, 0, 0);
+            uint2 s = make_uint2(0u, 0u), x0 = s, x1 = s, x2 = s, y = s;
+            if (valid) {
+                e = __ldg(a.nbr4 + site);
+                s = row(site << logW);
+                x0 = row((uint32_t)e.x & 0x7fffffffu);
+                x1 = row((uint32_t)e.y & 0x7fffffffu);
+                x2 = row((uint32_t)e.z & 0x7fffffffu);
+                y = row((uint32_t)e.w);
+            }
             u32x4 r[4];
             philox_planeN<4>(site, K.g, K.P, a.pks, r);
             const uint32_t m0s = (uint32_t)(e.x >> 31), m1s = (uint32_t)(e.y >> 31), m2s = (uint32_t)(e.z >> 31);
