@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtempergrid_b200.so")
 SOURCES = ["kernels.cu", "capi.cu", "host_common.cu", "host_plane.cu", "host_slot.cu",
-           "host_run.cu", "host_extras.cu", "host_ckpt.cu", "plane_sweep.cu", "plane_tpw.cu", "plane_c5.cu", "slot_engine.cu", "slot_fast.cu", "prep.cu"]
+           "host_run.cu", "host_extras.cu", "host_ckpt.cu", "plane_sweep.cu", "plane_tpw.cu", "plane_c5.cu", "plane_cl.cu", "slot_engine.cu", "slot_fast.cu", "prep.cu"]
 HEADERS = ["engine.cuh", "kernels.cuh", "philox.cuh", "philox_plane.cuh", "plane_device.cuh", "plane_round.cuh",
            "host.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -55,6 +55,7 @@ def build_engine(force: bool = False, verbose: bool = False) -> str:
              ("plane_tpw.cu", "tpw_r0.o", ["-DTG_PLANE_RULE=0"]),
              ("plane_tpw.cu", "tpw_r1.o", ["-DTG_PLANE_RULE=1"]),
              ("plane_c5.cu", "plane_c5.o", []),
+             ("plane_cl.cu", "plane_cl.o", []),
              ("slot_engine.cu", "slot_engine.o", []), ("slot_fast.cu", "slot_fast.o", []),
              ("prep.cu", "prep.o", [])]
     procs = []

@@ -140,6 +140,11 @@ struct RoundArgs {
     int n_warps;           // tpw kernel: warps of the launch
     int log_w;             // tpw kernel: log2 of the words per site
     int c5_nfree[2];       // c5 kernel: chain-free sites of colours 0, 1 (they precede the chain sites)
+    int cl_stage;          // cluster kernel: neighbour entries staged in shared memory (TMA)
+    int cl_size;           // cluster kernel: CTAs per cluster the host launched with
+    int cl_ktab;           // cluster kernel: ktab staged in shared memory
+    unsigned long long* cl_x;  // cluster kernel: (f, g) exchange words [2 parities][32 W], each
+                           // {round tag : 16 | chain count : 24 | cost count : 24}; [2 * 32 W] = error word
     const uint64_t* ktab;
     int ktab_row;
     uint32_t* kp;
@@ -306,15 +311,13 @@ TG_HD double dexp(double x) {
 
 // Attempt k of the round: P phase rows i ascending, pairs p = even, even+2..
 // (engine.cpp:148-167); beta phase columns j ascending, pairs b = even, ..
-// (engine.cpp:168-187).  One swap-stream draw per attempt in that order.
+// (engine.cpp:168-187).  One swap-stream draw per attempt in that order (u).
 // Returns 1 on accept and reports the two slots and the counter index.
-TG_HD int swap_attempt(int I, int J, const double* betas, const double* pens, int64_t round,
-                       int k, const double* f_all, const double* g_all, const int32_t* slot_state,
-                       uint64_t swap_seed, uint64_t swap_base, int& slot_a, int& slot_b,
-                       int& counter, int& is_p) {
+TG_HD int swap_attempt_u(int I, int J, const double* betas, const double* pens, int64_t round,
+                         int k, const double* f_all, const double* g_all, const int32_t* slot_state,
+                         double u, int& slot_a, int& slot_b, int& counter, int& is_p) {
     int even, dp, db;
     round_phase(I, J, round, even, dp, db);
-    const double u = (double)(stream_bits(swap_seed, swap_base + (uint64_t)k) >> 11) * 0x1.0p-53;
     double x;
     if (dp) {
         const int per = pairs_in(J, even);
@@ -341,6 +344,19 @@ TG_HD int swap_attempt(int I, int J, const double* betas, const double* pens, in
         is_p = 0;
     }
     return (x >= 0.0 || u < dexp(x)) ? 1 : 0;
+}
+
+// The attempt's uniform: draw swap_base + k of the swap stream.
+TG_HD double swap_uniform(uint64_t swap_seed, uint64_t swap_base, int k) {
+    return (double)(stream_bits(swap_seed, swap_base + (uint64_t)k) >> 11) * 0x1.0p-53;
+}
+
+TG_HD int swap_attempt(int I, int J, const double* betas, const double* pens, int64_t round,
+                       int k, const double* f_all, const double* g_all, const int32_t* slot_state,
+                       uint64_t swap_seed, uint64_t swap_base, int& slot_a, int& slot_b,
+                       int& counter, int& is_p) {
+    return swap_attempt_u(I, J, betas, pens, round, k, f_all, g_all, slot_state,
+                          swap_uniform(swap_seed, swap_base, k), slot_a, slot_b, counter, is_p);
 }
 
 }  // namespace tg

@@ -328,6 +328,9 @@ struct tg_ctx {
     int fused_tpw = 0, tpw_fast = 0;
     int fused_c5 = 0;                // config-5 kernel (plane_c5.cu) for the fused round loop
     int c5_nfree[2] = {0, 0};        // chain-free sites of colours 0, 1
+    int fused_cl = 0;                // cluster-per-word kernel (plane_cl.cu) instead of plane_c5
+    int cl_size = 0, cl_stage = 0;   // CTAs per cluster; neighbour entries staged in shared memory
+    int cl_ktab = 0, cl_small = 0;   // ktab staged in shared memory; <= 5 sites per thread and phase
     int tpw_sweep_grid = 0;          // sweep-only tpw kernel grid (0: plane_sweep_kernel)
     size_t tpw_sweep_smem = 0;
     const char* sweep_kernel = "";   // dominant sweep kernel of the last advance (tg_info)     // thread-per-(site, word) kernel (plane_tpw.cu) instead of plane_rounds_kernel
@@ -343,6 +346,7 @@ struct tg_ctx {
     DBuf<uint32_t> d_spins32, d_kp, d_kpc, d_active;
     DBuf<int32_t> d_nbr, d_cnt_c, d_cnt_q, d_cnt2;
     DBuf<int4> d_nbr4;
+    DBuf<unsigned long long> d_clx;  // cluster kernel: tagged (f, g) exchange words [2 parities][32 W] + error word
     DBuf<int> d_work;
     DBuf<Chunk> d_chunks;
     DBuf<int> d_chunk_off, d_color_start;

@@ -381,7 +381,93 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
             }
         }
     }
-    if (c.fused_tpw && !c.fused_c5) {
+    // cluster-per-word kernel (plane_cl.cu): the same config-5 path with one
+    // thread-block cluster per 32-replica word (cluster barriers per colour
+    // phase, one release-flag (f, g) exchange per round, neighbour entries
+    // staged by TMA).  It uses W * C SMs (C <= 10 for 8 words on B200: one
+    // GPC hosts no larger cluster), so it wins where the grid barriers and
+    // the per-round fixed cost dominate: auto for n <= 2^16 sites.
+    // TG_PLANE_CL = 0 never, 1 whenever eligible; TG_PLANE_CL_SIZE caps C.
+    c.fused_cl = 0;
+    {
+        bool ok = c.world == 1 && c.R <= 2048 && c.tpw_fast && c.n_colors == 2 && c.n_types <= 2 &&
+                  c.d_nbr4.p != nullptr && c.W <= kMaxWordsArg;
+        int nfree_type = 0;
+        for (const auto& t : types) nfree_type += t.dq == 0;
+        ok = ok && nfree_type <= 1;
+        int mode = -1;
+        if (const char* e = std::getenv("TG_PLANE_CL")) mode = std::atoi(e);
+        if (mode == 0 || (mode < 0 && n > (1 << 16))) ok = false;
+        int cmax = 16;
+        if (const char* e = std::getenv("TG_PLANE_CL_SIZE")) cmax = std::max(1, std::atoi(e));
+        // the exchange words carry 24-bit bond counts
+        ok = ok && c.m_cost < (1 << 24) && c.np < (1 << 24);
+        if (ok) {
+            int dev = 0, smem_max = 0;
+            CK(cudaGetDevice(&dev));
+            CK(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+            for (int C = 16; C >= 1 && !c.fused_cl; --C) {  // any size: GPCs differ in SM count
+                if (C > cmax || c.W * C > c.sms) continue;
+                // entries of the largest slice set (rank 0) and its sites per thread and phase
+                size_t total = 0;
+                int items[2] = {0, 0};
+                for (int q = 0; q < 4; ++q) {
+                    const int col = q >> 1;
+                    const int cs = c.color_start[col], ce = c.color_start[col + 1], cf = cs + c.c5_nfree[col];
+                    const int len = (q & 1) ? ce - cf : cf - cs;
+                    int per = (len + C - 1) / C;
+                    per = (per + 31) & ~31;
+                    total += (size_t)std::min(per, len);
+                    items[col] += (std::min(per, len) + kClThreads - 1) / kClThreads;
+                }
+                const int small = std::max(items[0], items[1]) <= 5 && !std::getenv("TG_PLANE_CL_BIGCNT");
+                const void* fn = plane_cl_fn(c.cfg.rule, small);
+                CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+                // staged in shared memory when they fit: ktab first (24 KB at 16x16), then the entries
+                const size_t ktw = (size_t)c.R * c.ktab_row;
+                int kt = 1, stage = 1;
+                if (std::getenv("TG_PLANE_CL_NOSTAGE")) stage = 0;
+                if (cl_smem_bytes(c.R, c.I, c.J, c.kpw, c.n_types, ktw, 0) > (size_t)smem_max || ktw * 8 > 64 * 1024)
+                    kt = 0;
+                if (cl_smem_bytes(c.R, c.I, c.J, c.kpw, c.n_types, kt ? ktw : 0, total) > (size_t)smem_max) stage = 0;
+                const size_t smem = cl_smem_bytes(c.R, c.I, c.J, c.kpw, c.n_types, kt ? ktw : 0, stage ? total : 0);
+                if (smem > (size_t)smem_max) continue;
+                CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                cudaLaunchConfig_t lc{};
+                lc.gridDim = dim3(c.W * C);
+                lc.blockDim = dim3(kClThreads);
+                lc.dynamicSmemBytes = smem;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = C;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                lc.attrs = at;
+                lc.numAttrs = 1;
+                int nact = 0;
+                if (cudaOccupancyMaxActiveClusters(&nact, fn, &lc) != cudaSuccess) {
+                    cudaGetLastError();
+                    continue;
+                }
+                if (std::getenv("TG_PLANE_CL_VERBOSE"))
+                    std::fprintf(stderr, "plane_cl: C=%d smem=%zu stage=%d ktab=%d small=%d active clusters=%d (need %d)\n",
+                                 C, smem, stage, kt, small, nact, c.W);
+                if (nact >= c.W) {
+                    c.fused_cl = 1;
+                    c.cl_size = C;
+                    c.cl_stage = stage;
+                    c.cl_ktab = kt;
+                    c.cl_small = small;
+                    c.fused_grid = c.W * C;
+                    c.fused_block = kClThreads;
+                    c.fused_smem = smem;
+                    c.d_clx.alloc((size_t)2 * c.W * 32 + 1);
+                }
+            }
+        }
+        if (c.fused_cl) c.fused_c5 = 0;
+    }
+    if (c.fused_tpw && !c.fused_c5 && !c.fused_cl) {
         const void* fn = plane_tpw_fn(c.cfg.rule, c.tpw_fast);
         c.fused_block = kernel_fit(fn, 0, 0).max_threads;  // the kernel's launch bound
         c.fused_smem = tpw_smem_bytes(c.R, c.W, c.fused_block);
@@ -389,7 +475,7 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
         if (fb >= 1) c.fused_grid = fb * c.sms;
         else c.fused_tpw = 0;
     }
-    if (!c.fused_tpw && c.world == 1 && c.R <= 2048) {
+    if (!c.fused_tpw && !c.fused_cl && c.world == 1 && c.R <= 2048) {
         c.fused_wv = c.WV;
         const void* fn = plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast);
         c.fused_block = c.fused_fast ? kPlaneThreadsFast : kPlaneThreads;
@@ -494,7 +580,7 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         r.work = nullptr;
         r.c5_nfree[0] = c.c5_nfree[0];
         r.c5_nfree[1] = c.c5_nfree[1];
-        if (c.fused_tpw && c.tpw_fast && !c.fused_c5) {
+        if (c.fused_tpw && c.tpw_fast && !c.fused_c5 && !c.fused_cl) {
             const size_t need = (size_t)2 * c.n_colors * c.cfg.sweeps_per_swap;
             if (c.d_work.n < need) { c.d_work.alloc(need); c.d_work.zero(st); }
             r.work = std::getenv("TG_TPW_STATIC") ? nullptr : c.d_work.p;
@@ -503,14 +589,42 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         r.rec = c.d_rec.p; r.rec_acc = c.d_rec_acc.p;
         r.rec_states = (flags & TG_REC_STATE) ? c.d_rec_states.p : nullptr;
         r.perm = c.d_perm.p;
+        if (c.fused_cl) {
+            r.cl_stage = c.cl_stage;
+            r.cl_size = c.cl_size;
+            r.cl_ktab = c.cl_ktab;
+            r.cl_x = c.d_clx.p;
+            CK(cudaMemsetAsync(c.d_clx.p, 0, sizeof(unsigned long long) * c.d_clx.n, st));
+        }
         void* args[] = {&a, &r};
         if (c.profiling) CK(cudaEventRecord(c.ev[0], st));
-        c.sweep_kernel = c.fused_c5 ? "plane_c5_rounds_kernel"
-                                    : c.fused_tpw ? "plane_tpw_rounds_kernel" : "plane_rounds_kernel";
-        const void* fn = c.fused_c5 ? plane_c5_fn(c.cfg.rule)
-                                    : c.fused_tpw ? plane_tpw_fn(c.cfg.rule, c.tpw_fast)
-                                                  : plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast);
-        CK(cudaLaunchCooperativeKernel(fn, dim3(c.fused_grid), dim3(c.fused_block), args, c.fused_smem, st));
+        c.sweep_kernel = c.fused_cl ? "plane_cl_rounds_kernel"
+                         : c.fused_c5 ? "plane_c5_rounds_kernel"
+                                      : c.fused_tpw ? "plane_tpw_rounds_kernel" : "plane_rounds_kernel";
+        const void* fn = c.fused_cl ? plane_cl_fn(c.cfg.rule, c.cl_small)
+                         : c.fused_c5 ? plane_c5_fn(c.cfg.rule)
+                                      : c.fused_tpw ? plane_tpw_fn(c.cfg.rule, c.tpw_fast)
+                                                    : plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast);
+        if (c.fused_cl) {
+            // W clusters of cl_size CTAs, all co-resident (cooperative launch)
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3(c.fused_grid);
+            lc.blockDim = dim3(c.fused_block);
+            lc.dynamicSmemBytes = c.fused_smem;
+            lc.stream = st;
+            cudaLaunchAttribute at[2];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = c.cl_size;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            at[1].id = cudaLaunchAttributeCooperative;
+            at[1].val.cooperative = 1;
+            lc.attrs = at;
+            lc.numAttrs = std::getenv("TG_PLANE_CL_NOCOOP") ? 1 : 2;
+            CK(cudaLaunchKernelExC(&lc, fn, args));
+        } else {
+            CK(cudaLaunchCooperativeKernel(fn, dim3(c.fused_grid), dim3(c.fused_block), args, c.fused_smem, st));
+        }
         if (c.profiling) CK(cudaEventRecord(c.ev[1], st));
         c.sweep_launches++;
         const int64_t first = c.rounds_done + 1;
@@ -527,7 +641,13 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
             sweep_ms += ms;
         }
     }
+    unsigned long long cl_err = 0;
+    if (c.fused_cl)
+        CK(cudaMemcpyAsync(&cl_err, c.d_clx.p + (size_t)2 * c.W * 32, sizeof(cl_err), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (cl_err)
+        fail(TG_ERR_CUDA, "plane_cl_rounds_kernel ran without its cluster dimension (profilers drop it from "
+                          "cooperative launches: set TG_PLANE_CL_NOCOOP=1)");
     c.last_sweep_ms = sweep_ms;
     c.last_swap_ms = 0;
 }

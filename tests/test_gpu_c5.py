@@ -13,6 +13,13 @@ from test_gpu_tpw import kernel_of, sched
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True)
+def _no_cluster_kernel(monkeypatch):
+    # these cases pin plane_c5_rounds_kernel: keep the cluster-per-word kernel
+    # (plane_cl.cu, tests/test_gpu_cl.py; the default up to 2^16 sites) out
+    monkeypatch.setenv("TG_PLANE_CL", "0")
+
 C5S = I.bipartite_3regular(512, seed=3)
 
 

@@ -23,6 +23,7 @@ def _no_c5_kernel(monkeypatch):
     # these cases pin the tpw / thread-per-site kernels: keep the config-5
     # kernel (plane_c5.cu, tests/test_gpu_c5.py) out of the dispatch
     monkeypatch.setenv("TG_PLANE_C5", "0")
+    monkeypatch.setenv("TG_PLANE_CL", "0")
 
 C5S = I.bipartite_3regular(512, seed=3)      # cost degree 3, chain degree 0/1, 2 colours
 K10 = I.k10_pm1(1)                           # non-bipartite, larger degrees: generic path
