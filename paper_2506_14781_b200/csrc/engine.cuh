@@ -143,6 +143,8 @@ struct RoundArgs {
     int cl_stage;          // cluster kernel: neighbour entries staged in shared memory (TMA)
     int cl_size;           // cluster kernel: CTAs per cluster the host launched with
     int cl_ktab;           // cluster kernel: ktab staged in shared memory
+    unsigned int* cl_bar;  // cluster kernel, group mode: per-word barrier counters [W][32] (one line each)
+    int32_t* cl_gtot;      // cluster kernel, group mode: word totals [2 parities][W][64]
     unsigned long long* cl_x;  // cluster kernel: (f, g) exchange words [2 parities][32 W], each
                            // {round tag : 16 | chain count : 24 | cost count : 24}; [2 * 32 W] = error word
     const uint64_t* ktab;

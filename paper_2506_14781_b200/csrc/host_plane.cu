@@ -402,12 +402,17 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
         if (const char* e = std::getenv("TG_PLANE_CL_SIZE")) cmax = std::max(1, std::atoi(e));
         // the exchange words carry 24-bit bond counts
         ok = ok && c.m_cost < (1 << 24) && c.np < (1 << 24);
+        // TG_PLANE_CL_MODE = cluster | group; auto: the hardware cluster barrier up to 2^14 sites, the
+        // software word barrier on all SMs above (one GPC of a B200 hosts no cluster > 10 CTAs when 8
+        // are needed, so cluster mode runs on 80 SMs)
+        int gmode = n > (1 << 14) ? 1 : 0;
+        if (const char* e = std::getenv("TG_PLANE_CL_MODE")) gmode = std::string(e) == "group";
         if (ok) {
             int dev = 0, smem_max = 0;
             CK(cudaGetDevice(&dev));
             CK(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-            for (int C = 16; C >= 1 && !c.fused_cl; --C) {  // any size: GPCs differ in SM count
-                if (C > cmax || c.W * C > c.sms) continue;
+            struct Plan { size_t smem; int stage, kt, small; const void* fn; };
+            auto plan = [&](int C, int group, Plan& P) -> bool {
                 // entries of the largest slice set (rank 0) and its sites per thread and phase
                 size_t total = 0;
                 int items[2] = {0, 0};
@@ -420,23 +425,55 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
                     total += (size_t)std::min(per, len);
                     items[col] += (std::min(per, len) + kClThreads - 1) / kClThreads;
                 }
-                const int small = std::max(items[0], items[1]) <= 5 && !std::getenv("TG_PLANE_CL_BIGCNT");
-                const void* fn = plane_cl_fn(c.cfg.rule, small);
-                CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+                P.small = std::max(items[0], items[1]) <= 5 && !std::getenv("TG_PLANE_CL_BIGCNT");
+                P.fn = plane_cl_fn(c.cfg.rule, P.small, group);
                 // staged in shared memory when they fit: ktab first (24 KB at 16x16), then the entries
                 const size_t ktw = (size_t)c.R * c.ktab_row;
-                int kt = 1, stage = 1;
-                if (std::getenv("TG_PLANE_CL_NOSTAGE")) stage = 0;
+                P.kt = 1;
+                P.stage = std::getenv("TG_PLANE_CL_NOSTAGE") ? 0 : 1;
                 if (cl_smem_bytes(c.R, c.I, c.J, c.kpw, c.n_types, ktw, 0) > (size_t)smem_max || ktw * 8 > 64 * 1024)
-                    kt = 0;
-                if (cl_smem_bytes(c.R, c.I, c.J, c.kpw, c.n_types, kt ? ktw : 0, total) > (size_t)smem_max) stage = 0;
-                const size_t smem = cl_smem_bytes(c.R, c.I, c.J, c.kpw, c.n_types, kt ? ktw : 0, stage ? total : 0);
-                if (smem > (size_t)smem_max) continue;
-                CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    P.kt = 0;
+                if (cl_smem_bytes(c.R, c.I, c.J, c.kpw, c.n_types, P.kt ? ktw : 0, total) > (size_t)smem_max)
+                    P.stage = 0;
+                P.smem = cl_smem_bytes(c.R, c.I, c.J, c.kpw, c.n_types, P.kt ? ktw : 0, P.stage ? total : 0);
+                if (P.smem > (size_t)smem_max) return false;
+                CK(cudaFuncSetAttribute(P.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
+                return true;
+            };
+            auto take = [&](int C, int group, const Plan& P) {
+                c.fused_cl = 1;
+                c.cl_group = group;
+                c.cl_size = C;
+                c.cl_stage = P.stage;
+                c.cl_ktab = P.kt;
+                c.cl_small = P.small;
+                c.fused_grid = c.W * C;
+                c.fused_block = kClThreads;
+                c.fused_smem = P.smem;
+                // exchange words [2][32 W] | error word | barrier lines [W][16] | group totals [2][W][32]
+                c.d_clx.alloc((size_t)2 * c.W * 32 + 1 + (size_t)16 * c.W + (size_t)64 * c.W);
+            };
+            if (gmode) {  // G CTAs per word of an ordinary cooperative launch
+                const int G = std::min(std::min(c.sms / c.W, 32), cmax);
+                Plan P;
+                if (G >= 1 && plan(G, 1, P)) {
+                    int per_sm = 0;
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P.fn, kClThreads, P.smem));
+                    if (std::getenv("TG_PLANE_CL_VERBOSE"))
+                        std::fprintf(stderr, "plane_cl: group G=%d smem=%zu stage=%d ktab=%d small=%d blocks/SM=%d\n", G,
+                                     P.smem, P.stage, P.kt, P.small, per_sm);
+                    if (per_sm >= 1) take(G, 1, P);
+                }
+            }
+            for (int C = 16; C >= 1 && !c.fused_cl; --C) {  // any size: GPCs differ in SM count
+                if (C > cmax || c.W * C > c.sms) continue;
+                Plan P;
+                if (!plan(C, 0, P)) continue;
+                CK(cudaFuncSetAttribute(P.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
                 cudaLaunchConfig_t lc{};
                 lc.gridDim = dim3(c.W * C);
                 lc.blockDim = dim3(kClThreads);
-                lc.dynamicSmemBytes = smem;
+                lc.dynamicSmemBytes = P.smem;
                 cudaLaunchAttribute at[1];
                 at[0].id = cudaLaunchAttributeClusterDimension;
                 at[0].val.clusterDim.x = C;
@@ -445,24 +482,14 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
                 lc.attrs = at;
                 lc.numAttrs = 1;
                 int nact = 0;
-                if (cudaOccupancyMaxActiveClusters(&nact, fn, &lc) != cudaSuccess) {
+                if (cudaOccupancyMaxActiveClusters(&nact, P.fn, &lc) != cudaSuccess) {
                     cudaGetLastError();
                     continue;
                 }
                 if (std::getenv("TG_PLANE_CL_VERBOSE"))
                     std::fprintf(stderr, "plane_cl: C=%d smem=%zu stage=%d ktab=%d small=%d active clusters=%d (need %d)\n",
-                                 C, smem, stage, kt, small, nact, c.W);
-                if (nact >= c.W) {
-                    c.fused_cl = 1;
-                    c.cl_size = C;
-                    c.cl_stage = stage;
-                    c.cl_ktab = kt;
-                    c.cl_small = small;
-                    c.fused_grid = c.W * C;
-                    c.fused_block = kClThreads;
-                    c.fused_smem = smem;
-                    c.d_clx.alloc((size_t)2 * c.W * 32 + 1);
-                }
+                                 C, P.smem, P.stage, P.kt, P.small, nact, c.W);
+                if (nact >= c.W) take(C, 0, P);
             }
         }
         if (c.fused_cl) c.fused_c5 = 0;
@@ -594,6 +621,8 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
             r.cl_size = c.cl_size;
             r.cl_ktab = c.cl_ktab;
             r.cl_x = c.d_clx.p;
+            r.cl_bar = reinterpret_cast<unsigned int*>(c.d_clx.p + (size_t)2 * c.W * 32 + 1);
+            r.cl_gtot = reinterpret_cast<int32_t*>(c.d_clx.p + (size_t)2 * c.W * 32 + 1 + (size_t)16 * c.W);
             CK(cudaMemsetAsync(c.d_clx.p, 0, sizeof(unsigned long long) * c.d_clx.n, st));
         }
         void* args[] = {&a, &r};
@@ -601,11 +630,11 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         c.sweep_kernel = c.fused_cl ? "plane_cl_rounds_kernel"
                          : c.fused_c5 ? "plane_c5_rounds_kernel"
                                       : c.fused_tpw ? "plane_tpw_rounds_kernel" : "plane_rounds_kernel";
-        const void* fn = c.fused_cl ? plane_cl_fn(c.cfg.rule, c.cl_small)
+        const void* fn = c.fused_cl ? plane_cl_fn(c.cfg.rule, c.cl_small, c.cl_group)
                          : c.fused_c5 ? plane_c5_fn(c.cfg.rule)
                                       : c.fused_tpw ? plane_tpw_fn(c.cfg.rule, c.tpw_fast)
                                                     : plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast);
-        if (c.fused_cl) {
+        if (c.fused_cl && !c.cl_group) {
             // W clusters of cl_size CTAs, all co-resident (cooperative launch)
             cudaLaunchConfig_t lc{};
             lc.gridDim = dim3(c.fused_grid);

@@ -66,7 +66,8 @@ inline size_t cl_smem_bytes(int R, int I, int J, int kpw, int n_types, size_t kt
            ((size_t)R * (2 * sizeof(double) + 2 * sizeof(int32_t)) + 8 + 15) / 16 * 16 +
            ((2 * ktab_words + 3) & ~(size_t)3) * 4 + stage_entries * 16;
 }
-void* plane_cl_fn(int rule, int small);  // small: <= 5 sites per thread and phase (4-plane counters)
+void* plane_cl_fn(int rule, int small, int group);  // small: <= 5 sites per thread and phase (4-plane
+                                                    // counters); group: software word barrier (no clusters)
 constexpr int kSlotThreads = 256;
 constexpr int kSwapThreads = 1024;
 

@@ -27,6 +27,14 @@
 //   * the target digest / snapshot is taken by the cluster that holds the
 //     target replica, each CTA over the sites it updates itself.
 // thread = (site, word); per-warp deferred-tail queue as in plane_c5.cu.
+//
+// Two launch modes share the kernel (template GROUP).  Cluster mode is the one
+// described above.  On B200 one GPC hosts no cluster larger than 10 CTAs when
+// 8 are needed, so cluster mode runs on 80 of the 148 SMs; group mode gives a
+// word G = floor(SMs / W) CTAs of an ordinary cooperative launch (144 SMs for
+// 8 words): the word's colour-phase barrier is then a software barrier on a
+// per-word global counter and the counts are reduced with global atomics.
+// The hardware barrier wins at 2^14 sites, the extra SMs from 2^15 up.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -161,6 +169,25 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long
 }
 __device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu_u32(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Group mode: barrier of the G CTAs of one word on the word's global counter
+// (monotonic: `target` = G x barriers so far); the fence of thread 0 after the
+// CTA barrier publishes the CTA's spin stores (read with ld.cg by the peers).
+__device__ __forceinline__ void cl_group_sync(unsigned int* bar, unsigned int target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        while (ld_acquire_gpu_u32(bar) < target) {}
+    }
+    __syncthreads();
 }
 
 // ------------------------------------------------------------ thresholds
@@ -377,18 +404,35 @@ __device__ __forceinline__ void cl_phase(const PlaneArgs& a, const RoundArgs& r,
     {
         uint4 k2a, k2b, k3a, k3b;
         if (RULE == 0) { k2a = kc[0]; k2b = kc[1]; k3a = kc[16]; k3b = kc[17]; }
+        // software pipeline: the rows of the next site and the entry of the
+        // one after it are in flight while the current site computes
+        auto entry = [&](int st) -> int4 {
+            int4 v = make_int4(0, 0, 0, 0);
+            if (st < fhi) v = fent ? fent[st] : __ldg(a.nbr4 + st);
+            return v;
+        };
+        auto rows = [&](int st, const int4& en, uint32_t& rs, uint32_t& r0, uint32_t& r1, uint32_t& r2) {
+            rs = 0u; r0 = 0u; r1 = 0u; r2 = 0u;
+            if (st < fhi) {
+                rs = __ldcg(base + ((size_t)st << logW));
+                r0 = __ldcg(base + ((uint32_t)en.x & 0x7fffffffu));
+                r1 = __ldcg(base + ((uint32_t)en.y & 0x7fffffffu));
+                r2 = __ldcg(base + ((uint32_t)en.z & 0x7fffffffu));
+            }
+        };
+        const int first = flo + (int)(threadIdx.x & ~31u) + lane;
+        int4 en = entry(first);
+        uint32_t ns_, n0, n1, n2;
+        rows(first, en, ns_, n0, n1, n2);
+        int4 en2 = entry(first + kClThreads);
         for (int b0 = flo + (int)(threadIdx.x & ~31u); b0 < fhi; b0 += kClThreads) {
             const int site = b0 + lane;
             const bool valid = site < fhi;
-            int4 e = make_int4(0, 0, 0, 0);
-            uint32_t s = 0u, x0 = 0u, x1 = 0u, x2 = 0u;
-            if (valid) {
-                e = fent ? fent[site] : __ldg(a.nbr4 + site);
-                s = __ldcg(base + ((size_t)site << logW));
-                x0 = __ldcg(base + ((uint32_t)e.x & 0x7fffffffu));
-                x1 = __ldcg(base + ((uint32_t)e.y & 0x7fffffffu));
-                x2 = __ldcg(base + ((uint32_t)e.z & 0x7fffffffu));
-            }
+            const int4 e = en;
+            const uint32_t s = ns_, x0 = n0, x1 = n1, x2 = n2;
+            en = en2;
+            rows(site + kClThreads, en, ns_, n0, n1, n2);
+            en2 = entry(site + 2 * kClThreads);
             u32x4 r0, r1;
             philox_plane2((uint32_t)site, g0, P, a.pks, r0, r1);
             const uint32_t bb0 = x0 ^ (uint32_t)(e.x >> 31), bb1 = x1 ^ (uint32_t)(e.y >> 31),
@@ -517,18 +561,20 @@ __device__ __forceinline__ void cl_phase(const PlaneArgs& a, const RoundArgs& r,
 // of C CTAs (cluster dimension set at launch), all co-resident.  NP: planes
 // of the per-thread vertical bond counters (4 when a thread updates <= 5 sites
 // per phase, else 8).
-template <int RULE, int NP>
+template <int RULE, int NP, int GROUP>
 __global__ void __launch_bounds__(kClThreads, 1)
 plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__ RoundArgs r) {
     cg::cluster_group cluster = cg::this_cluster();
-    const int C = (int)cluster.num_blocks();
+    const int C = GROUP ? r.cl_size : (int)cluster.num_blocks();
     const int nrep = a.W * 32;
     if (C != r.cl_size) {  // the launch lost its cluster attribute (seen under a profiler): report, touch nothing
         if (blockIdx.x == 0 && threadIdx.x == 0) r.cl_x[2 * nrep] = 1ull;
         return;
     }
-    const int rank = (int)cluster.block_rank();
+    const int rank = GROUP ? (int)(blockIdx.x % C) : (int)cluster.block_rank();
     const int w = blockIdx.x / C;
+    unsigned int* gbar = r.cl_bar + w * 32;  // group mode: the word's barrier counter (own 128-byte line)
+    unsigned int gtarget = 0;
     const int tid = threadIdx.x, lane = tid & 31;
     const ClSmem S = cl_smem(a, r);
     const RoundSmem s = S.rs;
@@ -584,8 +630,11 @@ plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
     cl_build_planes(a, r, s.state, w, S, false);
     if (r.cl_stage) mbar_wait(S.mbar, 0);
     __syncthreads();
-    cluster.sync();  // every CTA of the cluster has zeroed its totals
-    int* tot0 = cluster.map_shared_rank(S.tot, 0);
+    int* tot0 = S.tot;
+    if (!GROUP) {
+        cluster.sync();  // every CTA of the cluster has zeroed its totals
+        tot0 = cluster.map_shared_rank(S.tot, 0);
+    }
     uint32_t V[NP], Q[NP];
 #pragma unroll
     for (int b = 0; b < NP; ++b) { V[b] = 0u; Q[b] = 0u; }
@@ -602,27 +651,41 @@ plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
             cl_phase<RULE, NP>(a, r, S, w, t, false, t30, t31, V, Q, flo[0], fhi[0], fent[0], qlo[0], qhi[0],
                                qent[0]);
             CL_STAMP(k, 1);
-            cluster.sync();
+            if (GROUP) cl_group_sync(gbar, gtarget += (unsigned)C);
+            else cluster.sync();
             CL_STAMP(k, 2);
             cl_phase<RULE, NP>(a, r, S, w, t, count, t30, t31, V, Q, flo[1], fhi[1], fent[1], qlo[1], qhi[1],
                                qent[1]);
             CL_STAMP(k, 3);
-            if (count) {  // word totals through distributed shared memory
+            if (count) {  // word totals through distributed shared memory (group mode: global atomics)
                 __syncthreads();
                 if (tid < 64) {
                     const int v = S.loc[tid];
-                    if (v) { atomicAdd(tot0 + tid, v); S.loc[tid] = 0; }
+                    if (v) {
+                        atomicAdd(GROUP ? r.cl_gtot + ((size_t)(k & 1) * a.W + w) * 64 + tid : tot0 + tid, v);
+                        S.loc[tid] = 0;
+                    }
                 }
             }
-            cluster.sync();
+            if (GROUP) cl_group_sync(gbar, gtarget += (unsigned)C);
+            else cluster.sync();
             CL_STAMP(k, 4);
         }
         // ---- (f, g) exchange: the leader publishes the word's counts, tagged with the round
         if (rank == 0 && tid < 32) {
-            const unsigned long long cc = (unsigned long long)(uint32_t)S.tot[tid];
-            const unsigned long long cq = (unsigned long long)(uint32_t)S.tot[32 + tid];
-            S.tot[tid] = 0;
-            S.tot[32 + tid] = 0;
+            unsigned long long cc, cq;
+            if (GROUP) {
+                int* gt = r.cl_gtot + ((size_t)(k & 1) * a.W + w) * 64;
+                cc = (unsigned long long)(uint32_t)__ldcg(gt + tid);
+                cq = (unsigned long long)(uint32_t)__ldcg(gt + 32 + tid);
+                gt[tid] = 0;       // this parity's totals are next added to two rounds on
+                gt[32 + tid] = 0;
+            } else {
+                cc = (unsigned long long)(uint32_t)S.tot[tid];
+                cq = (unsigned long long)(uint32_t)S.tot[32 + tid];
+                S.tot[tid] = 0;
+                S.tot[32 + tid] = 0;
+            }
             st_relaxed_gpu(xw + w * 32 + tid, tag << 48 | cq << 24 | cc);
         }
         // the swap uniforms do not depend on the energies: drawn while the words arrive
@@ -709,17 +772,23 @@ plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
         __syncthreads();
         CL_STAMP(k, 8);
     }
-    cluster.sync();  // no CTA exits while a peer may still address its shared memory
+    if (!GROUP) cluster.sync();  // no CTA exits while a peer may still address its shared memory
 }
 
-template __global__ void plane_cl_rounds_kernel<0, 4>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
-template __global__ void plane_cl_rounds_kernel<1, 4>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
-template __global__ void plane_cl_rounds_kernel<0, 8>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
-template __global__ void plane_cl_rounds_kernel<1, 8>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
+#define TG_CL_INST(R, P, G) \
+    template __global__ void plane_cl_rounds_kernel<R, P, G>(const __grid_constant__ PlaneArgs, \
+                                                             const __grid_constant__ RoundArgs);
+TG_CL_INST(0, 4, 0) TG_CL_INST(1, 4, 0) TG_CL_INST(0, 8, 0) TG_CL_INST(1, 8, 0)
+TG_CL_INST(0, 4, 1) TG_CL_INST(1, 4, 1) TG_CL_INST(0, 8, 1) TG_CL_INST(1, 8, 1)
+#undef TG_CL_INST
 
-void* plane_cl_fn(int rule, int small) {
-    if (small) return rule ? (void*)plane_cl_rounds_kernel<1, 4> : (void*)plane_cl_rounds_kernel<0, 4>;
-    return rule ? (void*)plane_cl_rounds_kernel<1, 8> : (void*)plane_cl_rounds_kernel<0, 8>;
+void* plane_cl_fn(int rule, int small, int group) {
+    if (group) {
+        if (small) return rule ? (void*)plane_cl_rounds_kernel<1, 4, 1> : (void*)plane_cl_rounds_kernel<0, 4, 1>;
+        return rule ? (void*)plane_cl_rounds_kernel<1, 8, 1> : (void*)plane_cl_rounds_kernel<0, 8, 1>;
+    }
+    if (small) return rule ? (void*)plane_cl_rounds_kernel<1, 4, 0> : (void*)plane_cl_rounds_kernel<0, 4, 0>;
+    return rule ? (void*)plane_cl_rounds_kernel<1, 8, 0> : (void*)plane_cl_rounds_kernel<0, 8, 0>;
 }
 
 }  // namespace tg

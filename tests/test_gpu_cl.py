@@ -20,6 +20,14 @@ RULES = ["metropolis", "heat_bath"]
 KERNEL = "plane_cl_rounds_kernel"
 
 
+@pytest.fixture(autouse=True, params=["cluster", "group"])
+def _mode(request, monkeypatch):
+    # cluster: hardware clusters (cluster barrier, DSMEM totals); group: the same
+    # kernel as an ordinary cooperative launch, G CTAs per word behind a
+    # software word barrier, totals by global atomics (the default above 2^14)
+    monkeypatch.setenv("TG_PLANE_CL_MODE", request.param)
+
+
 # (I, J) -> words per site = clusters: 32 -> 1, 64 -> 2, 96 -> 4 (one padded
 # word), 128 -> 4, 256 -> 8, 512 -> 16, 1024 -> 32
 @pytest.mark.parametrize("rule", RULES)
