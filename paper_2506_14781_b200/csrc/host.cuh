@@ -332,6 +332,7 @@ struct tg_ctx {
     int cl_size = 0, cl_stage = 0;   // CTAs per cluster; neighbour entries staged in shared memory
     int cl_ktab = 0, cl_small = 0;   // ktab staged in shared memory; <= 5 sites per thread and phase
     int cl_group = 0;                // software word barrier on G = cl_size CTAs per word (no clusters)
+    int cl_pair = 0;                 // ... with two words per thread (G CTAs per word pair)
     int tpw_sweep_grid = 0;          // sweep-only tpw kernel grid (0: plane_sweep_kernel)
     size_t tpw_sweep_smem = 0;
     const char* sweep_kernel = "";   // dominant sweep kernel of the last advance (tg_info)     // thread-per-(site, word) kernel (plane_tpw.cu) instead of plane_rounds_kernel

@@ -381,13 +381,21 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
             }
         }
     }
-    // cluster-per-word kernel (plane_cl.cu): the same config-5 path with one
-    // thread-block cluster per 32-replica word (cluster barriers per colour
-    // phase, one release-flag (f, g) exchange per round, neighbour entries
-    // staged by TMA).  It uses W * C SMs (C <= 10 for 8 words on B200: one
-    // GPC hosts no larger cluster), so it wins where the grid barriers and
-    // the per-round fixed cost dominate: auto for n <= 2^16 sites.
-    // TG_PLANE_CL = 0 never, 1 whenever eligible; TG_PLANE_CL_SIZE caps C.
+    // word-local kernel (plane_cl.cu): the same config-5 path with the CTAs
+    // partitioned by 32-replica word (or word pair), so that a colour phase
+    // ends with a barrier among the word's CTAs only, one tagged-word (f, g)
+    // exchange per round replaces the other grid barriers, and neighbour
+    // entries, ktab and threshold planes live in shared memory (entries staged
+    // by TMA).  Two launch modes: hardware thread-block clusters (cluster
+    // barrier, DSMEM count reduction; on B200 at most 10 CTAs per word when 8
+    // words are needed, i.e. 80 SMs) and "group": an ordinary cooperative
+    // launch with G = SMs / groups CTAs per word behind a software barrier.
+    // Measured on B200 (profiles/r2/c5_sizes_r2.json) group mode is the faster
+    // from 2^14 sites up, with one word per thread up to 2^15 sites and a word
+    // pair per thread up to 2^18; above that plane_c5 (all words of a row in
+    // adjacent lanes: full 32-byte sectors) wins.  TG_PLANE_CL = 0 never, 1
+    // whenever eligible; TG_PLANE_CL_MODE = cluster | group; TG_PLANE_CL_PAIR
+    // = 0 | 1; TG_PLANE_CL_SIZE caps the CTAs per word.
     c.fused_cl = 0;
     {
         bool ok = c.world == 1 && c.R <= 2048 && c.tpw_fast && c.n_colors == 2 && c.n_types <= 2 &&
@@ -397,22 +405,19 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
         ok = ok && nfree_type <= 1;
         int mode = -1;
         if (const char* e = std::getenv("TG_PLANE_CL")) mode = std::atoi(e);
-        if (mode == 0 || (mode < 0 && n > (1 << 16))) ok = false;
-        int cmax = 16;
+        if (mode == 0 || (mode < 0 && n > (1 << 18))) ok = false;
+        int cmax = 1 << 20;  // cap on the CTAs per word (cluster mode: <= 16 anyway)
         if (const char* e = std::getenv("TG_PLANE_CL_SIZE")) cmax = std::max(1, std::atoi(e));
         // the exchange words carry 24-bit bond counts
         ok = ok && c.m_cost < (1 << 24) && c.np < (1 << 24);
-        // TG_PLANE_CL_MODE = cluster | group; auto: the hardware cluster barrier up to 2^14 sites, the
-        // software word barrier on all SMs above (one GPC of a B200 hosts no cluster > 10 CTAs when 8
-        // are needed, so cluster mode runs on 80 SMs)
-        int gmode = n > (1 << 14) ? 1 : 0;
+        int gmode = 1;
         if (const char* e = std::getenv("TG_PLANE_CL_MODE")) gmode = std::string(e) == "group";
         if (ok) {
             int dev = 0, smem_max = 0;
             CK(cudaGetDevice(&dev));
             CK(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
             struct Plan { size_t smem; int stage, kt, small; const void* fn; };
-            auto plan = [&](int C, int group, Plan& P) -> bool {
+            auto plan = [&](int C, int group, int wpt, Plan& P) -> bool {
                 // entries of the largest slice set (rank 0) and its sites per thread and phase
                 size_t total = 0;
                 int items[2] = {0, 0};
@@ -426,49 +431,54 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
                     items[col] += (std::min(per, len) + kClThreads - 1) / kClThreads;
                 }
                 P.small = std::max(items[0], items[1]) <= 5 && !std::getenv("TG_PLANE_CL_BIGCNT");
-                P.fn = plane_cl_fn(c.cfg.rule, P.small, group);
+                P.fn = plane_cl_fn(c.cfg.rule, P.small, group, wpt == 2);
                 // staged in shared memory when they fit: ktab first (24 KB at 16x16), then the entries
                 const size_t ktw = (size_t)c.R * c.ktab_row;
                 P.kt = 1;
                 P.stage = std::getenv("TG_PLANE_CL_NOSTAGE") ? 0 : 1;
-                if (cl_smem_bytes(c.R, c.I, c.J, c.kpw, c.n_types, ktw, 0) > (size_t)smem_max || ktw * 8 > 64 * 1024)
+                if (cl_smem_bytes(c.R, c.I, c.J, c.kpw, c.n_types, ktw, 0, wpt) > (size_t)smem_max || ktw * 8 > 64 * 1024)
                     P.kt = 0;
-                if (cl_smem_bytes(c.R, c.I, c.J, c.kpw, c.n_types, P.kt ? ktw : 0, total) > (size_t)smem_max)
+                if (cl_smem_bytes(c.R, c.I, c.J, c.kpw, c.n_types, P.kt ? ktw : 0, total, wpt) > (size_t)smem_max)
                     P.stage = 0;
-                P.smem = cl_smem_bytes(c.R, c.I, c.J, c.kpw, c.n_types, P.kt ? ktw : 0, P.stage ? total : 0);
+                P.smem = cl_smem_bytes(c.R, c.I, c.J, c.kpw, c.n_types, P.kt ? ktw : 0, P.stage ? total : 0, wpt);
                 if (P.smem > (size_t)smem_max) return false;
                 CK(cudaFuncSetAttribute(P.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
                 return true;
             };
-            auto take = [&](int C, int group, const Plan& P) {
+            auto take = [&](int C, int group, int wpt, const Plan& P) {
                 c.fused_cl = 1;
                 c.cl_group = group;
+                c.cl_pair = wpt == 2;
                 c.cl_size = C;
                 c.cl_stage = P.stage;
                 c.cl_ktab = P.kt;
                 c.cl_small = P.small;
-                c.fused_grid = c.W * C;
+                c.fused_grid = c.W / wpt * C;
                 c.fused_block = kClThreads;
                 c.fused_smem = P.smem;
                 // exchange words [2][32 W] | error word | barrier lines [W][16] | group totals [2][W][32]
                 c.d_clx.alloc((size_t)2 * c.W * 32 + 1 + (size_t)16 * c.W + (size_t)64 * c.W);
             };
-            if (gmode) {  // G CTAs per word of an ordinary cooperative launch
-                const int G = std::min(std::min(c.sms / c.W, 32), cmax);
+            if (gmode) {  // G CTAs per word (or word pair) of an ordinary cooperative launch
+                // two words per thread when the row has an even number of words: the pair shares the
+                // site's Philox products and row sectors (plane_c5.cu); TG_PLANE_CL_PAIR=0 disables
+                int wpt = (c.W % 2 == 0 && n > (1 << 15)) ? 2 : 1;
+                if (const char* e = std::getenv("TG_PLANE_CL_PAIR")) wpt = std::atoi(e) != 0 && c.W % 2 == 0 ? 2 : 1;
+                const int G = std::min(c.sms / (c.W / wpt), cmax);
                 Plan P;
-                if (G >= 1 && plan(G, 1, P)) {
+                if (G >= 1 && plan(G, 1, wpt, P)) {
                     int per_sm = 0;
                     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P.fn, kClThreads, P.smem));
                     if (std::getenv("TG_PLANE_CL_VERBOSE"))
-                        std::fprintf(stderr, "plane_cl: group G=%d smem=%zu stage=%d ktab=%d small=%d blocks/SM=%d\n", G,
-                                     P.smem, P.stage, P.kt, P.small, per_sm);
-                    if (per_sm >= 1) take(G, 1, P);
+                        std::fprintf(stderr, "plane_cl: group G=%d wpt=%d smem=%zu stage=%d ktab=%d small=%d blocks/SM=%d\n",
+                                     G, wpt, P.smem, P.stage, P.kt, P.small, per_sm);
+                    if (per_sm >= 1) take(G, 1, wpt, P);
                 }
             }
             for (int C = 16; C >= 1 && !c.fused_cl; --C) {  // any size: GPCs differ in SM count
                 if (C > cmax || c.W * C > c.sms) continue;
                 Plan P;
-                if (!plan(C, 0, P)) continue;
+                if (!plan(C, 0, 1, P)) continue;
                 CK(cudaFuncSetAttribute(P.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
                 cudaLaunchConfig_t lc{};
                 lc.gridDim = dim3(c.W * C);
@@ -489,7 +499,7 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
                 if (std::getenv("TG_PLANE_CL_VERBOSE"))
                     std::fprintf(stderr, "plane_cl: C=%d smem=%zu stage=%d ktab=%d small=%d active clusters=%d (need %d)\n",
                                  C, P.smem, P.stage, P.kt, P.small, nact, c.W);
-                if (nact >= c.W) take(C, 0, P);
+                if (nact >= c.W) take(C, 0, 1, P);
             }
         }
         if (c.fused_cl) c.fused_c5 = 0;
@@ -630,7 +640,7 @@ void do_advance_fused(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         c.sweep_kernel = c.fused_cl ? "plane_cl_rounds_kernel"
                          : c.fused_c5 ? "plane_c5_rounds_kernel"
                                       : c.fused_tpw ? "plane_tpw_rounds_kernel" : "plane_rounds_kernel";
-        const void* fn = c.fused_cl ? plane_cl_fn(c.cfg.rule, c.cl_small, c.cl_group)
+        const void* fn = c.fused_cl ? plane_cl_fn(c.cfg.rule, c.cl_small, c.cl_group, c.cl_pair)
                          : c.fused_c5 ? plane_c5_fn(c.cfg.rule)
                                       : c.fused_tpw ? plane_tpw_fn(c.cfg.rule, c.tpw_fast)
                                                     : plane_rounds_fn(c.cfg.rule, c.fused_wv, c.fused_fast);

@@ -59,15 +59,17 @@ void* plane_c5_fn(int rule);
 constexpr int kClThreads = 512;
 constexpr int kClQCap = 64;
 inline size_t cl_smem_bytes(int R, int I, int J, int kpw, int n_types, size_t ktab_words,
-                            size_t stage_entries) {
-    return (size_t)(kClThreads / 32) * kClQCap * 16 + (size_t)((kpw + 3) & ~3) * 4 +
-           (size_t)n_types * 128 * 4 + 24 * 4 + 128 * 4 + 16 + (size_t)((I + 1) & ~1) * 8 + (size_t)((J + 1) & ~1) * 8 +
+                            size_t stage_entries, int wpt) {
+    return (size_t)(kClThreads / 32) * kClQCap * 16 + (size_t)wpt * ((kpw + 3) & ~3) * 4 +
+           (size_t)wpt * n_types * 128 * 4 + 24 * 4 + (size_t)wpt * 128 * 4 + 16 +
+           (size_t)((I + 1) & ~1) * 8 + (size_t)((J + 1) & ~1) * 8 +
            (size_t)((I * (J > 1 ? J - 1 : 0) + (I > 1 ? I - 1 : 0) * J + 3) & ~3) * 4 +
            ((size_t)R * (2 * sizeof(double) + 2 * sizeof(int32_t)) + 8 + 15) / 16 * 16 +
            ((2 * ktab_words + 3) & ~(size_t)3) * 4 + stage_entries * 16;
 }
-void* plane_cl_fn(int rule, int small, int group);  // small: <= 5 sites per thread and phase (4-plane
-                                                    // counters); group: software word barrier (no clusters)
+// small: <= 5 sites per thread and phase (4-plane counters); group: software word barrier (no
+// clusters); pair: two words per thread (group mode)
+void* plane_cl_fn(int rule, int small, int group, int pair);
 constexpr int kSlotThreads = 256;
 constexpr int kSwapThreads = 1024;
 

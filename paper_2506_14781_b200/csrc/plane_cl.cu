@@ -94,21 +94,22 @@ struct ClSmem {
     int4* stage;
 };
 
-__device__ __forceinline__ ClSmem cl_smem(const PlaneArgs& a, const RoundArgs& r) {
+// wpt: words per thread (1 or 2): kp | kpc | loc | tot hold one block per word
+__device__ __forceinline__ ClSmem cl_smem(const PlaneArgs& a, const RoundArgs& r, int wpt) {
     ClSmem s;
     int* p = cl_sm;
     s.queue = reinterpret_cast<int4*>(p);
     p += (kClThreads / 32) * kClQCap * 4;
     s.kp = reinterpret_cast<uint32_t*>(p);
-    p += (a.kpw + 3) & ~3;
+    p += wpt * ((a.kpw + 3) & ~3);
     s.kpc = reinterpret_cast<uint32_t*>(p);
-    p += a.n_types * 128;
+    p += wpt * a.n_types * 128;
     s.pks = reinterpret_cast<uint32_t*>(p);
     p += 24;
     s.loc = p;
-    p += 64;
+    p += wpt * 64;
     s.tot = p;
-    p += 64;
+    p += wpt * 64;
     s.mbar = reinterpret_cast<unsigned long long*>(p);
     p += 4;
     s.betas = reinterpret_cast<double*>(p);
@@ -219,14 +220,17 @@ __device__ __forceinline__ void cl_compare8(const uint32_t* cb, const uint32_t* 
 // shared memory (and the global tables when to_global): one warp per (type,
 // class); plane b = bit 52 - b of the lanes' thresholds by two 32x32
 // transposes (plane_round.cuh).
+// w0: the CTA's first word, wpt its word count (word w0 + j fills block j).
 __device__ __forceinline__ void cl_build_planes(const PlaneArgs& a, const RoundArgs& r,
-                                                const int32_t* s_state, int w, const ClSmem& S,
+                                                const int32_t* s_state, int w0, int wpt, const ClSmem& S,
                                                 bool to_global) {
     const int lane = threadIdx.x & 31;
     int combos = 0;
     for (int ty = 0; ty < a.n_types; ++ty) combos += a.ty[ty].ncl;
-    for (int job = threadIdx.x >> 5; job < combos; job += blockDim.x >> 5) {
-        int c = job, ty = 0;
+    const int kpw4 = (a.kpw + 3) & ~3;
+    for (int job = threadIdx.x >> 5; job < combos * wpt; job += blockDim.x >> 5) {
+        const int jw = job / combos, w = w0 + jw;
+        int c = job % combos, ty = 0;
         while (c >= a.ty[ty].ncl) { c -= a.ty[ty].ncl; ++ty; }
         const PlaneType& pt = a.ty[ty];
         const int m = w * 32 + lane;
@@ -241,8 +245,9 @@ __device__ __forceinline__ void cl_build_planes(const PlaneArgs& a, const RoundA
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
             if (g == 1 && !to_global) break;
-            uint32_t* dst = (g ? r.kp + (size_t)w * a.kpw : S.kp) + pt.kp_off + c;
-            uint32_t* dstc = (g ? r.kpc + (size_t)w * a.n_types * 128 : S.kpc) + ty * 128 + (c - 2) * 64;
+            uint32_t* dst = (g ? r.kp + (size_t)w * a.kpw : S.kp + jw * kpw4) + pt.kp_off + c;
+            uint32_t* dstc = (g ? r.kpc + (size_t)w * a.n_types * 128 : S.kpc + jw * a.n_types * 128) + ty * 128 +
+                             (c - 2) * 64;
             dst[bh * pt.ncl] = th;
             if (cls) dstc[bh] = th;
             if (lane >= 11) {
@@ -278,8 +283,9 @@ __device__ __forceinline__ void cl_vadd(uint32_t (&V)[NP], uint32_t m0, uint32_t
 // same word): bit-sliced butterfly all-reduce, after which every lane holds
 // every plane and lane l reads replica l's count.  Added into dst[l].
 template <int NP>
-__device__ __noinline__ void cl_vflush(const uint32_t* Vin, int* dst) {
+__device__ __noinline__ void cl_vflush(uint4 lo, uint4 hi, int* dst) {  // by value: V stays in registers
     const int lane = threadIdx.x & 31;
+    const uint32_t Vin[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
     uint32_t E[NP + 5];
 #pragma unroll
     for (int b = 0; b < NP + 5; ++b) E[b] = b < NP ? Vin[b] : 0u;
@@ -302,29 +308,38 @@ __device__ __noinline__ void cl_vflush(const uint32_t* Vin, int* dst) {
 
 template <int NP>
 __device__ __forceinline__ void cl_flush(uint32_t (&V)[NP], int* dst) {
-    cl_vflush<NP>(V, dst);
+    if constexpr (NP == 8)
+        cl_vflush<NP>(make_uint4(V[0], V[1], V[2], V[3]), make_uint4(V[4], V[5], V[6], V[7]), dst);
+    else
+        cl_vflush<NP>(make_uint4(V[0], V[1], V[2], V[3]), make_uint4(0u, 0u, 0u, 0u), dst);
 #pragma unroll
     for (int b = 0; b < NP; ++b) V[b] = 0u;
 }
 
 // ------------------------------------------------------------ deferred tail
 
-// Resolve queue entries [base, base + n) (n <= 32) of the calling warp, one
-// per lane (plane_c5.cu c5_drain): Philox blocks 2.. of the entry's site,
+// Resolve queue entries [0, n) (n <= 32) of `queue`, one per lane
+// (plane_c5.cu c5_drain): Philox blocks 2.. of the entry's (site, word),
 // threshold planes 8.. of the word, late decisions applied to the stored word
-// and, when counting, the unsatisfied-bond correction.  Everything it reads
-// but the spin word is in shared memory.
+// and, when counting, the unsatisfied-bond correction.  Bit 30 of the entry's
+// site field selects the thread's second word (strides kcs / khs of its
+// threshold blocks).  Everything it reads but the spin word is in shared memory.
 template <int RULE>
 __device__ __noinline__ void cl_drain(uint32_t* spins_w, int logW, const int4* queue, const uint32_t* ks,
-                                      const uint4* kc2, const uint4* kh, int* loc, uint32_t grp4, int n,
-                                      uint32_t tlo, uint32_t thi, bool count) {
+                                      const uint4* kc2, const uint4* kh, int kcs, int khs, int* loc,
+                                      uint32_t grp4, int n, uint32_t tlo, uint32_t thi, bool count) {
     const int lane = threadIdx.x & 31;
     __syncwarp();
     int4 e = make_int4(0, 0, 0, 0);
     if (lane < n) e = queue[lane];
-    const uint32_t site = (uint32_t)e.x;
+    const uint32_t site = (uint32_t)e.x & 0x3fffffffu;
+    const int jw = (int)(((uint32_t)e.x >> 30) & 1u);
     uint32_t und = (uint32_t)e.y;
     const uint32_t c0 = (uint32_t)e.z, c1 = (uint32_t)e.w;
+    kc2 += jw * kcs;
+    kh += jw * khs;
+    loc += jw * 64;
+    grp4 += (uint32_t)jw << 4;
     uint32_t lt = 0u;
     const PhiloxT P = philox_t(tlo, thi, ks);
 #pragma unroll 1
@@ -348,7 +363,7 @@ __device__ __noinline__ void cl_drain(uint32_t* spins_w, int logW, const int4* q
         }
     }
     if (lt) {
-        uint32_t* p = spins_w + ((size_t)site << logW);
+        uint32_t* p = spins_w + ((size_t)site << logW) + jw;
         const uint32_t old = __ldcg(p);
         *p = RULE == 0 ? old ^ lt : old | lt;
         if (count) {
@@ -377,33 +392,51 @@ __device__ __forceinline__ void cl_slice(int b, int e, int rank, int C, int& lo,
     if (hi < lo) hi = lo;
 }
 
+// One row load of the thread's WPT words (an 8-byte access for a word pair).
+template <int WPT>
+__device__ __forceinline__ void cl_row(const uint32_t* p, uint32_t (&v)[WPT]) {
+    if constexpr (WPT == 2) {
+        const uint2 t = __ldcg(reinterpret_cast<const uint2*>(p));
+        v[0] = t.x;
+        v[1] = t.y;
+    } else {
+        v[0] = __ldcg(p);
+    }
+}
+
 // ------------------------------------------------------------ colour phase
 
 // One colour phase of this CTA: its chain-free slice [flo, fhi), then its
 // chain slice [qlo, qhi); fent / qent address the slices' staged entries by
-// site (null: the global table).
-template <int RULE, int NP>
-__device__ __forceinline__ void cl_phase(const PlaneArgs& a, const RoundArgs& r, const ClSmem& S, int w,
-                                         uint64_t t, bool count, int t30, int t31, uint32_t (&V)[NP],
-                                         uint32_t (&Q)[NP], int flo, int fhi, const int4* fent, int qlo,
+// site (null: the global table).  thread = (site, WPT words from word w0).
+template <int RULE, int NP, int WPT>
+__device__ __forceinline__ void cl_phase(const PlaneArgs& a, const RoundArgs& r, const ClSmem& S, int w0,
+                                         uint64_t t, bool count, int t30, int t31, uint32_t (&V)[WPT][NP],
+                                         uint32_t (&Q)[WPT][NP], int flo, int fhi, const int4* fent, int qlo,
                                          int qhi, const int4* qent) {
     constexpr int kFlushAt = NP == 8 ? 85 : 5;  // items between flushes: 3 bonds each, NP-bit counters
     const int lane = threadIdx.x & 31;
     const int logW = r.log_w;
-    const uint32_t act_w = a.active[w];
-    const uint32_t g0 = (uint32_t)(a.w_global0 + w) << 4;
+    uint32_t act_w[WPT];
+#pragma unroll
+    for (int j = 0; j < WPT; ++j) act_w[j] = a.active[w0 + j];
+    const uint32_t g0 = (uint32_t)(a.w_global0 + w0) << 4;
+    uint32_t gg[2 * WPT];  // Philox word 3 of the unconditional blocks
+#pragma unroll
+    for (int j = 0; j < WPT; ++j) { gg[2 * j] = g0 + 16u * j; gg[2 * j + 1] = (g0 + 16u * j) | 1u; }
     const uint32_t tlo = (uint32_t)t, thi = (uint32_t)(t >> 32);
     const PhiloxT P = philox_t(tlo, thi, a.pks);
-    uint32_t* base = a.spins + w;
+    uint32_t* base = a.spins + w0;
     int4* queue = S.queue + (threadIdx.x >> 5) * kClQCap;
+    const int kcs = a.n_types * 32, khs = ((a.kpw + 3) & ~3) >> 2;  // uint4 strides between the words' blocks
     const uint4* kc = reinterpret_cast<const uint4*>(S.kpc + t30 * 128);
     const uint4* kh = reinterpret_cast<const uint4*>(S.kp + a.ty[t30].kp_off);
     int qn = 0;
     int since = 0;
     // ---------------------------------------------------------- chain-free
     {
-        uint4 k2a, k2b, k3a, k3b;
-        if (RULE == 0) { k2a = kc[0]; k2b = kc[1]; k3a = kc[16]; k3b = kc[17]; }
+        uint4 k2a, k2b, k3a, k3b;  // one word per thread: its class-2/3 planes 0-7 stay in registers
+        if (RULE == 0 && WPT == 1) { k2a = kc[0]; k2b = kc[1]; k3a = kc[16]; k3b = kc[17]; }
         // software pipeline: the rows of the next site and the entry of the
         // one after it are in flight while the current site computes
         auto entry = [&](int st) -> int4 {
@@ -411,157 +444,219 @@ __device__ __forceinline__ void cl_phase(const PlaneArgs& a, const RoundArgs& r,
             if (st < fhi) v = fent ? fent[st] : __ldg(a.nbr4 + st);
             return v;
         };
-        auto rows = [&](int st, const int4& en, uint32_t& rs, uint32_t& r0, uint32_t& r1, uint32_t& r2) {
-            rs = 0u; r0 = 0u; r1 = 0u; r2 = 0u;
+        struct Rows { uint32_t s[WPT], x0[WPT], x1[WPT], x2[WPT]; };
+        auto rows = [&](int st, const int4& en) -> Rows {
+            Rows q;
+#pragma unroll
+            for (int j = 0; j < WPT; ++j) { q.s[j] = 0u; q.x0[j] = 0u; q.x1[j] = 0u; q.x2[j] = 0u; }
             if (st < fhi) {
-                rs = __ldcg(base + ((size_t)st << logW));
-                r0 = __ldcg(base + ((uint32_t)en.x & 0x7fffffffu));
-                r1 = __ldcg(base + ((uint32_t)en.y & 0x7fffffffu));
-                r2 = __ldcg(base + ((uint32_t)en.z & 0x7fffffffu));
+                cl_row<WPT>(base + ((size_t)st << logW), q.s);
+                cl_row<WPT>(base + ((uint32_t)en.x & 0x7fffffffu), q.x0);
+                cl_row<WPT>(base + ((uint32_t)en.y & 0x7fffffffu), q.x1);
+                cl_row<WPT>(base + ((uint32_t)en.z & 0x7fffffffu), q.x2);
             }
+            return q;
         };
         const int first = flo + (int)(threadIdx.x & ~31u) + lane;
         int4 en = entry(first);
-        uint32_t ns_, n0, n1, n2;
-        rows(first, en, ns_, n0, n1, n2);
+        Rows rn = rows(first, en);
         int4 en2 = entry(first + kClThreads);
         for (int b0 = flo + (int)(threadIdx.x & ~31u); b0 < fhi; b0 += kClThreads) {
             const int site = b0 + lane;
             const bool valid = site < fhi;
             const int4 e = en;
-            const uint32_t s = ns_, x0 = n0, x1 = n1, x2 = n2;
+            const Rows q = rn;
             en = en2;
-            rows(site + kClThreads, en, ns_, n0, n1, n2);
+            rn = rows(site + kClThreads, en);
             en2 = entry(site + 2 * kClThreads);
-            u32x4 r0, r1;
-            philox_plane2((uint32_t)site, g0, P, a.pks, r0, r1);
-            const uint32_t bb0 = x0 ^ (uint32_t)(e.x >> 31), bb1 = x1 ^ (uint32_t)(e.y >> 31),
-                           bb2 = x2 ^ (uint32_t)(e.z >> 31);
-            const uint32_t a0 = RULE == 0 ? ~(s ^ bb0) : bb0, a1 = RULE == 0 ? ~(s ^ bb1) : bb1,
-                           a2 = RULE == 0 ? ~(s ^ bb2) : bb2;
-            const uint32_t c0 = a0 ^ a1 ^ a2;
-            const uint32_t c1 = (a0 & a1) | (a2 & (a0 ^ a1));
-            const uint32_t act = valid ? act_w : 0u;
-            uint32_t u, lt = 0u, take, ns;
-            if (RULE == 0) {
-                u = c1 & act;  // classes 0, 1 (de <= 0): always taken
-                compare4_sel(c0, k2a, k3a, r0, u, lt);
-                compare4_sel(c0, k2b, k3b, r1, u, lt);
-                take = (~c1 & act) | lt;
-                ns = s ^ take;
-            } else {
-                const uint4 L = kh[kKPlanes];
-                const uint32_t always = sel(c1, sel(c0, L.w, L.z), sel(c0, L.y, L.x)) & act;
-                u = act & ~always;
-                const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+            u32x4 rr4[2 * WPT];
+            philox_planeN<2 * WPT>((uint32_t)site, gg, P, a.pks, rr4);
+            const uint32_t m0s = (uint32_t)(e.x >> 31), m1s = (uint32_t)(e.y >> 31), m2s = (uint32_t)(e.z >> 31);
+            uint32_t und[WPT], nsv[WPT], cl0[WPT], cl1[WPT];
 #pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    const uint4 T = kh[b];
-                    const uint32_t tb = sel(c1, sel(c0, T.w, T.z), sel(c0, T.y, T.x));
-                    lt |= u & tb & ~rr[b];
-                    u &= ~(tb ^ rr[b]);
-                }
-                take = (always | lt) & act;  // new spin +1 (undecided lanes provisionally -1)
-                ns = (s & ~act) | take;
-            }
-            if (count) {  // unsatisfied bonds after the update (all neighbours are colour 0)
-                uint32_t m0, m1;
+            for (int j = 0; j < WPT; ++j) {
+                const uint32_t s = q.s[j];
+                const uint32_t bb0 = q.x0[j] ^ m0s, bb1 = q.x1[j] ^ m1s, bb2 = q.x2[j] ^ m2s;
+                const uint32_t a0 = RULE == 0 ? ~(s ^ bb0) : bb0, a1 = RULE == 0 ? ~(s ^ bb1) : bb1,
+                               a2 = RULE == 0 ? ~(s ^ bb2) : bb2;
+                const uint32_t c0 = a0 ^ a1 ^ a2;
+                const uint32_t c1 = (a0 & a1) | (a2 & (a0 ^ a1));
+                const uint32_t act = valid ? act_w[j] : 0u;
+                const u32x4 r0 = rr4[2 * j], r1 = rr4[2 * j + 1];
+                uint32_t u, lt = 0u, take, ns;
                 if (RULE == 0) {
-                    m0 = ~(c0 ^ take) & act;
-                    m1 = ~(c1 ^ take) & act;
+                    u = c1 & act;  // classes 0, 1 (de <= 0): always taken
+                    if (WPT == 1) {
+                        compare4_sel(c0, k2a, k3a, r0, u, lt);
+                        compare4_sel(c0, k2b, k3b, r1, u, lt);
+                    } else {
+                        const uint4* kj = kc + j * kcs;
+                        compare4_sel(c0, kj[0], kj[16], r0, u, lt);
+                        compare4_sel(c0, kj[1], kj[17], r1, u, lt);
+                    }
+                    take = (~c1 & act) | lt;
+                    ns = s ^ take;
                 } else {
-                    const uint32_t u0 = ns ^ bb0, u1 = ns ^ bb1, u2 = ns ^ bb2;
-                    m0 = (u0 ^ u1 ^ u2) & act;
-                    m1 = ((u0 & u1) | (u2 & (u0 ^ u1))) & act;
+                    const uint4* kj = kh + j * khs;
+                    const uint4 L = kj[kKPlanes];
+                    const uint32_t always = sel(c1, sel(c0, L.w, L.z), sel(c0, L.y, L.x)) & act;
+                    u = act & ~always;
+                    const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        const uint4 T = kj[b];
+                        const uint32_t tb = sel(c1, sel(c0, T.w, T.z), sel(c0, T.y, T.x));
+                        lt |= u & tb & ~rr[b];
+                        u &= ~(tb ^ rr[b]);
+                    }
+                    take = (always | lt) & act;  // new spin +1 (undecided lanes provisionally -1)
+                    ns = (s & ~act) | take;
                 }
-                cl_vadd<2, NP>(V, m0, m1);
-                if (++since == kFlushAt) { cl_flush<NP>(V, S.loc); since = 0; }
+                if (count) {  // unsatisfied bonds after the update (all neighbours are colour 0)
+                    uint32_t m0, m1;
+                    if (RULE == 0) {
+                        m0 = ~(c0 ^ take) & act;
+                        m1 = ~(c1 ^ take) & act;
+                    } else {
+                        const uint32_t u0 = ns ^ bb0, u1 = ns ^ bb1, u2 = ns ^ bb2;
+                        m0 = (u0 ^ u1 ^ u2) & act;
+                        m1 = ((u0 & u1) | (u2 & (u0 ^ u1))) & act;
+                    }
+                    cl_vadd<2, NP>(V[j], m0, m1);
+                }
+                und[j] = u;
+                nsv[j] = ns;
+                cl0[j] = c0;
+                cl1[j] = c1;
             }
-            if (valid) base[(size_t)site << logW] = ns;
-            // deferred tail: sites with lanes still undecided after 8 planes
-            const uint32_t pend = __ballot_sync(0xffffffffu, u != 0u);
-            if (pend) {
-                if (u) queue[qn + __popc(pend & ((1u << lane) - 1u))] = make_int4(site, (int)u, (int)c0, (int)c1);
-                qn += __popc(pend);
-                if (qn >= 32) {
-                    qn -= 32;
-                    cl_drain<RULE>(base, logW, queue + qn, S.pks, kc, kh, S.loc, g0, 32, tlo, thi, count);
+            if (count && ++since == kFlushAt) {
+#pragma unroll
+                for (int j = 0; j < WPT; ++j) cl_flush<NP>(V[j], S.loc + j * 64);
+                since = 0;
+            }
+            if (valid) {
+                if constexpr (WPT == 2)
+                    *reinterpret_cast<uint2*>(base + ((size_t)site << logW)) = make_uint2(nsv[0], nsv[1]);
+                else
+                    base[(size_t)site << logW] = nsv[0];
+            }
+            // deferred tail: (site, word)s with lanes still undecided after 8 planes
+#pragma unroll
+            for (int j = 0; j < WPT; ++j) {
+                const uint32_t pend = __ballot_sync(0xffffffffu, und[j] != 0u);
+                if (pend) {
+                    if (und[j])
+                        queue[qn + __popc(pend & ((1u << lane) - 1u))] =
+                            make_int4((int)((uint32_t)site | ((uint32_t)j << 30)), (int)und[j], (int)cl0[j],
+                                      (int)cl1[j]);
+                    qn += __popc(pend);
+                    if (qn >= 32) {
+                        qn -= 32;
+                        cl_drain<RULE>(base, logW, queue + qn, S.pks, kc, kh, kcs, khs, S.loc, g0, 32, tlo, thi,
+                                       count);
+                    }
                 }
             }
         }
         if (count) CL_STAMP(g_cl_k, 9);
-        if (qn > 0) cl_drain<RULE>(base, logW, queue, S.pks, kc, kh, S.loc, g0, qn, tlo, thi, count);
+        if (qn > 0) cl_drain<RULE>(base, logW, queue, S.pks, kc, kh, kcs, khs, S.loc, g0, qn, tlo, thi, count);
         if (count) CL_STAMP(g_cl_k, 10);
     }
     // ---------------------------------------------------------- chain sites
     {
-        const uint32_t* kpb = S.kp + a.ty[t31].kp_off;
+        const int kpw4 = (a.kpw + 3) & ~3;
         // the last warps take the chain sites: they have the fewest chain-free sites
         for (int b0 = qlo + (int)((kClThreads - 32) - (threadIdx.x & ~31u)); b0 < qhi; b0 += kClThreads) {
             const int site = b0 + lane;
             const bool valid = site < qhi;
             int4 e = make_int4(0, 0, 0, 0);
-            uint32_t s = 0u, x0 = 0u, x1 = 0u, x2 = 0u, y = 0u;
+            uint32_t s[WPT], x0[WPT], x1[WPT], x2[WPT], y[WPT];
+#pragma unroll
+            for (int j = 0; j < WPT; ++j) { s[j] = 0u; x0[j] = 0u; x1[j] = 0u; x2[j] = 0u; y[j] = 0u; }
             if (valid) {
                 e = qent ? qent[site] : __ldg(a.nbr4 + site);
-                s = __ldcg(base + ((size_t)site << logW));
-                x0 = __ldcg(base + ((uint32_t)e.x & 0x7fffffffu));
-                x1 = __ldcg(base + ((uint32_t)e.y & 0x7fffffffu));
-                x2 = __ldcg(base + ((uint32_t)e.z & 0x7fffffffu));
-                y = __ldcg(base + (uint32_t)e.w);
+                cl_row<WPT>(base + ((size_t)site << logW), s);
+                cl_row<WPT>(base + ((uint32_t)e.x & 0x7fffffffu), x0);
+                cl_row<WPT>(base + ((uint32_t)e.y & 0x7fffffffu), x1);
+                cl_row<WPT>(base + ((uint32_t)e.z & 0x7fffffffu), x2);
+                cl_row<WPT>(base + (uint32_t)e.w, y);
             }
-            u32x4 r0, r1;
-            philox_plane2((uint32_t)site, g0, P, a.pks, r0, r1);
-            const uint32_t bb0 = x0 ^ (uint32_t)(e.x >> 31), bb1 = x1 ^ (uint32_t)(e.y >> 31),
-                           bb2 = x2 ^ (uint32_t)(e.z >> 31);
-            const uint32_t a0 = RULE == 0 ? ~(s ^ bb0) : bb0, a1 = RULE == 0 ? ~(s ^ bb1) : bb1,
-                           a2 = RULE == 0 ? ~(s ^ bb2) : bb2;
-            const uint32_t cb[3] = {a0 ^ a1 ^ a2, (a0 & a1) | (a2 & (a0 ^ a1)), RULE == 0 ? ~(s ^ y) : y};
-            const uint32_t act = valid ? act_w : 0u;
-            const uint32_t always = cl_mux8(cb, kpb + kKPlanes * 8) & act;
-            uint32_t u = act & ~always, lt = 0u;
-            cl_compare8(cb, kpb, 0, r0, u, lt);
-            cl_compare8(cb, kpb, 1, r1, u, lt);
+            u32x4 rr4[2 * WPT];
+            philox_planeN<2 * WPT>((uint32_t)site, gg, P, a.pks, rr4);
+            const uint32_t m0s = (uint32_t)(e.x >> 31), m1s = (uint32_t)(e.y >> 31), m2s = (uint32_t)(e.z >> 31);
+            uint32_t nsv[WPT];
+#pragma unroll
+            for (int j = 0; j < WPT; ++j) {
+                const uint32_t* kpb = S.kp + j * kpw4 + a.ty[t31].kp_off;
+                const uint32_t bb0 = x0[j] ^ m0s, bb1 = x1[j] ^ m1s, bb2 = x2[j] ^ m2s;
+                const uint32_t a0 = RULE == 0 ? ~(s[j] ^ bb0) : bb0, a1 = RULE == 0 ? ~(s[j] ^ bb1) : bb1,
+                               a2 = RULE == 0 ? ~(s[j] ^ bb2) : bb2;
+                const uint32_t cb[3] = {a0 ^ a1 ^ a2, (a0 & a1) | (a2 & (a0 ^ a1)),
+                                        RULE == 0 ? ~(s[j] ^ y[j]) : y[j]};
+                const uint32_t act = valid ? act_w[j] : 0u;
+                const uint32_t always = cl_mux8(cb, kpb + kKPlanes * 8) & act;
+                uint32_t u = act & ~always, lt = 0u;
+                cl_compare8(cb, kpb, 0, rr4[2 * j], u, lt);
+                cl_compare8(cb, kpb, 1, rr4[2 * j + 1], u, lt);
 #pragma unroll 1
-            for (int blk = 2; blk < 14; ++blk) {
-                if (!__any_sync(0xffffffffu, u)) break;
-                const u32x4 rb = philox_plane((uint32_t)site, g0 | (uint32_t)blk, P, S.pks);
-                cl_compare8(cb, kpb, blk, rb, u, lt);
-            }
-            const uint32_t take = (always | lt) & act;
-            const uint32_t ns = RULE == 0 ? s ^ take : (s & ~act) | take;
-            if (count) {
-                const uint32_t mq = (ns ^ y) & act;  // chain bond unsatisfied after the update
-                uint32_t m0, m1;
-                if (RULE == 0) {
-                    m0 = ~(cb[0] ^ take) & act;
-                    m1 = ~(cb[1] ^ take) & act;
-                } else {
-                    const uint32_t u0 = ns ^ bb0, u1 = ns ^ bb1, u2 = ns ^ bb2;
-                    m0 = (u0 ^ u1 ^ u2) & act;
-                    m1 = ((u0 & u1) | (u2 & (u0 ^ u1))) & act;
+                for (int blk = 2; blk < 14; ++blk) {
+                    if (!__any_sync(0xffffffffu, u)) break;
+                    const u32x4 rb = philox_plane((uint32_t)site, gg[2 * j] | (uint32_t)blk, P, S.pks);
+                    cl_compare8(cb, kpb, blk, rb, u, lt);
                 }
-                cl_vadd<2, NP>(V, m0, m1);
-                cl_vadd<1, NP>(Q, mq, 0u);
-                if (++since == kFlushAt) { cl_flush<NP>(V, S.loc); cl_flush<NP>(Q, S.loc + 32); since = 0; }
+                const uint32_t take = (always | lt) & act;
+                const uint32_t ns = RULE == 0 ? s[j] ^ take : (s[j] & ~act) | take;
+                if (count) {
+                    const uint32_t mq = (ns ^ y[j]) & act;  // chain bond unsatisfied after the update
+                    uint32_t m0, m1;
+                    if (RULE == 0) {
+                        m0 = ~(cb[0] ^ take) & act;
+                        m1 = ~(cb[1] ^ take) & act;
+                    } else {
+                        const uint32_t u0 = ns ^ bb0, u1 = ns ^ bb1, u2 = ns ^ bb2;
+                        m0 = (u0 ^ u1 ^ u2) & act;
+                        m1 = ((u0 & u1) | (u2 & (u0 ^ u1))) & act;
+                    }
+                    cl_vadd<2, NP>(V[j], m0, m1);
+                    cl_vadd<1, NP>(Q[j], mq, 0u);
+                }
+                nsv[j] = ns;
             }
-            if (valid) base[(size_t)site << logW] = ns;
+            if (count && ++since == kFlushAt) {
+#pragma unroll
+                for (int j = 0; j < WPT; ++j) {
+                    cl_flush<NP>(V[j], S.loc + j * 64);
+                    cl_flush<NP>(Q[j], S.loc + j * 64 + 32);
+                }
+                since = 0;
+            }
+            if (valid) {
+                if constexpr (WPT == 2)
+                    *reinterpret_cast<uint2*>(base + ((size_t)site << logW)) = make_uint2(nsv[0], nsv[1]);
+                else
+                    base[(size_t)site << logW] = nsv[0];
+            }
         }
     }
     if (count) CL_STAMP(g_cl_k, 11);
     if (count) {
-        cl_flush<NP>(V, S.loc);
-        if (qhi > qlo) cl_flush<NP>(Q, S.loc + 32);
+#pragma unroll
+        for (int j = 0; j < WPT; ++j) {
+            cl_flush<NP>(V[j], S.loc + j * 64);
+            if (qhi > qlo) cl_flush<NP>(Q[j], S.loc + j * 64 + 32);
+        }
     }
 }
 
 // ------------------------------------------------------------ the kernel
 
-// n_rounds whole rounds of run_2dpt (engine.cpp:121-216).  Grid = W clusters
-// of C CTAs (cluster dimension set at launch), all co-resident.  NP: planes
-// of the per-thread vertical bond counters (4 when a thread updates <= 5 sites
-// per phase, else 8).
-template <int RULE, int NP, int GROUP>
+// n_rounds whole rounds of run_2dpt (engine.cpp:121-216).  Grid = W / WPT
+// clusters (or groups) of C CTAs, all co-resident.  NP: planes of the
+// per-thread vertical bond counters (4 when a thread updates <= 5 sites per
+// phase, else 8); GROUP: software word barrier instead of clusters; WPT: words
+// per thread (2: the word pair shares the site's Philox products and row
+// sectors, as in plane_c5.cu).
+template <int RULE, int NP, int GROUP, int WPT>
 __global__ void __launch_bounds__(kClThreads, 1)
 plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constant__ RoundArgs r) {
     cg::cluster_group cluster = cg::this_cluster();
@@ -572,11 +667,12 @@ plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
         return;
     }
     const int rank = GROUP ? (int)(blockIdx.x % C) : (int)cluster.block_rank();
-    const int w = blockIdx.x / C;
-    unsigned int* gbar = r.cl_bar + w * 32;  // group mode: the word's barrier counter (own 128-byte line)
+    const int wq = blockIdx.x / C;       // the CTA's word group
+    const int w0 = wq * WPT;             // its first word
+    unsigned int* gbar = r.cl_bar + wq * 32;  // group mode: the word group's barrier counter (own 128-byte line)
     unsigned int gtarget = 0;
     const int tid = threadIdx.x, lane = tid & 31;
-    const ClSmem S = cl_smem(a, r);
+    const ClSmem S = cl_smem(a, r, WPT);
     const RoundSmem s = S.rs;
     const int np = r.I * (r.J > 1 ? r.J - 1 : 0);
     const int nb = (r.I > 1 ? r.I - 1 : 0) * r.J;
@@ -603,7 +699,7 @@ plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
         qent[0] = S.stage + off_q0 - qlo[0];
         qent[1] = S.stage + off_q1 - qlo[1];
     }
-    // ---- launch prologue: staged entries (TMA), tables, labels, this word's planes
+    // ---- launch prologue: staged entries (TMA), tables, labels, this word group's planes
     if (tid == 0) {
         mbar_init(S.mbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -616,7 +712,7 @@ plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
         if (qhi[0] > qlo[0]) tma_bulk_g2s(S.stage + off_q0, a.nbr4 + qlo[0], (uint32_t)(qhi[0] - qlo[0]) * 16u, S.mbar);
         if (qhi[1] > qlo[1]) tma_bulk_g2s(S.stage + off_q1, a.nbr4 + qlo[1], (uint32_t)(qhi[1] - qlo[1]) * 16u, S.mbar);
     }
-    for (int m = tid; m < 128; m += blockDim.x) S.loc[m] = 0;  // loc + tot
+    for (int m = tid; m < 128 * WPT; m += blockDim.x) S.loc[m] = 0;  // loc + tot
     if (tid < 20) S.pks[tid] = a.pks[tid];
     for (int m = tid; m < r.I; m += blockDim.x) S.betas[m] = r.betas[m];
     for (int m = tid; m < r.J; m += blockDim.x) S.pens[m] = r.pens[m];
@@ -627,7 +723,7 @@ plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
     }
     round_load_labels(r, s);
     __syncthreads();
-    cl_build_planes(a, r, s.state, w, S, false);
+    cl_build_planes(a, r, s.state, w0, WPT, S, false);
     if (r.cl_stage) mbar_wait(S.mbar, 0);
     __syncthreads();
     int* tot0 = S.tot;
@@ -635,34 +731,39 @@ plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
         cluster.sync();  // every CTA of the cluster has zeroed its totals
         tot0 = cluster.map_shared_rank(S.tot, 0);
     }
-    uint32_t V[NP], Q[NP];
+    uint32_t V[WPT][NP], Q[WPT][NP];
 #pragma unroll
-    for (int b = 0; b < NP; ++b) { V[b] = 0u; Q[b] = 0u; }
+    for (int j = 0; j < WPT; ++j) {
+#pragma unroll
+        for (int b = 0; b < NP; ++b) { V[j][b] = 0u; Q[j][b] = 0u; }
+    }
     uint64_t swap_base = r.swap_base0;
+    const int n_groups = a.W / WPT;
     for (int k = 0; k < r.n_rounds; ++k) {
         const int64_t round = r.round0 + k;
         unsigned long long* xw = r.cl_x + (size_t)(k & 1) * nrep;  // exchange words of this parity
         const unsigned long long tag = (unsigned long long)((k + 1) & 0xffff);
+        int* gt = r.cl_gtot + ((size_t)(k & 1) * n_groups + wq) * 64 * WPT;  // group mode: this group's totals
         CL_SETK(k);
         CL_STAMP(k, 0);
         for (int sw = 0; sw < r.sps; ++sw) {
             const uint64_t t = (uint64_t)((round - 1) * r.sps + sw);
             const bool count = (sw == r.sps - 1);
-            cl_phase<RULE, NP>(a, r, S, w, t, false, t30, t31, V, Q, flo[0], fhi[0], fent[0], qlo[0], qhi[0],
-                               qent[0]);
+            cl_phase<RULE, NP, WPT>(a, r, S, w0, t, false, t30, t31, V, Q, flo[0], fhi[0], fent[0], qlo[0],
+                                    qhi[0], qent[0]);
             CL_STAMP(k, 1);
             if (GROUP) cl_group_sync(gbar, gtarget += (unsigned)C);
             else cluster.sync();
             CL_STAMP(k, 2);
-            cl_phase<RULE, NP>(a, r, S, w, t, count, t30, t31, V, Q, flo[1], fhi[1], fent[1], qlo[1], qhi[1],
-                               qent[1]);
+            cl_phase<RULE, NP, WPT>(a, r, S, w0, t, count, t30, t31, V, Q, flo[1], fhi[1], fent[1], qlo[1],
+                                    qhi[1], qent[1]);
             CL_STAMP(k, 3);
             if (count) {  // word totals through distributed shared memory (group mode: global atomics)
                 __syncthreads();
-                if (tid < 64) {
+                if (tid < 64 * WPT) {
                     const int v = S.loc[tid];
                     if (v) {
-                        atomicAdd(GROUP ? r.cl_gtot + ((size_t)(k & 1) * a.W + w) * 64 + tid : tot0 + tid, v);
+                        atomicAdd(GROUP ? gt + tid : tot0 + tid, v);
                         S.loc[tid] = 0;
                     }
                 }
@@ -671,22 +772,22 @@ plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
             else cluster.sync();
             CL_STAMP(k, 4);
         }
-        // ---- (f, g) exchange: the leader publishes the word's counts, tagged with the round
-        if (rank == 0 && tid < 32) {
+        // ---- (f, g) exchange: the leader publishes the words' counts, tagged with the round
+        if (rank == 0 && tid < 32 * WPT) {
+            const int jw = tid >> 5, l = tid & 31;
             unsigned long long cc, cq;
             if (GROUP) {
-                int* gt = r.cl_gtot + ((size_t)(k & 1) * a.W + w) * 64;
-                cc = (unsigned long long)(uint32_t)__ldcg(gt + tid);
-                cq = (unsigned long long)(uint32_t)__ldcg(gt + 32 + tid);
-                gt[tid] = 0;       // this parity's totals are next added to two rounds on
-                gt[32 + tid] = 0;
+                cc = (unsigned long long)(uint32_t)__ldcg(gt + jw * 64 + l);
+                cq = (unsigned long long)(uint32_t)__ldcg(gt + jw * 64 + 32 + l);
+                gt[jw * 64 + l] = 0;       // this parity's totals are next added to two rounds on
+                gt[jw * 64 + 32 + l] = 0;
             } else {
-                cc = (unsigned long long)(uint32_t)S.tot[tid];
-                cq = (unsigned long long)(uint32_t)S.tot[32 + tid];
-                S.tot[tid] = 0;
-                S.tot[32 + tid] = 0;
+                cc = (unsigned long long)(uint32_t)S.tot[jw * 64 + l];
+                cq = (unsigned long long)(uint32_t)S.tot[jw * 64 + 32 + l];
+                S.tot[jw * 64 + l] = 0;
+                S.tot[jw * 64 + 32 + l] = 0;
             }
-            st_relaxed_gpu(xw + w * 32 + tid, tag << 48 | cq << 24 | cc);
+            st_relaxed_gpu(xw + (w0 + jw) * 32 + l, tag << 48 | cq << 24 | cc);
         }
         // the swap uniforms do not depend on the energies: drawn while the words arrive
         const int n_att = (int)round_attempts(r.I, r.J, round);
@@ -718,7 +819,7 @@ plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
         const int tg = s.slot[r.R - 1];
         CL_STAMP(k, 6);
         if (blockIdx.x == 0) {
-            if (tid == 0) {  // record, engine.cpp:189-208 (digest added atomically by the target's cluster)
+            if (tid == 0) {  // record, engine.cpp:189-208 (digest added atomically by the target's group)
                 TgRecordDev* rec = reinterpret_cast<TgRecordDev*>(r.rec) + k;
                 rec->round = round;
                 rec->sweep_count = round * r.sps;
@@ -743,17 +844,17 @@ plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
                 for (int q = tid; q < nb; q += blockDim.x) r.acc_b[q] += S.acc[np + q];
             }
         }
-        // ---- threshold planes of this word for the new labels
-        cl_build_planes(a, r, s.state, w, S, rank == 0 && k == r.n_rounds - 1);
+        // ---- threshold planes of this CTA's words for the new labels
+        cl_build_planes(a, r, s.state, w0, WPT, S, rank == 0 && k == r.n_rounds - 1);
         CL_STAMP(k, 7);
-        // ---- target digest / snapshot: the target's cluster, each CTA over its own sites
-        if ((r.rec_flags & 3) && (tg >> 5) == w) {
+        // ---- target digest / snapshot: the target's word group, each CTA over its own sites
+        if ((r.rec_flags & 3) && (tg >> 5) / WPT == wq) {
             uint64_t dsum = 0;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int lo = q < 2 ? flo[q & 1] : qlo[q & 1], hi = q < 2 ? fhi[q & 1] : qhi[q & 1];
                 for (int i = lo + tid; i < hi; i += blockDim.x) {
-                    const uint32_t wv = __ldcg(a.spins + (size_t)i * a.W + w);
+                    const uint32_t wv = __ldcg(a.spins + (size_t)i * a.W + (tg >> 5));
                     const int ci = r.perm[i];
                     const bool up = (wv >> (tg & 31)) & 1u;
                     if (r.rec_flags & 2) r.rec_states[(size_t)k * a.n + ci] = up ? 1 : -1;
@@ -775,20 +876,23 @@ plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
     if (!GROUP) cluster.sync();  // no CTA exits while a peer may still address its shared memory
 }
 
-#define TG_CL_INST(R, P, G) \
-    template __global__ void plane_cl_rounds_kernel<R, P, G>(const __grid_constant__ PlaneArgs, \
-                                                             const __grid_constant__ RoundArgs);
-TG_CL_INST(0, 4, 0) TG_CL_INST(1, 4, 0) TG_CL_INST(0, 8, 0) TG_CL_INST(1, 8, 0)
-TG_CL_INST(0, 4, 1) TG_CL_INST(1, 4, 1) TG_CL_INST(0, 8, 1) TG_CL_INST(1, 8, 1)
+#define TG_CL_INST(R, P, G, T) \
+    template __global__ void plane_cl_rounds_kernel<R, P, G, T>(const __grid_constant__ PlaneArgs, \
+                                                                const __grid_constant__ RoundArgs);
+TG_CL_INST(0, 4, 0, 1) TG_CL_INST(1, 4, 0, 1) TG_CL_INST(0, 8, 0, 1) TG_CL_INST(1, 8, 0, 1)
+TG_CL_INST(0, 4, 1, 1) TG_CL_INST(1, 4, 1, 1) TG_CL_INST(0, 8, 1, 1) TG_CL_INST(1, 8, 1, 1)
+TG_CL_INST(0, 4, 1, 2) TG_CL_INST(1, 4, 1, 2) TG_CL_INST(0, 8, 1, 2) TG_CL_INST(1, 8, 1, 2)
 #undef TG_CL_INST
 
-void* plane_cl_fn(int rule, int small, int group) {
-    if (group) {
-        if (small) return rule ? (void*)plane_cl_rounds_kernel<1, 4, 1> : (void*)plane_cl_rounds_kernel<0, 4, 1>;
-        return rule ? (void*)plane_cl_rounds_kernel<1, 8, 1> : (void*)plane_cl_rounds_kernel<0, 8, 1>;
-    }
-    if (small) return rule ? (void*)plane_cl_rounds_kernel<1, 4, 0> : (void*)plane_cl_rounds_kernel<0, 4, 0>;
-    return rule ? (void*)plane_cl_rounds_kernel<1, 8, 0> : (void*)plane_cl_rounds_kernel<0, 8, 0>;
+// small: 4-plane counters; group: software word barrier; pair: two words per thread (group mode only)
+void* plane_cl_fn(int rule, int small, int group, int pair) {
+#define TG_CL_PICK(G, T)                                                                               \
+    (small ? (rule ? (void*)plane_cl_rounds_kernel<1, 4, G, T> : (void*)plane_cl_rounds_kernel<0, 4, G, T>) \
+           : (rule ? (void*)plane_cl_rounds_kernel<1, 8, G, T> : (void*)plane_cl_rounds_kernel<0, 8, G, T>))
+    if (group && pair) return TG_CL_PICK(1, 2);
+    if (group) return TG_CL_PICK(1, 1);
+    return TG_CL_PICK(0, 1);
+#undef TG_CL_PICK
 }
 
 }  // namespace tg

@@ -1,11 +1,14 @@
-"""GPU parity of the cluster-per-word fused round kernel (plane_cl.cu): one
-thread-block cluster per 32-replica word, cluster barriers per colour phase,
-word counts reduced through distributed shared memory, one release-flag
-(f, g) exchange per round, neighbour entries staged by TMA bulk copies.  It is
-the default single-GPU path of both rules for config-5 instances (cost degree
-3, chain degree 0/1, 2 colours) up to 2^16 sites; every case is compared bit
-for bit with the oracle (f, g, feasibility, digests, final grid, counters)
-and checks which kernel ran."""
+"""GPU parity of the word-local fused round kernel (plane_cl.cu): the CTAs are
+partitioned by 32-replica word (or word pair), a colour phase ends with a
+barrier among the word's CTAs only, one tagged-word (f, g) exchange per round,
+neighbour entries staged by TMA bulk copies, threshold planes per CTA in
+shared memory.  Three variants share the code: hardware thread-block clusters
+(cluster barrier, word counts reduced through distributed shared memory), and
+the "group" launch (software word barrier on all SMs) with one word or a word
+pair per thread.  It is the default single-GPU path of both rules for config-5
+instances (cost degree 3, chain degree 0/1, 2 colours) up to 2^18 sites; every
+case is compared bit for bit with the oracle (f, g, feasibility, digests,
+final grid, counters) and checks which kernel ran."""
 import numpy as np
 import pytest
 
@@ -20,12 +23,14 @@ RULES = ["metropolis", "heat_bath"]
 KERNEL = "plane_cl_rounds_kernel"
 
 
-@pytest.fixture(autouse=True, params=["cluster", "group"])
+@pytest.fixture(autouse=True, params=["cluster", "group", "pair"])
 def _mode(request, monkeypatch):
     # cluster: hardware clusters (cluster barrier, DSMEM totals); group: the same
     # kernel as an ordinary cooperative launch, G CTAs per word behind a
-    # software word barrier, totals by global atomics (the default above 2^14)
-    monkeypatch.setenv("TG_PLANE_CL_MODE", request.param)
+    # software word barrier, totals by global atomics (the default up to 2^15
+    # sites); pair: group mode with two words per thread (2^15 .. 2^18)
+    monkeypatch.setenv("TG_PLANE_CL_MODE", "cluster" if request.param == "cluster" else "group")
+    monkeypatch.setenv("TG_PLANE_CL_PAIR", "1" if request.param == "pair" else "0")
 
 
 # (I, J) -> words per site = clusters: 32 -> 1, 64 -> 2, 96 -> 4 (one padded
