@@ -42,7 +42,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=1 << 20, help="physical spins")
-    ap.add_argument("--rounds", type=int, default=100, help="rounds per step")
+    ap.add_argument("--rounds", type=int, default=None,
+                    help="rounds per step (default: 1000 for c5 -- one launch, one record ring; 20 for the "
+                         "float workloads)")
     ap.add_argument("--sps", type=int, default=1, help="sweeps per swap")
     ap.add_argument("--rule", default="metropolis")
     ap.add_argument("--engine", default="plane")
@@ -52,7 +54,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-heat-bath", action="store_true", help="skip the heat-bath sub-record")
     ap.add_argument("--cpu-sweeps", type=int, default=16, help="marginal sweeps of the CPU sample")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.rounds is None:
+        args.rounds = 1000 if args.workload == "c5" else 20
+    return args
 
 
 def workload(n, kind="c5"):

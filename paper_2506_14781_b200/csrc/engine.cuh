@@ -314,38 +314,87 @@ TG_HD double dexp(double x) {
 // Attempt k of the round: P phase rows i ascending, pairs p = even, even+2..
 // (engine.cpp:148-167); beta phase columns j ascending, pairs b = even, ..
 // (engine.cpp:168-187).  One swap-stream draw per attempt in that order (u).
-// Returns 1 on accept and reports the two slots and the counter index.
-TG_HD int swap_attempt_u(int I, int J, const double* betas, const double* pens, int64_t round,
-                         int k, const double* f_all, const double* g_all, const int32_t* slot_state,
-                         double u, int& slot_a, int& slot_b, int& counter, int& is_p) {
+// Split in two so that the fused kernels can do everything that does not
+// depend on this round's energies (slots, labels, coefficients, the draw)
+// before the energies arrive: swap_prepare, then swap_decide.
+struct SwapPrep {
+    int slot_a, slot_b, counter, is_p;
+    int sa, sb;      // states in the two slots before the attempt
+    double c;        // P phase: beta_i (P_{p+1} - P_p); beta phase: beta_{b+1} - beta_b
+    double pj;       // beta phase: the column's penalty
+    double u;
+};
+
+TG_HD SwapPrep swap_prepare(int I, int J, const double* betas, const double* pens, int64_t round, int k,
+                            const int32_t* slot_state, double u) {
+    SwapPrep p;
     int even, dp, db;
     round_phase(I, J, round, even, dp, db);
-    double x;
+    p.u = u;
     if (dp) {
         const int per = pairs_in(J, even);
         const int i = k / per;
-        const int p = even + 2 * (k % per);
-        slot_a = i * J + p;
-        slot_b = slot_a + 1;
-        const int a = slot_state[slot_a], b = slot_state[slot_b];
-        x = betas[i] * (pens[p + 1] - pens[p]) * (g_all[b] - g_all[a]);
-        counter = i * (J - 1) + p;
-        is_p = 1;
+        const int q = even + 2 * (k % per);
+        p.slot_a = i * J + q;
+        p.slot_b = p.slot_a + 1;
+        p.c = betas[i] * (pens[q + 1] - pens[q]);
+        p.pj = 0.0;
+        p.counter = i * (J - 1) + q;
+        p.is_p = 1;
     } else {
         const int per = pairs_in(I, even);
         const int j = k / per;
         const int b = even + 2 * (k % per);
-        slot_a = b * J + j;
-        slot_b = (b + 1) * J + j;
-        const int lo = slot_state[slot_a], hi = slot_state[slot_b];
-        const double pj = pens[j];
-        const double e_lo = dadd_mul(f_all[lo], pj, g_all[lo]);
-        const double e_hi = dadd_mul(f_all[hi], pj, g_all[hi]);
-        x = (betas[b + 1] - betas[b]) * (e_hi - e_lo);
-        counter = b * J + j;
-        is_p = 0;
+        p.slot_a = b * J + j;
+        p.slot_b = (b + 1) * J + j;
+        p.pj = pens[j];
+        p.c = betas[b + 1] - betas[b];
+        p.counter = b * J + j;
+        p.is_p = 0;
     }
+    p.sa = slot_state[p.slot_a];
+    p.sb = slot_state[p.slot_b];
+    return p;
+}
+
+// Accept (1) or reject (0): x >= 0 or u < exp(x), the reference expressions
+// in the reference's operation order.
+TG_HD int swap_decide(const SwapPrep& p, const double* f_all, const double* g_all) {
+    double x;
+    if (p.is_p) {
+        x = p.c * (g_all[p.sb] - g_all[p.sa]);
+    } else {
+        const double e_lo = dadd_mul(f_all[p.sa], p.pj, g_all[p.sa]);
+        const double e_hi = dadd_mul(f_all[p.sb], p.pj, g_all[p.sb]);
+        x = p.c * (e_hi - e_lo);
+    }
+    const double u = p.u;
+#if defined(__CUDA_ARCH__)
+    // Certified shortcut around the FP64 exp (a long dependent chain in a
+    // phase that is one attempt per thread): an FP32 exp bounds exp(x) within
+    // 1e-4 relative for x in [-100, 0) (input rounding |x| 2^-24, ex2.approx
+    // 2^-22); only a uniform inside that band (probability ~2e-4) takes the
+    // FP64 expression, so the decisions are the FP64 ones.
+    if (x >= 0.0) return 1;
+    if (x < -100.0) return (u > 0.0) ? 0 : (u < dexp(x) ? 1 : 0);  // exp(x) < 2^-53 <= every u > 0
+    const double e32 = (double)__expf((float)x);
+    if (u < e32 * (1.0 - 1e-4)) return 1;
+    if (u > e32 * (1.0 + 1e-4)) return 0;
+    return u < dexp(x) ? 1 : 0;
+#else
     return (x >= 0.0 || u < dexp(x)) ? 1 : 0;
+#endif
+}
+
+TG_HD int swap_attempt_u(int I, int J, const double* betas, const double* pens, int64_t round,
+                         int k, const double* f_all, const double* g_all, const int32_t* slot_state,
+                         double u, int& slot_a, int& slot_b, int& counter, int& is_p) {
+    const SwapPrep p = swap_prepare(I, J, betas, pens, round, k, slot_state, u);
+    slot_a = p.slot_a;
+    slot_b = p.slot_b;
+    counter = p.counter;
+    is_p = p.is_p;
+    return swap_decide(p, f_all, g_all);
 }
 
 // The attempt's uniform: draw swap_base + k of the swap stream.

@@ -789,10 +789,14 @@ plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
             }
             st_relaxed_gpu(xw + (w0 + jw) * 32 + l, tag << 48 | cq << 24 | cc);
         }
-        // the swap uniforms do not depend on the energies: drawn while the words arrive
+        // everything of this thread's swap attempt that does not depend on the energies (slots,
+        // labels, coefficients, the draw) is done while the words arrive
         const int n_att = (int)round_attempts(r.I, r.J, round);
-        double u_swap = 0.0;
-        if (tid < n_att) u_swap = swap_uniform(r.swap_seed, swap_base, tid);
+        SwapPrep sp{};
+        if (tid < n_att)
+            sp = swap_prepare(r.I, r.J, S.betas, S.pens, round, tid, s.slot,
+                              swap_uniform(r.swap_seed, swap_base, tid));
+        CL_STAMP(k, 13);
         for (int m = tid; m < r.R; m += blockDim.x) {
             unsigned long long v;
             do { v = ld_relaxed_gpu(xw + m); } while ((v >> 48) != tag);
@@ -803,18 +807,20 @@ plane_cl_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
         CL_STAMP(k, 5);
         // ---- swap phase (engine.cpp:148-187), replayed identically by every CTA
         for (int q = tid; q < n_att; q += blockDim.x) {
-            int sa, sb, ctr, is_p;
-            const double u = q == tid ? u_swap : swap_uniform(r.swap_seed, swap_base, q);
-            if (swap_attempt_u(r.I, r.J, S.betas, S.pens, round, q, s.f, s.g, s.slot, u, sa, sb, ctr, is_p)) {
-                const int xa = s.slot[sa], xb = s.slot[sb];
-                s.slot[sa] = xb;
-                s.slot[sb] = xa;
-                s.state[xb] = sa;
-                s.state[xa] = sb;
-                S.acc[is_p ? ctr : np + ctr] += 1;  // one attempt per counter and round
+            if (q != tid)
+                sp = swap_prepare(r.I, r.J, S.betas, S.pens, round, q, s.slot,
+                                  swap_uniform(r.swap_seed, swap_base, q));
+            if (swap_decide(sp, s.f, s.g)) {
+                // the attempts of a round touch disjoint slot pairs
+                s.slot[sp.slot_a] = sp.sb;
+                s.slot[sp.slot_b] = sp.sa;
+                s.state[sp.sb] = sp.slot_a;
+                s.state[sp.sa] = sp.slot_b;
+                S.acc[sp.is_p ? sp.counter : np + sp.counter] += 1;  // one attempt per counter and round
             }
         }
         swap_base += (uint64_t)n_att;
+        CL_STAMP(k, 12);
         __syncthreads();
         const int tg = s.slot[r.R - 1];
         CL_STAMP(k, 6);

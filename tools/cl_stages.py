@@ -35,6 +35,8 @@ names = [(0, 1, "phase 0 items"), (1, 2, "phase 0 cluster barrier"), (2, 3, "pha
          (3, 4, "DSMEM totals + cluster barrier"), (4, 5, "publish + flag wait"),
          (2, 9, "  phase 1: chain-free loop"), (9, 10, "  phase 1: final drain"),
          (10, 11, "  phase 1: chain loop"), (11, 3, "  phase 1: counter flush"),
+         (4, 13, "  publish + swap uniform"), (13, 5, "  poll + CTA barrier"),
+         (5, 12, "  swap attempts (thread 0)"), (12, 6, "  CTA barrier after swaps"),
          (5, 6, "energies + swap replay"), (6, 7, "records + threshold planes"), (7, 8, "digest")]
 for a, b, name in names:
     print(f"N={n} {name:<34s} {np.mean(t[:, b] - t[:, a]) / 1e3:8.2f} us")
