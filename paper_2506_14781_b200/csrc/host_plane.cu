@@ -365,7 +365,8 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
     c.fused_c5 = 0;
     {
         bool ok = c.fused_tpw && c.tpw_fast && c.n_colors == 2 &&
-                  c.W >= 2 && c.n_types <= 2 && c.d_nbr4.p != nullptr;
+                  c.W >= 2 && c.n_types <= 2 && c.d_nbr4.p != nullptr &&
+                  (long long)n * c.W < (1ll << 30);  // 32-bit byte offsets of the rows
         int nfree_type = 0;
         for (const auto& t : types) nfree_type += t.dq == 0;
         ok = ok && nfree_type <= 1;

@@ -233,8 +233,17 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
     K.thi = (uint32_t)(t >> 32);
     K.P = philox_t(K.tlo, K.thi, a.pks);
     const char* base = reinterpret_cast<const char*>(a.spins + w0);
-    auto row = [&](uint32_t off) -> uint2 {   // off: word offset of a row (index << logW)
-        return *reinterpret_cast<const uint2*>(base + (size_t)off * 4u);
+#ifndef TG_ADDR32
+#define TG_ADDR32 1
+#endif
+    // off: word offset of a row (index << logW) below 2^30 (host check), flag
+    // bits 30-31 of an nbr4 entry fall off the 32-bit byte offset
+    auto row = [&](uint32_t off) -> uint2 {
+#if TG_ADDR32
+        return *reinterpret_cast<const uint2*>(base + (uint32_t)(off << 2));
+#else
+        return *reinterpret_cast<const uint2*>(base + (size_t)(off & 0x7fffffffu) * 4u);
+#endif
     };
     int qn = 0;
     // ---------------------------------------------------------- chain-free
@@ -254,9 +263,9 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
             const int st = cs + i * S + sl;
             if (i < n_it && st < cf) {
                 q.s = row((uint32_t)st << logW);
-                q.x0 = row((uint32_t)e.x & 0x7fffffffu);
-                q.x1 = row((uint32_t)e.y & 0x7fffffffu);
-                q.x2 = row((uint32_t)e.z & 0x7fffffffu);
+                q.x0 = row((uint32_t)e.x);
+                q.x1 = row((uint32_t)e.y);
+                q.x2 = row((uint32_t)e.z);
             }
             return q;
         };
@@ -294,9 +303,15 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
                 uint32_t u, lt = 0u, take;
                 if (RULE == 0) {
                     u = c1 & act;  // classes 0, 1 (de < 0): always taken
+#if TG_CMP8
+                    compare8_sel(c0, thr[j], thr[W + j], thr[2 * W + j], thr[3 * W + j], r[2 * j], r[2 * j + 1],
+                                 u, u, lt);
+                    take = act & (~c1 | lt);
+#else
                     compare4_sel(c0, thr[j], thr[2 * W + j], r[2 * j], u, lt);
                     compare4_sel(c0, thr[W + j], thr[3 * W + j], r[2 * j + 1], u, lt);
                     take = (~c1 & act) | lt;
+#endif
                     ns[j] = sj ^ take;
                 } else {
                     const uint4* tj = thr + j;
@@ -305,6 +320,15 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
                     u = act & ~always;
                     const uint32_t rr[8] = {r[2 * j].x, r[2 * j].y, r[2 * j].z, r[2 * j].w,
                                             r[2 * j + 1].x, r[2 * j + 1].y, r[2 * j + 1].z, r[2 * j + 1].w};
+#if TG_CMP8
+                    uint32_t tb[8];
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        const uint4 T = tj[b * W];
+                        tb[b] = sel(c1, sel(c0, T.w, T.z), sel(c0, T.y, T.x));
+                    }
+                    compare8(tb, rr, u, u, lt);  // lt beyond u: covered by `always` / masked by act
+#else
 #pragma unroll
                     for (int b = 0; b < 8; ++b) {
                         const uint4 T = tj[b * W];
@@ -312,6 +336,7 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
                         lt |= u & tb & ~rr[b];
                         u &= ~(tb ^ rr[b]);
                     }
+#endif
                     take = (always | lt) & act;  // new spin +1 (undecided lanes provisionally -1)
                     ns[j] = (sj & ~act) | take;
                 }
@@ -333,7 +358,7 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
                 cl1[j] = c1;
             }
             if (valid)
-                *reinterpret_cast<uint2*>(const_cast<char*>(base) + (size_t)(site << logW) * 4u) =
+                *reinterpret_cast<uint2*>(const_cast<char*>(base) + (uint32_t)(site << (logW + 2))) =
                     make_uint2(ns[0], ns[1]);
             // deferred tail: pairs with lanes still undecided after 8 planes
 #pragma unroll
@@ -379,9 +404,9 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
             if (valid) {
                 e = __ldg(a.nbr4 + site);
                 s = row(site << logW);
-                x0 = row((uint32_t)e.x & 0x7fffffffu);
-                x1 = row((uint32_t)e.y & 0x7fffffffu);
-                x2 = row((uint32_t)e.z & 0x7fffffffu);
+                x0 = row((uint32_t)e.x);
+                x1 = row((uint32_t)e.y);
+                x2 = row((uint32_t)e.z);
                 y = row((uint32_t)e.w);
             }
             u32x4 r[4];
@@ -401,8 +426,19 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
                 const uint32_t* kpb = j ? kpb1 : kpb0;
                 const uint32_t always = mux_tree<3>(cb, kpb + kKPlanes * 8) & act;
                 uint32_t u = act & ~always, lt = 0u;
+#if TG_CMP8
+                {
+                    const uint32_t rr[8] = {r[2 * j].x, r[2 * j].y, r[2 * j].z, r[2 * j].w,
+                                            r[2 * j + 1].x, r[2 * j + 1].y, r[2 * j + 1].z, r[2 * j + 1].w};
+                    uint32_t tb[8];
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) tb[b] = mux_tree<3>(cb, kpb + b * 8);
+                    compare8(tb, rr, u, u, lt);  // lt beyond u: covered by `always` / masked by act
+                }
+#else
                 compare_block<3>(cb, kpb, 8, 0, r[2 * j], u, lt);
                 compare_block<3>(cb, kpb, 8, 1, r[2 * j + 1], u, lt);
+#endif
 #pragma unroll 1
                 for (int blk = 2; blk < 14; ++blk) {
                     if (!__any_sync(0xffffffffu, u)) break;
@@ -432,7 +468,7 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
                 }
             }
             if (valid)
-                *reinterpret_cast<uint2*>(const_cast<char*>(base) + (size_t)(site << logW) * 4u) =
+                *reinterpret_cast<uint2*>(const_cast<char*>(base) + (uint32_t)(site << (logW + 2))) =
                     make_uint2(ns[0], ns[1]);
         }
         if (count) {

@@ -427,6 +427,11 @@ __device__ __forceinline__ void cl_phase(const PlaneArgs& a, const RoundArgs& r,
     const uint32_t tlo = (uint32_t)t, thi = (uint32_t)(t >> 32);
     const PhiloxT P = philox_t(tlo, thi, a.pks);
     uint32_t* base = a.spins + w0;
+    // row at word offset `off` (< 2^30: n <= 2^18 sites): 32-bit byte offset,
+    // the flag bits 30-31 of an nbr4 entry fall off the shift
+    auto rowp = [&](uint32_t off) -> uint32_t* {
+        return reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(base) + (uint32_t)(off << 2));
+    };
     int4* queue = S.queue + (threadIdx.x >> 5) * kClQCap;
     const int kcs = a.n_types * 32, khs = ((a.kpw + 3) & ~3) >> 2;  // uint4 strides between the words' blocks
     const uint4* kc = reinterpret_cast<const uint4*>(S.kpc + t30 * 128);
@@ -450,10 +455,10 @@ __device__ __forceinline__ void cl_phase(const PlaneArgs& a, const RoundArgs& r,
 #pragma unroll
             for (int j = 0; j < WPT; ++j) { q.s[j] = 0u; q.x0[j] = 0u; q.x1[j] = 0u; q.x2[j] = 0u; }
             if (st < fhi) {
-                cl_row<WPT>(base + ((size_t)st << logW), q.s);
-                cl_row<WPT>(base + ((uint32_t)en.x & 0x7fffffffu), q.x0);
-                cl_row<WPT>(base + ((uint32_t)en.y & 0x7fffffffu), q.x1);
-                cl_row<WPT>(base + ((uint32_t)en.z & 0x7fffffffu), q.x2);
+                cl_row<WPT>(rowp((uint32_t)st << logW), q.s);
+                cl_row<WPT>(rowp((uint32_t)en.x), q.x0);
+                cl_row<WPT>(rowp((uint32_t)en.y), q.x1);
+                cl_row<WPT>(rowp((uint32_t)en.z), q.x2);
             }
             return q;
         };
@@ -486,6 +491,15 @@ __device__ __forceinline__ void cl_phase(const PlaneArgs& a, const RoundArgs& r,
                 uint32_t u, lt = 0u, take, ns;
                 if (RULE == 0) {
                     u = c1 & act;  // classes 0, 1 (de <= 0): always taken
+#if TG_CMP8
+                    if (WPT == 1) {
+                        compare8_sel(c0, k2a, k2b, k3a, k3b, r0, r1, u, u, lt);
+                    } else {
+                        const uint4* kj = kc + j * kcs;
+                        compare8_sel(c0, kj[0], kj[1], kj[16], kj[17], r0, r1, u, u, lt);
+                    }
+                    take = act & (~c1 | lt);
+#else
                     if (WPT == 1) {
                         compare4_sel(c0, k2a, k3a, r0, u, lt);
                         compare4_sel(c0, k2b, k3b, r1, u, lt);
@@ -495,6 +509,7 @@ __device__ __forceinline__ void cl_phase(const PlaneArgs& a, const RoundArgs& r,
                         compare4_sel(c0, kj[1], kj[17], r1, u, lt);
                     }
                     take = (~c1 & act) | lt;
+#endif
                     ns = s ^ take;
                 } else {
                     const uint4* kj = kh + j * khs;
@@ -502,6 +517,15 @@ __device__ __forceinline__ void cl_phase(const PlaneArgs& a, const RoundArgs& r,
                     const uint32_t always = sel(c1, sel(c0, L.w, L.z), sel(c0, L.y, L.x)) & act;
                     u = act & ~always;
                     const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#if TG_CMP8
+                    uint32_t tb[8];
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        const uint4 T = kj[b];
+                        tb[b] = sel(c1, sel(c0, T.w, T.z), sel(c0, T.y, T.x));
+                    }
+                    compare8(tb, rr, u, u, lt);  // lt beyond u: covered by `always` / masked by act
+#else
 #pragma unroll
                     for (int b = 0; b < 8; ++b) {
                         const uint4 T = kj[b];
@@ -509,6 +533,7 @@ __device__ __forceinline__ void cl_phase(const PlaneArgs& a, const RoundArgs& r,
                         lt |= u & tb & ~rr[b];
                         u &= ~(tb ^ rr[b]);
                     }
+#endif
                     take = (always | lt) & act;  // new spin +1 (undecided lanes provisionally -1)
                     ns = (s & ~act) | take;
                 }
@@ -536,9 +561,9 @@ __device__ __forceinline__ void cl_phase(const PlaneArgs& a, const RoundArgs& r,
             }
             if (valid) {
                 if constexpr (WPT == 2)
-                    *reinterpret_cast<uint2*>(base + ((size_t)site << logW)) = make_uint2(nsv[0], nsv[1]);
+                    *reinterpret_cast<uint2*>(rowp((uint32_t)site << logW)) = make_uint2(nsv[0], nsv[1]);
                 else
-                    base[(size_t)site << logW] = nsv[0];
+                    *rowp((uint32_t)site << logW) = nsv[0];
             }
             // deferred tail: (site, word)s with lanes still undecided after 8 planes
 #pragma unroll
@@ -575,11 +600,11 @@ __device__ __forceinline__ void cl_phase(const PlaneArgs& a, const RoundArgs& r,
             for (int j = 0; j < WPT; ++j) { s[j] = 0u; x0[j] = 0u; x1[j] = 0u; x2[j] = 0u; y[j] = 0u; }
             if (valid) {
                 e = qent ? qent[site] : __ldg(a.nbr4 + site);
-                cl_row<WPT>(base + ((size_t)site << logW), s);
-                cl_row<WPT>(base + ((uint32_t)e.x & 0x7fffffffu), x0);
-                cl_row<WPT>(base + ((uint32_t)e.y & 0x7fffffffu), x1);
-                cl_row<WPT>(base + ((uint32_t)e.z & 0x7fffffffu), x2);
-                cl_row<WPT>(base + (uint32_t)e.w, y);
+                cl_row<WPT>(rowp((uint32_t)site << logW), s);
+                cl_row<WPT>(rowp((uint32_t)e.x), x0);
+                cl_row<WPT>(rowp((uint32_t)e.y), x1);
+                cl_row<WPT>(rowp((uint32_t)e.z), x2);
+                cl_row<WPT>(rowp((uint32_t)e.w), y);
             }
             u32x4 rr4[2 * WPT];
             philox_planeN<2 * WPT>((uint32_t)site, gg, P, a.pks, rr4);
@@ -596,8 +621,19 @@ __device__ __forceinline__ void cl_phase(const PlaneArgs& a, const RoundArgs& r,
                 const uint32_t act = valid ? act_w[j] : 0u;
                 const uint32_t always = cl_mux8(cb, kpb + kKPlanes * 8) & act;
                 uint32_t u = act & ~always, lt = 0u;
+#if TG_CMP8
+                {
+                    const u32x4 r0 = rr4[2 * j], r1 = rr4[2 * j + 1];
+                    const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+                    uint32_t tb[8];
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) tb[b] = cl_mux8(cb, kpb + b * 8);
+                    compare8(tb, rr, u, u, lt);  // lt beyond u: covered by `always` / masked by act
+                }
+#else
                 cl_compare8(cb, kpb, 0, rr4[2 * j], u, lt);
                 cl_compare8(cb, kpb, 1, rr4[2 * j + 1], u, lt);
+#endif
 #pragma unroll 1
                 for (int blk = 2; blk < 14; ++blk) {
                     if (!__any_sync(0xffffffffu, u)) break;
@@ -632,9 +668,9 @@ __device__ __forceinline__ void cl_phase(const PlaneArgs& a, const RoundArgs& r,
             }
             if (valid) {
                 if constexpr (WPT == 2)
-                    *reinterpret_cast<uint2*>(base + ((size_t)site << logW)) = make_uint2(nsv[0], nsv[1]);
+                    *reinterpret_cast<uint2*>(rowp((uint32_t)site << logW)) = make_uint2(nsv[0], nsv[1]);
                 else
-                    base[(size_t)site << logW] = nsv[0];
+                    *rowp((uint32_t)site << logW) = nsv[0];
             }
         }
     }

@@ -10,8 +10,24 @@ namespace tg {
 
 // ------------------------------------------------------------ helpers
 
+// One LOP3 with an explicit truth table (a = 0xF0, b = 0xCC, c = 0xAA).
+template <int LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+    return d;
+}
+
+#ifndef TG_CMP8
+#define TG_CMP8 1
+#endif
+
 __device__ __forceinline__ uint32_t sel(uint32_t m, uint32_t a1, uint32_t a0) {
+#if TG_CMP8
+    return lop3<0xCA>(m, a1, a0);  // (m & a1) | (~m & a0) as one instruction
+#else
     return (m & a1) | (~m & a0);
+#endif
 }
 
 // Select, per lane bit, leaves[class(lane)] where class bits are cb[0..B).
@@ -131,6 +147,33 @@ __device__ __forceinline__ void compare_block_sel(uint32_t c, const uint32_t* k0
             und &= ~(tb ^ rr[q]);
         }
     }
+}
+
+// The 8 unconditional planes (0 = most significant) of the lazy comparison in
+// two 3-input chains, two instructions per plane: walking the planes from
+// the least significant one up, "less than so far" needs no "equal so far"
+// term (lt' = ~r t | ~(r ^ t) lt), and the undecided lanes are the AND of the
+// planes' equalities.  Same (lt, und) as eight MSB-first steps from (0, u);
+// `lt` is only meaningful on the lanes of u.
+__device__ __forceinline__ void compare8(const uint32_t (&t)[8], const uint32_t (&r)[8], uint32_t u,
+                                         uint32_t& und, uint32_t& lt) {
+    uint32_t l = t[7] & ~r[7], e = u;
+#pragma unroll
+    for (int b = 6; b >= 0; --b) l = lop3<0x8E>(r[b], t[b], l);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) e = lop3<0x90>(e, r[b], t[b]);
+    lt = l;
+    und = e;
+}
+
+// compare8 with the one-level threshold select of compare4_sel.
+__device__ __forceinline__ void compare8_sel(uint32_t c, const uint4& k2a, const uint4& k2b, const uint4& k3a,
+                                             const uint4& k3b, const u32x4& r0, const u32x4& r1, uint32_t u,
+                                             uint32_t& und, uint32_t& lt) {
+    const uint32_t t[8] = {sel(c, k3a.x, k2a.x), sel(c, k3a.y, k2a.y), sel(c, k3a.z, k2a.z), sel(c, k3a.w, k2a.w),
+                           sel(c, k3b.x, k2b.x), sel(c, k3b.y, k2b.y), sel(c, k3b.z, k2b.z), sel(c, k3b.w, k2b.w)};
+    const uint32_t r[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    compare8(t, r, u, und, lt);
 }
 
 // Pruned compare of 4 planes with thresholds already in registers: lanes
