@@ -196,6 +196,61 @@ __device__ __noinline__ void c5_drain(const PlaneArgs& a, int base, int n, uint3
     __syncwarp();
 }
 
+#ifndef TG_C5_QDEFER
+#define TG_C5_QDEFER 1
+#endif
+
+// c5_drain for chain sites (8 classes: c = c0 + 2 c1 cost bits, q = chain
+// bit).  The record carries the cost bits; the chain bit is recomputed from
+// the stored rows (the partner has the other colour, and the own word's
+// undecided lanes still hold their old spin under Metropolis).  A late flip
+// changes the lane's unsatisfied cost bonds by 2c - 3 (heat bath, late +1:
+// 3 - 2c) and its unsatisfied chain bond by +1 if it was satisfied, else -1.
+template <int RULE>
+__device__ __noinline__ void c5_drain_chain(const PlaneArgs& a, int base, int n, uint32_t tlo, uint32_t thi,
+                                            int t31, bool count, int* s_cc, int* s_cq) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    const bool mine = lane < n;
+    int4 e = make_int4(0, 0, 0, 0);
+    if (mine) e = c5_queue(threadIdx.x >> 5)[base + lane];
+    const uint32_t site = (uint32_t)e.x & 0x07ffffffu;
+    const int w = (int)((uint32_t)e.x >> 27);
+    uint32_t und = (uint32_t)e.y;
+    uint32_t cb[3] = {(uint32_t)e.z, (uint32_t)e.w, 0u};
+    uint32_t* own = a.spins + (size_t)site * a.W + w;
+    if (mine) {
+        const uint32_t y = a.spins[(size_t)((uint32_t)__ldg(&a.nbr4[site].w)) + w];
+        cb[2] = RULE == 0 ? ~(*own ^ y) : y;
+    }
+    const uint32_t grp4 = (uint32_t)(a.w_global0 + w) << 4;
+    const uint32_t* kpb = a.kp + (size_t)w * a.kpw + a.ty[t31].kp_off;
+    uint32_t lt = 0u;
+    const PhiloxT P = philox_t(tlo, thi, a.pks);
+#pragma unroll 1
+    for (int blk = 2; blk < 14; ++blk) {
+        if (!__any_sync(0xffffffffu, und)) break;
+        const u32x4 r = philox_plane(site, grp4 | (uint32_t)blk, P, a.pks);
+        compare_block<3>(cb, kpb, 8, blk, r, und, lt);
+    }
+    if (lt) {
+        if (RULE == 0) *own ^= lt;
+        else *own |= lt;
+        if (count) {
+            uint32_t ex = lt;
+            while (ex) {
+                const int l = __ffs(ex) - 1;
+                ex &= ex - 1;
+                const int cl = (int)((cb[0] >> l) & 1u) + 2 * (int)((cb[1] >> l) & 1u);
+                const int q = (int)((cb[2] >> l) & 1u);
+                atomicAdd(s_cc + w * 32 + l, RULE == 0 ? 2 * cl - 3 : 3 - 2 * cl);
+                atomicAdd(s_cq + w * 32 + l, RULE == 0 ? (q ? 1 : -1) : (q ? -1 : 1));
+            }
+        }
+    }
+    __syncwarp();
+}
+
 // Per-thread constants of a colour phase.
 struct C5Ctx {
     uint32_t act[2];
@@ -413,6 +468,7 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
             philox_planeN<4>(site, K.g, K.P, a.pks, r);
             const uint32_t m0s = (uint32_t)(e.x >> 31), m1s = (uint32_t)(e.y >> 31), m2s = (uint32_t)(e.z >> 31);
             uint32_t ns[2];
+            uint32_t undq[2] = {0u, 0u}, clq0[2] = {0u, 0u}, clq1[2] = {0u, 0u};
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const uint32_t sj = j ? s.y : s.x;
@@ -439,12 +495,19 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
                 compare_block<3>(cb, kpb, 8, 0, r[2 * j], u, lt);
                 compare_block<3>(cb, kpb, 8, 1, r[2 * j + 1], u, lt);
 #endif
+#if TG_C5_QDEFER
+                lt &= ~u;  // undecided lanes: provisionally not taken, resolved by c5_drain_chain
+                undq[j] = u;
+                clq0[j] = cb[0];
+                clq1[j] = cb[1];
+#else
 #pragma unroll 1
                 for (int blk = 2; blk < 14; ++blk) {
                     if (!__any_sync(0xffffffffu, u)) break;
                     const u32x4 rb = philox_plane(site, K.g[2 * j] | (uint32_t)blk, K.P, a.pks);
                     compare_block<3>(cb, kpb, 8, blk, rb, u, lt);
                 }
+#endif
                 const uint32_t take = (always | lt) & act;
                 ns[j] = RULE == 0 ? sj ^ take : (sj & ~act) | take;
                 if (count) {
@@ -470,7 +533,31 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
             if (valid)
                 *reinterpret_cast<uint2*>(const_cast<char*>(base) + (uint32_t)(site << (logW + 2))) =
                     make_uint2(ns[0], ns[1]);
+#if TG_C5_QDEFER
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const uint32_t pend = __ballot_sync(0xffffffffu, undq[j] != 0u);
+                if (pend) {
+                    if (undq[j])  // {site | word << 27, undecided lanes, cost class bits}
+                        c5_queue(threadIdx.x >> 5)[qn + __popc(pend & ((1u << lane) - 1u))] =
+                            make_int4((int)(site | ((uint32_t)(w0 + j) << 27)), (int)undq[j], (int)clq0[j],
+                                      (int)clq1[j]);
+                    qn += __popc(pend);
+                }
+            }
+            if (qn >= 32) {
+                qn -= 32;
+                c5_drain_chain<RULE>(a, qn, 32, K.tlo, K.thi, t31, count, s_cc, s_cq);
+            }
+#endif
         }
+#if TG_C5_QDEFER
+        while (qn > 0) {
+            const int n = qn < 32 ? qn : 32;
+            qn -= n;
+            c5_drain_chain<RULE>(a, qn, n, K.tlo, K.thi, t31, count, s_cc, s_cq);
+        }
+#endif
         if (count) {
             c5_flush(V0, logWP, 0, s_cc);
             c5_flush(V1, logWP, 1, s_cc);

@@ -51,6 +51,23 @@ __device__ __forceinline__ float sf_signed(float w, uint32_t word, int k) {
     return __int_as_float(__float_as_int(w) ^ ((word << (24 - 8 * k)) & 0x80000000u));
 }
 
+#ifndef TG_SF_FASTDEC
+#define TG_SF_FASTDEC 2
+#endif
+
+// 2^x, one MUFU.EX2 (relative error 2^-22; results below 2^-126 flush to zero,
+// which the decisions below treat as "smaller than every nonzero prefix").
+__device__ __forceinline__ float sf_ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float sf_rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // FP64 decision of one replica with all 53 bits (the semantics the FP32 path
 // certifies): local field in the reference's merged-CSR order
 // (constraints.cpp:122-140, ising.cpp:79-88), then mc.cpp:27-29 / heat bath.
@@ -124,6 +141,7 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
             float bt[8], tp[8];       // beta, 2P of the lanes' replicas (current instance)
             uint32_t k0 = 0, k1 = 0;  // the instance's pack key
             float tol = 0.f, c1 = 0.f;  // de dead band; band coefficient of T (p)
+            float in_eps = 0.f;         // error bound of the FP32 field (dead band of s l)
             const SInst* in = nullptr;
             for (int item = lo; item < hi; ++item) {
                 if (item >= b_end) {  // next instance (flush the previous one's energies)
@@ -142,7 +160,11 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                         // heat bath eb + |y| 2^-19 + 2^-18, eb = 2 beta_max eps
                         const float eb = 2.0f * in->beta_max * in->eps;
                         tol = 2.0f * in->eps;
+                        in_eps = in->eps;
                         c1 = RULE == 0 ? 2.0f * eb + 0x1.0p-18f : eb + 0x1.0p-18f;
+#if TG_SF_FASTDEC == 2
+                        if (in->beta_max * in->eps > 0.125f) c1 = 0x1.0p+100f;  // nothing certified: all FP64
+#endif
                     }
                     if (lane_on) {
                         const float4* lp = reinterpret_cast<const float4*>(a.lab + (size_t)b * a.Rp + m0);
@@ -150,6 +172,11 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                         for (int q = 0; q < 4; ++q) {
                             const float4 v = lp[q];
                             bt[2 * q] = v.x; tp[2 * q] = v.y; bt[2 * q + 1] = v.z; tp[2 * q + 1] = v.w;
+#if TG_SF_FASTDEC
+                            // -2 beta log2(e): exp(-2 beta s l) = 2^(bt s l)
+                            bt[2 * q] *= -2.885390081777927f;
+                            bt[2 * q + 1] *= -2.885390081777927f;
+#endif
                         }
                     }
                 }
@@ -197,6 +224,60 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                 // (|u - T| inside the error band) take the FP64 path below
                 uint32_t fm0 = 0u, fm1 = 0u;  // bytes to flip (0xFE: +1 <-> -1)
                 uint32_t und = 0u;
+#if TG_SF_FASTDEC == 2
+                // One comparison per replica.  With w = T - uf0 (T = exp(-beta de)
+                // resp. the heat-bath p; uf0 = hi16 2^-16 <= u < uf0 + 2^-16) and
+                // A = band + 2^-16: u < T is certain when w >= A, u >= T is
+                // certain when w <= -A, and only |w| < A goes to the FP64 path
+                // (probability ~2^-15).  Metropolis needs no test of the sign
+                // of de: for de <= eps the band (>= T 4 beta_max eps, host
+                // guarantees beta_max eps <= 1/8) puts T + A above 1 > uf0, so a
+                // rejection is never certified there, and a certified
+                // acceptance is right for either sign.  The exponent is clamped
+                // at 2^64 (de < 0 deep: accepted for every u) so T stays finite.
+                float mu = -1.0f;  // max over replicas of A - |w|: > 0 <=> someone undecided
+                auto decide = [&](int j, float& w, float& A) {
+                    const uint32_t ow = j < 4 ? s0.x : s0.y;
+                    const float hwf = __uint2float_rn(((j < 2 ? o.x : j < 4 ? o.y : j < 6 ? o.z : o.w) >> (16 * (j & 1))) & 0xFFFFu);
+                    if (RULE == 0) {
+                        const float x2 = fminf(bt[j] * sf_signed(l[j], ow, j & 3), 64.0f);  // -2 beta s l log2(e)
+                        const float T = sf_ex2(x2);
+                        A = fmaf(T, fmaf(fabsf(x2), 0x1.62e430p-20f, c1), 0x1.0p-16f + 0x1.0p-40f);
+                        w = fmaf(hwf, -0x1.0p-16f, T);
+                    } else {
+                        const float y2 = bt[j] * l[j];                     // -2 beta l log2(e)
+                        const float p = sf_rcp(1.0f + sf_ex2(y2));
+                        A = fmaf(fabsf(y2), 0x1.62e430p-20f, c1 + 0x1.0p-16f);
+                        w = fmaf(hwf, -0x1.0p-16f, p);
+                    }
+                };
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    float w, A;
+                    decide(j, w, A);
+                    const uint32_t ow = j < 4 ? s0.x : s0.y;
+                    const int bj = j & 3;
+                    bool flip;
+                    if (RULE == 0) flip = w >= A;                      // u < T certain
+                    else {
+                        const bool up = ((ow >> (8 * bj + 7)) & 1u) == 0u;  // current spin +1
+                        flip = up ? (w <= -A) : (w >= A);
+                    }
+                    if (flip) {
+                        if (j < 4) fm0 |= 0xFEu << (8 * bj);
+                        else fm1 |= 0xFEu << (8 * bj);
+                    }
+                    mu = fmaxf(mu, A - fabsf(w));
+                }
+                if (mu > 0.0f) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        float w, A;
+                        decide(j, w, A);
+                        if (fabsf(w) < A) und |= 1u << j;
+                    }
+                }
+#else
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const uint32_t ow = j < 4 ? s0.x : s0.y;
@@ -206,6 +287,34 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                     const float uf0 = __uint2float_rn(hw) * 0x1.0p-16f;
                     const float uf1 = uf0 + 0x1.0p-16f;
                     bool flip, undec;
+#if TG_SF_FASTDEC
+                    // Same certified decisions with fewer instructions: the
+                    // exponent in base 2 (bt = -2 beta log2 e; one FMUL and one
+                    // MUFU.EX2), the band of s2_update around T resp. p
+                    // (|x| 2^-19 covers the roundings of bt and of the product,
+                    // 3 |x| 2^-24, and c1's 2^-18 the 2^-22 of ex2 / rcp), plus
+                    // 2^-40 so that a T flushed to zero still defers u < 2^-16
+                    // to the FP64 path.
+                    if (RULE == 0) {
+                        const float sl = sf_signed(lj, ow, bj);          // s_i l
+                        const float x2 = bt[j] * sl;                     // -2 beta s l log2(e)
+                        const float T = sf_ex2(x2);
+                        const float band = fmaf(T, fmaf(fabsf(x2), 0x1.62e430p-20f, c1), 0x1.0p-40f);
+                        const bool pos = sl > in_eps;
+                        const bool acc = sl < -in_eps || (pos && uf1 <= T - band);
+                        const bool rej = pos && uf0 >= T + band;
+                        flip = acc;
+                        undec = !(acc || rej);
+                    } else {
+                        const float y2 = bt[j] * lj;                     // -2 beta l log2(e)
+                        const float p = sf_rcp(1.0f + sf_ex2(y2));
+                        const float band = fmaf(fabsf(y2), 0x1.62e430p-20f, c1);
+                        const bool up = ((ow >> (8 * bj + 7)) & 1u) == 0u;  // current spin +1
+                        const bool nup = uf1 <= p - band, ndown = uf0 >= p + band;
+                        flip = up ? ndown : nup;
+                        undec = !(nup || ndown);
+                    }
+#else
                     if (RULE == 0) {
                         const float de = 2.0f * sf_signed(lj, ow, bj);  // 2 s_i l
                         const float x = -bt[j] * de;
@@ -225,12 +334,14 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                         flip = up ? ndown : nup;
                         undec = !(nup || ndown);
                     }
+#endif
                     if (flip) {
                         if (j < 4) fm0 |= 0xFEu << (8 * bj);
                         else fm1 |= 0xFEu << (8 * bj);
                     }
                     und |= (uint32_t)undec << j;
                 }
+#endif
                 while (und) {  // FP64 with all 53 bits (rare)
                     const int j = __ffs(und) - 1;
                     und &= und - 1;
