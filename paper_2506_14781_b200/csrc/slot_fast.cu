@@ -234,7 +234,9 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                 // guarantees beta_max eps <= 1/8) puts T + A above 1 > uf0, so a
                 // rejection is never certified there, and a certified
                 // acceptance is right for either sign.  The exponent is clamped
-                // at 2^64 (de < 0 deep: accepted for every u) so T stays finite.
+                // at 2^64 (de < 0 deep: accepted for every u) so T stays finite; a
+                // T flushed to zero (below 2^-126) leaves A = 2^-16, so the bucket
+                // of hi16 = 0 stays undecided and every other one is rejected.
                 float mu = -1.0f;  // max over replicas of A - |w|: > 0 <=> someone undecided
                 auto decide = [&](int j, float& w, float& A) {
                     const uint32_t ow = j < 4 ? s0.x : s0.y;
@@ -242,7 +244,7 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                     if (RULE == 0) {
                         const float x2 = fminf(bt[j] * sf_signed(l[j], ow, j & 3), 64.0f);  // -2 beta s l log2(e)
                         const float T = sf_ex2(x2);
-                        A = fmaf(T, fmaf(fabsf(x2), 0x1.62e430p-20f, c1), 0x1.0p-16f + 0x1.0p-40f);
+                        A = fmaf(T, fmaf(fabsf(x2), 0x1.62e430p-20f, c1), 0x1.0p-16f);
                         w = fmaf(hwf, -0x1.0p-16f, T);
                     } else {
                         const float y2 = bt[j] * l[j];                     // -2 beta l log2(e)
