@@ -130,7 +130,7 @@ class Engine:
                  nccl_id: Optional[bytes] = None):
         self._L = _lib.lib()
         h = C.c_void_p()
-        if world_size == 1:
+        if world_size == 1 and nccl_id is None:
             rc = self._L.tg_create(device, C.byref(h))
         else:
             buf = C.create_string_buffer(bytes(nccl_id), 128)

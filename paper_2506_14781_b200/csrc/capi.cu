@@ -48,10 +48,16 @@ static int create_impl(int device, int rank, int world, const void* nccl_id, tg_
             CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
             pool_set[device] = true;
         }
-        if (world > 1) {
+        // TG_DIST_SELFTEST=1 with an id and world == 1: a one-rank communicator, and the
+        // engine takes the multi-GPU round loop (sweep launches, NCCL all-gather /
+        // all-reduce inside the captured graph) so that path runs on a single GPU
+        const bool selftest = world == 1 && nccl_id && std::getenv("TG_DIST_SELFTEST") &&
+                              std::atoi(std::getenv("TG_DIST_SELFTEST")) != 0;
+        if (world > 1 || selftest) {
             ncclUniqueId id;
             std::memcpy(&id, nccl_id, sizeof(id));
             NK(nccl().CommInitRank(&c->comm, world, id, rank));
+            c->dist = true;
         }
     });
     if (rc != TG_OK) {
@@ -233,7 +239,7 @@ int tg_get_state(tg_ctx* ctx, int slot, int8_t* out) {
         e.digest = nullptr;
         extract_kernel<<<std::max(1, std::min((c.n + 255) / 256, c.sms * 8)), 256, 0, c.stream>>>(e);
         CK(cudaGetLastError());
-        if (c.world > 1) NK(nccl().AllReduce(dst.p, dst.p, c.n, ncclInt8, ncclSum, c.comm, c.stream));
+        if (c.dist) NK(nccl().AllReduce(dst.p, dst.p, c.n, ncclInt8, ncclSum, c.comm, c.stream));
         CK(cudaMemcpyAsync(out, dst.p, c.n, cudaMemcpyDeviceToHost, c.stream));
         CK(cudaStreamSynchronize(c.stream));
     });

@@ -288,6 +288,7 @@ struct tg_ctx {
     StreamOwner stream_owner;
     cudaStream_t stream = nullptr;
     ncclComm_t comm = nullptr;
+    bool dist = false;  // exchange over NCCL: world > 1, or a 1-rank communicator under TG_DIST_SELFTEST
     bool profiling = false;
 
     // problem (caller order) + canonical relabel

@@ -105,7 +105,7 @@ void do_init(tg_ctx& c, const tg_run_config* cfg) {
     cudaStream_t st = c.stream;
     CK(cudaSetDevice(c.device));
     c.use_s2 = false;
-    if ((eng == TG_ENGINE_SLOT && c.world == 1 && !std::getenv("TG_SLOT_V1")) || eng == TG_ENGINE_FLOAT) {
+    if ((eng == TG_ENGINE_SLOT && c.world == 1 && !c.dist && !std::getenv("TG_SLOT_V1")) || eng == TG_ENGINE_FLOAT) {
         // single instance = batch of one on the replica-fastest SLOT engine
         BatchInst bi;
         ensure_host_arrays(c);
@@ -250,7 +250,7 @@ void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         c.rounds_done = c.s2.rounds_done;
         return;
     }
-    if (c.engine == TG_ENGINE_PLANE && c.world == 1 && c.fused_grid > 0 &&
+    if (c.engine == TG_ENGINE_PLANE && c.world == 1 && !c.dist && c.fused_grid > 0 &&
         !(c.cfg.record_flags & TG_REC_GRID)) {
         do_advance_fused(c, n_rounds, sink);
         return;
@@ -301,7 +301,7 @@ void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         if (c.profiling)
             CK(capturing ? cudaEventRecordWithFlags(c.ev[2 * k + 1], st, cudaEventRecordExternal)
                          : cudaEventRecord(c.ev[2 * k + 1], st));
-        if (c.world > 1) {
+        if (c.dist) {
             NvtxRange nx_("tg: (f, g) all-gather");
             NK(nccl().GroupStart());
             NK(nccl().AllGather(c.d_f.p + c.state0, c.d_f.p, c.R_local, ncclDouble, c.comm, st));
@@ -365,7 +365,7 @@ void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         for (int k = 0; k < n; ++k) c.swap_base += (uint64_t)round_attempts(c.I, c.J, first_round + k);
         c.rounds_done += n;
         left -= n;
-        if (c.world > 1) {
+        if (c.dist) {
             // target digests and snapshots: every rank wrote zeros for states it
             // does not hold, one all-reduce per chunk instead of one per round
             if (flags & TG_REC_DIGEST) NK(nccl().AllReduce(c.d_dig.p, c.d_dig.p, n, ncclUint64, ncclSum, c.comm, st));

@@ -39,6 +39,7 @@ namespace cg = cooperative_groups;
 namespace tg {
 
 constexpr int kC5VB = 8;  // vertical counter planes (<= 255 per lane between flushes)
+constexpr int kC5FlushAt = 80;  // items (<= 3 bonds each) between flushes of the cost-bond counters
 
 extern __shared__ __align__(16) int c5_sm[];
 
@@ -301,6 +302,7 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
 #endif
     };
     int qn = 0;
+    int since = 0;  // items added to V0 / V1 since their last flush
     // ---------------------------------------------------------- chain-free
     {
         const int n_it = (nfree + S - 1) / S;
@@ -431,21 +433,45 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
                 qn -= 32;
                 c5_drain<RULE>(a, qn, 32, K.tlo, K.thi, t30, count, s_cc);
             }
+            if (count && ++since == kC5FlushAt) {  // 8-plane counters: at most 3 per item
+                c5_flush(V0, logWP, 0, s_cc);
+                c5_flush(V1, logWP, 1, s_cc);
+                since = 0;
+            }
         }
     }
+    // ---------------------------------------------------------- chain sites
+    const int nq = ce - cf;
+    const int n_itq = (nq + S - 1) / S;
+    auto centry = [&](int i) -> int4 {
+        int4 v = make_int4(0, 0, 0, 0);
+        if (i < n_itq) {
+            const int st = cf + i * S + sl;
+            if (st < ce) v = __ldg(a.nbr4 + st);
+        }
+        return v;
+    };
+    struct CRows { uint2 s, x0, x1, x2, y; };
+    auto crows = [&](int i, const int4& e) -> CRows {
+        const uint2 z = make_uint2(0u, 0u);
+        CRows q{z, z, z, z, z};
+        const int st = cf + i * S + sl;
+        if (i < n_itq && st < ce) {
+            q.s = row((uint32_t)st << logW);
+            q.x0 = row((uint32_t)e.x);
+            q.x1 = row((uint32_t)e.y);
+            q.x2 = row((uint32_t)e.z);
+            q.y = row((uint32_t)e.w);
+        }
+        return q;
+    };
     while (qn > 0) {
         const int n = qn < 32 ? qn : 32;
         qn -= n;
         c5_drain<RULE>(a, qn, n, K.tlo, K.thi, t30, count, s_cc);
     }
-    if (count) {
-        c5_flush(V0, logWP, 0, s_cc);
-        c5_flush(V1, logWP, 1, s_cc);
-    }
-    // ---------------------------------------------------------- chain sites
-    const int nq = ce - cf;
     if (nq > 0) {
-        const int n_it = (nq + S - 1) / S;
+        const int n_it = n_itq;
         const uint32_t* kpb0 = a.kp + (size_t)w0 * a.kpw + a.ty[t31].kp_off;
         const uint32_t* kpb1 = kpb0 + a.kpw;
         uint32_t Q0[kC5VB], Q1[kC5VB];
@@ -454,16 +480,11 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
         for (int it = gw; it < n_it; it += nw) {
             const uint32_t site = (uint32_t)(cf + it * S + sl);
             const bool valid = (int)site < ce;
-            int4 e = make_int4(0, 0, 0, 0);
-            uint2 s = make_uint2(0u, 0u), x0 = s, x1 = s, x2 = s, y = s;
-            if (valid) {
-                e = __ldg(a.nbr4 + site);
-                s = row(site << logW);
-                x0 = row((uint32_t)e.x);
-                x1 = row((uint32_t)e.y);
-                x2 = row((uint32_t)e.z);
-                y = row((uint32_t)e.w);
-            }
+            // (a software pipeline of these loads as in the chain-free loop was
+            // measured 1.3 % slower: profiles/r2/ab_c5_flush_chainpipe.txt)
+            const int4 e = centry(it);
+            const CRows cq_ = crows(it, e);
+            const uint2 s = cq_.s, x0 = cq_.x0, x1 = cq_.x1, x2 = cq_.x2, y = cq_.y;
             u32x4 r[4];
             philox_planeN<4>(site, K.g, K.P, a.pks, r);
             const uint32_t m0s = (uint32_t)(e.x >> 31), m1s = (uint32_t)(e.y >> 31), m2s = (uint32_t)(e.z >> 31);
@@ -550,6 +571,13 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
                 c5_drain_chain<RULE>(a, qn, 32, K.tlo, K.thi, t31, count, s_cc, s_cq);
             }
 #endif
+            if (count && ++since == kC5FlushAt) {
+                c5_flush(V0, logWP, 0, s_cc);
+                c5_flush(V1, logWP, 1, s_cc);
+                c5_flush(Q0, logWP, 0, s_cq);
+                c5_flush(Q1, logWP, 1, s_cq);
+                since = 0;
+            }
         }
 #if TG_C5_QDEFER
         while (qn > 0) {
@@ -559,11 +587,13 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
         }
 #endif
         if (count) {
-            c5_flush(V0, logWP, 0, s_cc);
-            c5_flush(V1, logWP, 1, s_cc);
             c5_flush(Q0, logWP, 0, s_cq);
             c5_flush(Q1, logWP, 1, s_cq);
         }
+    }
+    if (count) {  // one flush of the cost-bond counters per phase (chain-free + chain items)
+        c5_flush(V0, logWP, 0, s_cc);
+        c5_flush(V1, logWP, 1, s_cc);
     }
 }
 

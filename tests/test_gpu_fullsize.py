@@ -100,3 +100,24 @@ def test_oracle_parity_config5_smallest_size(rule):
     np.testing.assert_array_equal(grid, o.final_grid)
     np.testing.assert_array_equal(cp, o.accepts_p)
     np.testing.assert_array_equal(cb, o.accepts_b)
+
+
+@pytest.mark.parametrize("rule", ["metropolis", "heat_bath"])
+def test_bond_counters_beyond_one_flush_period(rule):
+    """2^21 sites x 1024 hot replicas: a warp of the config-5 kernel walks ~200
+    two-site items per colour phase, each adding up to 3 unsatisfied bonds
+    (~1.5 on average at beta = 0.01) to its 8-plane vertical counters, i.e.
+    past 255 without the periodic flush.  Every record's (f, g) must equal the
+    energy recomputed from the reported target state."""
+    pr = I.bipartite_3regular(1 << 21, seed=3)
+    betas = I.linear(0.01, 0.02, 32)
+    pens = I.dyadic(I.linear(0.0, 1.0, 32))
+    with Engine(0) as eng:
+        eng.set_problem(pr)
+        eng.set_schedule(betas, pens)
+        recs = records(eng, RunConfig(total_sweeps=3, seed=4, rule=rule, engine="plane", store_states=True))
+        assert eng.info()["sweep_kernel"] == "plane_c5_rounds_kernel"
+        assert len(recs) == 3
+        for rnd, f, g, dig, st in recs:
+            assert (f, g) == energy(pr, st)
+            assert dig == O.digest(st)

@@ -82,3 +82,19 @@ def test_two_gpus_equal_one_gpu(name):
     for rank, recs, grid in out:
         assert recs == ref_recs, rank
         np.testing.assert_array_equal(grid, ref_grid)
+
+
+@pytest.mark.parametrize("name", ["plane", "slot"])
+def test_one_rank_nccl_round_loop_equals_fused(name, monkeypatch):
+    """The multi-GPU round loop on one GPU: with TG_DIST_SELFTEST=1 a world-size-1
+    context initialises a one-rank NCCL communicator and takes the unfused path
+    (sweep launches, ncclAllGather of (f, g) per round and the per-chunk
+    ncclAllReduce of digests inside the captured CUDA graph).  Its records and
+    final grid must equal the fused single-GPU run's."""
+    from paper_2506_14781_b200.api import Engine
+    pr, b, p, engine = _case(name)
+    ref_recs, ref_grid = _run(pr, b, p, engine)
+    monkeypatch.setenv("TG_DIST_SELFTEST", "1")
+    recs, grid = _run(pr, b, p, engine, 0, 1, Engine.nccl_unique_id())
+    assert recs == ref_recs
+    np.testing.assert_array_equal(grid, ref_grid)
