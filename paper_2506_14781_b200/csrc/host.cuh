@@ -335,6 +335,8 @@ struct tg_ctx {
     int cl_group = 0;                // software word barrier on G = cl_size CTAs per word (no clusters)
     int cl_pair = 0;                 // ... with two words per thread (G CTAs per word pair)
     int tpw_sweep_grid = 0;          // sweep-only tpw kernel grid (0: plane_sweep_kernel)
+    int c5_sweep_grid = 0;           // sweep-only config-5 kernel grid (0: the tpw / plane sweep kernels)
+    size_t c5_sweep_smem = 0;
     size_t tpw_sweep_smem = 0;
     const char* sweep_kernel = "";   // dominant sweep kernel of the last advance (tg_info)     // thread-per-(site, word) kernel (plane_tpw.cu) instead of plane_rounds_kernel
     size_t fused_smem = 0;

@@ -363,14 +363,24 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
     // config-5 kernel (plane_c5.cu): either rule on the tpw config-5 path with
     // a 2-colouring, at least two words per site row; TG_PLANE_C5=0 disables
     c.fused_c5 = 0;
+    c.c5_sweep_grid = 0;
     {
-        bool ok = c.fused_tpw && c.tpw_fast && c.n_colors == 2 &&
-                  c.W >= 2 && c.n_types <= 2 && c.d_nbr4.p != nullptr &&
-                  (long long)n * c.W < (1ll << 30);  // 32-bit byte offsets of the rows
+        bool elig = tpw_ok && c.tpw_fast && c.n_colors == 2 &&
+                    c.W >= 2 && c.n_types <= 2 && c.d_nbr4.p != nullptr &&
+                    (long long)n * c.W < (1ll << 30);  // 32-bit byte offsets of the rows
         int nfree_type = 0;
         for (const auto& t : types) nfree_type += t.dq == 0;
-        ok = ok && nfree_type <= 1;
-        if (const char* e = std::getenv("TG_PLANE_C5")) ok = ok && std::atoi(e) != 0;
+        elig = elig && nfree_type <= 1;
+        if (const char* e = std::getenv("TG_PLANE_C5")) elig = elig && std::atoi(e) != 0;
+        if (elig) {  // its sweep-only form for the unfused round loop (multi-GPU ranks, full-grid records)
+            const size_t smem = c5_smem_bytes(c.R, c.W);
+            const int fb = kernel_fit(plane_c5_sweep_fn(c.cfg.rule), kC5Threads, smem).blocks_per_sm;
+            if (fb >= 1) {
+                c.c5_sweep_grid = fb * c.sms;
+                c.c5_sweep_smem = smem;
+            }
+        }
+        const bool ok = elig && c.fused_tpw;
         if (ok) {
             const size_t smem = c5_smem_bytes(c.R, c.W);
             const int fb = kernel_fit(plane_c5_fn(c.cfg.rule), kC5Threads, smem).blocks_per_sm;

@@ -42,7 +42,13 @@ void launch_sweep(tg_ctx& c, int64_t t0, const RoundState* rs) {
         int64_t t = t0;
         int nsw = sps;
         void* args[] = {&a, &t, &nsw};
-        if (c.tpw_sweep_grid > 0) {
+        if (c.c5_sweep_grid > 0) {
+            int nf0 = c.c5_nfree[0], nf1 = c.c5_nfree[1];
+            void* args5[] = {&a, &t, &nsw, &nf0, &nf1};
+            c.sweep_kernel = "plane_c5_sweep_kernel";
+            CK(cudaLaunchCooperativeKernel(plane_c5_sweep_fn(c.cfg.rule), dim3(c.c5_sweep_grid), dim3(kC5Threads),
+                                           args5, c.c5_sweep_smem, c.stream));
+        } else if (c.tpw_sweep_grid > 0) {
             c.sweep_kernel = "plane_tpw_sweep_kernel";
             CK(cudaLaunchCooperativeKernel(plane_tpw_sweep_fn(c.cfg.rule, c.tpw_fast), dim3(c.tpw_sweep_grid),
                                            dim3(kTpwThreads), args, c.tpw_sweep_smem, c.stream));
@@ -272,6 +278,9 @@ void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
     // sequence of a chunk is the same every time and is replayed as a graph
     SwapArgs sa = swap_args(c);
     sa.rs = c.d_rstate.p;
+    SwapArgs sa_noplane = sa;  // the swap kernel leaves the plane rebuild to plane_rebuild_kernel
+    sa_noplane.plane = 0;
+    const int rebuild_blocks = std::max(1, std::min(c.sms, (c.W * 16 + 7) / 8));
     ExtractArgs e{};
     if (need_extract) {
         e.n = c.n;
@@ -308,8 +317,12 @@ void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
             NK(nccl().AllGather(c.d_g.p + c.state0, c.d_g.p, c.R_local, ncclDouble, c.comm, st));
             NK(nccl().GroupEnd());
         }
-        swap_kernel<<<1, kSwapThreads, 0, st>>>(sa, 0, 0, 0, flags);
+        swap_kernel<<<1, kSwapThreads, 0, st>>>(sa_noplane, 0, 0, 0, flags);
         CK(cudaGetLastError());
+        if (sa.plane) {  // threshold planes of the new labels, grid-wide
+            plane_rebuild_kernel<<<rebuild_blocks, 256, 0, st>>>(sa);
+            CK(cudaGetLastError());
+        }
         if (need_extract) {
             extract_kernel<<<ex_blocks, 256, 0, st>>>(e);
             CK(cudaGetLastError());
@@ -317,10 +330,14 @@ void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         round_tick_kernel<<<1, 32, 0, st>>>(c.d_rstate.p, c.I, c.J);
         CK(cudaGetLastError());
     };
-    const int per_round_other = 2 + (need_extract ? 1 : 0);
+    const int per_round_other = 2 + (need_extract ? 1 : 0) + (sa.plane ? 1 : 0);
     // a graph of n rounds (captured once per chunk length); none if capture fails
     auto graph_for = [&](int n) -> cudaGraphExec_t {
-        if (!c.graphs_ok || std::getenv("TG_NO_GRAPHS")) return nullptr;
+        // Direct launches by default: measured on B200 (tools/dist_selftest_rate.py) a round of
+        // the unfused loop is ~23 us shorter launched directly (the host runs ahead of these
+        // 20-100 us kernels) than replayed as graph nodes; TG_GRAPHS=1 replays captured chunks.
+        const char* ge = std::getenv("TG_GRAPHS");
+        if (!c.graphs_ok || !ge || !std::atoi(ge) || std::getenv("TG_NO_GRAPHS")) return nullptr;
         auto it = c.graphs.find(n);
         if (it != c.graphs.end()) return it->second;
         const int64_t sl0 = c.sweep_launches;

@@ -419,6 +419,44 @@ __global__ void __launch_bounds__(kSwapThreads) swap_kernel(SwapArgs a, int64_t 
     }
 }
 
+// Threshold planes of this rank's words for the current labels, one warp per
+// (word, type, class) job over the whole grid (the unfused round loop runs it
+// after swap_kernel, which then skips its own single-block rebuild).  Plane b
+// holds bit 52 - b of the lanes' 53-bit thresholds: two 32x32 transposes
+// (plane_round.cuh) instead of 53 ballots.
+__global__ void __launch_bounds__(256) plane_rebuild_kernel(SwapArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int nw = gridDim.x * (blockDim.x >> 5);
+    int combos = 0;
+    for (int ty = 0; ty < a.n_types; ++ty) combos += a.types[ty].ncl;
+    const int total = a.W * combos;
+    for (int job = gw; job < total; job += nw) {
+        const int w = job / combos;
+        int c = job % combos, ty = 0;
+        while (c >= a.types[ty].ncl) { c -= a.types[ty].ncl; ++ty; }
+        const PlaneType pt = a.types[ty];
+        const int m = w * 32 + lane;  // local state
+        uint64_t K = 0;
+        const bool live = m < a.local_states;
+        if (live) K = a.ktab[(size_t)a.state_slot[a.state0 + m] * a.ktab_row + pt.ktab_off + c];
+        uint32_t* dst = a.kp + (size_t)w * a.kpw + pt.kp_off + c;
+        uint32_t* dstc = (c == 2 || c == 3) ? a.kpc + ((size_t)w * a.n_types + ty) * 128 + (c - 2) * 64
+                                            : nullptr;
+        const uint32_t th = warp_transpose32((uint32_t)(K >> 21));
+        const uint32_t tl = warp_transpose32((uint32_t)(K << 11));
+        const int bh = 31 - lane, bl = 63 - lane;
+        dst[bh * pt.ncl] = th;
+        if (dstc) dstc[bh] = th;
+        if (lane >= 11) {
+            dst[bl * pt.ncl] = tl;
+            if (dstc) dstc[bl] = tl;
+        }
+        const uint32_t alw = __ballot_sync(0xffffffffu, live && K >= (1ull << 53));
+        if (lane == 0) dst[kKPlanes * pt.ncl] = alw;
+    }
+}
+
 // -------------------------------------------------------- extract kernel
 
 // Advance the device round counters after a round of the unfused loop.

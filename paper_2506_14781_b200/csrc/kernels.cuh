@@ -53,6 +53,7 @@ inline size_t c5_smem_bytes(int R, int W) {
            (size_t)R * (2 * sizeof(double) + 2 * sizeof(int32_t)) + 8;
 }
 void* plane_c5_fn(int rule);
+void* plane_c5_sweep_fn(int rule);  // sweep-only (unfused round loop)
 // cluster-per-word fused round kernel (plane_cl.cu): threads per CTA, per-warp
 // tail queue entries (>= 31 + 32), dynamic shared memory = queues | the word's
 // kp / kpc planes | counts | mbarrier | labels and energies | staged entries.
@@ -170,6 +171,7 @@ cudaError_t plane_gen_chunks(const RunTable& rt, Chunk* chunks, cudaStream_t st)
 __global__ void probe_moments_kernel(const double* hist_f, const double* hist_g, int R, int kept,
                                      double penalty, double* out);
 
+__global__ void plane_rebuild_kernel(SwapArgs a);
 __global__ void swap_kernel(SwapArgs a, int64_t round, uint64_t swap_base, int rec_idx,
                             int rec_flags);
 __global__ void extract_kernel(ExtractArgs e);

@@ -666,6 +666,81 @@ plane_c5_rounds_kernel(const __grid_constant__ PlaneArgs a, const __grid_constan
     }
 }
 
+// Sweep-only kernel of the unfused round loop (multi-GPU ranks, full-grid
+// records; same contract as plane_tpw_sweep_kernel): n_sweeps sweeps over the
+// rank's words with the thresholds the swap kernel left in a.kp / a.kpc,
+// then the rank's per-replica (f, g) into a.f_loc / a.g_loc (counters
+// re-zeroed); the (f, g) exchange and the swap phase run after it.
+template <int RULE>
+__global__ void __launch_bounds__(kC5Threads, kC5MinBlocks)
+plane_c5_sweep_kernel(const __grid_constant__ PlaneArgs a, int64_t t0, int n_sweeps, int nfree0, int nfree1) {
+    if (a.rs) t0 = a.rs->round * n_sweeps;
+    cg::grid_group grid = cg::this_grid();
+    const int nrep = a.W * 32;
+    int* s_cc = c5_cnt();
+    int* s_cq = s_cc + nrep;
+    const int logW = __ffs(a.W) - 1;
+    const int gw = blockIdx.x * (kC5Threads >> 5) + (threadIdx.x >> 5);
+    const int nw = gridDim.x * (kC5Threads >> 5);
+    int t30 = 0, t31 = 0;
+    for (int ty = 0; ty < a.n_types; ++ty) {
+        if (a.ty[ty].dq == 0) t30 = ty;
+        else t31 = ty;
+    }
+    for (int m = threadIdx.x; m < 2 * nrep; m += blockDim.x) s_cc[m] = 0;
+    {   // thresholds of the chain-free type (the labels are fixed for the whole launch)
+        uint4* th = c5_thr();
+        if (RULE == 0) {
+            for (int q = threadIdx.x; q < 4 * a.W; q += blockDim.x) {
+                const int part = q / a.W, w = q % a.W;
+                th[q] = reinterpret_cast<const uint4*>(a.kpc + ((size_t)w * a.n_types + t30) * 128)
+                    [(part & 1) + 16 * (part >> 1)];
+            }
+        } else {
+            const int kp0 = a.ty[t30].kp_off;
+            for (int q = threadIdx.x; q < 9 * a.W; q += blockDim.x) {
+                const int b = q / a.W, w = q % a.W;
+                th[q] = *reinterpret_cast<const uint4*>(a.kp + (size_t)w * a.kpw + kp0 + (b < 8 ? b : kKPlanes) * 4);
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t V0[kC5VB], V1[kC5VB];
+#pragma unroll
+    for (int b = 0; b < kC5VB; ++b) { V0[b] = 0u; V1[b] = 0u; }
+    for (int sw = 0; sw < n_sweeps; ++sw) {
+        const uint64_t t = (uint64_t)(t0 + sw);
+        const bool count = (sw == n_sweeps - 1);
+        for (int c = 0; c < 2; ++c) {
+            c5_phase<RULE>(a, c, t, count, gw, nw, logW, V0, V1, t30, t31, c ? nfree1 : nfree0);
+            if (count && c == 1) {
+                __syncthreads();
+                for (int m = threadIdx.x; m < nrep; m += blockDim.x) {
+                    const int vc = s_cc[m], vqv = s_cq[m];
+                    if (vc) { atomicAdd(a.cnt_c + m, vc); s_cc[m] = 0; }
+                    if (vqv) { atomicAdd(a.cnt_q + m, vqv); s_cq[m] = 0; }
+                }
+            }
+            grid.sync();
+        }
+    }
+    // f = -(m - 2 u_c) for J = +-1, h = 0; g = sum (s_a - s_b)^2 = 4 u_q
+    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < a.local_states; m += gridDim.x * blockDim.x) {
+        const int uc = a.cnt_c[m], uq = a.cnt_q[m];
+        a.f_loc[m] = -((double)a.m_cost - 2.0 * (double)uc);
+        a.g_loc[m] = 4.0 * (double)uq;
+        a.cnt_c[m] = 0;
+        a.cnt_q[m] = 0;
+    }
+}
+
+template __global__ void plane_c5_sweep_kernel<0>(const __grid_constant__ PlaneArgs, int64_t, int, int, int);
+template __global__ void plane_c5_sweep_kernel<1>(const __grid_constant__ PlaneArgs, int64_t, int, int, int);
+
+void* plane_c5_sweep_fn(int rule) {
+    return rule ? (void*)plane_c5_sweep_kernel<1> : (void*)plane_c5_sweep_kernel<0>;
+}
+
 template __global__ void plane_c5_rounds_kernel<0>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
 template __global__ void plane_c5_rounds_kernel<1>(const __grid_constant__ PlaneArgs, const __grid_constant__ RoundArgs);
 

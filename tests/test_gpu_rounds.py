@@ -1,7 +1,7 @@
 """The unfused round loop (full-grid records on one GPU; every multi-GPU run)
-keeps its round counters on the device and replays each chunk of rounds as a
-captured CUDA graph.  It must give the oracle's trajectories, and the same
-records with graphs disabled (TG_NO_GRAPHS=1, direct launches), including
+keeps its round counters on the device, so a chunk of rounds is one fixed
+launch sequence: launched directly by default, replayed as a captured CUDA
+graph with TG_GRAPHS=1.  Both must give the oracle's trajectories, including
 across record-ring drains (chunks) and for the slot engine's multi-GPU
 kernel path (TG_SLOT_V1)."""
 import numpy as np
@@ -12,6 +12,11 @@ from paper_2506_14781_b200 import instances as I
 from paper_2506_14781_b200.api import Engine, RunConfig
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _graphs_on(monkeypatch):
+    monkeypatch.setenv("TG_GRAPHS", "1")  # the graph replay; TG_NO_GRAPHS=1 below overrides it
 
 
 def unfused(pr, b, p, rounds, rule, seed, engine, grid=True):
@@ -37,13 +42,16 @@ def unfused(pr, b, p, rounds, rule, seed, engine, grid=True):
     return recs, np.concatenate(states) if states else None, fin, kern
 
 
+@pytest.mark.parametrize("sweep", ["plane_c5_sweep_kernel", "plane_tpw_sweep_kernel"])
 @pytest.mark.parametrize("rule", ["metropolis", "heat_bath"])
-def test_graph_rounds_match_oracle_and_direct_launches(monkeypatch, rule):
+def test_graph_rounds_match_oracle_and_direct_launches(monkeypatch, rule, sweep):
     pr = I.bipartite_3regular(512, seed=3)
     b, p = I.config_schedule("c5")
     o = O.run(pr, b, p, 30, 1, seed=4, rule=rule, rng="plane")
+    if sweep == "plane_tpw_sweep_kernel":
+        monkeypatch.setenv("TG_PLANE_C5", "0")  # the thread-per-(site, word) sweep kernel
     g = unfused(pr, b, p, 30, rule, 4, "plane")
-    assert g[3] == "plane_tpw_sweep_kernel"
+    assert g[3] == sweep
     np.testing.assert_array_equal([r[1] for r in g[0]], o.f)
     np.testing.assert_array_equal(np.array([r[3] for r in g[0]], dtype=np.uint64), o.digest)
     np.testing.assert_array_equal(g[2], o.final_grid)

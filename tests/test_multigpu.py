@@ -95,6 +95,8 @@ def test_one_rank_nccl_round_loop_equals_fused(name, monkeypatch):
     pr, b, p, engine = _case(name)
     ref_recs, ref_grid = _run(pr, b, p, engine)
     monkeypatch.setenv("TG_DIST_SELFTEST", "1")
-    recs, grid = _run(pr, b, p, engine, 0, 1, Engine.nccl_unique_id())
-    assert recs == ref_recs
-    np.testing.assert_array_equal(grid, ref_grid)
+    for graphs in ("0", "1"):  # direct launches (default) and the captured-graph replay
+        monkeypatch.setenv("TG_GRAPHS", graphs)
+        recs, grid = _run(pr, b, p, engine, 0, 1, Engine.nccl_unique_id())
+        assert recs == ref_recs, graphs
+        np.testing.assert_array_equal(grid, ref_grid)
