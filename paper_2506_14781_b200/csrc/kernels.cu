@@ -478,6 +478,33 @@ __global__ void extract_kernel(ExtractArgs e) {
     const int tgt_slot_count = e.all_slots ? e.R : 1;
     const long long total = (long long)tgt_slot_count * e.n;
     uint64_t dsum = 0;
+    if (!e.all_slots) {
+        // the target slot only (every round of a traced run): one label lookup, 32-bit
+        // indexing, four independent gathers in flight per thread
+        const int m = e.slot_state[e.R - 1] - e.state0;
+        const bool here = m >= 0 && m < e.local_states;
+        const int stride = gridDim.x * blockDim.x;
+        for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < e.n; i0 += 4 * stride) {
+            int8_t v[4] = {0, 0, 0, 0};
+            int ci[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * stride;
+                if (i >= e.n) continue;
+                if (here) {
+                    if (e.plane) v[u] = ((e.spins32[(size_t)i * e.W + (m >> 5)] >> (m & 31)) & 1u) ? 1 : -1;
+                    else v[u] = e.spins8[(size_t)m * e.n + i];
+                }
+                ci[u] = e.perm[i];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (i0 + u * stride >= e.n) continue;
+                if (e.states) e.states[ci[u]] = v[u];
+                if (v[u] > 0) dsum += digest_term((uint64_t)ci[u]);
+            }
+        }
+    } else
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
          q += (long long)gridDim.x * blockDim.x) {
         const int sl = e.all_slots ? (int)(q / e.n) : e.R - 1;
