@@ -52,7 +52,7 @@ __device__ __forceinline__ float sf_signed(float w, uint32_t word, int k) {
 }
 
 #ifndef TG_SF_FASTDEC
-#define TG_SF_FASTDEC 2
+#define TG_SF_FASTDEC 2  // 2: one-comparison certified decisions; 0: the previous accept / reject predicates (A/B)
 #endif
 
 // 2^x, one MUFU.EX2 (relative error 2^-22; results below 2^-126 flush to zero,
@@ -141,7 +141,6 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
             float bt[8], tp[8];       // beta, 2P of the lanes' replicas (current instance)
             uint32_t k0 = 0, k1 = 0;  // the instance's pack key
             float tol = 0.f, c1 = 0.f;  // de dead band; band coefficient of T (p)
-            float in_eps = 0.f;         // error bound of the FP32 field (dead band of s l)
             const SInst* in = nullptr;
             for (int item = lo; item < hi; ++item) {
                 if (item >= b_end) {  // next instance (flush the previous one's energies)
@@ -160,7 +159,6 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                         // heat bath eb + |y| 2^-19 + 2^-18, eb = 2 beta_max eps
                         const float eb = 2.0f * in->beta_max * in->eps;
                         tol = 2.0f * in->eps;
-                        in_eps = in->eps;
                         c1 = RULE == 0 ? 2.0f * eb + 0x1.0p-18f : eb + 0x1.0p-18f;
 #if TG_SF_FASTDEC == 2
                         if (in->beta_max * in->eps > 0.125f) c1 = 0x1.0p+100f;  // nothing certified: all FP64
@@ -172,7 +170,7 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                         for (int q = 0; q < 4; ++q) {
                             const float4 v = lp[q];
                             bt[2 * q] = v.x; tp[2 * q] = v.y; bt[2 * q + 1] = v.z; tp[2 * q + 1] = v.w;
-#if TG_SF_FASTDEC
+#if TG_SF_FASTDEC == 2
                             // -2 beta log2(e): exp(-2 beta s l) = 2^(bt s l)
                             bt[2 * q] *= -2.885390081777927f;
                             bt[2 * q + 1] *= -2.885390081777927f;
@@ -289,34 +287,6 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                     const float uf0 = __uint2float_rn(hw) * 0x1.0p-16f;
                     const float uf1 = uf0 + 0x1.0p-16f;
                     bool flip, undec;
-#if TG_SF_FASTDEC
-                    // Same certified decisions with fewer instructions: the
-                    // exponent in base 2 (bt = -2 beta log2 e; one FMUL and one
-                    // MUFU.EX2), the band of s2_update around T resp. p
-                    // (|x| 2^-19 covers the roundings of bt and of the product,
-                    // 3 |x| 2^-24, and c1's 2^-18 the 2^-22 of ex2 / rcp), plus
-                    // 2^-40 so that a T flushed to zero still defers u < 2^-16
-                    // to the FP64 path.
-                    if (RULE == 0) {
-                        const float sl = sf_signed(lj, ow, bj);          // s_i l
-                        const float x2 = bt[j] * sl;                     // -2 beta s l log2(e)
-                        const float T = sf_ex2(x2);
-                        const float band = fmaf(T, fmaf(fabsf(x2), 0x1.62e430p-20f, c1), 0x1.0p-40f);
-                        const bool pos = sl > in_eps;
-                        const bool acc = sl < -in_eps || (pos && uf1 <= T - band);
-                        const bool rej = pos && uf0 >= T + band;
-                        flip = acc;
-                        undec = !(acc || rej);
-                    } else {
-                        const float y2 = bt[j] * lj;                     // -2 beta l log2(e)
-                        const float p = sf_rcp(1.0f + sf_ex2(y2));
-                        const float band = fmaf(fabsf(y2), 0x1.62e430p-20f, c1);
-                        const bool up = ((ow >> (8 * bj + 7)) & 1u) == 0u;  // current spin +1
-                        const bool nup = uf1 <= p - band, ndown = uf0 >= p + band;
-                        flip = up ? ndown : nup;
-                        undec = !(nup || ndown);
-                    }
-#else
                     if (RULE == 0) {
                         const float de = 2.0f * sf_signed(lj, ow, bj);  // 2 s_i l
                         const float x = -bt[j] * de;
@@ -336,7 +306,6 @@ slotf_sweep_kernel(const __grid_constant__ S2Args a, int64_t t0, int n_sweeps, i
                         flip = up ? ndown : nup;
                         undec = !(nup || ndown);
                     }
-#endif
                     if (flip) {
                         if (j < 4) fm0 |= 0xFEu << (8 * bj);
                         else fm1 |= 0xFEu << (8 * bj);
