@@ -19,7 +19,7 @@ def _graphs_on(monkeypatch):
     monkeypatch.setenv("TG_GRAPHS", "1")  # the graph replay; TG_NO_GRAPHS=1 below overrides it
 
 
-def unfused(pr, b, p, rounds, rule, seed, engine, grid=True):
+def unfused(pr, b, p, rounds, rule, seed, engine, grid=True, sps=1):
     eng = Engine(0)
     eng.set_problem(pr)
     eng.set_schedule(b, p)
@@ -34,7 +34,7 @@ def unfused(pr, b, p, rounds, rule, seed, engine, grid=True):
             states.append(np.ctypeslib.as_array(st, shape=(n * per,)).copy())
         return 0
 
-    eng.run(RunConfig(total_sweeps=rounds, sweeps_per_swap=1, seed=seed, rule=rule, engine=engine,
+    eng.run(RunConfig(total_sweeps=rounds * sps, sweeps_per_swap=sps, seed=seed, rule=rule, engine=engine,
                       store_states=not grid, store_target_only=not grid, digest=True), sink)
     fin = eng.grid()
     kern = eng.info()["sweep_kernel"]
@@ -83,5 +83,21 @@ def test_graph_rounds_slot_v1_kernels(monkeypatch):
     g = unfused(pr, b, p, 60, "metropolis", 2, "slot", grid=False)
     assert g[3].startswith("slot_sweep_kernel")
     np.testing.assert_array_equal([r[1] for r in g[0]], o.f)
+    np.testing.assert_array_equal(np.array([r[3] for r in g[0]], dtype=np.uint64), o.digest)
+    np.testing.assert_array_equal(g[2], o.final_grid)
+
+
+@pytest.mark.parametrize("rule", ["metropolis", "heat_bath"])
+def test_sweep_only_config5_kernel_several_sweeps_per_round(monkeypatch, rule):
+    # three sweeps per launch of plane_c5_sweep_kernel (only the last one counts bonds),
+    # direct launches, chain sites included
+    monkeypatch.setenv("TG_GRAPHS", "0")
+    pr = I.bipartite_3regular(2048, seed=8)
+    b, p = I.config_schedule("c5")
+    o = O.run(pr, b, p, 36, 3, seed=6, rule=rule, rng="plane")
+    g = unfused(pr, b, p, 12, rule, 6, "plane", sps=3)
+    assert g[3] == "plane_c5_sweep_kernel"
+    np.testing.assert_array_equal([r[1] for r in g[0]], o.f)
+    np.testing.assert_array_equal([r[2] for r in g[0]], o.g)
     np.testing.assert_array_equal(np.array([r[3] for r in g[0]], dtype=np.uint64), o.digest)
     np.testing.assert_array_equal(g[2], o.final_grid)
