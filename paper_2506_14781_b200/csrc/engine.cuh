@@ -181,6 +181,7 @@ struct SwapArgs {
     uint32_t* kp;
     uint32_t* kpc;
     const RoundState* rs;  // round = rs->round + 1, swap_base, record index from it (else arguments)
+    RoundState* tick;      // unfused loop: advance the round state once the record is written (else null)
 };
 
 // ------------------------------------------------- SLOT engine v2 (batched)

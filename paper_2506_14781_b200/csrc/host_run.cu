@@ -280,6 +280,7 @@ void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
     sa.rs = c.d_rstate.p;
     SwapArgs sa_noplane = sa;  // the swap kernel leaves the plane rebuild to plane_rebuild_kernel
     sa_noplane.plane = 0;
+    sa_noplane.tick = c.d_rstate.p;  // and advances the round state (no separate tick launch)
     const int rebuild_blocks = std::max(1, std::min(c.sms, (c.W * 16 + 7) / 8));
     ExtractArgs e{};
     if (need_extract) {
@@ -297,6 +298,7 @@ void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
         e.states = per_state ? c.d_rec_states.p : nullptr;
         e.digest = (flags & TG_REC_DIGEST) ? c.d_dig.p : nullptr;
         e.rs = c.d_rstate.p;
+        e.rs_back = 1;
         e.per_state = per_state;
     }
     const long long ex_total = (long long)(e.all_slots ? c.R : 1) * c.n;
@@ -327,10 +329,8 @@ void do_advance(tg_ctx& c, int64_t n_rounds, const SinkCtx& sink) {
             extract_kernel<<<ex_blocks, 256, 0, st>>>(e);
             CK(cudaGetLastError());
         }
-        round_tick_kernel<<<1, 32, 0, st>>>(c.d_rstate.p, c.I, c.J);
-        CK(cudaGetLastError());
     };
-    const int per_round_other = 2 + (need_extract ? 1 : 0) + (sa.plane ? 1 : 0);
+    const int per_round_other = 1 + (need_extract ? 1 : 0) + (sa.plane ? 1 : 0);
     // a graph of n rounds (captured once per chunk length); none if capture fails
     auto graph_for = [&](int n) -> cudaGraphExec_t {
         // Direct launches by default: measured on B200 (tools/dist_selftest_rate.py) a round of

@@ -382,6 +382,13 @@ __global__ void __launch_bounds__(kSwapThreads) swap_kernel(SwapArgs a, int64_t 
         for (int k = threadIdx.x; k < np; k += blockDim.x) dst[k] = a.acc_p[k];
         for (int k = threadIdx.x; k < nb; k += blockDim.x) dst[np + k] = a.acc_b[k];
     }
+    // every thread read the round state before the barrier above: advance it for the
+    // kernels that follow (extract_kernel indexes with filled - 1, the next sweep with round)
+    if (a.tick && threadIdx.x == 0) {
+        a.tick->swap_base = swap_base + (uint64_t)n_att;
+        a.tick->round = round;
+        a.tick->filled = rec_idx + 1;
+    }
     if (!a.plane) return;
     // Rebuild the threshold planes of this rank's words for the new labels:
     // bit l of plane b of (w, type, class) = bit (52-b) of K(slot(32w+l), type, class).
@@ -471,7 +478,7 @@ __global__ void round_tick_kernel(RoundState* rs, int I, int J) {
 
 __global__ void extract_kernel(ExtractArgs e) {
     if (e.rs) {  // this round's slot of the chunk's state ring and digest array
-        const int k = e.rs->filled;
+        const int k = e.rs->filled - e.rs_back;  // rs_back: swap_kernel already advanced the round state
         if (e.states) e.states += (size_t)k * e.per_state;
         if (e.digest) e.digest += k;
     }

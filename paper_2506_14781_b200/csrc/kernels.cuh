@@ -95,6 +95,7 @@ struct ExtractArgs {
     uint64_t* digest;     // record digest slot, or null
     // unfused loop: the chunk's state ring / digest array, indexed by rs->filled
     const RoundState* rs;
+    int rs_back;          // 1: the record slot is rs->filled - 1 (swap_kernel advanced the state already)
     size_t per_state;
 };
 __global__ void round_tick_kernel(RoundState* rs, int I, int J);
