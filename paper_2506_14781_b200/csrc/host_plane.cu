@@ -384,9 +384,6 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
         if (ok) {
             const size_t smem = c5_smem_bytes(c.R, c.W);
             const int fb = kernel_fit(plane_c5_fn(c.cfg.rule), kC5Threads, smem).blocks_per_sm;
-            if (const char* e = std::getenv("TG_PLANE_C5_CARVEOUT"))  // shared-memory share of the L1 array, percent
-                CK(cudaFuncSetAttribute(plane_c5_fn(c.cfg.rule), cudaFuncAttributePreferredSharedMemoryCarveout,
-                                        std::atoi(e)));
             if (fb >= 1) {
                 c.fused_c5 = 1;
                 c.fused_grid = fb * c.sms;
@@ -457,8 +454,6 @@ void build_plane_rest(tg_ctx& c, std::vector<PlaneType>& types, const std::vecto
                 P.smem = cl_smem_bytes(c.R, c.I, c.J, c.kpw, c.n_types, P.kt ? ktw : 0, P.stage ? total : 0, wpt);
                 if (P.smem > (size_t)smem_max) return false;
                 CK(cudaFuncSetAttribute(P.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
-                if (const char* e = std::getenv("TG_PLANE_CL_CARVEOUT"))  // shared-memory share of the L1 array, percent
-                    CK(cudaFuncSetAttribute(P.fn, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e)));
                 return true;
             };
             auto take = [&](int C, int group, int wpt, const Plan& P) {
