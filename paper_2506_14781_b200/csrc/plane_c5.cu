@@ -22,9 +22,13 @@
 // item is of one kind and no per-item type test or straddling exists.  Per
 // thread and phase: the class-2/3 threshold planes 0-7 of both words in
 // registers, 4 Philox blocks per chain-free item (the two unconditional blocks
-// of each word, sharing the site's round-1/2/3 products).  Chain-free pairs
-// still undecided after 8 planes go to a per-warp shared-memory queue (one
-// 16-byte record) resolved 32 at a time, one per lane.
+// of each word, sharing the site's round-1/2/3 products), the 8 unconditional
+// planes compared in two 3-input LOP3 chains (plane_device.cuh compare8).
+// (Site, word)s still undecided after 8 planes -- chain-free and chain sites
+// alike -- go to a per-warp shared-memory queue (one 16-byte record) resolved
+// 32 at a time, one per lane (c5_drain, c5_drain_chain).  The bit-sliced bond
+// counters are flushed once per phase (and every kC5FlushAt items).
+// plane_c5_sweep_kernel is the sweep-only form for the unfused round loop.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
