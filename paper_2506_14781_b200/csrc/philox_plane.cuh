@@ -10,6 +10,25 @@
 
 namespace tg {
 
+// The PLANE kernels take both halves of a Philox product from one 32x32->64
+// multiply (IMAD.WIDE.U32): measured +0.5 ... +1.2 % on the fused kernels once
+// the compare chains were shortened (profiles/r2/ab_mulwide_s5.txt); the FLOAT
+// and SLOT kernels keep the split form of philox.cuh (-2.5 % with the wide one).
+#ifndef TG_PLANE_MULWIDE
+#define TG_PLANE_MULWIDE 1
+#endif
+__device__ __forceinline__ void mulhilo_p(uint32_t a, uint32_t b, uint32_t& hi, uint32_t& lo) {
+#if TG_PLANE_MULWIDE
+    uint64_t p;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(b));
+    hi = (uint32_t)(p >> 32);
+    lo = (uint32_t)p;
+#else
+    hi = __umulhi(a, b);
+    lo = a * b;
+#endif
+}
+
 // Philox4x32-10 for the plane counters {site, t_lo, t_hi, group << 4 | blk}
 // with t and the key fixed for a colour phase: the products of round 1 on
 // (t_hi) and of round 2 on the resulting constant are per-phase constants
@@ -36,8 +55,8 @@ __device__ __forceinline__ u32x4 philox_rounds_3_10(u32x4 c, const uint32_t* ks)
 #pragma unroll
     for (int r = 2; r < 10; ++r) {
         uint32_t hi0, lo0, hi1, lo1;
-        mulhilo(kPhiloxM0, c.x, hi0, lo0);
-        mulhilo(kPhiloxM1, c.z, hi1, lo1);
+        mulhilo_p(kPhiloxM0, c.x, hi0, lo0);
+        mulhilo_p(kPhiloxM1, c.z, hi1, lo1);
         c = u32x4{hi1 ^ c.y ^ ks[2 * r], lo1, hi0 ^ c.w ^ ks[2 * r + 1], lo0};
     }
     return c;
@@ -70,10 +89,10 @@ __device__ __forceinline__ void philox_plane2(uint32_t site, uint32_t g0, const 
 #pragma unroll
     for (int r = 3; r < 10; ++r) {
         uint32_t p0, q0, p1, q1, s0, t0, s1, t1;
-        mulhilo(kPhiloxM0, a.x, p0, q0);
-        mulhilo(kPhiloxM1, a.z, p1, q1);
-        mulhilo(kPhiloxM0, b.x, s0, t0);
-        mulhilo(kPhiloxM1, b.z, s1, t1);
+        mulhilo_p(kPhiloxM0, a.x, p0, q0);
+        mulhilo_p(kPhiloxM1, a.z, p1, q1);
+        mulhilo_p(kPhiloxM0, b.x, s0, t0);
+        mulhilo_p(kPhiloxM1, b.z, s1, t1);
         a = u32x4{p1 ^ a.y ^ ks[2 * r], q1, p0 ^ a.w ^ ks[2 * r + 1], q0};
         b = u32x4{s1 ^ b.y ^ ks[2 * r], t1, s0 ^ b.w ^ ks[2 * r + 1], t0};
     }
@@ -103,8 +122,8 @@ __device__ __forceinline__ void philox_planeN(uint32_t site, const uint32_t (&g)
 #pragma unroll
         for (int j = 0; j < N; ++j) {
             uint32_t p0, q0, p1, q1;
-            mulhilo(kPhiloxM0, o[j].x, p0, q0);
-            mulhilo(kPhiloxM1, o[j].z, p1, q1);
+            mulhilo_p(kPhiloxM0, o[j].x, p0, q0);
+            mulhilo_p(kPhiloxM1, o[j].z, p1, q1);
             o[j] = u32x4{p1 ^ o[j].y ^ ks[2 * r], q1, p0 ^ o[j].w ^ ks[2 * r + 1], q0};
         }
     }
