@@ -103,18 +103,26 @@ __device__ __forceinline__ void philox_plane2(uint32_t site, uint32_t g0, const 
 
 // N blocks of one site, counter word 3 = g[j]: rounds 1-3 share the site's
 // round-1 product and the round-2 word-2 product (philox_plane2 for N = 2).
-template <int N>
+// WIDE1: also the shared first-round products as one wide multiply each
+// (plane_c5.cu: +1.3 %; the word-local kernel loses 1.4 % with it).
+template <int N, bool WIDE1 = false>
 __device__ __forceinline__ void philox_planeN(uint32_t site, const uint32_t (&g)[N], const PhiloxT& P,
                                               const uint32_t* ks, u32x4 (&o)[N]) {
-    const uint32_t hs = __umulhi(kPhiloxM0, site), ls = kPhiloxM0 * site;
+    uint32_t hs, ls, h3, l3;
+    if (WIDE1) mulhilo_p(kPhiloxM0, site, hs, ls);
+    else { hs = __umulhi(kPhiloxM0, site); ls = kPhiloxM0 * site; }
     const uint32_t z2 = P.h0x ^ ls;
-    const uint32_t h3 = __umulhi(kPhiloxM1, z2), l3 = kPhiloxM1 * z2;
+    if (WIDE1) mulhilo_p(kPhiloxM1, z2, h3, l3);
+    else { h3 = __umulhi(kPhiloxM1, z2); l3 = kPhiloxM1 * z2; }
 #pragma unroll
     for (int j = 0; j < N; ++j) {
         const uint32_t y = hs ^ g[j] ^ ks[1];
-        const uint32_t hq = __umulhi(kPhiloxM1, y), lq = kPhiloxM1 * y;
+        uint32_t hq, lq, h0, l0;
+        if (WIDE1) mulhilo_p(kPhiloxM1, y, hq, lq);
+        else { hq = __umulhi(kPhiloxM1, y); lq = kPhiloxM1 * y; }
         const uint32_t x = hq ^ P.c1x;
-        const uint32_t h0 = __umulhi(kPhiloxM0, x), l0 = kPhiloxM0 * x;
+        if (WIDE1) mulhilo_p(kPhiloxM0, x, h0, l0);
+        else { h0 = __umulhi(kPhiloxM0, x); l0 = kPhiloxM0 * x; }
         o[j] = u32x4{h3 ^ lq ^ ks[4], l3, h0 ^ P.l0 ^ ks[5], l0};
     }
 #pragma unroll

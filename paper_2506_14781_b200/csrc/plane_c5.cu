@@ -346,7 +346,7 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
             en2 = entries(it + 2 * nw);
             const uint2 s = q.s, x0 = q.x0, x1 = q.x1, x2 = q.x2;
             u32x4 r[4];
-            philox_planeN<4>(site, K.g, K.P, a.pks, r);
+            philox_planeN<4, true>(site, K.g, K.P, a.pks, r);
             const uint32_t m0s = (uint32_t)(e.x >> 31), m1s = (uint32_t)(e.y >> 31), m2s = (uint32_t)(e.z >> 31);
             uint32_t und[2], ns[2], cl0[2], cl1[2];
 #pragma unroll
@@ -490,7 +490,7 @@ __device__ __forceinline__ void c5_phase(const PlaneArgs& a, int c, uint64_t t, 
             const CRows cq_ = crows(it, e);
             const uint2 s = cq_.s, x0 = cq_.x0, x1 = cq_.x1, x2 = cq_.x2, y = cq_.y;
             u32x4 r[4];
-            philox_planeN<4>(site, K.g, K.P, a.pks, r);
+            philox_planeN<4, true>(site, K.g, K.P, a.pks, r);
             const uint32_t m0s = (uint32_t)(e.x >> 31), m1s = (uint32_t)(e.y >> 31), m2s = (uint32_t)(e.z >> 31);
             uint32_t ns[2];
             uint32_t undq[2] = {0u, 0u}, clq0[2] = {0u, 0u}, clq1[2] = {0u, 0u};
